@@ -1,0 +1,103 @@
+/* libcirr -- C ABI of the B200-native CIRR contour-integral stage.
+ *
+ * The reference (cieig, pure Python) has no FFI for this path; its plugin
+ * surface is the Python call cirr_solve / solve_multi
+ * (/root/reference/pkg/src/cieig/solvers.py:165-227, 312-339).  Each entry
+ * below replaces one reference call site, cited per function; the Python
+ * package paper_2511_01927_b200 binds them with ctypes (_lib.py) and keeps
+ * the reference's Python signatures above them.
+ *
+ * Conventions
+ *   - Every pointer is a DEVICE pointer (PyTorch-owned buffers); complex
+ *     values are complex128 interleaved (re, im) -- `cplx` = double2.
+ *   - Matrices are row-major; `ld*` are leading dimensions and `s*`/`*stride`
+ *     batch strides, in ELEMENTS.
+ *   - Return 0 on success, a cudaError_t (> 0) on a CUDA error, or
+ *     CIRR_EINVAL (100000) for invalid arguments.  No entry allocates device
+ *     memory or synchronises the stream.
+ *   - All work is enqueued on `stream`; results are deterministic
+ *     (fixed-order reductions, no floating-point atomics).
+ */
+#ifndef CIRR_H
+#define CIRR_H
+
+#include <cuda_runtime.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef double2 cirr_cplx;
+
+#define CIRR_EINVAL 100000
+
+/* K1 -- replaces linalg.py:62-63 (z*B - A and the max|M_ij| scale).
+ * pencils[j] = z[j]*B - A (bitwise equal to numpy), maxabs[j] = max |.|. */
+int cirr_assemble(const double* A, const double* B, int n, long long lda,
+                  const cirr_cplx* z, int nz, cirr_cplx* pencils, long long ldp,
+                  long long pencil_stride, double* maxabs, cudaStream_t stream);
+
+/* K2 -- replaces linalg.py:65-70 (splu + the 1e-14 pivot test inputs).
+ * In-place P M = L U of `batch` pencils; ipiv/perm: batch x n int32;
+ * minpiv[j] = min_i |U_ii|; info[j] = first exact zero pivot (1-based) or 0. */
+int cirr_zgetrf_batched(cirr_cplx* pencils, int n, long long ld, long long pencil_stride,
+                        int batch, int* ipiv, int* perm, double* minpiv, int* info,
+                        cudaStream_t stream);
+
+/* K3a -- replaces linalg.py:46-52 (SuperLU gstrs) as used at solvers.py:124.
+ * Y[j] = M_j^{-1} R[rhs_of[j]] (rhs_of: device int32[batch]). */
+int cirr_zgetrs_batched(const cirr_cplx* LU, int n, long long ld, long long pencil_stride,
+                        int batch, const int* perm, const cirr_cplx* R, long long ldr,
+                        long long rstride, const int* rhs_of, int K, cirr_cplx* Y,
+                        long long ldy, long long ystride, cudaStream_t stream);
+
+/* K3b -- replaces solvers.py:121-129 (acc[m] += w_j zeta_j^m Y_j).
+ * St[c] ((M*K) x n): row m*K+col = column col of S_m of contour c, summed over
+ * pencils off[c]..off[c+1]-1 in order with coef[j*M+m]. */
+int cirr_moments(const cirr_cplx* Y, long long ldy, long long ystride, int n, int K,
+                 const cirr_cplx* coef, int M, const int* off, int n_sets, cirr_cplx* St,
+                 long long ld_st, long long sstride, cudaStream_t stream);
+
+/* K4 -- replaces linalg.py:107-119 (thin SVD + sigma >= rel_tol*sigma_max).
+ * One-sided Jacobi on the rows of W (c x n per problem, overwritten);
+ * sigma/order: nprob x c (descending), kept: nprob, Qt: kept x n rows.
+ * ws: >= 64 bytes device scratch; *sweeps_out (device int). */
+int cirr_orth(cirr_cplx* W, long long ldw, long long wstride, int n, int c, int nprob,
+              double rel_tol, double* sigma, int* order, int* kept, cirr_cplx* Qt,
+              long long ldq, long long qstride, void* ws, int* sweeps_out, cudaStream_t stream);
+
+/* K5/K7 GEMM -- replaces sparse.py:98-103 (sparse_matmat for B V, A Q, B Q,
+ * A X, B X) and the dense products of solvers.py:153-158.
+ * C = beta*C + alpha*op(A)@B; a_kind 0: A complex, 1: conj(A), 2: A real f64. */
+int cirr_gemm(int a_kind, int M, int N, int K, int batch, const void* A, long long lda,
+              long long sA, const cirr_cplx* B, long long ldb, long long sB, cirr_cplx* C,
+              long long ldc, long long sC, double alpha, int beta, cudaStream_t stream);
+
+/* K6 -- replaces linalg.py:122-145 (dense_hermitian_gep) and adds the
+ * non-Hermitian Rayleigh-Ritz (SURVEY.md 8(c) delta 3). */
+long long cirr_small_eig_ws_bytes(int kmax);
+int cirr_small_eig(int hermitian, const cirr_cplx* At, const cirr_cplx* Bt, long long ldin,
+                   long long sin_, const int* kdim, int kmax, int nprob, void* ws, cirr_cplx* lam,
+                   cirr_cplx* S, long long lds, long long sS, int* info, cudaStream_t stream);
+
+/* K7 -- replaces solvers.py:140-147 (_residuals). */
+int cirr_residuals(const cirr_cplx* AX, const cirr_cplx* BX, long long ld, long long stride, int n,
+                   const cirr_cplx* lam, long long lstride, const int* kdim, int kmax, int nprob,
+                   double* res, long long rstride, cudaStream_t stream);
+
+/* solvers.py:196 (xs[:, keep]) */
+int cirr_gather_cols(const cirr_cplx* in, long long ldi, long long si, const int* idx, long long sidx,
+                     const int* cnt, int cmax, int n, int nprob, cirr_cplx* out, long long ldo,
+                     long long so, cudaStream_t stream);
+
+/* layout helper: out[b] = in[b]^T (or ^H when conj != 0) */
+int cirr_transpose(int conj, const cirr_cplx* in, long long ldi, long long si, int rows, int cols,
+                   int batch, cirr_cplx* out, long long ldo, long long so, cudaStream_t stream);
+
+/* library identification: compute capability the cubins target (100 = sm_100a) */
+int cirr_target_sm(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CIRR_H */

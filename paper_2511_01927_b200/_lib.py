@@ -1,0 +1,70 @@
+"""ctypes binding of libcirr.so (the C ABI declared in include/cirr.h).
+
+There is no CPU fallback: if the shared library is missing or CUDA is not
+available, every entry point raises ``DeviceError``.  Pointers are raw device
+addresses of PyTorch tensors; the stream is torch's current CUDA stream.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .errors import DeviceError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcirr.so")
+EINVAL = 100000
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_L = ctypes.c_longlong
+_D = ctypes.c_double
+
+# name -> argtypes (all return int unless listed in _RESTYPE)
+SIGNATURES = {
+    "cirr_assemble": [_P, _P, _I, _L, _P, _I, _P, _L, _L, _P, _P],
+    "cirr_zgetrf_batched": [_P, _I, _L, _L, _I, _P, _P, _P, _P, _P],
+    "cirr_zgetrs_batched": [_P, _I, _L, _L, _I, _P, _P, _L, _L, _P, _I, _P, _L, _L, _P],
+    "cirr_moments": [_P, _L, _L, _I, _I, _P, _I, _P, _I, _P, _L, _L, _P],
+    "cirr_orth": [_P, _L, _L, _I, _I, _I, _D, _P, _P, _P, _P, _L, _L, _P, _P, _P],
+    "cirr_gemm": [_I, _I, _I, _I, _I, _P, _L, _L, _P, _L, _L, _P, _L, _L, _D, _I, _P],
+    "cirr_small_eig_ws_bytes": [_I],
+    "cirr_small_eig": [_I, _P, _P, _L, _L, _P, _I, _I, _P, _P, _P, _L, _L, _P, _P],
+    "cirr_residuals": [_P, _P, _L, _L, _I, _P, _L, _P, _I, _I, _P, _L, _P],
+    "cirr_gather_cols": [_P, _L, _L, _P, _L, _P, _I, _I, _I, _P, _L, _L, _P],
+    "cirr_transpose": [_I, _P, _L, _L, _I, _I, _I, _P, _L, _L, _P],
+    "cirr_target_sm": [],
+}
+_RESTYPE = {"cirr_small_eig_ws_bytes": _L}
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load libcirr.so once (raises DeviceError when absent)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise DeviceError(f"libcirr.so not built at {path}; run `make` (or __graft_entry__.build())")
+    lib = ctypes.CDLL(path)
+    for name, argt in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = argt
+        fn.restype = _RESTYPE.get(name, _I)
+    _lib = lib
+    return lib
+
+
+def call(name: str, *args):
+    """Invoke an entry point and turn a non-zero status into DeviceError."""
+    fn = getattr(load(), name)
+    rc = fn(*args)
+    if name in _RESTYPE:
+        return rc
+    if rc != 0:
+        if rc == EINVAL:
+            raise DeviceError(f"{name}: invalid arguments")
+        raise DeviceError(f"{name}: CUDA error {rc}")
+    return rc

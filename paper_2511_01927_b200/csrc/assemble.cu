@@ -1,0 +1,82 @@
+// K1: shifted-pencil assembly M_j = z_j B - A for every quadrature node.
+//
+// Replaces linalg.py:62 (`z * B - A`) and the scale of linalg.py:63
+// (max |M_ij|, used by the singular-pivot test).  A and B are real float64,
+// row-major; the pencils are complex128 row-major.  Each CTA reads one
+// contiguous chunk of A and B once from HBM and writes it for a group of
+// pencils (coalesced 16-byte stores), so the read traffic is ~1/group of the
+// write traffic.  The arithmetic is written with __dmul_rn/__dsub_rn so the
+// result is bitwise identical to numpy's (z*B - A): two roundings, no FMA.
+#include "common.cuh"
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kPerThread = 8;          // elements per thread per chunk
+constexpr int kChunk = kThreads * kPerThread;
+constexpr int kGroup = 8;              // pencils written per CTA
+
+__global__ void __launch_bounds__(kThreads) assemble_kernel(
+    const double* __restrict__ A, const double* __restrict__ B, int n, long long lda,
+    const cplx* __restrict__ z, int nz, cplx* __restrict__ P, long long ldp, long long pstride,
+    unsigned long long* __restrict__ maxabs_bits) {
+  __shared__ double wmax[kThreads / 32][kGroup];
+  const long long total = (long long)n * n;
+  const long long base = (long long)blockIdx.x * kChunk;
+  const int j0 = blockIdx.y * kGroup;
+  double a[kPerThread], b[kPerThread];
+  long long src[kPerThread], dst[kPerThread];
+  bool ok[kPerThread];
+#pragma unroll
+  for (int e = 0; e < kPerThread; ++e) {
+    long long idx = base + (long long)e * kThreads + threadIdx.x;
+    ok[e] = idx < total;
+    long long r = ok[e] ? idx / n : 0, c = ok[e] ? idx - r * n : 0;
+    src[e] = r * lda + c;
+    dst[e] = r * ldp + c;
+    a[e] = ok[e] ? A[src[e]] : 0.0;
+    b[e] = ok[e] ? B[src[e]] : 0.0;
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int g = 0; g < kGroup; ++g) {
+    const int j = j0 + g;
+    if (j >= nz) break;
+    const cplx zj = z[j];
+    cplx* Pj = P + (long long)j * pstride;
+    double m = 0.0;
+#pragma unroll
+    for (int e = 0; e < kPerThread; ++e) {
+      if (ok[e]) {
+        cplx v = cmk(__dsub_rn(__dmul_rn(zj.x, b[e]), a[e]), __dmul_rn(zj.y, b[e]));
+        Pj[dst[e]] = v;
+        m = fmax(m, hypot(v.x, v.y));
+      }
+    }
+    m = warp_max(m);
+    if (lane == 0) wmax[wid][g] = m;
+  }
+  __syncthreads();
+  if (threadIdx.x < kGroup && j0 + threadIdx.x < nz) {
+    double m = 0.0;
+    for (int w = 0; w < kThreads / 32; ++w) m = fmax(m, wmax[w][threadIdx.x]);
+    // non-negative doubles order like their bit patterns
+    atomicMax(maxabs_bits + j0 + threadIdx.x, (unsigned long long)__double_as_longlong(m));
+  }
+}
+
+}  // namespace
+
+// pencils[j] = z[j]*B - A (j < nz); maxabs[j] = max_ij |pencils[j]_ij|.
+CIRR_API int cirr_assemble(const double* A, const double* B, int n, long long lda,
+                           const cplx* z, int nz, cplx* pencils, long long ldp,
+                           long long pencil_stride, double* maxabs, cudaStream_t stream) {
+  if (n <= 0 || nz <= 0 || lda < n || ldp < n) return CIRR_EINVAL;
+  cudaError_t e = cudaMemsetAsync(maxabs, 0, sizeof(double) * nz, stream);
+  if (e != cudaSuccess) return (int)e;
+  const long long total = (long long)n * n;
+  dim3 grid((unsigned)((total + kChunk - 1) / kChunk), (unsigned)((nz + kGroup - 1) / kGroup));
+  assemble_kernel<<<grid, kThreads, 0, stream>>>(A, B, n, lda, z, nz, pencils, ldp, pencil_stride,
+                                                  reinterpret_cast<unsigned long long*>(maxabs));
+  CIRR_CHECK_LAUNCH();
+  return 0;
+}

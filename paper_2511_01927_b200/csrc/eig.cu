@@ -1,0 +1,581 @@
+// K6: the small projected eigenproblem, one CTA per contour.
+//
+// Replaces linalg.py:122-145 (dense_hermitian_gep: Cholesky test +
+// scipy.linalg.eigh) as called from solvers.py:150-158, plus the
+// non-Hermitian Rayleigh-Ritz the reference lacks (SURVEY.md 8(c) delta 3).
+//
+//  * herm_eig_kernel: symmetrise A~, B~ (solvers.py:155-156); Cholesky
+//    B~ = L L^H (failure -> info > 0, raised as IndefiniteBError); A' =
+//    L^-1 A~ L^-H; cyclic parallel Jacobi (circle-method rounds) on A';
+//    s = L^-H W (B~-orthonormal); eigenvalues ascending.
+//  * gen_eig_kernel: M = B~^-1 A~ (partial-pivot LU), Householder Hessenberg
+//    reduction, single-shift complex QR (Wilkinson shift, exceptional shifts
+//    at 10/20 iterations, zlahqr-style deflation) accumulating Z, eigenvectors
+//    by back substitution on the Schur form, unit 2-norm; eigenvalues sorted
+//    by (re, im) as numpy sorts complex values.
+//
+// k <= 1024.  Matrices live in a global workspace (L2 resident at these
+// sizes); every reduction is fixed-order, so results are reproducible.
+#include "common.cuh"
+
+namespace {
+
+constexpr int ET = 1024;
+constexpr double EPS = 1.1102230246251565e-16;
+
+struct EigWs {
+  cplx* A;   // k x k
+  cplx* L;   // k x k
+  cplx* V;   // k x k
+  cplx* T;   // k x k
+  cplx* vec; // 4k
+  double* d; // 4k
+};
+
+__device__ __forceinline__ EigWs carve(void* ws, long long wstride_bytes, int prob, int kmax) {
+  unsigned char* base = reinterpret_cast<unsigned char*>(ws) + (long long)prob * wstride_bytes;
+  EigWs w;
+  const long long kk = (long long)kmax * kmax;
+  w.A = reinterpret_cast<cplx*>(base);
+  w.L = w.A + kk;
+  w.V = w.L + kk;
+  w.T = w.V + kk;
+  w.vec = w.T + kk;
+  w.d = reinterpret_cast<double*>(w.vec + 4 * (long long)kmax);
+  return w;
+}
+
+__device__ __forceinline__ void jrot(double app, double aqq, cplx apq, double& cs, cplx& se) {
+  // rotation J = [[c, s e^{i phi}], [-s e^{-i phi}, c]] zeroing apq of [[app, apq], [conj, aqq]]
+  const double ag = cabs(apq);
+  const double zeta = (aqq - app) / (2.0 * ag);
+  const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+  cs = 1.0 / sqrt(1.0 + t * t);
+  const double sn = t * cs;
+  se = cmk(sn * apq.x / ag, sn * apq.y / ag);
+}
+
+__device__ __forceinline__ void rr_pair(int round, int kk, int cp, int& p, int& q) {
+  if (kk == 0) { p = cp - 1; q = round; }
+  else { p = (round + kk) % (cp - 1); q = (round - kk + (cp - 1)) % (cp - 1); }
+  if (p > q) { int t = p; p = q; q = t; }
+}
+
+__global__ void __launch_bounds__(ET) herm_eig_kernel(const cplx* __restrict__ At, const cplx* __restrict__ Bt,
+                                                      long long ldin, long long sin_, const int* __restrict__ kdim,
+                                                      int kmax, void* ws, long long wstride,
+                                                      cplx* __restrict__ lam, cplx* __restrict__ S, long long lds,
+                                                      long long sS, int* __restrict__ info) {
+  __shared__ double red[32];
+  __shared__ double rot_c[512];
+  __shared__ cplx rot_s[512];
+  __shared__ int rot_p[512], rot_q[512];
+  __shared__ int s_flag, s_count;
+  const int prob = blockIdx.x;
+  const int k = kdim[prob];
+  const int tid = threadIdx.x;
+  EigWs w = carve(ws, wstride, prob, kmax);
+  const cplx* Ai = At + (long long)prob * sin_;
+  const cplx* Bi = Bt + (long long)prob * sin_;
+  cplx *A = w.A, *L = w.L, *V = w.V, *T = w.T;
+  const int ld = kmax;
+  if (tid == 0) s_flag = 0;
+  // 1. symmetrise
+  for (int e = tid; e < k * k; e += ET) {
+    int r = e / k, c = e % k;
+    cplx a = Ai[(long long)r * ldin + c], at = Ai[(long long)c * ldin + r];
+    cplx b = Bi[(long long)r * ldin + c], bt = Bi[(long long)c * ldin + r];
+    A[r * ld + c] = cmk(0.5 * (a.x + at.x), 0.5 * (a.y - at.y));
+    L[r * ld + c] = cmk(0.5 * (b.x + bt.x), 0.5 * (b.y - bt.y));
+  }
+  __syncthreads();
+  // 2. Cholesky (lower) of L in place
+  for (int j = 0; j < k; ++j) {
+    const double djj = L[j * ld + j].x;
+    if (!(djj > 0.0)) {
+      if (tid == 0) s_flag = j + 1;
+      __syncthreads();
+      break;
+    }
+    const double dj = sqrt(djj);
+    __syncthreads();
+    if (tid == 0) L[j * ld + j] = cmk(dj, 0.0);
+    for (int r = j + 1 + tid; r < k; r += ET) L[r * ld + j] = cscale(L[r * ld + j], 1.0 / dj);
+    __syncthreads();
+    const int m = k - j - 1;
+    for (int e = tid; e < m * m; e += ET) {
+      int r = j + 1 + e / m, c = j + 1 + e % m;
+      if (c <= r) cfms(L[r * ld + c], L[r * ld + j], cconj(L[c * ld + j]));
+    }
+    __syncthreads();
+  }
+  if (s_flag) {
+    if (tid == 0) info[prob] = s_flag;
+    return;
+  }
+  // 3. X = L^-1 A (column per thread), then A' = L^-1 X^H  (into T)
+  for (int c = tid; c < k; c += ET) {
+    for (int i = 0; i < k; ++i) {
+      cplx v = A[i * ld + c];
+      for (int l = 0; l < i; ++l) cfms(v, L[i * ld + l], A[l * ld + c]);
+      A[i * ld + c] = cscale(v, 1.0 / L[i * ld + i].x);
+    }
+  }
+  __syncthreads();
+  for (int c = tid; c < k; c += ET) {
+    for (int i = 0; i < k; ++i) {
+      cplx v = cconj(A[c * ld + i]);
+      for (int l = 0; l < i; ++l) cfms(v, L[i * ld + l], T[l * ld + c]);
+      T[i * ld + c] = cscale(v, 1.0 / L[i * ld + i].x);
+    }
+  }
+  __syncthreads();
+  double fro = 0.0;
+  for (int e = tid; e < k * k; e += ET) {
+    int r = e / k, c = e % k;
+    cplx a = T[r * ld + c], at = T[c * ld + r];
+    cplx v = cmk(0.5 * (a.x + at.x), 0.5 * (a.y - at.y));
+    A[r * ld + c] = v;
+    V[r * ld + c] = cmk(r == c ? 1.0 : 0.0, 0.0);
+    fro += cabs2(v);
+  }
+  fro = sqrt(block_sum(fro, red));
+  __syncthreads();
+  // 4. parallel cyclic Jacobi
+  const int cp = k + (k & 1), np = cp / 2;
+  const double small = 1e-300 + 1e-18 * fro;
+  for (int sweep = 0; sweep < 40 && k > 1; ++sweep) {
+    if (tid == 0) s_count = 0;
+    __syncthreads();
+    for (int round = 0; round < cp - 1; ++round) {
+      for (int t = tid; t < np; t += ET) {
+        int p, q;
+        rr_pair(round, t, cp, p, q);
+        rot_p[t] = p; rot_q[t] = q; rot_c[t] = 1.0; rot_s[t] = cmk(0.0, 0.0);
+        if (q < k) {
+          const double app = A[p * ld + p].x, aqq = A[q * ld + q].x;
+          const cplx apq = A[p * ld + q];
+          const double ag = cabs(apq);
+          if (ag > small && ag > EPS * sqrt(fabs(app)) * sqrt(fabs(aqq))) {
+            double cs; cplx se;
+            jrot(app, aqq, apq, cs, se);
+            rot_c[t] = cs; rot_s[t] = se;
+            atomicAdd(&s_count, 1);
+          } else {
+            rot_q[t] = k;  // skip
+          }
+        }
+      }
+      __syncthreads();
+      // columns: A <- A J, V <- V J
+      for (int e = tid; e < np * k; e += ET) {
+        const int t = e / k, r = e % k;
+        const int p = rot_p[t], q = rot_q[t];
+        if (q >= k) continue;
+        const double cs = rot_c[t];
+        const cplx se = rot_s[t], sec = cconj(se);
+        cplx x = A[r * ld + p], y = A[r * ld + q];
+        A[r * ld + p] = csub(cscale(x, cs), cmul(sec, y));
+        A[r * ld + q] = cadd(cmul(se, x), cscale(y, cs));
+        x = V[r * ld + p]; y = V[r * ld + q];
+        V[r * ld + p] = csub(cscale(x, cs), cmul(sec, y));
+        V[r * ld + q] = cadd(cmul(se, x), cscale(y, cs));
+      }
+      __syncthreads();
+      // rows: A <- J^H A
+      for (int e = tid; e < np * k; e += ET) {
+        const int t = e / k, c = e % k;
+        const int p = rot_p[t], q = rot_q[t];
+        if (q >= k) continue;
+        const double cs = rot_c[t];
+        const cplx se = rot_s[t], sec = cconj(se);
+        cplx x = A[p * ld + c], y = A[q * ld + c];
+        A[p * ld + c] = csub(cscale(x, cs), cmul(se, y));
+        A[q * ld + c] = cadd(cmul(sec, x), cscale(y, cs));
+      }
+      __syncthreads();
+      for (int t = tid; t < np; t += ET) {
+        const int p = rot_p[t], q = rot_q[t];
+        if (q >= k) continue;
+        A[p * ld + q] = cmk(0.0, 0.0);
+        A[q * ld + p] = cmk(0.0, 0.0);
+        A[p * ld + p].y = 0.0;
+        A[q * ld + q].y = 0.0;
+      }
+      __syncthreads();
+    }
+    if (s_count == 0) break;
+    __syncthreads();
+  }
+  // 5. sort ascending, s = L^-H W
+  for (int i = tid; i < k; i += ET) {
+    const double li = A[i * ld + i].x;
+    int rank = 0;
+    for (int j = 0; j < k; ++j) {
+      const double lj = A[j * ld + j].x;
+      rank += (lj < li) || (lj == li && j < i);
+    }
+    w.d[i] = (double)rank;
+    lam[(long long)prob * kmax + rank] = cmk(li, 0.0);
+  }
+  __syncthreads();
+  cplx* Sp = S + (long long)prob * sS;
+  for (int c = tid; c < k; c += ET) {
+    const int rank = (int)w.d[c];
+    for (int i = k - 1; i >= 0; --i) {
+      cplx v = V[i * ld + c];
+      for (int l = i + 1; l < k; ++l) cfms(v, cconj(L[l * ld + i]), T[l * ld + c]);
+      v = cscale(v, 1.0 / L[i * ld + i].x);
+      T[i * ld + c] = v;
+      Sp[(long long)i * lds + rank] = v;
+    }
+  }
+  if (tid == 0) info[prob] = 0;
+}
+
+// --------------------------------------------------------------------------
+// non-Hermitian
+
+__device__ cplx csqrt_(cplx z) {
+  const double r = cabs(z);
+  if (r == 0.0) return cmk(0.0, 0.0);
+  double x = sqrt(0.5 * (r + fabs(z.x)));
+  double y = 0.5 * z.y / x;
+  if (z.x >= 0.0) return cmk(x, y);
+  return cmk(fabs(y), z.y >= 0.0 ? x : -x);
+}
+
+__global__ void __launch_bounds__(ET) gen_eig_kernel(const cplx* __restrict__ At, const cplx* __restrict__ Bt,
+                                                     long long ldin, long long sin_, const int* __restrict__ kdim,
+                                                     int kmax, void* ws, long long wstride,
+                                                     cplx* __restrict__ lam, cplx* __restrict__ S, long long lds,
+                                                     long long sS, int* __restrict__ info) {
+  __shared__ double red[32];
+  __shared__ double rv[32];
+  __shared__ int ri[32];
+  __shared__ int s_int[4];
+  __shared__ cplx s_c[4];
+  __shared__ double s_d[4];
+  const int prob = blockIdx.x;
+  const int k = kdim[prob];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  EigWs w = carve(ws, wstride, prob, kmax);
+  const cplx* Ai = At + (long long)prob * sin_;
+  const cplx* Bi = Bt + (long long)prob * sin_;
+  cplx *H = w.A, *LU = w.L, *Z = w.V, *X = w.T;
+  int* piv = reinterpret_cast<int*>(w.d);
+  const int ld = kmax;
+  for (int e = tid; e < k * k; e += ET) {
+    int r = e / k, c = e % k;
+    LU[r * ld + c] = Bi[(long long)r * ldin + c];
+    H[r * ld + c] = Ai[(long long)r * ldin + c];
+    Z[r * ld + c] = cmk(r == c ? 1.0 : 0.0, 0.0);
+  }
+  if (tid == 0) s_int[3] = 0;
+  __syncthreads();
+  // 1. LU of B~ with partial pivoting; apply the same row swaps to H
+  for (int j = 0; j < k; ++j) {
+    double best = -1.0; int bi = j;
+    for (int r = j + tid; r < k; r += ET) {
+      double v = cabs1(LU[r * ld + j]);
+      if (v > best) { best = v; bi = r; }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      double ov = __shfl_xor_sync(0xffffffffu, best, o);
+      int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+    }
+    if (lane == 0) { rv[wid] = best; ri[wid] = bi; }
+    __syncthreads();
+    if (wid == 0) {
+      best = rv[lane]; bi = ri[lane];
+      for (int o = 16; o > 0; o >>= 1) {
+        double ov = __shfl_xor_sync(0xffffffffu, best, o);
+        int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+      }
+      if (lane == 0) { s_int[0] = bi; piv[j] = bi; if (best == 0.0) s_int[3] = j + 1; }
+    }
+    __syncthreads();
+    const int p = s_int[0];
+    if (p != j) {
+      for (int c = tid; c < k; c += ET) {
+        cplx t = LU[j * ld + c]; LU[j * ld + c] = LU[p * ld + c]; LU[p * ld + c] = t;
+        t = H[j * ld + c]; H[j * ld + c] = H[p * ld + c]; H[p * ld + c] = t;
+      }
+    }
+    __syncthreads();
+    const cplx pv = LU[j * ld + j];
+    if (pv.x != 0.0 || pv.y != 0.0) {
+      const cplx rp = crecip(pv);
+      for (int r = j + 1 + tid; r < k; r += ET) LU[r * ld + j] = cmul(LU[r * ld + j], rp);
+      __syncthreads();
+      const int m = k - j - 1;
+      for (int e = tid; e < m * m; e += ET) {
+        int r = j + 1 + e / m, c = j + 1 + e % m;
+        cfms(LU[r * ld + c], LU[r * ld + j], LU[j * ld + c]);
+      }
+    }
+    __syncthreads();
+  }
+  if (s_int[3]) {
+    if (tid == 0) info[prob] = s_int[3];
+    return;
+  }
+  // solve L U M = P A (column per thread), M into H
+  for (int c = tid; c < k; c += ET) {
+    for (int i = 0; i < k; ++i) {
+      cplx v = H[i * ld + c];
+      for (int l = 0; l < i; ++l) cfms(v, LU[i * ld + l], H[l * ld + c]);
+      H[i * ld + c] = v;
+    }
+    for (int i = k - 1; i >= 0; --i) {
+      cplx v = H[i * ld + c];
+      for (int l = i + 1; l < k; ++l) cfms(v, LU[i * ld + l], H[l * ld + c]);
+      H[i * ld + c] = cdiv(v, LU[i * ld + i]);
+    }
+  }
+  __syncthreads();
+  // 2. Householder Hessenberg reduction H <- Q^H H Q, Z <- Z Q
+  cplx* v = w.vec;          // Householder vector (length k)
+  cplx* wv = w.vec + kmax;  // work vectors (length 3k)
+  for (int j = 0; j + 2 < k; ++j) {
+    const int m = k - j - 1;  // rows j+1 .. k-1
+    double xs = 0.0;
+    for (int r = j + 2 + tid; r < k; r += ET) xs += cabs2(H[r * ld + j]);
+    xs = block_sum(xs, red);
+    const cplx alpha = H[(j + 1) * ld + j];
+    cplx tau = cmk(0.0, 0.0);
+    if (xs != 0.0 || alpha.y != 0.0) {
+      const double xnorm = sqrt(xs);
+      double beta = sqrt(alpha.x * alpha.x + alpha.y * alpha.y + xnorm * xnorm);
+      beta = alpha.x >= 0.0 ? -beta : beta;
+      tau = cmk((beta - alpha.x) / beta, -alpha.y / beta);
+      const cplx scal = crecip(cmk(alpha.x - beta, alpha.y));
+      for (int r = tid; r < m; r += ET) v[r] = r == 0 ? cmk(1.0, 0.0) : cmul(H[(j + 1 + r) * ld + j], scal);
+      __syncthreads();
+      if (tid == 0) H[(j + 1) * ld + j] = cmk(beta, 0.0);
+      for (int r = j + 2 + tid; r < k; r += ET) H[r * ld + j] = cmk(0.0, 0.0);
+      // left: H[j+1:, j+1:] -= conj(tau) v (v^H H)
+      for (int c = j + 1 + tid; c < k; c += ET) {
+        cplx s = cmk(0.0, 0.0);
+        for (int r = 0; r < m; ++r) cfma(s, cconj(v[r]), H[(j + 1 + r) * ld + c]);
+        wv[c] = s;
+      }
+      __syncthreads();
+      const cplx ct = cconj(tau);
+      for (int e = tid; e < m * (k - j - 1); e += ET) {
+        int r = e / (k - j - 1), c = j + 1 + e % (k - j - 1);
+        cfms(H[(j + 1 + r) * ld + c], cmul(ct, v[r]), wv[c]);
+      }
+      __syncthreads();
+      // right: H[:, j+1:] -= tau (H v) v^H ;  Z[:, j+1:] likewise
+      for (int r = tid; r < 2 * k; r += ET) {
+        const cplx* M = r < k ? H : Z;
+        const int rr = r < k ? r : r - k;
+        cplx s = cmk(0.0, 0.0);
+        for (int i = 0; i < m; ++i) cfma(s, M[rr * ld + j + 1 + i], v[i]);
+        wv[r] = s;
+      }
+      __syncthreads();
+      for (int e = tid; e < 2 * k * m; e += ET) {
+        int r = e / m, i = e % m;
+        cplx* M = r < k ? H : Z;
+        const int rr = r < k ? r : r - k;
+        cfms(M[rr * ld + j + 1 + i], cmul(tau, wv[r]), cconj(v[i]));
+      }
+      __syncthreads();
+    }
+  }
+  // 3. single-shift QR on the Hessenberg matrix (full Schur form + Z)
+  int ihi = k - 1;
+  const int itmax = 30 * (k > 10 ? k : 10);
+  int fail = 0;
+  while (ihi >= 0) {
+    int l = 0;
+    int its = 0;
+    for (; its <= itmax; ++its) {
+      // find the largest kk in (l, ihi] with a negligible subdiagonal
+      int found = l;
+      for (int kk = l + 1 + tid; kk <= ihi; kk += ET) {
+        const double hs = cabs1(H[kk * ld + kk - 1]);
+        double tst = cabs1(H[(kk - 1) * ld + kk - 1]) + cabs1(H[kk * ld + kk]);
+        if (tst == 0.0) {
+          if (kk - 2 >= l) tst += fabs(H[(kk - 1) * ld + kk - 2].x);
+          if (kk + 1 <= ihi) tst += fabs(H[(kk + 1) * ld + kk].x);
+        }
+        if (hs <= EPS * tst) found = max(found, kk);
+      }
+      for (int o = 16; o > 0; o >>= 1) found = max(found, __shfl_xor_sync(0xffffffffu, found, o));
+      if (lane == 0) ri[wid] = found;
+      __syncthreads();
+      if (tid == 0) {
+        int f = l;
+        for (int q = 0; q < ET / 32; ++q) f = max(f, ri[q]);
+        s_int[1] = f;
+        if (f > l) H[f * ld + f - 1] = cmk(0.0, 0.0);
+      }
+      __syncthreads();
+      l = s_int[1];
+      if (l >= ihi) break;
+      // shift
+      if (tid == 0) {
+        cplx mu;
+        if (its == 10) {
+          mu = cadd(cmk(0.75 * fabs(H[(l + 1) * ld + l].x), 0.0), H[l * ld + l]);
+        } else if (its == 20) {
+          mu = cadd(cmk(0.75 * fabs(H[ihi * ld + ihi - 1].x), 0.0), H[ihi * ld + ihi]);
+        } else {
+          cplx t = H[ihi * ld + ihi];
+          cplx u = cmul(csqrt_(H[(ihi - 1) * ld + ihi]), csqrt_(H[ihi * ld + ihi - 1]));
+          double s = cabs1(u);
+          if (s != 0.0) {
+            cplx x = cscale(csub(H[(ihi - 1) * ld + ihi - 1], t), 0.5);
+            double sx = cabs1(x);
+            s = fmax(s, sx);
+            cplx xs_ = cscale(x, 1.0 / s), us = cscale(u, 1.0 / s);
+            cplx y = cscale(csqrt_(cadd(cmul(xs_, xs_), cmul(us, us))), s);
+            if (sx > 0.0) {
+              cplx xn = cscale(x, 1.0 / sx);
+              if (xn.x * y.x + xn.y * y.y < 0.0) y = cmk(-y.x, -y.y);
+            }
+            t = csub(t, cmul(u, cdiv(u, cadd(x, y))));
+          }
+          mu = t;
+        }
+        s_c[0] = mu;
+      }
+      __syncthreads();
+      const cplx mu = s_c[0];
+      // QR sweep with Givens rotations over rows/cols l..ihi
+      for (int m = l; m < ihi; ++m) {
+        if (tid == 0) {
+          cplx x, y;
+          if (m == l) { x = csub(H[l * ld + l], mu); y = H[(l + 1) * ld + l]; }
+          else { x = H[m * ld + m - 1]; y = H[(m + 1) * ld + m - 1]; }
+          const double ax = cabs(x), ay = cabs(y);
+          double c; cplx s, r;
+          if (ay == 0.0) { c = 1.0; s = cmk(0.0, 0.0); r = x; }
+          else if (ax == 0.0) { c = 0.0; s = cscale(cconj(y), 1.0 / ay); r = cmk(ay, 0.0); }
+          else {
+            const double nrm = hypot(ax, ay);
+            c = ax / nrm;
+            const cplx ph = cscale(x, 1.0 / ax);
+            s = cscale(cmul(ph, cconj(y)), 1.0 / nrm);
+            r = cscale(ph, nrm);
+          }
+          if (m > l) { H[m * ld + m - 1] = r; H[(m + 1) * ld + m - 1] = cmk(0.0, 0.0); }
+          s_d[0] = c; s_c[1] = s;
+        }
+        __syncthreads();
+        const double c = s_d[0];
+        const cplx s = s_c[1], sc = cconj(s);
+        // left on rows m, m+1, columns m .. k-1
+        for (int col = m + tid; col < k; col += ET) {
+          cplx a = H[m * ld + col], b = H[(m + 1) * ld + col];
+          H[m * ld + col] = cadd(cscale(a, c), cmul(s, b));
+          H[(m + 1) * ld + col] = csub(cscale(b, c), cmul(sc, a));
+        }
+        __syncthreads();
+        // right on columns m, m+1: rows 0 .. min(m+2, ihi);  Z rows 0..k-1
+        const int rmax = min(m + 2, ihi);
+        for (int r = tid; r < k + rmax + 1; r += ET) {
+          cplx* M = r < k ? Z : H;
+          const int rr = r < k ? r : r - k;
+          cplx a = M[rr * ld + m], b = M[rr * ld + m + 1];
+          M[rr * ld + m] = cadd(cscale(a, c), cmul(sc, b));
+          M[rr * ld + m + 1] = csub(cscale(b, c), cmul(s, a));
+        }
+        __syncthreads();
+      }
+    }
+    if (its > itmax) { fail = ihi + 1; break; }
+    ihi = l - 1;
+  }
+  if (fail) {
+    if (tid == 0) info[prob] = -fail;
+    return;
+  }
+  // zero below the diagonal (Schur form is upper triangular)
+  for (int e = tid; e < k * k; e += ET) {
+    int r = e / k, c = e % k;
+    if (r > c) H[r * ld + c] = cmk(0.0, 0.0);
+  }
+  __syncthreads();
+  // 4. eigenvectors of T by back substitution: X[:, e]
+  double tnorm = 0.0;
+  for (int e = tid; e < k * k; e += ET) tnorm = fmax(tnorm, cabs1(H[e / k * ld + e % k]));
+  tnorm = block_max(tnorm, red);
+  const double smlnum = 1e-300 * (double)k / EPS;
+  for (int e = tid; e < k; e += ET) {
+    const cplx te = H[e * ld + e];
+    const double smin = fmax(EPS * cabs1(te), smlnum);
+    for (int r = k - 1; r > e; --r) X[r * ld + e] = cmk(0.0, 0.0);
+    X[e * ld + e] = cmk(1.0, 0.0);
+    for (int r = e - 1; r >= 0; --r) {
+      cplx acc = H[r * ld + e];
+      for (int c = r + 1; c < e; ++c) cfma(acc, H[r * ld + c], X[c * ld + e]);
+      cplx den = csub(H[r * ld + r], te);
+      if (cabs1(den) < smin) den = cmk(smin, 0.0);
+      X[r * ld + e] = cdiv(cmk(-acc.x, -acc.y), den);
+    }
+  }
+  __syncthreads();
+  // eigenvalue order: ascending by (re, im)
+  for (int i = tid; i < k; i += ET) {
+    const cplx li = H[i * ld + i];
+    int rank = 0;
+    for (int j = 0; j < k; ++j) {
+      const cplx lj = H[j * ld + j];
+      rank += (lj.x < li.x) || (lj.x == li.x && (lj.y < li.y || (lj.y == li.y && j < i)));
+    }
+    piv[i] = rank;
+    lam[(long long)prob * kmax + rank] = li;
+  }
+  __syncthreads();
+  // vectors Z X, unit 2-norm; column e of the Schur vectors -> S[:, rank]
+  cplx* Sp = S + (long long)prob * sS;
+  for (int e = wid; e < k; e += ET / 32) {
+    double nrm = 0.0;
+    for (int r = lane; r < k; r += 32) {
+      cplx acc = cmk(0.0, 0.0);
+      for (int c = 0; c <= e; ++c) cfma(acc, Z[r * ld + c], X[c * ld + e]);
+      Sp[(long long)r * lds + piv[e]] = acc;
+      nrm += cabs2(acc);
+    }
+    nrm = sqrt(warp_sum(nrm));
+    const double inv = nrm > 0.0 ? 1.0 / nrm : 1.0;
+    __syncwarp();
+    for (int r = lane; r < k; r += 32) {
+      cplx* p = Sp + (long long)r * lds + piv[e];
+      *p = cscale(*p, inv);
+    }
+  }
+  if (tid == 0) info[prob] = 0;
+}
+
+}  // namespace
+
+// Workspace bytes per problem for cirr_small_eig.
+CIRR_API long long cirr_small_eig_ws_bytes(int kmax) {
+  return (long long)kmax * kmax * 16 * 4 + (long long)kmax * 16 * 4 + (long long)kmax * 8 * 4 + 256;
+}
+
+// Eigen-decomposition of nprob projected pencils (A~, B~), each k_b x k_b
+// (kdim device array, k_b <= kmax <= 1024), row-major with ld ldin and batch
+// stride sin_.  hermitian != 0: Hermitian-definite path (eigh); else general
+// (eig).  lam: nprob x kmax complex (sorted); S: eigenvectors as columns;
+// info: 0 ok, >0 Cholesky/LU failure at that 1-based index, <0 QR failure.
+CIRR_API int cirr_small_eig(int hermitian, const cplx* At, const cplx* Bt, long long ldin, long long sin_,
+                            const int* kdim, int kmax, int nprob, void* ws, cplx* lam, cplx* S, long long lds,
+                            long long sS, int* info, cudaStream_t stream) {
+  if (kmax <= 0 || kmax > 1024 || nprob <= 0) return CIRR_EINVAL;
+  long long wstride = cirr_small_eig_ws_bytes(kmax);
+  wstride = (wstride + 255) / 256 * 256;
+  if (hermitian)
+    herm_eig_kernel<<<nprob, ET, 0, stream>>>(At, Bt, ldin, sin_, kdim, kmax, ws, wstride, lam, S, lds, sS, info);
+  else
+    gen_eig_kernel<<<nprob, ET, 0, stream>>>(At, Bt, ldin, sin_, kdim, kmax, ws, wstride, lam, S, lds, sS, info);
+  CIRR_CHECK_LAUNCH();
+  return 0;
+}

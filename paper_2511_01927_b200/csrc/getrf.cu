@@ -1,0 +1,263 @@
+// K2: batched blocked complex128 LU with partial pivoting (P M = L U).
+//
+// Replaces linalg.py:55-71 (`spla.splu` on z*B - A + the pivot test).  Per
+// panel step k (width NB): panel_kernel factors the m x NB panel in place
+// (one CTA per pencil; IB-wide sub-panels with a block-argmax pivot search,
+// then a TRSM+GEMM update of the rest of the panel), swap_kernel applies the
+// panel's interchanges outside it, trsm_kernel forms U12 = L11^-1 A12, and the
+// trailing update A22 -= L21 U12 runs on the FP64 tensor pipe (gemm.cuh,
+// DMMA).  Pivoting follows LAPACK zgetrf (izamax on |re|+|im|, first index on
+// ties).  The factorisation also reports per pencil min_i |U_ii| (the
+// reference's singular-shift test, linalg.py:68-70) and LAPACK-style info.
+#include "common.cuh"
+#include "gemm.cuh"
+
+namespace {
+
+constexpr int NB = 64;      // panel width
+constexpr int IB = 8;       // sub-panel width inside the panel kernel
+constexpr int PT = 512;     // panel kernel threads
+
+__global__ void __launch_bounds__(PT) panel_kernel(cplx* __restrict__ P, int n, long long ld,
+                                                   long long pstride, int k, int jb,
+                                                   int* __restrict__ ipiv, double* __restrict__ minpiv,
+                                                   int* __restrict__ info) {
+  __shared__ double rv[PT / 32];
+  __shared__ int ri[PT / 32];
+  __shared__ cplx prow[NB];           // pivot row segment of the sub-panel
+  __shared__ cplx ublk[IB][NB];       // U block for the panel-rest update
+  __shared__ int s_piv;
+  __shared__ cplx s_pval;
+  cplx* A = P + (long long)blockIdx.x * pstride;
+  int* piv = ipiv + (long long)blockIdx.x * n;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  double mp = minpiv[blockIdx.x];
+  int inf = info[blockIdx.x];
+
+  for (int c0 = 0; c0 < jb; c0 += IB) {
+    const int ib = min(IB, jb - c0);
+    for (int c = c0; c < c0 + ib; ++c) {
+      const int col = k + c, row0 = k + c;
+      // 1. pivot search (|re| + |im|, first maximal index)
+      double best = -1.0;
+      int bi = row0;
+      for (int r = row0 + tid; r < n; r += PT) {
+        double v = cabs1(A[(long long)r * ld + col]);
+        if (v > best) { best = v; bi = r; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        double ov = __shfl_xor_sync(0xffffffffu, best, o);
+        int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+      }
+      if (lane == 0) { rv[wid] = best; ri[wid] = bi; }
+      __syncthreads();
+      if (wid == 0) {
+        best = lane < PT / 32 ? rv[lane] : -1.0;
+        bi = lane < PT / 32 ? ri[lane] : n;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          double ov = __shfl_xor_sync(0xffffffffu, best, o);
+          int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+        }
+        if (lane == 0) {
+          s_piv = bi;
+          piv[row0] = bi;
+          s_pval = A[(long long)bi * ld + col];
+        }
+      }
+      __syncthreads();
+      const int p = s_piv;
+      const cplx pv = s_pval;
+      // 2. swap rows row0 <-> p over the whole panel width
+      if (p != row0) {
+        for (int cc = tid; cc < jb; cc += PT) {
+          cplx* x = A + (long long)row0 * ld + k + cc;
+          cplx* y = A + (long long)p * ld + k + cc;
+          cplx t = *x; *x = *y; *y = t;
+        }
+      }
+      __syncthreads();
+      // pivot row of the sub-panel (after the swap) to shared memory
+      for (int cc = tid; cc < c0 + ib - c; cc += PT) prow[cc] = A[(long long)row0 * ld + col + cc];
+      if (tid == 0) {
+        double a = cabs(pv);
+        mp = fmin(mp, a);
+        if (a == 0.0 && inf == 0) inf = row0 + 1;
+      }
+      __syncthreads();
+      // 3. scale + rank-1 update inside the sub-panel
+      const bool nz = (pv.x != 0.0 || pv.y != 0.0);
+      const cplx rp = nz ? crecip(pv) : cmk(0.0, 0.0);
+      const int rest = c0 + ib - c - 1;
+      for (int r = row0 + 1 + tid; r < n; r += PT) {
+        cplx* rowp = A + (long long)r * ld + col;
+        cplx l = nz ? cmul(rowp[0], rp) : rowp[0];
+        rowp[0] = l;
+        for (int cc = 1; cc <= rest; ++cc) {
+          cplx v = rowp[cc];
+          cfms(v, l, prow[cc]);
+          rowp[cc] = v;
+        }
+      }
+      __syncthreads();
+    }
+    // update the panel columns right of the sub-panel: [k+c0+ib, k+jb)
+    const int nr = jb - c0 - ib;
+    if (nr > 0) {
+      const int r0 = k + c0;
+      // U rows r0..r0+ib-1: forward substitution with the unit-lower L block
+      for (int cc = tid; cc < nr; cc += PT) {
+        const int colg = k + c0 + ib + cc;
+        cplx u[IB];
+        for (int i = 0; i < ib; ++i) {
+          cplx v = A[(long long)(r0 + i) * ld + colg];
+          for (int l = 0; l < i; ++l) cfms(v, A[(long long)(r0 + i) * ld + k + c0 + l], u[l]);
+          u[i] = v;
+          A[(long long)(r0 + i) * ld + colg] = v;
+          ublk[i][cc] = v;
+        }
+      }
+      __syncthreads();
+      // rows below: A[r][rest] -= L[r][c0:c0+ib] * U
+      for (int r = r0 + ib + tid; r < n; r += PT) {
+        cplx l[IB];
+        const cplx* lr = A + (long long)r * ld + k + c0;
+        for (int i = 0; i < ib; ++i) l[i] = lr[i];
+        cplx* dst = A + (long long)r * ld + k + c0 + ib;
+        for (int cc = 0; cc < nr; ++cc) {
+          cplx v = dst[cc];
+          for (int i = 0; i < ib; ++i) cfms(v, l[i], ublk[i][cc]);
+          dst[cc] = v;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (tid == 0) {
+    minpiv[blockIdx.x] = mp;
+    info[blockIdx.x] = inf;
+  }
+}
+
+// Apply interchanges ipiv[k .. k+jb) to the columns outside the panel.
+__global__ void swap_kernel(cplx* __restrict__ P, int n, long long ld, long long pstride, int k, int jb,
+                            const int* __restrict__ ipiv) {
+  const int other = n - jb;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= other) return;
+  const int col = t < k ? t : t + jb;
+  cplx* A = P + (long long)blockIdx.y * pstride;
+  const int* piv = ipiv + (long long)blockIdx.y * n;
+  for (int i = 0; i < jb; ++i) {
+    const int r1 = k + i, r2 = piv[k + i];
+    if (r1 != r2) {
+      cplx* x = A + (long long)r1 * ld + col;
+      cplx* y = A + (long long)r2 * ld + col;
+      cplx tt = *x; *x = *y; *y = tt;
+    }
+  }
+}
+
+// U12 = L11^{-1} A12 for a 32-column chunk; L11 unit lower (jb x jb).
+constexpr int TC = 32;
+constexpr int kTrsmSmem = (NB * (NB + 1) + NB * (TC + 1)) * 16;
+__global__ void __launch_bounds__(256) trsm_kernel(cplx* __restrict__ P, int n, long long ld,
+                                                   long long pstride, int k, int jb) {
+  extern __shared__ cplx tsm[];
+  cplx(*L)[NB + 1] = reinterpret_cast<cplx(*)[NB + 1]>(tsm);
+  cplx(*X)[TC + 1] = reinterpret_cast<cplx(*)[TC + 1]>(tsm + NB * (NB + 1));
+  cplx* A = P + (long long)blockIdx.y * pstride;
+  const int c0 = k + jb + blockIdx.x * TC;
+  const int nc = min(TC, n - c0);
+  for (int e = threadIdx.x; e < jb * jb; e += blockDim.x) {
+    int r = e / jb, c = e % jb;
+    L[r][c] = A[(long long)(k + r) * ld + k + c];
+  }
+  for (int e = threadIdx.x; e < jb * TC; e += blockDim.x) {
+    int r = e / TC, c = e % TC;
+    X[r][c] = c < nc ? A[(long long)(k + r) * ld + c0 + c] : cmk(0.0, 0.0);
+  }
+  __syncthreads();
+  const int c = threadIdx.x % TC, g = threadIdx.x / TC, ng = blockDim.x / TC;
+  for (int i = 0; i < jb - 1; ++i) {
+    const cplx xi = X[i][c];
+    for (int r = i + 1 + g; r < jb; r += ng) cfms(X[r][c], L[r][i], xi);
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < jb * TC; e += blockDim.x) {
+    int r = e / TC, cc = e % TC;
+    if (cc < nc) A[(long long)(k + r) * ld + c0 + cc] = X[r][cc];
+  }
+}
+
+// perm[i] = source row of row i of P*M (composition of the ipiv interchanges).
+__global__ void perm_kernel(const int* __restrict__ ipiv, int* __restrict__ perm, int n) {
+  extern __shared__ int sp[];
+  const int* piv = ipiv + (long long)blockIdx.x * n;
+  int* out = perm + (long long)blockIdx.x * n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) sp[i] = i;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < n; ++i) {
+      int p = piv[i];
+      if (p != i) { int t = sp[i]; sp[i] = sp[p]; sp[p] = t; }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = sp[i];
+}
+
+__global__ void init_kernel(double* minpiv, int* info, int batch) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < batch) { minpiv[i] = INFINITY; info[i] = 0; }
+}
+
+}  // namespace
+
+// In-place batched LU of `batch` complex n x n row-major matrices (stride
+// pencil_stride elements, leading dimension ld).  Outputs ipiv (batch x n,
+// 0-based LAPACK-style interchanges), perm (batch x n, row permutation),
+// minpiv (min_i |U_ii|) and info (first exact zero pivot, 1-based, or 0).
+CIRR_API int cirr_zgetrf_batched(cplx* pencils, int n, long long ld, long long pencil_stride, int batch,
+                                 int* ipiv, int* perm, double* minpiv, int* info, cudaStream_t stream) {
+  if (n <= 0 || batch <= 0 || ld < n) return CIRR_EINVAL;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrsmSmem);
+    attr = true;
+  }
+  init_kernel<<<(batch + 255) / 256, 256, 0, stream>>>(minpiv, info, batch);
+  CIRR_CHECK_LAUNCH();
+  for (int k = 0; k < n; k += NB) {
+    const int jb = min(NB, n - k);
+    panel_kernel<<<batch, PT, 0, stream>>>(pencils, n, ld, pencil_stride, k, jb, ipiv, minpiv, info);
+    CIRR_CHECK_LAUNCH();
+    if (n - jb > 0) {
+      dim3 g((n - jb + 255) / 256, batch);
+      swap_kernel<<<g, 256, 0, stream>>>(pencils, n, ld, pencil_stride, k, jb, ipiv);
+      CIRR_CHECK_LAUNCH();
+    }
+    const int rest = n - k - jb;
+    if (rest > 0) {
+      dim3 g2((rest + TC - 1) / TC, batch);
+      trsm_kernel<<<g2, 256, kTrsmSmem, stream>>>(pencils, n, ld, pencil_stride, k, jb);
+      CIRR_CHECK_LAUNCH();
+      cirr::GemmArgs ga{rest, rest, jb, batch,
+                        pencils + (long long)(k + jb) * ld + k, ld, pencil_stride,
+                        pencils + (long long)k * ld + k + jb, ld, pencil_stride,
+                        pencils + (long long)(k + jb) * ld + k + jb, ld, pencil_stride,
+                        -1.0, 1};
+      CIRR_TRY((cirr::gemm_launch<false, false>(ga, stream)));
+    }
+  }
+  if (perm) {
+    size_t sm = sizeof(int) * (size_t)n;
+    if (sm > 48 * 1024) cudaFuncSetAttribute(perm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    perm_kernel<<<batch, 256, sm, stream>>>(ipiv, perm, n);
+    CIRR_CHECK_LAUNCH();
+  }
+  return 0;
+}

@@ -1,0 +1,250 @@
+// K3: batched multi-RHS triangular solves against the LU factors, plus the
+// quadrature moment accumulation.
+//
+// Replaces linalg.py:46-52 (SuperLU gstrs) and solvers.py:113-130
+// (ProjectorContext.apply: BV once, then per node Y_j = (z_j B - A)^-1 BV and
+// S_m += w_j zeta_j^m Y_j).  Y_j = U^-1 L^-1 P BV_c(j):
+//   * permute_kernel gathers the contour's RHS rows through perm_j;
+//   * trsm_blocked_kernel<LOWER> walks 64-row blocks of one pencil for a
+//     32-column RHS chunk: the off-diagonal contribution sum_l T_il Y_l is a
+//     DMMA GEMM (cp.async double-buffered), the 64x64 diagonal block is
+//     solved in shared memory;
+//   * moments_kernel sums the nodes of each contour in fixed order
+//     (deterministic, test_solvers.py:192-198) reading every Y_j once and
+//     writes S transposed (one contiguous row per column of S) for K4.
+#include "common.cuh"
+
+namespace {
+
+constexpr int SNB = 64;           // block rows
+constexpr int SKC = 32;           // RHS columns per CTA
+constexpr int SBK = 16;           // GEMM k-step
+constexpr int SA_LD = SBK + 4;    // complex per A smem row
+constexpr int SB_LD = SKC + 2;    // complex per B smem row
+constexpr int SD_LD = SNB + 1;    // diagonal block row
+constexpr int SX_LD = SKC + 1;
+constexpr int kStageA = SNB * SA_LD;
+constexpr int kStageB = SBK * SB_LD;
+constexpr int kSolveSmem = (2 * (kStageA + kStageB) + SNB * SD_LD + SNB * SX_LD + SNB) * 16;
+
+template <bool LOWER>
+__global__ void __launch_bounds__(256, 1) trsm_blocked_kernel(const cplx* __restrict__ LU, long long ld,
+                                                              long long pstride, int n,
+                                                              cplx* __restrict__ Y, long long ldy,
+                                                              long long ystride, int K) {
+  extern __shared__ __align__(16) cplx ssm[];
+  cplx* stA = ssm;                                   // 2 stages
+  cplx* stB = ssm + 2 * kStageA;
+  cplx* D = ssm + 2 * (kStageA + kStageB);           // diagonal block
+  cplx* X = D + SNB * SD_LD;                         // RHS block
+  cplx* dinv = X + SNB * SX_LD;
+  const int b = blockIdx.y;
+  const int c0 = blockIdx.x * SKC;
+  const cplx* T = LU + (long long)b * pstride;
+  cplx* Yb = Y + (long long)b * ystride;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp >> 1) * 16, wn = (warp & 1) * 16;
+  const int nblk = (n + SNB - 1) / SNB;
+
+  for (int step = 0; step < nblk; ++step) {
+    const int bi = LOWER ? step : nblk - 1 - step;
+    const int i0 = bi * SNB;
+    const int nbi = min(SNB, n - i0);
+    // k-range of the off-diagonal product
+    const int kbeg = LOWER ? 0 : i0 + nbi;
+    const int kend = LOWER ? i0 : n;
+    const int klen = kend - kbeg;
+
+    double cr[2][2][2], ci[2][2][2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
+
+    auto load = [&](int stage, int kk) {
+      cplx* As = stA + stage * kStageA;
+      cplx* Bs = stB + stage * kStageB;
+#pragma unroll
+      for (int t = 0; t < (SNB * SBK) / 256; ++t) {
+        int e = tid + t * 256, r = e / SBK, c = e % SBK;
+        int gr = i0 + r, gc = kbeg + kk + c;
+        bool p = r < nbi && gc < kend;
+        cp_async16(As + r * SA_LD + c, p ? T + (long long)gr * ld + gc : T, p);
+      }
+#pragma unroll
+      for (int t = 0; t < (SBK * SKC) / 256; ++t) {
+        int e = tid + t * 256, r = e / SKC, c = e % SKC;
+        int gr = kbeg + kk + r, gc = c0 + c;
+        bool p = gr < kend && gc < K;
+        cp_async16(Bs + r * SB_LD + c, p ? Yb + (long long)gr * ldy + gc : Yb, p);
+      }
+    };
+
+    if (klen > 0) {
+      const int kt = (klen + SBK - 1) / SBK;
+      load(0, 0);
+      cp_async_commit();
+      for (int t = 0; t < kt; ++t) {
+        if (t + 1 < kt) load((t + 1) & 1, (t + 1) * SBK);
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncthreads();
+        const cplx* As = stA + (t & 1) * kStageA;
+        const cplx* Bs = stB + (t & 1) * kStageB;
+#pragma unroll
+        for (int kk = 0; kk < SBK; kk += 4) {
+          cplx af[2], bf[2];
+#pragma unroll
+          for (int i = 0; i < 2; ++i) af[i] = As[(wm + i * 8 + (lane >> 2)) * SA_LD + kk + (lane & 3)];
+#pragma unroll
+          for (int j = 0; j < 2; ++j) bf[j] = Bs[(kk + (lane & 3)) * SB_LD + wn + j * 8 + (lane >> 2)];
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              dmma884(cr[i][j][0], cr[i][j][1], af[i].x, bf[j].x);
+              dmma884(ci[i][j][0], ci[i][j][1], af[i].x, bf[j].y);
+            }
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              dmma884(cr[i][j][0], cr[i][j][1], -af[i].y, bf[j].y);
+              dmma884(ci[i][j][0], ci[i][j][1], af[i].y, bf[j].x);
+            }
+        }
+        __syncthreads();
+      }
+    }
+    // load the diagonal block and the RHS block
+    for (int e = tid; e < SNB * SNB; e += 256) {
+      int r = e / SNB, c = e % SNB;
+      D[r * SD_LD + c] = (r < nbi && c < nbi) ? T[(long long)(i0 + r) * ld + i0 + c] : cmk(0.0, 0.0);
+    }
+    for (int e = tid; e < SNB * SKC; e += 256) {
+      int r = e / SKC, c = e % SKC;
+      X[r * SX_LD + c] = (r < nbi && c0 + c < K) ? Yb[(long long)(i0 + r) * ldy + c0 + c] : cmk(0.0, 0.0);
+    }
+    __syncthreads();
+    // X -= accumulated off-diagonal product
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          int r = wm + i * 8 + (lane >> 2), c = wn + j * 8 + 2 * (lane & 3) + h;
+          cplx v = X[r * SX_LD + c];
+          X[r * SX_LD + c] = cmk(v.x - cr[i][j][h], v.y - ci[i][j][h]);
+        }
+    if (!LOWER && tid < SNB) dinv[tid] = tid < nbi ? crecip(D[tid * SD_LD + tid]) : cmk(0.0, 0.0);
+    __syncthreads();
+    // diagonal solve: thread column c, row group g
+    const int c = tid % SKC, g = tid / SKC;
+    if (LOWER) {
+      for (int i = 0; i < nbi - 1; ++i) {
+        const cplx xi = X[i * SX_LD + c];
+        for (int r = i + 1 + g; r < nbi; r += 8) cfms(X[r * SX_LD + c], D[r * SD_LD + i], xi);
+        __syncthreads();
+      }
+    } else {
+      for (int i = nbi - 1; i >= 0; --i) {
+        const cplx xi = cmul(X[i * SX_LD + c], dinv[i]);
+        __syncthreads();
+        if (g == 0) X[i * SX_LD + c] = xi;
+        for (int r = g; r < i; r += 8) cfms(X[r * SX_LD + c], D[r * SD_LD + i], xi);
+        __syncthreads();
+      }
+    }
+    for (int e = tid; e < nbi * SKC; e += 256) {
+      int r = e / SKC, cc = e % SKC;
+      if (c0 + cc < K) Yb[(long long)(i0 + r) * ldy + c0 + cc] = X[r * SX_LD + cc];
+    }
+    __syncthreads();
+  }
+}
+
+// Y[j][i][c] = R[rhs_of[j]][perm[j][i]][c]
+__global__ void permute_kernel(const cplx* __restrict__ R, long long ldr, long long rstride,
+                               const int* __restrict__ rhs_of, const int* __restrict__ perm, int n, int K,
+                               cplx* __restrict__ Y, long long ldy, long long ystride) {
+  const int j = blockIdx.y;
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (long long)n * K) return;
+  const int i = (int)(e / K), c = (int)(e % K);
+  const cplx* Rj = R + (long long)rhs_of[j] * rstride;
+  const int src = perm[(long long)j * n + i];
+  Y[(long long)j * ystride + (long long)i * ldy + c] = Rj[(long long)src * ldr + c];
+}
+
+constexpr int MAXM = 16;
+// St[c][m*K + col][r] = sum_{j in contour c, in order} coef[j][m] * Y_j[r][col]
+__global__ void __launch_bounds__(256) moments_kernel(const cplx* __restrict__ Y, long long ldy,
+                                                      long long ystride, int n, int K,
+                                                      const cplx* __restrict__ coef, int M,
+                                                      const int* __restrict__ off, cplx* __restrict__ St,
+                                                      long long ld_st, long long sstride) {
+  const int cidx = blockIdx.y;
+  const int r = blockIdx.x * 64 + (threadIdx.x & 63);
+  const int cg = threadIdx.x >> 6;
+  if (r >= n) return;
+  const int j0 = off[cidx], j1 = off[cidx + 1];
+  cplx* S = St + (long long)cidx * sstride;
+  for (int col = cg; col < K; col += 4) {
+    cplx acc[MAXM];
+#pragma unroll
+    for (int m = 0; m < MAXM; ++m) acc[m] = cmk(0.0, 0.0);
+    for (int j = j0; j < j1; ++j) {
+      const cplx y = Y[(long long)j * ystride + (long long)r * ldy + col];
+#pragma unroll
+      for (int m = 0; m < MAXM; ++m)
+        if (m < M) cfma(acc[m], coef[(long long)j * M + m], y);
+    }
+#pragma unroll
+    for (int m = 0; m < MAXM; ++m)
+      if (m < M) S[(long long)(m * K + col) * ld_st + r] = acc[m];
+  }
+}
+
+}  // namespace
+
+// Y_j = (P_j^T L_j U_j)^{-1} R_{rhs_of[j]} for j < batch.  LU/perm from
+// cirr_zgetrf_batched; R: (n_rhs_sets) x n x K, row-major, ld ldr, stride
+// rstride; Y: batch x n x K (ld ldy, stride ystride).  rhs_of is a device
+// int32 array.
+CIRR_API int cirr_zgetrs_batched(const cplx* LU, int n, long long ld, long long pencil_stride, int batch,
+                                 const int* perm, const cplx* R, long long ldr, long long rstride,
+                                 const int* rhs_of, int K, cplx* Y, long long ldy, long long ystride,
+                                 cudaStream_t stream) {
+  if (n <= 0 || batch <= 0 || K < 0 || ldy < K || ldr < K) return CIRR_EINVAL;
+  if (K == 0) return 0;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(trsm_blocked_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSolveSmem);
+    cudaFuncSetAttribute(trsm_blocked_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSolveSmem);
+    attr = true;
+  }
+  dim3 gp((unsigned)(((long long)n * K + 255) / 256), batch);
+  permute_kernel<<<gp, 256, 0, stream>>>(R, ldr, rstride, rhs_of, perm, n, K, Y, ldy, ystride);
+  CIRR_CHECK_LAUNCH();
+  dim3 gs((K + SKC - 1) / SKC, batch);
+  trsm_blocked_kernel<true><<<gs, 256, kSolveSmem, stream>>>(LU, ld, pencil_stride, n, Y, ldy, ystride, K);
+  CIRR_CHECK_LAUNCH();
+  trsm_blocked_kernel<false><<<gs, 256, kSolveSmem, stream>>>(LU, ld, pencil_stride, n, Y, ldy, ystride, K);
+  CIRR_CHECK_LAUNCH();
+  return 0;
+}
+
+// Moment blocks of n_sets contours: pencils off[c] .. off[c+1]-1 belong to
+// contour c; coef[j*M + m] = w_j zeta_j^m.  Output St[c] is (M*K) x n
+// row-major (row m*K+col = column col of S_m), ld ld_st, stride sstride.
+CIRR_API int cirr_moments(const cplx* Y, long long ldy, long long ystride, int n, int K, const cplx* coef,
+                          int M, const int* off, int n_sets, cplx* St, long long ld_st, long long sstride,
+                          cudaStream_t stream) {
+  if (n <= 0 || K < 0 || M < 1 || M > MAXM || n_sets <= 0) return CIRR_EINVAL;
+  if (K == 0) return 0;
+  dim3 g((n + 63) / 64, n_sets);
+  moments_kernel<<<g, 256, 0, stream>>>(Y, ldy, ystride, n, K, coef, M, off, St, ld_st, sstride);
+  CIRR_CHECK_LAUNCH();
+  return 0;
+}

@@ -1,0 +1,55 @@
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and libcirr.so")
+    config.addinivalue_line("markers", "slow: full-size BASELINE configs (minutes)")
+
+
+def golden(name):
+    return np.load(os.path.join(GOLDEN, name), allow_pickle=False)
+
+
+def csr_dense(g, prefix):
+    import scipy.sparse as sp
+    n = int(g[prefix.split("_")[0] + "_n"])
+    m = sp.csr_matrix((g[prefix + "_data"], g[prefix + "_indices"], g[prefix + "_indptr"]), shape=(n, n))
+    return m.toarray()
+
+
+class DensePencil:
+    """Minimal pencil object (duck-typed like cieig.MatrixPencil)."""
+
+    def __init__(self, a, b, hermitian=True):
+        self.a = np.asarray(a)
+        self.b = np.asarray(b)
+        self.hermitian = hermitian
+
+    @property
+    def n(self):
+        return self.a.shape[0]
+
+
+def diag_pencil(da, db=None):
+    a = np.diag(np.asarray(da, dtype=float))
+    b = np.eye(len(da)) if db is None else np.diag(np.asarray(db, dtype=float))
+    return DensePencil(a, b, True)
+
+
+@pytest.fixture(scope="session")
+def thermal():
+    g = golden("ref_thermal.npz")
+    return {
+        "t10": DensePencil(csr_dense(g, "t10_a").real, csr_dense(g, "t10_b").real),
+        "t20": DensePencil(csr_dense(g, "t20_a").real, csr_dense(g, "t20_b").real),
+        "g": g,
+    }

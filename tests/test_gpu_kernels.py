@@ -1,0 +1,195 @@
+"""Per-kernel numerics on the B200 (each kernel vs numpy/scipy on seeded inputs)."""
+import numpy as np
+import pytest
+import scipy.linalg as sla
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not torch.cuda.is_available():
+        pytest.fail("gpu test without CUDA")
+    from paper_2511_01927_b200 import _lib
+    return _lib
+
+
+def P(t):
+    return t.data_ptr()
+
+
+def S():
+    return torch.cuda.current_stream().cuda_stream
+
+
+_KEEP = []
+
+
+def cuda(x):
+    """Device copy kept alive for the test module (raw pointers outlive temporaries)."""
+    t = torch.from_numpy(np.ascontiguousarray(x)).to("cuda")
+    _KEEP.append(t)
+    if len(_KEEP) > 64:
+        del _KEEP[:32]
+    return t
+
+
+@pytest.mark.parametrize("n", [5, 64, 300])
+def test_assemble_bitwise(lib, n):
+    rng = np.random.default_rng(n)
+    a = rng.standard_normal((n, n))
+    b = rng.standard_normal((n, n))
+    z = rng.standard_normal(11) + 1j * rng.standard_normal(11)
+    out = torch.empty((11, n, n), dtype=torch.complex128, device="cuda")
+    mx = torch.empty(11, dtype=torch.float64, device="cuda")
+    lib.call("cirr_assemble", P(cuda(a)), P(cuda(b)), n, n, P(cuda(z)), 11, P(out), n, n * n, P(mx), S())
+    got = out.cpu().numpy()
+    for j in range(11):
+        ref = z[j] * b - a
+        assert np.array_equal(got[j].view(np.float64), ref.view(np.float64)), j
+        assert mx.cpu().numpy()[j] == pytest.approx(np.abs(ref).max(), rel=1e-15)
+
+
+@pytest.mark.parametrize("kind", [0, 1, 2])
+@pytest.mark.parametrize("shape", [(64, 64, 64), (100, 37, 250), (7, 130, 5), (256, 256, 4096)])
+def test_gemm(lib, kind, shape):
+    M, N, K = shape
+    rng = np.random.default_rng(M + N + K + kind)
+    batch = 2
+    if kind == 2:
+        A = rng.standard_normal((batch, M, K))
+    else:
+        A = rng.standard_normal((batch, M, K)) + 1j * rng.standard_normal((batch, M, K))
+    B = rng.standard_normal((batch, K, N)) + 1j * rng.standard_normal((batch, K, N))
+    C0 = rng.standard_normal((batch, M, N)) + 1j * rng.standard_normal((batch, M, N))
+    opA = np.conj(A) if kind == 1 else A
+    for beta in (0, 1):
+        C = cuda(C0.copy())
+        lib.call("cirr_gemm", kind, M, N, K, batch, P(cuda(A)), K, M * K, P(cuda(B)), N, K * N, P(C), N, M * N,
+                 -0.5, beta, S())
+        ref = beta * C0 - 0.5 * opA @ B
+        err = np.abs(C.cpu().numpy() - ref).max() / max(1.0, np.abs(ref).max())
+        assert err < 1e-13 * np.sqrt(K), (beta, err)
+
+
+@pytest.mark.parametrize("n,batch", [(3, 2), (100, 3), (256, 4), (333, 2), (1024, 2)])
+def test_getrf_getrs(lib, n, batch):
+    rng = np.random.default_rng(n)
+    A = rng.standard_normal((batch, n, n)) + 1j * rng.standard_normal((batch, n, n))
+    F = cuda(A.copy())
+    ipiv = torch.empty((batch, n), dtype=torch.int32, device="cuda")
+    perm = torch.empty((batch, n), dtype=torch.int32, device="cuda")
+    mp = torch.empty(batch, dtype=torch.float64, device="cuda")
+    info = torch.empty(batch, dtype=torch.int32, device="cuda")
+    lib.call("cirr_zgetrf_batched", P(F), n, n, n * n, batch, P(ipiv), P(perm), P(mp), P(info), S())
+    assert (info.cpu().numpy() == 0).all()
+    K = 37
+    R = rng.standard_normal((2, n, K)) + 1j * rng.standard_normal((2, n, K))
+    rhs_of = cuda(np.arange(batch, dtype=np.int32) % 2)
+    Y = torch.empty((batch, n, K), dtype=torch.complex128, device="cuda")
+    lib.call("cirr_zgetrs_batched", P(F), n, n, n * n, batch, P(perm), P(cuda(R)), K, n * K, P(rhs_of), K, P(Y), K,
+             n * K, S())
+    y = Y.cpu().numpy()
+    lu = F.cpu().numpy()
+    for j in range(batch):
+        r = R[j % 2]
+        res = np.linalg.norm(A[j] @ y[j] - r) / (np.linalg.norm(A[j]) * np.linalg.norm(y[j]))
+        assert res < 1e-14, res
+        # LAPACK agreement on the pivots' magnitudes
+        lu_ref, piv_ref = sla.lu_factor(A[j])
+        assert np.allclose(np.sort(np.abs(np.diag(lu[j]))), np.sort(np.abs(np.diag(lu_ref))), rtol=1e-8)
+        assert mp.cpu().numpy()[j] == pytest.approx(np.abs(np.diag(lu[j])).min())
+
+
+def test_getrf_singular(lib):
+    n = 70
+    A = np.diag(np.arange(1.0, n + 1)).astype(complex)
+    A[5, 5] = 0.0
+    F = cuda(A[None].copy())
+    ipiv = torch.empty((1, n), dtype=torch.int32, device="cuda")
+    mp = torch.empty(1, dtype=torch.float64, device="cuda")
+    info = torch.empty(1, dtype=torch.int32, device="cuda")
+    lib.call("cirr_zgetrf_batched", P(F), n, n, n * n, 1, P(ipiv), 0, P(mp), P(info), S())
+    assert info.item() == 6 and mp.item() == 0.0
+
+
+@pytest.mark.parametrize("n,c", [(500, 12), (4096, 64)])
+def test_orth_graded(lib, n, c):
+    rng = np.random.default_rng(c)
+    U, _ = np.linalg.qr(rng.standard_normal((n, c)) + 1j * rng.standard_normal((n, c)))
+    V, _ = np.linalg.qr(rng.standard_normal((c, c)) + 1j * rng.standard_normal((c, c)))
+    s = np.logspace(0, -14, c)
+    s[(s > 2e-13) & (s < 5e-12)] = 1e-11  # keep the 1e-12 cut away from any sigma
+    Smat = (U * s) @ V.conj().T
+    W = cuda(np.ascontiguousarray(Smat.T))
+    sig = torch.empty(c, dtype=torch.float64, device="cuda")
+    order = torch.empty(c, dtype=torch.int32, device="cuda")
+    kept = torch.empty(1, dtype=torch.int32, device="cuda")
+    Qt = torch.empty((c, n), dtype=torch.complex128, device="cuda")
+    ws = torch.zeros(16, dtype=torch.int32, device="cuda")
+    sw = torch.zeros(1, dtype=torch.int32, device="cuda")
+    lib.call("cirr_orth", P(W), n, c * n, n, c, 1, 1e-12, P(sig), P(order), P(kept), P(Qt), n, c * n, P(ws), P(sw),
+             S())
+    k = kept.item()
+    ref = np.linalg.svd(Smat, compute_uv=False)
+    got = sig.cpu().numpy()
+    assert np.allclose(got, ref, rtol=1e-3, atol=1e-15), (got, ref, sw.item())
+    assert np.allclose(got[:k], ref[:k], rtol=1e-6, atol=1e-15)
+    assert k == int(np.count_nonzero(ref >= 1e-12 * ref[0]))
+    q = Qt.cpu().numpy()[:k].T
+    assert np.abs(q.conj().T @ q - np.eye(k)).max() < 1e-12
+    # span: the kept basis captures S up to the dropped singular values
+    resid = np.linalg.norm(Smat - q @ (q.conj().T @ Smat), 2)
+    assert resid <= 1e-13 * ref[0] + (ref[k] if k < c else 0.0)
+
+
+@pytest.mark.parametrize("k", [1, 6, 64, 200])
+def test_small_eig_hermitian(lib, k):
+    rng = np.random.default_rng(k)
+    x = rng.standard_normal((k, k)) + 1j * rng.standard_normal((k, k))
+    a = x + x.conj().T
+    y = rng.standard_normal((k, k)) + 1j * rng.standard_normal((k, k))
+    b = y @ y.conj().T + k * np.eye(k)
+    lam, s, info = _small(lib, a, b, k, 1)
+    assert info == 0
+    w = sla.eigh(a, b, eigvals_only=True)
+    assert np.allclose(lam.real, w, rtol=1e-10, atol=1e-12 * np.abs(w).max())
+    r = a @ s - (b @ s) * lam.real[None, :]
+    assert np.abs(r).max() <= 1e-10 * (np.linalg.norm(a) + np.abs(lam).max() * np.linalg.norm(b))
+    assert np.abs(s.conj().T @ b @ s - np.eye(k)).max() < 1e-10
+
+
+@pytest.mark.parametrize("k", [2, 7, 64, 180])
+def test_small_eig_general(lib, k):
+    rng = np.random.default_rng(100 + k)
+    a = rng.standard_normal((k, k)) + 1j * rng.standard_normal((k, k))
+    b = np.eye(k) + 0.05 * (rng.standard_normal((k, k)) + 1j * rng.standard_normal((k, k)))
+    lam, s, info = _small(lib, a, b, k, 0)
+    assert info == 0
+    w = sla.eig(a, b, right=False)
+    w = w[np.lexsort((w.imag, w.real))]
+    assert np.abs(lam - w).max() < 1e-10 * np.abs(w).max()
+    r = a @ s - (b @ s) * lam[None, :]
+    rel = np.linalg.norm(r, axis=0) / (np.linalg.norm(a @ s, axis=0) + np.abs(lam) * np.linalg.norm(b @ s, axis=0))
+    assert rel.max() < 1e-11
+
+
+def test_small_eig_indefinite(lib):
+    a = np.eye(2, dtype=complex)
+    b = np.diag([1.0, -1.0]).astype(complex)
+    _, _, info = _small(lib, a, b, 2, 1)
+    assert info == 2
+
+
+def _small(lib, a, b, k, herm):
+    kd = torch.tensor([k], dtype=torch.int32, device="cuda")
+    wsb = lib.call("cirr_small_eig_ws_bytes", k)
+    ws = torch.empty(wsb + 256, dtype=torch.uint8, device="cuda")
+    lam = torch.empty(k, dtype=torch.complex128, device="cuda")
+    s = torch.empty((k, k), dtype=torch.complex128, device="cuda")
+    info = torch.zeros(1, dtype=torch.int32, device="cuda")
+    lib.call("cirr_small_eig", herm, P(cuda(a)), P(cuda(b)), k, k * k, P(kd), k, 1, P(ws), P(lam), P(s), k, k * k,
+             P(info), S())
+    return lam.cpu().numpy(), s.cpu().numpy(), info.item()
