@@ -37,6 +37,9 @@ int cirr_assemble(const double* A, const double* B, int n, long long lda,
                   const cirr_cplx* z, int nz, cirr_cplx* pencils, long long ldp,
                   long long pencil_stride, double* maxabs, cudaStream_t stream);
 
+/* sparse.py:83-87 (is_hermitian) for real A: out[0] = max|A - A^T|, out[1] = max|A|. */
+int cirr_symmetry(const double* A, int n, long long lda, double* out, cudaStream_t stream);
+
 /* K2 -- replaces linalg.py:65-70 (splu + the 1e-14 pivot test inputs).
  * In-place P M = L U of `batch` pencils; ipiv/perm: batch x n int32;
  * minpiv[j] = min_i |U_ii|; info[j] = first exact zero pivot (1-based) or 0. */
@@ -93,6 +96,9 @@ int cirr_gather_cols(const cirr_cplx* in, long long ldi, long long si, const int
 /* layout helper: out[b] = in[b]^T (or ^H when conj != 0) */
 int cirr_transpose(int conj, const cirr_cplx* in, long long ldi, long long si, int rows, int cols,
                    int batch, cirr_cplx* out, long long ldo, long long so, cudaStream_t stream);
+
+/* number of kernels this library has launched since it was loaded (host counter) */
+long long cirr_launch_count(void);
 
 /* library identification: compute capability the cubins target (100 = sm_100a) */
 int cirr_target_sm(void);

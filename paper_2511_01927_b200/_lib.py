@@ -24,6 +24,7 @@ _D = ctypes.c_double
 # name -> argtypes (all return int unless listed in _RESTYPE)
 SIGNATURES = {
     "cirr_assemble": [_P, _P, _I, _L, _P, _I, _P, _L, _L, _P, _P],
+    "cirr_symmetry": [_P, _I, _L, _P, _P],
     "cirr_zgetrf_batched": [_P, _I, _L, _L, _I, _P, _P, _P, _P, _P],
     "cirr_zgetrs_batched": [_P, _I, _L, _L, _I, _P, _P, _L, _L, _P, _I, _P, _L, _L, _P],
     "cirr_moments": [_P, _L, _L, _I, _I, _P, _I, _P, _I, _P, _L, _L, _P],
@@ -35,8 +36,10 @@ SIGNATURES = {
     "cirr_gather_cols": [_P, _L, _L, _P, _L, _P, _I, _I, _I, _P, _L, _L, _P],
     "cirr_transpose": [_I, _P, _L, _L, _I, _I, _I, _P, _L, _L, _P],
     "cirr_target_sm": [],
+    "cirr_launch_count": [],
 }
-_RESTYPE = {"cirr_small_eig_ws_bytes": _L}
+_RESTYPE = {"cirr_small_eig_ws_bytes": _L, "cirr_launch_count": _L}
+_RAW = {"cirr_small_eig_ws_bytes", "cirr_launch_count", "cirr_target_sm"}
 
 _lib = None
 
@@ -61,7 +64,7 @@ def call(name: str, *args):
     """Invoke an entry point and turn a non-zero status into DeviceError."""
     fn = getattr(load(), name)
     rc = fn(*args)
-    if name in _RESTYPE:
+    if name in _RAW:
         return rc
     if rc != 0:
         if rc == EINVAL:

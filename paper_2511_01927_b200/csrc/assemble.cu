@@ -64,7 +64,47 @@ __global__ void __launch_bounds__(kThreads) assemble_kernel(
   }
 }
 
+// out[0] = max_ij |A_ij - A_ji|, out[1] = max_ij |A_ij| (as ordered bit patterns)
+__global__ void symmetry_kernel(const double* __restrict__ A, int n, long long lda,
+                                unsigned long long* __restrict__ out) {
+  __shared__ double red[2][8];
+  double d = 0.0, m = 0.0;
+  const long long total = (long long)n * n;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long r = e / n, c = e - r * n;
+    const double a = A[r * lda + c];
+    m = fmax(m, fabs(a));
+    if (c > r) d = fmax(d, fabs(a - A[c * lda + r]));
+  }
+  d = warp_max(d);
+  m = warp_max(m);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) { red[0][wid] = d; red[1][wid] = m; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) { d = fmax(d, red[0][w]); m = fmax(m, red[1][w]); }
+    d = fmax(d, red[0][0]);
+    m = fmax(m, red[1][0]);
+    atomicMax(out, (unsigned long long)__double_as_longlong(d));
+    atomicMax(out + 1, (unsigned long long)__double_as_longlong(m));
+  }
+}
+
 }  // namespace
+
+// out[0] = max |A - A^T|, out[1] = max |A| for a real row-major matrix
+// (the Hermitian test of sparse.py:83-87 on device).
+CIRR_API int cirr_symmetry(const double* A, int n, long long lda, double* out, cudaStream_t stream) {
+  if (n <= 0 || lda < n) return CIRR_EINVAL;
+  cudaError_t e = cudaMemsetAsync(out, 0, 2 * sizeof(double), stream);
+  if (e != cudaSuccess) return (int)e;
+  long long total = (long long)n * n;
+  int blocks = (int)((total + 255) / 256 < 148 * 8 ? (total + 255) / 256 : 148 * 8);
+  symmetry_kernel<<<blocks, 256, 0, stream>>>(A, n, lda, reinterpret_cast<unsigned long long*>(out));
+  CIRR_CHECK_LAUNCH();
+  return 0;
+}
 
 // pencils[j] = z[j]*B - A (j < nz); maxabs[j] = max_ij |pencils[j]_ij|.
 CIRR_API int cirr_assemble(const double* A, const double* B, int n, long long lda,

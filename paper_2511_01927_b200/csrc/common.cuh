@@ -13,8 +13,13 @@ typedef double2 cplx;
 // Every C-ABI entry returns 0 on success or a cudaError_t value (> 0);
 // argument errors return CIRR_EINVAL.
 
+// Host-side count of kernels this library has launched (cirr_launch_count).
+extern long long g_cirr_launches;
+inline void cirr_note_launch() { __atomic_fetch_add(&g_cirr_launches, 1, __ATOMIC_RELAXED); }
+
 #define CIRR_CHECK_LAUNCH()                              \
   do {                                                   \
+    cirr_note_launch();                                  \
     cudaError_t _e = cudaGetLastError();                 \
     if (_e != cudaSuccess) return (int)_e;               \
   } while (0)

@@ -35,5 +35,10 @@ CIRR_API int cirr_gemm(int a_kind, int M, int N, int K, int batch,
   }
 }
 
+long long g_cirr_launches = 0;
+
+// Number of kernels launched by this library since load (host counter).
+CIRR_API long long cirr_launch_count(void) { return __atomic_load_n(&g_cirr_launches, __ATOMIC_RELAXED); }
+
 // 100 = the cubins in this library target sm_100a (B200).
 CIRR_API int cirr_target_sm(void) { return 100; }

@@ -176,6 +176,7 @@ inline int gemm_launch(const GemmArgs& g, cudaStream_t stream) {
   if (g.K <= 0) return 0;  // callers handle beta with K == 0 themselves
   dim3 grid((g.N + GBN - 1) / GBN, (g.M + GBM - 1) / GBM, g.batch);
   gemm_kernel<A_REAL, A_CONJ><<<grid, GTHREADS, S::total, stream>>>(g);
+  cirr_note_launch();
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : (int)e;
 }

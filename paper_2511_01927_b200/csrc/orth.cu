@@ -191,6 +191,7 @@ CIRR_API int cirr_orth(cplx* W, long long ldw, long long wstride, int n, int c, 
     int max_sweeps = 40;
     void* args[] = {&W, &ldw, &wstride, &n, &c, &nprob, &bar, &counters, &max_sweeps, &tol, &sweeps_out};
     e = cudaLaunchCooperativeKernel((void*)hestenes_kernel, dim3(grid), dim3(HT), args, 0, stream);
+    cirr_note_launch();
     if (e != cudaSuccess) return (int)e;
   } else {
     e = cudaMemsetAsync(sweeps_out, 0, sizeof(int), stream);

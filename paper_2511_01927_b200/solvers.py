@@ -175,6 +175,9 @@ class DevicePencil:
 
     def __init__(self, a, b, hermitian: bool | None = None):
         torch = _torch()
+        if isinstance(a, torch.Tensor) and isinstance(b, torch.Tensor):
+            self._from_tensors(torch, a, b, hermitian)
+            return
         a = np.asarray(_dense(a))
         b = np.asarray(_dense(b))
         if a.ndim != 2 or a.shape[0] != a.shape[1] or a.shape != b.shape:
@@ -186,11 +189,32 @@ class DevicePencil:
         a = np.ascontiguousarray(a.real, dtype=np.float64)
         b = np.ascontiguousarray(b.real, dtype=np.float64)
         self.n = a.shape[0]
-        if hermitian is None or hermitian is False:
-            hermitian = _is_symmetric(a) and _is_symmetric(b)
-        self.hermitian = bool(hermitian)
         self.a = torch.from_numpy(a).to("cuda")
         self.b = torch.from_numpy(b).to("cuda")
+        self.hermitian = bool(hermitian) if hermitian else self._device_symmetric()
+
+    def _device_symmetric(self, rel_tol: float = 1e-12) -> bool:
+        """sparse.py:83-87 applied to A and B on the device (a flag of False or
+        None means 'unknown' here, as the reference's default is False)."""
+        torch = _torch()
+        out = torch.empty((2, 2), dtype=torch.float64, device="cuda")
+        st = _stream()
+        _lib.call("cirr_symmetry", _ptr(self.a), self.n, self.n, _ptr(out[0]), st)
+        _lib.call("cirr_symmetry", _ptr(self.b), self.n, self.n, _ptr(out[1]), st)
+        o = out.cpu().numpy()
+        return bool(all(o[i, 0] <= rel_tol * max(o[i, 1], 1e-300) for i in range(2)))
+
+    def _from_tensors(self, torch, a, b, hermitian):
+        """Real float64 tensors (host, ideally pinned, or device): copied with
+        non_blocking H2D; the Hermitian flag must be given or is computed on host."""
+        if a.dim() != 2 or a.shape[0] != a.shape[1] or a.shape != b.shape:
+            raise DimensionError("pencil matrices must be square and equally sized")
+        if a.dtype != torch.float64 or b.dtype != torch.float64:
+            raise NotImplementedError("tensor pencils must be real float64")
+        self.n = a.shape[0]
+        self.a = a.to("cuda", non_blocking=True).contiguous()
+        self.b = b.to("cuda", non_blocking=True).contiguous()
+        self.hermitian = bool(hermitian) if hermitian else self._device_symmetric()
 
     @classmethod
     def of(cls, pencil):
@@ -202,6 +226,74 @@ class DevicePencil:
 def _is_symmetric(m: np.ndarray, rel_tol: float = 1e-12) -> bool:  # sparse.py:83-87
     scale = max(float(np.abs(m).max()) if m.size else 0.0, 1e-300)
     return float(np.abs(m - m.T).max(initial=0.0)) <= rel_tol * scale
+
+
+class StageTimer:
+    """CUDA-event timing of engine stages on the launching stream (bench.py).
+
+    ``with timer.stage("lu"):`` brackets the enqueue of a stage; ``totals()``
+    (after a synchronize) returns milliseconds per stage name summed over
+    every bracket, plus per-stage work counters the engine adds.
+    """
+
+    def __init__(self):
+        self.events = []
+        self.work = {}
+
+    def stage(self, name):
+        timer = self
+
+        class _Ctx:
+            def __enter__(self_inner):
+                torch = _torch()
+                self_inner.e0 = torch.cuda.Event(enable_timing=True)
+                self_inner.e1 = torch.cuda.Event(enable_timing=True)
+                self_inner.e0.record()
+
+            def __exit__(self_inner, *exc):
+                self_inner.e1.record()
+                timer.events.append((name, self_inner.e0, self_inner.e1))
+                return False
+
+        return _Ctx()
+
+    def add(self, name, amount):
+        self.work[name] = self.work.get(name, 0) + amount
+
+    def totals(self) -> dict:
+        out = {}
+        for name, e0, e1 in self.events:
+            out[name] = out.get(name, 0.0) + e0.elapsed_time(e1)
+        return out
+
+    def reset(self):
+        self.events.clear()
+        self.work.clear()
+
+
+_TIMER: StageTimer | None = None
+
+
+def set_stage_timer(timer: StageTimer | None) -> None:
+    global _TIMER
+    _TIMER = timer
+
+
+class _NoStage:
+    def __enter__(self):
+        return None
+
+    def __exit__(self, *exc):
+        return False
+
+
+def _stage(name):
+    return _TIMER.stage(name) if _TIMER is not None else _NoStage()
+
+
+def _work(name, amount):
+    if _TIMER is not None:
+        _TIMER.add(name, amount)
 
 
 def _stream():
@@ -279,10 +371,14 @@ class _Engine:
         self.perm = torch.empty((P, n), dtype=torch.int32, device="cuda")
         self.minpiv = torch.empty(P, dtype=torch.float64, device="cuda")
         self.info = torch.empty(P, dtype=torch.int32, device="cuda")
-        _lib.call("cirr_assemble", _ptr(self.dp.a), _ptr(self.dp.b), n, n, _ptr(z), P,
-                  _ptr(self.pencils), n, n * n, _ptr(self.maxabs), self.stream)
-        _lib.call("cirr_zgetrf_batched", _ptr(self.pencils), n, n, n * n, P, _ptr(self.ipiv),
-                  _ptr(self.perm), _ptr(self.minpiv), _ptr(self.info), self.stream)
+        with _stage("assemble"):
+            _lib.call("cirr_assemble", _ptr(self.dp.a), _ptr(self.dp.b), n, n, _ptr(z), P,
+                      _ptr(self.pencils), n, n * n, _ptr(self.maxabs), self.stream)
+        _work("assemble_bytes", P * n * n * 16 + 2 * n * n * 8)
+        with _stage("lu"):
+            _lib.call("cirr_zgetrf_batched", _ptr(self.pencils), n, n, n * n, P, _ptr(self.ipiv),
+                      _ptr(self.perm), _ptr(self.minpiv), _ptr(self.info), self.stream)
+        _work("lu_flops", P * 8.0 * n ** 3 / 3.0)
         maxabs = self.maxabs.cpu().numpy()
         minpiv = self.minpiv.cpu().numpy()
         info = self.info.cpu().numpy()
@@ -324,18 +420,24 @@ class _Engine:
         Y = torch.empty((Ptot, n, K), dtype=torch.complex128, device="cuda")
         rhs_of = torch.from_numpy(np.concatenate(
             [np.full(b - a, s, dtype=np.int32) for s, (a, b) in enumerate(pen_idx)])).to("cuda")
-        # solve contour ranges (each range is contiguous in the pencil buffer)
-        pos = 0
-        for s, (a, b) in enumerate(pen_idx):
-            cnt = b - a
-            _lib.call("cirr_zgetrs_batched", _ptr(self.pencils[a]), n, n, n * n, cnt, _ptr(self.perm[a]),
-                      _ptr(R), K, n * K, _ptr(rhs_of[pos:pos + cnt]), K, _ptr(Y[pos]), K, n * K, self.stream)
-            pos += cnt
         coef = torch.from_numpy(np.concatenate(coefs, axis=0)).to("cuda")
         off_t = torch.tensor(offs, dtype=torch.int32, device="cuda")
         St = torch.empty((nset, moments * K, n), dtype=torch.complex128, device="cuda")
-        _lib.call("cirr_moments", _ptr(Y), K, n * K, n, K, _ptr(coef), moments, _ptr(off_t), nset,
-                  _ptr(St), n, moments * K * n, self.stream)
+        # solve contour ranges (each range is contiguous in the pencil buffer)
+        with _stage("solve"):
+            pos = 0
+            for s, (a, b) in enumerate(pen_idx):
+                cnt = b - a
+                _lib.call("cirr_zgetrs_batched", _ptr(self.pencils[a]), n, n, n * n, cnt, _ptr(self.perm[a]),
+                          _ptr(R), K, n * K, _ptr(rhs_of[pos:pos + cnt]), K, _ptr(Y[pos]), K, n * K, self.stream)
+                pos += cnt
+        _work("solve_flops", Ptot * 8.0 * n * n * K)
+        _work("solve_flops_exec", sum((b - a) * 8.0 * n * n * rhs[ci].shape[1]
+                                      for (a, b), ci in zip(pen_idx, active)))
+        with _stage("moments"):
+            _lib.call("cirr_moments", _ptr(Y), K, n * K, n, K, _ptr(coef), moments, _ptr(off_t), nset,
+                      _ptr(St), n, moments * K * n, self.stream)
+        _work("moment_flops", Ptot * 8.0 * n * K * moments)
         for s, ci in enumerate(active):
             self.cs[ci].stats.n_linear_solves += len(self.cs[ci].nodes) * rhs[ci].shape[1]
         del Y
@@ -368,6 +470,16 @@ class _Engine:
         cols = St.shape[0]
         if cols == 0:
             raise RankZeroError("empty block")
+        _rr = _stage("rr")
+        _rr.__enter__()
+        try:
+            return self._rayleigh_ritz(c, St)
+        finally:
+            _rr.__exit__(None, None, None)
+
+    def _rayleigh_ritz(self, c: _Contour, St):
+        torch, n, cfg = self.torch, self.n, self.cfg
+        cols = St.shape[0]
         W = St.contiguous()
         sigma = torch.empty(cols, dtype=torch.float64, device="cuda")
         order = torch.empty(cols, dtype=torch.int32, device="cuda")
