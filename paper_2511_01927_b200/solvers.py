@@ -463,85 +463,136 @@ class _Engine:
         return out
 
     # -- K4..K7 for one contour --------------------------------------------
-    def rayleigh_ritz(self, c: _Contour, St):
-        """Returns (lam_inside, x_inside_dev, res_inside) or raises RankZero/Indefinite;
-        lam_inside None when nothing is inside."""
-        torch, n, cfg = self.torch, self.n, self.cfg
-        cols = St.shape[0]
-        if cols == 0:
-            raise RankZeroError("empty block")
-        _rr = _stage("rr")
-        _rr.__enter__()
-        try:
-            return self._rayleigh_ritz(c, St)
-        finally:
-            _rr.__exit__(None, None, None)
+    def rayleigh_ritz(self, items: list) -> dict:
+        """K4..K7 for several contours at once (solvers.py:187-198, batched).
 
-    def _rayleigh_ritz(self, c: _Contour, St):
-        torch, n, cfg = self.torch, self.n, self.cfg
-        cols = St.shape[0]
-        W = St.contiguous()
-        sigma = torch.empty(cols, dtype=torch.float64, device="cuda")
-        order = torch.empty(cols, dtype=torch.int32, device="cuda")
-        kept = torch.empty(1, dtype=torch.int32, device="cuda")
-        Qt = torch.empty((cols, n), dtype=torch.complex128, device="cuda")
+        items: [(ci, St)] with St the transposed stacked block of contour ci.
+        Returns {ci: ("ok", lam_in, x_in_dev, res_in) | ("none",) |
+        ("rankzero",) | ("indefinite", exc)}."""
+        with _stage("rr"):
+            return self._rayleigh_ritz(items)
+
+    def _rayleigh_ritz(self, items: list) -> dict:
+        torch, n, cfg, st = self.torch, self.n, self.cfg, self.stream
+        out = {}
+        for ci, S_ in items:
+            if S_.shape[0] == 0:
+                out[ci] = ("rankzero",)
+        items = [(ci, S_) for ci, S_ in items if S_.shape[0] > 0]
+        if not items:
+            return out
+        nb = len(items)
+        cmax = max(S_.shape[0] for _, S_ in items)
+        # K4: one-sided Jacobi on all blocks (zero rows pad to cmax and are dropped)
+        W = torch.zeros((nb, cmax, n), dtype=torch.complex128, device="cuda")
+        for b, (_, S_) in enumerate(items):
+            W[b, : S_.shape[0]].copy_(S_)
+        sigma = torch.empty((nb, cmax), dtype=torch.float64, device="cuda")
+        order = torch.empty((nb, cmax), dtype=torch.int32, device="cuda")
+        kept = torch.empty(nb, dtype=torch.int32, device="cuda")
+        Qt = torch.zeros((nb, cmax, n), dtype=torch.complex128, device="cuda")
         ws = torch.zeros(16, dtype=torch.int32, device="cuda")
         sweeps = torch.zeros(1, dtype=torch.int32, device="cuda")
-        _lib.call("cirr_orth", _ptr(W), n, cols * n, n, cols, 1, float(cfg.rank_rel_tol), _ptr(sigma),
-                  _ptr(order), _ptr(kept), _ptr(Qt), n, cols * n, _ptr(ws), _ptr(sweeps), self.stream)
-        k = int(kept.item())
-        if k == 0:
-            raise RankZeroError("zero block")
-        Qt = Qt[:k].contiguous()
-        Q = torch.empty((n, k), dtype=torch.complex128, device="cuda")
-        _lib.call("cirr_transpose", 0, _ptr(Qt), n, 0, k, n, 1, _ptr(Q), k, 0, self.stream)
-        AQ = self.amul(Q)
-        BQ = self.bmul(Q)
-        At = torch.empty((k, k), dtype=torch.complex128, device="cuda")
-        Bt = torch.empty((k, k), dtype=torch.complex128, device="cuda")
-        _lib.call("cirr_gemm", 1, k, k, n, 1, _ptr(Qt), n, 0, _ptr(AQ), k, 0, _ptr(At), k, 0, 1.0, 0, self.stream)
-        _lib.call("cirr_gemm", 1, k, k, n, 1, _ptr(Qt), n, 0, _ptr(BQ), k, 0, _ptr(Bt), k, 0, 1.0, 0, self.stream)
+        _lib.call("cirr_orth", _ptr(W), n, cmax * n, n, cmax, nb, float(cfg.rank_rel_tol), _ptr(sigma),
+                  _ptr(order), _ptr(kept), _ptr(Qt), n, cmax * n, _ptr(ws), _ptr(sweeps), st)
+        ks = kept.cpu().numpy()
+        live = [b for b in range(nb) if ks[b] > 0]
+        for b in range(nb):
+            if ks[b] == 0:
+                out[items[b][0]] = ("rankzero",)
+        if not live:
+            return out
+        if len(live) < nb:
+            sel = torch.tensor(live, dtype=torch.long, device="cuda")
+            Qt = Qt.index_select(0, sel)
+            ks = ks[live]
+            items = [items[b] for b in live]
+            nb = len(live)
+        kmax = int(ks.max())
+        Qt = Qt[:, :kmax].contiguous()  # rows beyond k_b are zero
+        # K5: projected pencil  A~ = Q^H A Q, B~ = Q^H B Q
+        Q = torch.empty((nb, n, kmax), dtype=torch.complex128, device="cuda")
+        _lib.call("cirr_transpose", 0, _ptr(Qt), n, kmax * n, kmax, n, nb, _ptr(Q), kmax, n * kmax, st)
+        AQ = torch.empty((nb, n, kmax), dtype=torch.complex128, device="cuda")
+        BQ = torch.empty_like(AQ)
+        _lib.call("cirr_gemm", 2, n, kmax, n, nb, _ptr(self.dp.a), n, 0, _ptr(Q), kmax, n * kmax, _ptr(AQ), kmax,
+                  n * kmax, 1.0, 0, st)
+        _lib.call("cirr_gemm", 2, n, kmax, n, nb, _ptr(self.dp.b), n, 0, _ptr(Q), kmax, n * kmax, _ptr(BQ), kmax,
+                  n * kmax, 1.0, 0, st)
+        At = torch.empty((nb, kmax, kmax), dtype=torch.complex128, device="cuda")
+        Bt = torch.empty_like(At)
+        kk = kmax * kmax
+        _lib.call("cirr_gemm", 1, kmax, kmax, n, nb, _ptr(Qt), n, kmax * n, _ptr(AQ), kmax, n * kmax, _ptr(At), kmax,
+                  kk, 1.0, 0, st)
+        _lib.call("cirr_gemm", 1, kmax, kmax, n, nb, _ptr(Qt), n, kmax * n, _ptr(BQ), kmax, n * kmax, _ptr(Bt), kmax,
+                  kk, 1.0, 0, st)
+        # K6: small eigenproblems, one CTA each
         herm = self.dp.hermitian
-        kdim = torch.tensor([k], dtype=torch.int32, device="cuda")
-        wsb = int(_lib.call("cirr_small_eig_ws_bytes", k))
-        ews = torch.empty((wsb + 255) // 256 * 256, dtype=torch.uint8, device="cuda")
-        lam = torch.empty(k, dtype=torch.complex128, device="cuda")
-        S = torch.empty((k, k), dtype=torch.complex128, device="cuda")
-        info = torch.zeros(1, dtype=torch.int32, device="cuda")
-        _lib.call("cirr_small_eig", 1 if herm else 0, _ptr(At), _ptr(Bt), k, k * k, _ptr(kdim), k, 1,
-                  _ptr(ews), _ptr(lam), _ptr(S), k, k * k, _ptr(info), self.stream)
-        inf = int(info.item())
-        if inf > 0:
-            if herm:
-                raise IndefiniteBError("projected B is not positive definite")
-            raise IndefiniteBError("projected B is singular")
-        if inf < 0:
-            raise DeviceError("small eigensolver: QR iteration failed to converge")
+        kdim = torch.from_numpy(ks.astype(np.int32)).to("cuda")
+        wsb = int(_lib.call("cirr_small_eig_ws_bytes", kmax))
+        ews = torch.empty(nb * ((wsb + 255) // 256 * 256), dtype=torch.uint8, device="cuda")
+        lam = torch.zeros((nb, kmax), dtype=torch.complex128, device="cuda")
+        Sv = torch.zeros((nb, kmax, kmax), dtype=torch.complex128, device="cuda")
+        info = torch.zeros(nb, dtype=torch.int32, device="cuda")
+        _lib.call("cirr_small_eig", 1 if herm else 0, _ptr(At), _ptr(Bt), kmax, kk, _ptr(kdim), kmax, nb,
+                  _ptr(ews), _ptr(lam), _ptr(Sv), kmax, kk, _ptr(info), st)
+        infos = info.cpu().numpy()
         lam_h = lam.cpu().numpy()
-        if herm:
-            lam_h = lam_h.real.copy()
-            keep = np.array([contains(c.contour, complex(v, 0.0)) for v in lam_h], dtype=bool)
-        else:
-            keep = np.array([contains(c.contour, v) for v in lam_h], dtype=bool)
-        if not np.any(keep):
-            return None, None, None
-        idx = np.nonzero(keep)[0]
-        kin = len(idx)
-        X = torch.empty((n, k), dtype=torch.complex128, device="cuda")
-        _lib.call("cirr_gemm", 0, n, k, k, 1, _ptr(Q), k, 0, _ptr(S), k, 0, _ptr(X), k, 0, 1.0, 0, self.stream)
-        idx_t = torch.from_numpy(idx.astype(np.int32)).to("cuda")
-        cnt_t = torch.tensor([kin], dtype=torch.int32, device="cuda")
-        Xi = torch.empty((n, kin), dtype=torch.complex128, device="cuda")
-        _lib.call("cirr_gather_cols", _ptr(X), k, 0, _ptr(idx_t), 0, _ptr(cnt_t), kin, n, 1, _ptr(Xi), kin, 0,
-                  self.stream)
-        AX = self.amul(Xi)
-        BX = self.bmul(Xi)
-        lam_in = torch.from_numpy(np.ascontiguousarray(lam_h[idx].astype(np.complex128))).to("cuda")
-        res = torch.empty(kin, dtype=torch.float64, device="cuda")
-        kin_t = torch.tensor([kin], dtype=torch.int32, device="cuda")
-        _lib.call("cirr_residuals", _ptr(AX), _ptr(BX), kin, 0, n, _ptr(lam_in), 0, _ptr(kin_t), kin, 1,
-                  _ptr(res), 0, self.stream)
-        return lam_h[idx], Xi, res.cpu().numpy()
+        keep_idx = {}
+        for b, (ci, _) in enumerate(items):
+            if infos[b] > 0:
+                msg = "projected B is not positive definite" if herm else "projected B is singular"
+                out[ci] = ("indefinite", IndefiniteBError(msg))
+                continue
+            if infos[b] < 0:
+                raise DeviceError("small eigensolver: QR iteration failed to converge")
+            lb = lam_h[b, : ks[b]]
+            if herm:
+                keep = np.array([contains(self.cs[ci].contour, complex(v.real, 0.0)) for v in lb], dtype=bool)
+            else:
+                keep = np.array([contains(self.cs[ci].contour, v) for v in lb], dtype=bool)
+            if not np.any(keep):
+                out[ci] = ("none",)
+                continue
+            keep_idx[b] = np.nonzero(keep)[0]
+        if not keep_idx:
+            return out
+        # K7: X = Q s, inside columns, A X, B X, residuals
+        X = torch.empty((nb, n, kmax), dtype=torch.complex128, device="cuda")
+        _lib.call("cirr_gemm", 0, n, kmax, kmax, nb, _ptr(Q), kmax, n * kmax, _ptr(Sv), kmax, kk, _ptr(X), kmax,
+                  n * kmax, 1.0, 0, st)
+        kin_max = max(len(v) for v in keep_idx.values())
+        idx = np.zeros((nb, kin_max), dtype=np.int32)
+        cnt = np.zeros(nb, dtype=np.int32)
+        lam_in = np.zeros((nb, kin_max), dtype=np.complex128)
+        for b, ix in keep_idx.items():
+            idx[b, : len(ix)] = ix
+            cnt[b] = len(ix)
+            lam_in[b, : len(ix)] = lam_h[b, ix]
+        idx_t = torch.from_numpy(idx).to("cuda")
+        cnt_t = torch.from_numpy(cnt).to("cuda")
+        Xi = torch.zeros((nb, n, kin_max), dtype=torch.complex128, device="cuda")
+        _lib.call("cirr_gather_cols", _ptr(X), kmax, n * kmax, _ptr(idx_t), kin_max, _ptr(cnt_t), kin_max, n, nb,
+                  _ptr(Xi), kin_max, n * kin_max, st)
+        AX = torch.empty_like(Xi)
+        BX = torch.empty_like(Xi)
+        _lib.call("cirr_gemm", 2, n, kin_max, n, nb, _ptr(self.dp.a), n, 0, _ptr(Xi), kin_max, n * kin_max,
+                  _ptr(AX), kin_max, n * kin_max, 1.0, 0, st)
+        _lib.call("cirr_gemm", 2, n, kin_max, n, nb, _ptr(self.dp.b), n, 0, _ptr(Xi), kin_max, n * kin_max,
+                  _ptr(BX), kin_max, n * kin_max, 1.0, 0, st)
+        lam_t = torch.from_numpy(lam_in).to("cuda")
+        res = torch.zeros((nb, kin_max), dtype=torch.float64, device="cuda")
+        _lib.call("cirr_residuals", _ptr(AX), _ptr(BX), kin_max, n * kin_max, n, _ptr(lam_t), kin_max, _ptr(cnt_t),
+                  kin_max, nb, _ptr(res), kin_max, st)
+        res_h = res.cpu().numpy()
+        for b, ix in keep_idx.items():
+            ci = items[b][0]
+            k_in = len(ix)
+            lam_b = lam_h[b, ix]
+            if herm:
+                lam_b = lam_b.real.copy()
+            out[ci] = ("ok", lam_b, Xi[b, :, :k_in].contiguous(), res_h[b, :k_in].copy())
+        return out
 
     # -- the reference control flow (solvers.py:165-227) for all contours ----
     def run(self, moments: int):
@@ -559,23 +610,25 @@ class _Engine:
         it_of = {ci: 0 for ci in active}
         for it in range(cfg.max_refine):
             refine = {}
+            for ci in active:
+                it_of[ci] = it
+            rr = self.rayleigh_ritz([(ci, stacked[ci]) for ci in active])
             for ci in list(active):
                 c = self.cs[ci]
-                it_of[ci] = it
-                try:
-                    lam, xi, res = self.rayleigh_ritz(c, stacked[ci])
-                except RankZeroError:
+                r = rr[ci]
+                if r[0] == "rankzero":
                     active.remove(ci)
                     continue
-                except IndefiniteBError as exc:
-                    c.error = exc
+                if r[0] == "indefinite":
+                    c.error = r[1]
                     c.fatal = True
                     active.remove(ci)
                     continue
-                if lam is None:
+                if r[0] == "none":
                     c.lam = None
                     active.remove(ci)
                     continue
+                _, lam, xi, res = r
                 c.lam, c.x_dev, c.res = lam, xi, res
                 c.best_res = min(c.best_res, float(res.max()))
                 if res.max() <= cfg.tol or it + 1 >= cfg.max_refine:

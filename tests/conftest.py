@@ -1,8 +1,17 @@
 import os
 import sys
 
-import numpy as np
-import pytest
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")  # SURVEY 0 finding 5: threaded OpenBLAS is pathological here
+
+import numpy as np  # noqa: E402
+import pytest  # noqa: E402
+
+try:  # numpy may already be loaded by a plugin: clamp the BLAS pool at runtime too
+    from threadpoolctl import threadpool_limits
+
+    threadpool_limits(1)
+except Exception:  # pragma: no cover
+    pass
 
 ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
 if ROOT not in sys.path:

@@ -1,0 +1,104 @@
+"""Parity of the GPU CIRR path with the CPU oracle on the BASELINE configs.
+
+Fixtures (tests/golden/oracle_configN.npz, made by make_oracle_golden.py in
+the build container) hold the oracle's per-contour eigenvalues and the dense
+truth inside each contour.  The bar (BASELINE.json north_star):
+  * in-contour count == oracle count == truth count (exact),
+  * eigenvalues agree with the oracle to 1e-8 relative,
+  * every pair: ||Ax - lam Bx|| / ((||A||_2 + |lam| ||B||_2) ||x||) <= 1e-10,
+    plus the reference's own residual metric (solvers.py:140-147) <= tol.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, golden
+
+pytestmark = pytest.mark.gpu
+
+from paper_2511_01927_b200 import Contour, DevicePencil, SolverConfig, solve_multi  # noqa: E402
+from paper_2511_01927_b200 import workloads as W  # noqa: E402
+
+
+def norm2_est(m, iters=30, seed=0):
+    """Power-iteration estimate of ||m||_2 (a lower bound: makes the check stricter)."""
+    v = np.random.default_rng(seed).standard_normal(m.shape[1])
+    for _ in range(iters):
+        w = m.T @ (m @ v)
+        v = w / np.linalg.norm(w)
+    return float(np.sqrt(np.linalg.norm(m.T @ (m @ v))))
+
+
+def check(a, b, fixture, tag, multi, contours):
+    na, nb = norm2_est(a), norm2_est(b)
+    for i, (res, err) in enumerate(zip(multi.results, multi.errors)):
+        truth = fixture[f"{tag}c{i}_truth"]
+        assert res is not None, (tag, i, err)
+        ref = fixture[f"{tag}c{i}_eigs"]
+        assert len(res.eigenvalues) == len(ref) == len(truth), (tag, i, len(res.eigenvalues), len(ref), len(truth))
+        rel = np.abs(res.eigenvalues - ref) / np.abs(ref)
+        assert rel.max() <= 1e-8, (tag, i, rel.max())
+        assert res.residuals.max() <= 1e-10
+        x, lam = res.eigenvectors, res.eigenvalues
+        ax, bx = a @ x, b @ x
+        ns = np.linalg.norm(ax - bx * lam[None, :], axis=0) / ((na + np.abs(lam) * nb) * np.linalg.norm(x, axis=0))
+        assert ns.max() <= 1e-10, (tag, i, ns.max())
+        mine = np.linalg.norm(ax - bx * lam[None, :], axis=0) / (np.linalg.norm(ax, axis=0)
+                                                                 + np.abs(lam) * np.linalg.norm(bx, axis=0))
+        assert np.allclose(mine, res.residuals, rtol=1e-6, atol=1e-15)
+        for v in lam:
+            assert contours[i].contains(complex(v))
+
+
+def run(fix, a, b, herm, nq, L, M, tag=""):
+    contours = [Contour.from_json_dict(d) for d in json.loads(str(fix[f"{tag}contours"]))]
+    cfg = SolverConfig(n_q=nq, source_cols=L, n_moments=M)
+    multi = solve_multi(DevicePencil(a, b, hermitian=herm), contours, cfg, seed=0)
+    check(a, b, fix, tag, multi, contours)
+    return multi
+
+
+def test_config1():
+    a, b = W.config1_matrices()
+    m = run(golden("oracle_config1.npz"), a, b, True, 32, 16, 4)
+    r = m.results[0]
+    assert np.abs(r.eigenvectors.conj().T @ b @ r.eigenvectors - np.eye(33)).max() < 1e-9
+
+
+def test_config2_all_256():
+    fix = golden("oracle_config2.npz")
+    for s in range(int(fix["n_gep"])):
+        a, b = W.config2_matrices(s)
+        run(fix, a, b, True, 16, 8, 4, tag=f"s{s}_")
+
+
+def test_config3():
+    a, b = W.config3_matrices()
+    run(golden("oracle_config3.npz"), a, b, True, 32, 32, 4)
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(GOLDEN, "oracle_config4.npz")), reason="fixture not built")
+def test_config4():
+    a, b = W.config4_matrices()
+    fix = golden("oracle_config4.npz")
+    m = run(fix, a, b, False, 64, 32, 8)
+    assert [r.stats.iterations for r in m.results] == [int(fix["c0_iters"]), int(fix["c1_iters"])]
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(GOLDEN, "oracle_config5.npz")), reason="fixture not built")
+def test_config5():
+    a, b = W.config5_matrices()
+    run(golden("oracle_config5.npz"), a, b, True, 32, 64, 4)
+
+
+def test_deterministic_config3():
+    a, b = W.config3_matrices()
+    fix = golden("oracle_config3.npz")
+    contours = [Contour.from_json_dict(d) for d in json.loads(str(fix["contours"]))]
+    dp = DevicePencil(a, b, hermitian=True)
+    cfg = SolverConfig(n_q=32, source_cols=32, n_moments=4)
+    e1 = solve_multi(dp, contours, cfg, seed=0).eigenvalues
+    e2 = solve_multi(dp, contours, cfg, seed=0).eigenvalues
+    assert np.array_equal(e1, e2)

@@ -1,0 +1,90 @@
+"""Host-side logic of the drop-in (no GPU needed)."""
+import ast
+import os
+
+import numpy as np
+import pytest
+
+from paper_2511_01927_b200 import solvers as S
+from paper_2511_01927_b200.contours import Contour
+from paper_2511_01927_b200.errors import DeviceError, ParameterError
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_solver_config_validation():
+    with pytest.raises(ParameterError):
+        S.SolverConfig(n_q=2)
+    with pytest.raises(ParameterError):
+        S.SolverConfig(tol=0.0)
+    assert S.SolverConfig().cols_for(3) == 8 and S.SolverConfig().cols_for(10) == 20
+    assert S.SolverConfig(source_cols=5).cols_for(100) == 5
+
+
+def test_sidecar_round_trip(tmp_path):
+    rng = np.random.default_rng(0)
+    block = rng.standard_normal((7, 3)) + 1j * rng.standard_normal((7, 3))
+    path = tmp_path / "v.bin"
+    S.write_eigenvectors(path, block)
+    assert path.stat().st_size == 16 + 7 * 3 * 16
+    assert np.array_equal(S.read_eigenvectors(path), block)
+
+
+def _res(vals, resid, c=None):
+    return S.EigenResult(np.array(vals), np.zeros((2, len(vals))), np.array(resid), c, S.SolveStats())
+
+
+def test_dedupe_keeps_smaller_residual():
+    rs = [_res([1.0, 2.0], [1e-12, 5e-11]), _res([2.0 + 1e-12, 3.0], [1e-13, 1e-12])]
+    S._dedupe(rs)
+    assert list(rs[0].eigenvalues) == [1.0]
+    assert len(rs[1].eigenvalues) == 2
+
+
+def test_dedupe_complex_values():
+    rs = [_res([0.5 + 0.1j, -0.5 + 0.0j], [1e-12, 1e-12]), _res([0.5 + 0.1j + 1e-13], [1e-11])]
+    S._dedupe(rs)
+    assert len(rs[0].eigenvalues) == 2 and len(rs[1].eigenvalues) == 0
+
+
+def test_moment_coefficients_match_oracle():
+    from oracle.cirr import moment_frame as ofr, quadrature as oq
+    e = Contour(shape="ellipse", center=0.5 + 0j, semi_re=0.3, semi_im=0.15)
+    c = S._Contour(0, e, S.SolverConfig(n_q=64, n_moments=8), 0, 10)
+    nodes, w = oq(e, 64)
+    g, r = ofr(e)
+    assert np.array_equal(c.nodes, nodes) and (c.gamma, c.rho) == (g, r)
+    coef = c.coef(8)
+    for j in (0, 17, 63):
+        zp, zeta = 1.0 + 0j, (nodes[j] - g) / r
+        for m in range(8):
+            assert coef[j, m] == w[j] * zp
+            zp *= zeta
+
+
+def test_waves_group_whole_contours():
+    cs = [S._Contour(i, Contour(shape="circle", center=0j, radius=1.0), S.SolverConfig(n_q=32), 0, 100)
+          for i in range(5)]
+    waves = S._waves(cs, 100, budget_bytes=100 * 100 * 16 * 64)
+    assert [len(w) for w in waves] == [2, 2, 1]
+
+
+def test_product_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_2511_01927_b200")
+    for fn in os.listdir(pkg):
+        if fn.endswith(".py"):
+            tree = ast.parse(open(os.path.join(pkg, fn)).read())
+            for node in ast.walk(tree):
+                if isinstance(node, ast.Import):
+                    assert not any(a.name.split(".")[0] == "oracle" for a in node.names), fn
+                if isinstance(node, ast.ImportFrom) and node.module:
+                    assert node.module.split(".")[0] != "oracle", fn
+
+
+def test_no_cuda_fails_loudly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("CUDA present")
+    with pytest.raises(DeviceError):
+        S.cirr_solve(type("P", (), {"a": np.eye(2), "b": np.eye(2), "hermitian": True})(),
+                     Contour(shape="circle", center=1 + 0j, radius=0.5))
