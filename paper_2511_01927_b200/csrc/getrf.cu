@@ -11,6 +11,7 @@
 // reference's singular-shift test, linalg.py:68-70) and LAPACK-style info.
 #include "common.cuh"
 #include "gemm.cuh"
+#include "lu_gemm.cuh"
 
 namespace {
 
@@ -231,6 +232,8 @@ CIRR_API int cirr_zgetrf_batched(cplx* pencils, int n, long long ld, long long p
   }
   init_kernel<<<(batch + 255) / 256, 256, 0, stream>>>(minpiv, info, batch);
   CIRR_CHECK_LAUNCH();
+  cirr::PencilMaps maps;
+  const bool use_tma = cirr::encode_pencil_maps(maps, pencils, n, ld, pencil_stride, batch) == 0;
   for (int k = 0; k < n; k += NB) {
     const int jb = min(NB, n - k);
     panel_kernel<<<batch, PT, 0, stream>>>(pencils, n, ld, pencil_stride, k, jb, ipiv, minpiv, info);
@@ -245,12 +248,16 @@ CIRR_API int cirr_zgetrf_batched(cplx* pencils, int n, long long ld, long long p
       dim3 g2((rest + TC - 1) / TC, batch);
       trsm_kernel<<<g2, 256, kTrsmSmem, stream>>>(pencils, n, ld, pencil_stride, k, jb);
       CIRR_CHECK_LAUNCH();
-      cirr::GemmArgs ga{rest, rest, jb, batch,
-                        pencils + (long long)(k + jb) * ld + k, ld, pencil_stride,
-                        pencils + (long long)k * ld + k + jb, ld, pencil_stride,
-                        pencils + (long long)(k + jb) * ld + k + jb, ld, pencil_stride,
-                        -1.0, 1};
-      CIRR_TRY((cirr::gemm_launch<false, false>(ga, stream)));
+      if (jb % cirr::PBK == 0 && use_tma) {
+        CIRR_TRY(cirr::lu_update_tma(maps, pencils, n, ld, pencil_stride, batch, k, jb, stream));
+      } else {
+        cirr::GemmArgs ga{rest, rest, jb, batch,
+                          pencils + (long long)(k + jb) * ld + k, ld, pencil_stride,
+                          pencils + (long long)k * ld + k + jb, ld, pencil_stride,
+                          pencils + (long long)(k + jb) * ld + k + jb, ld, pencil_stride,
+                          -1.0, 1};
+        CIRR_TRY((cirr::gemm_launch<false, false>(ga, stream)));
+      }
     }
   }
   if (perm) {

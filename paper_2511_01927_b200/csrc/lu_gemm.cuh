@@ -1,0 +1,249 @@
+// Persistent, warp-specialised complex128 GEMM  C[b] -= A[b] @ B[b]  for the
+// LU trailing update (A22 -= L21 U12), with every operand tile moved by the
+// Tensor Memory Accelerator.
+//
+// One CTA per SM loops over 64x64 output tiles of all pencils.  A producer
+// warp issues one cp.async.bulk.tensor (TMA, SASS UTMALDG) per operand tile
+// -- a 64x16 slice of L21, a 16x64 slice of U12 and the 64x64 C block -- into
+// a 4-stage ring (completion by mbarrier transaction bytes); out-of-range rows
+// and columns are zero-filled by the TMA unit.  The C block of a tile is
+// requested while that tile's main loop runs and the next tile's K slices
+// during its epilogue, so HBM traffic for C overlaps tensor work.  Eight
+// consumer warps run the complex DMMA main loop (mma.sync m8n8k4 f64 -> SASS
+// DMMA.8x8x4) with four independent accumulator sets per 8x8 block and write
+// C - acc straight to global memory.
+//
+// The three tensor maps describe the whole pencil batch as a 3-D float64
+// tensor {2n, n, batch} (complex128 = two doubles), so one encoding serves
+// every panel step of a factorisation.
+#pragma once
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include "common.cuh"
+
+namespace cirr {
+
+constexpr int PBM = 64, PBN = 64, PBK = 16, PSTAGES = 4;
+constexpr int PCONS = 8;         // consumer warps
+constexpr int PTHREADS = (PCONS + 1) * 32;
+constexpr int P_A_BYTES = PBM * PBK * 16;
+constexpr int P_B_BYTES = PBK * PBN * 16;
+constexpr int P_STAGE_BYTES = P_A_BYTES + P_B_BYTES;
+constexpr int P_C_BYTES = PBM * PBN * 16;
+constexpr int P_SMEM = PSTAGES * P_STAGE_BYTES + P_C_BYTES + 8 * (2 * PSTAGES + 2) + 128;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}"
+               ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+// TMA tile load of a 3-D box at (c0, c1, c2) (c0 in doubles), completion on `bar`
+__device__ __forceinline__ void tma_load3(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+      ::"r"(smem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)) : "memory");
+}
+
+struct SubGemmGeom {
+  int M, N, K, batch;
+  int a_row0, a_col0;   // L21 origin (rows, complex columns) inside each pencil
+  int b_row0, b_col0;   // U12 origin
+  int c_row0, c_col0;   // A22 origin
+  cplx* C; long long ldc, sC;
+  int tiles_m, tiles_n;
+};
+
+__global__ void __launch_bounds__(PTHREADS, 1) zgemm_sub_tma(const __grid_constant__ CUtensorMap mapA,
+                                                             const __grid_constant__ CUtensorMap mapB,
+                                                             const __grid_constant__ CUtensorMap mapC,
+                                                             SubGemmGeom g) {
+  extern __shared__ __align__(128) unsigned char psm_raw[];
+  unsigned char* psm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(psm_raw) + 127) & ~uintptr_t(127));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(psm + PSTAGES * P_STAGE_BYTES + P_C_BYTES);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + PSTAGES;
+  uint64_t* cfull = bars + 2 * PSTAGES;
+  uint64_t* cempty = bars + 2 * PSTAGES + 1;
+  const cplx* Cs = reinterpret_cast<const cplx*>(psm + PSTAGES * P_STAGE_BYTES);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    for (int s = 0; s < PSTAGES; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, PCONS); }
+    mbar_init(cfull, 1);
+    mbar_init(cempty, PCONS);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const long long tiles_per_b = (long long)g.tiles_m * g.tiles_n;
+  const long long total = tiles_per_b * g.batch;
+  const int ksteps = g.K / PBK;
+
+  if (warp == PCONS) {
+    // ---------------- producer warp (one elected lane) ----------------
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&mapB) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&mapC) : "memory");
+      int stage = 0;
+      unsigned phase = 0, cphase = 0;
+      for (long long t = blockIdx.x; t < total; t += gridDim.x) {
+        const int b = (int)(t / tiles_per_b);
+        const int rem = (int)(t % tiles_per_b);
+        const int m0 = (rem / g.tiles_n) * PBM, n0 = (rem % g.tiles_n) * PBN;
+        for (int ks = 0; ks < ksteps; ++ks) {
+          mbar_wait(empty + stage, phase ^ 1);
+          unsigned char* base = psm + stage * P_STAGE_BYTES;
+          mbar_arrive_expect_tx(full + stage, P_STAGE_BYTES);
+          const int k0 = ks * PBK;
+          tma_load3(base, &mapA, 2 * (g.a_col0 + k0), g.a_row0 + m0, b, full + stage);
+          tma_load3(base + P_A_BYTES, &mapB, 2 * (g.b_col0 + n0), g.b_row0 + k0, b, full + stage);
+          if (++stage == PSTAGES) { stage = 0; phase ^= 1; }
+        }
+        // C block of this tile: requested once the consumers released the
+        // previous tile's C, i.e. while this tile's main loop runs
+        mbar_wait(cempty, cphase ^ 1);
+        mbar_arrive_expect_tx(cfull, P_C_BYTES);
+        tma_load3(psm + PSTAGES * P_STAGE_BYTES, &mapC, 2 * (g.c_col0 + n0), g.c_row0 + m0, b, cfull);
+        cphase ^= 1;
+      }
+    }
+  } else {
+    // ---------------- consumer warps ----------------
+    const int wm = (warp >> 2) * 32, wn = (warp & 3) * 16;
+    int stage = 0;
+    unsigned phase = 0, cphase = 0;
+    for (long long t = blockIdx.x; t < total; t += gridDim.x) {
+      const int b = (int)(t / tiles_per_b);
+      const int rem = (int)(t % tiles_per_b);
+      const int m0 = (rem / g.tiles_n) * PBM, n0 = (rem % g.tiles_n) * PBN;
+      // four independent accumulator sets (re*re, im*im, re*im, im*re)
+      double arr[4][2][2], aii[4][2][2], ari[4][2][2], air[4][2][2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) arr[i][j][h] = aii[i][j][h] = ari[i][j][h] = air[i][j][h] = 0.0;
+      for (int ks = 0; ks < ksteps; ++ks) {
+        mbar_wait(full + stage, phase);
+        const unsigned char* base = psm + stage * P_STAGE_BYTES;
+        const cplx* As = reinterpret_cast<const cplx*>(base);
+        const cplx* Bs = reinterpret_cast<const cplx*>(base + P_A_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < PBK; kk += 4) {
+          cplx af[4], bf[2];
+#pragma unroll
+          for (int j = 0; j < 2; ++j) bf[j] = Bs[(kk + (lane & 3)) * PBN + wn + j * 8 + (lane >> 2)];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) af[i] = As[(wm + i * 8 + (lane >> 2)) * PBK + kk + (lane & 3)];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              dmma884(arr[i][j][0], arr[i][j][1], af[i].x, bf[j].x);
+              dmma884(aii[i][j][0], aii[i][j][1], af[i].y, bf[j].y);
+              dmma884(ari[i][j][0], ari[i][j][1], af[i].x, bf[j].y);
+              dmma884(air[i][j][0], air[i][j][1], af[i].y, bf[j].x);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + stage);
+        if (++stage == PSTAGES) { stage = 0; phase ^= 1; }
+      }
+      // epilogue: C - acc, straight to global
+      mbar_wait(cfull, cphase);
+      cphase ^= 1;
+      cplx* Cb = g.C + (long long)b * g.sC;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int rl = wm + i * 8 + (lane >> 2);
+        const int r = m0 + rl;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int cl = wn + j * 8 + 2 * (lane & 3);
+          const int c = n0 + cl;
+          if (r < g.M) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              if (c + h < g.N) {
+                const cplx v = Cs[rl * PBN + cl + h];
+                Cb[(long long)(g.c_row0 + r) * g.ldc + g.c_col0 + c + h] =
+                    cmk(v.x - (arr[i][j][h] - aii[i][j][h]), v.y - (ari[i][j][h] + air[i][j][h]));
+              }
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(cempty);
+    }
+  }
+}
+
+// Tensor maps over a pencil batch viewed as float64 {2n, n, batch}.
+struct PencilMaps {
+  CUtensorMap a, b, c;
+};
+
+inline int encode_pencil_maps(PencilMaps& pm, cplx* base, int n, long long ld, long long pstride, int batch) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return (int)cudaErrorNotSupported;
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  cuuint64_t dims[3] = {(cuuint64_t)2 * n, (cuuint64_t)n, (cuuint64_t)batch};
+  cuuint64_t strides[2] = {(cuuint64_t)ld * 16, (cuuint64_t)pstride * 16};
+  cuuint32_t estr[3] = {1, 1, 1};
+  cuuint32_t boxA[3] = {2 * PBK, PBM, 1}, boxB[3] = {2 * PBN, PBK, 1}, boxC[3] = {2 * PBN, PBM, 1};
+  CUtensorMap* maps[3] = {&pm.a, &pm.b, &pm.c};
+  cuuint32_t* boxes[3] = {boxA, boxB, boxC};
+  for (int i = 0; i < 3; ++i) {
+    CUresult r = encode(maps[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, boxes[i], estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return (int)cudaErrorInvalidValue;
+  }
+  return 0;
+}
+
+// A22 -= L21 U12 for panel step (k, jb) of every pencil, via the TMA kernel.
+inline int lu_update_tma(const PencilMaps& pm, cplx* pencils, int n, long long ld, long long pstride, int batch,
+                         int k, int jb, cudaStream_t stream) {
+  const int rest = n - k - jb;
+  if (rest <= 0) return 0;
+  static bool attr = false;
+  static int sms = 0;
+  if (!attr) {
+    cudaFuncSetAttribute(zgemm_sub_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    attr = true;
+  }
+  SubGemmGeom g{rest, rest, jb, batch, k + jb, k, k, k + jb, k + jb, k + jb, pencils, ld, pstride,
+                (rest + PBM - 1) / PBM, (rest + PBN - 1) / PBN};
+  const long long tiles = (long long)g.tiles_m * g.tiles_n * batch;
+  const int grid = (int)(tiles < sms ? tiles : sms);
+  zgemm_sub_tma<<<grid, PTHREADS, P_SMEM, stream>>>(pm.a, pm.b, pm.c, g);
+  cirr_note_launch();
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : (int)e;
+}
+
+}  // namespace cirr
