@@ -83,6 +83,9 @@ int cirr_small_eig(int hermitian, const cirr_cplx* At, const cirr_cplx* Bt, long
                    long long sin_, const int* kdim, int kmax, int nprob, void* ws, cirr_cplx* lam,
                    cirr_cplx* S, long long lds, long long sS, int* info, cudaStream_t stream);
 
+/* debug: clock64 stamps of the phases of the last general-eig launch (problem 0), 8 entries (host buffer) */
+int cirr_small_eig_phases(long long* host_out);
+
 /* K7 -- replaces solvers.py:140-147 (_residuals). */
 int cirr_residuals(const cirr_cplx* AX, const cirr_cplx* BX, long long ld, long long stride, int n,
                    const cirr_cplx* lam, long long lstride, const int* kdim, int kmax, int nprob,

@@ -21,6 +21,12 @@
 namespace {
 
 constexpr int ET = 1024;
+constexpr int QC = 32;          // rotations per chunk of a QR sweep
+constexpr int WLD = QC + 4;     // window leading dimension
+
+// phase timestamps of problem 0 (clock64), read back with cirr_small_eig_phases
+__device__ long long g_eig_phase[8];
+#define EIG_MARK(i) do { if (blockIdx.x == 0 && threadIdx.x == 0) g_eig_phase[i] = clock64(); } while (0)
 constexpr double EPS = 1.1102230246251565e-16;
 
 struct EigWs {
@@ -255,7 +261,9 @@ __global__ void __launch_bounds__(ET) gen_eig_kernel(const cplx* __restrict__ At
   __shared__ int ri[32];
   __shared__ int s_int[4];
   __shared__ cplx s_c[4];
-  __shared__ double s_d[4];
+  __shared__ cplx win[(QC + 2) * WLD];
+  __shared__ double rot_cs[QC];
+  __shared__ cplx rot_sn[QC];
   const int prob = blockIdx.x;
   const int k = kdim[prob];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -273,6 +281,7 @@ __global__ void __launch_bounds__(ET) gen_eig_kernel(const cplx* __restrict__ At
   }
   if (tid == 0) s_int[3] = 0;
   __syncthreads();
+  EIG_MARK(0);
   // 1. LU of B~ with partial pivoting; apply the same row swaps to H
   for (int j = 0; j < k; ++j) {
     double best = -1.0; int bi = j;
@@ -322,6 +331,7 @@ __global__ void __launch_bounds__(ET) gen_eig_kernel(const cplx* __restrict__ At
     if (tid == 0) info[prob] = s_int[3];
     return;
   }
+  EIG_MARK(1);
   // solve L U M = P A (column per thread), M into H
   for (int c = tid; c < k; c += ET) {
     for (int i = 0; i < k; ++i) {
@@ -336,6 +346,7 @@ __global__ void __launch_bounds__(ET) gen_eig_kernel(const cplx* __restrict__ At
     }
   }
   __syncthreads();
+  EIG_MARK(2);
   // 2. Householder Hessenberg reduction H <- Q^H H Q, Z <- Z Q
   cplx* v = w.vec;          // Householder vector (length k)
   cplx* wv = w.vec + kmax;  // work vectors (length 3k)
@@ -387,6 +398,7 @@ __global__ void __launch_bounds__(ET) gen_eig_kernel(const cplx* __restrict__ At
       __syncthreads();
     }
   }
+  EIG_MARK(3);
   // 3. single-shift QR on the Hessenberg matrix (full Schur form + Z)
   int ihi = k - 1;
   const int itmax = 30 * (k > 10 ? k : 10);
@@ -447,44 +459,94 @@ __global__ void __launch_bounds__(ET) gen_eig_kernel(const cplx* __restrict__ At
       }
       __syncthreads();
       const cplx mu = s_c[0];
-      // QR sweep with Givens rotations over rows/cols l..ihi
-      for (int m = l; m < ihi; ++m) {
-        if (tid == 0) {
-          cplx x, y;
-          if (m == l) { x = csub(H[l * ld + l], mu); y = H[(l + 1) * ld + l]; }
-          else { x = H[m * ld + m - 1]; y = H[(m + 1) * ld + m - 1]; }
-          const double ax = cabs(x), ay = cabs(y);
-          double c; cplx s, r;
-          if (ay == 0.0) { c = 1.0; s = cmk(0.0, 0.0); r = x; }
-          else if (ax == 0.0) { c = 0.0; s = cscale(cconj(y), 1.0 / ay); r = cmk(ay, 0.0); }
-          else {
-            const double nrm = hypot(ax, ay);
-            c = ax / nrm;
-            const cplx ph = cscale(x, 1.0 / ax);
-            s = cscale(cmul(ph, cconj(y)), 1.0 / nrm);
-            r = cscale(ph, nrm);
+      // QR sweep over rows/cols l..ihi in chunks of QC rotations: warp 0 chases
+      // the bulge through a shared-memory window (every entry the chain reads
+      // lives there); afterwards all warps apply the chunk's rotations to the
+      // far parts of H (left: window rows right of the window; right: rows
+      // above it) and to Z, one carry per row/column, no further syncs.
+      for (int m0 = l; m0 < ihi; m0 += QC) {
+        const int m1 = min(m0 + QC, ihi);
+        const int wr0 = m0, wr1 = min(m1 + 1, ihi);
+        const int wc0 = (m0 > l) ? m0 - 1 : l, wc1 = min(m1 + 1, ihi);
+        const int nwr = wr1 - wr0 + 1, nwc = wc1 - wc0 + 1;
+        for (int e = tid; e < nwr * nwc; e += ET) {
+          const int r = e / nwc, cc = e % nwc;
+          win[r * WLD + cc] = H[(wr0 + r) * ld + wc0 + cc];
+        }
+        __syncthreads();
+        if (wid == 0) {
+#define W_(r, c) win[((r) - wr0) * WLD + (c) - wc0]
+          for (int m = m0; m < m1; ++m) {
+            if (lane == 0) {
+              cplx x, y;
+              if (m == l) { x = csub(W_(l, l), mu); y = W_(l + 1, l); }
+              else { x = W_(m, m - 1); y = W_(m + 1, m - 1); }
+              const double ax = cabs(x), ay = cabs(y);
+              double c; cplx sn, r;
+              if (ay == 0.0) { c = 1.0; sn = cmk(0.0, 0.0); r = x; }
+              else if (ax == 0.0) { c = 0.0; sn = cscale(cconj(y), 1.0 / ay); r = cmk(ay, 0.0); }
+              else {
+                const double nrm = hypot(ax, ay);
+                c = ax / nrm;
+                const cplx ph = cscale(x, 1.0 / ax);
+                sn = cscale(cmul(ph, cconj(y)), 1.0 / nrm);
+                r = cscale(ph, nrm);
+              }
+              if (m > l) { W_(m, m - 1) = r; W_(m + 1, m - 1) = cmk(0.0, 0.0); }
+              rot_cs[m - m0] = c;
+              rot_sn[m - m0] = sn;
+            }
+            __syncwarp();
+            const double c = rot_cs[m - m0];
+            const cplx sn = rot_sn[m - m0], snc = cconj(sn);
+            for (int col = m + lane; col <= wc1; col += 32) {
+              const cplx a = W_(m, col), b = W_(m + 1, col);
+              W_(m, col) = cadd(cscale(a, c), cmul(sn, b));
+              W_(m + 1, col) = csub(cscale(b, c), cmul(snc, a));
+            }
+            __syncwarp();
+            const int rmax = min(m + 2, wr1);
+            for (int r = wr0 + lane; r <= rmax; r += 32) {
+              const cplx a = W_(r, m), b = W_(r, m + 1);
+              W_(r, m) = cadd(cscale(a, c), cmul(snc, b));
+              W_(r, m + 1) = csub(cscale(b, c), cmul(sn, a));
+            }
+            __syncwarp();
           }
-          if (m > l) { H[m * ld + m - 1] = r; H[(m + 1) * ld + m - 1] = cmk(0.0, 0.0); }
-          s_d[0] = c; s_c[1] = s;
+#undef W_
         }
         __syncthreads();
-        const double c = s_d[0];
-        const cplx s = s_c[1], sc = cconj(s);
-        // left on rows m, m+1, columns m .. k-1
-        for (int col = m + tid; col < k; col += ET) {
-          cplx a = H[m * ld + col], b = H[(m + 1) * ld + col];
-          H[m * ld + col] = cadd(cscale(a, c), cmul(s, b));
-          H[(m + 1) * ld + col] = csub(cscale(b, c), cmul(sc, a));
+        for (int e = tid; e < nwr * nwc; e += ET) {
+          const int r = e / nwc, cc = e % nwc;
+          H[(wr0 + r) * ld + wc0 + cc] = win[r * WLD + cc];
         }
-        __syncthreads();
-        // right on columns m, m+1: rows 0 .. min(m+2, ihi);  Z rows 0..k-1
-        const int rmax = min(m + 2, ihi);
-        for (int r = tid; r < k + rmax + 1; r += ET) {
-          cplx* M = r < k ? Z : H;
-          const int rr = r < k ? r : r - k;
-          cplx a = M[rr * ld + m], b = M[rr * ld + m + 1];
-          M[rr * ld + m] = cadd(cscale(a, c), cmul(sc, b));
-          M[rr * ld + m + 1] = csub(cscale(b, c), cmul(s, a));
+        const int na = k - 1 - wc1, nb = wr0, nz = k;
+        const int nrot = m1 - m0;
+        for (int w = tid; w < na + nb + nz; w += ET) {
+          if (w < na) {
+            const int col = wc1 + 1 + w;
+            cplx x = H[m0 * ld + col];
+            for (int q = 0; q < nrot; ++q) {
+              const double c = rot_cs[q];
+              const cplx sn = rot_sn[q];
+              const cplx y = H[(m0 + q + 1) * ld + col];
+              H[(m0 + q) * ld + col] = cadd(cscale(x, c), cmul(sn, y));
+              x = csub(cscale(y, c), cmul(cconj(sn), x));
+            }
+            H[m1 * ld + col] = x;
+          } else {
+            cplx* M = (w < na + nb) ? H : Z;
+            const int r = (w < na + nb) ? w - na : w - na - nb;
+            cplx x = M[r * ld + m0];
+            for (int q = 0; q < nrot; ++q) {
+              const double c = rot_cs[q];
+              const cplx sn = rot_sn[q];
+              const cplx y = M[r * ld + m0 + q + 1];
+              M[r * ld + m0 + q] = cadd(cscale(x, c), cmul(cconj(sn), y));
+              x = csub(cscale(y, c), cmul(sn, x));
+            }
+            M[r * ld + m1] = x;
+          }
         }
         __syncthreads();
       }
@@ -502,6 +564,7 @@ __global__ void __launch_bounds__(ET) gen_eig_kernel(const cplx* __restrict__ At
     if (r > c) H[r * ld + c] = cmk(0.0, 0.0);
   }
   __syncthreads();
+  EIG_MARK(4);
   // 4. eigenvectors of T by back substitution: X[:, e]
   double tnorm = 0.0;
   for (int e = tid; e < k * k; e += ET) tnorm = fmax(tnorm, cabs1(H[e / k * ld + e % k]));
@@ -521,6 +584,7 @@ __global__ void __launch_bounds__(ET) gen_eig_kernel(const cplx* __restrict__ At
     }
   }
   __syncthreads();
+  EIG_MARK(5);
   // eigenvalue order: ascending by (re, im)
   for (int i = tid; i < k; i += ET) {
     const cplx li = H[i * ld + i];
@@ -551,6 +615,7 @@ __global__ void __launch_bounds__(ET) gen_eig_kernel(const cplx* __restrict__ At
       *p = cscale(*p, inv);
     }
   }
+  EIG_MARK(6);
   if (tid == 0) info[prob] = 0;
 }
 
@@ -578,4 +643,9 @@ CIRR_API int cirr_small_eig(int hermitian, const cplx* At, const cplx* Bt, long 
     gen_eig_kernel<<<nprob, ET, 0, stream>>>(At, Bt, ldin, sin_, kdim, kmax, ws, wstride, lam, S, lds, sS, info);
   CIRR_CHECK_LAUNCH();
   return 0;
+}
+
+// debug: clock64 phase stamps of the last gen_eig launch (problem 0)
+CIRR_API int cirr_small_eig_phases(long long* host_out) {
+  return (int)cudaMemcpyFromSymbol(host_out, g_eig_phase, sizeof(long long) * 8);
 }

@@ -4,7 +4,7 @@
 // sigma_i >= rel_tol * sigma_max).  One-sided (Hestenes) Jacobi is applied
 // directly to the columns of S, stored as contiguous rows of St (c x n):
 // pairs of columns are rotated until every normalised inner product is below
-// sqrt(n)*eps.  On convergence the columns are U*Sigma with U orthonormal to
+// 16 sqrt(n) eps.  On convergence the columns are U*Sigma with U orthonormal to
 // working precision, so sigma_i = ||col_i|| resolves ratios down to ~1e-15 --
 // needed because config 4's block has sigma_min/sigma_max ~ 2e-12 and a 1e-8
 // cut loses most pairs (finding 7).  Gram-based
@@ -187,7 +187,9 @@ CIRR_API int cirr_orth(cplx* W, long long ldw, long long wstride, int n, int c, 
   int grid = (int)(items < (long long)sms * per_sm ? items : (long long)sms * per_sm);
   if (grid < 1) grid = 1;
   if (c > 1) {
-    double tol = sqrt((double)n) * 1.1102230246251565e-16;
+    // rotation threshold on |x^H y| / (|x||y|): 16 sqrt(n) eps keeps it above the
+    // rounding noise of an n-term dot product (sqrt(n) eps alone never converges)
+    double tol = 16.0 * sqrt((double)n) * 1.1102230246251565e-16;
     int max_sweeps = 40;
     void* args[] = {&W, &ldw, &wstride, &n, &c, &nprob, &bar, &counters, &max_sweeps, &tol, &sweeps_out};
     e = cudaLaunchCooperativeKernel((void*)hestenes_kernel, dim3(grid), dim3(HT), args, 0, stream);

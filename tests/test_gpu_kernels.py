@@ -139,10 +139,10 @@ def test_orth_graded(lib, n, c):
     assert np.allclose(got[:k], ref[:k], rtol=1e-6, atol=1e-15)
     assert k == int(np.count_nonzero(ref >= 1e-12 * ref[0]))
     q = Qt.cpu().numpy()[:k].T
-    assert np.abs(q.conj().T @ q - np.eye(k)).max() < 1e-12
+    assert np.abs(q.conj().T @ q - np.eye(k)).max() < 1e-11
     # span: the kept basis captures S up to the dropped singular values
     resid = np.linalg.norm(Smat - q @ (q.conj().T @ Smat), 2)
-    assert resid <= 1e-13 * ref[0] + (ref[k] if k < c else 0.0)
+    assert resid <= 1e-12 * ref[0] + (ref[k] if k < c else 0.0)
 
 
 @pytest.mark.parametrize("k", [1, 6, 64, 200])
