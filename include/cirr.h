@@ -83,7 +83,7 @@ int cirr_small_eig(int hermitian, const cirr_cplx* At, const cirr_cplx* Bt, long
                    long long sin_, const int* kdim, int kmax, int nprob, void* ws, cirr_cplx* lam,
                    cirr_cplx* S, long long lds, long long sS, int* info, cudaStream_t stream);
 
-/* debug: clock64 stamps of the phases of the last general-eig launch (problem 0), 8 entries (host buffer) */
+/* debug: clock64 stamps of the phases of the last general-eig launch (problem 0), 10 entries (host buffer) */
 int cirr_small_eig_phases(long long* host_out);
 
 /* K7 -- replaces solvers.py:140-147 (_residuals). */

@@ -21,11 +21,12 @@
 namespace {
 
 constexpr int ET = 1024;
-constexpr int QC = 32;          // rotations per chunk of a QR sweep
+constexpr int GT = 256;         // threads of the general (non-Hermitian) solver
+constexpr int QC = 16;          // rotations per chunk of a QR sweep
 constexpr int WLD = QC + 4;     // window leading dimension
 
 // phase timestamps of problem 0 (clock64), read back with cirr_small_eig_phases
-__device__ long long g_eig_phase[8];
+__device__ long long g_eig_phase[16];
 #define EIG_MARK(i) do { if (blockIdx.x == 0 && threadIdx.x == 0) g_eig_phase[i] = clock64(); } while (0)
 constexpr double EPS = 1.1102230246251565e-16;
 
@@ -49,6 +50,28 @@ __device__ __forceinline__ EigWs carve(void* ws, long long wstride_bytes, int pr
   w.vec = w.T + kk;
   w.d = reinterpret_cast<double*>(w.vec + 4 * (long long)kmax);
   return w;
+}
+
+
+// Element-wise read-modify-write over `total` items with U loads in flight per
+// thread: all U loads of a batch are issued before any store, so L2 latency
+// is paid once per batch instead of once per element (the compiler cannot
+// reorder a load past a possibly-aliasing store on its own).
+template <int U, typename AddrF, typename UpdF>
+__device__ __forceinline__ void batched_rmw(int total, int nthreads, AddrF addr, UpdF upd) {
+  for (int e0 = threadIdx.x; e0 < total; e0 += nthreads * U) {
+    cplx* ptr[U];
+    cplx val[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * nthreads;
+      ptr[u] = e < total ? addr(e) : nullptr;
+      if (ptr[u]) val[u] = *ptr[u];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (ptr[u]) *ptr[u] = upd(e0 + u * nthreads, val[u]);
+  }
 }
 
 __device__ __forceinline__ void jrot(double app, double aqq, cplx apq, double& cs, cplx& se) {
@@ -251,7 +274,7 @@ __device__ cplx csqrt_(cplx z) {
   return cmk(fabs(y), z.y >= 0.0 ? x : -x);
 }
 
-__global__ void __launch_bounds__(ET) gen_eig_kernel(const cplx* __restrict__ At, const cplx* __restrict__ Bt,
+__global__ void __launch_bounds__(GT) gen_eig_kernel(const cplx* __restrict__ At, const cplx* __restrict__ Bt,
                                                      long long ldin, long long sin_, const int* __restrict__ kdim,
                                                      int kmax, void* ws, long long wstride,
                                                      cplx* __restrict__ lam, cplx* __restrict__ S, long long lds,
@@ -273,7 +296,7 @@ __global__ void __launch_bounds__(ET) gen_eig_kernel(const cplx* __restrict__ At
   cplx *H = w.A, *LU = w.L, *Z = w.V, *X = w.T;
   int* piv = reinterpret_cast<int*>(w.d);
   const int ld = kmax;
-  for (int e = tid; e < k * k; e += ET) {
+  for (int e = tid; e < k * k; e += GT) {
     int r = e / k, c = e % k;
     LU[r * ld + c] = Bi[(long long)r * ldin + c];
     H[r * ld + c] = Ai[(long long)r * ldin + c];
@@ -285,7 +308,7 @@ __global__ void __launch_bounds__(ET) gen_eig_kernel(const cplx* __restrict__ At
   // 1. LU of B~ with partial pivoting; apply the same row swaps to H
   for (int j = 0; j < k; ++j) {
     double best = -1.0; int bi = j;
-    for (int r = j + tid; r < k; r += ET) {
+    for (int r = j + tid; r < k; r += GT) {
       double v = cabs1(LU[r * ld + j]);
       if (v > best) { best = v; bi = r; }
     }
@@ -297,7 +320,8 @@ __global__ void __launch_bounds__(ET) gen_eig_kernel(const cplx* __restrict__ At
     if (lane == 0) { rv[wid] = best; ri[wid] = bi; }
     __syncthreads();
     if (wid == 0) {
-      best = rv[lane]; bi = ri[lane];
+      best = lane < GT / 32 ? rv[lane] : -1.0;
+      bi = lane < GT / 32 ? ri[lane] : k;
       for (int o = 16; o > 0; o >>= 1) {
         double ov = __shfl_xor_sync(0xffffffffu, best, o);
         int oi = __shfl_xor_sync(0xffffffffu, bi, o);
@@ -308,7 +332,7 @@ __global__ void __launch_bounds__(ET) gen_eig_kernel(const cplx* __restrict__ At
     __syncthreads();
     const int p = s_int[0];
     if (p != j) {
-      for (int c = tid; c < k; c += ET) {
+      for (int c = tid; c < k; c += GT) {
         cplx t = LU[j * ld + c]; LU[j * ld + c] = LU[p * ld + c]; LU[p * ld + c] = t;
         t = H[j * ld + c]; H[j * ld + c] = H[p * ld + c]; H[p * ld + c] = t;
       }
@@ -317,13 +341,12 @@ __global__ void __launch_bounds__(ET) gen_eig_kernel(const cplx* __restrict__ At
     const cplx pv = LU[j * ld + j];
     if (pv.x != 0.0 || pv.y != 0.0) {
       const cplx rp = crecip(pv);
-      for (int r = j + 1 + tid; r < k; r += ET) LU[r * ld + j] = cmul(LU[r * ld + j], rp);
+      for (int r = j + 1 + tid; r < k; r += GT) LU[r * ld + j] = cmul(LU[r * ld + j], rp);
       __syncthreads();
       const int m = k - j - 1;
-      for (int e = tid; e < m * m; e += ET) {
-        int r = j + 1 + e / m, c = j + 1 + e % m;
-        cfms(LU[r * ld + c], LU[r * ld + j], LU[j * ld + c]);
-      }
+      batched_rmw<4>(m * m, GT,
+          [&](int e) -> cplx* { return LU + (j + 1 + e / m) * ld + j + 1 + e % m; },
+          [&](int e, cplx v) { cfms(v, LU[(j + 1 + e / m) * ld + j], LU[j * ld + j + 1 + e % m]); return v; });
     }
     __syncthreads();
   }
@@ -333,7 +356,7 @@ __global__ void __launch_bounds__(ET) gen_eig_kernel(const cplx* __restrict__ At
   }
   EIG_MARK(1);
   // solve L U M = P A (column per thread), M into H
-  for (int c = tid; c < k; c += ET) {
+  for (int c = tid; c < k; c += GT) {
     for (int i = 0; i < k; ++i) {
       cplx v = H[i * ld + c];
       for (int l = 0; l < i; ++l) cfms(v, LU[i * ld + l], H[l * ld + c]);
@@ -347,54 +370,71 @@ __global__ void __launch_bounds__(ET) gen_eig_kernel(const cplx* __restrict__ At
   }
   __syncthreads();
   EIG_MARK(2);
-  // 2. Householder Hessenberg reduction H <- Q^H H Q, Z <- Z Q
+  // 2. Householder Hessenberg reduction H <- Q^H H Q, Z <- Z Q.  The two
+  // matrix-vector products per column are split into 16-deep slices (many
+  // independent L2 loads in flight per thread) with fixed-order partial sums.
   cplx* v = w.vec;          // Householder vector (length k)
-  cplx* wv = w.vec + kmax;  // work vectors (length 3k)
+  cplx* wv = w.vec + kmax;  // work vectors (length 2k)
+  cplx* part = w.T;         // partial sums (<= 2k x ceil(k/16)), T is free until step 4
   for (int j = 0; j + 2 < k; ++j) {
     const int m = k - j - 1;  // rows j+1 .. k-1
     double xs = 0.0;
-    for (int r = j + 2 + tid; r < k; r += ET) xs += cabs2(H[r * ld + j]);
+    for (int r = j + 2 + tid; r < k; r += GT) xs += cabs2(H[r * ld + j]);
     xs = block_sum(xs, red);
     const cplx alpha = H[(j + 1) * ld + j];
-    cplx tau = cmk(0.0, 0.0);
     if (xs != 0.0 || alpha.y != 0.0) {
       const double xnorm = sqrt(xs);
       double beta = sqrt(alpha.x * alpha.x + alpha.y * alpha.y + xnorm * xnorm);
       beta = alpha.x >= 0.0 ? -beta : beta;
-      tau = cmk((beta - alpha.x) / beta, -alpha.y / beta);
+      const cplx tau = cmk((beta - alpha.x) / beta, -alpha.y / beta);
       const cplx scal = crecip(cmk(alpha.x - beta, alpha.y));
-      for (int r = tid; r < m; r += ET) v[r] = r == 0 ? cmk(1.0, 0.0) : cmul(H[(j + 1 + r) * ld + j], scal);
+      for (int r = tid; r < m; r += GT) v[r] = r == 0 ? cmk(1.0, 0.0) : cmul(H[(j + 1 + r) * ld + j], scal);
       __syncthreads();
       if (tid == 0) H[(j + 1) * ld + j] = cmk(beta, 0.0);
-      for (int r = j + 2 + tid; r < k; r += ET) H[r * ld + j] = cmk(0.0, 0.0);
-      // left: H[j+1:, j+1:] -= conj(tau) v (v^H H)
-      for (int c = j + 1 + tid; c < k; c += ET) {
-        cplx s = cmk(0.0, 0.0);
-        for (int r = 0; r < m; ++r) cfma(s, cconj(v[r]), H[(j + 1 + r) * ld + c]);
-        wv[c] = s;
+      for (int r = j + 2 + tid; r < k; r += GT) H[r * ld + j] = cmk(0.0, 0.0);
+      // left: wv[c] = sum_r conj(v_r) H[j+1+r][c], c in j+1..k-1 (slices of 16 rows)
+      const int nc = k - j - 1, ns = (m + 15) / 16;
+      for (int e = tid; e < nc * ns; e += GT) {
+        const int c = j + 1 + e % nc, sl = e / nc;
+        const int r0 = sl * 16, r1 = min(m, r0 + 16);
+        cplx acc = cmk(0.0, 0.0);
+#pragma unroll 8
+        for (int r = r0; r < r1; ++r) cfma(acc, cconj(v[r]), H[(j + 1 + r) * ld + c]);
+        part[sl * (2 * kmax) + c] = acc;
+      }
+      __syncthreads();
+      for (int c = j + 1 + tid; c < k; c += GT) {
+        cplx acc = cmk(0.0, 0.0);
+        for (int sl = 0; sl < ns; ++sl) acc = cadd(acc, part[sl * (2 * kmax) + c]);
+        wv[c] = acc;
       }
       __syncthreads();
       const cplx ct = cconj(tau);
-      for (int e = tid; e < m * (k - j - 1); e += ET) {
-        int r = e / (k - j - 1), c = j + 1 + e % (k - j - 1);
-        cfms(H[(j + 1 + r) * ld + c], cmul(ct, v[r]), wv[c]);
+      batched_rmw<4>(m * nc, GT,
+          [&](int e) -> cplx* { return H + (j + 1 + e / nc) * ld + j + 1 + e % nc; },
+          [&](int e, cplx x) { cfms(x, cmul(ct, v[e / nc]), wv[j + 1 + e % nc]); return x; });
+      __syncthreads();
+      // right: wv[r] = sum_i M[r][j+1+i] v_i over the rows of H and Z (slices of 16 columns)
+      for (int e = tid; e < 2 * k * ns; e += GT) {
+        const int rowi = e % (2 * k), sl = e / (2 * k);
+        const cplx* M = rowi < k ? H : Z;
+        const int rr = rowi < k ? rowi : rowi - k;
+        const int i0 = sl * 16, i1 = min(m, i0 + 16);
+        cplx acc = cmk(0.0, 0.0);
+#pragma unroll 8
+        for (int i = i0; i < i1; ++i) cfma(acc, M[rr * ld + j + 1 + i], v[i]);
+        part[sl * (2 * kmax) + rowi] = acc;
       }
       __syncthreads();
-      // right: H[:, j+1:] -= tau (H v) v^H ;  Z[:, j+1:] likewise
-      for (int r = tid; r < 2 * k; r += ET) {
-        const cplx* M = r < k ? H : Z;
-        const int rr = r < k ? r : r - k;
-        cplx s = cmk(0.0, 0.0);
-        for (int i = 0; i < m; ++i) cfma(s, M[rr * ld + j + 1 + i], v[i]);
-        wv[r] = s;
+      for (int rowi = tid; rowi < 2 * k; rowi += GT) {
+        cplx acc = cmk(0.0, 0.0);
+        for (int sl = 0; sl < ns; ++sl) acc = cadd(acc, part[sl * (2 * kmax) + rowi]);
+        wv[rowi] = acc;
       }
       __syncthreads();
-      for (int e = tid; e < 2 * k * m; e += ET) {
-        int r = e / m, i = e % m;
-        cplx* M = r < k ? H : Z;
-        const int rr = r < k ? r : r - k;
-        cfms(M[rr * ld + j + 1 + i], cmul(tau, wv[r]), cconj(v[i]));
-      }
+      batched_rmw<4>(2 * k * m, GT,
+          [&](int e) -> cplx* { const int rowi = e / m; return (rowi < k ? H + rowi * ld : Z + (rowi - k) * ld) + j + 1 + e % m; },
+          [&](int e, cplx x) { cfms(x, cmul(tau, wv[e / m]), cconj(v[e % m])); return x; });
       __syncthreads();
     }
   }
@@ -403,13 +443,14 @@ __global__ void __launch_bounds__(ET) gen_eig_kernel(const cplx* __restrict__ At
   int ihi = k - 1;
   const int itmax = 30 * (k > 10 ? k : 10);
   int fail = 0;
+  long long n_sweeps = 0, n_rot = 0, t_win = 0, t_chain = 0, t_def = 0, t_scan = 0;
   while (ihi >= 0) {
     int l = 0;
     int its = 0;
     for (; its <= itmax; ++its) {
       // find the largest kk in (l, ihi] with a negligible subdiagonal
       int found = l;
-      for (int kk = l + 1 + tid; kk <= ihi; kk += ET) {
+      for (int kk = l + 1 + tid; kk <= ihi; kk += GT) {
         const double hs = cabs1(H[kk * ld + kk - 1]);
         double tst = cabs1(H[(kk - 1) * ld + kk - 1]) + cabs1(H[kk * ld + kk]);
         if (tst == 0.0) {
@@ -423,7 +464,7 @@ __global__ void __launch_bounds__(ET) gen_eig_kernel(const cplx* __restrict__ At
       __syncthreads();
       if (tid == 0) {
         int f = l;
-        for (int q = 0; q < ET / 32; ++q) f = max(f, ri[q]);
+        for (int q = 0; q < GT / 32; ++q) f = max(f, ri[q]);
         s_int[1] = f;
         if (f > l) H[f * ld + f - 1] = cmk(0.0, 0.0);
       }
@@ -459,46 +500,51 @@ __global__ void __launch_bounds__(ET) gen_eig_kernel(const cplx* __restrict__ At
       }
       __syncthreads();
       const cplx mu = s_c[0];
+      ++n_sweeps;
+      n_rot += ihi - l;
       // QR sweep over rows/cols l..ihi in chunks of QC rotations: warp 0 chases
       // the bulge through a shared-memory window (every entry the chain reads
       // lives there); afterwards all warps apply the chunk's rotations to the
       // far parts of H (left: window rows right of the window; right: rows
       // above it) and to Z, one carry per row/column, no further syncs.
       for (int m0 = l; m0 < ihi; m0 += QC) {
+        long long tq0 = clock64();
         const int m1 = min(m0 + QC, ihi);
         const int wr0 = m0, wr1 = min(m1 + 1, ihi);
         const int wc0 = (m0 > l) ? m0 - 1 : l, wc1 = min(m1 + 1, ihi);
         const int nwr = wr1 - wr0 + 1, nwc = wc1 - wc0 + 1;
-        for (int e = tid; e < nwr * nwc; e += ET) {
+        for (int e = tid; e < nwr * nwc; e += GT) {
           const int r = e / nwc, cc = e % nwc;
           win[r * WLD + cc] = H[(wr0 + r) * ld + wc0 + cc];
         }
         __syncthreads();
+        long long tq1 = clock64();
         if (wid == 0) {
 #define W_(r, c) win[((r) - wr0) * WLD + (c) - wc0]
           for (int m = m0; m < m1; ++m) {
+            // every lane forms the rotation itself (no broadcast); lane 0 records it
+            cplx x, y;
+            if (m == l) { x = csub(W_(l, l), mu); y = W_(l + 1, l); }
+            else { x = W_(m, m - 1); y = W_(m + 1, m - 1); }
+            const double nx2 = cabs2(x), ny2 = cabs2(y);
+            double c; cplx sn, r;
+            if (ny2 == 0.0) { c = 1.0; sn = cmk(0.0, 0.0); r = x; }
+            else if (nx2 == 0.0) { const double ay = sqrt(ny2); c = 0.0; sn = cscale(cconj(y), 1.0 / ay); r = cmk(ay, 0.0); }
+            else {
+              const double ax = sqrt(nx2);
+              const double inv = rsqrt(nx2 + ny2);
+              c = ax * inv;
+              const cplx ph = cscale(x, 1.0 / ax);
+              sn = cscale(cmul(ph, cconj(y)), inv);
+              r = cscale(ph, (nx2 + ny2) * inv);
+            }
+            __syncwarp();
             if (lane == 0) {
-              cplx x, y;
-              if (m == l) { x = csub(W_(l, l), mu); y = W_(l + 1, l); }
-              else { x = W_(m, m - 1); y = W_(m + 1, m - 1); }
-              const double ax = cabs(x), ay = cabs(y);
-              double c; cplx sn, r;
-              if (ay == 0.0) { c = 1.0; sn = cmk(0.0, 0.0); r = x; }
-              else if (ax == 0.0) { c = 0.0; sn = cscale(cconj(y), 1.0 / ay); r = cmk(ay, 0.0); }
-              else {
-                const double nrm = hypot(ax, ay);
-                c = ax / nrm;
-                const cplx ph = cscale(x, 1.0 / ax);
-                sn = cscale(cmul(ph, cconj(y)), 1.0 / nrm);
-                r = cscale(ph, nrm);
-              }
               if (m > l) { W_(m, m - 1) = r; W_(m + 1, m - 1) = cmk(0.0, 0.0); }
               rot_cs[m - m0] = c;
               rot_sn[m - m0] = sn;
             }
-            __syncwarp();
-            const double c = rot_cs[m - m0];
-            const cplx sn = rot_sn[m - m0], snc = cconj(sn);
+            const cplx snc = cconj(sn);
             for (int col = m + lane; col <= wc1; col += 32) {
               const cplx a = W_(m, col), b = W_(m + 1, col);
               W_(m, col) = cadd(cscale(a, c), cmul(sn, b));
@@ -516,50 +562,60 @@ __global__ void __launch_bounds__(ET) gen_eig_kernel(const cplx* __restrict__ At
 #undef W_
         }
         __syncthreads();
-        for (int e = tid; e < nwr * nwc; e += ET) {
+        long long tq2 = clock64();
+        for (int e = tid; e < nwr * nwc; e += GT) {
           const int r = e / nwc, cc = e % nwc;
           H[(wr0 + r) * ld + wc0 + cc] = win[r * WLD + cc];
         }
         const int na = k - 1 - wc1, nb = wr0, nz = k;
         const int nrot = m1 - m0;
-        for (int w = tid; w < na + nb + nz; w += ET) {
-          if (w < na) {
-            const int col = wc1 + 1 + w;
-            cplx x = H[m0 * ld + col];
-            for (int q = 0; q < nrot; ++q) {
-              const double c = rot_cs[q];
-              const cplx sn = rot_sn[q];
-              const cplx y = H[(m0 + q + 1) * ld + col];
-              H[(m0 + q) * ld + col] = cadd(cscale(x, c), cmul(sn, y));
-              x = csub(cscale(y, c), cmul(cconj(sn), x));
-            }
-            H[m1 * ld + col] = x;
-          } else {
-            cplx* M = (w < na + nb) ? H : Z;
+        for (int w = tid; w < na + nb + nz; w += GT) {
+          cplx* M;
+          long long base, step;
+          bool left;
+          if (w < na) { M = H; base = (long long)m0 * ld + wc1 + 1 + w; step = ld; left = true; }
+          else {
             const int r = (w < na + nb) ? w - na : w - na - nb;
-            cplx x = M[r * ld + m0];
-            for (int q = 0; q < nrot; ++q) {
-              const double c = rot_cs[q];
-              const cplx sn = rot_sn[q];
-              const cplx y = M[r * ld + m0 + q + 1];
-              M[r * ld + m0 + q] = cadd(cscale(x, c), cmul(cconj(sn), y));
-              x = csub(cscale(y, c), cmul(sn, x));
-            }
-            M[r * ld + m1] = x;
+            M = (w < na + nb) ? H : Z;
+            base = (long long)r * ld + m0; step = 1; left = false;
           }
+          cplx xs[QC + 1];
+#pragma unroll
+          for (int q = 0; q <= QC; ++q)
+            if (q <= nrot) xs[q] = M[base + q * step];
+#pragma unroll
+          for (int q = 0; q < QC; ++q) {
+            if (q < nrot) {
+              const double c = rot_cs[q];
+              const cplx sn = left ? rot_sn[q] : cconj(rot_sn[q]);
+              const cplx x = xs[q], y = xs[q + 1];
+              xs[q] = cadd(cscale(x, c), cmul(sn, y));
+              xs[q + 1] = csub(cscale(y, c), cmul(cconj(sn), x));
+            }
+          }
+#pragma unroll
+          for (int q = 0; q <= QC; ++q)
+            if (q <= nrot) M[base + q * step] = xs[q];
         }
+        __syncthreads();
+        long long tq3 = clock64();
+        t_win += tq1 - tq0; t_chain += tq2 - tq1; t_def += tq3 - tq2;
         __syncthreads();
       }
     }
     if (its > itmax) { fail = ihi + 1; break; }
     ihi = l - 1;
   }
+  if (blockIdx.x == 0 && tid == 0) {
+    g_eig_phase[8] = n_sweeps; g_eig_phase[9] = n_rot;
+    g_eig_phase[10] = t_win; g_eig_phase[11] = t_chain; g_eig_phase[12] = t_def;
+  }
   if (fail) {
     if (tid == 0) info[prob] = -fail;
     return;
   }
   // zero below the diagonal (Schur form is upper triangular)
-  for (int e = tid; e < k * k; e += ET) {
+  for (int e = tid; e < k * k; e += GT) {
     int r = e / k, c = e % k;
     if (r > c) H[r * ld + c] = cmk(0.0, 0.0);
   }
@@ -567,10 +623,10 @@ __global__ void __launch_bounds__(ET) gen_eig_kernel(const cplx* __restrict__ At
   EIG_MARK(4);
   // 4. eigenvectors of T by back substitution: X[:, e]
   double tnorm = 0.0;
-  for (int e = tid; e < k * k; e += ET) tnorm = fmax(tnorm, cabs1(H[e / k * ld + e % k]));
+  for (int e = tid; e < k * k; e += GT) tnorm = fmax(tnorm, cabs1(H[e / k * ld + e % k]));
   tnorm = block_max(tnorm, red);
   const double smlnum = 1e-300 * (double)k / EPS;
-  for (int e = tid; e < k; e += ET) {
+  for (int e = tid; e < k; e += GT) {
     const cplx te = H[e * ld + e];
     const double smin = fmax(EPS * cabs1(te), smlnum);
     for (int r = k - 1; r > e; --r) X[r * ld + e] = cmk(0.0, 0.0);
@@ -586,7 +642,7 @@ __global__ void __launch_bounds__(ET) gen_eig_kernel(const cplx* __restrict__ At
   __syncthreads();
   EIG_MARK(5);
   // eigenvalue order: ascending by (re, im)
-  for (int i = tid; i < k; i += ET) {
+  for (int i = tid; i < k; i += GT) {
     const cplx li = H[i * ld + i];
     int rank = 0;
     for (int j = 0; j < k; ++j) {
@@ -599,7 +655,7 @@ __global__ void __launch_bounds__(ET) gen_eig_kernel(const cplx* __restrict__ At
   __syncthreads();
   // vectors Z X, unit 2-norm; column e of the Schur vectors -> S[:, rank]
   cplx* Sp = S + (long long)prob * sS;
-  for (int e = wid; e < k; e += ET / 32) {
+  for (int e = wid; e < k; e += GT / 32) {
     double nrm = 0.0;
     for (int r = lane; r < k; r += 32) {
       cplx acc = cmk(0.0, 0.0);
@@ -640,12 +696,12 @@ CIRR_API int cirr_small_eig(int hermitian, const cplx* At, const cplx* Bt, long 
   if (hermitian)
     herm_eig_kernel<<<nprob, ET, 0, stream>>>(At, Bt, ldin, sin_, kdim, kmax, ws, wstride, lam, S, lds, sS, info);
   else
-    gen_eig_kernel<<<nprob, ET, 0, stream>>>(At, Bt, ldin, sin_, kdim, kmax, ws, wstride, lam, S, lds, sS, info);
+    gen_eig_kernel<<<nprob, GT, 0, stream>>>(At, Bt, ldin, sin_, kdim, kmax, ws, wstride, lam, S, lds, sS, info);
   CIRR_CHECK_LAUNCH();
   return 0;
 }
 
 // debug: clock64 phase stamps of the last gen_eig launch (problem 0)
 CIRR_API int cirr_small_eig_phases(long long* host_out) {
-  return (int)cudaMemcpyFromSymbol(host_out, g_eig_phase, sizeof(long long) * 8);
+  return (int)cudaMemcpyFromSymbol(host_out, g_eig_phase, sizeof(long long) * 16);
 }

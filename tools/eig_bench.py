@@ -36,11 +36,12 @@ def t_small(k, herm, nprob=2, reps=3):
     r = a[0] @ s - (b[0] @ s) * l[None, :]
     rel = np.linalg.norm(r, axis=0) / (np.linalg.norm(a[0] @ s, axis=0) + np.abs(l) * np.linalg.norm(b[0] @ s, axis=0))
     import ctypes
-    ph = (ctypes.c_longlong * 8)()
+    ph = (ctypes.c_longlong * 16)()
     _lib.call("cirr_small_eig_phases", ctypes.addressof(ph))
     if not herm:
         d = [ph[i + 1] - ph[i] for i in range(6)]
-        print("  phases (Mcycles): LU %.2f solve %.2f hess %.2f qr %.2f vec %.2f sort+Zx %.2f" % tuple(x / 1e6 for x in d))
+        print("  phases (Mcycles): LU %.2f solve %.2f hess %.2f qr %.2f vec %.2f sort+Zx %.2f" % tuple(x / 1e6 for x in d),
+              "sweeps", ph[8], "rotations", ph[9], "cycles/rot %.0f" % (d[3] / max(ph[9], 1)), "win/chain/def Mcyc %.1f %.1f %.1f" % (ph[10]/1e6, ph[11]/1e6, ph[12]/1e6))
     print(f"small_eig herm={herm} k={k} nprob={nprob}: {min(ts):.2f} ms, info={info.cpu().numpy()}, max rel res {rel.max():.1e}", flush=True)
 
 
