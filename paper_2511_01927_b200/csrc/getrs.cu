@@ -13,6 +13,7 @@
 //     (deterministic, test_solvers.py:192-198) reading every Y_j once and
 //     writes S transposed (one contiguous row per column of S) for K4.
 #include "common.cuh"
+#include "lu_gemm.cuh"
 
 namespace {
 
@@ -206,6 +207,57 @@ __global__ void __launch_bounds__(256) moments_kernel(const cplx* __restrict__ Y
   }
 }
 
+// Right-looking solve, diagonal step: Y[i0:i0+nb, c0:c0+64] <- T_ii^{-1} Y[...]
+// (unit lower when LOWER, else upper with its diagonal), one CTA per
+// (64-column chunk, pencil).
+constexpr int DSC = 64;
+constexpr int kDiagSmem = (SNB * SD_LD + SNB * (DSC + 1) + SNB) * 16;
+
+template <bool LOWER>
+__global__ void __launch_bounds__(256) diag_solve_kernel(const cplx* __restrict__ LU, long long ld, long long pstride,
+                                                         int i0, int nb, cplx* __restrict__ Y, long long ldy,
+                                                         long long ystride, int K) {
+  extern __shared__ __align__(16) cplx dsm[];
+  cplx* D = dsm;
+  cplx* X = D + SNB * SD_LD;
+  cplx* dinv = X + SNB * (DSC + 1);
+  const int b = blockIdx.y, c0 = blockIdx.x * DSC, tid = threadIdx.x;
+  const cplx* T = LU + (long long)b * pstride;
+  cplx* Yb = Y + (long long)b * ystride;
+  const int nc = min(DSC, K - c0);
+  for (int e = tid; e < nb * nb; e += 256) {
+    const int r = e / nb, c = e % nb;
+    D[r * SD_LD + c] = T[(long long)(i0 + r) * ld + i0 + c];
+  }
+  for (int e = tid; e < nb * DSC; e += 256) {
+    const int r = e / DSC, c = e % DSC;
+    X[r * (DSC + 1) + c] = c < nc ? Yb[(long long)(i0 + r) * ldy + c0 + c] : cmk(0.0, 0.0);
+  }
+  __syncthreads();
+  if (!LOWER && tid < nb) dinv[tid] = crecip(D[tid * SD_LD + tid]);
+  __syncthreads();
+  const int c = tid % DSC, g = tid / DSC;  // 4 row groups
+  if (LOWER) {
+    for (int i = 0; i < nb - 1; ++i) {
+      const cplx xi = X[i * (DSC + 1) + c];
+      for (int r = i + 1 + g; r < nb; r += 4) cfms(X[r * (DSC + 1) + c], D[r * SD_LD + i], xi);
+      __syncthreads();
+    }
+  } else {
+    for (int i = nb - 1; i >= 0; --i) {
+      const cplx xi = cmul(X[i * (DSC + 1) + c], dinv[i]);
+      __syncthreads();
+      if (g == 0) X[i * (DSC + 1) + c] = xi;
+      for (int r = g; r < i; r += 4) cfms(X[r * (DSC + 1) + c], D[r * SD_LD + i], xi);
+      __syncthreads();
+    }
+  }
+  for (int e = tid; e < nb * DSC; e += 256) {
+    const int r = e / DSC, cc = e % DSC;
+    if (cc < nc) Yb[(long long)(i0 + r) * ldy + c0 + cc] = X[r * (DSC + 1) + cc];
+  }
+}
+
 }  // namespace
 
 // Y_j = (P_j^T L_j U_j)^{-1} R_{rhs_of[j]} for j < batch.  LU/perm from
@@ -227,6 +279,39 @@ CIRR_API int cirr_zgetrs_batched(const cplx* LU, int n, long long ld, long long 
   dim3 gp((unsigned)(((long long)n * K + 255) / 256), batch);
   permute_kernel<<<gp, 256, 0, stream>>>(R, ldr, rstride, rhs_of, perm, n, K, Y, ldy, ystride);
   CIRR_CHECK_LAUNCH();
+  // right-looking blocked solves: per 64-row block a diagonal solve, then the
+  // rank-64 update of the remaining rows on the TMA/DMMA GEMM (zgemm_sub_tma)
+  // narrow RHS blocks (K <= 48) stay on the left-looking kernel: the 64-wide
+  // GEMM tile of the right-looking path would be mostly padding there
+  cirr::OperandMaps mT, mY;
+  bool tma = K > 48 && cirr::encode_c128_map(&mT.a, LU, n, n, batch, ld, pencil_stride, cirr::PBK, cirr::PBM) == 0 &&
+             cirr::encode_c128_map(&mY.b, Y, K, n, batch, ldy, ystride, cirr::PBN, cirr::PBK) == 0 &&
+             cirr::encode_c128_map(&mY.c, Y, K, n, batch, ldy, ystride, cirr::PBN, cirr::PBM) == 0;
+  if (tma) {
+    static bool dattr = false;
+    if (!dattr) {
+      cudaFuncSetAttribute(diag_solve_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDiagSmem);
+      cudaFuncSetAttribute(diag_solve_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDiagSmem);
+      dattr = true;
+    }
+    const int nblk = (n + SNB - 1) / SNB;
+    dim3 gd((K + DSC - 1) / DSC, batch);
+    for (int bi = 0; bi < nblk; ++bi) {  // forward: L (unit lower)
+      const int i0 = bi * SNB, nb = min(SNB, n - i0);
+      diag_solve_kernel<true><<<gd, 256, kDiagSmem, stream>>>(LU, ld, pencil_stride, i0, nb, Y, ldy, ystride, K);
+      CIRR_CHECK_LAUNCH();
+      CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, n - i0 - nb, K, nb, batch, i0 + nb, i0, i0, 0, i0 + nb, 0,
+                                    Y, ldy, ystride, stream));
+    }
+    for (int bi = nblk - 1; bi >= 0; --bi) {  // backward: U
+      const int i0 = bi * SNB, nb = min(SNB, n - i0);
+      diag_solve_kernel<false><<<gd, 256, kDiagSmem, stream>>>(LU, ld, pencil_stride, i0, nb, Y, ldy, ystride, K);
+      CIRR_CHECK_LAUNCH();
+      CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, i0, K, nb, batch, 0, i0, i0, 0, 0, 0, Y, ldy, ystride,
+                                    stream));
+    }
+    return 0;
+  }
   dim3 gs((K + SKC - 1) / SKC, batch);
   trsm_blocked_kernel<true><<<gs, 256, kSolveSmem, stream>>>(LU, ld, pencil_stride, n, Y, ldy, ystride, K);
   CIRR_CHECK_LAUNCH();

@@ -66,7 +66,7 @@ struct SubGemmGeom {
   int tiles_m, tiles_n;
 };
 
-__global__ void __launch_bounds__(PTHREADS, 1) zgemm_sub_tma(const __grid_constant__ CUtensorMap mapA,
+static __global__ void __launch_bounds__(PTHREADS, 1) zgemm_sub_tma(const __grid_constant__ CUtensorMap mapA,
                                                              const __grid_constant__ CUtensorMap mapB,
                                                              const __grid_constant__ CUtensorMap mapC,
                                                              SubGemmGeom g) {
@@ -192,12 +192,11 @@ __global__ void __launch_bounds__(PTHREADS, 1) zgemm_sub_tma(const __grid_consta
   }
 }
 
-// Tensor maps over a pencil batch viewed as float64 {2n, n, batch}.
-struct PencilMaps {
-  CUtensorMap a, b, c;
-};
-
-inline int encode_pencil_maps(PencilMaps& pm, cplx* base, int n, long long ld, long long pstride, int batch) {
+// Encode a TMA map over a batch of row-major complex128 matrices viewed as a
+// float64 tensor {2*cols, rows, batch}, with a box of box_rows x box_cols
+// complex elements.  Out-of-range boxes are zero-filled by the hardware.
+static inline int encode_c128_map(CUtensorMap* map, const cplx* base, int cols, int rows, int batch, long long ld,
+                           long long bstride, int box_cols, int box_rows) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
@@ -207,26 +206,38 @@ inline int encode_pencil_maps(PencilMaps& pm, cplx* base, int n, long long ld, l
       return (int)cudaErrorNotSupported;
     encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
-  cuuint64_t dims[3] = {(cuuint64_t)2 * n, (cuuint64_t)n, (cuuint64_t)batch};
-  cuuint64_t strides[2] = {(cuuint64_t)ld * 16, (cuuint64_t)pstride * 16};
+  if ((reinterpret_cast<uintptr_t>(base) & 15) != 0) return (int)cudaErrorInvalidValue;
+  cuuint64_t dims[3] = {(cuuint64_t)2 * cols, (cuuint64_t)rows, (cuuint64_t)batch};
+  cuuint64_t strides[2] = {(cuuint64_t)ld * 16, (cuuint64_t)(bstride > 0 ? bstride : ld * rows) * 16};
   cuuint32_t estr[3] = {1, 1, 1};
-  cuuint32_t boxA[3] = {2 * PBK, PBM, 1}, boxB[3] = {2 * PBN, PBK, 1}, boxC[3] = {2 * PBN, PBM, 1};
-  CUtensorMap* maps[3] = {&pm.a, &pm.b, &pm.c};
-  cuuint32_t* boxes[3] = {boxA, boxB, boxC};
-  for (int i = 0; i < 3; ++i) {
-    CUresult r = encode(maps[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, boxes[i], estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return (int)cudaErrorInvalidValue;
-  }
+  cuuint32_t box[3] = {(cuuint32_t)(2 * box_cols), (cuuint32_t)box_rows, 1};
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<cplx*>(base), dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : (int)cudaErrorInvalidValue;
+}
+
+// Maps for the three operand roles: A (64 x 16 boxes), B (16 x 64), C (64 x 64).
+struct OperandMaps {
+  CUtensorMap a, b, c;
+};
+using PencilMaps = OperandMaps;
+
+static inline int encode_pencil_maps(PencilMaps& pm, cplx* base, int n, long long ld, long long pstride, int batch) {
+  CIRR_TRY(encode_c128_map(&pm.a, base, n, n, batch, ld, pstride, PBK, PBM));
+  CIRR_TRY(encode_c128_map(&pm.b, base, n, n, batch, ld, pstride, PBN, PBK));
+  CIRR_TRY(encode_c128_map(&pm.c, base, n, n, batch, ld, pstride, PBN, PBM));
   return 0;
 }
 
-// A22 -= L21 U12 for panel step (k, jb) of every pencil, via the TMA kernel.
-inline int lu_update_tma(const PencilMaps& pm, cplx* pencils, int n, long long ld, long long pstride, int batch,
-                         int k, int jb, cudaStream_t stream) {
-  const int rest = n - k - jb;
-  if (rest <= 0) return 0;
+// C[b] -= A[b] @ B[b] on sub-blocks addressed through TMA maps (A: mapA with
+// origin (a_row0, a_col0), etc.); C is also written through (C, ldc, sC).
+// K is rounded up to a multiple of 16: the extra slice must lie outside the
+// tensors (zero-filled) or hold zeros.
+static inline int zgemm_sub_maps(const CUtensorMap& mapA, const CUtensorMap& mapB, const CUtensorMap& mapC, int M, int N,
+                          int K, int batch, int a_row0, int a_col0, int b_row0, int b_col0, int c_row0, int c_col0,
+                          cplx* C, long long ldc, long long sC, cudaStream_t stream) {
+  if (M <= 0 || N <= 0 || K <= 0 || batch <= 0) return 0;
   static bool attr = false;
   static int sms = 0;
   if (!attr) {
@@ -236,14 +247,23 @@ inline int lu_update_tma(const PencilMaps& pm, cplx* pencils, int n, long long l
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     attr = true;
   }
-  SubGemmGeom g{rest, rest, jb, batch, k + jb, k, k, k + jb, k + jb, k + jb, pencils, ld, pstride,
-                (rest + PBM - 1) / PBM, (rest + PBN - 1) / PBN};
+  const int Kr = (K + PBK - 1) / PBK * PBK;
+  SubGemmGeom g{M, N, Kr, batch, a_row0, a_col0, b_row0, b_col0, c_row0, c_col0, C, ldc, sC,
+                (M + PBM - 1) / PBM, (N + PBN - 1) / PBN};
   const long long tiles = (long long)g.tiles_m * g.tiles_n * batch;
   const int grid = (int)(tiles < sms ? tiles : sms);
-  zgemm_sub_tma<<<grid, PTHREADS, P_SMEM, stream>>>(pm.a, pm.b, pm.c, g);
+  zgemm_sub_tma<<<grid, PTHREADS, P_SMEM, stream>>>(mapA, mapB, mapC, g);
   cirr_note_launch();
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : (int)e;
+}
+
+// A22 -= L21 U12 for panel step (k, jb) of every pencil, via the TMA kernel.
+static inline int lu_update_tma(const PencilMaps& pm, cplx* pencils, int n, long long ld, long long pstride, int batch,
+                         int k, int jb, cudaStream_t stream) {
+  const int rest = n - k - jb;
+  return zgemm_sub_maps(pm.a, pm.b, pm.c, rest, rest, jb, batch, k + jb, k, k, k + jb, k + jb, k + jb, pencils, ld,
+                        pstride, stream);
 }
 
 }  // namespace cirr
