@@ -40,6 +40,7 @@ from .errors import (
 )
 
 PIVOT_REL_TOL = 1e-14  # linalg.py:26
+_DEBUG = bool(int(__import__("os").environ.get("CIRR_DEBUG", "0")))
 
 
 def _torch():
@@ -496,6 +497,8 @@ class _Engine:
         _lib.call("cirr_orth", _ptr(W), n, cmax * n, n, cmax, nb, float(cfg.rank_rel_tol), _ptr(sigma),
                   _ptr(order), _ptr(kept), _ptr(Qt), n, cmax * n, _ptr(ws), _ptr(sweeps), st)
         ks = kept.cpu().numpy()
+        if _DEBUG:
+            print(f"[cirr] orth: c={cmax} nprob={nb} kept={ks.tolist()} sweeps={int(sweeps.item())}", flush=True)
         live = [b for b in range(nb) if ks[b] > 0]
         for b in range(nb):
             if ks[b] == 0:
