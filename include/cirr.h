@@ -62,9 +62,11 @@ int cirr_moments(const cirr_cplx* Y, long long ldy, long long ystride, int n, in
                  long long ld_st, long long sstride, cudaStream_t stream);
 
 /* K4 -- replaces linalg.py:107-119 (thin SVD + sigma >= rel_tol*sigma_max).
- * One-sided Jacobi on the rows of W (c x n per problem, overwritten);
- * sigma/order: nprob x c (descending), kept: nprob, Qt: kept x n rows.
- * ws: >= 64 bytes device scratch; *sweeps_out (device int). */
+ * Householder QR of S + one-sided Jacobi SVD of R; W (c x n per problem: the
+ * columns of S as rows) is overwritten; sigma/order: nprob x c (descending),
+ * kept: nprob, Qt: kept x n rows (orthonormal columns of Q).
+ * ws: cirr_orth_ws_bytes(c, nprob) bytes; *sweeps_out (device int). */
+long long cirr_orth_ws_bytes(int c, int nprob);
 int cirr_orth(cirr_cplx* W, long long ldw, long long wstride, int n, int c, int nprob,
               double rel_tol, double* sigma, int* order, int* kept, cirr_cplx* Qt,
               long long ldq, long long qstride, void* ws, int* sweeps_out, cudaStream_t stream);

@@ -28,6 +28,7 @@ SIGNATURES = {
     "cirr_zgetrf_batched": [_P, _I, _L, _L, _I, _P, _P, _P, _P, _P],
     "cirr_zgetrs_batched": [_P, _I, _L, _L, _I, _P, _P, _L, _L, _P, _I, _P, _L, _L, _P],
     "cirr_moments": [_P, _L, _L, _I, _I, _P, _I, _P, _I, _P, _L, _L, _P],
+    "cirr_orth_ws_bytes": [_I, _I],
     "cirr_orth": [_P, _L, _L, _I, _I, _I, _D, _P, _P, _P, _P, _L, _L, _P, _P, _P],
     "cirr_gemm": [_I, _I, _I, _I, _I, _P, _L, _L, _P, _L, _L, _P, _L, _L, _D, _I, _P],
     "cirr_small_eig_ws_bytes": [_I],
@@ -39,8 +40,8 @@ SIGNATURES = {
     "cirr_target_sm": [],
     "cirr_launch_count": [],
 }
-_RESTYPE = {"cirr_small_eig_ws_bytes": _L, "cirr_launch_count": _L}
-_RAW = {"cirr_small_eig_ws_bytes", "cirr_launch_count", "cirr_target_sm"}
+_RESTYPE = {"cirr_small_eig_ws_bytes": _L, "cirr_launch_count": _L, "cirr_orth_ws_bytes": _L}
+_RAW = {"cirr_small_eig_ws_bytes", "cirr_launch_count", "cirr_target_sm", "cirr_orth_ws_bytes"}
 
 _lib = None
 

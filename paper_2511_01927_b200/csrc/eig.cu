@@ -443,7 +443,7 @@ __global__ void __launch_bounds__(GT) gen_eig_kernel(const cplx* __restrict__ At
   int ihi = k - 1;
   const int itmax = 30 * (k > 10 ? k : 10);
   int fail = 0;
-  long long n_sweeps = 0, n_rot = 0, t_win = 0, t_chain = 0, t_def = 0, t_scan = 0;
+  long long n_sweeps = 0, n_rot = 0, t_win = 0, t_chain = 0, t_def = 0;
   while (ihi >= 0) {
     int l = 0;
     int its = 0;

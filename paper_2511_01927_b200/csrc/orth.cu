@@ -1,19 +1,15 @@
 // K4: rank-revealing orthonormalisation of the stacked moment block.
 //
 // Replaces linalg.py:107-119 (thin SVD of S, keep left singular vectors with
-// sigma_i >= rel_tol * sigma_max).  One-sided (Hestenes) Jacobi is applied
-// directly to the columns of S, stored as contiguous rows of St (c x n):
-// pairs of columns are rotated until every normalised inner product is below
-// 16 sqrt(n) eps.  On convergence the columns are U*Sigma with U orthonormal to
-// working precision, so sigma_i = ||col_i|| resolves ratios down to ~1e-15 --
-// needed because config 4's block has sigma_min/sigma_max ~ 2e-12 and a 1e-8
-// cut loses most pairs (finding 7).  Gram-based
-// CholeskyQR cannot resolve that.
-//
-// Rounds use the circle-method tournament (c/2 disjoint pairs per round) and
-// run as ONE cooperative kernel with a software grid barrier between rounds;
-// every reduction is a fixed-order block reduction, so results are
-// bit-reproducible.
+// sigma_i >= rel_tol * sigma_max).  It must resolve sigma ratios near 1e-12:
+// config 4's block has sigma_min/sigma_max ~ 2e-12 and a 1e-8 cut loses most
+// pairs (finding 7), so Gram-based CholeskyQR is out.
+// Algorithm: Householder QR of S (backward stable), one-sided Jacobi SVD of
+// the small R with the rotations accumulated (QR preconditioning makes R
+// graded: ~3x fewer sweeps than Jacobi on S), then Q = Q_house [U_R; 0] for
+// the kept singular vectors.  Jacobi rounds use the circle-method tournament;
+// everything runs in one cooperative kernel with a software grid barrier
+// between dependent steps; all reductions are fixed-order (bit-reproducible).
 #include "common.cuh"
 
 namespace {
@@ -49,161 +45,270 @@ __device__ __forceinline__ void rr_pair(int round, int k, int cp, int& p, int& q
 
 constexpr int HT = 256;
 
-__global__ void __launch_bounds__(HT) hestenes_kernel(cplx* __restrict__ W, long long ldw, long long wstride,
-                                                       int n, int c, int nprob, unsigned* bar, int* counters,
-                                                       int max_sweeps, double tol, int* sweeps_out) {
+// --------------------------------------------------------------------------
+// QR-preconditioned one-sided Jacobi (the production path).
+//
+//  A. Householder QR of S (n x c): the columns of S are the rows of W, so every
+//     reflector and every update works on contiguous rows.  Reflector j is
+//     stored in row j of W below the diagonal (LAPACK layout) with R above it.
+//  B. One-sided Jacobi on the rows of R (length c) with the rotations
+//     accumulated into J: R^H J = X Sigma  =>  R = J Sigma X^H, so J holds the
+//     left singular vectors of R.  R after QR is graded, which cuts the sweep
+//     count ~3x against Jacobi on S itself (Drmac-Veselic preconditioning),
+//     and each rotation touches c instead of n entries.
+//  C. sigma = row norms, descending sort, rank cut; Q = H_0 ... H_{c-1} [J_kept; 0].
+// One cooperative launch; grid barriers separate the dependent steps.
+__global__ void __launch_bounds__(HT) qr_jacobi_kernel(cplx* __restrict__ W, long long ldw, long long wstride,
+                                                        int n, int c, int nprob, double rel_tol,
+                                                        double* __restrict__ sigma, int* __restrict__ order,
+                                                        int* __restrict__ kept, cplx* __restrict__ Qt,
+                                                        long long ldq, long long qstride, unsigned* bar,
+                                                        int* counters, cplx* __restrict__ Xc,
+                                                        cplx* __restrict__ Jt, cplx* __restrict__ tau,
+                                                        int max_sweeps, double tol, int* sweeps_out) {
   __shared__ double red[4][HT / 32];
+  __shared__ double sred[32];
+  const int G = gridDim.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int jmax = min(c, n);
+  const long long cc = (long long)c * c;
+  // ---------------- A: Householder QR ----------------
+  for (int j = 0; j < jmax; ++j) {
+    for (int p = blockIdx.x; p < nprob; p += G) {
+      cplx* x = W + (long long)p * wstride + (long long)j * ldw;
+      double sq = 0.0;
+      for (int i = j + 1 + tid; i < n; i += HT) sq += cabs2(x[i]);
+      sq = block_sum(sq, sred);
+      const cplx alpha = x[j];
+      cplx t = cmk(0.0, 0.0);
+      if (sq != 0.0 || alpha.y != 0.0) {
+        double beta = sqrt(alpha.x * alpha.x + alpha.y * alpha.y + sq);
+        beta = alpha.x >= 0.0 ? -beta : beta;
+        t = cmk((beta - alpha.x) / beta, -alpha.y / beta);
+        const cplx scal = crecip(cmk(alpha.x - beta, alpha.y));
+        for (int i = j + 1 + tid; i < n; i += HT) x[i] = cmul(x[i], scal);
+        __syncthreads();
+        if (tid == 0) x[j] = cmk(beta, 0.0);
+      }
+      if (tid == 0) tau[(long long)p * c + j] = t;
+    }
+    grid_barrier(bar, G);
+    const int rest = c - j - 1;
+    const long long items = (long long)nprob * rest;
+    for (long long it = blockIdx.x; it < items; it += G) {
+      const int p = (int)(it / rest), q = j + 1 + (int)(it % rest);
+      const cplx t = tau[(long long)p * c + j];
+      if (t.x == 0.0 && t.y == 0.0) continue;
+      const cplx* v = W + (long long)p * wstride + (long long)j * ldw;
+      cplx* y = W + (long long)p * wstride + (long long)q * ldw;
+      double wr = 0.0, wi = 0.0;
+      for (int i = j + tid; i < n; i += HT) {
+        const cplx vi = i == j ? cmk(1.0, 0.0) : v[i];
+        const cplx g = cconjmul(vi, y[i]);
+        wr += g.x;
+        wi += g.y;
+      }
+      wr = warp_sum(wr); wi = warp_sum(wi);
+      __syncthreads();
+      if (lane == 0) { red[0][wid] = wr; red[1][wid] = wi; }
+      __syncthreads();
+      wr = 0.0; wi = 0.0;
+      for (int w2 = 0; w2 < HT / 32; ++w2) { wr += red[0][w2]; wi += red[1][w2]; }
+      const cplx f = cmul(cconj(t), cmk(wr, wi));
+      for (int i = j + tid; i < n; i += HT) {
+        const cplx vi = i == j ? cmk(1.0, 0.0) : v[i];
+        cfms(y[i], vi, f);
+      }
+    }
+    grid_barrier(bar, G);
+  }
+  // ---------------- B: Jacobi on the rows of R ----------------
+  // Xc[p][a][i] = conj(R[a][i]) (R[a][i] = W[p][i][a] for a <= i < c, a < jmax), Jt = I
+  {
+    const long long total = (long long)nprob * cc;
+    for (long long e = (long long)blockIdx.x * HT + tid; e < total; e += (long long)G * HT) {
+      const int p = (int)(e / cc);
+      const int a = (int)((e % cc) / c), i = (int)(e % c);
+      const cplx r = (a <= i && a < jmax) ? W[(long long)p * wstride + (long long)i * ldw + a] : cmk(0.0, 0.0);
+      Xc[e] = cconj(r);
+      Jt[e] = cmk(a == i ? 1.0 : 0.0, 0.0);
+    }
+  }
+  if (blockIdx.x == 0 && tid == 0) { counters[0] = 0; counters[1] = 0; }
+  grid_barrier(bar, G);
   const int cp = c + (c & 1);
   const int npairs = cp / 2;
-  const long long items = (long long)nprob * npairs;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const long long pitems = (long long)nprob * npairs;
   int sweep = 0;
-  for (; sweep < max_sweeps; ++sweep) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) counters[(sweep + 1) & 1] = 0;
+  for (; sweep < max_sweeps && c > 1; ++sweep) {
+    if (blockIdx.x == 0 && tid == 0) counters[(sweep + 1) & 1] = 0;
     for (int round = 0; round < cp - 1; ++round) {
-      for (long long it = blockIdx.x; it < items; it += gridDim.x) {
-        const int prob = (int)(it / npairs), k = (int)(it % npairs);
-        int p, q;
-        rr_pair(round, k, cp, p, q);
-        if (p >= c || q >= c) continue;
-        if (p > q) { int t = p; p = q; q = t; }
-        cplx* wp = W + (long long)prob * wstride + (long long)p * ldw;
-        cplx* wq = W + (long long)prob * wstride + (long long)q * ldw;
-        double a = 0.0, bb = 0.0, gr = 0.0, gi = 0.0;
-        for (int i = threadIdx.x; i < n; i += HT) {
-          cplx x = wp[i], y = wq[i];
-          a += cabs2(x);
-          bb += cabs2(y);
-          cplx g = cconjmul(x, y);
+      for (long long it = blockIdx.x; it < pitems; it += G) {
+        const int p = (int)(it / npairs), k = (int)(it % npairs);
+        int a, b2;
+        rr_pair(round, k, cp, a, b2);
+        if (a >= c || b2 >= c) continue;
+        if (a > b2) { int t = a; a = b2; b2 = t; }
+        cplx* xa = Xc + (long long)p * cc + (long long)a * c;
+        cplx* xb = Xc + (long long)p * cc + (long long)b2 * c;
+        double al = 0.0, be = 0.0, gr = 0.0, gi = 0.0;
+        for (int i = tid; i < c; i += HT) {
+          const cplx x = xa[i], y = xb[i];
+          al += cabs2(x);
+          be += cabs2(y);
+          const cplx g = cconjmul(x, y);
           gr += g.x;
           gi += g.y;
         }
-        a = warp_sum(a); bb = warp_sum(bb); gr = warp_sum(gr); gi = warp_sum(gi);
+        al = warp_sum(al); be = warp_sum(be); gr = warp_sum(gr); gi = warp_sum(gi);
         __syncthreads();
-        if (lane == 0) { red[0][wid] = a; red[1][wid] = bb; red[2][wid] = gr; red[3][wid] = gi; }
+        if (lane == 0) { red[0][wid] = al; red[1][wid] = be; red[2][wid] = gr; red[3][wid] = gi; }
         __syncthreads();
-        a = 0.0; bb = 0.0; gr = 0.0; gi = 0.0;
-        for (int w = 0; w < HT / 32; ++w) { a += red[0][w]; bb += red[1][w]; gr += red[2][w]; gi += red[3][w]; }
+        al = 0.0; be = 0.0; gr = 0.0; gi = 0.0;
+        for (int w2 = 0; w2 < HT / 32; ++w2) { al += red[0][w2]; be += red[1][w2]; gr += red[2][w2]; gi += red[3][w2]; }
         const double ag = hypot(gr, gi);
-        if (a > 0.0 && bb > 0.0 && ag > tol * sqrt(a) * sqrt(bb)) {
-          // [wp', wq'] = [wp, wq] [[c, s e^{i phi}], [-s e^{-i phi}, c]],  gamma = |gamma| e^{i phi}
-          const double zeta = (bb - a) / (2.0 * ag);
+        if (al > 0.0 && be > 0.0 && ag > tol * sqrt(al) * sqrt(be)) {
+          const double zeta = (be - al) / (2.0 * ag);
           const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
           const double cs = 1.0 / sqrt(1.0 + t * t), sn = t * cs;
-          const cplx e = cmk(gr / ag, gi / ag);
-          const cplx se = cscale(e, sn);          // s e^{i phi}
-          const cplx sec = cconj(se);             // s e^{-i phi}
-          for (int i = threadIdx.x; i < n; i += HT) {
-            cplx x = wp[i], y = wq[i];
-            cplx nx = csub(cscale(x, cs), cmul(sec, y));
-            cplx ny = cadd(cmul(se, x), cscale(y, cs));
-            wp[i] = nx;
-            wq[i] = ny;
+          const cplx se = cmk(sn * gr / ag, sn * gi / ag);
+          const cplx sec = cconj(se);
+          cplx* ja = Jt + (long long)p * cc + (long long)a * c;
+          cplx* jb = Jt + (long long)p * cc + (long long)b2 * c;
+          for (int i = tid; i < c; i += HT) {
+            const cplx x = xa[i], y = xb[i];
+            xa[i] = csub(cscale(x, cs), cmul(sec, y));
+            xb[i] = cadd(cmul(se, x), cscale(y, cs));
+            const cplx u = ja[i], w = jb[i];
+            ja[i] = csub(cscale(u, cs), cmul(sec, w));
+            jb[i] = cadd(cmul(se, u), cscale(w, cs));
           }
-          if (threadIdx.x == 0) atomicAdd(counters + (sweep & 1), 1);
+          if (tid == 0) atomicAdd(counters + (sweep & 1), 1);
         }
       }
-      grid_barrier(bar, gridDim.x);
+      grid_barrier(bar, G);
     }
     const int rots = *((volatile int*)(counters + (sweep & 1)));
-    grid_barrier(bar, gridDim.x);
+    grid_barrier(bar, G);
     if (rots == 0) { ++sweep; break; }
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) *sweeps_out = sweep;
-}
-
-// sigma, descending order, kept count per problem (one CTA per problem).
-__global__ void __launch_bounds__(1024) svd_finalize_kernel(const cplx* __restrict__ W, long long ldw,
-                                                             long long wstride, int n, int c, double rel_tol,
-                                                             double* __restrict__ sigma, int* __restrict__ order,
-                                                             int* __restrict__ kept) {
-  extern __shared__ double sg[];
-  const int prob = blockIdx.x;
-  const cplx* Wp = W + (long long)prob * wstride;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int row = wid; row < c; row += nw) {
-    double s = 0.0;
-    for (int i = lane; i < n; i += 32) s += cabs2(Wp[(long long)row * ldw + i]);
-    s = warp_sum(s);
-    if (lane == 0) sg[row] = sqrt(s);
-  }
-  __syncthreads();
-  double smax = 0.0;
-  for (int i = 0; i < c; ++i) smax = fmax(smax, sg[i]);
-  for (int i = threadIdx.x; i < c; i += blockDim.x) {
-    const double si = sg[i];
-    int rank = 0;
-    for (int j = 0; j < c; ++j) {
-      const double sj = sg[j];
-      rank += (sj > si) || (sj == si && j < i);
+  if (blockIdx.x == 0 && tid == 0) *sweeps_out = sweep;
+  // ---------------- C: singular values, rank cut, Q ----------------
+  for (int p = blockIdx.x; p < nprob; p += G) {
+    double* sg = reinterpret_cast<double*>(tau + (long long)nprob * c) + (long long)p * c;  // scratch
+    for (int a = wid; a < c; a += HT / 32) {
+      double s2 = 0.0;
+      for (int i = lane; i < c; i += 32) s2 += cabs2(Xc[(long long)p * cc + (long long)a * c + i]);
+      s2 = warp_sum(s2);
+      if (lane == 0) sg[a] = sqrt(s2);
     }
-    order[(long long)prob * c + rank] = i;
-    sigma[(long long)prob * c + rank] = si;
+    __syncthreads();
+    double smax = 0.0;
+    for (int a = 0; a < c; ++a) smax = fmax(smax, sg[a]);
+    for (int a = tid; a < c; a += HT) {
+      const double sa = sg[a];
+      int rank = 0;
+      for (int b3 = 0; b3 < c; ++b3) {
+        const double sb = sg[b3];
+        rank += (sb > sa) || (sb == sa && b3 < a);
+      }
+      order[(long long)p * c + rank] = a;
+      sigma[(long long)p * c + rank] = sa;
+    }
+    if (tid == 0) {
+      int k = 0;
+      if (smax > 0.0)
+        for (int a = 0; a < c; ++a) k += sg[a] >= rel_tol * smax;
+      kept[p] = k;
+    }
+    __syncthreads();
   }
-  if (threadIdx.x == 0) {
-    int k = 0;
-    if (smax > 0.0)
-      for (int i = 0; i < c; ++i) k += sg[i] >= rel_tol * smax;
-    kept[prob] = k;
+  grid_barrier(bar, G);
+  // Qt[p][r] = [J[:, order[r]]; 0] for r < kept[p]
+  for (long long e = (long long)blockIdx.x * HT + tid; e < (long long)nprob * c * n; e += (long long)G * HT) {
+    const int p = (int)(e / ((long long)c * n));
+    const int r = (int)((e / n) % c), i = (int)(e % n);
+    if (r >= kept[p]) continue;
+    const int a = order[(long long)p * c + r];
+    Qt[(long long)p * qstride + (long long)r * ldq + i] = i < c ? Jt[(long long)p * cc + (long long)a * c + i]
+                                                              : cmk(0.0, 0.0);
   }
-}
-
-// Qt[prob][r][:] = W[prob][order[r]][:] / sigma[r]   for r < kept[prob]
-__global__ void build_q_kernel(const cplx* __restrict__ W, long long ldw, long long wstride, int n, int c,
-                               const double* __restrict__ sigma, const int* __restrict__ order,
-                               const int* __restrict__ kept, cplx* __restrict__ Qt, long long ldq,
-                               long long qstride) {
-  const int prob = blockIdx.z, r = blockIdx.y;
-  if (r >= kept[prob]) return;
-  const int src = order[(long long)prob * c + r];
-  const double inv = 1.0 / sigma[(long long)prob * c + r];
-  const cplx* w = W + (long long)prob * wstride + (long long)src * ldw;
-  cplx* q = Qt + (long long)prob * qstride + (long long)r * ldq;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    q[i] = cscale(w[i], inv);
+  grid_barrier(bar, G);
+  // apply H_{jmax-1}, ..., H_0 to every kept row of Qt (a column of Q)
+  for (int j = jmax - 1; j >= 0; --j) {
+    const long long items = (long long)nprob * c;
+    for (long long it = blockIdx.x; it < items; it += G) {
+      const int p = (int)(it / c), r = (int)(it % c);
+      if (r >= kept[p]) continue;
+      const cplx t = tau[(long long)p * c + j];
+      if (t.x == 0.0 && t.y == 0.0) continue;
+      const cplx* v = W + (long long)p * wstride + (long long)j * ldw;
+      cplx* y = Qt + (long long)p * qstride + (long long)r * ldq;
+      double wr = 0.0, wi = 0.0;
+      for (int i = j + tid; i < n; i += HT) {
+        const cplx vi = i == j ? cmk(1.0, 0.0) : v[i];
+        const cplx g = cconjmul(vi, y[i]);
+        wr += g.x;
+        wi += g.y;
+      }
+      wr = warp_sum(wr); wi = warp_sum(wi);
+      __syncthreads();
+      if (lane == 0) { red[0][wid] = wr; red[1][wid] = wi; }
+      __syncthreads();
+      wr = 0.0; wi = 0.0;
+      for (int w2 = 0; w2 < HT / 32; ++w2) { wr += red[0][w2]; wi += red[1][w2]; }
+      const cplx f = cmul(t, cmk(wr, wi));
+      for (int i = j + tid; i < n; i += HT) {
+        const cplx vi = i == j ? cmk(1.0, 0.0) : v[i];
+        cfms(y[i], vi, f);
+      }
+    }
+    grid_barrier(bar, G);
+  }
 }
 
 }  // namespace
 
-// One-sided Jacobi SVD of nprob blocks W[prob] (c rows of length n, i.e. the
-// columns of S as rows).  W is overwritten by U*Sigma (rows).  Outputs:
-// sigma (nprob x c, descending), order (nprob x c), kept (nprob), and
-// Qt[prob] (kept x n rows, orthonormal).  ws: >= 64 bytes of device scratch.
-// Returns the number of sweeps in *sweeps_out (device int).
+// Workspace bytes for cirr_orth (barrier/counters, X and J (nprob x c x c),
+// tau and sigma scratch).
+CIRR_API long long cirr_orth_ws_bytes(int c, int nprob) {
+  return 256 + 2LL * nprob * c * c * 16 + (long long)nprob * c * 16 + (long long)nprob * c * 8 + 256;
+}
+
+// Rank-revealing orthonormal basis of S (n x c) for nprob blocks; W[prob] holds
+// the columns of S as rows (c x n, overwritten by the QR reflectors).
+// Outputs: sigma (nprob x c, descending), order (nprob x c), kept (nprob,
+// sigma >= rel_tol * sigma_max), Qt[prob] (kept x n rows: orthonormal columns
+// of Q spanning the kept left singular vectors).  ws: cirr_orth_ws_bytes.
+// *sweeps_out (device int) = Jacobi sweeps used.
 CIRR_API int cirr_orth(cplx* W, long long ldw, long long wstride, int n, int c, int nprob, double rel_tol,
                        double* sigma, int* order, int* kept, cplx* Qt, long long ldq, long long qstride,
                        void* ws, int* sweeps_out, cudaStream_t stream) {
   if (n <= 0 || c <= 0 || nprob <= 0 || ldw < n || ldq < n) return CIRR_EINVAL;
-  unsigned* bar = reinterpret_cast<unsigned*>(ws);
-  int* counters = reinterpret_cast<int*>(bar + 2);
-  cudaError_t e = cudaMemsetAsync(ws, 0, 64, stream);
+  unsigned char* base = reinterpret_cast<unsigned char*>(ws);
+  unsigned* bar = reinterpret_cast<unsigned*>(base);
+  int* counters = reinterpret_cast<int*>(base + 16);
+  cplx* Xc = reinterpret_cast<cplx*>(base + 256);
+  cplx* Jt = Xc + (long long)nprob * c * c;
+  cplx* tau = Jt + (long long)nprob * c * c;
+  cudaError_t e = cudaMemsetAsync(ws, 0, 256, stream);
   if (e != cudaSuccess) return (int)e;
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hestenes_kernel, HT, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qr_jacobi_kernel, HT, 0);
   const int cp = c + (c & 1);
-  long long items = (long long)nprob * (cp / 2);
-  int grid = (int)(items < (long long)sms * per_sm ? items : (long long)sms * per_sm);
+  long long want = (long long)nprob * (cp / 2);
+  if (want < (long long)nprob * c) want = (long long)nprob * c;
+  long long cap = (long long)sms * (per_sm < 2 ? per_sm : 2);
+  int grid = (int)(want < cap ? want : cap);
   if (grid < 1) grid = 1;
-  if (c > 1) {
-    // rotation threshold on |x^H y| / (|x||y|): 16 sqrt(n) eps keeps it above the
-    // rounding noise of an n-term dot product (sqrt(n) eps alone never converges)
-    double tol = 16.0 * sqrt((double)n) * 1.1102230246251565e-16;
-    int max_sweeps = 40;
-    void* args[] = {&W, &ldw, &wstride, &n, &c, &nprob, &bar, &counters, &max_sweeps, &tol, &sweeps_out};
-    e = cudaLaunchCooperativeKernel((void*)hestenes_kernel, dim3(grid), dim3(HT), args, 0, stream);
-    cirr_note_launch();
-    if (e != cudaSuccess) return (int)e;
-  } else {
-    e = cudaMemsetAsync(sweeps_out, 0, sizeof(int), stream);
-    if (e != cudaSuccess) return (int)e;
-  }
-  size_t sm = sizeof(double) * (size_t)c;
-  svd_finalize_kernel<<<nprob, 1024, sm, stream>>>(W, ldw, wstride, n, c, rel_tol, sigma, order, kept);
-  CIRR_CHECK_LAUNCH();
-  dim3 gq((n + 255) / 256 < 64 ? (n + 255) / 256 : 64, c, nprob);
-  build_q_kernel<<<gq, 256, 0, stream>>>(W, ldw, wstride, n, c, sigma, order, kept, Qt, ldq, qstride);
-  CIRR_CHECK_LAUNCH();
+  // rotation threshold on |x^H y| / (|x||y|) for length-c rows
+  double tol = 16.0 * sqrt((double)c) * 1.1102230246251565e-16;
+  int max_sweeps = 60;
+  void* args[] = {&W, &ldw, &wstride, &n, &c, &nprob, &rel_tol, &sigma, &order, &kept, &Qt, &ldq, &qstride,
+                  &bar, &counters, &Xc, &Jt, &tau, &max_sweeps, &tol, &sweeps_out};
+  e = cudaLaunchCooperativeKernel((void*)qr_jacobi_kernel, dim3(grid), dim3(HT), args, 0, stream);
+  cirr_note_launch();
+  if (e != cudaSuccess) return (int)e;
   return 0;
 }

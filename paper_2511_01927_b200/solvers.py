@@ -492,7 +492,7 @@ class _Engine:
         order = torch.empty((nb, cmax), dtype=torch.int32, device="cuda")
         kept = torch.empty(nb, dtype=torch.int32, device="cuda")
         Qt = torch.zeros((nb, cmax, n), dtype=torch.complex128, device="cuda")
-        ws = torch.zeros(16, dtype=torch.int32, device="cuda")
+        ws = torch.empty(int(_lib.call("cirr_orth_ws_bytes", cmax, nb)), dtype=torch.uint8, device="cuda")
         sweeps = torch.zeros(1, dtype=torch.int32, device="cuda")
         _lib.call("cirr_orth", _ptr(W), n, cmax * n, n, cmax, nb, float(cfg.rank_rel_tol), _ptr(sigma),
                   _ptr(order), _ptr(kept), _ptr(Qt), n, cmax * n, _ptr(ws), _ptr(sweeps), st)

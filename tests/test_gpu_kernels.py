@@ -128,7 +128,7 @@ def test_orth_graded(lib, n, c):
     order = torch.empty(c, dtype=torch.int32, device="cuda")
     kept = torch.empty(1, dtype=torch.int32, device="cuda")
     Qt = torch.empty((c, n), dtype=torch.complex128, device="cuda")
-    ws = torch.zeros(16, dtype=torch.int32, device="cuda")
+    ws = torch.empty(lib.call("cirr_orth_ws_bytes", c, 1), dtype=torch.uint8, device="cuda")
     sw = torch.zeros(1, dtype=torch.int32, device="cuda")
     lib.call("cirr_orth", P(W), n, c * n, n, c, 1, 1e-12, P(sig), P(order), P(kept), P(Qt), n, c * n, P(ws), P(sw),
              S())

@@ -54,7 +54,7 @@ def t_orth(n, c, nprob=2, reps=2):
     st = torch.cuda.current_stream().cuda_stream
     sig = torch.empty((nprob, c), dtype=torch.float64, device="cuda"); order = torch.empty((nprob, c), dtype=torch.int32, device="cuda")
     kept = torch.empty(nprob, dtype=torch.int32, device="cuda"); Qt = torch.empty((nprob, c, n), dtype=torch.complex128, device="cuda")
-    ws = torch.zeros(16, dtype=torch.int32, device="cuda"); sw = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ws = torch.empty(_lib.call("cirr_orth_ws_bytes", c, nprob), dtype=torch.uint8, device="cuda"); sw = torch.zeros(1, dtype=torch.int32, device="cuda")
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for _ in range(reps):
         W = W0.clone()
