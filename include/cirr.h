@@ -85,6 +85,18 @@ int cirr_small_eig(int hermitian, const cirr_cplx* At, const cirr_cplx* Bt, long
                    long long sin_, const int* kdim, int kmax, int nprob, void* ws, cirr_cplx* lam,
                    cirr_cplx* S, long long lds, long long sS, int* info, cudaStream_t stream);
 
+/* K6 non-Hermitian (k <= 256): phase 1 eigenvalues (sorted by re, im) of
+ * B~^-1 A~ via batched LU/solve, cooperative Hessenberg reduction and an
+ * eigenvalue-only QR; phase 2 unit-norm eigenvectors for selected sorted
+ * indices by inverse iteration + Householder back-transform. */
+long long cirr_gen_eig_ws_bytes(int kmax, int nprob);
+long long cirr_gen_eig_vec_scratch_bytes(int kmax, int nprob, int smax);
+int cirr_gen_eig_values(const cirr_cplx* At, const cirr_cplx* Bt, const int* kdim, int kmax, int nprob, void* ws,
+                        cirr_cplx* lam, int* info, cudaStream_t stream);
+int cirr_gen_eig_vectors(void* ws, const int* kdim, int kmax, int nprob, const cirr_cplx* lam, const int* sel,
+                         const int* sel_cnt, int smax, void* scratch, cirr_cplx* S, long long lds, long long sS,
+                         cudaStream_t stream);
+
 /* debug: clock64 stamps of the phases of the last general-eig launch (problem 0), 10 entries (host buffer) */
 int cirr_small_eig_phases(long long* host_out);
 

@@ -34,14 +34,20 @@ SIGNATURES = {
     "cirr_small_eig_ws_bytes": [_I],
     "cirr_small_eig": [_I, _P, _P, _L, _L, _P, _I, _I, _P, _P, _P, _L, _L, _P, _P],
     "cirr_small_eig_phases": [_P],
+    "cirr_gen_eig_ws_bytes": [_I, _I],
+    "cirr_gen_eig_vec_scratch_bytes": [_I, _I, _I],
+    "cirr_gen_eig_values": [_P, _P, _P, _I, _I, _P, _P, _P, _P],
+    "cirr_gen_eig_vectors": [_P, _P, _I, _I, _P, _P, _P, _I, _P, _P, _L, _L, _P],
     "cirr_residuals": [_P, _P, _L, _L, _I, _P, _L, _P, _I, _I, _P, _L, _P],
     "cirr_gather_cols": [_P, _L, _L, _P, _L, _P, _I, _I, _I, _P, _L, _L, _P],
     "cirr_transpose": [_I, _P, _L, _L, _I, _I, _I, _P, _L, _L, _P],
     "cirr_target_sm": [],
     "cirr_launch_count": [],
 }
-_RESTYPE = {"cirr_small_eig_ws_bytes": _L, "cirr_launch_count": _L, "cirr_orth_ws_bytes": _L}
-_RAW = {"cirr_small_eig_ws_bytes", "cirr_launch_count", "cirr_target_sm", "cirr_orth_ws_bytes"}
+_RESTYPE = {"cirr_small_eig_ws_bytes": _L, "cirr_launch_count": _L, "cirr_orth_ws_bytes": _L,
+            "cirr_gen_eig_ws_bytes": _L, "cirr_gen_eig_vec_scratch_bytes": _L}
+_RAW = {"cirr_small_eig_ws_bytes", "cirr_launch_count", "cirr_target_sm", "cirr_orth_ws_bytes",
+        "cirr_gen_eig_ws_bytes", "cirr_gen_eig_vec_scratch_bytes"}
 
 _lib = None
 

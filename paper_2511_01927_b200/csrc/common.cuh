@@ -140,3 +140,24 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pre
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+
+// Software grid barrier for cooperative launches (all CTAs co-resident).
+// bar[0] = arrival counter, bar[1] = generation.
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* vgen = bar + 1;
+    unsigned gen = *vgen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == nblocks - 1) {
+      bar[0] = 0;
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*vgen == gen) { __nanosleep(32); }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+

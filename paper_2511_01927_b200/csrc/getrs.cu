@@ -284,7 +284,7 @@ CIRR_API int cirr_zgetrs_batched(const cplx* LU, int n, long long ld, long long 
   // narrow RHS blocks (K <= 48) stay on the left-looking kernel: the 64-wide
   // GEMM tile of the right-looking path would be mostly padding there
   cirr::OperandMaps mT, mY;
-  bool tma = K > 48 && cirr::encode_c128_map(&mT.a, LU, n, n, batch, ld, pencil_stride, cirr::PBK, cirr::PBM) == 0 &&
+  bool tma = K > 48 && n >= 64 && cirr::encode_c128_map(&mT.a, LU, n, n, batch, ld, pencil_stride, cirr::PBK, cirr::PBM) == 0 &&
              cirr::encode_c128_map(&mY.b, Y, K, n, batch, ldy, ystride, cirr::PBN, cirr::PBK) == 0 &&
              cirr::encode_c128_map(&mY.c, Y, K, n, batch, ldy, ystride, cirr::PBN, cirr::PBM) == 0;
   if (tma) {

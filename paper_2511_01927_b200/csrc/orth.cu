@@ -14,24 +14,6 @@
 
 namespace {
 
-__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    volatile unsigned* vgen = bar + 1;
-    unsigned gen = *vgen;
-    __threadfence();
-    if (atomicAdd(bar, 1u) == nblocks - 1) {
-      bar[0] = 0;
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
-    } else {
-      while (*vgen == gen) { __nanosleep(32); }
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-
 __device__ __forceinline__ void rr_pair(int round, int k, int cp, int& p, int& q) {
   // circle method over cp (even) players; player cp-1 is fixed
   if (k == 0) {

@@ -529,16 +529,23 @@ class _Engine:
                   kk, 1.0, 0, st)
         _lib.call("cirr_gemm", 1, kmax, kmax, n, nb, _ptr(Qt), n, kmax * n, _ptr(BQ), kmax, n * kmax, _ptr(Bt), kmax,
                   kk, 1.0, 0, st)
-        # K6: small eigenproblems, one CTA each
+        # K6: small eigenproblems
         herm = self.dp.hermitian
         kdim = torch.from_numpy(ks.astype(np.int32)).to("cuda")
-        wsb = int(_lib.call("cirr_small_eig_ws_bytes", kmax))
-        ews = torch.empty(nb * ((wsb + 255) // 256 * 256), dtype=torch.uint8, device="cuda")
-        lam = torch.zeros((nb, kmax), dtype=torch.complex128, device="cuda")
-        Sv = torch.zeros((nb, kmax, kmax), dtype=torch.complex128, device="cuda")
         info = torch.zeros(nb, dtype=torch.int32, device="cuda")
-        _lib.call("cirr_small_eig", 1 if herm else 0, _ptr(At), _ptr(Bt), kmax, kk, _ptr(kdim), kmax, nb,
-                  _ptr(ews), _ptr(lam), _ptr(Sv), kmax, kk, _ptr(info), st)
+        lam = torch.zeros((nb, kmax), dtype=torch.complex128, device="cuda")
+        general_split = (not herm) and kmax <= 256
+        if general_split:
+            # eigenvalues first; eigenvectors later only for the inside ones
+            gws = torch.empty(int(_lib.call("cirr_gen_eig_ws_bytes", kmax, nb)), dtype=torch.uint8, device="cuda")
+            _lib.call("cirr_gen_eig_values", _ptr(At), _ptr(Bt), _ptr(kdim), kmax, nb, _ptr(gws), _ptr(lam),
+                      _ptr(info), st)
+        else:
+            wsb = int(_lib.call("cirr_small_eig_ws_bytes", kmax))
+            ews = torch.empty(nb * ((wsb + 255) // 256 * 256), dtype=torch.uint8, device="cuda")
+            Sv = torch.zeros((nb, kmax, kmax), dtype=torch.complex128, device="cuda")
+            _lib.call("cirr_small_eig", 1 if herm else 0, _ptr(At), _ptr(Bt), kmax, kk, _ptr(kdim), kmax, nb,
+                      _ptr(ews), _ptr(lam), _ptr(Sv), kmax, kk, _ptr(info), st)
         infos = info.cpu().numpy()
         lam_h = lam.cpu().numpy()
         keep_idx = {}
@@ -560,10 +567,7 @@ class _Engine:
             keep_idx[b] = np.nonzero(keep)[0]
         if not keep_idx:
             return out
-        # K7: X = Q s, inside columns, A X, B X, residuals
-        X = torch.empty((nb, n, kmax), dtype=torch.complex128, device="cuda")
-        _lib.call("cirr_gemm", 0, n, kmax, kmax, nb, _ptr(Q), kmax, n * kmax, _ptr(Sv), kmax, kk, _ptr(X), kmax,
-                  n * kmax, 1.0, 0, st)
+        # K7: X = Q s for the inside columns, A X, B X, residuals
         kin_max = max(len(v) for v in keep_idx.values())
         idx = np.zeros((nb, kin_max), dtype=np.int32)
         cnt = np.zeros(nb, dtype=np.int32)
@@ -575,8 +579,20 @@ class _Engine:
         idx_t = torch.from_numpy(idx).to("cuda")
         cnt_t = torch.from_numpy(cnt).to("cuda")
         Xi = torch.zeros((nb, n, kin_max), dtype=torch.complex128, device="cuda")
-        _lib.call("cirr_gather_cols", _ptr(X), kmax, n * kmax, _ptr(idx_t), kin_max, _ptr(cnt_t), kin_max, n, nb,
-                  _ptr(Xi), kin_max, n * kin_max, st)
+        if general_split:
+            scr = torch.empty(int(_lib.call("cirr_gen_eig_vec_scratch_bytes", kmax, nb, kin_max)), dtype=torch.uint8,
+                              device="cuda")
+            Sin = torch.zeros((nb, kmax, kin_max), dtype=torch.complex128, device="cuda")
+            _lib.call("cirr_gen_eig_vectors", _ptr(gws), _ptr(kdim), kmax, nb, _ptr(lam), _ptr(idx_t), _ptr(cnt_t),
+                      kin_max, _ptr(scr), _ptr(Sin), kin_max, kmax * kin_max, st)
+            _lib.call("cirr_gemm", 0, n, kin_max, kmax, nb, _ptr(Q), kmax, n * kmax, _ptr(Sin), kin_max,
+                      kmax * kin_max, _ptr(Xi), kin_max, n * kin_max, 1.0, 0, st)
+        else:
+            X = torch.empty((nb, n, kmax), dtype=torch.complex128, device="cuda")
+            _lib.call("cirr_gemm", 0, n, kmax, kmax, nb, _ptr(Q), kmax, n * kmax, _ptr(Sv), kmax, kk, _ptr(X), kmax,
+                      n * kmax, 1.0, 0, st)
+            _lib.call("cirr_gather_cols", _ptr(X), kmax, n * kmax, _ptr(idx_t), kin_max, _ptr(cnt_t), kin_max, n, nb,
+                      _ptr(Xi), kin_max, n * kin_max, st)
         AX = torch.empty_like(Xi)
         BX = torch.empty_like(Xi)
         _lib.call("cirr_gemm", 2, n, kin_max, n, nb, _ptr(self.dp.a), n, 0, _ptr(Xi), kin_max, n * kin_max,
