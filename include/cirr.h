@@ -44,8 +44,10 @@ int cirr_symmetry(const double* A, int n, long long lda, double* out, cudaStream
  * In-place P M = L U of `batch` pencils; ipiv/perm: batch x n int32;
  * minpiv[j] = min_i |U_ii|; info[j] = first exact zero pivot (1-based) or 0. */
 int cirr_zgetrf_batched(cirr_cplx* pencils, int n, long long ld, long long pencil_stride,
-                        int batch, int* ipiv, int* perm, double* minpiv, int* info,
+                        int batch, int* ipiv, int* perm, double* minpiv, int* info, void* ws,
                         cudaStream_t stream);
+/* ws bytes for cirr_zgetrf_batched (L11^-1 blocks; ws may be NULL: slower TRSM path) */
+long long cirr_zgetrf_ws_bytes(int n, int batch);
 
 /* K3a -- replaces linalg.py:46-52 (SuperLU gstrs) as used at solvers.py:124.
  * Y[j] = M_j^{-1} R[rhs_of[j]] (rhs_of: device int32[batch]). */

@@ -93,15 +93,23 @@ __global__ void __launch_bounds__(PT) panel_kernel(cplx* __restrict__ P, int n, 
       const bool nz = (pv.x != 0.0 || pv.y != 0.0);
       const cplx rp = nz ? crecip(pv) : cmk(0.0, 0.0);
       const int rest = c0 + ib - c - 1;
+      // every row segment is loaded whole before it is written back, so the
+      // (up to IB) loads of a row are in flight together
       for (int r = row0 + 1 + tid; r < n; r += PT) {
         cplx* rowp = A + (long long)r * ld + col;
-        cplx l = nz ? cmul(rowp[0], rp) : rowp[0];
+        cplx seg[IB];
+#pragma unroll
+        for (int cc = 0; cc < IB; ++cc)
+          if (cc <= rest) seg[cc] = rowp[cc];
+        const cplx l = nz ? cmul(seg[0], rp) : seg[0];
         rowp[0] = l;
-        for (int cc = 1; cc <= rest; ++cc) {
-          cplx v = rowp[cc];
-          cfms(v, l, prow[cc]);
-          rowp[cc] = v;
-        }
+#pragma unroll
+        for (int cc = 1; cc < IB; ++cc)
+          if (cc <= rest) {
+            cplx v = seg[cc];
+            cfms(v, l, prow[cc]);
+            rowp[cc] = v;
+          }
       }
       __syncthreads();
     }
@@ -126,12 +134,22 @@ __global__ void __launch_bounds__(PT) panel_kernel(cplx* __restrict__ P, int n, 
       for (int r = r0 + ib + tid; r < n; r += PT) {
         cplx l[IB];
         const cplx* lr = A + (long long)r * ld + k + c0;
-        for (int i = 0; i < ib; ++i) l[i] = lr[i];
+#pragma unroll
+        for (int i = 0; i < IB; ++i) l[i] = i < ib ? lr[i] : cmk(0.0, 0.0);
         cplx* dst = A + (long long)r * ld + k + c0 + ib;
-        for (int cc = 0; cc < nr; ++cc) {
-          cplx v = dst[cc];
-          for (int i = 0; i < ib; ++i) cfms(v, l[i], ublk[i][cc]);
-          dst[cc] = v;
+        // 8-column chunks: all loads of a chunk issue before its stores
+        for (int c1 = 0; c1 < nr; c1 += 8) {
+          cplx v[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (c1 + q < nr) v[q] = dst[c1 + q];
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (c1 + q < nr) {
+#pragma unroll
+              for (int i = 0; i < IB; ++i) cfms(v[q], l[i], ublk[i][c1 + q]);
+              dst[c1 + q] = v[q];
+            }
         }
       }
       __syncthreads();
@@ -194,6 +212,33 @@ __global__ void __launch_bounds__(256) trsm_kernel(cplx* __restrict__ P, int n, 
   }
 }
 
+// Linv[b] = L11^{-1} for the unit-lower 64x64 diagonal block of panel step k
+// (|l_ij| <= 1 under partial pivoting, so the explicit inverse is benign --
+// the MAGMA trtri+gemm approach).  U12 = Linv A12 then runs on the TMA GEMM.
+constexpr int kLinvSmem = NB * (NB + 1) * 16 * 2;
+__global__ void __launch_bounds__(256) linv_kernel(const cplx* __restrict__ P, long long ld, long long pstride, int k,
+                                                   cplx* __restrict__ Linv) {
+  extern __shared__ cplx lsm[];
+  cplx(*L)[NB + 1] = reinterpret_cast<cplx(*)[NB + 1]>(lsm);
+  cplx(*X)[NB + 1] = reinterpret_cast<cplx(*)[NB + 1]>(lsm + NB * (NB + 1));
+  const cplx* A = P + (long long)blockIdx.x * pstride;
+  for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
+    const int r = e / NB, c = e % NB;
+    L[r][c] = A[(long long)(k + r) * ld + k + c];
+    X[r][c] = cmk(r == c ? 1.0 : 0.0, 0.0);
+  }
+  __syncthreads();
+  // forward substitution on all 64 unit columns at once: thread column c, row group g
+  const int c = threadIdx.x % NB, g = threadIdx.x / NB;
+  for (int i = 0; i < NB - 1; ++i) {
+    const cplx xi = X[i][c];
+    for (int r = i + 1 + g; r < NB; r += 4) cfms(X[r][c], L[r][i], xi);
+    __syncthreads();
+  }
+  cplx* out = Linv + (long long)blockIdx.x * NB * NB;
+  for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) out[e] = X[e / NB][e % NB];
+}
+
 // perm[i] = source row of row i of P*M (composition of the ipiv interchanges).
 __global__ void perm_kernel(const int* __restrict__ ipiv, int* __restrict__ perm, int n) {
   extern __shared__ int sp[];
@@ -222,8 +267,11 @@ __global__ void init_kernel(double* minpiv, int* info, int batch) {
 // pencil_stride elements, leading dimension ld).  Outputs ipiv (batch x n,
 // 0-based LAPACK-style interchanges), perm (batch x n, row permutation),
 // minpiv (min_i |U_ii|) and info (first exact zero pivot, 1-based, or 0).
+// Workspace for cirr_zgetrf_batched (L11^{-1} blocks); 0 disables that path.
+CIRR_API long long cirr_zgetrf_ws_bytes(int n, int batch) { return (long long)batch * NB * NB * 16 + 256; }
+
 CIRR_API int cirr_zgetrf_batched(cplx* pencils, int n, long long ld, long long pencil_stride, int batch,
-                                 int* ipiv, int* perm, double* minpiv, int* info, cudaStream_t stream) {
+                                 int* ipiv, int* perm, double* minpiv, int* info, void* ws, cudaStream_t stream) {
   if (n <= 0 || batch <= 0 || ld < n) return CIRR_EINVAL;
   static bool attr = false;
   if (!attr) {
@@ -234,6 +282,17 @@ CIRR_API int cirr_zgetrf_batched(cplx* pencils, int n, long long ld, long long p
   CIRR_CHECK_LAUNCH();
   cirr::PencilMaps maps;
   const bool use_tma = cirr::encode_pencil_maps(maps, pencils, n, ld, pencil_stride, batch) == 0;
+  cplx* linv = reinterpret_cast<cplx*>(ws);
+  CUtensorMap mapL;
+  const bool use_linv = use_tma && linv != nullptr &&
+                        cirr::encode_c128_map(&mapL, linv, NB, NB, batch, NB, (long long)NB * NB, cirr::PBK, cirr::PBM) == 0;
+  if (use_linv) {
+    static bool la = false;
+    if (!la) {
+      cudaFuncSetAttribute(linv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kLinvSmem);
+      la = true;
+    }
+  }
   for (int k = 0; k < n; k += NB) {
     const int jb = min(NB, n - k);
     panel_kernel<<<batch, PT, 0, stream>>>(pencils, n, ld, pencil_stride, k, jb, ipiv, minpiv, info);
@@ -245,9 +304,18 @@ CIRR_API int cirr_zgetrf_batched(cplx* pencils, int n, long long ld, long long p
     }
     const int rest = n - k - jb;
     if (rest > 0) {
-      dim3 g2((rest + TC - 1) / TC, batch);
-      trsm_kernel<<<g2, 256, kTrsmSmem, stream>>>(pencils, n, ld, pencil_stride, k, jb);
-      CIRR_CHECK_LAUNCH();
+      if (use_linv && jb == NB) {
+        // U12 = L11^{-1} A12 as a TMA/DMMA GEMM (each output tile reads exactly
+        // the A12 tile it overwrites, so in place is safe)
+        linv_kernel<<<batch, 256, kLinvSmem, stream>>>(pencils, ld, pencil_stride, k, linv);
+        CIRR_CHECK_LAUNCH();
+        CIRR_TRY(cirr::zgemm_sub_maps(mapL, maps.b, maps.c, NB, rest, NB, batch, 0, 0, k, k + jb, k, k + jb, pencils,
+                                      ld, pencil_stride, stream, /*beta=*/0));
+      } else {
+        dim3 g2((rest + TC - 1) / TC, batch);
+        trsm_kernel<<<g2, 256, kTrsmSmem, stream>>>(pencils, n, ld, pencil_stride, k, jb);
+        CIRR_CHECK_LAUNCH();
+      }
       if (jb % cirr::PBK == 0 && use_tma) {
         CIRR_TRY(cirr::lu_update_tma(maps, pencils, n, ld, pencil_stride, batch, k, jb, stream));
       } else {

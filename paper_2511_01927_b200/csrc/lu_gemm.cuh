@@ -64,6 +64,7 @@ struct SubGemmGeom {
   int c_row0, c_col0;   // A22 origin
   cplx* C; long long ldc, sC;
   int tiles_m, tiles_n;
+  int beta;        // 1: C = C - A B (C tile streamed in by TMA); 0: C = A B
 };
 
 static __global__ void __launch_bounds__(PTHREADS, 1) zgemm_sub_tma(const __grid_constant__ CUtensorMap mapA,
@@ -113,10 +114,12 @@ static __global__ void __launch_bounds__(PTHREADS, 1) zgemm_sub_tma(const __grid
         }
         // C block of this tile: requested once the consumers released the
         // previous tile's C, i.e. while this tile's main loop runs
-        mbar_wait(cempty, cphase ^ 1);
-        mbar_arrive_expect_tx(cfull, P_C_BYTES);
-        tma_load3(psm + PSTAGES * P_STAGE_BYTES, &mapC, 2 * (g.c_col0 + n0), g.c_row0 + m0, b, cfull);
-        cphase ^= 1;
+        if (g.beta) {
+          mbar_wait(cempty, cphase ^ 1);
+          mbar_arrive_expect_tx(cfull, P_C_BYTES);
+          tma_load3(psm + PSTAGES * P_STAGE_BYTES, &mapC, 2 * (g.c_col0 + n0), g.c_row0 + m0, b, cfull);
+          cphase ^= 1;
+        }
       }
     }
   } else {
@@ -162,9 +165,11 @@ static __global__ void __launch_bounds__(PTHREADS, 1) zgemm_sub_tma(const __grid
         if (lane == 0) mbar_arrive(empty + stage);
         if (++stage == PSTAGES) { stage = 0; phase ^= 1; }
       }
-      // epilogue: C - acc, straight to global
-      mbar_wait(cfull, cphase);
-      cphase ^= 1;
+      // epilogue: C - acc (or +acc when beta == 0), straight to global
+      if (g.beta) {
+        mbar_wait(cfull, cphase);
+        cphase ^= 1;
+      }
       cplx* Cb = g.C + (long long)b * g.sC;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
@@ -178,16 +183,22 @@ static __global__ void __launch_bounds__(PTHREADS, 1) zgemm_sub_tma(const __grid
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               if (c + h < g.N) {
-                const cplx v = Cs[rl * PBN + cl + h];
-                Cb[(long long)(g.c_row0 + r) * g.ldc + g.c_col0 + c + h] =
-                    cmk(v.x - (arr[i][j][h] - aii[i][j][h]), v.y - (ari[i][j][h] + air[i][j][h]));
+                const double pr = arr[i][j][h] - aii[i][j][h], pi = ari[i][j][h] + air[i][j][h];
+                cplx outv;
+                if (g.beta) {
+                  const cplx v = Cs[rl * PBN + cl + h];
+                  outv = cmk(v.x - pr, v.y - pi);
+                } else {
+                  outv = cmk(pr, pi);
+                }
+                Cb[(long long)(g.c_row0 + r) * g.ldc + g.c_col0 + c + h] = outv;
               }
             }
           }
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(cempty);
+      if (g.beta && lane == 0) mbar_arrive(cempty);
     }
   }
 }
@@ -230,13 +241,13 @@ static inline int encode_pencil_maps(PencilMaps& pm, cplx* base, int n, long lon
   return 0;
 }
 
-// C[b] -= A[b] @ B[b] on sub-blocks addressed through TMA maps (A: mapA with
+// C[b] -= A[b] @ B[b] (beta = 1) or C[b] = A[b] @ B[b] (beta = 0) on sub-blocks addressed through TMA maps (A: mapA with
 // origin (a_row0, a_col0), etc.); C is also written through (C, ldc, sC).
 // K is rounded up to a multiple of 16: the extra slice must lie outside the
 // tensors (zero-filled) or hold zeros.
 static inline int zgemm_sub_maps(const CUtensorMap& mapA, const CUtensorMap& mapB, const CUtensorMap& mapC, int M, int N,
                           int K, int batch, int a_row0, int a_col0, int b_row0, int b_col0, int c_row0, int c_col0,
-                          cplx* C, long long ldc, long long sC, cudaStream_t stream) {
+                          cplx* C, long long ldc, long long sC, cudaStream_t stream, int beta = 1) {
   if (M <= 0 || N <= 0 || K <= 0 || batch <= 0) return 0;
   static bool attr = false;
   static int sms = 0;
@@ -249,7 +260,7 @@ static inline int zgemm_sub_maps(const CUtensorMap& mapA, const CUtensorMap& map
   }
   const int Kr = (K + PBK - 1) / PBK * PBK;
   SubGemmGeom g{M, N, Kr, batch, a_row0, a_col0, b_row0, b_col0, c_row0, c_col0, C, ldc, sC,
-                (M + PBM - 1) / PBM, (N + PBN - 1) / PBN};
+                (M + PBM - 1) / PBM, (N + PBN - 1) / PBN, beta};
   const long long tiles = (long long)g.tiles_m * g.tiles_n * batch;
   const int grid = (int)(tiles < sms ? tiles : sms);
   zgemm_sub_tma<<<grid, PTHREADS, P_SMEM, stream>>>(mapA, mapB, mapC, g);

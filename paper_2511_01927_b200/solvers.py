@@ -377,8 +377,9 @@ class _Engine:
                       _ptr(self.pencils), n, n * n, _ptr(self.maxabs), self.stream)
         _work("assemble_bytes", P * n * n * 16 + 2 * n * n * 8)
         with _stage("lu"):
+            lws = torch.empty(int(_lib.call("cirr_zgetrf_ws_bytes", n, P)), dtype=torch.uint8, device="cuda")
             _lib.call("cirr_zgetrf_batched", _ptr(self.pencils), n, n, n * n, P, _ptr(self.ipiv),
-                      _ptr(self.perm), _ptr(self.minpiv), _ptr(self.info), self.stream)
+                      _ptr(self.perm), _ptr(self.minpiv), _ptr(self.info), _ptr(lws), self.stream)
         _work("lu_flops", P * 8.0 * n ** 3 / 3.0)
         maxabs = self.maxabs.cpu().numpy()
         minpiv = self.minpiv.cpu().numpy()
@@ -494,8 +495,9 @@ class _Engine:
         Qt = torch.zeros((nb, cmax, n), dtype=torch.complex128, device="cuda")
         ws = torch.empty(int(_lib.call("cirr_orth_ws_bytes", cmax, nb)), dtype=torch.uint8, device="cuda")
         sweeps = torch.zeros(1, dtype=torch.int32, device="cuda")
-        _lib.call("cirr_orth", _ptr(W), n, cmax * n, n, cmax, nb, float(cfg.rank_rel_tol), _ptr(sigma),
-                  _ptr(order), _ptr(kept), _ptr(Qt), n, cmax * n, _ptr(ws), _ptr(sweeps), st)
+        with _stage("rr.orth"):
+            _lib.call("cirr_orth", _ptr(W), n, cmax * n, n, cmax, nb, float(cfg.rank_rel_tol), _ptr(sigma),
+                      _ptr(order), _ptr(kept), _ptr(Qt), n, cmax * n, _ptr(ws), _ptr(sweeps), st)
         ks = kept.cpu().numpy()
         if _DEBUG:
             print(f"[cirr] orth: c={cmax} nprob={nb} kept={ks.tolist()} sweeps={int(sweeps.item())}", flush=True)
@@ -514,38 +516,40 @@ class _Engine:
         kmax = int(ks.max())
         Qt = Qt[:, :kmax].contiguous()  # rows beyond k_b are zero
         # K5: projected pencil  A~ = Q^H A Q, B~ = Q^H B Q
-        Q = torch.empty((nb, n, kmax), dtype=torch.complex128, device="cuda")
-        _lib.call("cirr_transpose", 0, _ptr(Qt), n, kmax * n, kmax, n, nb, _ptr(Q), kmax, n * kmax, st)
-        AQ = torch.empty((nb, n, kmax), dtype=torch.complex128, device="cuda")
-        BQ = torch.empty_like(AQ)
-        _lib.call("cirr_gemm", 2, n, kmax, n, nb, _ptr(self.dp.a), n, 0, _ptr(Q), kmax, n * kmax, _ptr(AQ), kmax,
-                  n * kmax, 1.0, 0, st)
-        _lib.call("cirr_gemm", 2, n, kmax, n, nb, _ptr(self.dp.b), n, 0, _ptr(Q), kmax, n * kmax, _ptr(BQ), kmax,
-                  n * kmax, 1.0, 0, st)
-        At = torch.empty((nb, kmax, kmax), dtype=torch.complex128, device="cuda")
-        Bt = torch.empty_like(At)
-        kk = kmax * kmax
-        _lib.call("cirr_gemm", 1, kmax, kmax, n, nb, _ptr(Qt), n, kmax * n, _ptr(AQ), kmax, n * kmax, _ptr(At), kmax,
-                  kk, 1.0, 0, st)
-        _lib.call("cirr_gemm", 1, kmax, kmax, n, nb, _ptr(Qt), n, kmax * n, _ptr(BQ), kmax, n * kmax, _ptr(Bt), kmax,
-                  kk, 1.0, 0, st)
+        with _stage("rr.project"):
+            Q = torch.empty((nb, n, kmax), dtype=torch.complex128, device="cuda")
+            _lib.call("cirr_transpose", 0, _ptr(Qt), n, kmax * n, kmax, n, nb, _ptr(Q), kmax, n * kmax, st)
+            AQ = torch.empty((nb, n, kmax), dtype=torch.complex128, device="cuda")
+            BQ = torch.empty_like(AQ)
+            _lib.call("cirr_gemm", 2, n, kmax, n, nb, _ptr(self.dp.a), n, 0, _ptr(Q), kmax, n * kmax, _ptr(AQ), kmax,
+                      n * kmax, 1.0, 0, st)
+            _lib.call("cirr_gemm", 2, n, kmax, n, nb, _ptr(self.dp.b), n, 0, _ptr(Q), kmax, n * kmax, _ptr(BQ), kmax,
+                      n * kmax, 1.0, 0, st)
+            At = torch.empty((nb, kmax, kmax), dtype=torch.complex128, device="cuda")
+            Bt = torch.empty_like(At)
+            kk = kmax * kmax
+            _lib.call("cirr_gemm", 1, kmax, kmax, n, nb, _ptr(Qt), n, kmax * n, _ptr(AQ), kmax, n * kmax, _ptr(At), kmax,
+                      kk, 1.0, 0, st)
+            _lib.call("cirr_gemm", 1, kmax, kmax, n, nb, _ptr(Qt), n, kmax * n, _ptr(BQ), kmax, n * kmax, _ptr(Bt), kmax,
+                      kk, 1.0, 0, st)
         # K6: small eigenproblems
         herm = self.dp.hermitian
         kdim = torch.from_numpy(ks.astype(np.int32)).to("cuda")
         info = torch.zeros(nb, dtype=torch.int32, device="cuda")
         lam = torch.zeros((nb, kmax), dtype=torch.complex128, device="cuda")
-        general_split = (not herm) and kmax <= 256
-        if general_split:
-            # eigenvalues first; eigenvectors later only for the inside ones
-            gws = torch.empty(int(_lib.call("cirr_gen_eig_ws_bytes", kmax, nb)), dtype=torch.uint8, device="cuda")
-            _lib.call("cirr_gen_eig_values", _ptr(At), _ptr(Bt), _ptr(kdim), kmax, nb, _ptr(gws), _ptr(lam),
-                      _ptr(info), st)
-        else:
-            wsb = int(_lib.call("cirr_small_eig_ws_bytes", kmax))
-            ews = torch.empty(nb * ((wsb + 255) // 256 * 256), dtype=torch.uint8, device="cuda")
-            Sv = torch.zeros((nb, kmax, kmax), dtype=torch.complex128, device="cuda")
-            _lib.call("cirr_small_eig", 1 if herm else 0, _ptr(At), _ptr(Bt), kmax, kk, _ptr(kdim), kmax, nb,
-                      _ptr(ews), _ptr(lam), _ptr(Sv), kmax, kk, _ptr(info), st)
+        with _stage("rr.eigvals"):
+            general_split = (not herm) and kmax <= 256
+            if general_split:
+                # eigenvalues first; eigenvectors later only for the inside ones
+                gws = torch.empty(int(_lib.call("cirr_gen_eig_ws_bytes", kmax, nb)), dtype=torch.uint8, device="cuda")
+                _lib.call("cirr_gen_eig_values", _ptr(At), _ptr(Bt), _ptr(kdim), kmax, nb, _ptr(gws), _ptr(lam),
+                          _ptr(info), st)
+            else:
+                wsb = int(_lib.call("cirr_small_eig_ws_bytes", kmax))
+                ews = torch.empty(nb * ((wsb + 255) // 256 * 256), dtype=torch.uint8, device="cuda")
+                Sv = torch.zeros((nb, kmax, kmax), dtype=torch.complex128, device="cuda")
+                _lib.call("cirr_small_eig", 1 if herm else 0, _ptr(At), _ptr(Bt), kmax, kk, _ptr(kdim), kmax, nb,
+                          _ptr(ews), _ptr(lam), _ptr(Sv), kmax, kk, _ptr(info), st)
         infos = info.cpu().numpy()
         lam_h = lam.cpu().numpy()
         keep_idx = {}

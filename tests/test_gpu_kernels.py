@@ -20,6 +20,11 @@ def P(t):
     return t.data_ptr()
 
 
+def ws_lu(n, batch):
+    from paper_2511_01927_b200 import _lib
+    return cuda(np.zeros(_lib.call("cirr_zgetrf_ws_bytes", n, batch), dtype=np.uint8))
+
+
 def S():
     return torch.cuda.current_stream().cuda_stream
 
@@ -83,7 +88,7 @@ def test_getrf_getrs(lib, n, batch):
     perm = torch.empty((batch, n), dtype=torch.int32, device="cuda")
     mp = torch.empty(batch, dtype=torch.float64, device="cuda")
     info = torch.empty(batch, dtype=torch.int32, device="cuda")
-    lib.call("cirr_zgetrf_batched", P(F), n, n, n * n, batch, P(ipiv), P(perm), P(mp), P(info), S())
+    lib.call("cirr_zgetrf_batched", P(F), n, n, n * n, batch, P(ipiv), P(perm), P(mp), P(info), P(ws_lu(n, batch)), S())
     assert (info.cpu().numpy() == 0).all()
     K = 37
     R = rng.standard_normal((2, n, K)) + 1j * rng.standard_normal((2, n, K))
@@ -111,7 +116,7 @@ def test_getrf_singular(lib):
     ipiv = torch.empty((1, n), dtype=torch.int32, device="cuda")
     mp = torch.empty(1, dtype=torch.float64, device="cuda")
     info = torch.empty(1, dtype=torch.int32, device="cuda")
-    lib.call("cirr_zgetrf_batched", P(F), n, n, n * n, 1, P(ipiv), 0, P(mp), P(info), S())
+    lib.call("cirr_zgetrf_batched", P(F), n, n, n * n, 1, P(ipiv), 0, P(mp), P(info), P(ws_lu(n, 1)), S())
     assert info.item() == 6 and mp.item() == 0.0
 
 

@@ -26,6 +26,7 @@ def main(n=4096, P=128, reps=3, K=32):
     rhs_of = torch.zeros(P, dtype=torch.int32, device="cuda")
     Y = torch.empty((P, n, K), dtype=torch.complex128, device="cuda")
     st = torch.cuda.current_stream().cuda_stream
+    lws = torch.empty(_lib.call("cirr_zgetrf_ws_bytes", n, P), dtype=torch.uint8, device="cuda")
     e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     for r in range(reps):
         e[0].record()
@@ -33,7 +34,7 @@ def main(n=4096, P=128, reps=3, K=32):
                   mx.data_ptr(), st)
         e[1].record()
         _lib.call("cirr_zgetrf_batched", pen.data_ptr(), n, n, n * n, P, ipiv.data_ptr(), perm.data_ptr(),
-                  mp.data_ptr(), info.data_ptr(), st)
+                  mp.data_ptr(), info.data_ptr(), lws.data_ptr(), st)
         e[2].record()
         _lib.call("cirr_zgetrs_batched", pen.data_ptr(), n, n, n * n, P, perm.data_ptr(), R.data_ptr(), K, n * K,
                   rhs_of.data_ptr(), K, Y.data_ptr(), K, n * K, st)
