@@ -17,7 +17,7 @@ exceed L2 (126 MB), so no L2 flush is needed between steps.
 
 `--impl reference` times the CPU oracle (oracle/cirr.py, the restated
 reference path with LAPACK dense LU) on the host cores: a bounded sample of the
-same GEP (2 of the 128 pencils: assembly + LU + every solve pass; one
+same GEP (6 of the 128 pencils: assembly + LU + every solve pass; one
 Rayleigh-Ritz round), extrapolated to one GEP.
 """
 
@@ -124,7 +124,7 @@ class ClockSampler:
 # CPU baseline (oracle) -- bounded sample of one GEP
 
 
-def cpu_sample(wl, refine_cols=None, passes=None, sample_pencils=2):
+def cpu_sample(wl, refine_cols=None, passes=None, sample_pencils=6):
     """Time the oracle's per-pencil work (assembly, LAPACK LU, every solve pass)
     on `sample_pencils` pencils and one Rayleigh-Ritz round; extrapolate to
     one GEP.  Returns (seconds_per_gep, description)."""
