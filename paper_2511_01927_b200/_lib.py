@@ -35,6 +35,7 @@ SIGNATURES = {
     "cirr_small_eig_ws_bytes": [_I],
     "cirr_small_eig": [_I, _P, _P, _L, _L, _P, _I, _I, _P, _P, _P, _L, _L, _P, _P],
     "cirr_small_eig_phases": [_P],
+    "cirr_gen_eig_qr_stats": [_P],
     "cirr_gen_eig_ws_bytes": [_I, _I],
     "cirr_gen_eig_vec_scratch_bytes": [_I, _I, _I],
     "cirr_gen_eig_values": [_P, _P, _P, _I, _I, _P, _P, _P, _P],

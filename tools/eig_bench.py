@@ -65,9 +65,37 @@ def t_orth(n, c, nprob=2, reps=2):
     print(f"orth n={n} c={c} nprob={nprob}: {e0.elapsed_time(e1):.2f} ms sweeps={sw.item()} kept={kept.cpu().numpy()}", flush=True)
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and len(sys.argv) == 1:
     for k in (120, 256):
         t_small(k, False)
         t_small(k, True)
     t_orth(4096, 256)
     t_orth(4096, 120)
+
+
+def t_gen_split(k, nprob=2, reps=2):
+    import ctypes
+    rng = np.random.default_rng(k + 7)
+    A = rng.standard_normal((nprob, k, k)) + 1j * rng.standard_normal((nprob, k, k))
+    B = np.eye(k) + 0.05 * (rng.standard_normal((nprob, k, k)) + 1j * rng.standard_normal((nprob, k, k)))
+    At, Bt = torch.from_numpy(A).cuda(), torch.from_numpy(np.ascontiguousarray(B)).cuda()
+    kd = torch.full((nprob,), k, dtype=torch.int32, device="cuda")
+    ws = torch.empty(_lib.call("cirr_gen_eig_ws_bytes", k, nprob), dtype=torch.uint8, device="cuda")
+    lam = torch.empty((nprob, k), dtype=torch.complex128, device="cuda")
+    info = torch.zeros(nprob, dtype=torch.int32, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(reps):
+        e0.record()
+        _lib.call("cirr_gen_eig_values", At.data_ptr(), Bt.data_ptr(), kd.data_ptr(), k, nprob, ws.data_ptr(),
+                  lam.data_ptr(), info.data_ptr(), st)
+        e1.record(); torch.cuda.synchronize()
+    q = (ctypes.c_longlong * 8)()
+    _lib.call("cirr_gen_eig_qr_stats", ctypes.addressof(q))
+    print(f"gen_eig_values k={k} nprob={nprob}: {e0.elapsed_time(e1):.2f} ms  sweeps {q[0]} rot {q[1]} "
+          f"defl {q[2]/1e6:.1f}M chain {q[3]/1e6:.1f}M far {q[4]/1e6:.1f}M cycles", flush=True)
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "split":
+    for k in (120, 256):
+        t_gen_split(k)
