@@ -73,6 +73,11 @@ int cirr_orth(cirr_cplx* W, long long ldw, long long wstride, int n, int c, int 
               double rel_tol, double* sigma, int* order, int* kept, cirr_cplx* Qt,
               long long ldq, long long qstride, void* ws, int* sweeps_out, cudaStream_t stream);
 
+/* FEAST basis -- replaces linalg.py:79-104 (orthonormalize, MGS x2 with drop_tol):
+ * CGS2 per problem on the rows of Y (c x n); Qt[p] gets kept[p] orthonormal rows. */
+int cirr_orthonormalize(const cirr_cplx* Y, long long ldy, long long sy, int n, int c, int nprob, double drop_tol,
+                        cirr_cplx* Qt, long long ldq, long long sq, int* kept, cudaStream_t stream);
+
 /* K5/K7 GEMM -- replaces sparse.py:98-103 (sparse_matmat for B V, A Q, B Q,
  * A X, B X) and the dense products of solvers.py:153-158.
  * C = beta*C + alpha*op(A)@B; a_kind 0: A complex, 1: conj(A), 2: A real f64. */

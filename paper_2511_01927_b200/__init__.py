@@ -28,6 +28,7 @@ from .solvers import (  # noqa: F401
     SolveStats,
     apply_projector,
     cirr_solve,
+    feast_solve,
     read_eigenvectors,
     solve_multi,
     write_eigenvectors,

@@ -294,3 +294,78 @@ CIRR_API int cirr_orth(cplx* W, long long ldw, long long wstride, int n, int c, 
   if (e != cudaSuccess) return (int)e;
   return 0;
 }
+
+// --------------------------------------------------------------------------
+// FEAST basis: Gram-Schmidt with re-orthogonalisation and column dropping.
+//
+// Replaces linalg.py:79-104 (orthonormalize: two MGS passes per column, drop a
+// column whose norm falls below drop_tol * its original norm).  Classical
+// Gram-Schmidt applied twice (CGS2) gives the same result to rounding and turns
+// each pass into two parallel products; one CTA per problem, rows of length n
+// (the columns of the block), fixed-order reductions.
+namespace {
+constexpr int GT2 = 512;
+__global__ void __launch_bounds__(GT2) cgs2_kernel(const cplx* __restrict__ Y, long long ldy, long long sy, int n,
+                                                   int c, double drop_tol, cplx* __restrict__ Qt, long long ldq,
+                                                   long long sq, int* __restrict__ kept_out) {
+  extern __shared__ cplx coef[];
+  __shared__ double red[32];
+  const int p = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = GT2 / 32;
+  const cplx* Yp = Y + (long long)p * sy;
+  cplx* Q = Qt + (long long)p * sq;
+  int kept = 0;
+  for (int j = 0; j < c; ++j) {
+    cplx* v = Q + (long long)kept * ldq;  // work in the next free output row
+    double o2 = 0.0;
+    for (int e = tid; e < n; e += GT2) {
+      const cplx y = Yp[(long long)j * ldy + e];
+      v[e] = y;
+      o2 += cabs2(y);
+    }
+    const double orig = sqrt(block_sum(o2, red));
+    if (orig == 0.0) continue;
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int i = wid; i < kept; i += nw) {
+        const cplx* q = Q + (long long)i * ldq;
+        double sr = 0.0, si = 0.0;
+        for (int e = lane; e < n; e += 32) {
+          const cplx g = cconjmul(q[e], v[e]);
+          sr += g.x;
+          si += g.y;
+        }
+        sr = warp_sum(sr);
+        si = warp_sum(si);
+        if (lane == 0) coef[i] = cmk(sr, si);
+      }
+      __syncthreads();
+      for (int e = tid; e < n; e += GT2) {
+        cplx x = v[e];
+        for (int i = 0; i < kept; ++i) cfms(x, coef[i], Q[(long long)i * ldq + e]);
+        v[e] = x;
+      }
+      __syncthreads();
+    }
+    double n2 = 0.0;
+    for (int e = tid; e < n; e += GT2) n2 += cabs2(v[e]);
+    const double nrm = sqrt(block_sum(n2, red));
+    if (nrm <= drop_tol * orig) continue;
+    const double inv = 1.0 / nrm;
+    for (int e = tid; e < n; e += GT2) v[e] = cscale(v[e], inv);
+    __syncthreads();
+    ++kept;
+  }
+  if (tid == 0) kept_out[p] = kept;
+}
+}  // namespace
+
+// Orthonormal basis of each block (rows of Y = columns of the block, c x n),
+// dropping columns below drop_tol relative norm; Qt[p] rows 0..kept[p]-1.
+CIRR_API int cirr_orthonormalize(const cplx* Y, long long ldy, long long sy, int n, int c, int nprob, double drop_tol,
+                                 cplx* Qt, long long ldq, long long sq, int* kept, cudaStream_t stream) {
+  if (n <= 0 || c <= 0 || nprob <= 0 || c > 4096) return CIRR_EINVAL;
+  const size_t smem = sizeof(cplx) * (size_t)c;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(cgs2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cgs2_kernel<<<nprob, GT2, smem, stream>>>(Y, ldy, sy, n, c, drop_tol, Qt, ldq, sq, kept);
+  CIRR_CHECK_LAUNCH();
+  return 0;
+}

@@ -17,7 +17,7 @@ Patch points:
 Results come back as the reference's own ``EigenResult`` / ``SolveStats`` /
 ``MultiResult`` objects and errors as the reference's own exception classes,
 so reference code that catches ``cieig.errors.*`` keeps working.  FEAST
-(``solver="feast"``) is forwarded to the original reference implementation.
+(``solver="feast"``) runs on the same device path.
 """
 
 from __future__ import annotations
@@ -63,12 +63,19 @@ def gpu_cirr_solve_for(cieig):
     return cirr_solve
 
 
-def gpu_solve_multi_for(cieig):
-    orig = _ORIG.get("solvers.solve_multi", cieig.solvers.solve_multi)
+def gpu_feast_solve_for(cieig):
+    def feast_solve(pencil, contour, cfg=None, seed: int = 0):
+        try:
+            return _to_ref_result(cieig, S.feast_solve(pencil, contour, cfg, seed=seed))
+        except E.CieigError as exc:
+            raise _to_ref_error(cieig, exc) from exc
 
+    feast_solve.__doc__ = "B200 FEAST behind the reference signature (solvers.py:230)."
+    return feast_solve
+
+
+def gpu_solve_multi_for(cieig):
     def solve_multi(pencil, contours, cfg=None, solver: str = "cirr", seed: int = 0):
-        if solver == "feast":
-            return orig(pencil, contours, cfg, solver=solver, seed=seed)
         try:
             m = S.solve_multi(pencil, contours, cfg, solver=solver, seed=seed)
         except E.CieigError as exc:
@@ -93,11 +100,13 @@ def install(cieig) -> None:
     if _ORIG:
         return
     _ORIG["solvers.cirr_solve"] = cieig.solvers.cirr_solve
+    _ORIG["solvers.feast_solve"] = cieig.solvers.feast_solve
     _ORIG["solvers.solve_multi"] = cieig.solvers.solve_multi
     _ORIG["bench.solve_multi"] = cieig.bench.solve_multi
     _ORIG["cli.solve_multi"] = cieig.cli.solve_multi
     sm = gpu_solve_multi_for(cieig)
     cieig.solvers.cirr_solve = gpu_cirr_solve_for(cieig)
+    cieig.solvers.feast_solve = gpu_feast_solve_for(cieig)
     cieig.solvers.solve_multi = sm
     cieig.bench.solve_multi = sm
     cieig.cli.solve_multi = sm
@@ -107,6 +116,7 @@ def uninstall(cieig) -> None:
     if not _ORIG:
         return
     cieig.solvers.cirr_solve = _ORIG.pop("solvers.cirr_solve")
+    cieig.solvers.feast_solve = _ORIG.pop("solvers.feast_solve")
     cieig.solvers.solve_multi = _ORIG.pop("solvers.solve_multi")
     cieig.bench.solve_multi = _ORIG.pop("bench.solve_multi")
     cieig.cli.solve_multi = _ORIG.pop("cli.solve_multi")

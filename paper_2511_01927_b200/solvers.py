@@ -465,18 +465,63 @@ class _Engine:
         return out
 
     # -- K4..K7 for one contour --------------------------------------------
-    def rayleigh_ritz(self, items: list) -> dict:
+    def rayleigh_ritz(self, items: list, feast: bool = False) -> dict:
         """K4..K7 for several contours at once (solvers.py:187-198, batched).
 
-        items: [(ci, St)] with St the transposed stacked block of contour ci.
-        Returns {ci: ("ok", lam_in, x_in_dev, res_in) | ("none",) |
-        ("rankzero",) | ("indefinite", exc)}."""
+        items: [(ci, St)] with St the transposed block of contour ci (its columns
+        as rows).  CIRR: rank-truncated SVD basis (linalg.py:107-119); FEAST:
+        Gram-Schmidt basis with drop_tol (linalg.py:79-104) and every Ritz vector
+        returned (solvers.py:253).  Returns {ci: ("ok", lam_in, x_in_dev,
+        res_in, x_all_or_None) | ("none", x_all_or_None) | ("rankzero",) |
+        ("indefinite", exc)}."""
         with _stage("rr"):
-            return self._rayleigh_ritz(items)
+            out = {}
+            if feast:
+                basis = self._basis_cgs2(items, out)
+            else:
+                basis = self._basis_svd(items, out)
+            if basis is None:
+                return out
+            items, Qt, ks = basis
+            return self._rr_core(items, Qt, ks, out, all_vectors=feast)
 
-    def _rayleigh_ritz(self, items: list) -> dict:
+    def _basis_cgs2(self, items: list, out: dict):
         torch, n, cfg, st = self.torch, self.n, self.cfg, self.stream
-        out = {}
+        for ci, S_ in items:
+            if S_.shape[0] == 0:
+                out[ci] = ("rankzero",)
+        items = [(ci, S_) for ci, S_ in items if S_.shape[0] > 0]
+        if not items:
+            return None
+        nb = len(items)
+        cmax = max(S_.shape[0] for _, S_ in items)
+        Y = torch.zeros((nb, cmax, n), dtype=torch.complex128, device="cuda")
+        for b, (_, S_) in enumerate(items):
+            Y[b, : S_.shape[0]].copy_(S_)
+        Qt = torch.zeros((nb, cmax, n), dtype=torch.complex128, device="cuda")
+        kept = torch.zeros(nb, dtype=torch.int32, device="cuda")
+        _lib.call("cirr_orthonormalize", _ptr(Y), n, cmax * n, n, cmax, nb, float(cfg.drop_tol), _ptr(Qt), n,
+                  cmax * n, _ptr(kept), st)
+        return self._live(items, Qt, kept.cpu().numpy(), out)
+
+    def _live(self, items, Qt, ks, out):
+        nb = len(items)
+        live = [b for b in range(nb) if ks[b] > 0]
+        for b in range(nb):
+            if ks[b] == 0:
+                out[items[b][0]] = ("rankzero",)
+        if not live:
+            return None
+        if len(live) < nb:
+            sel = self.torch.tensor(live, dtype=self.torch.long, device="cuda")
+            Qt = Qt.index_select(0, sel)
+            ks = ks[live]
+            items = [items[b] for b in live]
+        kmax = int(ks.max())
+        return items, Qt[:, :kmax].contiguous(), ks
+
+    def _basis_svd(self, items: list, out: dict):
+        torch, n, cfg, st = self.torch, self.n, self.cfg, self.stream
         for ci, S_ in items:
             if S_.shape[0] == 0:
                 out[ci] = ("rankzero",)
@@ -501,20 +546,12 @@ class _Engine:
         ks = kept.cpu().numpy()
         if _DEBUG:
             print(f"[cirr] orth: c={cmax} nprob={nb} kept={ks.tolist()} sweeps={int(sweeps.item())}", flush=True)
-        live = [b for b in range(nb) if ks[b] > 0]
-        for b in range(nb):
-            if ks[b] == 0:
-                out[items[b][0]] = ("rankzero",)
-        if not live:
-            return out
-        if len(live) < nb:
-            sel = torch.tensor(live, dtype=torch.long, device="cuda")
-            Qt = Qt.index_select(0, sel)
-            ks = ks[live]
-            items = [items[b] for b in live]
-            nb = len(live)
+        return self._live(items, Qt, ks, out)
+
+    def _rr_core(self, items, Qt, ks, out, all_vectors: bool):
+        torch, n, cfg, st = self.torch, self.n, self.cfg, self.stream
+        nb = len(items)
         kmax = int(ks.max())
-        Qt = Qt[:, :kmax].contiguous()  # rows beyond k_b are zero
         # K5: projected pencil  A~ = Q^H A Q, B~ = Q^H B Q
         with _stage("rr.project"):
             Q = torch.empty((nb, n, kmax), dtype=torch.complex128, device="cuda")
@@ -538,7 +575,7 @@ class _Engine:
         info = torch.zeros(nb, dtype=torch.int32, device="cuda")
         lam = torch.zeros((nb, kmax), dtype=torch.complex128, device="cuda")
         with _stage("rr.eigvals"):
-            general_split = (not herm) and kmax <= 256
+            general_split = (not herm) and kmax <= 256 and not all_vectors
             if general_split:
                 # eigenvalues first; eigenvectors later only for the inside ones
                 gws = torch.empty(int(_lib.call("cirr_gen_eig_ws_bytes", kmax, nb)), dtype=torch.uint8, device="cuda")
@@ -566,9 +603,17 @@ class _Engine:
             else:
                 keep = np.array([contains(self.cs[ci].contour, v) for v in lb], dtype=bool)
             if not np.any(keep):
-                out[ci] = ("none",)
+                out[ci] = ("none", None)
                 continue
             keep_idx[b] = np.nonzero(keep)[0]
+        X = None
+        if all_vectors:
+            X = torch.empty((nb, n, kmax), dtype=torch.complex128, device="cuda")
+            _lib.call("cirr_gemm", 0, n, kmax, kmax, nb, _ptr(Q), kmax, n * kmax, _ptr(Sv), kmax, kk, _ptr(X), kmax,
+                      n * kmax, 1.0, 0, st)
+            for b, (ci, _) in enumerate(items):
+                if ci in out and out[ci][0] == "none":
+                    out[ci] = ("none", X[b, :, : ks[b]].contiguous())
         if not keep_idx:
             return out
         # K7: X = Q s for the inside columns, A X, B X, residuals
@@ -592,9 +637,10 @@ class _Engine:
             _lib.call("cirr_gemm", 0, n, kin_max, kmax, nb, _ptr(Q), kmax, n * kmax, _ptr(Sin), kin_max,
                       kmax * kin_max, _ptr(Xi), kin_max, n * kin_max, 1.0, 0, st)
         else:
-            X = torch.empty((nb, n, kmax), dtype=torch.complex128, device="cuda")
-            _lib.call("cirr_gemm", 0, n, kmax, kmax, nb, _ptr(Q), kmax, n * kmax, _ptr(Sv), kmax, kk, _ptr(X), kmax,
-                      n * kmax, 1.0, 0, st)
+            if X is None:
+                X = torch.empty((nb, n, kmax), dtype=torch.complex128, device="cuda")
+                _lib.call("cirr_gemm", 0, n, kmax, kmax, nb, _ptr(Q), kmax, n * kmax, _ptr(Sv), kmax, kk, _ptr(X),
+                          kmax, n * kmax, 1.0, 0, st)
             _lib.call("cirr_gather_cols", _ptr(X), kmax, n * kmax, _ptr(idx_t), kin_max, _ptr(cnt_t), kin_max, n, nb,
                       _ptr(Xi), kin_max, n * kin_max, st)
         AX = torch.empty_like(Xi)
@@ -614,7 +660,8 @@ class _Engine:
             lam_b = lam_h[b, ix]
             if herm:
                 lam_b = lam_b.real.copy()
-            out[ci] = ("ok", lam_b, Xi[b, :, :k_in].contiguous(), res_h[b, :k_in].copy())
+            xall = X[b, :, : ks[b]].contiguous() if all_vectors else None
+            out[ci] = ("ok", lam_b, Xi[b, :, :k_in].contiguous(), res_h[b, :k_in].copy(), xall)
         return out
 
     # -- the reference control flow (solvers.py:165-227) for all contours ----
@@ -651,7 +698,7 @@ class _Engine:
                     c.lam = None
                     active.remove(ci)
                     continue
-                _, lam, xi, res = r
+                _, lam, xi, res, _ = r
                 c.lam, c.x_dev, c.res = lam, xi, res
                 c.best_res = min(c.best_res, float(res.max()))
                 if res.max() <= cfg.tol or it + 1 >= cfg.max_refine:
@@ -669,6 +716,58 @@ class _Engine:
             c.stats.elapsed = time.perf_counter() - c.t0
             if getattr(c, "fatal", False):
                 continue
+            self.finish(c)
+
+    # -- FEAST (solvers.py:230-285) on the same resident factors -------------
+    def run_feast(self):
+        torch, cfg, n = self.torch, self.cfg, self.n
+        active = [i for i, c in enumerate(self.cs) if not c.done]
+        u = {}
+        for ci in active:
+            c = self.cs[ci]
+            rng = np.random.default_rng(c.seed)
+            u[ci] = torch.from_numpy(rng.standard_normal((n, c.ncols)).astype(complex)).to("cuda")  # 238-240
+            c.found_any = False
+        it_of = {ci: 0 for ci in active}
+        for it in range(cfg.max_refine):
+            if not active:
+                break
+            for ci in active:
+                it_of[ci] = it
+            stacked = self.apply(active, {ci: self.bmul(u[ci]) for ci in active}, 1)  # y = P u (246)
+            rr = self.rayleigh_ritz([(ci, stacked[ci]) for ci in active], feast=True)
+            nxt = []
+            for ci in active:
+                c = self.cs[ci]
+                r = rr[ci]
+                if r[0] == "rankzero":  # 249-250
+                    continue
+                if r[0] == "indefinite":
+                    c.error, c.fatal = r[1], True
+                    continue
+                if r[0] == "none":  # 253-255: u = xs, keep iterating
+                    if r[1] is not None:
+                        u[ci] = r[1]
+                    nxt.append(ci)
+                    continue
+                _, lam, xi, res, xall = r
+                u[ci] = xall
+                c.found_any = True
+                c.lam, c.x_dev, c.res = lam, xi, res
+                c.best_res = min(c.best_res, float(res.max()))
+                if res.max() <= cfg.tol:  # 260-261
+                    continue
+                nxt.append(ci)
+            active = nxt
+        for ci, c in enumerate(self.cs):
+            if c.done:
+                continue
+            c.stats.iterations = it_of.get(ci, 0) + 1
+            c.stats.elapsed = time.perf_counter() - c.t0
+            if getattr(c, "fatal", False):
+                continue
+            if not getattr(c, "found_any", False):
+                c.lam = None
             self.finish(c)
 
     def finish(self, c: _Contour):
@@ -721,14 +820,17 @@ def _hbm_budget(n: int, cstates: list) -> int:
     return max(int(free - reserve), n * n * 16 * 64)
 
 
-def _run_contours(pencil, contours, cfg, seeds, moments_override=None):
+def _run_contours(pencil, contours, cfg, seeds, moments_override=None, solver: str = "cirr"):
     cfg = _cfg_view(cfg)
     dp = DevicePencil.of(pencil)
     cstates = [_Contour(i, c, cfg, s, dp.n) for i, (c, s) in enumerate(zip(contours, seeds))]
     for wave in _waves(cstates, dp.n, _hbm_budget(dp.n, cstates)):
         eng = _Engine(dp, wave, cfg)
         eng.factor()
-        eng.run(cfg.n_moments if moments_override is None else moments_override)
+        if solver == "feast":
+            eng.run_feast()
+        else:
+            eng.run(cfg.n_moments if moments_override is None else moments_override)
         eng.free()
         del eng
     return cstates
@@ -746,6 +848,15 @@ def cirr_solve(pencil, contour, cfg: SolverConfig | None = None, seed: int = 0) 
     return c.result
 
 
+def feast_solve(pencil, contour, cfg: SolverConfig | None = None, seed: int = 0) -> EigenResult:
+    """Filtered subspace iteration on the device factors (solvers.py:230-285):
+    U <- orthonormalize(P U), Rayleigh-Ritz after each projector application."""
+    c = _run_contours(pencil, [contour], cfg, [seed], solver="feast")[0]
+    if c.error is not None:
+        raise c.error
+    return c.result
+
+
 def solve_multi(pencil, contours, cfg: SolverConfig | None = None, solver: str = "cirr",
                 seed: int = 0) -> MultiResult:
     """Every contour solved in one batched device pass (solvers.py:312-339);
@@ -753,11 +864,9 @@ def solve_multi(pencil, contours, cfg: SolverConfig | None = None, solver: str =
     propagate, duplicates across contours keep the smaller residual."""
     if solver not in ("cirr", "feast"):
         raise ParameterError(f"unknown solver {solver!r}")
-    if solver == "feast":
-        raise NotImplementedError("FEAST on the device path is SURVEY 8(f) row 1 (next)")
     t0 = time.perf_counter()
     contours = list(contours)
-    cstates = _run_contours(pencil, contours, cfg, [seed + i for i in range(len(contours))])
+    cstates = _run_contours(pencil, contours, cfg, [seed + i for i in range(len(contours))], solver=solver)
     results, errors = [], []
     agg = SolveStats()
     for c in cstates:

@@ -84,3 +84,22 @@ def test_cli_solve_dropin(tmp_path):
     b = json.load(open(out_gpu))["eigenvalues"]
     assert len(a) == len(b) and np.allclose(a, b, rtol=1e-9)
     assert vec.stat().st_size > 16
+
+
+def test_feast_dropin(thermal):
+    pencil, truth = thermal
+    from cieig.contours import Contour
+    c = Contour(shape="circle", center=complex(0.5 * (truth.eigenvalues[0] + truth.eigenvalues[3])),
+                radius=0.5 * (truth.eigenvalues[4] - truth.eigenvalues[0]) + 1e-9 * truth.eigenvalues[4],
+                expected_count=4)
+    cfg = cieig.solvers.SolverConfig(tol=1e-9)
+    cpu = cieig.solvers.solve_multi(pencil, [c], cfg, solver="feast", seed=0)
+    patch.install(cieig)
+    try:
+        gpu = cieig.solvers.solve_multi(pencil, [c], cfg, solver="feast", seed=0)
+        r = cieig.solvers.feast_solve(pencil, c, cfg, seed=0)
+        assert isinstance(r, cieig.solvers.EigenResult)
+    finally:
+        patch.uninstall(cieig)
+    assert len(gpu.eigenvalues) == len(cpu.eigenvalues)
+    assert np.allclose(gpu.eigenvalues, cpu.eigenvalues, rtol=1e-8)
