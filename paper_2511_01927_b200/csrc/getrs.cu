@@ -165,6 +165,48 @@ __global__ void __launch_bounds__(256, 1) trsm_blocked_kernel(const cplx* __rest
   }
 }
 
+// Inverses of the 64x64 diagonal blocks of L (unit lower, slot 0) and U (slot 1)
+// of every pencil: Dinv[(b * nblk + bi) * 2 + slot] (64 x 64, zero outside nb x nb).
+template <bool LOWER>
+__global__ void __launch_bounds__(256) diag_inv_kernel(const cplx* __restrict__ LU, long long ld, long long pstride,
+                                                       int n, cplx* __restrict__ Dinv) {
+  extern __shared__ __align__(16) cplx ism[];
+  cplx* D = ism;
+  cplx* X = D + SNB * SD_LD;
+  cplx* dinv = X + SNB * SD_LD;
+  const int bi = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
+  const int nblk = gridDim.x;
+  const int i0 = bi * SNB, nb = min(SNB, n - i0);
+  const cplx* T = LU + (long long)b * pstride;
+  for (int e = tid; e < SNB * SNB; e += 256) {
+    const int r = e / SNB, c = e % SNB;
+    D[r * SD_LD + c] = (r < nb && c < nb) ? T[(long long)(i0 + r) * ld + i0 + c] : cmk(0.0, 0.0);
+    X[r * SD_LD + c] = cmk((r == c && r < nb) ? 1.0 : 0.0, 0.0);
+  }
+  __syncthreads();
+  if (!LOWER && tid < nb) dinv[tid] = crecip(D[tid * SD_LD + tid]);
+  __syncthreads();
+  const int c = tid % SNB, g = tid / SNB;  // 4 row groups, all 64 unit columns at once
+  if (LOWER) {
+    for (int i = 0; i < nb - 1; ++i) {
+      const cplx xi = X[i * SD_LD + c];
+      for (int r = i + 1 + g; r < nb; r += 4) cfms(X[r * SD_LD + c], D[r * SD_LD + i], xi);
+      __syncthreads();
+    }
+  } else {
+    for (int i = nb - 1; i >= 0; --i) {
+      const cplx xi = cmul(X[i * SD_LD + c], dinv[i]);
+      __syncthreads();
+      if (g == 0) X[i * SD_LD + c] = xi;
+      for (int r = g; r < i; r += 4) cfms(X[r * SD_LD + c], D[r * SD_LD + i], xi);
+      __syncthreads();
+    }
+  }
+  cplx* out = Dinv + (((long long)b * nblk + bi) * 2 + (LOWER ? 0 : 1)) * SNB * SNB;
+  for (int e = tid; e < SNB * SNB; e += 256) out[e] = X[(e / SNB) * SD_LD + e % SNB];
+}
+constexpr int kDiagInvSmem = (2 * SNB * SD_LD + SNB) * 16;
+
 // Y[j][i][c] = R[rhs_of[j]][perm[j][i]][c]
 __global__ void permute_kernel(const cplx* __restrict__ R, long long ldr, long long rstride,
                                const int* __restrict__ rhs_of, const int* __restrict__ perm, int n, int K,
@@ -264,10 +306,35 @@ __global__ void __launch_bounds__(256) diag_solve_kernel(const cplx* __restrict_
 // cirr_zgetrf_batched; R: (n_rhs_sets) x n x K, row-major, ld ldr, stride
 // rstride; Y: batch x n x K (ld ldy, stride ystride).  rhs_of is a device
 // int32 array.
+// Bytes of the diagonal-block inverses cirr_diag_inverses writes.
+CIRR_API long long cirr_diag_inv_bytes(int n, int batch) {
+  const long long nblk = (n + SNB - 1) / SNB;
+  return (long long)batch * nblk * 2 * SNB * SNB * 16;
+}
+
+// Inverses of the 64x64 diagonal blocks of every factor (once per factorisation,
+// reused by every solve pass).
+CIRR_API int cirr_diag_inverses(const cplx* LU, int n, long long ld, long long pencil_stride, int batch, cplx* Dinv,
+                                cudaStream_t stream) {
+  if (n <= 0 || batch <= 0) return CIRR_EINVAL;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(diag_inv_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDiagInvSmem);
+    cudaFuncSetAttribute(diag_inv_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDiagInvSmem);
+    attr = true;
+  }
+  dim3 g((n + SNB - 1) / SNB, batch);
+  diag_inv_kernel<true><<<g, 256, kDiagInvSmem, stream>>>(LU, ld, pencil_stride, n, Dinv);
+  CIRR_CHECK_LAUNCH();
+  diag_inv_kernel<false><<<g, 256, kDiagInvSmem, stream>>>(LU, ld, pencil_stride, n, Dinv);
+  CIRR_CHECK_LAUNCH();
+  return 0;
+}
+
 CIRR_API int cirr_zgetrs_batched(const cplx* LU, int n, long long ld, long long pencil_stride, int batch,
                                  const int* perm, const cplx* R, long long ldr, long long rstride,
                                  const int* rhs_of, int K, cplx* Y, long long ldy, long long ystride,
-                                 cudaStream_t stream) {
+                                 const cplx* Dinv, cudaStream_t stream) {
   if (n <= 0 || batch <= 0 || K < 0 || ldy < K || ldr < K) return CIRR_EINVAL;
   if (K == 0) return 0;
   static bool attr = false;
@@ -296,17 +363,31 @@ CIRR_API int cirr_zgetrs_batched(const cplx* LU, int n, long long ld, long long 
     }
     const int nblk = (n + SNB - 1) / SNB;
     dim3 gd((K + DSC - 1) / DSC, batch);
+    CUtensorMap mD;
+    const bool use_dinv = Dinv != nullptr &&
+                          cirr::encode_c128_map(&mD, Dinv, SNB, SNB, batch * nblk * 2, SNB, (long long)SNB * SNB,
+                                                cirr::PBK, cirr::PBM) == 0;
     for (int bi = 0; bi < nblk; ++bi) {  // forward: L (unit lower)
       const int i0 = bi * SNB, nb = min(SNB, n - i0);
-      diag_solve_kernel<true><<<gd, 256, kDiagSmem, stream>>>(LU, ld, pencil_stride, i0, nb, Y, ldy, ystride, K);
-      CIRR_CHECK_LAUNCH();
+      if (use_dinv) {  // Y_i <- L_ii^-1 Y_i on the GEMM (in place: each tile reads only its own rows)
+        CIRR_TRY(cirr::zgemm_sub_maps(mD, mY.b, mY.c, nb, K, nb, batch, 0, 0, i0, 0, i0, 0, Y, ldy, ystride, stream,
+                                      /*beta=*/0, nblk * 2, bi * 2));
+      } else {
+        diag_solve_kernel<true><<<gd, 256, kDiagSmem, stream>>>(LU, ld, pencil_stride, i0, nb, Y, ldy, ystride, K);
+        CIRR_CHECK_LAUNCH();
+      }
       CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, n - i0 - nb, K, nb, batch, i0 + nb, i0, i0, 0, i0 + nb, 0,
                                     Y, ldy, ystride, stream));
     }
     for (int bi = nblk - 1; bi >= 0; --bi) {  // backward: U
       const int i0 = bi * SNB, nb = min(SNB, n - i0);
-      diag_solve_kernel<false><<<gd, 256, kDiagSmem, stream>>>(LU, ld, pencil_stride, i0, nb, Y, ldy, ystride, K);
-      CIRR_CHECK_LAUNCH();
+      if (use_dinv) {
+        CIRR_TRY(cirr::zgemm_sub_maps(mD, mY.b, mY.c, nb, K, nb, batch, 0, 0, i0, 0, i0, 0, Y, ldy, ystride, stream,
+                                      /*beta=*/0, nblk * 2, bi * 2 + 1));
+      } else {
+        diag_solve_kernel<false><<<gd, 256, kDiagSmem, stream>>>(LU, ld, pencil_stride, i0, nb, Y, ldy, ystride, K);
+        CIRR_CHECK_LAUNCH();
+      }
       CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, i0, K, nb, batch, 0, i0, i0, 0, 0, 0, Y, ldy, ystride,
                                     stream));
     }

@@ -65,6 +65,7 @@ struct SubGemmGeom {
   cplx* C; long long ldc, sC;
   int tiles_m, tiles_n;
   int beta;        // 1: C = C - A B (C tile streamed in by TMA); 0: C = A B
+  int a_bmul, a_badd;  // 3rd TMA coordinate of the A operand: b * a_bmul + a_badd
 };
 
 static __global__ void __launch_bounds__(PTHREADS, 1) zgemm_sub_tma(const __grid_constant__ CUtensorMap mapA,
@@ -108,7 +109,7 @@ static __global__ void __launch_bounds__(PTHREADS, 1) zgemm_sub_tma(const __grid
           unsigned char* base = psm + stage * P_STAGE_BYTES;
           mbar_arrive_expect_tx(full + stage, P_STAGE_BYTES);
           const int k0 = ks * PBK;
-          tma_load3(base, &mapA, 2 * (g.a_col0 + k0), g.a_row0 + m0, b, full + stage);
+          tma_load3(base, &mapA, 2 * (g.a_col0 + k0), g.a_row0 + m0, b * g.a_bmul + g.a_badd, full + stage);
           tma_load3(base + P_A_BYTES, &mapB, 2 * (g.b_col0 + n0), g.b_row0 + k0, b, full + stage);
           if (++stage == PSTAGES) { stage = 0; phase ^= 1; }
         }
@@ -247,7 +248,8 @@ static inline int encode_pencil_maps(PencilMaps& pm, cplx* base, int n, long lon
 // tensors (zero-filled) or hold zeros.
 static inline int zgemm_sub_maps(const CUtensorMap& mapA, const CUtensorMap& mapB, const CUtensorMap& mapC, int M, int N,
                           int K, int batch, int a_row0, int a_col0, int b_row0, int b_col0, int c_row0, int c_col0,
-                          cplx* C, long long ldc, long long sC, cudaStream_t stream, int beta = 1) {
+                          cplx* C, long long ldc, long long sC, cudaStream_t stream, int beta = 1,
+                          int a_bmul = 1, int a_badd = 0) {
   if (M <= 0 || N <= 0 || K <= 0 || batch <= 0) return 0;
   static bool attr = false;
   static int sms = 0;
@@ -260,7 +262,7 @@ static inline int zgemm_sub_maps(const CUtensorMap& mapA, const CUtensorMap& map
   }
   const int Kr = (K + PBK - 1) / PBK * PBK;
   SubGemmGeom g{M, N, Kr, batch, a_row0, a_col0, b_row0, b_col0, c_row0, c_col0, C, ldc, sC,
-                (M + PBM - 1) / PBM, (N + PBN - 1) / PBN, beta};
+                (M + PBM - 1) / PBM, (N + PBN - 1) / PBN, beta, a_bmul, a_badd};
   const long long tiles = (long long)g.tiles_m * g.tiles_n * batch;
   const int grid = (int)(tiles < sms ? tiles : sms);
   zgemm_sub_tma<<<grid, PTHREADS, P_SMEM, stream>>>(mapA, mapB, mapC, g);

@@ -430,8 +430,11 @@ class _Engine:
             pos = 0
             for s, (a, b) in enumerate(pen_idx):
                 cnt = b - a
+                dinv = self._dinv()
+                dptr = _ptr(dinv) + a * self._dinv_per_pencil if dinv is not None else 0
                 _lib.call("cirr_zgetrs_batched", _ptr(self.pencils[a]), n, n, n * n, cnt, _ptr(self.perm[a]),
-                          _ptr(R), K, n * K, _ptr(rhs_of[pos:pos + cnt]), K, _ptr(Y[pos]), K, n * K, self.stream)
+                          _ptr(R), K, n * K, _ptr(rhs_of[pos:pos + cnt]), K, _ptr(Y[pos]), K, n * K, dptr,
+                          self.stream)
                 pos += cnt
         _work("solve_flops", Ptot * 8.0 * n * n * K)
         _work("solve_flops_exec", sum((b - a) * 8.0 * n * n * rhs[ci].shape[1]
@@ -444,6 +447,18 @@ class _Engine:
             self.cs[ci].stats.n_linear_solves += len(self.cs[ci].nodes) * rhs[ci].shape[1]
         del Y
         return {ci: St[s] for s, ci in enumerate(active)}
+
+    def _dinv(self):
+        """Inverses of the 64x64 diagonal blocks of every factor (computed once per
+        factorisation on first use; each pencil's slice is contiguous)."""
+        if getattr(self, "dinv", None) is None:
+            torch, n = self.torch, self.n
+            nbytes = int(_lib.call("cirr_diag_inv_bytes", n, self.P))
+            self._dinv_per_pencil = nbytes // self.P
+            self.dinv = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+            with _stage("solve"):
+                _lib.call("cirr_diag_inverses", _ptr(self.pencils), n, n, n * n, self.P, _ptr(self.dinv), self.stream)
+        return self.dinv
 
     def bmul(self, x):
         """B @ x for a device (n x k) complex block."""
@@ -789,7 +804,7 @@ class _Engine:
                                contour=c.contour, stats=c.stats)
 
     def free(self):
-        for name in ("pencils", "maxabs", "ipiv", "perm", "minpiv", "info"):
+        for name in ("pencils", "maxabs", "ipiv", "perm", "minpiv", "info", "dinv"):
             if hasattr(self, name):
                 delattr(self, name)
 

@@ -79,8 +79,9 @@ def test_gemm(lib, kind, shape):
         assert err < 1e-13 * np.sqrt(K), (beta, err)
 
 
+@pytest.mark.parametrize("K,use_dinv", [(37, False), (100, False), (100, True)])
 @pytest.mark.parametrize("n,batch", [(3, 2), (100, 3), (256, 4), (333, 2), (1024, 2)])
-def test_getrf_getrs(lib, n, batch):
+def test_getrf_getrs(lib, n, batch, K, use_dinv):
     rng = np.random.default_rng(n)
     A = rng.standard_normal((batch, n, n)) + 1j * rng.standard_normal((batch, n, n))
     F = cuda(A.copy())
@@ -90,12 +91,16 @@ def test_getrf_getrs(lib, n, batch):
     info = torch.empty(batch, dtype=torch.int32, device="cuda")
     lib.call("cirr_zgetrf_batched", P(F), n, n, n * n, batch, P(ipiv), P(perm), P(mp), P(info), P(ws_lu(n, batch)), S())
     assert (info.cpu().numpy() == 0).all()
-    K = 37
+    dinv = 0
+    if use_dinv:
+        dinv_t = cuda(np.zeros(lib.call("cirr_diag_inv_bytes", n, batch), dtype=np.uint8))
+        lib.call("cirr_diag_inverses", P(F), n, n, n * n, batch, P(dinv_t), S())
+        dinv = P(dinv_t)
     R = rng.standard_normal((2, n, K)) + 1j * rng.standard_normal((2, n, K))
     rhs_of = cuda(np.arange(batch, dtype=np.int32) % 2)
     Y = torch.empty((batch, n, K), dtype=torch.complex128, device="cuda")
     lib.call("cirr_zgetrs_batched", P(F), n, n, n * n, batch, P(perm), P(cuda(R)), K, n * K, P(rhs_of), K, P(Y), K,
-             n * K, S())
+             n * K, dinv, S())
     y = Y.cpu().numpy()
     lu = F.cpu().numpy()
     for j in range(batch):

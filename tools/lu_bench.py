@@ -27,6 +27,7 @@ def main(n=4096, P=128, reps=3, K=32):
     Y = torch.empty((P, n, K), dtype=torch.complex128, device="cuda")
     st = torch.cuda.current_stream().cuda_stream
     lws = torch.empty(_lib.call("cirr_zgetrf_ws_bytes", n, P), dtype=torch.uint8, device="cuda")
+    dinv = torch.empty(_lib.call("cirr_diag_inv_bytes", n, P), dtype=torch.uint8, device="cuda")
     e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     for r in range(reps):
         e[0].record()
@@ -35,9 +36,10 @@ def main(n=4096, P=128, reps=3, K=32):
         e[1].record()
         _lib.call("cirr_zgetrf_batched", pen.data_ptr(), n, n, n * n, P, ipiv.data_ptr(), perm.data_ptr(),
                   mp.data_ptr(), info.data_ptr(), lws.data_ptr(), st)
+        _lib.call("cirr_diag_inverses", pen.data_ptr(), n, n, n * n, P, dinv.data_ptr(), st)
         e[2].record()
         _lib.call("cirr_zgetrs_batched", pen.data_ptr(), n, n, n * n, P, perm.data_ptr(), R.data_ptr(), K, n * K,
-                  rhs_of.data_ptr(), K, Y.data_ptr(), K, n * K, st)
+                  rhs_of.data_ptr(), K, Y.data_ptr(), K, n * K, dinv.data_ptr(), st)
         e[3].record()
         torch.cuda.synchronize()
         t_as, t_lu, t_s = e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), e[2].elapsed_time(e[3])
