@@ -109,6 +109,9 @@ int cirr_gen_eig_vectors(void* ws, const int* kdim, int kmax, int nprob, const c
                          const int* sel_cnt, int smax, void* scratch, cirr_cplx* S, long long lds, long long sS,
                          cudaStream_t stream);
 
+/* debug: clock64 marks of the last cirr_orth launch (4 entries) */
+int cirr_orth_phases(long long* host_out);
+
 /* debug: sweeps, rotations and clock64 cycles of the last eigenvalue-QR launch (8 entries) */
 int cirr_gen_eig_qr_stats(long long* host_out);
 

@@ -32,6 +32,7 @@ SIGNATURES = {
     "cirr_diag_inverses": [_P, _I, _L, _L, _I, _P, _P],
     "cirr_moments": [_P, _L, _L, _I, _I, _P, _I, _P, _I, _P, _L, _L, _P],
     "cirr_orth_ws_bytes": [_I, _I],
+    "cirr_orth_phases": [_P],
     "cirr_orth": [_P, _L, _L, _I, _I, _I, _D, _P, _P, _P, _P, _L, _L, _P, _P, _P],
     "cirr_orthonormalize": [_P, _L, _L, _I, _I, _I, _D, _P, _L, _L, _P, _P],
     "cirr_gemm": [_I, _I, _I, _I, _I, _P, _L, _L, _P, _L, _L, _P, _L, _L, _D, _I, _P],

@@ -142,22 +142,36 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
 
 // Software grid barrier for cooperative launches (all CTAs co-resident).
-// bar[0] = arrival counter, bar[1] = generation.
+// Two-level: CTAs arrive on one of ceil(G/16) group counters, the last of a
+// group arrives on the top counter, the last overall bumps the generation --
+// no single L2 address sees more than 16 atomics per barrier.  Every counter
+// sits on its own 128-byte line: bar[0] generation, bar[32] top counter,
+// bar[64 + 32*g] group g.  Needs (64 + 32*ceil(G/16)) * 4 bytes, zeroed.
+constexpr int GB_GROUP = 16;
+__host__ __device__ constexpr long long grid_barrier_bytes(int nblocks) {
+  return (64LL + 32LL * ((nblocks + GB_GROUP - 1) / GB_GROUP)) * 4;
+}
 __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    volatile unsigned* vgen = bar + 1;
-    unsigned gen = *vgen;
+    volatile unsigned* vgen = bar;
+    const unsigned gen = *vgen;
+    const unsigned g = blockIdx.x / GB_GROUP;
+    const unsigned ngroups = (nblocks + GB_GROUP - 1) / GB_GROUP;
+    const unsigned gsize = min((unsigned)GB_GROUP, nblocks - g * GB_GROUP);
+    unsigned* gcnt = bar + 64 + 32 * g;
     __threadfence();
-    if (atomicAdd(bar, 1u) == nblocks - 1) {
-      bar[0] = 0;
+    if (atomicAdd(gcnt, 1u) == gsize - 1) {
+      *gcnt = 0;
       __threadfence();
-      atomicAdd(bar + 1, 1u);
-    } else {
-      while (*vgen == gen) { __nanosleep(32); }
+      if (atomicAdd(bar + 32, 1u) == ngroups - 1) {
+        bar[32] = 0;
+        __threadfence();
+        atomicAdd(bar, 1u);
+      }
     }
+    while (*vgen == gen) { __nanosleep(20); }
     __threadfence();
   }
   __syncthreads();
 }
-

@@ -457,7 +457,19 @@ __global__ void __launch_bounds__(GT) gen_eig_kernel(const cplx* __restrict__ At
           if (kk - 2 >= l) tst += fabs(H[(kk - 1) * ld + kk - 2].x);
           if (kk + 1 <= ihi) tst += fabs(H[(kk + 1) * ld + kk].x);
         }
-        if (hs <= EPS * tst) found = max(found, kk);
+        bool neg = hs <= 1e-300;
+        if (!neg && hs <= EPS * tst) {
+          // zlahqr's Ahues & Tisseur test: also deflate when the off-diagonal
+          // product is negligible against the local eigenvalue gap
+          const double h01 = cabs1(H[(kk - 1) * ld + kk]);
+          const double ab = fmax(hs, h01), ba = fmin(hs, h01);
+          const double hkk = cabs1(H[kk * ld + kk]);
+          const double dd = cabs1(csub(H[(kk - 1) * ld + kk - 1], H[kk * ld + kk]));
+          const double aa = fmax(hkk, dd), bb = fmin(hkk, dd);
+          const double s = aa + ab;
+          neg = ba * (ab / s) <= fmax(1e-300, EPS * (bb * (aa / s)));
+        }
+        if (neg) found = max(found, kk);
       }
       for (int o = 16; o > 0; o >>= 1) found = max(found, __shfl_xor_sync(0xffffffffu, found, o));
       if (lane == 0) ri[wid] = found;

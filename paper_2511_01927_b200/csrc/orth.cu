@@ -26,6 +26,9 @@ __device__ __forceinline__ void rr_pair(int round, int k, int cp, int& p, int& q
 }
 
 constexpr int HT = 256;
+constexpr int JB = 8;   // rows per Jacobi block
+__device__ long long g_orth_phase[4];
+#define ORTH_MARK(i) do { if (blockIdx.x == 0 && threadIdx.x == 0) g_orth_phase[i] = clock64(); } while (0)
 
 // --------------------------------------------------------------------------
 // QR-preconditioned one-sided Jacobi (the production path).
@@ -53,6 +56,7 @@ __global__ void __launch_bounds__(HT) qr_jacobi_kernel(cplx* __restrict__ W, lon
   const int G = gridDim.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int jmax = min(c, n);
   const long long cc = (long long)c * c;
+  ORTH_MARK(0);
   // ---------------- A: Householder QR ----------------
   for (int j = 0; j < jmax; ++j) {
     for (int p = blockIdx.x; p < nprob; p += G) {
@@ -103,6 +107,7 @@ __global__ void __launch_bounds__(HT) qr_jacobi_kernel(cplx* __restrict__ W, lon
     }
     grid_barrier(bar, G);
   }
+  ORTH_MARK(1);
   // ---------------- B: Jacobi on the rows of R ----------------
   // Xc[p][a][i] = conj(R[a][i]) (R[a][i] = W[p][i][a] for a <= i < c, a < jmax), Jt = I
   {
@@ -117,55 +122,93 @@ __global__ void __launch_bounds__(HT) qr_jacobi_kernel(cplx* __restrict__ W, lon
   }
   if (blockIdx.x == 0 && tid == 0) { counters[0] = 0; counters[1] = 0; }
   grid_barrier(bar, G);
-  const int cp = c + (c & 1);
-  const int npairs = cp / 2;
+  // block-cyclic one-sided Jacobi: rows are grouped in blocks of JB; each outer
+  // round pairs blocks (circle method) and a CTA rotates every row pair of its
+  // 2*JB rows in shared memory (one local sweep), so the grid synchronises once
+  // per block round instead of once per row round.
+  extern __shared__ __align__(16) cplx jsm[];
+  cplx* sx = jsm;                       // 2*JB rows of Xc (length c)
+  cplx* sj = jsm + 2 * JB * (long long)c; // 2*JB rows of Jt
+  __shared__ int s_rot;
+  const int nblk = (c + JB - 1) / JB;
+  const int bp = nblk + (nblk & 1);
+  const int npairs = bp / 2;
   const long long pitems = (long long)nprob * npairs;
   int sweep = 0;
   for (; sweep < max_sweeps && c > 1; ++sweep) {
     if (blockIdx.x == 0 && tid == 0) counters[(sweep + 1) & 1] = 0;
-    for (int round = 0; round < cp - 1; ++round) {
+    for (int round = 0; round < max(bp - 1, 1); ++round) {
       for (long long it = blockIdx.x; it < pitems; it += G) {
-        const int p = (int)(it / npairs), k = (int)(it % npairs);
-        int a, b2;
-        rr_pair(round, k, cp, a, b2);
-        if (a >= c || b2 >= c) continue;
-        if (a > b2) { int t = a; a = b2; b2 = t; }
-        cplx* xa = Xc + (long long)p * cc + (long long)a * c;
-        cplx* xb = Xc + (long long)p * cc + (long long)b2 * c;
-        double al = 0.0, be = 0.0, gr = 0.0, gi = 0.0;
-        for (int i = tid; i < c; i += HT) {
-          const cplx x = xa[i], y = xb[i];
-          al += cabs2(x);
-          be += cabs2(y);
-          const cplx g = cconjmul(x, y);
-          gr += g.x;
-          gi += g.y;
+        const int p = (int)(it / npairs), kk = (int)(it % npairs);
+        int bI, bJ;
+        if (nblk == 1) { bI = 0; bJ = bp; }  // single block: local sweep only
+        else rr_pair(round, kk, bp, bI, bJ);
+        if (bI >= nblk && bJ >= nblk) continue;
+        if (bI >= nblk) { bI = bJ; bJ = nblk; }
+        // local rows: block I then block J (J may be absent)
+        const int r0 = bI * JB, n0 = min(JB, c - r0);
+        const int r1 = bJ < nblk ? bJ * JB : 0, n1 = bJ < nblk ? min(JB, c - r1) : 0;
+        const int nl = n0 + n1;
+        cplx* Xp = Xc + (long long)p * cc;
+        cplx* Jp = Jt + (long long)p * cc;
+        for (int e = tid; e < nl * c; e += HT) {
+          const int lr = e / c, i = e % c;
+          const int gr = lr < n0 ? r0 + lr : r1 + lr - n0;
+          sx[(long long)lr * c + i] = Xp[(long long)gr * c + i];
+          sj[(long long)lr * c + i] = Jp[(long long)gr * c + i];
         }
-        al = warp_sum(al); be = warp_sum(be); gr = warp_sum(gr); gi = warp_sum(gi);
+        if (tid == 0) s_rot = 0;
         __syncthreads();
-        if (lane == 0) { red[0][wid] = al; red[1][wid] = be; red[2][wid] = gr; red[3][wid] = gi; }
-        __syncthreads();
-        al = 0.0; be = 0.0; gr = 0.0; gi = 0.0;
-        for (int w2 = 0; w2 < HT / 32; ++w2) { al += red[0][w2]; be += red[1][w2]; gr += red[2][w2]; gi += red[3][w2]; }
-        const double ag = hypot(gr, gi);
-        if (al > 0.0 && be > 0.0 && ag > tol * sqrt(al) * sqrt(be)) {
-          const double zeta = (be - al) / (2.0 * ag);
-          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          const double cs = 1.0 / sqrt(1.0 + t * t), sn = t * cs;
-          const cplx se = cmk(sn * gr / ag, sn * gi / ag);
-          const cplx sec = cconj(se);
-          cplx* ja = Jt + (long long)p * cc + (long long)a * c;
-          cplx* jb = Jt + (long long)p * cc + (long long)b2 * c;
-          for (int i = tid; i < c; i += HT) {
-            const cplx x = xa[i], y = xb[i];
-            xa[i] = csub(cscale(x, cs), cmul(sec, y));
-            xb[i] = cadd(cmul(se, x), cscale(y, cs));
-            const cplx u = ja[i], w = jb[i];
-            ja[i] = csub(cscale(u, cs), cmul(sec, w));
-            jb[i] = cadd(cmul(se, u), cscale(w, cs));
+        // one local sweep over all pairs of the nl rows (circle method, a warp per pair)
+        const int lp = nl + (nl & 1);
+        for (int lround = 0; lround < lp - 1; ++lround) {
+          for (int pk = wid; pk < lp / 2; pk += HT / 32) {
+            int a, b2;
+            rr_pair(lround, pk, lp, a, b2);
+            if (a >= nl || b2 >= nl) continue;
+            if (a > b2) { int t = a; a = b2; b2 = t; }
+            cplx* xa = sx + (long long)a * c;
+            cplx* xb = sx + (long long)b2 * c;
+            double al = 0.0, be = 0.0, gr = 0.0, gi = 0.0;
+            for (int i = lane; i < c; i += 32) {
+              const cplx x = xa[i], y = xb[i];
+              al += cabs2(x);
+              be += cabs2(y);
+              const cplx g = cconjmul(x, y);
+              gr += g.x;
+              gi += g.y;
+            }
+            al = warp_sum(al); be = warp_sum(be); gr = warp_sum(gr); gi = warp_sum(gi);
+            const double ag = hypot(gr, gi);
+            if (al > 0.0 && be > 0.0 && ag > tol * sqrt(al) * sqrt(be)) {
+              const double zeta = (be - al) / (2.0 * ag);
+              const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+              const double cs = 1.0 / sqrt(1.0 + t * t), sn = t * cs;
+              const cplx se = cmk(sn * gr / ag, sn * gi / ag);
+              const cplx sec = cconj(se);
+              cplx* ja = sj + (long long)a * c;
+              cplx* jb = sj + (long long)b2 * c;
+              for (int i = lane; i < c; i += 32) {
+                const cplx x = xa[i], y = xb[i];
+                xa[i] = csub(cscale(x, cs), cmul(sec, y));
+                xb[i] = cadd(cmul(se, x), cscale(y, cs));
+                const cplx u = ja[i], w = jb[i];
+                ja[i] = csub(cscale(u, cs), cmul(sec, w));
+                jb[i] = cadd(cmul(se, u), cscale(w, cs));
+              }
+              if (lane == 0) atomicAdd(&s_rot, 1);
+            }
           }
-          if (tid == 0) atomicAdd(counters + (sweep & 1), 1);
+          __syncthreads();
         }
+        for (int e = tid; e < nl * c; e += HT) {
+          const int lr = e / c, i = e % c;
+          const int gr = lr < n0 ? r0 + lr : r1 + lr - n0;
+          Xp[(long long)gr * c + i] = sx[(long long)lr * c + i];
+          Jp[(long long)gr * c + i] = sj[(long long)lr * c + i];
+        }
+        if (tid == 0 && s_rot > 0) atomicAdd(counters + (sweep & 1), s_rot);
+        __syncthreads();
       }
       grid_barrier(bar, G);
     }
@@ -174,6 +217,7 @@ __global__ void __launch_bounds__(HT) qr_jacobi_kernel(cplx* __restrict__ W, lon
     if (rots == 0) { ++sweep; break; }
   }
   if (blockIdx.x == 0 && tid == 0) *sweeps_out = sweep;
+  ORTH_MARK(2);
   // ---------------- C: singular values, rank cut, Q ----------------
   for (int p = blockIdx.x; p < nprob; p += G) {
     double* sg = reinterpret_cast<double*>(tau + (long long)nprob * c) + (long long)p * c;  // scratch
@@ -246,6 +290,7 @@ __global__ void __launch_bounds__(HT) qr_jacobi_kernel(cplx* __restrict__ W, lon
     }
     grid_barrier(bar, G);
   }
+  ORTH_MARK(3);
 }
 
 }  // namespace
@@ -253,7 +298,7 @@ __global__ void __launch_bounds__(HT) qr_jacobi_kernel(cplx* __restrict__ W, lon
 // Workspace bytes for cirr_orth (barrier/counters, X and J (nprob x c x c),
 // tau and sigma scratch).
 CIRR_API long long cirr_orth_ws_bytes(int c, int nprob) {
-  return 256 + 2LL * nprob * c * c * 16 + (long long)nprob * c * 16 + (long long)nprob * c * 8 + 256;
+  return 4096 + 2LL * nprob * c * c * 16 + (long long)nprob * c * 16 + (long long)nprob * c * 8 + 256;
 }
 
 // Rank-revealing orthonormal basis of S (n x c) for nprob blocks; W[prob] holds
@@ -268,16 +313,20 @@ CIRR_API int cirr_orth(cplx* W, long long ldw, long long wstride, int n, int c, 
   if (n <= 0 || c <= 0 || nprob <= 0 || ldw < n || ldq < n) return CIRR_EINVAL;
   unsigned char* base = reinterpret_cast<unsigned char*>(ws);
   unsigned* bar = reinterpret_cast<unsigned*>(base);
-  int* counters = reinterpret_cast<int*>(base + 16);
-  cplx* Xc = reinterpret_cast<cplx*>(base + 256);
+  int* counters = reinterpret_cast<int*>(base + 3072);  // after the barrier lines (<= 296 CTAs)
+  cplx* Xc = reinterpret_cast<cplx*>(base + 4096);
   cplx* Jt = Xc + (long long)nprob * c * c;
   cplx* tau = Jt + (long long)nprob * c * c;
-  cudaError_t e = cudaMemsetAsync(ws, 0, 256, stream);
+  cudaError_t e = cudaMemsetAsync(ws, 0, 4096, stream);
   if (e != cudaSuccess) return (int)e;
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qr_jacobi_kernel, HT, 0);
+  const size_t jsmem = sizeof(cplx) * 4 * JB * (size_t)c;
+  if (jsmem > 227 * 1024) return CIRR_EINVAL;
+  cudaFuncSetAttribute(qr_jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jsmem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qr_jacobi_kernel, HT, jsmem);
+  if (per_sm < 1) return CIRR_EINVAL;
   const int cp = c + (c & 1);
   long long want = (long long)nprob * (cp / 2);
   if (want < (long long)nprob * c) want = (long long)nprob * c;
@@ -289,7 +338,7 @@ CIRR_API int cirr_orth(cplx* W, long long ldw, long long wstride, int n, int c, 
   int max_sweeps = 60;
   void* args[] = {&W, &ldw, &wstride, &n, &c, &nprob, &rel_tol, &sigma, &order, &kept, &Qt, &ldq, &qstride,
                   &bar, &counters, &Xc, &Jt, &tau, &max_sweeps, &tol, &sweeps_out};
-  e = cudaLaunchCooperativeKernel((void*)qr_jacobi_kernel, dim3(grid), dim3(HT), args, 0, stream);
+  e = cudaLaunchCooperativeKernel((void*)qr_jacobi_kernel, dim3(grid), dim3(HT), args, jsmem, stream);
   cirr_note_launch();
   if (e != cudaSuccess) return (int)e;
   return 0;
@@ -368,4 +417,9 @@ CIRR_API int cirr_orthonormalize(const cplx* Y, long long ldy, long long sy, int
   cgs2_kernel<<<nprob, GT2, smem, stream>>>(Y, ldy, sy, n, c, drop_tol, Qt, ldq, sq, kept);
   CIRR_CHECK_LAUNCH();
   return 0;
+}
+
+// debug: clock64 marks of the last cirr_orth launch (start, after QR, after Jacobi, end)
+CIRR_API int cirr_orth_phases(long long* host_out) {
+  return (int)cudaMemcpyFromSymbol(host_out, g_orth_phase, sizeof(long long) * 4);
 }

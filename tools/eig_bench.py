@@ -62,7 +62,11 @@ def t_orth(n, c, nprob=2, reps=2):
         _lib.call("cirr_orth", W.data_ptr(), n, c * n, n, c, nprob, 1e-12, sig.data_ptr(), order.data_ptr(), kept.data_ptr(),
                   Qt.data_ptr(), n, c * n, ws.data_ptr(), sw.data_ptr(), st)
         e1.record(); torch.cuda.synchronize()
-    print(f"orth n={n} c={c} nprob={nprob}: {e0.elapsed_time(e1):.2f} ms sweeps={sw.item()} kept={kept.cpu().numpy()}", flush=True)
+    import ctypes
+    ph = (ctypes.c_longlong * 4)()
+    _lib.call("cirr_orth_phases", ctypes.addressof(ph))
+    print(f"orth n={n} c={c} nprob={nprob}: {e0.elapsed_time(e1):.2f} ms sweeps={sw.item()} kept={kept.cpu().numpy()} "
+          f"QR {(ph[1]-ph[0])/1e6:.2f} Jacobi {(ph[2]-ph[1])/1e6:.2f} Q {(ph[3]-ph[2])/1e6:.2f} Mcycles", flush=True)
 
 
 if __name__ == "__main__" and len(sys.argv) == 1:
