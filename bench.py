@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--config", type=int, default=4, choices=[4])
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-variants", action="store_true", help="skip the labelled (non-reference) variants")
     return ap.parse_args()
 
 
@@ -295,6 +296,36 @@ def run_cirr(args):
     e2e_s = max_over_ranks(statistics.median(e2e_times))
     e2e_value = world / e2e_s
 
+    # labelled variant (NOT the path of record, SURVEY.md finding 9):
+    # conjugate-pair halving of the node set, same workload and tolerance
+    variants = {}
+    if not args.no_variants:
+        import dataclasses
+        vcfg = dataclasses.replace(cfg, conjugate_pairs=True)
+        solve_multi(dp, wl.contours, vcfg, seed=0)
+        barrier()
+        torch.cuda.synchronize()
+        v0 = torch.cuda.Event(enable_timing=True)
+        v1 = torch.cuda.Event(enable_timing=True)
+        v0.record(stream)
+        for _ in range(args.steps):
+            vm = solve_multi(dp, wl.contours, vcfg, seed=0)
+        v1.record(stream)
+        torch.cuda.synchronize()
+        vms = max_over_ranks(v0.elapsed_time(v1))
+        vcounts = [len(r.eigenvalues) if r is not None else 0 for r in vm.results]
+        diff = 0.0
+        for rv, rr in zip(vm.results, last.results):
+            if rv is not None and rr is not None and len(rv.eigenvalues) == len(rr.eigenvalues):
+                for lam in rr.eigenvalues:
+                    diff = max(diff, float(np.min(np.abs(rv.eigenvalues - lam)) / abs(lam)))
+        variants["conjugate_pairs"] = {
+            "label": "variant, not the reference's algorithm: factor the N/2 upper-half nodes of each "
+                     "real-axis-symmetric contour, mirror the rest by conjugation",
+            "value": world * args.steps / (vms / 1e3), "unit": UNIT, "ms_per_step": vms / args.steps,
+            "eigenpairs": vcounts, "n_factorizations": vm.stats.n_factorizations,
+            "n_linear_solves": vm.stats.n_linear_solves, "max_rel_eig_diff_vs_record": diff}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         passes = max(iters) if iters else 8
@@ -326,11 +357,14 @@ def run_cirr(args):
             "eigenpairs_per_s": pairs * world / (per_step / 1e3),
             "shifted_solves_per_s": solves * world / (per_step / 1e3),
             "eigenpairs": counts, "iterations": iters,
+            "n_factorizations": last.stats.n_factorizations, "n_linear_solves": solves,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "seconds_per_step": e2e_s},
             "gpu_launches": launches,
             "clocks": clocks.summary(),
         }
+        if variants:
+            line["variants"] = variants
         if cpu is not None:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)

@@ -128,6 +128,11 @@ int cirr_gather_cols(const cirr_cplx* in, long long ldi, long long si, const int
                      const int* cnt, int cmax, int n, int nprob, cirr_cplx* out, long long ldo,
                      long long so, cudaStream_t stream);
 
+/* out[b][r][c] = op(in[src[b]][r][col0[b] + c]), op = conj when cj[b] (conjugate-pair variant) */
+int cirr_copy_cols(const cirr_cplx* in, long long ldi, long long si, const int* src, const int* col0,
+                   const int* cj, int n, int K, int count, cirr_cplx* out, long long ldo, long long so,
+                   cudaStream_t stream);
+
 /* layout helper: out[b] = in[b]^T (or ^H when conj != 0) */
 int cirr_transpose(int conj, const cirr_cplx* in, long long ldi, long long si, int rows, int cols,
                    int batch, cirr_cplx* out, long long ldo, long long so, cudaStream_t stream);

@@ -46,6 +46,7 @@ SIGNATURES = {
     "cirr_gen_eig_vectors": [_P, _P, _I, _I, _P, _P, _P, _I, _P, _P, _L, _L, _P],
     "cirr_residuals": [_P, _P, _L, _L, _I, _P, _L, _P, _I, _I, _P, _L, _P],
     "cirr_gather_cols": [_P, _L, _L, _P, _L, _P, _I, _I, _I, _P, _L, _L, _P],
+    "cirr_copy_cols": [_P, _L, _L, _P, _P, _P, _I, _I, _I, _P, _L, _L, _P],
     "cirr_transpose": [_I, _P, _L, _L, _I, _I, _I, _P, _L, _L, _P],
     "cirr_target_sm": [],
     "cirr_launch_count": [],

@@ -110,3 +110,31 @@ CIRR_API int cirr_transpose(int conj, const cplx* in, long long ldi, long long s
   CIRR_CHECK_LAUNCH();
   return 0;
 }
+
+namespace {
+// out[b][r][c] = op_b(in[src[b]][r][col0[b] + c]),  op = conj when cj[b]
+__global__ void copy_cols_kernel(const cplx* __restrict__ in, long long ldi, long long si, const int* __restrict__ src,
+                                 const int* __restrict__ col0, const int* __restrict__ cj, int n, int K,
+                                 cplx* __restrict__ out, long long ldo, long long so) {
+  const int b = blockIdx.y;
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (long long)n * K) return;
+  const int r = (int)(e / K), c = (int)(e % K);
+  cplx v = in[(long long)src[b] * si + (long long)r * ldi + col0[b] + c];
+  if (cj[b]) v.y = -v.y;
+  out[(long long)b * so + (long long)r * ldo + c] = v;
+}
+}  // namespace
+
+// Batched column-block copy with optional conjugation (builds the mirrored
+// solutions Y_{N-1-j} = conj(M_j^-1 conj(R)) of the conjugate-pair variant).
+CIRR_API int cirr_copy_cols(const cplx* in, long long ldi, long long si, const int* src, const int* col0,
+                            const int* cj, int n, int K, int count, cplx* out, long long ldo, long long so,
+                            cudaStream_t stream) {
+  if (n <= 0 || K < 0 || count < 0) return CIRR_EINVAL;
+  if (K == 0 || count == 0) return 0;
+  dim3 g((unsigned)(((long long)n * K + 255) / 256), count);
+  copy_cols_kernel<<<g, 256, 0, stream>>>(in, ldi, si, src, col0, cj, n, K, out, ldo, so);
+  CIRR_CHECK_LAUNCH();
+  return 0;
+}

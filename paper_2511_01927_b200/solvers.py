@@ -64,6 +64,11 @@ class SolverConfig:
     tol: float = 1e-10
     rank_rel_tol: float = 1e-12
     drop_tol: float = 1e-10
+    # Labelled variant, not the reference's behaviour (SURVEY.md finding 9):
+    # for the real pencils this path holds and a conjugate-symmetric node set,
+    # factor only the upper-half nodes and recover the lower half from
+    # M(conj z)^-1 R = conj(M(z)^-1 conj R).  Halves K1+K2 work.
+    conjugate_pairs: bool = False
 
     def __post_init__(self):
         if self.n_q < 4 or self.n_moments < 1 or self.max_refine < 1:
@@ -85,7 +90,8 @@ def _cfg_view(cfg) -> SolverConfig:
         return cfg
     return SolverConfig(n_q=cfg.n_q, source_cols=cfg.source_cols, n_moments=cfg.n_moments,
                         max_refine=cfg.max_refine, tol=cfg.tol, rank_rel_tol=cfg.rank_rel_tol,
-                        drop_tol=getattr(cfg, "drop_tol", 1e-10))
+                        drop_tol=getattr(cfg, "drop_tol", 1e-10),
+                        conjugate_pairs=bool(getattr(cfg, "conjugate_pairs", False)))
 
 
 @dataclass
@@ -333,6 +339,30 @@ class _Contour:
         self.best_res = np.inf
         self.x_dev = None  # inside Ritz vectors on device (n x kin)
         self.done = False
+        # factored nodes (all of them unless the conjugate-pair variant applies)
+        self.half = False
+        self.fidx = np.arange(len(self.nodes))
+        if cfg.conjugate_pairs:
+            self._pair()
+
+    def _pair(self):
+        """fidx = upper-half nodes; mate[j] = position in fidx of conj(z_j)."""
+        z = self.nodes
+        N = len(z)
+        up = np.flatnonzero(z.imag > 0)
+        if N % 2 or len(up) * 2 != N:
+            return
+        scale = max(float(np.abs(z).max()), 1e-300)
+        mate = np.full(N, -1)
+        for r, j in enumerate(up):
+            mate[j] = r
+            k = int(np.argmin(np.abs(z - np.conj(z[j]))))
+            if abs(z[k] - np.conj(z[j])) > 1e-13 * scale or z[k].imag >= 0 or mate[k] >= 0:
+                return
+            mate[k] = r
+        if np.any(mate < 0):
+            return
+        self.half, self.fidx, self.mate = True, up, mate
 
     def coef(self, moments: int) -> np.ndarray:
         """c[j, m] = w_j zeta_j^m with zeta_j = (z_j - gamma)/rho (sequential powers)."""
@@ -362,10 +392,10 @@ class _Engine:
         torch, n = self.torch, self.n
         self.node_off = [0]
         for c in self.cs:
-            self.node_off.append(self.node_off[-1] + len(c.nodes))
+            self.node_off.append(self.node_off[-1] + len(c.fidx))
         P = self.node_off[-1]
         self.P = P
-        z = torch.from_numpy(np.concatenate([c.nodes for c in self.cs])).to("cuda")
+        z = torch.from_numpy(np.concatenate([c.nodes[c.fidx] for c in self.cs])).to("cuda")
         self.pencils = torch.empty((P, n, n), dtype=torch.complex128, device="cuda")
         self.maxabs = torch.empty(P, dtype=torch.float64, device="cuda")
         self.ipiv = torch.empty((P, n), dtype=torch.int32, device="cuda")
@@ -385,16 +415,17 @@ class _Engine:
         minpiv = self.minpiv.cpu().numpy()
         info = self.info.cpu().numpy()
         for ci, c in enumerate(self.cs):
-            c.stats.n_factorizations = len(c.nodes)
-            for jl in range(len(c.nodes)):
+            c.stats.n_factorizations = len(c.fidx)
+            for jl in range(len(c.fidx)):
                 j = self.node_off[ci] + jl
                 scale = max(maxabs[j], 1e-300)
                 if info[j] != 0 or not (minpiv[j] >= PIVOT_REL_TOL * scale):
-                    c.error = SingularShiftError(complex(c.nodes[jl]), node_index=jl)
+                    jn = int(c.fidx[jl])
+                    c.error = SingularShiftError(complex(c.nodes[jn]), node_index=jn)
                     c.done = True
                     break
         self.contour_of = torch.from_numpy(
-            np.concatenate([np.full(len(c.nodes), i, dtype=np.int32) for i, c in enumerate(self.cs)])
+            np.concatenate([np.full(len(c.fidx), i, dtype=np.int32) for i, c in enumerate(self.cs)])
         ).to("cuda")
 
     # -- K3: solve all pencils of the listed contours against per-contour RHS
@@ -406,20 +437,31 @@ class _Engine:
         if K == 0:
             return {ci: torch.zeros((0, n), dtype=torch.complex128, device="cuda") for ci in active}
         nset = len(active)
-        R = torch.zeros((nset, n, K), dtype=torch.complex128, device="cuda")
+        # solve width per contour: conjugate-pair contours with a complex
+        # block solve [R | conj R] on their upper-half factors
+        ks, cplx_rhs = [], []
+        for ci in active:
+            kc = rhs[ci].shape[1]
+            cx = self.cs[ci].half and bool(torch.any(rhs[ci].imag != 0))
+            cplx_rhs.append(cx)
+            ks.append(2 * kc if cx else kc)
+        Ks = max(ks)
+        R = torch.zeros((nset, n, Ks), dtype=torch.complex128, device="cuda")
         for s, ci in enumerate(active):
-            R[s, :, : rhs[ci].shape[1]].copy_(rhs[ci])
-        # pencils of the active contours (contiguous ranges)
-        offs = [0]
-        pen_idx = []
-        coefs = []
+            kc = rhs[ci].shape[1]
+            R[s, :, :kc].copy_(rhs[ci])
+            if cplx_rhs[s]:
+                R[s, :, kc:2 * kc].copy_(rhs[ci].conj())
+        pen_idx, spos = [], [0]
+        offs, coefs = [0], []
         for s, ci in enumerate(active):
             a, b = self.node_off[ci], self.node_off[ci + 1]
             pen_idx.append((a, b))
-            offs.append(offs[-1] + (b - a))
+            spos.append(spos[-1] + (b - a))
+            offs.append(offs[-1] + len(self.cs[ci].nodes))
             coefs.append(self.cs[ci].coef(moments))
-        Ptot = offs[-1]
-        Y = torch.empty((Ptot, n, K), dtype=torch.complex128, device="cuda")
+        Psolve, Ptot = spos[-1], offs[-1]
+        Ysol = torch.empty((Psolve, n, Ks), dtype=torch.complex128, device="cuda")
         rhs_of = torch.from_numpy(np.concatenate(
             [np.full(b - a, s, dtype=np.int32) for s, (a, b) in enumerate(pen_idx)])).to("cuda")
         coef = torch.from_numpy(np.concatenate(coefs, axis=0)).to("cuda")
@@ -433,18 +475,38 @@ class _Engine:
                 dinv = self._dinv()
                 dptr = _ptr(dinv) + a * self._dinv_per_pencil if dinv is not None else 0
                 _lib.call("cirr_zgetrs_batched", _ptr(self.pencils[a]), n, n, n * n, cnt, _ptr(self.perm[a]),
-                          _ptr(R), K, n * K, _ptr(rhs_of[pos:pos + cnt]), K, _ptr(Y[pos]), K, n * K, dptr,
+                          _ptr(R), Ks, n * Ks, _ptr(rhs_of[pos:pos + cnt]), Ks, _ptr(Ysol[pos]), Ks, n * Ks, dptr,
                           self.stream)
                 pos += cnt
-        _work("solve_flops", Ptot * 8.0 * n * n * K)
-        _work("solve_flops_exec", sum((b - a) * 8.0 * n * n * rhs[ci].shape[1]
-                                      for (a, b), ci in zip(pen_idx, active)))
+        _work("solve_flops", Psolve * 8.0 * n * n * Ks)
+        _work("solve_flops_exec", sum((b - a) * 8.0 * n * n * k for (a, b), k in zip(pen_idx, ks)))
+        if Psolve == Ptot and Ks == K:
+            Y = Ysol
+        else:  # conjugate-pair variant: expand to every node in quadrature order
+            Y = torch.zeros((Ptot, n, K), dtype=torch.complex128, device="cuda")
+            with _stage("solve"):
+                for s, ci in enumerate(active):
+                    c = self.cs[ci]
+                    kc = rhs[ci].shape[1]
+                    N = len(c.nodes)
+                    if c.half:
+                        up = np.zeros(N, dtype=bool)
+                        up[c.fidx] = True
+                        src = spos[s] + c.mate
+                        cj = (~up).astype(np.int32)
+                        col0 = np.where(up, 0, kc if cplx_rhs[s] else 0)
+                    else:
+                        src, cj, col0 = spos[s] + np.arange(N), np.zeros(N, np.int32), np.zeros(N)
+                    meta = torch.from_numpy(np.stack([src, col0, cj]).astype(np.int32)).to("cuda")
+                    _lib.call("cirr_copy_cols", _ptr(Ysol), Ks, n * Ks, _ptr(meta[0]), _ptr(meta[1]),
+                              _ptr(meta[2]), n, kc, N, _ptr(Y[offs[s]]), K, n * K, self.stream)
+            del Ysol
         with _stage("moments"):
             _lib.call("cirr_moments", _ptr(Y), K, n * K, n, K, _ptr(coef), moments, _ptr(off_t), nset,
                       _ptr(St), n, moments * K * n, self.stream)
         _work("moment_flops", Ptot * 8.0 * n * K * moments)
         for s, ci in enumerate(active):
-            self.cs[ci].stats.n_linear_solves += len(self.cs[ci].nodes) * rhs[ci].shape[1]
+            self.cs[ci].stats.n_linear_solves += len(self.cs[ci].fidx) * ks[s]
         del Y
         return {ci: St[s] for s, ci in enumerate(active)}
 
@@ -948,6 +1010,8 @@ class ProjectorContext:
         self._c.stats = SolveStats()
         self._c.error = None
         self._c.done = False
+        self._c.half = False
+        self._c.fidx = np.arange(len(self._c.nodes))
         self._eng = _Engine(self._dp, [self._c], SolverConfig())
         self._eng.factor()
         if self._c.error is not None:

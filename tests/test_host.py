@@ -88,3 +88,23 @@ def test_no_cuda_fails_loudly():
     with pytest.raises(DeviceError):
         S.cirr_solve(type("P", (), {"a": np.eye(2), "b": np.eye(2), "hermitian": True})(),
                      Contour(shape="circle", center=1 + 0j, radius=0.5))
+
+
+def test_conjugate_pair_selection():
+    """Conjugate-pair variant: upper-half nodes factor, lower half mirrors."""
+    from paper_2511_01927_b200.solvers import SolverConfig, _Contour
+    from paper_2511_01927_b200 import Contour
+
+    cfg = SolverConfig(n_q=32, conjugate_pairs=True)
+    for c in (Contour(shape="circle", center=1.5 + 0j, radius=0.7),
+              Contour(shape="ellipse", center=-0.5 + 0j, semi_re=0.3, semi_im=0.15)):
+        st = _Contour(0, c, cfg, 0, 10)
+        assert st.half and len(st.fidx) == 16
+        z = st.nodes
+        assert np.all(z[st.fidx].imag > 0)
+        for j in range(32):
+            src = z[st.fidx[st.mate[j]]]
+            assert abs(src - (z[j] if z[j].imag > 0 else np.conj(z[j]))) <= 1e-13
+    assert not _Contour(0, Contour(shape="circle", center=0.2 + 0.3j, radius=0.5), cfg, 0, 10).half
+    assert not _Contour(0, Contour(shape="circle", center=1.0 + 0j, radius=0.5),
+                        SolverConfig(n_q=32), 0, 10).half
