@@ -285,7 +285,7 @@ CIRR_API int cirr_zgetrf_batched(cplx* pencils, int n, long long ld, long long p
   cplx* linv = reinterpret_cast<cplx*>(ws);
   CUtensorMap mapL;
   const bool use_linv = use_tma && linv != nullptr &&
-                        cirr::encode_c128_map(&mapL, linv, NB, NB, batch, NB, (long long)NB * NB, cirr::PBK, cirr::PBM) == 0;
+                        cirr::encode_a_map(&mapL, linv, NB, NB, batch, NB, (long long)NB * NB) == 0;
   if (use_linv) {
     static bool la = false;
     if (!la) {

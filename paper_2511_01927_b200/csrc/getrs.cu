@@ -351,7 +351,7 @@ CIRR_API int cirr_zgetrs_batched(const cplx* LU, int n, long long ld, long long 
   // narrow RHS blocks (K <= 48) stay on the left-looking kernel: the 64-wide
   // GEMM tile of the right-looking path would be mostly padding there
   cirr::OperandMaps mT, mY;
-  bool tma = K > 48 && n >= 64 && cirr::encode_c128_map(&mT.a, LU, n, n, batch, ld, pencil_stride, cirr::PBK, cirr::PBM) == 0 &&
+  bool tma = K > 48 && n >= 64 && cirr::encode_a_map(&mT.a, LU, n, n, batch, ld, pencil_stride) == 0 &&
              cirr::encode_c128_map(&mY.b, Y, K, n, batch, ldy, ystride, cirr::PBN, cirr::PBK) == 0 &&
              cirr::encode_c128_map(&mY.c, Y, K, n, batch, ldy, ystride, cirr::PBN, cirr::PBM) == 0;
   if (tma) {
@@ -365,8 +365,7 @@ CIRR_API int cirr_zgetrs_batched(const cplx* LU, int n, long long ld, long long 
     dim3 gd((K + DSC - 1) / DSC, batch);
     CUtensorMap mD;
     const bool use_dinv = Dinv != nullptr &&
-                          cirr::encode_c128_map(&mD, Dinv, SNB, SNB, batch * nblk * 2, SNB, (long long)SNB * SNB,
-                                                cirr::PBK, cirr::PBM) == 0;
+                          cirr::encode_a_map(&mD, Dinv, SNB, SNB, batch * nblk * 2, SNB, (long long)SNB * SNB) == 0;
     for (int bi = 0; bi < nblk; ++bi) {  // forward: L (unit lower)
       const int i0 = bi * SNB, nb = min(SNB, n - i0);
       if (use_dinv) {  // Y_i <- L_ii^-1 Y_i on the GEMM (in place: each tile reads only its own rows)

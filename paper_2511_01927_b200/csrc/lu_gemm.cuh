@@ -5,12 +5,14 @@
 // One CTA per SM loops over 64x64 output tiles of all pencils.  A producer
 // warp issues one cp.async.bulk.tensor (TMA, SASS UTMALDG) per operand tile
 // -- a 64x16 slice of L21, a 16x64 slice of U12 and the 64x64 C block -- into
-// a 4-stage ring (completion by mbarrier transaction bytes); out-of-range rows
+// a 4-stage ring (completion by mbarrier transaction bytes; the L21 slice is
+// two 64x8 boxes with the 128-byte swizzle so the DMMA A-fragment loads are
+// bank-conflict free); out-of-range rows
 // and columns are zero-filled by the TMA unit.  The C block of a tile is
 // requested while that tile's main loop runs and the next tile's K slices
 // during its epilogue, so HBM traffic for C overlaps tensor work.  Eight
 // consumer warps run the complex DMMA main loop (mma.sync m8n8k4 f64 -> SASS
-// DMMA.8x8x4) with four independent accumulator sets per 8x8 block and write
+// DMMA.8x8x4) with two accumulator sets (re, im) per 8x8 block and write
 // C - acc straight to global memory.
 //
 // The three tensor maps describe the whole pencil batch as a 3-D float64
@@ -30,7 +32,9 @@ constexpr int P_A_BYTES = PBM * PBK * 16;
 constexpr int P_B_BYTES = PBK * PBN * 16;
 constexpr int P_STAGE_BYTES = P_A_BYTES + P_B_BYTES;
 constexpr int P_C_BYTES = PBM * PBN * 16;
-constexpr int P_SMEM = PSTAGES * P_STAGE_BYTES + P_C_BYTES + 8 * (2 * PSTAGES + 2) + 128;
+constexpr int P_SMEM = PSTAGES * P_STAGE_BYTES + P_C_BYTES + 8 * (2 * PSTAGES + 2) + 1024;
+constexpr int PAK = 8;                          // complex columns per swizzled A box (128 bytes)
+constexpr int P_A_HALF = PBM * PAK * 16;        // one A box
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
@@ -49,6 +53,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       "{\n .reg .pred p;\n WAIT_%=:\n"
       " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
       " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ cplx lds_c(unsigned addr) {
+  cplx v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  return v;
 }
 // TMA tile load of a 3-D box at (c0, c1, c2) (c0 in doubles), completion on `bar`
 __device__ __forceinline__ void tma_load3(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
@@ -72,14 +81,16 @@ static __global__ void __launch_bounds__(PTHREADS, 1) zgemm_sub_tma(const __grid
                                                              const __grid_constant__ CUtensorMap mapB,
                                                              const __grid_constant__ CUtensorMap mapC,
                                                              SubGemmGeom g) {
-  extern __shared__ __align__(128) unsigned char psm_raw[];
-  unsigned char* psm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(psm_raw) + 127) & ~uintptr_t(127));
+  extern __shared__ __align__(1024) unsigned char psm_raw[];
+  // 1024-byte alignment for the swizzled A boxes, kept in the shared window
+  unsigned char* psm = psm_raw + ((1024u - (smem_u32(psm_raw) & 1023u)) & 1023u);
+  const unsigned psm_s = smem_u32(psm);
   uint64_t* bars = reinterpret_cast<uint64_t*>(psm + PSTAGES * P_STAGE_BYTES + P_C_BYTES);
   uint64_t* full = bars;
   uint64_t* empty = bars + PSTAGES;
   uint64_t* cfull = bars + 2 * PSTAGES;
   uint64_t* cempty = bars + 2 * PSTAGES + 1;
-  const cplx* Cs = reinterpret_cast<const cplx*>(psm + PSTAGES * P_STAGE_BYTES);
+  const unsigned Cs = psm_s + PSTAGES * P_STAGE_BYTES;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
     for (int s = 0; s < PSTAGES; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, PCONS); }
@@ -109,7 +120,9 @@ static __global__ void __launch_bounds__(PTHREADS, 1) zgemm_sub_tma(const __grid
           unsigned char* base = psm + stage * P_STAGE_BYTES;
           mbar_arrive_expect_tx(full + stage, P_STAGE_BYTES);
           const int k0 = ks * PBK;
-          tma_load3(base, &mapA, 2 * (g.a_col0 + k0), g.a_row0 + m0, b * g.a_bmul + g.a_badd, full + stage);
+          const int ab = b * g.a_bmul + g.a_badd;
+          tma_load3(base, &mapA, 2 * (g.a_col0 + k0), g.a_row0 + m0, ab, full + stage);
+          tma_load3(base + P_A_HALF, &mapA, 2 * (g.a_col0 + k0 + PAK), g.a_row0 + m0, ab, full + stage);
           tma_load3(base + P_A_BYTES, &mapB, 2 * (g.b_col0 + n0), g.b_row0 + k0, b, full + stage);
           if (++stage == PSTAGES) { stage = 0; phase ^= 1; }
         }
@@ -132,35 +145,46 @@ static __global__ void __launch_bounds__(PTHREADS, 1) zgemm_sub_tma(const __grid
       const int b = (int)(t / tiles_per_b);
       const int rem = (int)(t % tiles_per_b);
       const int m0 = (rem / g.tiles_n) * PBM, n0 = (rem % g.tiles_n) * PBN;
-      // four independent accumulator sets (re*re, im*im, re*im, im*re)
-      double arr[4][2][2], aii[4][2][2], ari[4][2][2], air[4][2][2];
+      // two accumulator sets per 8x8 block: re += ar br - ai bi, im += ar bi + ai br
+      // (16 independent chains per warp keep the DMMA pipe fed; 64 accumulator
+      // registers leave room under the 168-register cap of a 9-warp CTA)
+      double are[4][2][2], aim[4][2][2];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 2; ++j)
 #pragma unroll
-          for (int h = 0; h < 2; ++h) arr[i][j][h] = aii[i][j][h] = ari[i][j][h] = air[i][j][h] = 0.0;
+          for (int h = 0; h < 2; ++h) are[i][j][h] = aim[i][j][h] = 0.0;
       for (int ks = 0; ks < ksteps; ++ks) {
         mbar_wait(full + stage, phase);
-        const unsigned char* base = psm + stage * P_STAGE_BYTES;
-        const cplx* As = reinterpret_cast<const cplx*>(base);
-        const cplx* Bs = reinterpret_cast<const cplx*>(base + P_A_BYTES);
+        const unsigned As = psm_s + stage * P_STAGE_BYTES;
+        const unsigned Bs = As + P_A_BYTES;
 #pragma unroll
         for (int kk = 0; kk < PBK; kk += 4) {
           cplx af[4], bf[2];
 #pragma unroll
-          for (int j = 0; j < 2; ++j) bf[j] = Bs[(kk + (lane & 3)) * PBN + wn + j * 8 + (lane >> 2)];
+          for (int j = 0; j < 2; ++j) bf[j] = lds_c(Bs + ((kk + (lane & 3)) * PBN + wn + j * 8 + (lane >> 2)) * 16);
+          // A element (r, k): box k/8, row r (128 B), 16-B chunk (k%8) ^ (r%8)
+          const unsigned achunk = (((kk & 7) + (lane & 3)) ^ (lane >> 2)) << 4;
 #pragma unroll
-          for (int i = 0; i < 4; ++i) af[i] = As[(wm + i * 8 + (lane >> 2)) * PBK + kk + (lane & 3)];
+          for (int i = 0; i < 4; ++i)
+            af[i] = lds_c(As + (kk >> 3) * P_A_HALF + (wm + i * 8 + (lane >> 2)) * 128 + achunk);
 #pragma unroll
           for (int i = 0; i < 4; ++i)
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
-              dmma884(arr[i][j][0], arr[i][j][1], af[i].x, bf[j].x);
-              dmma884(aii[i][j][0], aii[i][j][1], af[i].y, bf[j].y);
-              dmma884(ari[i][j][0], ari[i][j][1], af[i].x, bf[j].y);
-              dmma884(air[i][j][0], air[i][j][1], af[i].y, bf[j].x);
+              dmma884(are[i][j][0], are[i][j][1], af[i].x, bf[j].x);
+              dmma884(aim[i][j][0], aim[i][j][1], af[i].x, bf[j].y);
             }
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const double nai = -af[i].y;
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              dmma884(are[i][j][0], are[i][j][1], nai, bf[j].y);
+              dmma884(aim[i][j][0], aim[i][j][1], af[i].y, bf[j].x);
+            }
+          }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(empty + stage);
@@ -184,10 +208,10 @@ static __global__ void __launch_bounds__(PTHREADS, 1) zgemm_sub_tma(const __grid
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               if (c + h < g.N) {
-                const double pr = arr[i][j][h] - aii[i][j][h], pi = ari[i][j][h] + air[i][j][h];
+                const double pr = are[i][j][h], pi = aim[i][j][h];
                 cplx outv;
                 if (g.beta) {
-                  const cplx v = Cs[rl * PBN + cl + h];
+                  const cplx v = lds_c(Cs + (rl * PBN + cl + h) * 16);
                   outv = cmk(v.x - pr, v.y - pi);
                 } else {
                   outv = cmk(pr, pi);
@@ -208,7 +232,7 @@ static __global__ void __launch_bounds__(PTHREADS, 1) zgemm_sub_tma(const __grid
 // float64 tensor {2*cols, rows, batch}, with a box of box_rows x box_cols
 // complex elements.  Out-of-range boxes are zero-filled by the hardware.
 static inline int encode_c128_map(CUtensorMap* map, const cplx* base, int cols, int rows, int batch, long long ld,
-                           long long bstride, int box_cols, int box_rows) {
+                           long long bstride, int box_cols, int box_rows, bool swizzle128 = false) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
@@ -224,19 +248,26 @@ static inline int encode_c128_map(CUtensorMap* map, const cplx* base, int cols, 
   cuuint32_t estr[3] = {1, 1, 1};
   cuuint32_t box[3] = {(cuuint32_t)(2 * box_cols), (cuuint32_t)box_rows, 1};
   CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<cplx*>(base), dims, strides, box, estr,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : (int)cudaErrorInvalidValue;
 }
 
-// Maps for the three operand roles: A (64 x 16 boxes), B (16 x 64), C (64 x 64).
+// A-operand map: 64 x 8 boxes with the 128-byte swizzle (two per K slice).
+static inline int encode_a_map(CUtensorMap* map, const cplx* base, int cols, int rows, int batch, long long ld,
+                               long long bstride) {
+  return encode_c128_map(map, base, cols, rows, batch, ld, bstride, PAK, PBM, true);
+}
+
+// Maps for the three operand roles: A (64 x 8 swizzled boxes), B (16 x 64), C (64 x 64).
 struct OperandMaps {
   CUtensorMap a, b, c;
 };
 using PencilMaps = OperandMaps;
 
 static inline int encode_pencil_maps(PencilMaps& pm, cplx* base, int n, long long ld, long long pstride, int batch) {
-  CIRR_TRY(encode_c128_map(&pm.a, base, n, n, batch, ld, pstride, PBK, PBM));
+  CIRR_TRY(encode_a_map(&pm.a, base, n, n, batch, ld, pstride));
   CIRR_TRY(encode_c128_map(&pm.b, base, n, n, batch, ld, pstride, PBN, PBK));
   CIRR_TRY(encode_c128_map(&pm.c, base, n, n, batch, ld, pstride, PBN, PBM));
   return 0;
