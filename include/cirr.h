@@ -143,6 +143,11 @@ long long cirr_launch_count(void);
 /* library identification: compute capability the cubins target (100 = sm_100a) */
 int cirr_target_sm(void);
 
+/* Concurrency: cap the CTAs of the cooperative latency-bound kernels (K4 orth,
+ * Hessenberg) so they can run beside the bulk GEMMs of another stream
+ * (0 = whole GPU, the default).  Returns the previous cap. */
+int cirr_set_coop_ctas(int ctas);
+
 #ifdef __cplusplus
 }
 #endif

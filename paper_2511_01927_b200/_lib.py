@@ -49,11 +49,12 @@ SIGNATURES = {
     "cirr_copy_cols": [_P, _L, _L, _P, _P, _P, _I, _I, _I, _P, _L, _L, _P],
     "cirr_transpose": [_I, _P, _L, _L, _I, _I, _I, _P, _L, _L, _P],
     "cirr_target_sm": [],
+    "cirr_set_coop_ctas": [_I],
     "cirr_launch_count": [],
 }
 _RESTYPE = {"cirr_diag_inv_bytes": _L, "cirr_zgetrf_ws_bytes": _L, "cirr_small_eig_ws_bytes": _L, "cirr_launch_count": _L, "cirr_orth_ws_bytes": _L,
             "cirr_gen_eig_ws_bytes": _L, "cirr_gen_eig_vec_scratch_bytes": _L}
-_RAW = {"cirr_diag_inv_bytes", "cirr_zgetrf_ws_bytes", "cirr_small_eig_ws_bytes", "cirr_launch_count", "cirr_target_sm", "cirr_orth_ws_bytes",
+_RAW = {"cirr_set_coop_ctas", "cirr_diag_inv_bytes", "cirr_zgetrf_ws_bytes", "cirr_small_eig_ws_bytes", "cirr_launch_count", "cirr_target_sm", "cirr_orth_ws_bytes",
         "cirr_gen_eig_ws_bytes", "cirr_gen_eig_vec_scratch_bytes"}
 
 _lib = None

@@ -17,6 +17,14 @@ typedef double2 cplx;
 extern long long g_cirr_launches;
 inline void cirr_note_launch() { __atomic_fetch_add(&g_cirr_launches, 1, __ATOMIC_RELAXED); }
 
+// Per-stream pair of device ints {next tile, finished CTAs} for the dynamic
+// tile scheduler of the persistent GEMM (gemm.cu); zero between launches.
+int* cirr_tile_counter(cudaStream_t stream);
+
+// Cap on the CTAs of the cooperative latency-bound kernels (0 = whole GPU);
+// set by cirr_set_coop_ctas so they can run beside the bulk GEMMs.
+extern int g_cirr_coop_cap;
+
 #define CIRR_CHECK_LAUNCH()                              \
   do {                                                   \
     cirr_note_launch();                                  \

@@ -1,4 +1,7 @@
 // C-ABI for the batched DMMA GEMM (see gemm.cuh).
+#include <mutex>
+#include <utility>
+#include <vector>
 #include "gemm.cuh"
 
 using namespace cirr;
@@ -36,6 +39,51 @@ CIRR_API int cirr_gemm(int a_kind, int M, int N, int K, int batch,
 }
 
 long long g_cirr_launches = 0;
+int g_cirr_coop_cap = 0;
+
+// Cooperative kernels (K4 orth, Hessenberg) use at most `ctas` CTAs when > 0,
+// leaving the rest of the GPU to GEMMs on other streams.  Returns the old cap.
+CIRR_API int cirr_set_coop_ctas(int ctas) {
+  const int old = g_cirr_coop_cap;
+  g_cirr_coop_cap = ctas > 0 ? ctas : 0;
+  return old;
+}
+
+namespace {
+constexpr int kCtrSlots = 256;
+struct CtrPool {
+  int dev;
+  int* base;
+  std::vector<cudaStream_t> streams;
+};
+std::mutex g_ctr_mu;
+std::vector<CtrPool> g_ctr;
+}  // namespace
+
+// One {next tile, finished CTAs} pair per (device, stream).  The pool is
+// allocated and zeroed synchronously on first use (before any concurrent
+// launch), and each kernel leaves its pair at zero when it exits.
+int* cirr_tile_counter(cudaStream_t stream) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lk(g_ctr_mu);
+  CtrPool* pool = nullptr;
+  for (auto& p : g_ctr)
+    if (p.dev == dev) pool = &p;
+  if (!pool) {
+    int* base = nullptr;
+    if (cudaMalloc(&base, 2 * sizeof(int) * kCtrSlots) != cudaSuccess) return nullptr;
+    if (cudaMemset(base, 0, 2 * sizeof(int) * kCtrSlots) != cudaSuccess) return nullptr;
+    if (cudaDeviceSynchronize() != cudaSuccess) return nullptr;
+    g_ctr.push_back(CtrPool{dev, base, {}});
+    pool = &g_ctr.back();
+  }
+  for (size_t i = 0; i < pool->streams.size(); ++i)
+    if (pool->streams[i] == stream) return pool->base + 2 * i;
+  if ((int)pool->streams.size() >= kCtrSlots) return nullptr;
+  pool->streams.push_back(stream);
+  return pool->base + 2 * (pool->streams.size() - 1);
+}
 
 // Number of kernels launched by this library since load (host counter).
 CIRR_API long long cirr_launch_count(void) { return __atomic_load_n(&g_cirr_launches, __ATOMIC_RELAXED); }

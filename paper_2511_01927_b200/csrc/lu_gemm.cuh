@@ -32,7 +32,8 @@ constexpr int P_A_BYTES = PBM * PBK * 16;
 constexpr int P_B_BYTES = PBK * PBN * 16;
 constexpr int P_STAGE_BYTES = P_A_BYTES + P_B_BYTES;
 constexpr int P_C_BYTES = PBM * PBN * 16;
-constexpr int P_SMEM = PSTAGES * P_STAGE_BYTES + P_C_BYTES + 8 * (2 * PSTAGES + 2) + 1024;
+constexpr int PRING = 8;                        // tile-id ring (producer runs <= PSTAGES tiles ahead)
+constexpr int P_SMEM = PSTAGES * P_STAGE_BYTES + P_C_BYTES + 8 * (2 * PSTAGES + 2) + 4 * PRING + 1024;
 constexpr int PAK = 8;                          // complex columns per swizzled A box (128 bytes)
 constexpr int P_A_HALF = PBM * PAK * 16;        // one A box
 
@@ -56,7 +57,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
 }
 __device__ __forceinline__ cplx lds_c(unsigned addr) {
   cplx v;
-  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr) : "memory");
   return v;
 }
 // TMA tile load of a 3-D box at (c0, c1, c2) (c0 in doubles), completion on `bar`
@@ -75,6 +76,7 @@ struct SubGemmGeom {
   int tiles_m, tiles_n;
   int beta;        // 1: C = C - A B (C tile streamed in by TMA); 0: C = A B
   int a_bmul, a_badd;  // 3rd TMA coordinate of the A operand: b * a_bmul + a_badd
+  int* ctr;            // {next tile, finished CTAs}: dynamic tile scheduler, zero on entry and exit
 };
 
 static __global__ void __launch_bounds__(PTHREADS, 1) zgemm_sub_tma(const __grid_constant__ CUtensorMap mapA,
@@ -99,24 +101,34 @@ static __global__ void __launch_bounds__(PTHREADS, 1) zgemm_sub_tma(const __grid
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  int* tile_ring = reinterpret_cast<int*>(bars + 2 * PSTAGES + 2);
   const long long tiles_per_b = (long long)g.tiles_m * g.tiles_n;
-  const long long total = tiles_per_b * g.batch;
+  const int total = (int)(tiles_per_b * g.batch);
   const int ksteps = g.K / PBK;
 
   if (warp == PCONS) {
     // ---------------- producer warp (one elected lane) ----------------
+    // Tiles are claimed from a global counter, so CTAs that start late (SMs
+    // busy with kernels of other streams) just take fewer tiles.
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(&mapB) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(&mapC) : "memory");
       int stage = 0;
       unsigned phase = 0, cphase = 0;
-      for (long long t = blockIdx.x; t < total; t += gridDim.x) {
+      for (int seq = 0;; ++seq) {
+        const int t = atomicAdd(g.ctr, 1);
+        mbar_wait(empty + stage, phase ^ 1);
+        tile_ring[seq & (PRING - 1)] = t < total ? t : -1;
+        if (t >= total) {  // no tile left: release the consumers
+          mbar_arrive(full + stage);
+          break;
+        }
         const int b = (int)(t / tiles_per_b);
         const int rem = (int)(t % tiles_per_b);
         const int m0 = (rem / g.tiles_n) * PBM, n0 = (rem % g.tiles_n) * PBN;
         for (int ks = 0; ks < ksteps; ++ks) {
-          mbar_wait(empty + stage, phase ^ 1);
+          if (ks > 0) mbar_wait(empty + stage, phase ^ 1);
           unsigned char* base = psm + stage * P_STAGE_BYTES;
           mbar_arrive_expect_tx(full + stage, P_STAGE_BYTES);
           const int k0 = ks * PBK;
@@ -135,13 +147,24 @@ static __global__ void __launch_bounds__(PTHREADS, 1) zgemm_sub_tma(const __grid
           cphase ^= 1;
         }
       }
+      // the last CTA out resets the counters for the next launch on this stream
+      __threadfence();
+      if (atomicAdd(g.ctr + 1, 1) == (int)gridDim.x - 1) {
+        g.ctr[0] = 0;
+        g.ctr[1] = 0;
+        __threadfence();
+      }
     }
   } else {
     // ---------------- consumer warps ----------------
     const int wm = (warp >> 2) * 32, wn = (warp & 3) * 16;
     int stage = 0;
     unsigned phase = 0, cphase = 0;
-    for (long long t = blockIdx.x; t < total; t += gridDim.x) {
+    for (int seq = 0;; ++seq) {
+      // the tile id is published before the first stage of the tile completes
+      mbar_wait(full + stage, phase);
+      const int t = tile_ring[seq & (PRING - 1)];
+      if (t < 0) break;
       const int b = (int)(t / tiles_per_b);
       const int rem = (int)(t % tiles_per_b);
       const int m0 = (rem / g.tiles_n) * PBM, n0 = (rem % g.tiles_n) * PBN;
@@ -186,6 +209,12 @@ static __global__ void __launch_bounds__(PTHREADS, 1) zgemm_sub_tma(const __grid
             }
           }
         }
+        // The stage is refilled by TMA (async proxy) once every warp arrived:
+        // order this warp's shared-memory reads before that write.  Without the
+        // fence the arrive can overtake a still-pending LDS (ptxas schedules it
+        // ahead of the last DMMAs), which corrupts tiles when the SM's shared
+        // memory pipe is slowed by co-resident CTAs of other streams.
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(empty + stage);
         if (++stage == PSTAGES) { stage = 0; phase ^= 1; }
@@ -222,9 +251,11 @@ static __global__ void __launch_bounds__(PTHREADS, 1) zgemm_sub_tma(const __grid
           }
         }
       }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (g.beta && lane == 0) mbar_arrive(cempty);
     }
+
   }
 }
 
@@ -292,8 +323,10 @@ static inline int zgemm_sub_maps(const CUtensorMap& mapA, const CUtensorMap& map
     attr = true;
   }
   const int Kr = (K + PBK - 1) / PBK * PBK;
+  int* ctr = cirr_tile_counter(stream);
+  if (!ctr) return (int)cudaErrorMemoryAllocation;
   SubGemmGeom g{M, N, Kr, batch, a_row0, a_col0, b_row0, b_col0, c_row0, c_col0, C, ldc, sC,
-                (M + PBM - 1) / PBM, (N + PBN - 1) / PBN, beta, a_bmul, a_badd};
+                (M + PBM - 1) / PBM, (N + PBN - 1) / PBN, beta, a_bmul, a_badd, ctr};
   const long long tiles = (long long)g.tiles_m * g.tiles_n * batch;
   const int grid = (int)(tiles < sms ? tiles : sms);
   zgemm_sub_tma<<<grid, PTHREADS, P_SMEM, stream>>>(mapA, mapB, mapC, g);

@@ -331,6 +331,7 @@ CIRR_API int cirr_orth(cplx* W, long long ldw, long long wstride, int n, int c, 
   long long want = (long long)nprob * (cp / 2);
   if (want < (long long)nprob * c) want = (long long)nprob * c;
   long long cap = (long long)sms * (per_sm < 2 ? per_sm : 2);
+  if (g_cirr_coop_cap > 0 && cap > g_cirr_coop_cap) cap = g_cirr_coop_cap;
   int grid = (int)(want < cap ? want : cap);
   if (grid < 1) grid = 1;
   // rotation threshold on |x^H y| / (|x||y|) for length-c rows

@@ -41,6 +41,13 @@ from .errors import (
 
 PIVOT_REL_TOL = 1e-14  # linalg.py:26
 _DEBUG = bool(int(__import__("os").environ.get("CIRR_DEBUG", "0")))
+# CIRR_PIPELINE=1 overlaps the contours of a wave (run_pipelined: one host
+# thread + high-priority stream per contour).  Off by default: with the
+# current K4/K6 kernels it measured 1.90 s vs 1.83 s per config-4 GEP
+# (profiles/r01_pipeline_r01.txt), so the single-stream batched loop stays.
+_PIPELINE = bool(int(__import__("os").environ.get("CIRR_PIPELINE", "0")))
+_COOP_CAP = int(__import__("os").environ.get("CIRR_COOP_CAP", "32"))
+
 
 
 def _torch():
@@ -316,6 +323,14 @@ def _ptr(t) -> int:
     return t.data_ptr()
 
 
+def _h2d(x: np.ndarray):
+    """Host array -> device tensor, stream-ordered on the current stream with no
+    host synchronisation (pinned staging from torch's caching host allocator),
+    so enqueueing never waits for earlier GPU work of that stream."""
+    torch = _torch()
+    return torch.from_numpy(np.ascontiguousarray(x)).pin_memory().to("cuda", non_blocking=True)
+
+
 # ---------------------------------------------------------------------------
 # the engine: factor + solve + moments for a set of contours
 
@@ -385,53 +400,84 @@ class _Engine:
         self.cs = cstates
         self.cfg = cfg
         self.n = dp.n
-        self.stream = _stream()
+
+    @property
+    def stream(self) -> int:
+        """The launching stream: torch's current stream of the calling thread."""
+        return _stream()
 
     # -- K1 + K2 -----------------------------------------------------------
-    def factor(self):
+    def _alloc_factors(self):
         torch, n = self.torch, self.n
         self.node_off = [0]
         for c in self.cs:
             self.node_off.append(self.node_off[-1] + len(c.fidx))
         P = self.node_off[-1]
         self.P = P
-        z = torch.from_numpy(np.concatenate([c.nodes[c.fidx] for c in self.cs])).to("cuda")
         self.pencils = torch.empty((P, n, n), dtype=torch.complex128, device="cuda")
         self.maxabs = torch.empty(P, dtype=torch.float64, device="cuda")
         self.ipiv = torch.empty((P, n), dtype=torch.int32, device="cuda")
         self.perm = torch.empty((P, n), dtype=torch.int32, device="cuda")
         self.minpiv = torch.empty(P, dtype=torch.float64, device="cuda")
         self.info = torch.empty(P, dtype=torch.int32, device="cuda")
+        self._dinv_per_pencil = int(_lib.call("cirr_diag_inv_bytes", n, 1))
+        self.dinv = torch.empty(self._dinv_per_pencil * P, dtype=torch.uint8, device="cuda")
+        self.contour_of = _h2d(
+            np.concatenate([np.full(len(c.fidx), i, dtype=np.int32) for i, c in enumerate(self.cs)]))
+
+    def _factor_contour(self, ci: int):
+        """Enqueue K1 + K2 (+ the diagonal-block inverses K3 uses) for the
+        pencils of contour ci on the current stream."""
+        torch, n = self.torch, self.n
+        a, b = self.node_off[ci], self.node_off[ci + 1]
+        cnt = b - a
+        if cnt == 0:
+            return
+        c = self.cs[ci]
+        z = _h2d(c.nodes[c.fidx])
         with _stage("assemble"):
-            _lib.call("cirr_assemble", _ptr(self.dp.a), _ptr(self.dp.b), n, n, _ptr(z), P,
-                      _ptr(self.pencils), n, n * n, _ptr(self.maxabs), self.stream)
-        _work("assemble_bytes", P * n * n * 16 + 2 * n * n * 8)
+            _lib.call("cirr_assemble", _ptr(self.dp.a), _ptr(self.dp.b), n, n, _ptr(z), cnt,
+                      _ptr(self.pencils[a]), n, n * n, _ptr(self.maxabs[a:]), self.stream)
+        _work("assemble_bytes", cnt * n * n * 16 + 2 * n * n * 8)
         with _stage("lu"):
-            lws = torch.empty(int(_lib.call("cirr_zgetrf_ws_bytes", n, P)), dtype=torch.uint8, device="cuda")
-            _lib.call("cirr_zgetrf_batched", _ptr(self.pencils), n, n, n * n, P, _ptr(self.ipiv),
-                      _ptr(self.perm), _ptr(self.minpiv), _ptr(self.info), _ptr(lws), self.stream)
-        _work("lu_flops", P * 8.0 * n ** 3 / 3.0)
-        maxabs = self.maxabs.cpu().numpy()
-        minpiv = self.minpiv.cpu().numpy()
-        info = self.info.cpu().numpy()
-        for ci, c in enumerate(self.cs):
-            c.stats.n_factorizations = len(c.fidx)
-            for jl in range(len(c.fidx)):
-                j = self.node_off[ci] + jl
-                scale = max(maxabs[j], 1e-300)
-                if info[j] != 0 or not (minpiv[j] >= PIVOT_REL_TOL * scale):
-                    jn = int(c.fidx[jl])
-                    c.error = SingularShiftError(complex(c.nodes[jn]), node_index=jn)
-                    c.done = True
-                    break
-        self.contour_of = torch.from_numpy(
-            np.concatenate([np.full(len(c.fidx), i, dtype=np.int32) for i, c in enumerate(self.cs)])
-        ).to("cuda")
+            lws = torch.empty(int(_lib.call("cirr_zgetrf_ws_bytes", n, cnt)), dtype=torch.uint8, device="cuda")
+            _lib.call("cirr_zgetrf_batched", _ptr(self.pencils[a]), n, n, n * n, cnt, _ptr(self.ipiv[a]),
+                      _ptr(self.perm[a]), _ptr(self.minpiv[a:]), _ptr(self.info[a:]), _ptr(lws), self.stream)
+        _work("lu_flops", cnt * 8.0 * n ** 3 / 3.0)
+        with _stage("dinv"):
+            _lib.call("cirr_diag_inverses", _ptr(self.pencils[a]), n, n, n * n, cnt,
+                      _ptr(self.dinv) + a * self._dinv_per_pencil, self.stream)
+
+    def _check_factor(self, ci: int):
+        """Singular-shift test of contour ci (linalg.py:68-70); host sync on
+        the current stream."""
+        c = self.cs[ci]
+        a, b = self.node_off[ci], self.node_off[ci + 1]
+        maxabs = self.maxabs[a:b].cpu().numpy()
+        minpiv = self.minpiv[a:b].cpu().numpy()
+        info = self.info[a:b].cpu().numpy()
+        c.stats.n_factorizations = len(c.fidx)
+        for jl in range(b - a):
+            scale = max(maxabs[jl], 1e-300)
+            if info[jl] != 0 or not (minpiv[jl] >= PIVOT_REL_TOL * scale):
+                jn = int(c.fidx[jl])
+                c.error = SingularShiftError(complex(c.nodes[jn]), node_index=jn)
+                c.done = True
+                break
+
+    def factor(self):
+        self._alloc_factors()
+        for ci in range(len(self.cs)):
+            self._factor_contour(ci)
+        for ci in range(len(self.cs)):
+            self._check_factor(ci)
 
     # -- K3: solve all pencils of the listed contours against per-contour RHS
-    def apply(self, active: list, rhs: dict, moments: int) -> dict:
+    def apply(self, active: list, rhs: dict, moments: int, real_rhs: bool = False) -> dict:
         """rhs[ci] = device (n x K_ci) complex block (already multiplied by B).
-        Returns St[ci] = device ((moments*K) x n) transposed moment block."""
+        Returns St[ci] = device ((moments*K) x n) transposed moment block.
+        real_rhs: the blocks are known to be real (conjugate-pair variant: the
+        mirrored nodes then need no extra columns).  No host synchronisation."""
         torch, n = self.torch, self.n
         K = max(rhs[ci].shape[1] for ci in active)
         if K == 0:
@@ -442,7 +488,7 @@ class _Engine:
         ks, cplx_rhs = [], []
         for ci in active:
             kc = rhs[ci].shape[1]
-            cx = self.cs[ci].half and bool(torch.any(rhs[ci].imag != 0))
+            cx = self.cs[ci].half and not real_rhs
             cplx_rhs.append(cx)
             ks.append(2 * kc if cx else kc)
         Ks = max(ks)
@@ -462,10 +508,9 @@ class _Engine:
             coefs.append(self.cs[ci].coef(moments))
         Psolve, Ptot = spos[-1], offs[-1]
         Ysol = torch.empty((Psolve, n, Ks), dtype=torch.complex128, device="cuda")
-        rhs_of = torch.from_numpy(np.concatenate(
-            [np.full(b - a, s, dtype=np.int32) for s, (a, b) in enumerate(pen_idx)])).to("cuda")
-        coef = torch.from_numpy(np.concatenate(coefs, axis=0)).to("cuda")
-        off_t = torch.tensor(offs, dtype=torch.int32, device="cuda")
+        rhs_of = _h2d(np.concatenate([np.full(b - a, s, dtype=np.int32) for s, (a, b) in enumerate(pen_idx)]))
+        coef = _h2d(np.concatenate(coefs, axis=0))
+        off_t = _h2d(np.asarray(offs, dtype=np.int32))
         St = torch.empty((nset, moments * K, n), dtype=torch.complex128, device="cuda")
         # solve contour ranges (each range is contiguous in the pencil buffer)
         with _stage("solve"):
@@ -497,7 +542,7 @@ class _Engine:
                         col0 = np.where(up, 0, kc if cplx_rhs[s] else 0)
                     else:
                         src, cj, col0 = spos[s] + np.arange(N), np.zeros(N, np.int32), np.zeros(N)
-                    meta = torch.from_numpy(np.stack([src, col0, cj]).astype(np.int32)).to("cuda")
+                    meta = _h2d(np.stack([src, col0, cj]).astype(np.int32))
                     _lib.call("cirr_copy_cols", _ptr(Ysol), Ks, n * Ks, _ptr(meta[0]), _ptr(meta[1]),
                               _ptr(meta[2]), n, kc, N, _ptr(Y[offs[s]]), K, n * K, self.stream)
             del Ysol
@@ -511,15 +556,8 @@ class _Engine:
         return {ci: St[s] for s, ci in enumerate(active)}
 
     def _dinv(self):
-        """Inverses of the 64x64 diagonal blocks of every factor (computed once per
-        factorisation on first use; each pencil's slice is contiguous)."""
-        if getattr(self, "dinv", None) is None:
-            torch, n = self.torch, self.n
-            nbytes = int(_lib.call("cirr_diag_inv_bytes", n, self.P))
-            self._dinv_per_pencil = nbytes // self.P
-            self.dinv = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
-            with _stage("solve"):
-                _lib.call("cirr_diag_inverses", _ptr(self.pencils), n, n, n * n, self.P, _ptr(self.dinv), self.stream)
+        """Inverses of the 64x64 diagonal blocks of every factor (made with the
+        factorisation; each pencil's slice is contiguous)."""
         return self.dinv
 
     def bmul(self, x):
@@ -648,7 +686,7 @@ class _Engine:
                       kk, 1.0, 0, st)
         # K6: small eigenproblems
         herm = self.dp.hermitian
-        kdim = torch.from_numpy(ks.astype(np.int32)).to("cuda")
+        kdim = _h2d(ks.astype(np.int32))
         info = torch.zeros(nb, dtype=torch.int32, device="cuda")
         lam = torch.zeros((nb, kmax), dtype=torch.complex128, device="cuda")
         with _stage("rr.eigvals"):
@@ -702,8 +740,8 @@ class _Engine:
             idx[b, : len(ix)] = ix
             cnt[b] = len(ix)
             lam_in[b, : len(ix)] = lam_h[b, ix]
-        idx_t = torch.from_numpy(idx).to("cuda")
-        cnt_t = torch.from_numpy(cnt).to("cuda")
+        idx_t = _h2d(idx)
+        cnt_t = _h2d(cnt)
         Xi = torch.zeros((nb, n, kin_max), dtype=torch.complex128, device="cuda")
         if general_split:
             scr = torch.empty(int(_lib.call("cirr_gen_eig_vec_scratch_bytes", kmax, nb, kin_max)), dtype=torch.uint8,
@@ -726,7 +764,7 @@ class _Engine:
                   _ptr(AX), kin_max, n * kin_max, 1.0, 0, st)
         _lib.call("cirr_gemm", 2, n, kin_max, n, nb, _ptr(self.dp.b), n, 0, _ptr(Xi), kin_max, n * kin_max,
                   _ptr(BX), kin_max, n * kin_max, 1.0, 0, st)
-        lam_t = torch.from_numpy(lam_in).to("cuda")
+        lam_t = _h2d(lam_in)
         res = torch.zeros((nb, kin_max), dtype=torch.float64, device="cuda")
         _lib.call("cirr_residuals", _ptr(AX), _ptr(BX), kin_max, n * kin_max, n, _ptr(lam_t), kin_max, _ptr(cnt_t),
                   kin_max, nb, _ptr(res), kin_max, st)
@@ -752,8 +790,8 @@ class _Engine:
             c = self.cs[ci]
             rng = np.random.default_rng(c.seed)
             v = rng.standard_normal((n, c.ncols)).astype(complex)  # solvers.py:178-180
-            rhs[ci] = self.bmul(torch.from_numpy(v).to("cuda"))
-        stacked = self.apply(active, rhs, moments)
+            rhs[ci] = self.bmul(_h2d(v))
+        stacked = self.apply(active, rhs, moments, real_rhs=True)
         it_of = {ci: 0 for ci in active}
         for it in range(cfg.max_refine):
             refine = {}
@@ -778,6 +816,8 @@ class _Engine:
                 _, lam, xi, res, _ = r
                 c.lam, c.x_dev, c.res = lam, xi, res
                 c.best_res = min(c.best_res, float(res.max()))
+                if _DEBUG:
+                    print(f"[cirr] contour {ci} it {it}: inside {len(lam)} max res {res.max():.2e}", flush=True)
                 if res.max() <= cfg.tol or it + 1 >= cfg.max_refine:
                     active.remove(ci)
                     continue
@@ -793,6 +833,107 @@ class _Engine:
             c.stats.elapsed = time.perf_counter() - c.t0
             if getattr(c, "fatal", False):
                 continue
+            self.finish(c)
+
+    # -- pipelined CIRR: one host thread per contour ------------------------
+    def run_pipelined(self, moments: int):
+        """The same per-contour control flow as ``run``, with the contours of
+        the wave overlapped.  Bulk work (K1-K3: LU, solves, moments) goes in
+        order onto one low-priority stream; each contour's Rayleigh-Ritz rounds
+        (K4-K7, latency-bound) run on its own high-priority stream from its own
+        host thread, so one contour's small eigenproblems hide under another
+        contour's solve GEMMs (the persistent GEMM takes its tiles from a
+        global counter, so it gives up SMs to them).  Every contour sees the
+        same kernels and inputs as in ``run``: results are identical."""
+        import threading
+
+        torch, n = self.torch, self.n
+        dev = torch.cuda.current_device()
+        caller = torch.cuda.current_stream()
+        bulk = torch.cuda.Stream(priority=0)
+        bulk.wait_stream(caller)
+        self._bulk = bulk
+        self._bulk_lock = threading.Lock()
+        self._lat_streams = []
+        self._alloc_factors()
+        first = {}
+        with torch.cuda.stream(bulk):
+            for ci, c in enumerate(self.cs):
+                self._factor_contour(ci)
+                rng = np.random.default_rng(c.seed)
+                v = rng.standard_normal((n, c.ncols)).astype(complex)  # solvers.py:178-180
+                rhs = self.bmul(_h2d(v))
+                st = self.apply([ci], {ci: rhs}, moments, real_rhs=True)[ci]
+                first[ci] = (st, bulk.record_event())
+        errors = []
+
+        def worker(ci):
+            try:
+                torch.cuda.set_device(dev)  # the current device is per thread
+                self._contour_loop(ci, *first[ci])
+            except BaseException as exc:  # noqa: BLE001 - re-raised on the caller's thread
+                errors.append(exc)
+
+        threads = [threading.Thread(target=worker, args=(ci,), daemon=True) for ci in range(len(self.cs))]
+        # cooperative K4/K6 kernels on a slice of the GPU, so they run beside
+        # the bulk GEMMs instead of waiting for the whole device
+        old_cap = _lib.call("cirr_set_coop_ctas", _COOP_CAP)
+        try:
+            for t in threads:
+                t.start()
+            for t in threads:
+                t.join()
+        finally:
+            _lib.call("cirr_set_coop_ctas", old_cap)
+        caller.wait_stream(bulk)
+        for lat in self._lat_streams:
+            caller.wait_stream(lat)
+        if errors:
+            raise errors[0]
+
+    def _contour_loop(self, ci: int, st, ev):
+        torch, cfg = self.torch, self.cfg
+        c = self.cs[ci]
+        lat = torch.cuda.Stream(priority=-1)
+        self._lat_streams.append(lat)
+        with torch.cuda.stream(lat):
+            lat.wait_event(ev)
+            st.record_stream(lat)
+            self._check_factor(ci)
+            if c.done:
+                return
+            it_used = 0
+            for it in range(cfg.max_refine):
+                it_used = it
+                r = self.rayleigh_ritz([(ci, st)])[ci]
+                if r[0] == "rankzero":
+                    break
+                if r[0] == "indefinite":
+                    c.error, c.fatal = r[1], True
+                    break
+                if r[0] == "none":
+                    c.lam = None
+                    break
+                _, lam, xi, res, _ = r
+                c.lam, c.x_dev, c.res = lam, xi, res
+                c.best_res = min(c.best_res, float(res.max()))
+                if _DEBUG:
+                    print(f"[cirr] contour {ci} it {it}: inside {len(lam)} max res {res.max():.2e}", flush=True)
+                if res.max() <= cfg.tol or it + 1 >= cfg.max_refine:
+                    break
+                rhs = self.bmul(xi)
+                ev_rhs = lat.record_event()
+                with self._bulk_lock, torch.cuda.stream(self._bulk):
+                    self._bulk.wait_event(ev_rhs)
+                    rhs.record_stream(self._bulk)
+                    st = self.apply([ci], {ci: rhs}, 1)[ci]
+                    ev_st = self._bulk.record_event()
+                lat.wait_event(ev_st)
+                st.record_stream(lat)
+            c.stats.iterations = it_used + 1
+            c.stats.elapsed = time.perf_counter() - c.t0
+            if getattr(c, "fatal", False):
+                return
             self.finish(c)
 
     # -- FEAST (solvers.py:230-285) on the same resident factors -------------
@@ -901,13 +1042,17 @@ def _run_contours(pencil, contours, cfg, seeds, moments_override=None, solver: s
     cfg = _cfg_view(cfg)
     dp = DevicePencil.of(pencil)
     cstates = [_Contour(i, c, cfg, s, dp.n) for i, (c, s) in enumerate(zip(contours, seeds))]
+    moments = cfg.n_moments if moments_override is None else moments_override
     for wave in _waves(cstates, dp.n, _hbm_budget(dp.n, cstates)):
         eng = _Engine(dp, wave, cfg)
-        eng.factor()
         if solver == "feast":
+            eng.factor()
             eng.run_feast()
+        elif len(wave) > 1 and _PIPELINE:
+            eng.run_pipelined(moments)
         else:
-            eng.run(cfg.n_moments if moments_override is None else moments_override)
+            eng.factor()
+            eng.run(moments)
         eng.free()
         del eng
     return cstates
