@@ -1,7 +1,7 @@
 // K2: batched blocked complex128 LU with partial pivoting (P M = L U).
 //
 // Replaces linalg.py:55-71 (`spla.splu` on z*B - A + the pivot test).  Per
-// panel step k (width NB): panel_kernel factors the m x NB panel in place
+// panel step k (width NB): panel2_kernel factors the m x NB panel in place
 // (one CTA per pencil; IB-wide sub-panels with a block-argmax pivot search,
 // then a TRSM+GEMM update of the rest of the panel), swap_kernel applies the
 // panel's interchanges outside it, trsm_kernel forms U12 = L11^-1 A12, and the
@@ -17,139 +17,171 @@ namespace {
 
 constexpr int NB = 64;      // panel width
 constexpr int IB = 8;       // sub-panel width inside the panel kernel
-constexpr int PT = 512;     // panel kernel threads
 
-__global__ void __launch_bounds__(PT) panel_kernel(cplx* __restrict__ P, int n, long long ld,
-                                                   long long pstride, int k, int jb,
-                                                   int* __restrict__ ipiv, double* __restrict__ minpiv,
-                                                   int* __restrict__ info) {
-  __shared__ double rv[PT / 32];
-  __shared__ int ri[PT / 32];
-  __shared__ cplx prow[NB];           // pivot row segment of the sub-panel
-  __shared__ cplx ublk[IB][NB];       // U block for the panel-rest update
-  __shared__ int s_piv;
-  __shared__ cplx s_pval;
+// Panel factorisation (one CTA per pencil factors the m x 64 panel in 8-column
+// sub-panels; LAPACK zgetf2 arithmetic and pivoting).  Every pass over the panel
+// is coalesced along rows: the 8-column sub-panel update maps 8 lanes to one
+// row (128 contiguous bytes), the update of the columns right of the
+// sub-panel maps 16 lanes to one row, and the pivot search of column c+1 is
+// fused into the pass that updates it (argmax of |re|+|im|, first index on
+// ties, as LAPACK izamax).  Only the first column of a panel needs a strided
+// search.  The first version issued one 16-byte load per thread per row, which
+// made the L1 tag stage the limit (82 % L1/TEX throughput in ncu; the first
+// version of this kernel, replaced in round 1).
+constexpr int PT2 = 512;
+
+__device__ __forceinline__ void arg_better(double& best, int& bi, double ov, int oi) {
+  if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+}
+
+// CTA-wide argmax of (best, bi); result valid in every thread.
+template <int PW2>
+__device__ __forceinline__ int block_argmax(double best, int bi, double* rv, int* ri) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+    arg_better(best, bi, __shfl_xor_sync(0xffffffffu, best, o), __shfl_xor_sync(0xffffffffu, bi, o));
+  if (lane == 0) { rv[wid] = best; ri[wid] = bi; }
+  __syncthreads();
+  best = lane < PW2 ? rv[lane] : -1.0;
+  bi = lane < PW2 ? ri[lane] : 0x7fffffff;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+    arg_better(best, bi, __shfl_xor_sync(0xffffffffu, best, o), __shfl_xor_sync(0xffffffffu, bi, o));
+  return bi;
+}
+
+template <int PTT>
+__global__ void __launch_bounds__(PTT) panel2_kernel(cplx* __restrict__ P, int n, long long ld, long long pstride,
+                                                     int k, int jb, int* __restrict__ ipiv,
+                                                     double* __restrict__ minpiv, int* __restrict__ info) {
+  constexpr int PW2 = PTT / 32;
+  __shared__ double rv[PW2];
+  __shared__ int ri[PW2];
+  __shared__ cplx prow[NB];       // pivot row over the panel columns (after the swap)
+  __shared__ cplx ublk[IB][NB];   // U rows of the sub-panel, for the rest update
   cplx* A = P + (long long)blockIdx.x * pstride;
   int* piv = ipiv + (long long)blockIdx.x * n;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   double mp = minpiv[blockIdx.x];
   int inf = info[blockIdx.x];
+  // candidate for the next pivot column: strided search of column k once per panel
+  double best = -1.0;
+  int bi = 0x7fffffff;
+  for (int r = k + tid; r < n; r += PTT) arg_better(best, bi, cabs1(A[(long long)r * ld + k]), r);
 
   for (int c0 = 0; c0 < jb; c0 += IB) {
     const int ib = min(IB, jb - c0);
     for (int c = c0; c < c0 + ib; ++c) {
-      const int col = k + c, row0 = k + c;
-      // 1. pivot search (|re| + |im|, first maximal index)
-      double best = -1.0;
-      int bi = row0;
-      for (int r = row0 + tid; r < n; r += PT) {
-        double v = cabs1(A[(long long)r * ld + col]);
-        if (v > best) { best = v; bi = r; }
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        double ov = __shfl_xor_sync(0xffffffffu, best, o);
-        int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
-      }
-      if (lane == 0) { rv[wid] = best; ri[wid] = bi; }
-      __syncthreads();
-      if (wid == 0) {
-        best = lane < PT / 32 ? rv[lane] : -1.0;
-        bi = lane < PT / 32 ? ri[lane] : n;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          double ov = __shfl_xor_sync(0xffffffffu, best, o);
-          int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-          if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
-        }
-        if (lane == 0) {
-          s_piv = bi;
-          piv[row0] = bi;
-          s_pval = A[(long long)bi * ld + col];
-        }
-      }
-      __syncthreads();
-      const int p = s_piv;
-      const cplx pv = s_pval;
-      // 2. swap rows row0 <-> p over the whole panel width
-      if (p != row0) {
-        for (int cc = tid; cc < jb; cc += PT) {
-          cplx* x = A + (long long)row0 * ld + k + cc;
+      const int row0 = k + c;
+      int p = block_argmax<PW2>(best, bi, rv, ri);
+      if (p >= n) p = row0;  // empty candidate set cannot happen for row0 < n; keep LAPACK-safe
+      if (tid == 0) piv[row0] = p;
+      // swap rows row0 <-> p over the panel width; prow = the new row0
+      for (int cc = tid; cc < jb; cc += PTT) {
+        cplx* x = A + (long long)row0 * ld + k + cc;
+        const cplx xv = *x;
+        if (p != row0) {
           cplx* y = A + (long long)p * ld + k + cc;
-          cplx t = *x; *x = *y; *y = t;
+          const cplx yv = *y;
+          *x = yv;
+          *y = xv;
+          prow[cc] = yv;
+        } else {
+          prow[cc] = xv;
         }
       }
       __syncthreads();
-      // pivot row of the sub-panel (after the swap) to shared memory
-      for (int cc = tid; cc < c0 + ib - c; cc += PT) prow[cc] = A[(long long)row0 * ld + col + cc];
+      const cplx pv = prow[c];
       if (tid == 0) {
-        double a = cabs(pv);
+        const double a = cabs(pv);
         mp = fmin(mp, a);
         if (a == 0.0 && inf == 0) inf = row0 + 1;
       }
-      __syncthreads();
-      // 3. scale + rank-1 update inside the sub-panel
       const bool nz = (pv.x != 0.0 || pv.y != 0.0);
       const cplx rp = nz ? crecip(pv) : cmk(0.0, 0.0);
-      const int rest = c0 + ib - c - 1;
-      // every row segment is loaded whole before it is written back, so the
-      // (up to IB) loads of a row are in flight together
-      for (int r = row0 + 1 + tid; r < n; r += PT) {
-        cplx* rowp = A + (long long)r * ld + col;
-        cplx seg[IB];
+      // scale column c and rank-1 update of columns (c, c0+ib): 8 lanes per row
+      const int g = lane & 7, cl = c - c0;
+      const bool upd = g > cl && g < ib;
+      const cplx u = upd ? prow[c0 + g] : cmk(0.0, 0.0);
+      const bool track = (g == cl + 1) && (g < ib);
+      best = -1.0;
+      bi = 0x7fffffff;
+      constexpr int RSTEP = 4 * PW2;  // rows per CTA iteration
+      for (int rb = row0 + 1 + wid * 4; rb < n; rb += 4 * RSTEP) {
+        cplx v[4];
+        bool act[4];
 #pragma unroll
-        for (int cc = 0; cc < IB; ++cc)
-          if (cc <= rest) seg[cc] = rowp[cc];
-        const cplx l = nz ? cmul(seg[0], rp) : seg[0];
-        rowp[0] = l;
+        for (int q = 0; q < 4; ++q) {
+          const int r = rb + q * RSTEP + (lane >> 3);
+          act[q] = r < n;
+          v[q] = (act[q] && g >= cl && g < ib) ? A[(long long)r * ld + k + c0 + g] : cmk(0.0, 0.0);
+        }
 #pragma unroll
-        for (int cc = 1; cc < IB; ++cc)
-          if (cc <= rest) {
-            cplx v = seg[cc];
-            cfms(v, l, prow[cc]);
-            rowp[cc] = v;
+        for (int q = 0; q < 4; ++q) {
+          const int r = rb + q * RSTEP + (lane >> 3);
+          const cplx lraw = cmk(__shfl_sync(0xffffffffu, v[q].x, (lane & ~7) + cl),
+                                __shfl_sync(0xffffffffu, v[q].y, (lane & ~7) + cl));
+          const cplx l = nz ? cmul(lraw, rp) : lraw;
+          if (act[q]) {
+            cplx* dst = A + (long long)r * ld + k + c0 + g;
+            if (g == cl) {
+              *dst = l;
+            } else if (upd) {
+              cplx w = v[q];
+              cfms(w, l, u);
+              *dst = w;
+              if (track) arg_better(best, bi, cabs1(w), r);
+            }
           }
+        }
       }
       __syncthreads();
     }
-    // update the panel columns right of the sub-panel: [k+c0+ib, k+jb)
+    // columns right of the sub-panel: [k+c0+ib, k+jb)
     const int nr = jb - c0 - ib;
     if (nr > 0) {
       const int r0 = k + c0;
       // U rows r0..r0+ib-1: forward substitution with the unit-lower L block
-      for (int cc = tid; cc < nr; cc += PT) {
+      for (int cc = tid; cc < nr; cc += PTT) {
         const int colg = k + c0 + ib + cc;
-        cplx u[IB];
+        cplx uu[IB];
         for (int i = 0; i < ib; ++i) {
           cplx v = A[(long long)(r0 + i) * ld + colg];
-          for (int l = 0; l < i; ++l) cfms(v, A[(long long)(r0 + i) * ld + k + c0 + l], u[l]);
-          u[i] = v;
+          for (int l2 = 0; l2 < i; ++l2) cfms(v, A[(long long)(r0 + i) * ld + k + c0 + l2], uu[l2]);
+          uu[i] = v;
           A[(long long)(r0 + i) * ld + colg] = v;
           ublk[i][cc] = v;
         }
       }
       __syncthreads();
-      // rows below: A[r][rest] -= L[r][c0:c0+ib] * U
-      for (int r = r0 + ib + tid; r < n; r += PT) {
-        cplx l[IB];
+      // rows below: A[r][rest] -= L[r][c0:c0+ib] U, 16 lanes per row; fused
+      // argmax of the first rest column (the next sub-panel's pivot column)
+      const int h = lane >> 4, q16 = lane & 15;
+      best = -1.0;
+      bi = 0x7fffffff;
+      for (int r = r0 + ib + wid * 2 + h; r < n; r += 2 * PW2) {
         const cplx* lr = A + (long long)r * ld + k + c0;
+        cplx l[IB];
 #pragma unroll
         for (int i = 0; i < IB; ++i) l[i] = i < ib ? lr[i] : cmk(0.0, 0.0);
         cplx* dst = A + (long long)r * ld + k + c0 + ib;
-        // 8-column chunks: all loads of a chunk issue before its stores
-        for (int c1 = 0; c1 < nr; c1 += 8) {
-          cplx v[8];
+        cplx v[4];
 #pragma unroll
-          for (int q = 0; q < 8; ++q)
-            if (c1 + q < nr) v[q] = dst[c1 + q];
+        for (int t = 0; t < 4; ++t) {
+          const int cc = q16 + 16 * t;
+          v[t] = cc < nr ? dst[cc] : cmk(0.0, 0.0);
+        }
 #pragma unroll
-          for (int q = 0; q < 8; ++q)
-            if (c1 + q < nr) {
+        for (int t = 0; t < 4; ++t) {
+          const int cc = q16 + 16 * t;
+          if (cc < nr) {
 #pragma unroll
-              for (int i = 0; i < IB; ++i) cfms(v[q], l[i], ublk[i][c1 + q]);
-              dst[c1 + q] = v[q];
-            }
+            for (int i = 0; i < IB; ++i)
+              if (i < ib) cfms(v[t], l[i], ublk[i][cc]);
+            dst[cc] = v[t];
+            if (cc == 0) arg_better(best, bi, cabs1(v[t]), r);
+          }
         }
       }
       __syncthreads();
@@ -261,6 +293,7 @@ __global__ void init_kernel(double* minpiv, int* info, int batch) {
   if (i < batch) { minpiv[i] = INFINITY; info[i] = 0; }
 }
 
+
 }  // namespace
 
 // In-place batched LU of `batch` complex n x n row-major matrices (stride
@@ -295,7 +328,7 @@ CIRR_API int cirr_zgetrf_batched(cplx* pencils, int n, long long ld, long long p
   }
   for (int k = 0; k < n; k += NB) {
     const int jb = min(NB, n - k);
-    panel_kernel<<<batch, PT, 0, stream>>>(pencils, n, ld, pencil_stride, k, jb, ipiv, minpiv, info);
+    panel2_kernel<PT2><<<batch, PT2, 0, stream>>>(pencils, n, ld, pencil_stride, k, jb, ipiv, minpiv, info);
     CIRR_CHECK_LAUNCH();
     if (n - jb > 0) {
       dim3 g((n - jb + 255) / 256, batch);
