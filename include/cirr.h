@@ -55,7 +55,7 @@ int cirr_zgetrs_batched(const cirr_cplx* LU, int n, long long ld, long long penc
                         int batch, const int* perm, const cirr_cplx* R, long long ldr,
                         long long rstride, const int* rhs_of, int K, cirr_cplx* Y,
                         long long ldy, long long ystride, const cirr_cplx* Dinv, cudaStream_t stream);
-/* Inverses of the 64x64 diagonal blocks of L and U (optional input of
+/* Inverses of the 128x128 diagonal blocks of L and U (optional input of
  * cirr_zgetrs_batched: the diagonal solves become TMA/DMMA GEMMs). */
 long long cirr_diag_inv_bytes(int n, int batch);
 int cirr_diag_inverses(const cirr_cplx* LU, int n, long long ld, long long pencil_stride, int batch,

@@ -165,28 +165,28 @@ __global__ void __launch_bounds__(256, 1) trsm_blocked_kernel(const cplx* __rest
   }
 }
 
-// Inverses of the 64x64 diagonal blocks of L (unit lower, slot 0) and U (slot 1)
-// of every pencil: Dinv[(b * nblk + bi) * 2 + slot] (64 x 64, zero outside nb x nb).
+
+// ---------------------------------------------------------------------------
+// 128 x 128 diagonal-block inverses for the right-looking solve: with DB = 128
+// the trailing GEMMs run with k = 128 (half the launches and half the C-tile
+// traffic of k = 64).  Each inverse is assembled from two 64 x 64 triangular
+// inverses and one off-diagonal block:
+//   lower  [[L11, 0], [L21, L22]]^-1 = [[X1, 0], [-X2 L21 X1, X2]]
+//   upper  [[U11, U12], [0, U22]]^-1 = [[X1, -X1 U12 X2], [0, X2]]
+constexpr int DB = 128;
+
+// X = T^-1 for the nb x nb (nb <= 64) triangular block in D (smem, ld SD_LD);
+// lower: unit diagonal; X is identity-padded outside nb.  256 threads.
 template <bool LOWER>
-__global__ void __launch_bounds__(256) diag_inv_kernel(const cplx* __restrict__ LU, long long ld, long long pstride,
-                                                       int n, cplx* __restrict__ Dinv) {
-  extern __shared__ __align__(16) cplx ism[];
-  cplx* D = ism;
-  cplx* X = D + SNB * SD_LD;
-  cplx* dinv = X + SNB * SD_LD;
-  const int bi = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
-  const int nblk = gridDim.x;
-  const int i0 = bi * SNB, nb = min(SNB, n - i0);
-  const cplx* T = LU + (long long)b * pstride;
+__device__ void tri_inv64(const cplx* D, cplx* X, cplx* dinv, int nb) {
+  const int tid = threadIdx.x;
   for (int e = tid; e < SNB * SNB; e += 256) {
     const int r = e / SNB, c = e % SNB;
-    D[r * SD_LD + c] = (r < nb && c < nb) ? T[(long long)(i0 + r) * ld + i0 + c] : cmk(0.0, 0.0);
     X[r * SD_LD + c] = cmk((r == c && r < nb) ? 1.0 : 0.0, 0.0);
   }
-  __syncthreads();
   if (!LOWER && tid < nb) dinv[tid] = crecip(D[tid * SD_LD + tid]);
   __syncthreads();
-  const int c = tid % SNB, g = tid / SNB;  // 4 row groups, all 64 unit columns at once
+  const int c = tid % SNB, g = tid / SNB;
   if (LOWER) {
     for (int i = 0; i < nb - 1; ++i) {
       const cplx xi = X[i * SD_LD + c];
@@ -202,10 +202,78 @@ __global__ void __launch_bounds__(256) diag_inv_kernel(const cplx* __restrict__ 
       __syncthreads();
     }
   }
-  cplx* out = Dinv + (((long long)b * nblk + bi) * 2 + (LOWER ? 0 : 1)) * SNB * SNB;
-  for (int e = tid; e < SNB * SNB; e += 256) out[e] = X[(e / SNB) * SD_LD + e % SNB];
+  __syncthreads();
 }
-constexpr int kDiagInvSmem = (2 * SNB * SD_LD + SNB) * 16;
+
+// T <- sign * (L @ R) for 64 x 64 smem blocks (in place into T allowed when T
+// aliases L or R: every product is held in registers before the write-back).
+__device__ void mm64_inplace(const cplx* L, const cplx* R, cplx* T, double sign) {
+  const int tid = threadIdx.x;
+  cplx acc[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const int e = tid + q * 256, r = e / SNB, c = e % SNB;
+    cplx a = cmk(0.0, 0.0);
+    for (int k = 0; k < SNB; ++k) cfma(a, L[r * SD_LD + k], R[k * SD_LD + c]);
+    acc[q] = cmk(sign * a.x, sign * a.y);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const int e = tid + q * 256;
+    T[(e / SNB) * SD_LD + e % SNB] = acc[q];
+  }
+  __syncthreads();
+}
+
+template <bool LOWER>
+__global__ void __launch_bounds__(256) diag_inv128_kernel(const cplx* __restrict__ LU, long long ld,
+                                                          long long pstride, int n, cplx* __restrict__ Dinv) {
+  extern __shared__ __align__(16) cplx ism[];
+  cplx* X1 = ism;
+  cplx* X2 = X1 + SNB * SD_LD;
+  cplx* T = X2 + SNB * SD_LD;
+  cplx* dinv = T + SNB * SD_LD;
+  const int bi = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
+  const int nblk = gridDim.x;
+  const int i0 = bi * DB, nb = min(DB, n - i0);
+  const int na = min(SNB, nb), nb2 = nb - na;
+  const cplx* A = LU + (long long)b * pstride;
+  auto load = [&](cplx* dst, int r0, int c0, int nr, int nc) {
+    for (int e = tid; e < SNB * SNB; e += 256) {
+      const int r = e / SNB, c = e % SNB;
+      dst[r * SD_LD + c] = (r < nr && c < nc) ? A[(long long)(r0 + r) * ld + c0 + c] : cmk(0.0, 0.0);
+    }
+    __syncthreads();
+  };
+  load(T, i0, i0, na, na);
+  tri_inv64<LOWER>(T, X1, dinv, na);
+  if (nb2 > 0) {
+    load(T, i0 + SNB, i0 + SNB, nb2, nb2);
+    tri_inv64<LOWER>(T, X2, dinv, nb2);
+    if (LOWER) {
+      load(T, i0 + SNB, i0, nb2, na);       // L21
+      mm64_inplace(T, X1, T, 1.0);          // L21 X1
+      mm64_inplace(X2, T, T, -1.0);         // -X2 L21 X1
+    } else {
+      load(T, i0, i0 + SNB, na, nb2);       // U12
+      mm64_inplace(T, X2, T, 1.0);          // U12 X2
+      mm64_inplace(X1, T, T, -1.0);         // -X1 U12 X2
+    }
+  }
+  cplx* out = Dinv + (((long long)b * nblk + bi) * 2 + (LOWER ? 0 : 1)) * DB * DB;
+  for (int e = tid; e < DB * DB; e += 256) {
+    const int r = e / DB, c = e % DB;
+    const bool top = r < SNB, left = c < SNB;
+    cplx v = cmk(0.0, 0.0);
+    if (top && left) v = X1[r * SD_LD + c];
+    else if (!top && !left) v = nb2 > 0 ? X2[(r - SNB) * SD_LD + c - SNB] : cmk(0.0, 0.0);
+    else if (LOWER && !top && left) v = nb2 > 0 ? T[(r - SNB) * SD_LD + c] : cmk(0.0, 0.0);
+    else if (!LOWER && top && !left) v = nb2 > 0 ? T[r * SD_LD + c - SNB] : cmk(0.0, 0.0);
+    out[e] = v;
+  }
+}
+constexpr int kDiagInv128Smem = (3 * SNB * SD_LD + SNB) * 16;
 
 // Y[j][i][c] = R[rhs_of[j]][perm[j][i]][c]
 __global__ void permute_kernel(const cplx* __restrict__ R, long long ldr, long long rstride,
@@ -308,25 +376,25 @@ __global__ void __launch_bounds__(256) diag_solve_kernel(const cplx* __restrict_
 // int32 array.
 // Bytes of the diagonal-block inverses cirr_diag_inverses writes.
 CIRR_API long long cirr_diag_inv_bytes(int n, int batch) {
-  const long long nblk = (n + SNB - 1) / SNB;
-  return (long long)batch * nblk * 2 * SNB * SNB * 16;
+  const long long nblk = (n + DB - 1) / DB;
+  return (long long)batch * nblk * 2 * DB * DB * 16;
 }
 
-// Inverses of the 64x64 diagonal blocks of every factor (once per factorisation,
+// Inverses of the 128x128 diagonal blocks of every factor (once per factorisation,
 // reused by every solve pass).
 CIRR_API int cirr_diag_inverses(const cplx* LU, int n, long long ld, long long pencil_stride, int batch, cplx* Dinv,
                                 cudaStream_t stream) {
   if (n <= 0 || batch <= 0) return CIRR_EINVAL;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(diag_inv_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDiagInvSmem);
-    cudaFuncSetAttribute(diag_inv_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDiagInvSmem);
+    cudaFuncSetAttribute(diag_inv128_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDiagInv128Smem);
+    cudaFuncSetAttribute(diag_inv128_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDiagInv128Smem);
     attr = true;
   }
-  dim3 g((n + SNB - 1) / SNB, batch);
-  diag_inv_kernel<true><<<g, 256, kDiagInvSmem, stream>>>(LU, ld, pencil_stride, n, Dinv);
+  dim3 g((n + DB - 1) / DB, batch);
+  diag_inv128_kernel<true><<<g, 256, kDiagInv128Smem, stream>>>(LU, ld, pencil_stride, n, Dinv);
   CIRR_CHECK_LAUNCH();
-  diag_inv_kernel<false><<<g, 256, kDiagInvSmem, stream>>>(LU, ld, pencil_stride, n, Dinv);
+  diag_inv128_kernel<false><<<g, 256, kDiagInv128Smem, stream>>>(LU, ld, pencil_stride, n, Dinv);
   CIRR_CHECK_LAUNCH();
   return 0;
 }
@@ -361,32 +429,50 @@ CIRR_API int cirr_zgetrs_batched(const cplx* LU, int n, long long ld, long long 
       cudaFuncSetAttribute(diag_solve_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDiagSmem);
       dattr = true;
     }
+    CUtensorMap mD;
+    const int nblk2 = (n + DB - 1) / DB;
+    const bool use_dinv = Dinv != nullptr &&
+                          cirr::encode_a_map(&mD, Dinv, DB, DB, batch * nblk2 * 2, DB, (long long)DB * DB) == 0;
+    if (use_dinv) {
+      // 128-row blocks; each diagonal block is applied as two in-place GEMMs
+      // (M = 64 each, so every output tile reads only its own rows plus rows
+      // that GEMM does not write), then one k = 128 trailing update.
+      for (int bi = 0; bi < nblk2; ++bi) {  // forward: L (unit lower)
+        const int i0 = bi * DB, nb = min(DB, n - i0), na = min(SNB, nb), nb2 = nb - na;
+        if (nb2 > 0)  // rows i0+64.. : [L21inv L22inv] [Y_a; Y_b]
+          CIRR_TRY(cirr::zgemm_sub_maps(mD, mY.b, mY.c, nb2, K, nb, batch, SNB, 0, i0, 0, i0 + SNB, 0, Y, ldy,
+                                        ystride, stream, /*beta=*/0, nblk2 * 2, bi * 2));
+        CIRR_TRY(cirr::zgemm_sub_maps(mD, mY.b, mY.c, na, K, na, batch, 0, 0, i0, 0, i0, 0, Y, ldy, ystride, stream,
+                                      /*beta=*/0, nblk2 * 2, bi * 2));
+        CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, n - i0 - nb, K, nb, batch, i0 + nb, i0, i0, 0, i0 + nb, 0,
+                                      Y, ldy, ystride, stream));
+      }
+      for (int bi = nblk2 - 1; bi >= 0; --bi) {  // backward: U
+        const int i0 = bi * DB, nb = min(DB, n - i0), na = min(SNB, nb), nb2 = nb - na;
+        // rows i0.. : [U11inv U12inv] [Y_a; Y_b] first (reads the old Y_b), then Y_b
+        CIRR_TRY(cirr::zgemm_sub_maps(mD, mY.b, mY.c, na, K, nb, batch, 0, 0, i0, 0, i0, 0, Y, ldy, ystride, stream,
+                                      /*beta=*/0, nblk2 * 2, bi * 2 + 1));
+        if (nb2 > 0)
+          CIRR_TRY(cirr::zgemm_sub_maps(mD, mY.b, mY.c, nb2, K, nb2, batch, SNB, SNB, i0 + SNB, 0, i0 + SNB, 0, Y,
+                                        ldy, ystride, stream, /*beta=*/0, nblk2 * 2, bi * 2 + 1));
+        CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, i0, K, nb, batch, 0, i0, i0, 0, 0, 0, Y, ldy, ystride,
+                                      stream));
+      }
+      return 0;
+    }
     const int nblk = (n + SNB - 1) / SNB;
     dim3 gd((K + DSC - 1) / DSC, batch);
-    CUtensorMap mD;
-    const bool use_dinv = Dinv != nullptr &&
-                          cirr::encode_a_map(&mD, Dinv, SNB, SNB, batch * nblk * 2, SNB, (long long)SNB * SNB) == 0;
     for (int bi = 0; bi < nblk; ++bi) {  // forward: L (unit lower)
       const int i0 = bi * SNB, nb = min(SNB, n - i0);
-      if (use_dinv) {  // Y_i <- L_ii^-1 Y_i on the GEMM (in place: each tile reads only its own rows)
-        CIRR_TRY(cirr::zgemm_sub_maps(mD, mY.b, mY.c, nb, K, nb, batch, 0, 0, i0, 0, i0, 0, Y, ldy, ystride, stream,
-                                      /*beta=*/0, nblk * 2, bi * 2));
-      } else {
-        diag_solve_kernel<true><<<gd, 256, kDiagSmem, stream>>>(LU, ld, pencil_stride, i0, nb, Y, ldy, ystride, K);
-        CIRR_CHECK_LAUNCH();
-      }
+      diag_solve_kernel<true><<<gd, 256, kDiagSmem, stream>>>(LU, ld, pencil_stride, i0, nb, Y, ldy, ystride, K);
+      CIRR_CHECK_LAUNCH();
       CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, n - i0 - nb, K, nb, batch, i0 + nb, i0, i0, 0, i0 + nb, 0,
                                     Y, ldy, ystride, stream));
     }
     for (int bi = nblk - 1; bi >= 0; --bi) {  // backward: U
       const int i0 = bi * SNB, nb = min(SNB, n - i0);
-      if (use_dinv) {
-        CIRR_TRY(cirr::zgemm_sub_maps(mD, mY.b, mY.c, nb, K, nb, batch, 0, 0, i0, 0, i0, 0, Y, ldy, ystride, stream,
-                                      /*beta=*/0, nblk * 2, bi * 2 + 1));
-      } else {
-        diag_solve_kernel<false><<<gd, 256, kDiagSmem, stream>>>(LU, ld, pencil_stride, i0, nb, Y, ldy, ystride, K);
-        CIRR_CHECK_LAUNCH();
-      }
+      diag_solve_kernel<false><<<gd, 256, kDiagSmem, stream>>>(LU, ld, pencil_stride, i0, nb, Y, ldy, ystride, K);
+      CIRR_CHECK_LAUNCH();
       CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, i0, K, nb, batch, 0, i0, i0, 0, 0, 0, Y, ldy, ystride,
                                     stream));
     }

@@ -426,27 +426,9 @@ class _Engine:
             np.concatenate([np.full(len(c.fidx), i, dtype=np.int32) for i, c in enumerate(self.cs)]))
 
     def _factor_contour(self, ci: int):
-        """Enqueue K1 + K2 (+ the diagonal-block inverses K3 uses) for the
-        pencils of contour ci on the current stream."""
-        torch, n = self.torch, self.n
-        a, b = self.node_off[ci], self.node_off[ci + 1]
-        cnt = b - a
-        if cnt == 0:
-            return
+        """K1 + K2 for the pencils of contour ci only (pipelined engine)."""
         c = self.cs[ci]
-        z = _h2d(c.nodes[c.fidx])
-        with _stage("assemble"):
-            _lib.call("cirr_assemble", _ptr(self.dp.a), _ptr(self.dp.b), n, n, _ptr(z), cnt,
-                      _ptr(self.pencils[a]), n, n * n, _ptr(self.maxabs[a:]), self.stream)
-        _work("assemble_bytes", cnt * n * n * 16 + 2 * n * n * 8)
-        with _stage("lu"):
-            lws = torch.empty(int(_lib.call("cirr_zgetrf_ws_bytes", n, cnt)), dtype=torch.uint8, device="cuda")
-            _lib.call("cirr_zgetrf_batched", _ptr(self.pencils[a]), n, n, n * n, cnt, _ptr(self.ipiv[a]),
-                      _ptr(self.perm[a]), _ptr(self.minpiv[a:]), _ptr(self.info[a:]), _ptr(lws), self.stream)
-        _work("lu_flops", cnt * 8.0 * n ** 3 / 3.0)
-        with _stage("dinv"):
-            _lib.call("cirr_diag_inverses", _ptr(self.pencils[a]), n, n, n * n, cnt,
-                      _ptr(self.dinv) + a * self._dinv_per_pencil, self.stream)
+        self._factor_range(self.node_off[ci], self.node_off[ci + 1], c.nodes[c.fidx])
 
     def _check_factor(self, ci: int):
         """Singular-shift test of contour ci (linalg.py:68-70); host sync on
@@ -465,10 +447,32 @@ class _Engine:
                 c.done = True
                 break
 
+    def _factor_range(self, a: int, b: int, nodes: np.ndarray):
+        """Enqueue K1 + K2 (+ the diagonal-block inverses K3 uses) for pencils
+        a..b-1 (shifts `nodes`) on the current stream, as one batched call: the
+        panel steps are latency-bound per launch, so one launch over every
+        pencil of the wave costs the same as one over a single contour."""
+        torch, n = self.torch, self.n
+        cnt = b - a
+        if cnt == 0:
+            return
+        z = _h2d(nodes)
+        with _stage("assemble"):
+            _lib.call("cirr_assemble", _ptr(self.dp.a), _ptr(self.dp.b), n, n, _ptr(z), cnt,
+                      _ptr(self.pencils[a]), n, n * n, _ptr(self.maxabs[a:]), self.stream)
+        _work("assemble_bytes", cnt * n * n * 16 + 2 * n * n * 8)
+        with _stage("lu"):
+            lws = torch.empty(int(_lib.call("cirr_zgetrf_ws_bytes", n, cnt)), dtype=torch.uint8, device="cuda")
+            _lib.call("cirr_zgetrf_batched", _ptr(self.pencils[a]), n, n, n * n, cnt, _ptr(self.ipiv[a]),
+                      _ptr(self.perm[a]), _ptr(self.minpiv[a:]), _ptr(self.info[a:]), _ptr(lws), self.stream)
+        _work("lu_flops", cnt * 8.0 * n ** 3 / 3.0)
+        with _stage("dinv"):
+            _lib.call("cirr_diag_inverses", _ptr(self.pencils[a]), n, n, n * n, cnt,
+                      _ptr(self.dinv) + a * self._dinv_per_pencil, self.stream)
+
     def factor(self):
         self._alloc_factors()
-        for ci in range(len(self.cs)):
-            self._factor_contour(ci)
+        self._factor_range(0, self.P, np.concatenate([c.nodes[c.fidx] for c in self.cs]))
         for ci in range(len(self.cs)):
             self._check_factor(ci)
 
@@ -556,7 +560,7 @@ class _Engine:
         return {ci: St[s] for s, ci in enumerate(active)}
 
     def _dinv(self):
-        """Inverses of the 64x64 diagonal blocks of every factor (made with the
+        """Inverses of the 128x128 diagonal blocks of every factor (made with the
         factorisation; each pencil's slice is contiguous)."""
         return self.dinv
 
