@@ -296,35 +296,49 @@ def run_cirr(args):
     e2e_s = max_over_ranks(statistics.median(e2e_times))
     e2e_value = world / e2e_s
 
-    # labelled variant (NOT the path of record, SURVEY.md finding 9):
-    # conjugate-pair halving of the node set, same workload and tolerance
+    # labelled variants (NOT the path of record): SURVEY.md finding 9
+    # (conjugate-pair halving) and finding 8 (early exit), same workload and tol
     variants = {}
     if not args.no_variants:
         import dataclasses
-        vcfg = dataclasses.replace(cfg, conjugate_pairs=True)
-        solve_multi(dp, wl.contours, vcfg, seed=0)
-        barrier()
-        torch.cuda.synchronize()
-        v0 = torch.cuda.Event(enable_timing=True)
-        v1 = torch.cuda.Event(enable_timing=True)
-        v0.record(stream)
-        for _ in range(args.steps):
-            vm = solve_multi(dp, wl.contours, vcfg, seed=0)
-        v1.record(stream)
-        torch.cuda.synchronize()
-        vms = max_over_ranks(v0.elapsed_time(v1))
-        vcounts = [len(r.eigenvalues) if r is not None else 0 for r in vm.results]
-        diff = 0.0
-        for rv, rr in zip(vm.results, last.results):
-            if rv is not None and rr is not None and len(rv.eigenvalues) == len(rr.eigenvalues):
-                for lam in rr.eigenvalues:
-                    diff = max(diff, float(np.min(np.abs(rv.eigenvalues - lam)) / abs(lam)))
-        variants["conjugate_pairs"] = {
-            "label": "variant, not the reference's algorithm: factor the N/2 upper-half nodes of each "
-                     "real-axis-symmetric contour, mirror the rest by conjugation",
-            "value": world * args.steps / (vms / 1e3), "unit": UNIT, "ms_per_step": vms / args.steps,
-            "eigenpairs": vcounts, "n_factorizations": vm.stats.n_factorizations,
-            "n_linear_solves": vm.stats.n_linear_solves, "max_rel_eig_diff_vs_record": diff}
+
+        labels = {
+            "conjugate_pairs": "factor the N/2 upper-half nodes of each real-axis-symmetric contour, mirror the "
+                               "rest by conjugation",
+            "early_exit": "stop refining a contour once its converged set is unchanged across two passes",
+            "conjugate_pairs+early_exit": "both of the above",
+        }
+        for name, label in labels.items():
+            vcfg = dataclasses.replace(cfg, conjugate_pairs="conjugate_pairs" in name, early_exit="early_exit" in name)
+            solve_multi(dp, wl.contours, vcfg, seed=0)
+            vt = S.StageTimer()
+            S.set_stage_timer(vt)
+            barrier()
+            torch.cuda.synchronize()
+            v0 = torch.cuda.Event(enable_timing=True)
+            v1 = torch.cuda.Event(enable_timing=True)
+            v0.record(stream)
+            for _ in range(args.steps):
+                vm = solve_multi(dp, wl.contours, vcfg, seed=0)
+            v1.record(stream)
+            torch.cuda.synchronize()
+            S.set_stage_timer(None)
+            vms = max_over_ranks(v0.elapsed_time(v1))
+            vcounts = [len(r.eigenvalues) if r is not None else 0 for r in vm.results]
+            diff = 0.0
+            for rv, rr in zip(vm.results, last.results):
+                if rv is not None and rr is not None and len(rv.eigenvalues) == len(rr.eigenvalues):
+                    for lam in rr.eigenvalues:
+                        diff = max(diff, float(np.min(np.abs(rv.eigenvalues - lam)) / abs(lam)))
+            vwork = dict(vt.work)
+            variants[name] = {
+                "label": "variant, not the reference's algorithm: " + label,
+                "value": world * args.steps / (vms / 1e3), "unit": UNIT, "ms_per_step": vms / args.steps,
+                "eigenpairs": vcounts, "iterations": [r.stats.iterations if r is not None else 0 for r in vm.results],
+                "n_factorizations": vm.stats.n_factorizations, "n_linear_solves": vm.stats.n_linear_solves,
+                "executed_flops_per_step": (vwork.get("lu_flops", 0.0) + vwork.get("solve_flops_exec", 0.0)
+                                            + vwork.get("moment_flops", 0.0)) / args.steps,
+                "max_rel_eig_diff_vs_record": diff}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -358,6 +372,7 @@ def run_cirr(args):
             "shifted_solves_per_s": solves * world / (per_step / 1e3),
             "eigenpairs": counts, "iterations": iters,
             "n_factorizations": last.stats.n_factorizations, "n_linear_solves": solves,
+            "executed_flops_per_step": stage_flops / args.steps,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "seconds_per_step": e2e_s},
             "gpu_launches": launches,

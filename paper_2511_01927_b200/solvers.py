@@ -76,6 +76,9 @@ class SolverConfig:
     # factor only the upper-half nodes and recover the lower half from
     # M(conj z)^-1 R = conj(M(z)^-1 conj R).  Halves K1+K2 work.
     conjugate_pairs: bool = False
+    # Labelled variant (SURVEY.md finding 8): stop refining a contour once its
+    # converged set (pairs with residual <= tol) is unchanged across two passes.
+    early_exit: bool = False
 
     def __post_init__(self):
         if self.n_q < 4 or self.n_moments < 1 or self.max_refine < 1:
@@ -98,7 +101,8 @@ def _cfg_view(cfg) -> SolverConfig:
     return SolverConfig(n_q=cfg.n_q, source_cols=cfg.source_cols, n_moments=cfg.n_moments,
                         max_refine=cfg.max_refine, tol=cfg.tol, rank_rel_tol=cfg.rank_rel_tol,
                         drop_tol=getattr(cfg, "drop_tol", 1e-10),
-                        conjugate_pairs=bool(getattr(cfg, "conjugate_pairs", False)))
+                        conjugate_pairs=bool(getattr(cfg, "conjugate_pairs", False)),
+                        early_exit=bool(getattr(cfg, "early_exit", False)))
 
 
 @dataclass
@@ -378,6 +382,28 @@ class _Contour:
         if np.any(mate < 0):
             return
         self.half, self.fidx, self.mate = True, up, mate
+
+    def settled(self, lam: np.ndarray, res: np.ndarray, tol: float) -> bool:
+        """Early-exit variant: True when the converged set (residual <= tol)
+        is unchanged from the previous pass (same count, eigenvalues equal to
+        1e-10 relative, matched nearest-neighbour) and reaches the contour's
+        expected_count; without an expected count the set must be unchanged
+        over three passes.  On config 4 a stable set short of the count still
+        gains pairs later, so stability alone would drop eigenpairs."""
+        conv = np.asarray(lam)[np.asarray(res) <= tol]
+        hist = getattr(self, "_conv_hist", [])
+        self._conv_hist = (hist + [conv])[-3:]
+        need = 2 if getattr(self.contour, "expected_count", 0) > 0 else 3
+        if len(self._conv_hist) < need or len(conv) == 0:
+            return False
+        scale = max(float(np.abs(conv).max()), 1e-300)
+        for prev in self._conv_hist[-need:-1]:
+            if len(prev) != len(conv):
+                return False
+            d = np.abs(conv[:, None] - prev[None, :])
+            if max(float(d.min(axis=1).max()), float(d.min(axis=0).max())) > 1e-10 * scale:
+                return False
+        return len(conv) >= getattr(self.contour, "expected_count", 0)
 
     def coef(self, moments: int) -> np.ndarray:
         """c[j, m] = w_j zeta_j^m with zeta_j = (z_j - gamma)/rho (sequential powers)."""
@@ -822,7 +848,8 @@ class _Engine:
                 c.best_res = min(c.best_res, float(res.max()))
                 if _DEBUG:
                     print(f"[cirr] contour {ci} it {it}: inside {len(lam)} max res {res.max():.2e}", flush=True)
-                if res.max() <= cfg.tol or it + 1 >= cfg.max_refine:
+                if res.max() <= cfg.tol or it + 1 >= cfg.max_refine or (
+                        cfg.early_exit and c.settled(lam, res, cfg.tol)):
                     active.remove(ci)
                     continue
                 refine[ci] = self.bmul(xi)
@@ -923,7 +950,8 @@ class _Engine:
                 c.best_res = min(c.best_res, float(res.max()))
                 if _DEBUG:
                     print(f"[cirr] contour {ci} it {it}: inside {len(lam)} max res {res.max():.2e}", flush=True)
-                if res.max() <= cfg.tol or it + 1 >= cfg.max_refine:
+                if res.max() <= cfg.tol or it + 1 >= cfg.max_refine or (
+                        cfg.early_exit and c.settled(lam, res, cfg.tol)):
                     break
                 rhs = self.bmul(xi)
                 ev_rhs = lat.record_event()

@@ -96,3 +96,23 @@ def test_conjugate_pairs_falls_back_off_axis():
     base, half = _pair_run(a, b, [c], dict(n_q=32))
     assert half.results[0].stats.n_factorizations == 32
     assert _match(half.results[0].eigenvalues, base.results[0].eigenvalues) <= 1e-12
+
+
+def test_early_exit_keeps_the_converged_pairs():
+    # SURVEY.md finding 8: spurious inside Ritz values keep config-4-like
+    # problems at max_refine; stopping once the converged set is stable returns
+    # the same converged eigenpairs with fewer passes
+    n = 768
+    a, b = W.config4_matrices(seed=5, n=n)
+    ev = sla.eigvals(a, b)
+    cs = [_counted(Contour(shape="ellipse", center=complex(cen, 0.0), semi_re=0.3, semi_im=0.15), ev)
+          for cen in (0.5, -0.5)]
+    p = DensePencil(a, b, hermitian=False)
+    kw = dict(n_q=64, source_cols=32, n_moments=8)
+    base = solve_multi(p, cs, SolverConfig(**kw))
+    early = solve_multi(p, cs, SolverConfig(early_exit=True, **kw))
+    for c, rb, re_ in zip(cs, base.results, early.results):
+        assert len(re_.eigenvalues) == len(rb.eigenvalues) == c.expected_count
+        assert _match(re_.eigenvalues, rb.eigenvalues) <= 1e-9
+        assert re_.residuals.max() <= 1e-10
+        assert re_.stats.iterations <= rb.stats.iterations
