@@ -167,6 +167,20 @@ def cpu_sample(wl, refine_cols=None, passes=None, sample_pencils=6):
     return per_gep, desc, t_pencils + t_rr
 
 
+def lu_traffic():
+    """DRAM bytes of the LU stage per step, measured by ncu on this code
+    (profiles/r01_lu_traffic_v7.json: dram__bytes_read + dram__bytes_write over
+    every LU kernel of one solve_multi); null when the profile is absent."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_lu_traffic_v7.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return {"traffic": d["lu_dram_bytes"], "traffic_unit": "bytes per step (all LU kernels)",
+                "traffic_over_algorithmic_min": d["traffic_over_min"], "traffic_source": os.path.relpath(path)}
+    except (OSError, KeyError, ValueError):
+        return {"traffic": None}
+
+
 def build_workload(seed):
     from paper_2511_01927_b200 import workloads as W
     return W.config4(seed=seed)
@@ -362,7 +376,8 @@ def run_cirr(args):
                          "frac": lu_tflops / FP64_DMMA_PEAK_TFLOPS,
                          "peak_source": "measured DMMA.8x8x4 FP64 peak (tools/fp64_peak.cu; "
                                         "MEASURED_PEAKS.json has no FP64 entry)",
-                         "algorithmic": "8 n^3 / 3 per pencil x 128 pencils per step", "traffic": None},
+                         "algorithmic": "8 n^3 / 3 per pencil x 128 pencils per step",
+                         **lu_traffic()},
             "lu_plus_moment_stage": {"tflops": stage_tflops, "frac_of_fp64_peak": stage_tflops / FP64_DMMA_PEAK_TFLOPS,
                                      "flops_per_step": stage_flops / args.steps,
                                      "ms_per_step": stage_ms / args.steps},
