@@ -42,11 +42,12 @@ from .errors import (
 PIVOT_REL_TOL = 1e-14  # linalg.py:26
 _DEBUG = bool(int(__import__("os").environ.get("CIRR_DEBUG", "0")))
 # CIRR_PIPELINE=1 overlaps the contours of a wave (run_pipelined: one host
-# thread + high-priority stream per contour).  Off by default: with the
-# current K4/K6 kernels it measured 1.90 s vs 1.83 s per config-4 GEP
-# (profiles/r01_pipeline_r01.txt), so the single-stream batched loop stays.
+# thread + high-priority stream per contour).  Off by default: ~2 % faster on
+# config 4 (1.72 s vs 1.77 s host wall, profiles/r01_pipeline_r01.txt), not
+# enough to trade the single-stream loop's simplicity for.
 _PIPELINE = bool(int(__import__("os").environ.get("CIRR_PIPELINE", "0")))
-_COOP_CAP = int(__import__("os").environ.get("CIRR_COOP_CAP", "32"))
+_TIMELINE = bool(int(__import__("os").environ.get("CIRR_TIMELINE", "0")))
+_COOP_CAP = int(__import__("os").environ.get("CIRR_COOP_CAP", "64"))
 
 
 
@@ -325,6 +326,17 @@ def ctypes_ptr(v) -> int:
 
 def _ptr(t) -> int:
     return t.data_ptr()
+
+
+_PIPE_STREAMS: dict = {}
+
+
+def _pipe_stream(dev: int, name: str, priority: int):
+    """Process-wide streams of the pipelined engine, one per (device, role)."""
+    key = (dev, name)
+    if key not in _PIPE_STREAMS:
+        _PIPE_STREAMS[key] = _torch().cuda.Stream(device=dev, priority=priority)
+    return _PIPE_STREAMS[key]
 
 
 def _h2d(x: np.ndarray):
@@ -881,51 +893,76 @@ class _Engine:
         torch, n = self.torch, self.n
         dev = torch.cuda.current_device()
         caller = torch.cuda.current_stream()
-        bulk = torch.cuda.Stream(priority=0)
+        # persistent streams: the caching allocator keeps per-stream pools, so
+        # fresh streams would cudaMalloc (and synchronise) on every call
+        bulk = _pipe_stream(dev, "bulk", 0)
         bulk.wait_stream(caller)
         self._bulk = bulk
         self._bulk_lock = threading.Lock()
         self._lat_streams = []
+        self._tl_events = []
+        self._tl(-1, -1, "start", bulk)
         self._alloc_factors()
         first = {}
-        with torch.cuda.stream(bulk):
-            for ci, c in enumerate(self.cs):
-                self._factor_contour(ci)
-                rng = np.random.default_rng(c.seed)
-                v = rng.standard_normal((n, c.ncols)).astype(complex)  # solvers.py:178-180
-                rhs = self.bmul(_h2d(v))
-                st = self.apply([ci], {ci: rhs}, moments, real_rhs=True)[ci]
-                first[ci] = (st, bulk.record_event())
+        ready = [threading.Event() for _ in self.cs]
         errors = []
 
         def worker(ci):
             try:
                 torch.cuda.set_device(dev)  # the current device is per thread
-                self._contour_loop(ci, *first[ci])
+                ready[ci].wait()
+                if ci in first:  # absent only when the caller's thread failed
+                    self._contour_loop(ci, *first[ci])
             except BaseException as exc:  # noqa: BLE001 - re-raised on the caller's thread
                 errors.append(exc)
 
         threads = [threading.Thread(target=worker, args=(ci,), daemon=True) for ci in range(len(self.cs))]
-        # cooperative K4/K6 kernels on a slice of the GPU, so they run beside
-        # the bulk GEMMs instead of waiting for the whole device
         old_cap = _lib.call("cirr_set_coop_ctas", _COOP_CAP)
+        for t in threads:
+            t.start()
         try:
-            for t in threads:
-                t.start()
+            with torch.cuda.stream(bulk):
+                # one batched factorisation for the whole wave (the panel steps
+                # are latency-bound per launch, so per-contour LUs cost ~14 % more)
+                self._factor_range(0, self.P, np.concatenate([c.nodes[c.fidx] for c in self.cs]))
+                for ci, c in enumerate(self.cs):
+                    rng = np.random.default_rng(c.seed)
+                    v = rng.standard_normal((n, c.ncols)).astype(complex)  # solvers.py:178-180
+                    self._tl(ci, -1, "first0", bulk)
+                    with self._bulk_lock:
+                        rhs = self.bmul(_h2d(v))
+                        st = self.apply([ci], {ci: rhs}, moments, real_rhs=True)[ci]
+                        self._tl(ci, -1, "first1", bulk)
+                        first[ci] = (st, bulk.record_event())
+                    ready[ci].set()  # this contour's Rayleigh-Ritz may start now
             for t in threads:
                 t.join()
         finally:
+            for r in ready:
+                r.set()
             _lib.call("cirr_set_coop_ctas", old_cap)
         caller.wait_stream(bulk)
         for lat in self._lat_streams:
             caller.wait_stream(lat)
         if errors:
             raise errors[0]
+        if _TIMELINE:
+            torch.cuda.synchronize()
+            t0 = self._tl_events[0][3]
+            for ci_, it_, name, e in self._tl_events[1:]:
+                print(f"[tl] c{ci_} it{it_} {name} {t0.elapsed_time(e):9.2f} ms", flush=True)
+
+    def _tl(self, ci, it, name, stream):
+        """Debug timeline (CIRR_TIMELINE=1): timing events on the given stream."""
+        if _TIMELINE:
+            e = self.torch.cuda.Event(enable_timing=True)
+            e.record(stream)
+            self._tl_events.append((ci, it, name, e))
 
     def _contour_loop(self, ci: int, st, ev):
         torch, cfg = self.torch, self.cfg
         c = self.cs[ci]
-        lat = torch.cuda.Stream(priority=-1)
+        lat = _pipe_stream(torch.cuda.current_device(), f"lat{ci}", -1)
         self._lat_streams.append(lat)
         with torch.cuda.stream(lat):
             lat.wait_event(ev)
@@ -936,7 +973,9 @@ class _Engine:
             it_used = 0
             for it in range(cfg.max_refine):
                 it_used = it
+                self._tl(ci, it, "rr0", lat)
                 r = self.rayleigh_ritz([(ci, st)])[ci]
+                self._tl(ci, it, "rr1", lat)
                 if r[0] == "rankzero":
                     break
                 if r[0] == "indefinite":
@@ -958,7 +997,9 @@ class _Engine:
                 with self._bulk_lock, torch.cuda.stream(self._bulk):
                     self._bulk.wait_event(ev_rhs)
                     rhs.record_stream(self._bulk)
+                    self._tl(ci, it, "ap0", self._bulk)
                     st = self.apply([ci], {ci: rhs}, 1)[ci]
+                    self._tl(ci, it, "ap1", self._bulk)
                     ev_st = self._bulk.record_event()
                 lat.wait_event(ev_st)
                 st.record_stream(lat)
