@@ -8,11 +8,14 @@ reference's Python API.  See DESIGN.md and include/cirr.h.
 """
 
 from .contours import Contour, QuadratureRule, contours_from_json, contours_to_json, quadrature_for  # noqa: F401
+from .datasets import Dataset, DatasetPencil, read_dataset, read_matrix_market, write_dataset  # noqa: F401
+from .datasets import write_matrix_market  # noqa: F401
 from .errors import (  # noqa: F401
     CieigError,
     ConvergenceError,
     DeviceError,
     DimensionError,
+    FormatError,
     IndefiniteBError,
     NoEigenvaluesFound,
     ParameterError,
