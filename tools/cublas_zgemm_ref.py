@@ -22,7 +22,8 @@ def main():
     b = torch.randn(n, n, dtype=torch.complex128, device=dev)
     t, tf = bench(lambda: a @ b, 8.0 * n ** 3)
     print(f"cuBLAS zgemm {n}^3: {t:.2f} ms {tf:.2f} TF/s")
-    for (bs, m, k, nn) in [(128, 4032, 64, 4032), (64, 4032, 64, 128), (16, 4032, 64, 4032)]:
+    for (bs, m, k, nn) in [(128, 4032, 64, 4032), (128, 3968, 128, 3968), (64, 4032, 64, 128), (64, 3968, 128, 128),
+                           (16, 4032, 64, 4032), (16, 3968, 128, 3968), (16, 3840, 256, 3840)]:
         A = torch.randn(bs, m, k, dtype=torch.complex128, device=dev)
         B = torch.randn(bs, k, nn, dtype=torch.complex128, device=dev)
         C = torch.randn(bs, m, nn, dtype=torch.complex128, device=dev)
