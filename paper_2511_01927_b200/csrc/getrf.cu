@@ -328,49 +328,45 @@ CIRR_API int cirr_zgetrf_batched(cplx* pencils, int n, long long ld, long long p
   }
   int k0 = 0;
   if (use_linv && use_tma && n >= 256) {
-    // Two-level blocking: 128-column steps made of two 64-column panels, so the
-    // big trailing update runs with k = 128 (fewer C-tile round trips per flop:
-    // cuBLAS batched ZGEMM goes 32.8 -> 34.6 TF/s from k = 64 to 128 on these
-    // shapes).  The first half's update of the columns right of the 128-block
-    // is deferred into that k = 128 GEMM (and one 64-row GEMM for the second
-    // half's own rows); row interchanges commute with those row-wise updates.
-    for (; k0 + 2 * NB <= n; k0 += 2 * NB) {
-      const int k = k0, kb = k0 + NB, rest = n - k0 - 2 * NB;
-      auto swap_out = [&](int kk) -> int {  // interchanges of panel kk, all columns outside it
-        dim3 g((n - NB + 255) / 256, batch);
-        swap_kernel<<<g, 256, 0, stream>>>(pencils, n, ld, pencil_stride, kk, NB, ipiv);
+    // Multi-level blocking: steps of W = PB x 64 columns made of PB 64-column
+    // panels, so the big trailing update runs with k = W (fewer C-tile round
+    // trips per flop: cuBLAS batched ZGEMM on these shapes goes 32.8 / 34.6 /
+    // 35.7 TF/s at k = 64 / 128 / 256).  Inside a block the panels are
+    // left-looking: just before panel i is factored, its columns receive the
+    // updates of panels 0..i-1 of the block (one GEMM, k = 64 i); after it is
+    // factored, its rows right of it receive the same deferred updates and
+    // L_ii^-1 (U rows, in place).  Row interchanges of a panel go to every
+    // column outside it and commute with the deferred row-wise updates.
+    const int PB = n >= 2048 ? 8 : (n >= 1024 ? 4 : 2);
+    const int W = PB * NB;
+    for (; k0 + W <= n; k0 += W) {
+      const int k = k0, rest = n - k0 - W;
+      for (int i = 0; i < PB; ++i) {
+        const int ki = k + i * NB;
+        if (i > 0)  // this panel's columns: A[ki:, ki:ki+64] -= L[ki:, k:ki] U[k:ki, ki:ki+64]
+          CIRR_TRY(cirr::zgemm_sub_maps(maps.a, maps.b, maps.c, n - ki, NB, i * NB, batch, ki, k, k, ki, ki, ki,
+                                        pencils, ld, pencil_stride, stream));
+        panel2_kernel<PT2><<<batch, PT2, 0, stream>>>(pencils, n, ld, pencil_stride, ki, NB, ipiv, minpiv, info);
         CIRR_CHECK_LAUNCH();
-        return 0;
-      };
-      // first half
-      panel2_kernel<PT2><<<batch, PT2, 0, stream>>>(pencils, n, ld, pencil_stride, k, NB, ipiv, minpiv, info);
-      CIRR_CHECK_LAUNCH();
-      CIRR_TRY(swap_out(k));
-      linv_kernel<<<batch, 256, kLinvSmem, stream>>>(pencils, ld, pencil_stride, k, linv);
-      CIRR_CHECK_LAUNCH();
-      // U12 of the first half's rows for every column right of it (in place)
-      CIRR_TRY(cirr::zgemm_sub_maps(mapL, maps.b, maps.c, NB, n - kb, NB, batch, 0, 0, k, kb, k, kb, pencils, ld,
-                                    pencil_stride, stream, /*beta=*/0));
-      // the second half's columns: A[kb:, kb:kb+64] -= L21a U12a
-      CIRR_TRY(cirr::zgemm_sub_maps(maps.a, maps.b, maps.c, n - kb, NB, NB, batch, kb, k, k, kb, kb, kb, pencils, ld,
-                                    pencil_stride, stream));
-      // second half
-      panel2_kernel<PT2><<<batch, PT2, 0, stream>>>(pencils, n, ld, pencil_stride, kb, NB, ipiv, minpiv, info);
-      CIRR_CHECK_LAUNCH();
-      CIRR_TRY(swap_out(kb));
-      if (rest > 0) {
-        linv_kernel<<<batch, 256, kLinvSmem, stream>>>(pencils, ld, pencil_stride, kb, linv);
-        CIRR_CHECK_LAUNCH();
-        // the second half's rows in the rest columns: first the deferred
-        // update by the first half, then L_bb^-1 (in place)
-        CIRR_TRY(cirr::zgemm_sub_maps(maps.a, maps.b, maps.c, NB, rest, NB, batch, kb, k, k, kb + NB, kb, kb + NB,
-                                      pencils, ld, pencil_stride, stream));
-        CIRR_TRY(cirr::zgemm_sub_maps(mapL, maps.b, maps.c, NB, rest, NB, batch, 0, 0, kb, kb + NB, kb, kb + NB,
-                                      pencils, ld, pencil_stride, stream, /*beta=*/0));
-        // trailing update with k = 128: A22 -= A[k+128:, k:k+128] A[k:k+128, k+128:]
-        CIRR_TRY(cirr::zgemm_sub_maps(maps.a, maps.b, maps.c, rest, rest, 2 * NB, batch, kb + NB, k, k, kb + NB,
-                                      kb + NB, kb + NB, pencils, ld, pencil_stride, stream));
+        {
+          dim3 g((n - NB + 255) / 256, batch);
+          swap_kernel<<<g, 256, 0, stream>>>(pencils, n, ld, pencil_stride, ki, NB, ipiv);
+          CIRR_CHECK_LAUNCH();
+        }
+        const int right = n - ki - NB;  // columns right of this panel
+        if (right > 0) {
+          linv_kernel<<<batch, 256, kLinvSmem, stream>>>(pencils, ld, pencil_stride, ki, linv);
+          CIRR_CHECK_LAUNCH();
+          if (i > 0)  // deferred updates of this panel's rows: A[ki:ki+64, ki+64:] -= L[ki:ki+64, k:ki] U[k:ki, ki+64:]
+            CIRR_TRY(cirr::zgemm_sub_maps(maps.a, maps.b, maps.c, NB, right, i * NB, batch, ki, k, k, ki + NB, ki,
+                                          ki + NB, pencils, ld, pencil_stride, stream));
+          CIRR_TRY(cirr::zgemm_sub_maps(mapL, maps.b, maps.c, NB, right, NB, batch, 0, 0, ki, ki + NB, ki, ki + NB,
+                                        pencils, ld, pencil_stride, stream, /*beta=*/0));
+        }
       }
+      if (rest > 0)  // trailing update with k = W
+        CIRR_TRY(cirr::zgemm_sub_maps(maps.a, maps.b, maps.c, rest, rest, W, batch, k + W, k, k, k + W, k + W, k + W,
+                                      pencils, ld, pencil_stride, stream));
     }
   }
   for (int k = k0; k < n; k += NB) {
