@@ -435,29 +435,61 @@ CIRR_API int cirr_zgetrs_batched(const cplx* LU, int n, long long ld, long long 
     const bool use_dinv = Dinv != nullptr &&
                           cirr::encode_a_map(&mD, Dinv, DB, DB, batch * nblk2 * 2, DB, (long long)DB * DB) == 0;
     if (use_dinv) {
-      // 128-row blocks; each diagonal block is applied as two in-place GEMMs
-      // (M = 64 each, so every output tile reads only its own rows plus rows
-      // that GEMM does not write), then one k = 128 trailing update.
-      for (int bi = 0; bi < nblk2; ++bi) {  // forward: L (unit lower)
+      // 128-row blocks grouped into super-blocks of SBK blocks.  Inside a
+      // super-block the blocks are left-looking (block j first receives the
+      // contributions of blocks 0..j-1 of the super-block, one GEMM), and each
+      // diagonal block is applied as two in-place GEMMs (M = 64 each, so every
+      // output tile reads only its own rows plus rows that GEMM does not
+      // write); the rows below/above then get one trailing update with
+      // k = 128 * SBK (fewer C-tile round trips per flop than k = 128).
+      const int SBK = n >= 2048 ? 4 : (n >= 512 ? 2 : 1);
+      auto apply_dinv = [&](int bi, bool lower) -> int {
         const int i0 = bi * DB, nb = min(DB, n - i0), na = min(SNB, nb), nb2 = nb - na;
-        if (nb2 > 0)  // rows i0+64.. : [L21inv L22inv] [Y_a; Y_b]
-          CIRR_TRY(cirr::zgemm_sub_maps(mD, mY.b, mY.c, nb2, K, nb, batch, SNB, 0, i0, 0, i0 + SNB, 0, Y, ldy,
-                                        ystride, stream, /*beta=*/0, nblk2 * 2, bi * 2));
-        CIRR_TRY(cirr::zgemm_sub_maps(mD, mY.b, mY.c, na, K, na, batch, 0, 0, i0, 0, i0, 0, Y, ldy, ystride, stream,
-                                      /*beta=*/0, nblk2 * 2, bi * 2));
-        CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, n - i0 - nb, K, nb, batch, i0 + nb, i0, i0, 0, i0 + nb, 0,
-                                      Y, ldy, ystride, stream));
+        const int slot = bi * 2 + (lower ? 0 : 1);
+        if (lower) {
+          if (nb2 > 0)  // rows i0+64.. : [L21inv L22inv] [Y_a; Y_b]
+            CIRR_TRY(cirr::zgemm_sub_maps(mD, mY.b, mY.c, nb2, K, nb, batch, SNB, 0, i0, 0, i0 + SNB, 0, Y, ldy,
+                                          ystride, stream, /*beta=*/0, nblk2 * 2, slot));
+          CIRR_TRY(cirr::zgemm_sub_maps(mD, mY.b, mY.c, na, K, na, batch, 0, 0, i0, 0, i0, 0, Y, ldy, ystride, stream,
+                                        /*beta=*/0, nblk2 * 2, slot));
+        } else {
+          // rows i0.. : [U11inv U12inv] [Y_a; Y_b] first (reads the old Y_b), then Y_b
+          CIRR_TRY(cirr::zgemm_sub_maps(mD, mY.b, mY.c, na, K, nb, batch, 0, 0, i0, 0, i0, 0, Y, ldy, ystride, stream,
+                                        /*beta=*/0, nblk2 * 2, slot));
+          if (nb2 > 0)
+            CIRR_TRY(cirr::zgemm_sub_maps(mD, mY.b, mY.c, nb2, K, nb2, batch, SNB, SNB, i0 + SNB, 0, i0 + SNB, 0, Y,
+                                          ldy, ystride, stream, /*beta=*/0, nblk2 * 2, slot));
+        }
+        return 0;
+      };
+      for (int sb0 = 0; sb0 < nblk2; sb0 += SBK) {  // forward: L (unit lower)
+        const int sb1 = min(nblk2, sb0 + SBK);
+        const int s0 = sb0 * DB, s1 = min(n, sb1 * DB);
+        for (int bi = sb0; bi < sb1; ++bi) {
+          const int i0 = bi * DB, nb = min(DB, n - i0);
+          if (bi > sb0)  // Y[i0:i0+nb] -= L[i0:i0+nb, s0:i0] Y[s0:i0]
+            CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, nb, K, i0 - s0, batch, i0, s0, s0, 0, i0, 0, Y, ldy,
+                                          ystride, stream));
+          CIRR_TRY(apply_dinv(bi, true));
+        }
+        if (n - s1 > 0)  // Y[s1:] -= L[s1:, s0:s1] Y[s0:s1]
+          CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, n - s1, K, s1 - s0, batch, s1, s0, s0, 0, s1, 0, Y, ldy,
+                                        ystride, stream));
       }
-      for (int bi = nblk2 - 1; bi >= 0; --bi) {  // backward: U
-        const int i0 = bi * DB, nb = min(DB, n - i0), na = min(SNB, nb), nb2 = nb - na;
-        // rows i0.. : [U11inv U12inv] [Y_a; Y_b] first (reads the old Y_b), then Y_b
-        CIRR_TRY(cirr::zgemm_sub_maps(mD, mY.b, mY.c, na, K, nb, batch, 0, 0, i0, 0, i0, 0, Y, ldy, ystride, stream,
-                                      /*beta=*/0, nblk2 * 2, bi * 2 + 1));
-        if (nb2 > 0)
-          CIRR_TRY(cirr::zgemm_sub_maps(mD, mY.b, mY.c, nb2, K, nb2, batch, SNB, SNB, i0 + SNB, 0, i0 + SNB, 0, Y,
-                                        ldy, ystride, stream, /*beta=*/0, nblk2 * 2, bi * 2 + 1));
-        CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, i0, K, nb, batch, 0, i0, i0, 0, 0, 0, Y, ldy, ystride,
-                                      stream));
+      const int nsb = (nblk2 + SBK - 1) / SBK;
+      for (int sb = nsb - 1; sb >= 0; --sb) {  // backward: U
+        const int sb0 = sb * SBK, sb1 = min(nblk2, sb0 + SBK);
+        const int s0 = sb0 * DB, s1 = min(n, sb1 * DB);
+        for (int bi = sb1 - 1; bi >= sb0; --bi) {
+          const int i0 = bi * DB, nb = min(DB, n - i0);
+          if (bi < sb1 - 1)  // Y[i0:i0+nb] -= U[i0:i0+nb, i0+nb:s1] Y[i0+nb:s1]
+            CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, nb, K, s1 - i0 - nb, batch, i0, i0 + nb, i0 + nb, 0, i0,
+                                          0, Y, ldy, ystride, stream));
+          CIRR_TRY(apply_dinv(bi, false));
+        }
+        if (s0 > 0)  // Y[:s0] -= U[:s0, s0:s1] Y[s0:s1]
+          CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, s0, K, s1 - s0, batch, 0, s0, s0, 0, 0, 0, Y, ldy, ystride,
+                                        stream));
       }
       return 0;
     }
