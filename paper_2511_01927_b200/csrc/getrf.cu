@@ -107,18 +107,19 @@ __global__ void __launch_bounds__(PTT) panel2_kernel(cplx* __restrict__ P, int n
       const bool track = (g == cl + 1) && (g < ib);
       best = -1.0;
       bi = 0x7fffffff;
-      constexpr int RSTEP = 4 * PW2;  // rows per CTA iteration
-      for (int rb = row0 + 1 + wid * 4; rb < n; rb += 4 * RSTEP) {
-        cplx v[4];
-        bool act[4];
+      constexpr int RSTEP = 4 * PW2;  // rows per CTA pass of one row group
+      constexpr int RU = 8;           // row groups in flight per thread
+      for (int rb = row0 + 1 + wid * 4; rb < n; rb += RU * RSTEP) {
+        cplx v[RU];
+        bool act[RU];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < RU; ++q) {
           const int r = rb + q * RSTEP + (lane >> 3);
           act[q] = r < n;
           v[q] = (act[q] && g >= cl && g < ib) ? A[(long long)r * ld + k + c0 + g] : cmk(0.0, 0.0);
         }
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < RU; ++q) {
           const int r = rb + q * RSTEP + (lane >> 3);
           const cplx lraw = cmk(__shfl_sync(0xffffffffu, v[q].x, (lane & ~7) + cl),
                                 __shfl_sync(0xffffffffu, v[q].y, (lane & ~7) + cl));
@@ -160,27 +161,37 @@ __global__ void __launch_bounds__(PTT) panel2_kernel(cplx* __restrict__ P, int n
       const int h = lane >> 4, q16 = lane & 15;
       best = -1.0;
       bi = 0x7fffffff;
-      for (int r = r0 + ib + wid * 2 + h; r < n; r += 2 * PW2) {
-        const cplx* lr = A + (long long)r * ld + k + c0;
-        cplx l[IB];
+      for (int rA = r0 + ib + wid * 2 + h; rA < n; rA += 4 * PW2) {
+        // two rows per thread (rA and rA + 2*PW2): all their loads in flight together
+        const int rr2[2] = {rA, rA + 2 * PW2};
+        cplx l[2][IB], v[2][4];
 #pragma unroll
-        for (int i = 0; i < IB; ++i) l[i] = i < ib ? lr[i] : cmk(0.0, 0.0);
-        cplx* dst = A + (long long)r * ld + k + c0 + ib;
-        cplx v[4];
+        for (int u2 = 0; u2 < 2; ++u2) {
+          const bool ok = rr2[u2] < n;
+          const cplx* lr = A + (long long)rr2[u2] * ld + k + c0;
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const int cc = q16 + 16 * t;
-          v[t] = cc < nr ? dst[cc] : cmk(0.0, 0.0);
+          for (int i = 0; i < IB; ++i) l[u2][i] = (ok && i < ib) ? lr[i] : cmk(0.0, 0.0);
+          const cplx* src = lr + ib;
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int cc = q16 + 16 * t;
+            v[u2][t] = (ok && cc < nr) ? src[cc] : cmk(0.0, 0.0);
+          }
         }
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const int cc = q16 + 16 * t;
-          if (cc < nr) {
+        for (int u2 = 0; u2 < 2; ++u2) {
+          if (rr2[u2] >= n) continue;
+          cplx* dst = A + (long long)rr2[u2] * ld + k + c0 + ib;
 #pragma unroll
-            for (int i = 0; i < IB; ++i)
-              if (i < ib) cfms(v[t], l[i], ublk[i][cc]);
-            dst[cc] = v[t];
-            if (cc == 0) arg_better(best, bi, cabs1(v[t]), r);
+          for (int t = 0; t < 4; ++t) {
+            const int cc = q16 + 16 * t;
+            if (cc < nr) {
+#pragma unroll
+              for (int i = 0; i < IB; ++i)
+                if (i < ib) cfms(v[u2][t], l[u2][i], ublk[i][cc]);
+              dst[cc] = v[u2][t];
+              if (cc == 0) arg_better(best, bi, cabs1(v[u2][t]), rr2[u2]);
+            }
           }
         }
       }
