@@ -109,6 +109,17 @@ int cirr_gen_eig_vectors(void* ws, const int* kdim, int kmax, int nprob, const c
                          const int* sel_cnt, int smax, void* scratch, cirr_cplx* S, long long lds, long long sS,
                          cudaStream_t stream);
 
+/* Certified CholeskyQR2 basis (the fast path of cirr_orth for full-rank blocks):
+ * W[p] (c x n rows = the columns of S, cdim[p] valid) -> Qt[p] (cdim[p]
+ * orthonormal rows spanning range(S), zero rows after); ok[p] = 1 when
+ * ||R||_F ||R^-1||_F <= kappa_max (full rank certified), else 0 and the caller
+ * uses cirr_orth.  Replaces linalg.py:107-119 when no singular value is cut.
+ * ws: cirr_orth_cholqr2_ws_bytes(n, c, nprob). */
+long long cirr_orth_cholqr2_ws_bytes(int n, int c, int nprob);
+int cirr_orth_cholqr2(const cirr_cplx* W, long long ldw, long long wstride, int n, int c, int nprob,
+                      const int* cdim, double kappa_max, cirr_cplx* Qt, long long ldq, long long qstride,
+                      void* ws, int* ok, cudaStream_t stream);
+
 /* debug: clock64 marks of the last cirr_orth launch (4 entries) */
 int cirr_orth_phases(long long* host_out);
 

@@ -35,6 +35,8 @@ SIGNATURES = {
     "cirr_orth_phases": [_P],
     "cirr_orth": [_P, _L, _L, _I, _I, _I, _D, _P, _P, _P, _P, _L, _L, _P, _P, _P],
     "cirr_orthonormalize": [_P, _L, _L, _I, _I, _I, _D, _P, _L, _L, _P, _P],
+    "cirr_orth_cholqr2_ws_bytes": [_I, _I, _I],
+    "cirr_orth_cholqr2": [_P, _L, _L, _I, _I, _I, _P, _D, _P, _L, _L, _P, _P, _P],
     "cirr_gemm": [_I, _I, _I, _I, _I, _P, _L, _L, _P, _L, _L, _P, _L, _L, _D, _I, _P],
     "cirr_small_eig_ws_bytes": [_I],
     "cirr_small_eig": [_I, _P, _P, _L, _L, _P, _I, _I, _P, _P, _P, _L, _L, _P, _P],
@@ -53,9 +55,9 @@ SIGNATURES = {
     "cirr_launch_count": [],
 }
 _RESTYPE = {"cirr_diag_inv_bytes": _L, "cirr_zgetrf_ws_bytes": _L, "cirr_small_eig_ws_bytes": _L, "cirr_launch_count": _L, "cirr_orth_ws_bytes": _L,
-            "cirr_gen_eig_ws_bytes": _L, "cirr_gen_eig_vec_scratch_bytes": _L}
+            "cirr_gen_eig_ws_bytes": _L, "cirr_gen_eig_vec_scratch_bytes": _L, "cirr_orth_cholqr2_ws_bytes": _L}
 _RAW = {"cirr_set_coop_ctas", "cirr_diag_inv_bytes", "cirr_zgetrf_ws_bytes", "cirr_small_eig_ws_bytes", "cirr_launch_count", "cirr_target_sm", "cirr_orth_ws_bytes",
-        "cirr_gen_eig_ws_bytes", "cirr_gen_eig_vec_scratch_bytes"}
+        "cirr_gen_eig_ws_bytes", "cirr_gen_eig_vec_scratch_bytes", "cirr_orth_cholqr2_ws_bytes"}
 
 _lib = None
 

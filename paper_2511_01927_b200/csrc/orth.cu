@@ -424,3 +424,126 @@ CIRR_API int cirr_orthonormalize(const cplx* Y, long long ldy, long long sy, int
 CIRR_API int cirr_orth_phases(long long* host_out) {
   return (int)cudaMemcpyFromSymbol(host_out, g_orth_phase, sizeof(long long) * 4);
 }
+
+// --------------------------------------------------------------------------
+// Certified CholeskyQR2: the fast basis for full-rank blocks.
+//
+// linalg.py:107-119 keeps the left singular vectors with sigma >= rel_tol *
+// sigma_max.  When every sigma passes, that basis spans range(S), and the
+// Rayleigh-Ritz values and vectors depend only on that span (up to rounding
+// and the phase of each unit eigenvector).  So when S is certifiably full
+// rank, an orthonormal basis from CholeskyQR2 (the north star's
+// "CholeskyQR2 plus an SVD threshold") replaces the Householder QR + Jacobi
+// SVD: Gram matrix on the DMMA GEMM, one-CTA Cholesky and triangular
+// inverse, Q = S R^-1 on the GEMM, twice.  The certificate is
+// kappa_F(R1) = ||R1||_F ||R1^-1||_F <= kappa_max (>= kappa_2(S), up to the
+// rounding of the Gram matrix); with kappa_max far below both 1/rel_tol and
+// eps^-1/2 the block is full rank and CholeskyQR2 is accurate.  Otherwise
+// ok = 0 and the caller runs cirr_orth.
+namespace {
+constexpr int CT = 256;
+
+// G (c x c, ld cmax) = S^H S  ->  R (upper, in place), RinvT = (R^-1)^T (cmax x cmax,
+// zero outside c x c), ok &= certificate.  One CTA per problem.
+__global__ void __launch_bounds__(CT) chol_inv_kernel(cplx* __restrict__ Gall, const int* __restrict__ cdim,
+                                                      int cmax, double kappa_max, cplx* __restrict__ RinvT_all,
+                                                      int* __restrict__ ok, int first_pass) {
+  __shared__ double sred[32];
+  __shared__ int s_fail;
+  const int p = blockIdx.x, c = cdim[p], tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  cplx* G = Gall + (long long)p * cmax * cmax;
+  cplx* RT = RinvT_all + (long long)p * cmax * cmax;
+  for (int e = tid; e < cmax * cmax; e += CT) RT[e] = cmk(0.0, 0.0);
+  if (tid == 0) s_fail = (c <= 0);
+  __syncthreads();
+  // right-looking Cholesky, upper factor in the upper triangle of G
+  double dmax = 0.0;
+  for (int j = 0; j < c; ++j) dmax = fmax(dmax, G[(long long)j * cmax + j].x);
+  for (int j = 0; j < c && !s_fail; ++j) {
+    const double d = G[(long long)j * cmax + j].x;
+    if (!(d > 1e-300 && d > 1e-24 * dmax && d < 1e300)) {
+      if (tid == 0) s_fail = 1;
+      __syncthreads();
+      break;
+    }
+    const double r = sqrt(d), ir = 1.0 / r;
+    __syncthreads();
+    if (tid == 0) G[(long long)j * cmax + j] = cmk(r, 0.0);
+    for (int i = j + 1 + tid; i < c; i += CT) G[(long long)j * cmax + i] = cscale(G[(long long)j * cmax + i], ir);
+    __syncthreads();
+    const int rest = c - j - 1;
+    for (int e = tid; e < rest * rest; e += CT) {
+      const int a = j + 1 + e / rest, b = j + 1 + e % rest;
+      if (b < a) continue;
+      cfms(G[(long long)a * cmax + b], cconj(G[(long long)j * cmax + a]), G[(long long)j * cmax + b]);
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  if (s_fail) {
+    if (tid == 0) ok[p] = 0;
+    return;
+  }
+  // R^-1 column by column (a warp per column, back substitution), stored transposed
+  for (int j = wid; j < c; j += CT / 32) {
+    for (int i = j; i >= 0; --i) {
+      double sr = 0.0, si = 0.0;
+      for (int k = i + 1 + lane; k <= j; k += 32) {
+        const cplx g = cmul(G[(long long)i * cmax + k], RT[(long long)j * cmax + k]);
+        sr += g.x;
+        si += g.y;
+      }
+      sr = warp_sum(sr);
+      si = warp_sum(si);
+      if (lane == 0) {
+        const cplx rhs = cmk((i == j ? 1.0 : 0.0) - sr, -si);
+        RT[(long long)j * cmax + i] = cscale(rhs, 1.0 / G[(long long)i * cmax + i].x);
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  // certificate on the first pass: ||R||_F ||R^-1||_F
+  if (first_pass) {
+    double a = 0.0, b = 0.0;
+    for (int e = tid; e < c * c; e += CT) {
+      const int i = e / c, k = e % c;
+      if (k >= i) a += cabs2(G[(long long)i * cmax + k]);
+      b += cabs2(RT[(long long)i * cmax + k]);
+    }
+    a = block_sum(a, sred);
+    b = block_sum(b, sred);
+    if (tid == 0) ok[p] = (sqrt(a) * sqrt(b) <= kappa_max) ? 1 : 0;
+  }
+}
+}  // namespace
+
+CIRR_API long long cirr_orth_cholqr2_ws_bytes(int n, int c, int nprob) {
+  return (long long)nprob * (2LL * n * c + 2LL * c * c) * 16 + 1024;
+}
+
+// W[p] (c x n rows: the columns of S) -> Qt[p] (cdim[p] orthonormal rows
+// spanning the same space, zero rows after), ok[p] = certificate.  W is not
+// modified.  ws: cirr_orth_cholqr2_ws_bytes.  No host synchronisation.
+CIRR_API int cirr_orth_cholqr2(const cplx* W, long long ldw, long long wstride, int n, int c, int nprob,
+                               const int* cdim, double kappa_max, cplx* Qt, long long ldq, long long qstride,
+                               void* ws, int* ok, cudaStream_t stream) {
+  if (n <= 0 || c <= 0 || nprob <= 0 || ldw < n || ldq < n || c > n) return CIRR_EINVAL;
+  cplx* S = reinterpret_cast<cplx*>(ws);               // n x c per problem
+  cplx* Q1 = S + (long long)nprob * n * c;             // c x n per problem
+  cplx* G = Q1 + (long long)nprob * n * c;             // c x c
+  cplx* RT = G + (long long)nprob * c * c;             // c x c
+  const long long nc = (long long)n * c, cc = (long long)c * c;
+  for (int pass = 0; pass < 2; ++pass) {
+    const cplx* Wi = pass == 0 ? W : Q1;
+    const long long ldi = pass == 0 ? ldw : n, si = pass == 0 ? wstride : nc;
+    cplx* Wo = pass == 0 ? Q1 : Qt;
+    const long long ldo = pass == 0 ? n : ldq, so = pass == 0 ? nc : qstride;
+    CIRR_TRY(cirr_transpose(0, Wi, ldi, si, c, n, nprob, S, c, nc, stream));
+    CIRR_TRY(cirr_gemm(1, c, c, n, nprob, Wi, ldi, si, S, c, nc, G, c, cc, 1.0, 0, stream));
+    chol_inv_kernel<<<nprob, CT, 0, stream>>>(G, cdim, c, kappa_max, RT, ok, pass == 0);
+    CIRR_CHECK_LAUNCH();
+    CIRR_TRY(cirr_gemm(0, c, n, c, nprob, RT, c, cc, Wi, ldi, si, Wo, ldo, so, 1.0, 0, stream));
+  }
+  return 0;
+}

@@ -41,6 +41,9 @@ from .errors import (
 
 PIVOT_REL_TOL = 1e-14  # linalg.py:26
 _DEBUG = bool(int(__import__("os").environ.get("CIRR_DEBUG", "0")))
+# certified CholeskyQR2 basis for refinement blocks (CIRR_CHOLQR=0 forces the SVD path)
+_CHOLQR = bool(int(__import__("os").environ.get("CIRR_CHOLQR", "1")))
+_CHOLQR_KAPPA = 1e5
 # CIRR_PIPELINE=1 overlaps the contours of a wave (run_pipelined: one host
 # thread + high-priority stream per contour).  Off by default: ~2 % faster on
 # config 4 (1.72 s vs 1.77 s host wall, profiles/r01_pipeline_r01.txt), not
@@ -595,7 +598,12 @@ class _Engine:
         for s, ci in enumerate(active):
             self.cs[ci].stats.n_linear_solves += len(self.cs[ci].fidx) * ks[s]
         del Y
-        return {ci: St[s] for s, ci in enumerate(active)}
+        out = {}
+        for s, ci in enumerate(active):
+            kc = rhs[ci].shape[1]
+            # drop the zero rows a narrower block got from the common width K
+            out[ci] = St[s] if kc == K else St[s].view(moments, K, n)[:, :kc].reshape(moments * kc, n)
+        return out
 
     def _dinv(self):
         """Inverses of the 128x128 diagonal blocks of every factor (made with the
@@ -622,7 +630,7 @@ class _Engine:
         return out
 
     # -- K4..K7 for one contour --------------------------------------------
-    def rayleigh_ritz(self, items: list, feast: bool = False) -> dict:
+    def rayleigh_ritz(self, items: list, feast: bool = False, refine: bool = False) -> dict:
         """K4..K7 for several contours at once (solvers.py:187-198, batched).
 
         items: [(ci, St)] with St the transposed block of contour ci (its columns
@@ -636,7 +644,7 @@ class _Engine:
             if feast:
                 basis = self._basis_cgs2(items, out)
             else:
-                basis = self._basis_svd(items, out)
+                basis = self._basis_svd(items, out, try_cholqr=refine and _CHOLQR)
             if basis is None:
                 return out
             items, Qt, ks = basis
@@ -677,7 +685,7 @@ class _Engine:
         kmax = int(ks.max())
         return items, Qt[:, :kmax].contiguous(), ks
 
-    def _basis_svd(self, items: list, out: dict):
+    def _basis_svd(self, items: list, out: dict, try_cholqr: bool = False):
         torch, n, cfg, st = self.torch, self.n, self.cfg, self.stream
         for ci, S_ in items:
             if S_.shape[0] == 0:
@@ -687,10 +695,32 @@ class _Engine:
             return out
         nb = len(items)
         cmax = max(S_.shape[0] for _, S_ in items)
-        # K4: one-sided Jacobi on all blocks (zero rows pad to cmax and are dropped)
         W = torch.zeros((nb, cmax, n), dtype=torch.complex128, device="cuda")
         for b, (_, S_) in enumerate(items):
             W[b, : S_.shape[0]].copy_(S_)
+        if try_cholqr and cmax <= n:
+            # refinement blocks are normally far from rank deficient: when
+            # ||R||_F ||R^-1||_F <= 1e5 certifies that no singular value is cut
+            # (rank_rel_tol <= 1e-12), the CholeskyQR2 basis spans the same
+            # space as the kept singular vectors (linalg.py:107-119)
+            cdim = _h2d(np.array([S_.shape[0] for _, S_ in items], dtype=np.int32))
+            Qt = torch.zeros((nb, cmax, n), dtype=torch.complex128, device="cuda")
+            ws = torch.empty(int(_lib.call("cirr_orth_cholqr2_ws_bytes", n, cmax, nb)), dtype=torch.uint8,
+                             device="cuda")
+            ok = torch.zeros(nb, dtype=torch.int32, device="cuda")
+            with _stage("rr.orth"):
+                _lib.call("cirr_orth_cholqr2", _ptr(W), n, cmax * n, n, cmax, nb, _ptr(cdim), _CHOLQR_KAPPA,
+                          _ptr(Qt), n, cmax * n, _ptr(ws), _ptr(ok), st)
+            if _DEBUG:
+                sv = [torch.linalg.svdvals(S_.T).cpu().numpy() for _, S_ in items]
+                print(f"[cirr] cholqr2 ok={ok.cpu().numpy().tolist()} kappa={[float(v[0] / v[-1]) for v in sv]}",
+                      flush=True)
+            if cfg.rank_rel_tol * _CHOLQR_KAPPA < 1.0 and bool(ok.cpu().numpy().all()):
+                if _DEBUG:
+                    print(f"[cirr] orth: c={cmax} nprob={nb} certified CholeskyQR2", flush=True)
+                ks = np.array([S_.shape[0] for _, S_ in items], dtype=np.int64)
+                return self._live(items, Qt, ks, out)
+        # K4: one-sided Jacobi on all blocks (zero rows pad to cmax and are dropped)
         sigma = torch.empty((nb, cmax), dtype=torch.float64, device="cuda")
         order = torch.empty((nb, cmax), dtype=torch.int32, device="cuda")
         kept = torch.empty(nb, dtype=torch.int32, device="cuda")
@@ -839,7 +869,7 @@ class _Engine:
             refine = {}
             for ci in active:
                 it_of[ci] = it
-            rr = self.rayleigh_ritz([(ci, stacked[ci]) for ci in active])
+            rr = self.rayleigh_ritz([(ci, stacked[ci]) for ci in active], refine=it > 0)
             for ci in list(active):
                 c = self.cs[ci]
                 r = rr[ci]
@@ -974,7 +1004,7 @@ class _Engine:
             for it in range(cfg.max_refine):
                 it_used = it
                 self._tl(ci, it, "rr0", lat)
-                r = self.rayleigh_ritz([(ci, st)])[ci]
+                r = self.rayleigh_ritz([(ci, st)], refine=it > 0)[ci]
                 self._tl(ci, it, "rr1", lat)
                 if r[0] == "rankzero":
                     break

@@ -155,6 +155,48 @@ def test_orth_graded(lib, n, c):
     assert resid <= 1e-12 * ref[0] + (ref[k] if k < c else 0.0)
 
 
+def _cholqr2(lib, mats, c, kappa_max=1e5):
+    """mats: list of n x c_p blocks (c_p <= c); returns (Qt rows, ok) per block."""
+    nb, n = len(mats), mats[0].shape[0]
+    Wh = np.zeros((nb, c, n), dtype=np.complex128)
+    for b, m in enumerate(mats):
+        Wh[b, : m.shape[1]] = m.T
+    W = cuda(Wh)
+    cd = cuda(np.array([m.shape[1] for m in mats], dtype=np.int32))
+    Qt = torch.empty((nb, c, n), dtype=torch.complex128, device="cuda")
+    ws = torch.empty(lib.call("cirr_orth_cholqr2_ws_bytes", n, c, nb), dtype=torch.uint8, device="cuda")
+    ok = torch.full((nb,), -1, dtype=torch.int32, device="cuda")
+    assert lib.call("cirr_orth_cholqr2", P(W), n, c * n, n, c, nb, P(cd), kappa_max, P(Qt), n, c * n, P(ws), P(ok),
+                    S()) == 0
+    assert np.array_equal(Wh, W.cpu().numpy())  # input untouched
+    return Qt.cpu().numpy(), ok.cpu().numpy()
+
+
+def test_orth_cholqr2(lib):
+    """Certified CholeskyQR2: orthonormal rows spanning range(S) when
+    ||R||_F ||R^-1||_F <= kappa_max; rejected (ok = 0) for a graded block
+    the SVD path must truncate, and for a zero block."""
+    n, c = 4096, 120
+    rng = np.random.default_rng(5)
+    good = []
+    for cp, cond in ((120, 1e3), (97, 1e2)):
+        U, _ = np.linalg.qr(rng.standard_normal((n, cp)) + 1j * rng.standard_normal((n, cp)))
+        V, _ = np.linalg.qr(rng.standard_normal((cp, cp)) + 1j * rng.standard_normal((cp, cp)))
+        good.append((U * np.logspace(0, -np.log10(cond), cp)) @ V.conj().T * 3.7)
+    Qt, ok = _cholqr2(lib, good, c)
+    assert ok.tolist() == [1, 1]
+    for b, m in enumerate(good):
+        cp = m.shape[1]
+        q = Qt[b, :cp].T
+        assert np.abs(q.conj().T @ q - np.eye(cp)).max() < 1e-13
+        assert cp == c or np.abs(Qt[b, cp:]).max() == 0.0
+        assert np.linalg.norm(m - q @ (q.conj().T @ m), 2) <= 1e-13 * np.linalg.norm(m, 2)
+    U, _ = np.linalg.qr(rng.standard_normal((n, c)) + 1j * rng.standard_normal((n, c)))
+    graded = (U * np.logspace(0, -12, c))
+    _, ok = _cholqr2(lib, [graded, np.zeros((n, c), dtype=np.complex128)], c)
+    assert ok.tolist() == [0, 0]
+
+
 @pytest.mark.parametrize("k", [1, 6, 64, 200])
 def test_small_eig_hermitian(lib, k):
     rng = np.random.default_rng(k)

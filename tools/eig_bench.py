@@ -103,3 +103,29 @@ def t_gen_split(k, nprob=2, reps=2):
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "split":
     for k in (120, 256):
         t_gen_split(k)
+
+
+def t_cholqr2(n, c, nprob=2, reps=3):
+    rng = np.random.default_rng(c)
+    u = np.linalg.qr(rng.standard_normal((n, c)) + 1j * rng.standard_normal((n, c)))[0]
+    m = (u * np.logspace(0, -3, c)) @ np.linalg.qr(rng.standard_normal((c, c)) + 0j)[0]
+    W = torch.from_numpy(np.ascontiguousarray(np.broadcast_to(m.T, (nprob, c, n)))).cuda()
+    cd = torch.full((nprob,), c, dtype=torch.int32, device="cuda")
+    Qt = torch.empty((nprob, c, n), dtype=torch.complex128, device="cuda")
+    ws = torch.empty(_lib.call("cirr_orth_cholqr2_ws_bytes", n, c, nprob), dtype=torch.uint8, device="cuda")
+    ok = torch.zeros(nprob, dtype=torch.int32, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ts = []
+    for _ in range(reps):
+        e0.record()
+        _lib.call("cirr_orth_cholqr2", W.data_ptr(), n, c * n, n, c, nprob, cd.data_ptr(), 1e5, Qt.data_ptr(), n,
+                  c * n, ws.data_ptr(), ok.data_ptr(), st)
+        e1.record(); torch.cuda.synchronize(); ts.append(e0.elapsed_time(e1))
+    print(f"cholqr2 n={n} c={c} nprob={nprob}: {min(ts):.2f} ms ok={ok.cpu().numpy()}", flush=True)
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "orth":
+    for c in (120, 256):
+        t_orth(4096, c)
+        t_cholqr2(4096, c)
