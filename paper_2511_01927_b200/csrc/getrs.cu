@@ -289,31 +289,70 @@ __global__ void permute_kernel(const cplx* __restrict__ R, long long ldr, long l
 }
 
 constexpr int MAXM = 16;
-// St[c][m*K + col][r] = sum_{j in contour c, in order} coef[j][m] * Y_j[r][col]
+constexpr int MTR = 32;       // rows per tile
+constexpr int MTC = 32;       // columns per tile
+// St[c][m*K + col][r] = sum_{j in contour c, in order} coef[j][m] * Y_j[r][col].
+// One CTA per (32-row x 32-column tile, contour): every node's tile is read as
+// 32 contiguous 512-byte row segments, the sums stay in registers (4 elements
+// per thread), and S^T is written back through a shared-memory transpose so
+// its rows (contiguous along r) are also written in 512-byte runs.  HBM-bound:
+// each Y_j is read exactly once.
+template <int MM>
 __global__ void __launch_bounds__(256) moments_kernel(const cplx* __restrict__ Y, long long ldy,
                                                       long long ystride, int n, int K,
                                                       const cplx* __restrict__ coef, int M,
                                                       const int* __restrict__ off, cplx* __restrict__ St,
                                                       long long ld_st, long long sstride) {
-  const int cidx = blockIdx.y;
-  const int r = blockIdx.x * 64 + (threadIdx.x & 63);
-  const int cg = threadIdx.x >> 6;
-  if (r >= n) return;
+  __shared__ cplx tile[MTC][MTR + 1];
+  const int cidx = blockIdx.z;
+  const int r0 = blockIdx.y * MTR, c0 = blockIdx.x * MTC;
+  const int tid = threadIdx.x;
   const int j0 = off[cidx], j1 = off[cidx + 1];
+  const int nj = j1 - j0;
+  const cplx* cj = coef + (long long)j0 * M;   // broadcast loads (same address in a warp)
+  // element q of this thread: row r0 + (tid >> 5) + 8 q, column c0 + (tid & 31)
+  const int cl = tid & 31, rl = tid >> 5;
+  const int col = c0 + cl;
+  cplx acc[4][MM];
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int m = 0; m < MM; ++m) acc[q][m] = cmk(0.0, 0.0);
+  bool ok[4];
+  long long base[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int r = r0 + rl + 8 * q;
+    ok[q] = r < n && col < K;
+    base[q] = (long long)r * ldy + col;
+  }
+  const cplx* Yc = Y + (long long)j0 * ystride;
+  for (int j = 0; j < nj; ++j, Yc += ystride) {
+    cplx y[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) y[q] = ok[q] ? Yc[base[q]] : cmk(0.0, 0.0);
+#pragma unroll
+    for (int m = 0; m < MM; ++m)
+      if (m < M) {
+        const cplx cf = cj[j * M + m];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) cfma(acc[q][m], cf, y[q]);
+      }
+  }
   cplx* S = St + (long long)cidx * sstride;
-  for (int col = cg; col < K; col += 4) {
-    cplx acc[MAXM];
 #pragma unroll
-    for (int m = 0; m < MAXM; ++m) acc[m] = cmk(0.0, 0.0);
-    for (int j = j0; j < j1; ++j) {
-      const cplx y = Y[(long long)j * ystride + (long long)r * ldy + col];
+  for (int m = 0; m < MM; ++m) {
+    if (m >= M) break;
 #pragma unroll
-      for (int m = 0; m < MAXM; ++m)
-        if (m < M) cfma(acc[m], coef[(long long)j * M + m], y);
+    for (int q = 0; q < 4; ++q) tile[cl][rl + 8 * q] = acc[q][m];
+    __syncthreads();
+    // write rows m*K + col of S^T: thread (rl', cl') writes S^T[c0 + rl' + 8q][r0 + cl']
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int cc = c0 + rl + 8 * q, rr = r0 + cl;
+      if (cc < K && rr < n) S[(long long)(m * K + cc) * ld_st + rr] = tile[rl + 8 * q][cl];
     }
-#pragma unroll
-    for (int m = 0; m < MAXM; ++m)
-      if (m < M) S[(long long)(m * K + col) * ld_st + r] = acc[m];
+    __syncthreads();
   }
 }
 
@@ -527,8 +566,12 @@ CIRR_API int cirr_moments(const cplx* Y, long long ldy, long long ystride, int n
                           cudaStream_t stream) {
   if (n <= 0 || K < 0 || M < 1 || M > MAXM || n_sets <= 0) return CIRR_EINVAL;
   if (K == 0) return 0;
-  dim3 g((n + 63) / 64, n_sets);
-  moments_kernel<<<g, 256, 0, stream>>>(Y, ldy, ystride, n, K, coef, M, off, St, ld_st, sstride);
+  dim3 g((K + MTC - 1) / MTC, (n + MTR - 1) / MTR, n_sets);
+  if (M <= 1) moments_kernel<1><<<g, 256, 0, stream>>>(Y, ldy, ystride, n, K, coef, M, off, St, ld_st, sstride);
+  else if (M <= 2) moments_kernel<2><<<g, 256, 0, stream>>>(Y, ldy, ystride, n, K, coef, M, off, St, ld_st, sstride);
+  else if (M <= 4) moments_kernel<4><<<g, 256, 0, stream>>>(Y, ldy, ystride, n, K, coef, M, off, St, ld_st, sstride);
+  else if (M <= 8) moments_kernel<8><<<g, 256, 0, stream>>>(Y, ldy, ystride, n, K, coef, M, off, St, ld_st, sstride);
+  else moments_kernel<16><<<g, 256, 0, stream>>>(Y, ldy, ystride, n, K, coef, M, off, St, ld_st, sstride);
   CIRR_CHECK_LAUNCH();
   return 0;
 }

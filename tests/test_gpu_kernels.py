@@ -155,6 +155,27 @@ def test_orth_graded(lib, n, c):
     assert resid <= 1e-12 * ref[0] + (ref[k] if k < c else 0.0)
 
 
+@pytest.mark.parametrize("M", [1, 3, 8])
+def test_moments(lib, M):
+    """S_m = sum_j coef[j][m] Y_j per contour, written transposed (K3 epilogue)."""
+    n, K = 300, 37
+    nodes = [5, 7]
+    rng = np.random.default_rng(M)
+    npen = sum(nodes)
+    Y = rng.standard_normal((npen, n, K)) + 1j * rng.standard_normal((npen, n, K))
+    coef = rng.standard_normal((npen, M)) + 1j * rng.standard_normal((npen, M))
+    off = np.concatenate([[0], np.cumsum(nodes)]).astype(np.int32)
+    St = torch.zeros((len(nodes), M * K, n), dtype=torch.complex128, device="cuda")
+    assert lib.call("cirr_moments", P(cuda(Y)), K, n * K, n, K, P(cuda(coef)), M, P(cuda(off)), len(nodes), P(St),
+                    n, M * K * n, S()) == 0
+    torch.cuda.synchronize()
+    got = St.cpu().numpy()
+    for c in range(len(nodes)):
+        for m in range(M):
+            ref = np.einsum("j,jrk->rk", coef[off[c]:off[c + 1], m], Y[off[c]:off[c + 1]])
+            assert np.allclose(got[c, m * K:(m + 1) * K].T, ref, rtol=0, atol=1e-13 * np.abs(ref).max())
+
+
 def _cholqr2(lib, mats, c, kappa_max=1e5):
     """mats: list of n x c_p blocks (c_p <= c); returns (Qt rows, ok) per block."""
     nb, n = len(mats), mats[0].shape[0]
