@@ -21,6 +21,8 @@ struct GemmArgs {
   const cplx* B; long long ldb, sB;
   cplx* C; long long ldc, sC;
   double alpha; int beta;             // beta: 0 -> overwrite, 1 -> accumulate
+  int splits = 1;                     // split-K slices (> 1: raw partial sums into part)
+  cplx* part = nullptr;               // splits x batch x M x N partials
 };
 
 constexpr int GBM = 64, GBN = 64, GBK = 16;
@@ -41,7 +43,10 @@ template <bool A_REAL, bool A_CONJ>
 __global__ void __launch_bounds__(GTHREADS, 2) gemm_kernel(GemmArgs g) {
   extern __shared__ __align__(16) unsigned char gsm[];
   using S = GemmSmem<A_REAL>;
-  const int b = blockIdx.z;
+  const int b = blockIdx.z / g.splits, ks = blockIdx.z % g.splits;
+  // k range of this slice (a multiple of GBK wide)
+  const int kc = ((g.K + g.splits - 1) / g.splits + GBK - 1) / GBK * GBK;
+  const int kbeg = ks * kc, kend = min(g.K, kbeg + kc);
   const int m0 = blockIdx.y * GBM, n0 = blockIdx.x * GBN;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = (warp >> 2) * 32, wn = (warp & 3) * 16;  // warp tile origin
@@ -57,7 +62,7 @@ __global__ void __launch_bounds__(GTHREADS, 2) gemm_kernel(GemmArgs g) {
       for (int i = 0; i < (GBM * GBK) / GTHREADS; ++i) {
         int e = tid + i * GTHREADS, r = e / GBK, c = e % GBK;
         int gr = m0 + r, gc = k0 + c;
-        bool p = gr < g.M && gc < g.K;
+        bool p = gr < g.M && gc < kend;
         const double* src = p ? Ag + (long long)gr * g.lda + gc : Ag;
         cp_async8(As + r * GAR_LD + c, src, p);
       }
@@ -68,7 +73,7 @@ __global__ void __launch_bounds__(GTHREADS, 2) gemm_kernel(GemmArgs g) {
       for (int i = 0; i < (GBM * GBK) / GTHREADS; ++i) {
         int e = tid + i * GTHREADS, r = e / GBK, c = e % GBK;
         int gr = m0 + r, gc = k0 + c;
-        bool p = gr < g.M && gc < g.K;
+        bool p = gr < g.M && gc < kend;
         const cplx* src = p ? Ag + (long long)gr * g.lda + gc : Ag;
         cp_async16(As + r * GA_LD + c, src, p);
       }
@@ -78,7 +83,7 @@ __global__ void __launch_bounds__(GTHREADS, 2) gemm_kernel(GemmArgs g) {
     for (int i = 0; i < (GBK * GBN) / GTHREADS; ++i) {
       int e = tid + i * GTHREADS, r = e / GBN, c = e % GBN;
       int gr = k0 + r, gc = n0 + c;
-      bool p = gr < g.K && gc < g.N;
+      bool p = gr < kend && gc < g.N;
       const cplx* src = p ? Bg + (long long)gr * g.ldb + gc : Bg;
       cp_async16(Bs + r * GB_LD + c, src, p);
     }
@@ -90,11 +95,11 @@ __global__ void __launch_bounds__(GTHREADS, 2) gemm_kernel(GemmArgs g) {
 #pragma unroll
     for (int j = 0; j < 2; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
 
-  const int ktiles = (g.K + GBK - 1) / GBK;
-  load_tile(0, 0);
+  const int ktiles = kend > kbeg ? (kend - kbeg + GBK - 1) / GBK : 0;
+  if (ktiles > 0) load_tile(0, kbeg);
   cp_async_commit();
   for (int kt = 0; kt < ktiles; ++kt) {
-    if (kt + 1 < ktiles) load_tile((kt + 1) & 1, (kt + 1) * GBK);
+    if (kt + 1 < ktiles) load_tile((kt + 1) & 1, kbeg + (kt + 1) * GBK);
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
@@ -152,7 +157,9 @@ __global__ void __launch_bounds__(GTHREADS, 2) gemm_kernel(GemmArgs g) {
       int c = n0 + wn + j * 8 + 2 * (lane & 3);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        if (c + h < g.N) {
+        if (c + h < g.N && g.splits > 1) {
+          g.part[((long long)(ks * g.batch + b) * g.M + r) * g.N + c + h] = cmk(cr[i][j][h], ci[i][j][h]);
+        } else if (c + h < g.N) {
           cplx* dst = Cg + (long long)r * g.ldc + c + h;
           cplx v = cmk(g.alpha * cr[i][j][h], g.alpha * ci[i][j][h]);
           if (g.beta) v = cadd(*dst, v);
@@ -163,22 +170,82 @@ __global__ void __launch_bounds__(GTHREADS, 2) gemm_kernel(GemmArgs g) {
   }
 }
 
-// Launch helper (host).  Returns 0 or a cudaError_t.
+// C = beta C + alpha sum_s part[s] in fixed slice order (deterministic split-K)
+static __global__ void splitk_reduce_kernel(GemmArgs g) {
+  const long long mn = (long long)g.M * g.N;
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= mn * g.batch) return;
+  const int b = (int)(e / mn);
+  const long long rc = e % mn;
+  const int r = (int)(rc / g.N), c = (int)(rc % g.N);
+  double sr = 0.0, si = 0.0;
+  for (int s = 0; s < g.splits; ++s) {
+    const cplx v = g.part[(long long)(s * g.batch + b) * mn + rc];
+    sr += v.x;
+    si += v.y;
+  }
+  cplx* dst = g.C + (long long)b * g.sC + (long long)r * g.ldc + c;
+  cplx v = cmk(g.alpha * sr, g.alpha * si);
+  if (g.beta) v = cadd(*dst, v);
+  *dst = v;
+}
+
+// Launch helper (host).  Returns 0 or a cudaError_t.  When the output tiles
+// cannot fill the GPU twice over and K is long (the Q^H (A Q) and Gram
+// products: 118 x 118 outputs over K = 4096), K is split into slices whose
+// partial sums go to a stream-ordered scratch buffer and are reduced in a
+// fixed order.
 template <bool A_REAL, bool A_CONJ>
-inline int gemm_launch(const GemmArgs& g, cudaStream_t stream) {
-  if (g.M <= 0 || g.N <= 0 || g.batch <= 0) return 0;
+inline int gemm_launch(const GemmArgs& g0, cudaStream_t stream) {
+  if (g0.M <= 0 || g0.N <= 0 || g0.batch <= 0) return 0;
   using S = GemmSmem<A_REAL>;
   static bool attr_set = false;
+  static int sms = 0;
   if (!attr_set) {
     cudaFuncSetAttribute(gemm_kernel<A_REAL, A_CONJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::total);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // keep the split-K scratch in the stream-ordered pool across synchronisations
+    // (the default release threshold of 0 would hand it back to the OS every time)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      unsigned long long keep = 1ull << 30;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
     attr_set = true;
   }
-  if (g.K <= 0) return 0;  // callers handle beta with K == 0 themselves
-  dim3 grid((g.N + GBN - 1) / GBN, (g.M + GBM - 1) / GBM, g.batch);
+  if (g0.K <= 0) return 0;  // callers handle beta with K == 0 themselves
+  GemmArgs g = g0;
+  const long long tiles = (long long)((g.N + GBN - 1) / GBN) * ((g.M + GBM - 1) / GBM) * g.batch;
+  int splits = 1;
+  if (tiles < 2LL * sms && g.K >= 8 * GBK) {
+    splits = (int)((2LL * sms + tiles - 1) / tiles);
+    splits = splits < g.K / (4 * GBK) ? splits : g.K / (4 * GBK);   // >= 4 k-tiles per slice
+    splits = splits < 64 ? splits : 64;
+  }
+  cudaError_t e;
+  if (splits > 1) {
+    g.splits = splits;
+    e = cudaMallocAsync(reinterpret_cast<void**>(&g.part), sizeof(cplx) * (size_t)splits * g.batch * g.M * g.N,
+                        stream);
+    if (e != cudaSuccess) return (int)e;
+  }
+  dim3 grid((g.N + GBN - 1) / GBN, (g.M + GBM - 1) / GBM, g.batch * g.splits);
   gemm_kernel<A_REAL, A_CONJ><<<grid, GTHREADS, S::total, stream>>>(g);
   cirr_note_launch();
-  cudaError_t e = cudaGetLastError();
-  return e == cudaSuccess ? 0 : (int)e;
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return (int)e;
+  if (splits > 1) {
+    const long long total = (long long)g.batch * g.M * g.N;
+    splitk_reduce_kernel<<<(unsigned)((total + 255) / 256), 256, 0, stream>>>(g);
+    cirr_note_launch();
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return (int)e;
+    e = cudaFreeAsync(g.part, stream);
+    if (e != cudaSuccess) return (int)e;
+  }
+  return 0;
 }
 
 }  // namespace cirr
