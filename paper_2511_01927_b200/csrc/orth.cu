@@ -516,6 +516,86 @@ __global__ void __launch_bounds__(CT) chol_inv_kernel(cplx* __restrict__ Gall, c
     if (tid == 0) ok[p] = (sqrt(a) * sqrt(b) <= kappa_max) ? 1 : 0;
   }
 }
+
+// The same for c <= CSM_MAX with the factor in shared memory (packed upper
+// triangle): Cholesky in place, then each thread back-substitutes one column
+// of R^-1 (no inter-thread dependence, coalesced stores of R^-1 by rows into
+// G), and a final transpose into RinvT.
+constexpr int CSM_MAX = 160;
+__device__ __forceinline__ int pk(int i, int k, int c) { return i * c - (i * (i - 1)) / 2 + (k - i); }
+
+__global__ void __launch_bounds__(CT) chol_inv_smem_kernel(cplx* __restrict__ Gall, const int* __restrict__ cdim,
+                                                           int cmax, double kappa_max, cplx* __restrict__ RinvT_all,
+                                                           int* __restrict__ ok, int first_pass) {
+  extern __shared__ __align__(16) cplx R[];
+  __shared__ double sred[32];
+  __shared__ int s_fail;
+  const int p = blockIdx.x, c = cdim[p], tid = threadIdx.x;
+  cplx* G = Gall + (long long)p * cmax * cmax;
+  cplx* RT = RinvT_all + (long long)p * cmax * cmax;
+  double dmax = 0.0;
+  for (int i = 0; i < c; ++i) dmax = fmax(dmax, G[(long long)i * cmax + i].x);
+  for (int e = tid; e < c * c; e += CT) {
+    const int i = e / c, k = e % c;
+    if (k >= i) R[pk(i, k, c)] = G[(long long)i * cmax + k];
+  }
+  if (tid == 0) s_fail = (c <= 0);
+  __syncthreads();
+  for (int j = 0; j < c; ++j) {
+    const double d = R[pk(j, j, c)].x;
+    if (!(d > 1e-300 && d > 1e-24 * dmax && d < 1e300)) {
+      if (tid == 0) s_fail = 1;
+      break;                                  // d is the same in every thread
+    }
+    const double r = sqrt(d), ir = 1.0 / r;
+    __syncthreads();
+    if (tid == 0) R[pk(j, j, c)] = cmk(r, 0.0);
+    for (int i = j + 1 + tid; i < c; i += CT) R[pk(j, i, c)] = cscale(R[pk(j, i, c)], ir);
+    __syncthreads();
+    const int rest = c - j - 1;
+    for (int e = tid; e < rest * rest; e += CT) {
+      const int a = j + 1 + e / rest, b = j + 1 + e % rest;
+      if (b < a) continue;
+      cfms(R[pk(a, b, c)], cconj(R[pk(j, a, c)]), R[pk(j, b, c)]);
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  for (int e = tid; e < cmax * cmax; e += CT) RT[e] = cmk(0.0, 0.0);
+  if (s_fail) {
+    if (tid == 0) ok[p] = 0;
+    return;
+  }
+  // column j of R^-1 (rows 0..j) into G[.][j]: back substitution, one thread per column
+  for (int j = tid; j < c; j += CT) {
+    for (int i = j; i >= 0; --i) {
+      double ar = (i == j) ? 1.0 : 0.0, ai = 0.0;
+      const int base = pk(i, 0, c);         // R[i][k] = R[base + k]
+      for (int k = i + 1; k <= j; ++k) {
+        const cplx rk = R[base + k], xk = G[(long long)k * cmax + j];
+        ar -= rk.x * xk.x - rk.y * xk.y;
+        ai -= rk.x * xk.y + rk.y * xk.x;
+      }
+      G[(long long)i * cmax + j] = cscale(cmk(ar, ai), 1.0 / R[base + i].x);
+    }
+  }
+  __syncthreads();
+  double a = 0.0, b = 0.0;
+  for (int e = tid; e < c * c; e += CT) {
+    const int i = e / c, k = e % c;
+    if (k >= i) {
+      const cplx x = G[(long long)i * cmax + k];
+      RT[(long long)k * cmax + i] = x;
+      b += cabs2(x);
+      a += cabs2(R[pk(i, k, c)]);
+    }
+  }
+  if (first_pass) {
+    a = block_sum(a, sred);
+    b = block_sum(b, sred);
+    if (tid == 0) ok[p] = (sqrt(a) * sqrt(b) <= kappa_max) ? 1 : 0;
+  }
+}
 }  // namespace
 
 CIRR_API long long cirr_orth_cholqr2_ws_bytes(int n, int c, int nprob) {
@@ -541,7 +621,18 @@ CIRR_API int cirr_orth_cholqr2(const cplx* W, long long ldw, long long wstride, 
     const long long ldo = pass == 0 ? n : ldq, so = pass == 0 ? nc : qstride;
     CIRR_TRY(cirr_transpose(0, Wi, ldi, si, c, n, nprob, S, c, nc, stream));
     CIRR_TRY(cirr_gemm(1, c, c, n, nprob, Wi, ldi, si, S, c, nc, G, c, cc, 1.0, 0, stream));
-    chol_inv_kernel<<<nprob, CT, 0, stream>>>(G, cdim, c, kappa_max, RT, ok, pass == 0);
+    if (c <= CSM_MAX) {
+      const int smem = (int)(sizeof(cplx) * ((long long)c * (c + 1) / 2));
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(chol_inv_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(sizeof(cplx) * CSM_MAX * (CSM_MAX + 1) / 2));
+        attr = true;
+      }
+      chol_inv_smem_kernel<<<nprob, CT, smem, stream>>>(G, cdim, c, kappa_max, RT, ok, pass == 0);
+    } else {
+      chol_inv_kernel<<<nprob, CT, 0, stream>>>(G, cdim, c, kappa_max, RT, ok, pass == 0);
+    }
     CIRR_CHECK_LAUNCH();
     CIRR_TRY(cirr_gemm(0, c, n, c, nprob, RT, c, cc, Wi, ldi, si, Wo, ldo, so, 1.0, 0, stream));
   }

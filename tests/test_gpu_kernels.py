@@ -217,14 +217,15 @@ def _cholqr2(lib, mats, c, kappa_max=1e5):
     return Qt.cpu().numpy(), ok.cpu().numpy()
 
 
-def test_orth_cholqr2(lib):
+@pytest.mark.parametrize("c", [120, 200])   # shared-memory factor (c <= 160) and the global-memory one
+def test_orth_cholqr2(lib, c):
     """Certified CholeskyQR2: orthonormal rows spanning range(S) when
     ||R||_F ||R^-1||_F <= kappa_max; rejected (ok = 0) for a graded block
     the SVD path must truncate, and for a zero block."""
-    n, c = 4096, 120
+    n = 4096
     rng = np.random.default_rng(5)
     good = []
-    for cp, cond in ((120, 1e3), (97, 1e2)):
+    for cp, cond in ((c, 1e3), (c - 23, 1e2)):
         U, _ = np.linalg.qr(rng.standard_normal((n, cp)) + 1j * rng.standard_normal((n, cp)))
         V, _ = np.linalg.qr(rng.standard_normal((cp, cp)) + 1j * rng.standard_normal((cp, cp)))
         good.append((U * np.logspace(0, -np.log10(cond), cp)) @ V.conj().T * 3.7)
