@@ -13,12 +13,15 @@ from .datasets import write_matrix_market  # noqa: F401
 from .errors import (  # noqa: F401
     CieigError,
     ConvergenceError,
+    CutUndefinedError,
     DeviceError,
     DimensionError,
+    EmptyPredictionError,
     FormatError,
     IndefiniteBError,
     NoEigenvaluesFound,
     ParameterError,
+    ParameterWarning,
     RankZeroError,
     SingularShiftError,
 )
@@ -36,5 +39,7 @@ from .solvers import (  # noqa: F401
     solve_multi,
     write_eigenvectors,
 )
+
+from .scouting import SCOUT_METHODS, RitzEstimate, calibrate_margin, scout, scout_contour  # noqa: F401
 
 __version__ = "0.1.0"
