@@ -148,6 +148,12 @@ int cirr_copy_cols(const cirr_cplx* in, long long ldi, long long si, const int* 
 int cirr_transpose(int conj, const cirr_cplx* in, long long ldi, long long si, int rows, int cols,
                    int batch, cirr_cplx* out, long long ldo, long long so, cudaStream_t stream);
 
+/* KDE sparsity upstream of the solve (kernels.py:38-67 kde_eval, used by
+ * contours.py:175-192): out[i] = sum_j exp(-coef (ts[i] - eigs[j])^2), summed in
+ * j order.  ts (nt), eigs (ne), out (nt): device float64. */
+int cirr_kde_eval(const double* ts, int nt, const double* eigs, int ne, double coef, double* out,
+                  cudaStream_t stream);
+
 /* number of kernels this library has launched since it was loaded (host counter) */
 long long cirr_launch_count(void);
 

@@ -40,6 +40,8 @@ from .solvers import (  # noqa: F401
     write_eigenvectors,
 )
 
+from .kde import Interval, IntervalPartition, SpectrumPrediction, construct_contours, find_cut  # noqa: F401
+from .kde import kde_eval, kde_sparsity  # noqa: F401
 from .scouting import SCOUT_METHODS, RitzEstimate, calibrate_margin, scout, scout_contour  # noqa: F401
 
 __version__ = "0.1.0"

@@ -50,6 +50,7 @@ SIGNATURES = {
     "cirr_gather_cols": [_P, _L, _L, _P, _L, _P, _I, _I, _I, _P, _L, _L, _P],
     "cirr_copy_cols": [_P, _L, _L, _P, _P, _P, _I, _I, _I, _P, _L, _L, _P],
     "cirr_transpose": [_I, _P, _L, _L, _I, _I, _I, _P, _L, _L, _P],
+    "cirr_kde_eval": [_P, _I, _P, _I, _D, _P, _P],
     "cirr_target_sm": [],
     "cirr_set_coop_ctas": [_I],
     "cirr_launch_count": [],

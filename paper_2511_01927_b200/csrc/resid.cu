@@ -138,3 +138,39 @@ CIRR_API int cirr_copy_cols(const cplx* in, long long ldi, long long si, const i
   CIRR_CHECK_LAUNCH();
   return 0;
 }
+
+// --------------------------------------------------------------------------
+// KDE sparsity for the contour construction upstream of the solve
+// (kernels.py:38-67, contours.py:175-192):
+// out[i] = sum_j exp(-coef * (ts[i] - eigs[j])^2), summed in j order.
+namespace {
+constexpr int KT = 256;
+__global__ void __launch_bounds__(KT) kde_kernel(const double* __restrict__ ts, int nt,
+                                                 const double* __restrict__ eigs, int ne, double coef,
+                                                 double* __restrict__ out) {
+  __shared__ double se[KT * 4];
+  const int i = blockIdx.x * KT + threadIdx.x;
+  const double t = i < nt ? ts[i] : 0.0;
+  double acc = 0.0;
+  for (int j0 = 0; j0 < ne; j0 += KT * 4) {
+    const int cnt = min(KT * 4, ne - j0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < cnt; e += KT) se[e] = eigs[j0 + e];
+    __syncthreads();
+    for (int e = 0; e < cnt; ++e) {
+      const double d = t - se[e];
+      acc += exp(-coef * d * d);
+    }
+  }
+  if (i < nt) out[i] = acc;
+}
+}  // namespace
+
+CIRR_API int cirr_kde_eval(const double* ts, int nt, const double* eigs, int ne, double coef, double* out,
+                           cudaStream_t stream) {
+  if (nt < 0 || ne < 0) return CIRR_EINVAL;
+  if (nt == 0) return 0;
+  kde_kernel<<<(nt + KT - 1) / KT, KT, 0, stream>>>(ts, nt, eigs, ne, coef, out);
+  CIRR_CHECK_LAUNCH();
+  return 0;
+}
