@@ -407,6 +407,124 @@ __global__ void __launch_bounds__(256) diag_solve_kernel(const cplx* __restrict_
   }
 }
 
+// Narrow right-hand sides (K <= 2, e.g. the Krylov scouts' single vector):
+// decoupled look-back triangular solve.  One CTA per 128-row block of one
+// pencil: it accumulates -T_ik y_k for the blocks k it depends on as soon as
+// each y_k is published (flag per block, written after a release fence), then
+// applies the precomputed inverse of its diagonal block and publishes y_i.
+// Dependencies only point to lower CTA indices (the backward solve walks the
+// blocks in reverse index order), so the launch order guarantees progress.
+// Every tile is read once, coalesced (a warp reads 32 consecutive columns of
+// 16 rows), and the chain costs one tile GEMV plus one handoff per block.
+constexpr int TV_BS = 128;       // block rows (= the diagonal-inverse block DB)
+constexpr int TV_T = 256;
+template <int KK, bool LOWER>
+__global__ void __launch_bounds__(TV_T) trsv_lookback_kernel(const cplx* __restrict__ LU, long long ld,
+                                                             long long pstride, int n, const cplx* __restrict__ Dinv,
+                                                             cplx* __restrict__ Y, long long ldy, long long ystride,
+                                                             int* __restrict__ flags) {
+  __shared__ cplx sacc[TV_BS][KK];
+  __shared__ cplx sy[TV_BS][KK];
+  const int nblk = gridDim.x, b = blockIdx.y;
+  const int bi = LOWER ? blockIdx.x : nblk - 1 - blockIdx.x;
+  const int i0 = bi * TV_BS, nb = min(TV_BS, n - i0);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const cplx* T = LU + (long long)b * pstride;
+  cplx* Yb = Y + (long long)b * ystride;
+  int* fl = flags + (long long)b * nblk;
+  // warp wid owns rows i0 + 16 wid .. +15; lane covers columns c0 + lane (+32, +64, +96)
+  cplx part[16][KK];
+#pragma unroll
+  for (int q = 0; q < 16; ++q)
+#pragma unroll
+    for (int c = 0; c < KK; ++c) part[q][c] = cmk(0.0, 0.0);
+  auto tile = [&](const cplx* Tt, long long ldt, int ncols, const cplx (*yv)[KK], int nrows_here) {
+    // part[q] += Tt[row q][col] * yv[col] over this lane's columns
+#pragma unroll
+    for (int cc = 0; cc < TV_BS; cc += 32) {
+      const int col = cc + lane;
+      cplx yc[KK];
+#pragma unroll
+      for (int c = 0; c < KK; ++c) yc[c] = col < ncols ? yv[col][c] : cmk(0.0, 0.0);
+      cplx t[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int r = wid * 16 + q;
+        t[q] = (r < nrows_here && col < ncols) ? Tt[(long long)r * ldt + col] : cmk(0.0, 0.0);
+      }
+#pragma unroll
+      for (int q = 0; q < 16; ++q)
+#pragma unroll
+        for (int c = 0; c < KK; ++c) cfma(part[q][c], t[q], yc[c]);
+    }
+  };
+  // dependencies in the order they are published: forward 0, 1, ..; backward nblk-1, nblk-2, ..
+  const int ndep = LOWER ? bi : nblk - 1 - bi;
+  for (int t = 0; t < ndep; ++t) {
+    const int kb = LOWER ? t : nblk - 1 - t;
+    const int k0 = kb * TV_BS, nk = min(TV_BS, n - k0);
+    if (tid == 0) {
+      while (*((volatile int*)(fl + kb)) == 0) __nanosleep(32);
+      __threadfence();
+    }
+    __syncthreads();
+    for (int e = tid; e < TV_BS * KK; e += TV_T) {
+      const int r = e / KK, c = e % KK;
+      sy[r][c] = r < nk ? Yb[(long long)(k0 + r) * ldy + c] : cmk(0.0, 0.0);
+    }
+    __syncthreads();
+    tile(T + (long long)i0 * ld + k0, ld, nk, sy, nb);
+    __syncthreads();
+  }
+  // acc = rhs - sum (lane partials reduced per row)
+#pragma unroll
+  for (int q = 0; q < 16; ++q)
+#pragma unroll
+    for (int c = 0; c < KK; ++c) {
+      const double re = warp_sum(part[q][c].x), im = warp_sum(part[q][c].y);
+      const int r = wid * 16 + q;
+      if (lane == 0) sacc[r][c] = r < nb ? csub(Yb[(long long)(i0 + r) * ldy + c], cmk(re, im)) : cmk(0.0, 0.0);
+    }
+  __syncthreads();
+  // y_i = Dinv_i acc
+#pragma unroll
+  for (int q = 0; q < 16; ++q)
+#pragma unroll
+    for (int c = 0; c < KK; ++c) part[q][c] = cmk(0.0, 0.0);
+  const cplx* D = Dinv + (((long long)b * nblk + bi) * 2 + (LOWER ? 0 : 1)) * TV_BS * TV_BS;
+  tile(D, TV_BS, nb, sacc, nb);
+#pragma unroll
+  for (int q = 0; q < 16; ++q)
+#pragma unroll
+    for (int c = 0; c < KK; ++c) {
+      const double re = warp_sum(part[q][c].x), im = warp_sum(part[q][c].y);
+      const int r = wid * 16 + q;
+      if (lane == 0 && r < nb) Yb[(long long)(i0 + r) * ldy + c] = cmk(re, im);
+    }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    *((volatile int*)(fl + bi)) = 1;
+  }
+}
+
+template <int KK>
+int trsv_lookback(const cplx* LU, int n, long long ld, long long pstride, int batch, const cplx* Dinv, cplx* Y,
+                  long long ldy, long long ystride, cudaStream_t stream) {
+  const int nblk = (n + TV_BS - 1) / TV_BS;
+  int* flags = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&flags), sizeof(int) * 2 * (size_t)nblk * batch, stream);
+  if (e != cudaSuccess) return (int)e;
+  if ((e = cudaMemsetAsync(flags, 0, sizeof(int) * 2 * (size_t)nblk * batch, stream)) != cudaSuccess) return (int)e;
+  dim3 g(nblk, batch);
+  trsv_lookback_kernel<KK, true><<<g, TV_T, 0, stream>>>(LU, ld, pstride, n, Dinv, Y, ldy, ystride, flags);
+  CIRR_CHECK_LAUNCH();
+  trsv_lookback_kernel<KK, false><<<g, TV_T, 0, stream>>>(LU, ld, pstride, n, Dinv, Y, ldy, ystride,
+                                                          flags + (long long)nblk * batch);
+  CIRR_CHECK_LAUNCH();
+  return (int)cudaFreeAsync(flags, stream);
+}
+
 }  // namespace
 
 // Y_j = (P_j^T L_j U_j)^{-1} R_{rhs_of[j]} for j < batch.  LU/perm from
@@ -453,6 +571,10 @@ CIRR_API int cirr_zgetrs_batched(const cplx* LU, int n, long long ld, long long 
   dim3 gp((unsigned)(((long long)n * K + 255) / 256), batch);
   permute_kernel<<<gp, 256, 0, stream>>>(R, ldr, rstride, rhs_of, perm, n, K, Y, ldy, ystride);
   CIRR_CHECK_LAUNCH();
+  if (Dinv != nullptr && K <= 2) {  // one or two RHS: look-back triangular solves
+    if (K == 1) return trsv_lookback<1>(LU, n, ld, pencil_stride, batch, Dinv, Y, ldy, ystride, stream);
+    return trsv_lookback<2>(LU, n, ld, pencil_stride, batch, Dinv, Y, ldy, ystride, stream);
+  }
   // right-looking blocked solves: per 64-row block a diagonal solve, then the
   // rank-64 update of the remaining rows on the TMA/DMMA GEMM (zgemm_sub_tma)
   // narrow RHS blocks (K <= 16) stay on the left-looking kernel: the 64-wide

@@ -79,7 +79,7 @@ def test_gemm(lib, kind, shape):
         assert err < 1e-13 * np.sqrt(K), (beta, err)
 
 
-@pytest.mark.parametrize("K,use_dinv", [(37, False), (100, False), (100, True)])
+@pytest.mark.parametrize("K,use_dinv", [(37, False), (100, False), (100, True), (1, True), (2, True), (1, False)])
 @pytest.mark.parametrize("n,batch", [(3, 2), (100, 3), (256, 4), (333, 2), (700, 2), (1024, 2)])
 def test_getrf_getrs(lib, n, batch, K, use_dinv):
     rng = np.random.default_rng(n)
