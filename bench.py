@@ -169,9 +169,9 @@ def cpu_sample(wl, refine_cols=None, passes=None, sample_pencils=6):
 
 def lu_traffic():
     """DRAM bytes of the LU stage per step, measured by ncu on this code
-    (profiles/r01_lu_traffic_v9.json: dram__bytes_read + dram__bytes_write over
+    (profiles/r01_lu_traffic_v14.json: dram__bytes_read + dram__bytes_write over
     every LU kernel of one solve_multi); null when the profile is absent."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_lu_traffic_v9.json")
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_lu_traffic_v14.json")
     try:
         with open(path) as f:
             d = json.load(f)
