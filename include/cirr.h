@@ -165,6 +165,11 @@ int cirr_target_sm(void);
  * (0 = whole GPU, the default).  Returns the previous cap. */
 int cirr_set_coop_ctas(int ctas);
 
+/* Concurrency: cap the CTAs of the persistent TMA GEMM (LU trailing updates and
+ * blocked solves) so latency-bound kernels of another stream find free SMs
+ * (0 = every SM, the default).  Returns the previous cap. */
+int cirr_set_gemm_ctas(int ctas);
+
 #ifdef __cplusplus
 }
 #endif

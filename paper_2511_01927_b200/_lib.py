@@ -53,11 +53,12 @@ SIGNATURES = {
     "cirr_kde_eval": [_P, _I, _P, _I, _D, _P, _P],
     "cirr_target_sm": [],
     "cirr_set_coop_ctas": [_I],
+    "cirr_set_gemm_ctas": [_I],
     "cirr_launch_count": [],
 }
 _RESTYPE = {"cirr_diag_inv_bytes": _L, "cirr_zgetrf_ws_bytes": _L, "cirr_small_eig_ws_bytes": _L, "cirr_launch_count": _L, "cirr_orth_ws_bytes": _L,
             "cirr_gen_eig_ws_bytes": _L, "cirr_gen_eig_vec_scratch_bytes": _L, "cirr_orth_cholqr2_ws_bytes": _L}
-_RAW = {"cirr_set_coop_ctas", "cirr_diag_inv_bytes", "cirr_zgetrf_ws_bytes", "cirr_small_eig_ws_bytes", "cirr_launch_count", "cirr_target_sm", "cirr_orth_ws_bytes",
+_RAW = {"cirr_set_coop_ctas", "cirr_set_gemm_ctas", "cirr_diag_inv_bytes", "cirr_zgetrf_ws_bytes", "cirr_small_eig_ws_bytes", "cirr_launch_count", "cirr_target_sm", "cirr_orth_ws_bytes",
         "cirr_gen_eig_ws_bytes", "cirr_gen_eig_vec_scratch_bytes", "cirr_orth_cholqr2_ws_bytes"}
 
 _lib = None

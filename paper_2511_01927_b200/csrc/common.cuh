@@ -24,6 +24,9 @@ int* cirr_tile_counter(cudaStream_t stream);
 // Cap on the CTAs of the cooperative latency-bound kernels (0 = whole GPU);
 // set by cirr_set_coop_ctas so they can run beside the bulk GEMMs.
 extern int g_cirr_coop_cap;
+// Cap on the CTAs of the persistent TMA GEMM (0 = every SM); set by
+// cirr_set_gemm_ctas so latency-bound kernels on other streams find free SMs.
+extern int g_cirr_gemm_cap;
 
 #define CIRR_CHECK_LAUNCH()                              \
   do {                                                   \

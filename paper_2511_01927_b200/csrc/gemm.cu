@@ -40,6 +40,15 @@ CIRR_API int cirr_gemm(int a_kind, int M, int N, int K, int batch,
 
 long long g_cirr_launches = 0;
 int g_cirr_coop_cap = 0;
+int g_cirr_gemm_cap = 0;
+
+// The persistent TMA GEMM uses at most `ctas` CTAs when > 0 (SMs left free for
+// the latency-bound kernels of another stream).  Returns the old cap.
+CIRR_API int cirr_set_gemm_ctas(int ctas) {
+  const int old = g_cirr_gemm_cap;
+  g_cirr_gemm_cap = ctas > 0 ? ctas : 0;
+  return old;
+}
 
 // Cooperative kernels (K4 orth, Hessenberg) use at most `ctas` CTAs when > 0,
 // leaving the rest of the GPU to GEMMs on other streams.  Returns the old cap.

@@ -328,7 +328,10 @@ static inline int zgemm_sub_maps(const CUtensorMap& mapA, const CUtensorMap& map
   SubGemmGeom g{M, N, Kr, batch, a_row0, a_col0, b_row0, b_col0, c_row0, c_col0, C, ldc, sC,
                 (M + PBM - 1) / PBM, (N + PBN - 1) / PBN, beta, a_bmul, a_badd, ctr};
   const long long tiles = (long long)g.tiles_m * g.tiles_n * batch;
-  const int grid = (int)(tiles < sms ? tiles : sms);
+  // persistent grid: every SM, or fewer when cirr_set_gemm_ctas leaves SMs to
+  // latency-bound kernels on other streams (the dynamic tile scheduler adapts)
+  const int cap = (g_cirr_gemm_cap > 0 && g_cirr_gemm_cap < sms) ? g_cirr_gemm_cap : sms;
+  const int grid = (int)(tiles < cap ? tiles : cap);
   zgemm_sub_tma<<<grid, PTHREADS, P_SMEM, stream>>>(mapA, mapB, mapC, g);
   cirr_note_launch();
   cudaError_t e = cudaGetLastError();

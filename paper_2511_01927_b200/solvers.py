@@ -51,6 +51,7 @@ _CHOLQR_KAPPA = 1e5
 _PIPELINE = bool(int(__import__("os").environ.get("CIRR_PIPELINE", "0")))
 _TIMELINE = bool(int(__import__("os").environ.get("CIRR_TIMELINE", "0")))
 _COOP_CAP = int(__import__("os").environ.get("CIRR_COOP_CAP", "64"))
+_GEMM_CAP = int(__import__("os").environ.get("CIRR_GEMM_CAP", "0"))
 
 
 
@@ -948,6 +949,7 @@ class _Engine:
 
         threads = [threading.Thread(target=worker, args=(ci,), daemon=True) for ci in range(len(self.cs))]
         old_cap = _lib.call("cirr_set_coop_ctas", _COOP_CAP)
+        old_gemm = _lib.call("cirr_set_gemm_ctas", _GEMM_CAP)
         for t in threads:
             t.start()
         try:
@@ -971,6 +973,7 @@ class _Engine:
             for r in ready:
                 r.set()
             _lib.call("cirr_set_coop_ctas", old_cap)
+            _lib.call("cirr_set_gemm_ctas", old_gemm)
         caller.wait_stream(bulk)
         for lat in self._lat_streams:
             caller.wait_stream(lat)
