@@ -558,10 +558,18 @@ class _Engine:
         coef = _h2d(np.concatenate(coefs, axis=0))
         off_t = _h2d(np.asarray(offs, dtype=np.int32))
         St = torch.empty((nset, moments * K, n), dtype=torch.complex128, device="cuda")
-        # solve contour ranges (each range is contiguous in the pencil buffer)
+        # solve contour ranges; ranges that are adjacent in the pencil buffer go
+        # in one batched call (rhs_of picks each pencil's block), so the small
+        # diagonal-block GEMMs of the blocked solve get twice the tiles per launch
+        runs = []
+        for s, (a, b) in enumerate(pen_idx):
+            if runs and runs[-1][1] == a:
+                runs[-1][1] = b
+            else:
+                runs.append([a, b])
         with _stage("solve"):
             pos = 0
-            for s, (a, b) in enumerate(pen_idx):
+            for a, b in runs:
                 cnt = b - a
                 dinv = self._dinv()
                 dptr = _ptr(dinv) + a * self._dinv_per_pencil if dinv is not None else 0
