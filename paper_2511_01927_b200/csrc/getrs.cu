@@ -13,6 +13,7 @@
 //     (deterministic, test_solvers.py:192-198) reading every Y_j once and
 //     writes S transposed (one contiguous row per column of S) for K4.
 #include "common.cuh"
+#include <cstdlib>
 #include "lu_gemm.cuh"
 
 namespace {
@@ -603,7 +604,8 @@ CIRR_API int cirr_zgetrs_batched(const cplx* LU, int n, long long ld, long long 
       // output tile reads only its own rows plus rows that GEMM does not
       // write); the rows below/above then get one trailing update with
       // k = 128 * SBK (fewer C-tile round trips per flop than k = 128).
-      const int SBK = n >= 2048 ? 4 : (n >= 512 ? 2 : 1);
+      static const int sbk_env = getenv("CIRR_SOLVE_SBK") ? atoi(getenv("CIRR_SOLVE_SBK")) : 0;
+      const int SBK = sbk_env > 0 ? sbk_env : (n >= 2048 ? 4 : (n >= 512 ? 2 : 1));
       auto apply_dinv = [&](int bi, bool lower) -> int {
         const int i0 = bi * DB, nb = min(DB, n - i0), na = min(SNB, nb), nb2 = nb - na;
         const int slot = bi * 2 + (lower ? 0 : 1);
