@@ -105,6 +105,13 @@ long long cirr_gen_eig_ws_bytes(int kmax, int nprob);
 long long cirr_gen_eig_vec_scratch_bytes(int kmax, int nprob, int smax);
 int cirr_gen_eig_values(const cirr_cplx* At, const cirr_cplx* Bt, const int* kdim, int kmax, int nprob, void* ws,
                         cirr_cplx* lam, int* info, cudaStream_t stream);
+/* As cirr_gen_eig_values, with shift hints for the QR iteration: hint[p]
+ * (ld hint_ld) holds hint_cnt[p] <= 256 approximate eigenvalues, e.g. the
+ * previous refinement round's; when the Wilkinson shift lies within 5 % of an
+ * unused hint the hint is the shift.  Same eigenvalues to rounding, fewer sweeps. */
+int cirr_gen_eig_values_hinted(const cirr_cplx* At, const cirr_cplx* Bt, const int* kdim, int kmax, int nprob,
+                               void* ws, cirr_cplx* lam, int* info, const cirr_cplx* hint, const int* hint_cnt,
+                               int hint_ld, cudaStream_t stream);
 int cirr_gen_eig_vectors(void* ws, const int* kdim, int kmax, int nprob, const cirr_cplx* lam, const int* sel,
                          const int* sel_cnt, int smax, void* scratch, cirr_cplx* S, long long lds, long long sS,
                          cudaStream_t stream);

@@ -45,6 +45,7 @@ SIGNATURES = {
     "cirr_gen_eig_ws_bytes": [_I, _I],
     "cirr_gen_eig_vec_scratch_bytes": [_I, _I, _I],
     "cirr_gen_eig_values": [_P, _P, _P, _I, _I, _P, _P, _P, _P],
+    "cirr_gen_eig_values_hinted": [_P, _P, _P, _I, _I, _P, _P, _P, _P, _P, _I, _P],
     "cirr_gen_eig_vectors": [_P, _P, _I, _I, _P, _P, _P, _I, _P, _P, _L, _L, _P],
     "cirr_residuals": [_P, _P, _L, _L, _I, _P, _L, _P, _I, _I, _P, _L, _P],
     "cirr_gather_cols": [_P, _L, _L, _P, _L, _P, _I, _I, _I, _P, _L, _L, _P],
