@@ -621,6 +621,15 @@ class _Engine:
         factorisation; each pencil's slice is contiguous)."""
         return self.dinv
 
+    def _bx(self, c, xi):
+        """B X for the inside Ritz vectors: the product kept from the residual
+        step when it belongs to this X, else computed."""
+        bx = getattr(c, "bx_dev", None)
+        c.bx_dev = None
+        if bx is not None and bx.shape == xi.shape:
+            return bx
+        return self.bmul(xi)
+
     def bmul(self, x):
         """B @ x for a device (n x k) complex block."""
         torch, n = self.torch, self.n
@@ -840,27 +849,26 @@ class _Engine:
         idx_t = _h2d(idx)
         cnt_t = _h2d(cnt)
         Xi = torch.zeros((nb, n, kin_max), dtype=torch.complex128, device="cuda")
+        Sin = torch.zeros((nb, kmax, kin_max), dtype=torch.complex128, device="cuda")
         if general_split:
             scr = torch.empty(int(_lib.call("cirr_gen_eig_vec_scratch_bytes", kmax, nb, kin_max)), dtype=torch.uint8,
                               device="cuda")
-            Sin = torch.zeros((nb, kmax, kin_max), dtype=torch.complex128, device="cuda")
             _lib.call("cirr_gen_eig_vectors", _ptr(gws), _ptr(kdim), kmax, nb, _ptr(lam), _ptr(idx_t), _ptr(cnt_t),
                       kin_max, _ptr(scr), _ptr(Sin), kin_max, kmax * kin_max, st)
-            _lib.call("cirr_gemm", 0, n, kin_max, kmax, nb, _ptr(Q), kmax, n * kmax, _ptr(Sin), kin_max,
-                      kmax * kin_max, _ptr(Xi), kin_max, n * kin_max, 1.0, 0, st)
-        else:
-            if X is None:
-                X = torch.empty((nb, n, kmax), dtype=torch.complex128, device="cuda")
-                _lib.call("cirr_gemm", 0, n, kmax, kmax, nb, _ptr(Q), kmax, n * kmax, _ptr(Sv), kmax, kk, _ptr(X),
-                          kmax, n * kmax, 1.0, 0, st)
-            _lib.call("cirr_gather_cols", _ptr(X), kmax, n * kmax, _ptr(idx_t), kin_max, _ptr(cnt_t), kin_max, n, nb,
-                      _ptr(Xi), kin_max, n * kin_max, st)
+        else:  # the inside columns of the projected eigenvectors
+            _lib.call("cirr_gather_cols", _ptr(Sv), kmax, kk, _ptr(idx_t), kin_max, _ptr(cnt_t), kin_max, kmax, nb,
+                      _ptr(Sin), kin_max, kmax * kin_max, st)
+        _lib.call("cirr_gemm", 0, n, kin_max, kmax, nb, _ptr(Q), kmax, n * kmax, _ptr(Sin), kin_max,
+                  kmax * kin_max, _ptr(Xi), kin_max, n * kin_max, 1.0, 0, st)
+        # A X = (A Q) s and B X = (B Q) s from the projection products: n x k x k_in
+        # instead of n x n x k_in (solvers.py:142-143 computes A X, B X directly;
+        # the two agree to rounding)
         AX = torch.empty_like(Xi)
         BX = torch.empty_like(Xi)
-        _lib.call("cirr_gemm", 2, n, kin_max, n, nb, _ptr(self.dp.a), n, 0, _ptr(Xi), kin_max, n * kin_max,
-                  _ptr(AX), kin_max, n * kin_max, 1.0, 0, st)
-        _lib.call("cirr_gemm", 2, n, kin_max, n, nb, _ptr(self.dp.b), n, 0, _ptr(Xi), kin_max, n * kin_max,
-                  _ptr(BX), kin_max, n * kin_max, 1.0, 0, st)
+        _lib.call("cirr_gemm", 0, n, kin_max, kmax, nb, _ptr(AQ), kmax, n * kmax, _ptr(Sin), kin_max,
+                  kmax * kin_max, _ptr(AX), kin_max, n * kin_max, 1.0, 0, st)
+        _lib.call("cirr_gemm", 0, n, kin_max, kmax, nb, _ptr(BQ), kmax, n * kmax, _ptr(Sin), kin_max,
+                  kmax * kin_max, _ptr(BX), kin_max, n * kin_max, 1.0, 0, st)
         lam_t = _h2d(lam_in)
         res = torch.zeros((nb, kin_max), dtype=torch.float64, device="cuda")
         _lib.call("cirr_residuals", _ptr(AX), _ptr(BX), kin_max, n * kin_max, n, _ptr(lam_t), kin_max, _ptr(cnt_t),
@@ -874,6 +882,7 @@ class _Engine:
                 lam_b = lam_b.real.copy()
             xall = X[b, :, : ks[b]].contiguous() if all_vectors else None
             out[ci] = ("ok", lam_b, Xi[b, :, :k_in].contiguous(), res_h[b, :k_in].copy(), xall)
+            self.cs[ci].bx_dev = BX[b, :, :k_in].contiguous()   # B X, the next refinement's right-hand side
         return out
 
     # -- the reference control flow (solvers.py:165-227) for all contours ----
@@ -919,7 +928,7 @@ class _Engine:
                         cfg.early_exit and c.settled(lam, res, cfg.tol)):
                     active.remove(ci)
                     continue
-                refine[ci] = self.bmul(xi)
+                refine[ci] = self._bx(c, xi)
             if not refine:
                 break
             stacked = self.apply(list(refine.keys()), refine, 1)
@@ -1049,7 +1058,7 @@ class _Engine:
                 if res.max() <= cfg.tol or it + 1 >= cfg.max_refine or (
                         cfg.early_exit and c.settled(lam, res, cfg.tol)):
                     break
-                rhs = self.bmul(xi)
+                rhs = self._bx(c, xi)
                 ev_rhs = lat.record_event()
                 with self._bulk_lock, torch.cuda.stream(self._bulk):
                     self._bulk.wait_event(ev_rhs)
