@@ -36,6 +36,14 @@ typedef double2 cirr_cplx;
 int cirr_assemble(const double* A, const double* B, int n, long long lda,
                   const cirr_cplx* z, int nz, cirr_cplx* pencils, long long ldp,
                   long long pencil_stride, double* maxabs, cudaStream_t stream);
+/* Complex-valued A and B (complex128, row-major, ld lda): pencils[j] = z[j] B - A
+ * with numpy's complex arithmetic (the reference's MatrixPencil carries complex
+ * CSR values, sparse.py:14-43); maxabs as cirr_assemble. */
+int cirr_assemble_c(const cirr_cplx* A, const cirr_cplx* B, int n, long long lda, const cirr_cplx* z, int nz,
+                    cirr_cplx* pencils, long long ldp, long long pencil_stride, double* maxabs,
+                    cudaStream_t stream);
+/* out[0] = max |A - A^H|, out[1] = max |A| of a complex128 matrix (sparse.py:83-87). */
+int cirr_hermitian_c(const cirr_cplx* A, int n, long long lda, double* out, cudaStream_t stream);
 
 /* sparse.py:83-87 (is_hermitian) for real A: out[0] = max|A - A^T|, out[1] = max|A|. */
 int cirr_symmetry(const double* A, int n, long long lda, double* out, cudaStream_t stream);

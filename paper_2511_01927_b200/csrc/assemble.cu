@@ -120,3 +120,112 @@ CIRR_API int cirr_assemble(const double* A, const double* B, int n, long long ld
   CIRR_CHECK_LAUNCH();
   return 0;
 }
+
+// --------------------------------------------------------------------------
+// Complex-valued A and B (the reference's MatrixPencil holds complex128 CSR
+// values, sparse.py:14-43; complex Hermitian pencils are valid input).
+namespace {
+__global__ void __launch_bounds__(kThreads) assemble_c_kernel(
+    const cplx* __restrict__ A, const cplx* __restrict__ B, int n, long long lda,
+    const cplx* __restrict__ z, int nz, cplx* __restrict__ P, long long ldp, long long pstride,
+    unsigned long long* __restrict__ maxabs_bits) {
+  __shared__ double wmax[kThreads / 32][kGroup];
+  const long long total = (long long)n * n;
+  const long long base = (long long)blockIdx.x * kChunk;
+  const int j0 = blockIdx.y * kGroup;
+  cplx a[kPerThread], b[kPerThread];
+  long long dst[kPerThread];
+  bool ok[kPerThread];
+#pragma unroll
+  for (int e = 0; e < kPerThread; ++e) {
+    long long idx = base + (long long)e * kThreads + threadIdx.x;
+    ok[e] = idx < total;
+    long long r = ok[e] ? idx / n : 0, c = ok[e] ? idx - r * n : 0;
+    dst[e] = r * ldp + c;
+    a[e] = ok[e] ? A[r * lda + c] : cmk(0.0, 0.0);
+    b[e] = ok[e] ? B[r * lda + c] : cmk(0.0, 0.0);
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int g = 0; g < kGroup; ++g) {
+    const int j = j0 + g;
+    if (j >= nz) break;
+    const cplx zj = z[j];
+    cplx* Pj = P + (long long)j * pstride;
+    double m = 0.0;
+#pragma unroll
+    for (int e = 0; e < kPerThread; ++e) {
+      if (ok[e]) {
+        // numpy's complex product (rounded products, rounded sums, no FMA), then - A
+        const double pr = __dsub_rn(__dmul_rn(zj.x, b[e].x), __dmul_rn(zj.y, b[e].y));
+        const double pi = __dadd_rn(__dmul_rn(zj.x, b[e].y), __dmul_rn(zj.y, b[e].x));
+        const cplx v = cmk(__dsub_rn(pr, a[e].x), __dsub_rn(pi, a[e].y));
+        Pj[dst[e]] = v;
+        m = fmax(m, hypot(v.x, v.y));
+      }
+    }
+    m = warp_max(m);
+    if (lane == 0) wmax[wid][g] = m;
+  }
+  __syncthreads();
+  if (threadIdx.x < kGroup && j0 + threadIdx.x < nz) {
+    double m = 0.0;
+    for (int w = 0; w < kThreads / 32; ++w) m = fmax(m, wmax[w][threadIdx.x]);
+    atomicMax(maxabs_bits + j0 + threadIdx.x, (unsigned long long)__double_as_longlong(m));
+  }
+}
+
+// out[0] = max_ij |A_ij - conj(A_ji)| (diagonal included), out[1] = max_ij |A_ij|
+__global__ void hermitian_c_kernel(const cplx* __restrict__ A, int n, long long lda,
+                                   unsigned long long* __restrict__ out) {
+  __shared__ double red[2][8];
+  double d = 0.0, m = 0.0;
+  const long long total = (long long)n * n;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long r = e / n, c = e - r * n;
+    const cplx a = A[r * lda + c];
+    m = fmax(m, cabs(a));
+    if (c >= r) d = fmax(d, cabs(csub(a, cconj(A[c * lda + r]))));
+  }
+  d = warp_max(d);
+  m = warp_max(m);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) { red[0][wid] = d; red[1][wid] = m; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) { d = fmax(d, red[0][w]); m = fmax(m, red[1][w]); }
+    d = fmax(d, red[0][0]);
+    m = fmax(m, red[1][0]);
+    atomicMax(out, (unsigned long long)__double_as_longlong(d));
+    atomicMax(out + 1, (unsigned long long)__double_as_longlong(m));
+  }
+}
+}  // namespace
+
+// pencils[j] = z[j]*B - A for complex128 A, B (row-major, ld lda); maxabs as cirr_assemble.
+CIRR_API int cirr_assemble_c(const cplx* A, const cplx* B, int n, long long lda, const cplx* z, int nz,
+                             cplx* pencils, long long ldp, long long pencil_stride, double* maxabs,
+                             cudaStream_t stream) {
+  if (n <= 0 || nz <= 0 || lda < n || ldp < n) return CIRR_EINVAL;
+  cudaError_t e = cudaMemsetAsync(maxabs, 0, sizeof(double) * nz, stream);
+  if (e != cudaSuccess) return (int)e;
+  const long long total = (long long)n * n;
+  dim3 grid((unsigned)((total + kChunk - 1) / kChunk), (unsigned)((nz + kGroup - 1) / kGroup));
+  assemble_c_kernel<<<grid, kThreads, 0, stream>>>(A, B, n, lda, z, nz, pencils, ldp, pencil_stride,
+                                                    reinterpret_cast<unsigned long long*>(maxabs));
+  CIRR_CHECK_LAUNCH();
+  return 0;
+}
+
+// out[0] = max |A - A^H|, out[1] = max |A| for a complex128 row-major matrix
+// (the Hermitian test of sparse.py:83-87 on device).
+CIRR_API int cirr_hermitian_c(const cplx* A, int n, long long lda, double* out, cudaStream_t stream) {
+  if (n <= 0 || lda < n) return CIRR_EINVAL;
+  cudaError_t e = cudaMemsetAsync(out, 0, 2 * sizeof(double), stream);
+  if (e != cudaSuccess) return (int)e;
+  long long total = (long long)n * n;
+  int blocks = (int)((total + 255) / 256 < 148 * 8 ? (total + 255) / 256 : 148 * 8);
+  hermitian_c_kernel<<<blocks, 256, 0, stream>>>(A, n, lda, reinterpret_cast<unsigned long long*>(out));
+  CIRR_CHECK_LAUNCH();
+  return 0;
+}

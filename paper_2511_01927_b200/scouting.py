@@ -61,8 +61,7 @@ class _Device:
         minpiv = torch.empty(1, dtype=torch.float64, device="cuda")
         info = torch.empty(1, dtype=torch.int32, device="cuda")
         z = _h2d(np.zeros(1, dtype=np.complex128))
-        _lib.call("cirr_assemble", _ptr(dp.a), _ptr(dp.b), n, n, _ptr(z), 1, _ptr(self.fac), n, n * n,
-                  _ptr(maxabs), st)
+        dp.assemble(z, 1, self.fac, maxabs, st)
         lws = torch.empty(int(_lib.call("cirr_zgetrf_ws_bytes", n, 1)), dtype=torch.uint8, device="cuda")
         _lib.call("cirr_zgetrf_batched", _ptr(self.fac), n, n, n * n, 1, _ptr(ipiv), _ptr(self.perm),
                   _ptr(minpiv), _ptr(info), _ptr(lws), st)
@@ -90,7 +89,8 @@ class _Device:
     def bmul(self, x):
         n = self.n
         out = self.new(x.shape[1])
-        _lib.call("cirr_gemm", 2, n, x.shape[1], n, 1, _ptr(self.dp.b), n, 0, _ptr(x), x.shape[1], 0, _ptr(out),
+        _lib.call("cirr_gemm", self.dp.gemm_kind, n, x.shape[1], n, 1, _ptr(self.dp.b), n, 0, _ptr(x), x.shape[1], 0,
+                  _ptr(out),
                   x.shape[1], 0, 1.0, 0, _stream())
         return out
 

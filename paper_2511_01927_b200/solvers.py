@@ -196,7 +196,9 @@ def _dense(m) -> np.ndarray:
 
 
 class DevicePencil:
-    """A, B resident in HBM as dense real float64 (row-major)."""
+    """A, B resident in HBM, dense and row-major: real float64 when both are
+    real (the configs), complex128 when either has a nonzero imaginary part
+    (the reference's MatrixPencil holds complex128 CSR values, sparse.py:14-43)."""
 
     def __init__(self, a, b, hermitian: bool | None = None):
         torch = _torch()
@@ -207,16 +209,26 @@ class DevicePencil:
         b = np.asarray(_dense(b))
         if a.ndim != 2 or a.shape[0] != a.shape[1] or a.shape != b.shape:
             raise DimensionError("pencil matrices must be square and equally sized")
-        if np.iscomplexobj(a) and np.abs(a.imag).max(initial=0.0) != 0.0:
-            raise NotImplementedError("complex-valued A is not supported by the device path yet")
-        if np.iscomplexobj(b) and np.abs(b.imag).max(initial=0.0) != 0.0:
-            raise NotImplementedError("complex-valued B is not supported by the device path yet")
-        a = np.ascontiguousarray(a.real, dtype=np.float64)
-        b = np.ascontiguousarray(b.real, dtype=np.float64)
+        cx = any(np.iscomplexobj(m) and np.abs(m.imag).max(initial=0.0) != 0.0 for m in (a, b))
+        self.complex = cx
+        dt = np.complex128 if cx else np.float64
+        a = np.ascontiguousarray(a if cx else a.real, dtype=dt)
+        b = np.ascontiguousarray(b if cx else b.real, dtype=dt)
         self.n = a.shape[0]
         self.a = torch.from_numpy(a).to("cuda")
         self.b = torch.from_numpy(b).to("cuda")
         self.hermitian = bool(hermitian) if hermitian else self._device_symmetric()
+
+    @property
+    def gemm_kind(self) -> int:
+        """cirr_gemm operand kind of A and B: 2 = real float64, 0 = complex128."""
+        return 0 if self.complex else 2
+
+    def assemble(self, z, cnt: int, pencils, maxabs, stream):
+        """K1: pencils[j] = z[j] B - A for cnt shifts (cirr_assemble / cirr_assemble_c)."""
+        n = self.n
+        _lib.call("cirr_assemble_c" if self.complex else "cirr_assemble", _ptr(self.a), _ptr(self.b), n, n, _ptr(z),
+                  cnt, _ptr(pencils), n, n * n, _ptr(maxabs), stream)
 
     def _device_symmetric(self, rel_tol: float = 1e-12) -> bool:
         """sparse.py:83-87 applied to A and B on the device (a flag of False or
@@ -224,21 +236,26 @@ class DevicePencil:
         torch = _torch()
         out = torch.empty((2, 2), dtype=torch.float64, device="cuda")
         st = _stream()
-        _lib.call("cirr_symmetry", _ptr(self.a), self.n, self.n, _ptr(out[0]), st)
-        _lib.call("cirr_symmetry", _ptr(self.b), self.n, self.n, _ptr(out[1]), st)
+        fn = "cirr_hermitian_c" if self.complex else "cirr_symmetry"
+        _lib.call(fn, _ptr(self.a), self.n, self.n, _ptr(out[0]), st)
+        _lib.call(fn, _ptr(self.b), self.n, self.n, _ptr(out[1]), st)
         o = out.cpu().numpy()
         return bool(all(o[i, 0] <= rel_tol * max(o[i, 1], 1e-300) for i in range(2)))
 
     def _from_tensors(self, torch, a, b, hermitian):
-        """Real float64 tensors (host, ideally pinned, or device): copied with
-        non_blocking H2D; the Hermitian flag must be given or is computed on host."""
+        """float64 or complex128 tensors (host, ideally pinned, or device): copied
+        with non_blocking H2D; the Hermitian flag must be given or is computed on
+        the device."""
         if a.dim() != 2 or a.shape[0] != a.shape[1] or a.shape != b.shape:
             raise DimensionError("pencil matrices must be square and equally sized")
-        if a.dtype != torch.float64 or b.dtype != torch.float64:
-            raise NotImplementedError("tensor pencils must be real float64")
+        ok = (torch.float64, torch.complex128)
+        if a.dtype not in ok or b.dtype not in ok:
+            raise NotImplementedError("tensor pencils must be float64 or complex128")
+        self.complex = a.dtype == torch.complex128 or b.dtype == torch.complex128
+        dt = torch.complex128 if self.complex else torch.float64
         self.n = a.shape[0]
-        self.a = a.to("cuda", non_blocking=True).contiguous()
-        self.b = b.to("cuda", non_blocking=True).contiguous()
+        self.a = a.to("cuda", non_blocking=True).to(dt).contiguous()
+        self.b = b.to("cuda", non_blocking=True).to(dt).contiguous()
         self.hermitian = bool(hermitian) if hermitian else self._device_symmetric()
 
     @classmethod
@@ -358,7 +375,7 @@ def _h2d(x: np.ndarray):
 
 
 class _Contour:
-    def __init__(self, idx, contour, cfg: SolverConfig, seed: int, n: int):
+    def __init__(self, idx, contour, cfg: SolverConfig, seed: int, n: int, complex_pencil: bool = False):
         self.idx = idx
         self.contour = contour
         rule = quadrature_for(contour, cfg.n_q)
@@ -379,8 +396,8 @@ class _Contour:
         # factored nodes (all of them unless the conjugate-pair variant applies)
         self.half = False
         self.fidx = np.arange(len(self.nodes))
-        if cfg.conjugate_pairs:
-            self._pair()
+        if cfg.conjugate_pairs and not complex_pencil:
+            self._pair()      # M(conj z) = conj(M(z)) needs real A and B
 
     def _pair(self):
         """fidx = upper-half nodes; mate[j] = position in fidx of conj(z_j)."""
@@ -502,8 +519,7 @@ class _Engine:
             return
         z = _h2d(nodes)
         with _stage("assemble"):
-            _lib.call("cirr_assemble", _ptr(self.dp.a), _ptr(self.dp.b), n, n, _ptr(z), cnt,
-                      _ptr(self.pencils[a]), n, n * n, _ptr(self.maxabs[a:]), self.stream)
+            self.dp.assemble(z, cnt, self.pencils[a], self.maxabs[a:], self.stream)
         _work("assemble_bytes", cnt * n * n * 16 + 2 * n * n * 8)
         with _stage("lu"):
             lws = torch.empty(int(_lib.call("cirr_zgetrf_ws_bytes", n, cnt)), dtype=torch.uint8, device="cuda")
@@ -636,7 +652,7 @@ class _Engine:
         k = x.shape[1]
         out = torch.empty((n, k), dtype=torch.complex128, device="cuda")
         if k:
-            _lib.call("cirr_gemm", 2, n, k, n, 1, _ptr(self.dp.b), n, 0, _ptr(x), k, 0, _ptr(out), k, 0,
+            _lib.call("cirr_gemm", self.dp.gemm_kind, n, k, n, 1, _ptr(self.dp.b), n, 0, _ptr(x), k, 0, _ptr(out), k, 0,
                       1.0, 0, self.stream)
         return out
 
@@ -645,7 +661,7 @@ class _Engine:
         k = x.shape[1]
         out = torch.empty((n, k), dtype=torch.complex128, device="cuda")
         if k:
-            _lib.call("cirr_gemm", 2, n, k, n, 1, _ptr(self.dp.a), n, 0, _ptr(x), k, 0, _ptr(out), k, 0,
+            _lib.call("cirr_gemm", self.dp.gemm_kind, n, k, n, 1, _ptr(self.dp.a), n, 0, _ptr(x), k, 0, _ptr(out), k, 0,
                       1.0, 0, self.stream)
         return out
 
@@ -765,9 +781,9 @@ class _Engine:
             _lib.call("cirr_transpose", 0, _ptr(Qt), n, kmax * n, kmax, n, nb, _ptr(Q), kmax, n * kmax, st)
             AQ = torch.empty((nb, n, kmax), dtype=torch.complex128, device="cuda")
             BQ = torch.empty_like(AQ)
-            _lib.call("cirr_gemm", 2, n, kmax, n, nb, _ptr(self.dp.a), n, 0, _ptr(Q), kmax, n * kmax, _ptr(AQ), kmax,
+            _lib.call("cirr_gemm", self.dp.gemm_kind, n, kmax, n, nb, _ptr(self.dp.a), n, 0, _ptr(Q), kmax, n * kmax, _ptr(AQ), kmax,
                       n * kmax, 1.0, 0, st)
-            _lib.call("cirr_gemm", 2, n, kmax, n, nb, _ptr(self.dp.b), n, 0, _ptr(Q), kmax, n * kmax, _ptr(BQ), kmax,
+            _lib.call("cirr_gemm", self.dp.gemm_kind, n, kmax, n, nb, _ptr(self.dp.b), n, 0, _ptr(Q), kmax, n * kmax, _ptr(BQ), kmax,
                       n * kmax, 1.0, 0, st)
             At = torch.empty((nb, kmax, kmax), dtype=torch.complex128, device="cuda")
             Bt = torch.empty_like(At)
@@ -1180,7 +1196,7 @@ def _hbm_budget(n: int, cstates: list) -> int:
 def _run_contours(pencil, contours, cfg, seeds, moments_override=None, solver: str = "cirr"):
     cfg = _cfg_view(cfg)
     dp = DevicePencil.of(pencil)
-    cstates = [_Contour(i, c, cfg, s, dp.n) for i, (c, s) in enumerate(zip(contours, seeds))]
+    cstates = [_Contour(i, c, cfg, s, dp.n, dp.complex) for i, (c, s) in enumerate(zip(contours, seeds))]
     moments = cfg.n_moments if moments_override is None else moments_override
     for wave in _waves(cstates, dp.n, _hbm_budget(dp.n, cstates)):
         eng = _Engine(dp, wave, cfg)
