@@ -26,7 +26,7 @@ __device__ __forceinline__ void rr_pair(int round, int k, int cp, int& p, int& q
 }
 
 constexpr int HT = 256;
-constexpr int JB = 8;   // rows per Jacobi block
+constexpr int JB_MAX = 8;   // rows per Jacobi block (fewer for wide blocks: 4 * jb rows of length c in smem)
 __device__ long long g_orth_phase[4];
 #define ORTH_MARK(i) do { if (blockIdx.x == 0 && threadIdx.x == 0) g_orth_phase[i] = clock64(); } while (0)
 
@@ -50,7 +50,7 @@ __global__ void __launch_bounds__(HT) qr_jacobi_kernel(cplx* __restrict__ W, lon
                                                         long long ldq, long long qstride, unsigned* bar,
                                                         int* counters, cplx* __restrict__ Xc,
                                                         cplx* __restrict__ Jt, cplx* __restrict__ tau,
-                                                        int max_sweeps, double tol, int* sweeps_out) {
+                                                        int max_sweeps, double tol, int* sweeps_out, int JB) {
   __shared__ double red[4][HT / 32];
   __shared__ double sred[32];
   const int G = gridDim.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -322,7 +322,9 @@ CIRR_API int cirr_orth(cplx* W, long long ldw, long long wstride, int n, int c, 
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const size_t jsmem = sizeof(cplx) * 4 * JB * (size_t)c;
+  int jb = JB_MAX;
+  while (jb > 1 && sizeof(cplx) * 4 * jb * (size_t)c > 227 * 1024) jb >>= 1;
+  const size_t jsmem = sizeof(cplx) * 4 * jb * (size_t)c;
   if (jsmem > 227 * 1024) return CIRR_EINVAL;
   cudaFuncSetAttribute(qr_jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jsmem);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qr_jacobi_kernel, HT, jsmem);
@@ -338,7 +340,7 @@ CIRR_API int cirr_orth(cplx* W, long long ldw, long long wstride, int n, int c, 
   double tol = 16.0 * sqrt((double)c) * 1.1102230246251565e-16;
   int max_sweeps = 60;
   void* args[] = {&W, &ldw, &wstride, &n, &c, &nprob, &rel_tol, &sigma, &order, &kept, &Qt, &ldq, &qstride,
-                  &bar, &counters, &Xc, &Jt, &tau, &max_sweeps, &tol, &sweeps_out};
+                  &bar, &counters, &Xc, &Jt, &tau, &max_sweeps, &tol, &sweeps_out, &jb};
   e = cudaLaunchCooperativeKernel((void*)qr_jacobi_kernel, dim3(grid), dim3(HT), args, jsmem, stream);
   cirr_note_launch();
   if (e != cudaSuccess) return (int)e;

@@ -96,3 +96,23 @@ def test_complex_kernels():
     o = out.cpu().numpy()
     assert o[0] == pytest.approx(np.abs(hm - hm.conj().T).max(), rel=1e-12)
     assert o[1] == pytest.approx(np.abs(hm).max(), rel=1e-15)
+
+
+def test_wide_moment_block_default_source_cols():
+    """A contour expecting 100 eigenvalues with the reference's default
+    source_cols (max(8, 2 * expected) = 200, solvers.py:41-44) and M = 4: the
+    moment block is 800 columns wide (K4 with smaller Jacobi blocks)."""
+    from paper_2511_01927_b200 import Contour, DevicePencil, SolverConfig, solve_multi
+    n = 1200
+    a = 2.0 * np.eye(n) - np.eye(n, k=1) - np.eye(n, k=-1)
+    b = np.eye(n)
+    w = 2.0 - 2.0 * np.cos(np.arange(1, n + 1) * np.pi / (n + 1))
+    lo, hi = 0.5 * (w[199] + w[200]), 0.5 * (w[299] + w[300])
+    c = Contour(shape="circle", center=complex(0.5 * (lo + hi), 0.0), radius=0.5 * (hi - lo), expected_count=100)
+    cfg = SolverConfig(n_q=32, n_moments=4, tol=1e-10)
+    assert cfg.cols_for(100) == 200
+    m = solve_multi(DevicePencil(a, b), [c], cfg, seed=0)
+    r = m.results[0]
+    assert r is not None and len(r.eigenvalues) == 100
+    assert _match(r.eigenvalues, w[200:300]) <= 1e-8
+    assert r.residuals.max() <= 1e-10

@@ -125,7 +125,7 @@ def test_getrf_singular(lib):
     assert info.item() == 6 and mp.item() == 0.0
 
 
-@pytest.mark.parametrize("n,c", [(500, 12), (4096, 64)])
+@pytest.mark.parametrize("n,c", [(500, 12), (4096, 64), (1500, 800), (1200, 1000)])   # wide blocks: smaller Jacobi blocks
 def test_orth_graded(lib, n, c):
     rng = np.random.default_rng(c)
     U, _ = np.linalg.qr(rng.standard_normal((n, c)) + 1j * rng.standard_normal((n, c)))
