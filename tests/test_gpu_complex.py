@@ -116,3 +116,23 @@ def test_wide_moment_block_default_source_cols():
     assert r is not None and len(r.eigenvalues) == 100
     assert _match(r.eigenvalues, w[200:300]) <= 1e-8
     assert r.residuals.max() <= 1e-10
+
+
+def test_conjugate_pair_variant_off_for_complex_pencils():
+    """M(conj z) = conj(M(z)) needs real A and B: with complex values the
+    labelled conjugate-pair variant must factor every node (same result)."""
+    from paper_2511_01927_b200 import Contour, DevicePencil, SolverConfig, solve_multi
+    n = 200
+    rng = np.random.default_rng(6)
+    g = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    a = (g + g.conj().T) / (2 * np.sqrt(n)) + np.diag(np.linspace(0.0, 5.0, n))
+    b = np.eye(n)
+    w = np.linalg.eigvalsh(a)
+    lo, hi = 0.5 * (w[19] + w[20]), 0.5 * (w[29] + w[30])
+    c = Contour(shape="circle", center=complex(0.5 * (lo + hi), 0.0), radius=0.5 * (hi - lo), expected_count=10)
+    dp = DevicePencil(a, b)
+    base = solve_multi(dp, [c], SolverConfig(n_q=32, source_cols=20, n_moments=4), seed=0)
+    var = solve_multi(dp, [c], SolverConfig(n_q=32, source_cols=20, n_moments=4, conjugate_pairs=True), seed=0)
+    assert var.results[0].stats.n_factorizations == 32 == base.results[0].stats.n_factorizations
+    assert np.array_equal(var.eigenvalues, base.eigenvalues)
+    assert _match(base.eigenvalues, w[20:30]) <= 1e-8
