@@ -62,7 +62,9 @@ def main(cfgno: int, reps: int = 2):
                 truth = g[f"c{i}_truth"]
                 line += f" | oracle {len(ref)} truth {len(truth)} iters {int(g[f'c{i}_iters'])}"
                 if len(ref) == len(res.eigenvalues):
-                    rel = np.abs(res.eigenvalues - ref) / np.abs(ref)
+                    # nearest matching (complex eigenvalues need not share the sort order)
+                    got = np.asarray(res.eigenvalues, complex)
+                    rel = np.array([np.min(np.abs(got - r)) / abs(r) for r in np.asarray(ref, complex)])
                     line += f" max rel diff {rel.max():.2e}"
         print(line, flush=True)
 
