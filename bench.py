@@ -125,7 +125,7 @@ class ClockSampler:
 # CPU baseline (oracle) -- bounded sample of one GEP
 
 
-def cpu_sample(wl, refine_cols=None, passes=None, sample_pencils=6):
+def cpu_sample(wl, refine_cols=None, passes=None, sample_pencils=6, threads_label=None):
     """Time the oracle's per-pencil work (assembly, LAPACK LU, every solve pass)
     on `sample_pencils` pencils and one Rayleigh-Ritz round; extrapolate to
     one GEP.  Returns (seconds_per_gep, description)."""
@@ -158,13 +158,24 @@ def cpu_sample(wl, refine_cols=None, passes=None, sample_pencils=6):
     rayleigh_ritz(p, q, "general" if not wl.hermitian else "hermitian")
     t_rr = time.perf_counter() - t1
     per_gep = t_pencils / sample_pencils * total_pencils + t_rr * passes * len(wl.contours)
-    desc = (f"oracle (scipy LAPACK, OPENBLAS threads={os.environ.get('OPENBLAS_NUM_THREADS', 'default')}) on "
+    desc = (f"oracle (scipy LAPACK, BLAS threads={threads_label or os.environ.get('OPENBLAS_NUM_THREADS', 'default')}) on "
             f"{sample_pencils}/{total_pencils} pencils (assemble+zgetrf+{passes} solve passes, L={wl.source_cols} "
             f"then K={refine_cols}) + 1 RR round (SVD n x {wl.source_cols * wl.n_moments}, A Q, B Q, eig), "
             f"extrapolated x{total_pencils / sample_pencils:.0f} pencils and x{passes * len(wl.contours)} RR rounds; "
             f"sample wall {t_pencils + t_rr:.1f} s")
     del cores, OracleConfig
     return per_gep, desc, t_pencils + t_rr
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def lu_traffic():
@@ -207,7 +218,8 @@ def run_reference(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic (seeded config 4)",
         "config": {"workload": "BASELINE config 4: n=4096 dense non-Hermitian GEP, 2 ellipses, N=64, L=32, M=8",
                    "parallelism": "cpu"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": desc},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": desc,
+                         "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -360,7 +372,16 @@ def run_cirr(args):
         ref_cols = max(counts) if counts else 118
         per_gep, desc, wall = cpu_sample(wl, refine_cols=ref_cols, passes=passes)
         cpu = {"value": 1.0 / per_gep, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port",
-               "sample": desc}
+               "sample": desc, "cpu_model": cpu_model()}
+        # the same sample with the BLAS pinned to one thread as well
+        try:
+            from threadpoolctl import threadpool_limits
+            with threadpool_limits(limits=1):
+                per1, desc1, _ = cpu_sample(wl, refine_cols=ref_cols, passes=passes, sample_pencils=1,
+                                             threads_label="1 (threadpoolctl)")
+            cpu["single_thread"] = {"value": 1.0 / per1, "unit": UNIT, "cores": 1, "sample": desc1}
+        except ImportError:
+            pass
 
     if rank == 0:
         line = {
@@ -384,7 +405,9 @@ def run_cirr(args):
             "stage_ms_per_step": {k: v / args.steps for k, v in sorted(stages.items())},
             "time_per_gep_s": per_step / 1e3,
             "eigenpairs_per_s": pairs * world / (per_step / 1e3),
-            "shifted_solves_per_s": solves * world / (per_step / 1e3),
+            # shifted solves = pencils x passes; RHS columns = sum of n_linear_solves
+            "shifted_solves_per_s": (last.stats.n_factorizations * max(iters or [1])) * world / (per_step / 1e3),
+            "rhs_columns_per_s": solves * world / (per_step / 1e3),
             "eigenpairs": counts, "iterations": iters,
             "n_factorizations": last.stats.n_factorizations, "n_linear_solves": solves,
             "executed_flops_per_step": stage_flops / args.steps,
