@@ -63,11 +63,22 @@ int cirr_zgetrs_batched(const cirr_cplx* LU, int n, long long ld, long long penc
                         int batch, const int* perm, const cirr_cplx* R, long long ldr,
                         long long rstride, const int* rhs_of, int K, cirr_cplx* Y,
                         long long ldy, long long ystride, const cirr_cplx* Dinv, cudaStream_t stream);
+/* The same solves for any subset of the nfac factors at LU: batch entry j uses
+ * factor pencil_of[j] (device int32[batch]); perm and Dinv are indexed by
+ * factor, rhs_of and Y by entry.  Lets contours that are not adjacent in the
+ * factor buffer (refinement passes of a multi-pencil batch) share one call. */
+int cirr_zgetrs_gather(const cirr_cplx* LU, int n, long long ld, long long pencil_stride, int nfac,
+                       const int* pencil_of, int batch, const int* perm, const cirr_cplx* R, long long ldr,
+                       long long rstride, const int* rhs_of, int K, cirr_cplx* Y, long long ldy,
+                       long long ystride, const cirr_cplx* Dinv, cudaStream_t stream);
 /* Inverses of the 128x128 diagonal blocks of L and U (optional input of
  * cirr_zgetrs_batched: the diagonal solves become TMA/DMMA GEMMs). */
 long long cirr_diag_inv_bytes(int n, int batch);
 int cirr_diag_inverses(const cirr_cplx* LU, int n, long long ld, long long pencil_stride, int batch,
                        cirr_cplx* Dinv, cudaStream_t stream);
+/* 1 when cirr_zgetrs_batched reads Dinv for an n x K solve (K <= 2, or K > 16),
+ * 0 when it does not (callers may then skip cirr_diag_inverses). */
+int cirr_zgetrs_uses_dinv(int n, int K);
 
 /* K3b -- replaces solvers.py:121-129 (acc[m] += w_j zeta_j^m Y_j).
  * St[c] ((M*K) x n): row m*K+col = column col of S_m of contour c, summed over

@@ -37,6 +37,7 @@ from .solvers import (  # noqa: F401
     feast_solve,
     read_eigenvectors,
     solve_multi,
+    solve_multi_batch,
     write_eigenvectors,
 )
 

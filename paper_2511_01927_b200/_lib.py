@@ -30,8 +30,10 @@ SIGNATURES = {
     "cirr_zgetrf_batched": [_P, _I, _L, _L, _I, _P, _P, _P, _P, _P, _P],
     "cirr_zgetrf_ws_bytes": [_I, _I],
     "cirr_zgetrs_batched": [_P, _I, _L, _L, _I, _P, _P, _L, _L, _P, _I, _P, _L, _L, _P, _P],
+    "cirr_zgetrs_gather": [_P, _I, _L, _L, _I, _P, _I, _P, _P, _L, _L, _P, _I, _P, _L, _L, _P, _P],
     "cirr_diag_inv_bytes": [_I, _I],
     "cirr_diag_inverses": [_P, _I, _L, _L, _I, _P, _P],
+    "cirr_zgetrs_uses_dinv": [_I, _I],
     "cirr_moments": [_P, _L, _L, _I, _I, _P, _I, _P, _I, _P, _L, _L, _P],
     "cirr_orth_ws_bytes": [_I, _I],
     "cirr_orth_phases": [_P],
@@ -61,7 +63,7 @@ SIGNATURES = {
 }
 _RESTYPE = {"cirr_diag_inv_bytes": _L, "cirr_zgetrf_ws_bytes": _L, "cirr_small_eig_ws_bytes": _L, "cirr_launch_count": _L, "cirr_orth_ws_bytes": _L,
             "cirr_gen_eig_ws_bytes": _L, "cirr_gen_eig_vec_scratch_bytes": _L, "cirr_orth_cholqr2_ws_bytes": _L}
-_RAW = {"cirr_set_coop_ctas", "cirr_set_gemm_ctas", "cirr_diag_inv_bytes", "cirr_zgetrf_ws_bytes", "cirr_small_eig_ws_bytes", "cirr_launch_count", "cirr_target_sm", "cirr_orth_ws_bytes",
+_RAW = {"cirr_zgetrs_uses_dinv", "cirr_set_coop_ctas", "cirr_set_gemm_ctas", "cirr_diag_inv_bytes", "cirr_zgetrf_ws_bytes", "cirr_small_eig_ws_bytes", "cirr_launch_count", "cirr_target_sm", "cirr_orth_ws_bytes",
         "cirr_gen_eig_ws_bytes", "cirr_gen_eig_vec_scratch_bytes", "cirr_orth_cholqr2_ws_bytes"}
 
 _lib = None

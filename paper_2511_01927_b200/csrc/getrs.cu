@@ -33,7 +33,8 @@ template <bool LOWER>
 __global__ void __launch_bounds__(256, 1) trsm_blocked_kernel(const cplx* __restrict__ LU, long long ld,
                                                               long long pstride, int n,
                                                               cplx* __restrict__ Y, long long ldy,
-                                                              long long ystride, int K) {
+                                                              long long ystride, int K,
+                                                              const int* __restrict__ pmap) {
   extern __shared__ __align__(16) cplx ssm[];
   cplx* stA = ssm;                                   // 2 stages
   cplx* stB = ssm + 2 * kStageA;
@@ -42,7 +43,7 @@ __global__ void __launch_bounds__(256, 1) trsm_blocked_kernel(const cplx* __rest
   cplx* dinv = X + SNB * SX_LD;
   const int b = blockIdx.y;
   const int c0 = blockIdx.x * SKC;
-  const cplx* T = LU + (long long)b * pstride;
+  const cplx* T = LU + (long long)(pmap ? pmap[b] : b) * pstride;
   cplx* Yb = Y + (long long)b * ystride;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = (warp >> 1) * 16, wn = (warp & 1) * 16;
@@ -279,13 +280,14 @@ constexpr int kDiagInv128Smem = (3 * SNB * SD_LD + SNB) * 16;
 // Y[j][i][c] = R[rhs_of[j]][perm[j][i]][c]
 __global__ void permute_kernel(const cplx* __restrict__ R, long long ldr, long long rstride,
                                const int* __restrict__ rhs_of, const int* __restrict__ perm, int n, int K,
-                               cplx* __restrict__ Y, long long ldy, long long ystride) {
+                               cplx* __restrict__ Y, long long ldy, long long ystride,
+                               const int* __restrict__ pmap) {
   const int j = blockIdx.y;
   const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (long long)n * K) return;
   const int i = (int)(e / K), c = (int)(e % K);
   const cplx* Rj = R + (long long)rhs_of[j] * rstride;
-  const int src = perm[(long long)j * n + i];
+  const int src = perm[(long long)(pmap ? pmap[j] : j) * n + i];
   Y[(long long)j * ystride + (long long)i * ldy + c] = Rj[(long long)src * ldr + c];
 }
 
@@ -366,13 +368,13 @@ constexpr int kDiagSmem = (SNB * SD_LD + SNB * (DSC + 1) + SNB) * 16;
 template <bool LOWER>
 __global__ void __launch_bounds__(256) diag_solve_kernel(const cplx* __restrict__ LU, long long ld, long long pstride,
                                                          int i0, int nb, cplx* __restrict__ Y, long long ldy,
-                                                         long long ystride, int K) {
+                                                         long long ystride, int K, const int* __restrict__ pmap) {
   extern __shared__ __align__(16) cplx dsm[];
   cplx* D = dsm;
   cplx* X = D + SNB * SD_LD;
   cplx* dinv = X + SNB * (DSC + 1);
   const int b = blockIdx.y, c0 = blockIdx.x * DSC, tid = threadIdx.x;
-  const cplx* T = LU + (long long)b * pstride;
+  const cplx* T = LU + (long long)(pmap ? pmap[b] : b) * pstride;
   cplx* Yb = Y + (long long)b * ystride;
   const int nc = min(DSC, K - c0);
   for (int e = tid; e < nb * nb; e += 256) {
@@ -423,14 +425,15 @@ template <int KK, bool LOWER>
 __global__ void __launch_bounds__(TV_T) trsv_lookback_kernel(const cplx* __restrict__ LU, long long ld,
                                                              long long pstride, int n, const cplx* __restrict__ Dinv,
                                                              cplx* __restrict__ Y, long long ldy, long long ystride,
-                                                             int* __restrict__ flags) {
+                                                             int* __restrict__ flags, const int* __restrict__ pmap) {
   __shared__ cplx sacc[TV_BS][KK];
   __shared__ cplx sy[TV_BS][KK];
   const int nblk = gridDim.x, b = blockIdx.y;
   const int bi = LOWER ? blockIdx.x : nblk - 1 - blockIdx.x;
   const int i0 = bi * TV_BS, nb = min(TV_BS, n - i0);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const cplx* T = LU + (long long)b * pstride;
+  const int pb = pmap ? pmap[b] : b;
+  const cplx* T = LU + (long long)pb * pstride;
   cplx* Yb = Y + (long long)b * ystride;
   int* fl = flags + (long long)b * nblk;
   // warp wid owns rows i0 + 16 wid .. +15; lane covers columns c0 + lane (+32, +64, +96)
@@ -492,7 +495,7 @@ __global__ void __launch_bounds__(TV_T) trsv_lookback_kernel(const cplx* __restr
   for (int q = 0; q < 16; ++q)
 #pragma unroll
     for (int c = 0; c < KK; ++c) part[q][c] = cmk(0.0, 0.0);
-  const cplx* D = Dinv + (((long long)b * nblk + bi) * 2 + (LOWER ? 0 : 1)) * TV_BS * TV_BS;
+  const cplx* D = Dinv + (((long long)pb * nblk + bi) * 2 + (LOWER ? 0 : 1)) * TV_BS * TV_BS;
   tile(D, TV_BS, nb, sacc, nb);
 #pragma unroll
   for (int q = 0; q < 16; ++q)
@@ -511,17 +514,17 @@ __global__ void __launch_bounds__(TV_T) trsv_lookback_kernel(const cplx* __restr
 
 template <int KK>
 int trsv_lookback(const cplx* LU, int n, long long ld, long long pstride, int batch, const cplx* Dinv, cplx* Y,
-                  long long ldy, long long ystride, cudaStream_t stream) {
+                  long long ldy, long long ystride, cudaStream_t stream, const int* pmap) {
   const int nblk = (n + TV_BS - 1) / TV_BS;
   int* flags = nullptr;
   cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&flags), sizeof(int) * 2 * (size_t)nblk * batch, stream);
   if (e != cudaSuccess) return (int)e;
   if ((e = cudaMemsetAsync(flags, 0, sizeof(int) * 2 * (size_t)nblk * batch, stream)) != cudaSuccess) return (int)e;
   dim3 g(nblk, batch);
-  trsv_lookback_kernel<KK, true><<<g, TV_T, 0, stream>>>(LU, ld, pstride, n, Dinv, Y, ldy, ystride, flags);
+  trsv_lookback_kernel<KK, true><<<g, TV_T, 0, stream>>>(LU, ld, pstride, n, Dinv, Y, ldy, ystride, flags, pmap);
   CIRR_CHECK_LAUNCH();
   trsv_lookback_kernel<KK, false><<<g, TV_T, 0, stream>>>(LU, ld, pstride, n, Dinv, Y, ldy, ystride,
-                                                          flags + (long long)nblk * batch);
+                                                          flags + (long long)nblk * batch, pmap);
   CIRR_CHECK_LAUNCH();
   return (int)cudaFreeAsync(flags, stream);
 }
@@ -557,11 +560,27 @@ CIRR_API int cirr_diag_inverses(const cplx* LU, int n, long long ld, long long p
   return 0;
 }
 
-CIRR_API int cirr_zgetrs_batched(const cplx* LU, int n, long long ld, long long pencil_stride, int batch,
-                                 const int* perm, const cplx* R, long long ldr, long long rstride,
-                                 const int* rhs_of, int K, cplx* Y, long long ldy, long long ystride,
-                                 const cplx* Dinv, cudaStream_t stream) {
-  if (n <= 0 || batch <= 0 || K < 0 || ldy < K || ldr < K) return CIRR_EINVAL;
+// The right-looking TMA path serves K > 16; for small factors (n <= 512,
+// CIRR_SOLVE_SMALL_N) the left-looking kernel keeps up to K = 32 (one 32-column
+// chunk per pencil), so those solves need no diagonal-block inverses.
+static bool solve_tma_path(int n, int K) {
+  static const int small_n = getenv("CIRR_SOLVE_SMALL_N") ? atoi(getenv("CIRR_SOLVE_SMALL_N")) : 512;
+  return K > 16 && n >= 64 && !(n <= small_n && K <= SKC);
+}
+
+// Whether cirr_zgetrs_batched reads Dinv for an n x K solve: the look-back
+// TRSV (K <= 2) and the TMA blocked path do; the left-looking kernel does not,
+// so callers can skip cirr_diag_inverses there.
+CIRR_API int cirr_zgetrs_uses_dinv(int n, int K) { return K <= 2 || solve_tma_path(n, K); }
+
+// Solves for batch entries j = 0..batch-1 against factor pmap[j] (pmap null:
+// factor j) of the nfac factors at LU (pencil_stride apart); perm and Dinv are
+// indexed by factor, R by rhs_of[j], Y by j.
+static int getrs_impl(const cplx* LU, int n, long long ld, long long pencil_stride, int batch, int nfac,
+                      const int* pmap, const int* perm, const cplx* R, long long ldr, long long rstride,
+                      const int* rhs_of, int K, cplx* Y, long long ldy, long long ystride, const cplx* Dinv,
+                      cudaStream_t stream) {
+  if (n <= 0 || batch <= 0 || nfac <= 0 || K < 0 || ldy < K || ldr < K) return CIRR_EINVAL;
   if (K == 0) return 0;
   static bool attr = false;
   if (!attr) {
@@ -570,11 +589,11 @@ CIRR_API int cirr_zgetrs_batched(const cplx* LU, int n, long long ld, long long 
     attr = true;
   }
   dim3 gp((unsigned)(((long long)n * K + 255) / 256), batch);
-  permute_kernel<<<gp, 256, 0, stream>>>(R, ldr, rstride, rhs_of, perm, n, K, Y, ldy, ystride);
+  permute_kernel<<<gp, 256, 0, stream>>>(R, ldr, rstride, rhs_of, perm, n, K, Y, ldy, ystride, pmap);
   CIRR_CHECK_LAUNCH();
   if (Dinv != nullptr && K <= 2) {  // one or two RHS: look-back triangular solves
-    if (K == 1) return trsv_lookback<1>(LU, n, ld, pencil_stride, batch, Dinv, Y, ldy, ystride, stream);
-    return trsv_lookback<2>(LU, n, ld, pencil_stride, batch, Dinv, Y, ldy, ystride, stream);
+    if (K == 1) return trsv_lookback<1>(LU, n, ld, pencil_stride, batch, Dinv, Y, ldy, ystride, stream, pmap);
+    return trsv_lookback<2>(LU, n, ld, pencil_stride, batch, Dinv, Y, ldy, ystride, stream, pmap);
   }
   // right-looking blocked solves: per 64-row block a diagonal solve, then the
   // rank-64 update of the remaining rows on the TMA/DMMA GEMM (zgemm_sub_tma)
@@ -582,7 +601,7 @@ CIRR_API int cirr_zgetrs_batched(const cplx* LU, int n, long long ld, long long 
   // GEMM tile of the right-looking path would be mostly padding there (at K = 32
   // the TMA path is still faster: 18.7 ms vs 24.3 ms for 64 pencils, n = 4096)
   cirr::OperandMaps mT, mY;
-  bool tma = K > 16 && n >= 64 && cirr::encode_a_map(&mT.a, LU, n, n, batch, ld, pencil_stride) == 0 &&
+  bool tma = solve_tma_path(n, K) && cirr::encode_a_map(&mT.a, LU, n, n, nfac, ld, pencil_stride) == 0 &&
              cirr::encode_c128_map(&mY.b, Y, K, n, batch, ldy, ystride, cirr::PBN, cirr::PBK) == 0 &&
              cirr::encode_c128_map(&mY.c, Y, K, n, batch, ldy, ystride, cirr::PBN, cirr::PBM) == 0;
   if (tma) {
@@ -595,7 +614,7 @@ CIRR_API int cirr_zgetrs_batched(const cplx* LU, int n, long long ld, long long 
     CUtensorMap mD;
     const int nblk2 = (n + DB - 1) / DB;
     const bool use_dinv = Dinv != nullptr &&
-                          cirr::encode_a_map(&mD, Dinv, DB, DB, batch * nblk2 * 2, DB, (long long)DB * DB) == 0;
+                          cirr::encode_a_map(&mD, Dinv, DB, DB, nfac * nblk2 * 2, DB, (long long)DB * DB) == 0;
     if (use_dinv) {
       // 128-row blocks grouped into super-blocks of SBK blocks.  Inside a
       // super-block the blocks are left-looking (block j first receives the
@@ -612,16 +631,16 @@ CIRR_API int cirr_zgetrs_batched(const cplx* LU, int n, long long ld, long long 
         if (lower) {
           if (nb2 > 0)  // rows i0+64.. : [L21inv L22inv] [Y_a; Y_b]
             CIRR_TRY(cirr::zgemm_sub_maps(mD, mY.b, mY.c, nb2, K, nb, batch, SNB, 0, i0, 0, i0 + SNB, 0, Y, ldy,
-                                          ystride, stream, /*beta=*/0, nblk2 * 2, slot));
+                                          ystride, stream, /*beta=*/0, nblk2 * 2, slot, pmap));
           CIRR_TRY(cirr::zgemm_sub_maps(mD, mY.b, mY.c, na, K, na, batch, 0, 0, i0, 0, i0, 0, Y, ldy, ystride, stream,
-                                        /*beta=*/0, nblk2 * 2, slot));
+                                        /*beta=*/0, nblk2 * 2, slot, pmap));
         } else {
           // rows i0.. : [U11inv U12inv] [Y_a; Y_b] first (reads the old Y_b), then Y_b
           CIRR_TRY(cirr::zgemm_sub_maps(mD, mY.b, mY.c, na, K, nb, batch, 0, 0, i0, 0, i0, 0, Y, ldy, ystride, stream,
-                                        /*beta=*/0, nblk2 * 2, slot));
+                                        /*beta=*/0, nblk2 * 2, slot, pmap));
           if (nb2 > 0)
             CIRR_TRY(cirr::zgemm_sub_maps(mD, mY.b, mY.c, nb2, K, nb2, batch, SNB, SNB, i0 + SNB, 0, i0 + SNB, 0, Y,
-                                          ldy, ystride, stream, /*beta=*/0, nblk2 * 2, slot));
+                                          ldy, ystride, stream, /*beta=*/0, nblk2 * 2, slot, pmap));
         }
         return 0;
       };
@@ -632,12 +651,12 @@ CIRR_API int cirr_zgetrs_batched(const cplx* LU, int n, long long ld, long long 
           const int i0 = bi * DB, nb = min(DB, n - i0);
           if (bi > sb0)  // Y[i0:i0+nb] -= L[i0:i0+nb, s0:i0] Y[s0:i0]
             CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, nb, K, i0 - s0, batch, i0, s0, s0, 0, i0, 0, Y, ldy,
-                                          ystride, stream));
+                                          ystride, stream, 1, 1, 0, pmap));
           CIRR_TRY(apply_dinv(bi, true));
         }
         if (n - s1 > 0)  // Y[s1:] -= L[s1:, s0:s1] Y[s0:s1]
           CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, n - s1, K, s1 - s0, batch, s1, s0, s0, 0, s1, 0, Y, ldy,
-                                        ystride, stream));
+                                        ystride, stream, 1, 1, 0, pmap));
       }
       const int nsb = (nblk2 + SBK - 1) / SBK;
       for (int sb = nsb - 1; sb >= 0; --sb) {  // backward: U
@@ -647,12 +666,12 @@ CIRR_API int cirr_zgetrs_batched(const cplx* LU, int n, long long ld, long long 
           const int i0 = bi * DB, nb = min(DB, n - i0);
           if (bi < sb1 - 1)  // Y[i0:i0+nb] -= U[i0:i0+nb, i0+nb:s1] Y[i0+nb:s1]
             CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, nb, K, s1 - i0 - nb, batch, i0, i0 + nb, i0 + nb, 0, i0,
-                                          0, Y, ldy, ystride, stream));
+                                          0, Y, ldy, ystride, stream, 1, 1, 0, pmap));
           CIRR_TRY(apply_dinv(bi, false));
         }
         if (s0 > 0)  // Y[:s0] -= U[:s0, s0:s1] Y[s0:s1]
           CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, s0, K, s1 - s0, batch, 0, s0, s0, 0, 0, 0, Y, ldy, ystride,
-                                        stream));
+                                        stream, 1, 1, 0, pmap));
       }
       return 0;
     }
@@ -660,26 +679,46 @@ CIRR_API int cirr_zgetrs_batched(const cplx* LU, int n, long long ld, long long 
     dim3 gd((K + DSC - 1) / DSC, batch);
     for (int bi = 0; bi < nblk; ++bi) {  // forward: L (unit lower)
       const int i0 = bi * SNB, nb = min(SNB, n - i0);
-      diag_solve_kernel<true><<<gd, 256, kDiagSmem, stream>>>(LU, ld, pencil_stride, i0, nb, Y, ldy, ystride, K);
+      diag_solve_kernel<true><<<gd, 256, kDiagSmem, stream>>>(LU, ld, pencil_stride, i0, nb, Y, ldy, ystride, K, pmap);
       CIRR_CHECK_LAUNCH();
       CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, n - i0 - nb, K, nb, batch, i0 + nb, i0, i0, 0, i0 + nb, 0,
-                                    Y, ldy, ystride, stream));
+                                    Y, ldy, ystride, stream, 1, 1, 0, pmap));
     }
     for (int bi = nblk - 1; bi >= 0; --bi) {  // backward: U
       const int i0 = bi * SNB, nb = min(SNB, n - i0);
-      diag_solve_kernel<false><<<gd, 256, kDiagSmem, stream>>>(LU, ld, pencil_stride, i0, nb, Y, ldy, ystride, K);
+      diag_solve_kernel<false><<<gd, 256, kDiagSmem, stream>>>(LU, ld, pencil_stride, i0, nb, Y, ldy, ystride, K, pmap);
       CIRR_CHECK_LAUNCH();
       CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, i0, K, nb, batch, 0, i0, i0, 0, 0, 0, Y, ldy, ystride,
-                                    stream));
+                                    stream, 1, 1, 0, pmap));
     }
     return 0;
   }
   dim3 gs((K + SKC - 1) / SKC, batch);
-  trsm_blocked_kernel<true><<<gs, 256, kSolveSmem, stream>>>(LU, ld, pencil_stride, n, Y, ldy, ystride, K);
+  trsm_blocked_kernel<true><<<gs, 256, kSolveSmem, stream>>>(LU, ld, pencil_stride, n, Y, ldy, ystride, K, pmap);
   CIRR_CHECK_LAUNCH();
-  trsm_blocked_kernel<false><<<gs, 256, kSolveSmem, stream>>>(LU, ld, pencil_stride, n, Y, ldy, ystride, K);
+  trsm_blocked_kernel<false><<<gs, 256, kSolveSmem, stream>>>(LU, ld, pencil_stride, n, Y, ldy, ystride, K, pmap);
   CIRR_CHECK_LAUNCH();
   return 0;
+}
+
+CIRR_API int cirr_zgetrs_batched(const cplx* LU, int n, long long ld, long long pencil_stride, int batch,
+                                 const int* perm, const cplx* R, long long ldr, long long rstride,
+                                 const int* rhs_of, int K, cplx* Y, long long ldy, long long ystride,
+                                 const cplx* Dinv, cudaStream_t stream) {
+  return getrs_impl(LU, n, ld, pencil_stride, batch, batch, nullptr, perm, R, ldr, rstride, rhs_of, K, Y, ldy,
+                    ystride, Dinv, stream);
+}
+
+// The same solves for any subset of the factors: entry j uses factor
+// pencil_of[j] (device int32, each < nfac), so contours that are not adjacent
+// in the factor buffer still share one call (and one launch per GEMM step).
+CIRR_API int cirr_zgetrs_gather(const cplx* LU, int n, long long ld, long long pencil_stride, int nfac,
+                                const int* pencil_of, int batch, const int* perm, const cplx* R, long long ldr,
+                                long long rstride, const int* rhs_of, int K, cplx* Y, long long ldy,
+                                long long ystride, const cplx* Dinv, cudaStream_t stream) {
+  if (pencil_of == nullptr) return CIRR_EINVAL;
+  return getrs_impl(LU, n, ld, pencil_stride, batch, nfac, pencil_of, perm, R, ldr, rstride, rhs_of, K, Y, ldy,
+                    ystride, Dinv, stream);
 }
 
 // Moment blocks of n_sets contours: pencils off[c] .. off[c+1]-1 belong to

@@ -77,6 +77,7 @@ struct SubGemmGeom {
   int beta;        // 1: C = C - A B (C tile streamed in by TMA); 0: C = A B
   int a_bmul, a_badd;  // 3rd TMA coordinate of the A operand: b * a_bmul + a_badd
   int* ctr;            // {next tile, finished CTAs}: dynamic tile scheduler, zero on entry and exit
+  const int* a_bmap;   // optional: the A operand of batch entry b is A entry a_bmap[b] (gathered solves)
 };
 
 static __global__ void __launch_bounds__(PTHREADS, 1) zgemm_sub_tma(const __grid_constant__ CUtensorMap mapA,
@@ -127,12 +128,12 @@ static __global__ void __launch_bounds__(PTHREADS, 1) zgemm_sub_tma(const __grid
         const int b = (int)(t / tiles_per_b);
         const int rem = (int)(t % tiles_per_b);
         const int m0 = (rem / g.tiles_n) * PBM, n0 = (rem % g.tiles_n) * PBN;
+        const int ab = (g.a_bmap ? __ldg(g.a_bmap + b) : b) * g.a_bmul + g.a_badd;
         for (int ks = 0; ks < ksteps; ++ks) {
           if (ks > 0) mbar_wait(empty + stage, phase ^ 1);
           unsigned char* base = psm + stage * P_STAGE_BYTES;
           mbar_arrive_expect_tx(full + stage, P_STAGE_BYTES);
           const int k0 = ks * PBK;
-          const int ab = b * g.a_bmul + g.a_badd;
           tma_load3(base, &mapA, 2 * (g.a_col0 + k0), g.a_row0 + m0, ab, full + stage);
           tma_load3(base + P_A_HALF, &mapA, 2 * (g.a_col0 + k0 + PAK), g.a_row0 + m0, ab, full + stage);
           tma_load3(base + P_A_BYTES, &mapB, 2 * (g.b_col0 + n0), g.b_row0 + k0, b, full + stage);
@@ -311,7 +312,7 @@ static inline int encode_pencil_maps(PencilMaps& pm, cplx* base, int n, long lon
 static inline int zgemm_sub_maps(const CUtensorMap& mapA, const CUtensorMap& mapB, const CUtensorMap& mapC, int M, int N,
                           int K, int batch, int a_row0, int a_col0, int b_row0, int b_col0, int c_row0, int c_col0,
                           cplx* C, long long ldc, long long sC, cudaStream_t stream, int beta = 1,
-                          int a_bmul = 1, int a_badd = 0) {
+                          int a_bmul = 1, int a_badd = 0, const int* a_bmap = nullptr) {
   if (M <= 0 || N <= 0 || K <= 0 || batch <= 0) return 0;
   static bool attr = false;
   static int sms = 0;
@@ -326,7 +327,7 @@ static inline int zgemm_sub_maps(const CUtensorMap& mapA, const CUtensorMap& map
   int* ctr = cirr_tile_counter(stream);
   if (!ctr) return (int)cudaErrorMemoryAllocation;
   SubGemmGeom g{M, N, Kr, batch, a_row0, a_col0, b_row0, b_col0, c_row0, c_col0, C, ldc, sC,
-                (M + PBM - 1) / PBM, (N + PBN - 1) / PBN, beta, a_bmul, a_badd, ctr};
+                (M + PBM - 1) / PBM, (N + PBN - 1) / PBN, beta, a_bmul, a_badd, ctr, a_bmap};
   const long long tiles = (long long)g.tiles_m * g.tiles_n * batch;
   // persistent grid: every SM, or fewer when cirr_set_gemm_ctas leaves SMs to
   // latency-bound kernels on other streams (the dynamic tile scheduler adapts)

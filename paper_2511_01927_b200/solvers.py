@@ -453,7 +453,12 @@ class _Contour:
 
 
 class _Engine:
-    """Batched CIRR over the contours of one wave (factors stay resident)."""
+    """Batched CIRR over the contours of one wave (factors stay resident).
+
+    Every contour normally belongs to one pencil ``dp``; under
+    ``solve_multi_batch`` each contour carries its own (``_Contour.dp``, same
+    n, dtype and Hermitian flag), and the per-pencil products gather A and B
+    per contour."""
 
     def __init__(self, dp: DevicePencil, cstates: list, cfg: SolverConfig):
         self.torch = _torch()
@@ -461,6 +466,35 @@ class _Engine:
         self.cs = cstates
         self.cfg = cfg
         self.n = dp.n
+        self.multi = any(getattr(c, "dp", dp) is not dp for c in cstates)
+        self.eager_dinv = False     # run_pipelined makes them per contour with its factors
+        self._dinv_made = False
+
+    def _dp_of(self, ci: int) -> DevicePencil:
+        return getattr(self.cs[ci], "dp", None) or self.dp
+
+    def _mats(self, cis: list):
+        """(A, B, batch stride) for the pencils of contours cis in order: the
+        shared pencil with stride 0, else stacked copies (n^2 apart)."""
+        dps = [self._dp_of(ci) for ci in cis]
+        if all(d is dps[0] for d in dps):
+            return dps[0].a, dps[0].b, 0
+        torch = self.torch
+        return torch.stack([d.a for d in dps]), torch.stack([d.b for d in dps]), self.n * self.n
+
+    def _pencil_runs(self, a: int, b: int):
+        """Maximal ranges [lo, hi) of pencils a..b-1 that share one DevicePencil."""
+        runs = []
+        for ci in range(len(self.cs)):
+            lo, hi = max(self.node_off[ci], a), min(self.node_off[ci + 1], b)
+            if lo >= hi:
+                continue
+            d = self._dp_of(ci)
+            if runs and runs[-1][2] is d and runs[-1][1] == lo:
+                runs[-1][1] = hi
+            else:
+                runs.append([lo, hi, d])
+        return runs
 
     @property
     def stream(self) -> int:
@@ -519,22 +553,40 @@ class _Engine:
             return
         z = _h2d(nodes)
         with _stage("assemble"):
-            self.dp.assemble(z, cnt, self.pencils[a], self.maxabs[a:], self.stream)
+            for lo, hi, d in self._pencil_runs(a, b):
+                d.assemble(z[lo - a:], hi - lo, self.pencils[lo], self.maxabs[lo:], self.stream)
         _work("assemble_bytes", cnt * n * n * 16 + 2 * n * n * 8)
         with _stage("lu"):
             lws = torch.empty(int(_lib.call("cirr_zgetrf_ws_bytes", n, cnt)), dtype=torch.uint8, device="cuda")
             _lib.call("cirr_zgetrf_batched", _ptr(self.pencils[a]), n, n, n * n, cnt, _ptr(self.ipiv[a]),
                       _ptr(self.perm[a]), _ptr(self.minpiv[a:]), _ptr(self.info[a:]), _ptr(lws), self.stream)
         _work("lu_flops", cnt * 8.0 * n ** 3 / 3.0)
+        if self.eager_dinv:
+            self._diag_inverses(a, b)
+
+    def _diag_inverses(self, a: int, b: int):
         with _stage("dinv"):
-            _lib.call("cirr_diag_inverses", _ptr(self.pencils[a]), n, n, n * n, cnt,
+            _lib.call("cirr_diag_inverses", _ptr(self.pencils[a]), self.n, self.n, self.n * self.n, b - a,
                       _ptr(self.dinv) + a * self._dinv_per_pencil, self.stream)
 
     def factor(self):
         self._alloc_factors()
         self._factor_range(0, self.P, np.concatenate([c.nodes[c.fidx] for c in self.cs]))
-        for ci in range(len(self.cs)):
-            self._check_factor(ci)
+        if len(self.cs) == 1:
+            self._check_factor(0)
+            return
+        # one read-back for every contour of the wave
+        maxabs, minpiv, info = (t.cpu().numpy() for t in (self.maxabs, self.minpiv, self.info))
+        for ci, c in enumerate(self.cs):
+            a = self.node_off[ci]
+            c.stats.n_factorizations = len(c.fidx)
+            for jl in range(len(c.fidx)):
+                scale = max(maxabs[a + jl], 1e-300)
+                if info[a + jl] != 0 or not (minpiv[a + jl] >= PIVOT_REL_TOL * scale):
+                    jn = int(c.fidx[jl])
+                    c.error = SingularShiftError(complex(c.nodes[jn]), node_index=jn)
+                    c.done = True
+                    break
 
     # -- K3: solve all pencils of the listed contours against per-contour RHS
     def apply(self, active: list, rhs: dict, moments: int, real_rhs: bool = False) -> dict:
@@ -586,15 +638,19 @@ class _Engine:
             else:
                 runs.append([a, b])
         with _stage("solve"):
-            pos = 0
-            for a, b in runs:
-                cnt = b - a
-                dinv = self._dinv()
+            dinv = self._dinv(Ks)
+            if len(runs) > 1:
+                # scattered contours (refinement passes of a multi-pencil batch):
+                # one gathered call over their factors instead of one per run
+                pen_of = _h2d(np.concatenate([np.arange(a, b, dtype=np.int32) for a, b in pen_idx]))
+                _lib.call("cirr_zgetrs_gather", _ptr(self.pencils), n, n, n * n, self.P, _ptr(pen_of), Psolve,
+                          _ptr(self.perm), _ptr(R), Ks, n * Ks, _ptr(rhs_of), Ks, _ptr(Ysol), Ks, n * Ks,
+                          _ptr(dinv) if dinv is not None else 0, self.stream)
+            else:
+                a, b = runs[0]
                 dptr = _ptr(dinv) + a * self._dinv_per_pencil if dinv is not None else 0
-                _lib.call("cirr_zgetrs_batched", _ptr(self.pencils[a]), n, n, n * n, cnt, _ptr(self.perm[a]),
-                          _ptr(R), Ks, n * Ks, _ptr(rhs_of[pos:pos + cnt]), Ks, _ptr(Ysol[pos]), Ks, n * Ks, dptr,
-                          self.stream)
-                pos += cnt
+                _lib.call("cirr_zgetrs_batched", _ptr(self.pencils[a]), n, n, n * n, b - a, _ptr(self.perm[a]),
+                          _ptr(R), Ks, n * Ks, _ptr(rhs_of), Ks, _ptr(Ysol), Ks, n * Ks, dptr, self.stream)
         _work("solve_flops", Psolve * 8.0 * n * n * Ks)
         _work("solve_flops_exec", sum((b - a) * 8.0 * n * n * k for (a, b), k in zip(pen_idx, ks)))
         if Psolve == Ptot and Ks == K:
@@ -632,9 +688,16 @@ class _Engine:
             out[ci] = St[s] if kc == K else St[s].view(moments, K, n)[:, :kc].reshape(moments * kc, n)
         return out
 
-    def _dinv(self):
-        """Inverses of the 128x128 diagonal blocks of every factor (made with the
-        factorisation; each pencil's slice is contiguous)."""
+    def _dinv(self, K: int):
+        """Inverses of the 128x128 diagonal blocks of every factor (each
+        pencil's slice is contiguous), or None when an n x K solve does not read
+        them.  Made on first use after the factorisation (the pipelined
+        engine makes them with each contour's factors)."""
+        if not int(_lib.call("cirr_zgetrs_uses_dinv", self.n, K)):
+            return None
+        if not self.eager_dinv and not self._dinv_made:
+            self._diag_inverses(0, self.P)
+            self._dinv_made = True
         return self.dinv
 
     def _bx(self, c, xi):
@@ -644,26 +707,46 @@ class _Engine:
         c.bx_dev = None
         if bx is not None and bx.shape == xi.shape:
             return bx
-        return self.bmul(xi)
+        return self.bmul(xi, self.cs.index(c))
 
-    def bmul(self, x):
-        """B @ x for a device (n x k) complex block."""
+    def bmul(self, x, ci: int | None = None):
+        """B @ x for a device (n x k) complex block (B of contour ci's pencil)."""
+        d = self.dp if ci is None else self._dp_of(ci)
         torch, n = self.torch, self.n
         k = x.shape[1]
         out = torch.empty((n, k), dtype=torch.complex128, device="cuda")
         if k:
-            _lib.call("cirr_gemm", self.dp.gemm_kind, n, k, n, 1, _ptr(self.dp.b), n, 0, _ptr(x), k, 0, _ptr(out), k, 0,
+            _lib.call("cirr_gemm", d.gemm_kind, n, k, n, 1, _ptr(d.b), n, 0, _ptr(x), k, 0, _ptr(out), k, 0,
                       1.0, 0, self.stream)
         return out
 
-    def amul(self, x):
+    def amul(self, x, ci: int | None = None):
+        d = self.dp if ci is None else self._dp_of(ci)
         torch, n = self.torch, self.n
         k = x.shape[1]
         out = torch.empty((n, k), dtype=torch.complex128, device="cuda")
         if k:
-            _lib.call("cirr_gemm", self.dp.gemm_kind, n, k, n, 1, _ptr(self.dp.a), n, 0, _ptr(x), k, 0, _ptr(out), k, 0,
+            _lib.call("cirr_gemm", d.gemm_kind, n, k, n, 1, _ptr(d.a), n, 0, _ptr(x), k, 0, _ptr(out), k, 0,
                       1.0, 0, self.stream)
         return out
+
+    def source_blocks(self, active: list) -> dict:
+        """B V for the seeded source blocks V = default_rng(seed).standard_normal
+        ((n, L)).astype(complex) of every active contour (solvers.py:178-182):
+        one upload and one batched GEMM when the contours share L."""
+        torch, n = self.torch, self.n
+        vs = {ci: np.random.default_rng(self.cs[ci].seed).standard_normal((n, self.cs[ci].ncols)) for ci in active}
+        widths = {v.shape[1] for v in vs.values()}
+        if not self.multi or len(widths) != 1:
+            return {ci: self.bmul(_h2d(vs[ci].astype(complex)), ci) for ci in active}
+        k = widths.pop()
+        V = _h2d(np.stack([vs[ci] for ci in active]).astype(complex))
+        _, B, stride = self._mats(active)
+        out = torch.empty((len(active), n, k), dtype=torch.complex128, device="cuda")
+        if k:
+            _lib.call("cirr_gemm", self._dp_of(active[0]).gemm_kind, n, k, n, len(active), _ptr(B), n, stride,
+                      _ptr(V), k, n * k, _ptr(out), k, n * k, 1.0, 0, self.stream)
+        return {ci: out[s] for s, ci in enumerate(active)}
 
     # -- K4..K7 for one contour --------------------------------------------
     def rayleigh_ritz(self, items: list, feast: bool = False, refine: bool = False) -> dict:
@@ -781,10 +864,13 @@ class _Engine:
             _lib.call("cirr_transpose", 0, _ptr(Qt), n, kmax * n, kmax, n, nb, _ptr(Q), kmax, n * kmax, st)
             AQ = torch.empty((nb, n, kmax), dtype=torch.complex128, device="cuda")
             BQ = torch.empty_like(AQ)
-            _lib.call("cirr_gemm", self.dp.gemm_kind, n, kmax, n, nb, _ptr(self.dp.a), n, 0, _ptr(Q), kmax, n * kmax, _ptr(AQ), kmax,
+            Am, Bm, mstride = self._mats([ci for ci, _ in items])
+            gk = self.dp.gemm_kind
+            _lib.call("cirr_gemm", gk, n, kmax, n, nb, _ptr(Am), n, mstride, _ptr(Q), kmax, n * kmax, _ptr(AQ), kmax,
                       n * kmax, 1.0, 0, st)
-            _lib.call("cirr_gemm", self.dp.gemm_kind, n, kmax, n, nb, _ptr(self.dp.b), n, 0, _ptr(Q), kmax, n * kmax, _ptr(BQ), kmax,
+            _lib.call("cirr_gemm", gk, n, kmax, n, nb, _ptr(Bm), n, mstride, _ptr(Q), kmax, n * kmax, _ptr(BQ), kmax,
                       n * kmax, 1.0, 0, st)
+            del Am, Bm
             At = torch.empty((nb, kmax, kmax), dtype=torch.complex128, device="cuda")
             Bt = torch.empty_like(At)
             kk = kmax * kmax
@@ -907,12 +993,7 @@ class _Engine:
         active = [i for i, c in enumerate(self.cs) if not c.done]
         if not active:
             return
-        rhs = {}
-        for ci in active:
-            c = self.cs[ci]
-            rng = np.random.default_rng(c.seed)
-            v = rng.standard_normal((n, c.ncols)).astype(complex)  # solvers.py:178-180
-            rhs[ci] = self.bmul(_h2d(v))
+        rhs = self.source_blocks(active)  # solvers.py:178-182
         stacked = self.apply(active, rhs, moments, real_rhs=True)
         it_of = {ci: 0 for ci in active}
         for it in range(cfg.max_refine):
@@ -982,6 +1063,7 @@ class _Engine:
         self._lat_streams = []
         self._tl_events = []
         self._tl(-1, -1, "start", bulk)
+        self.eager_dinv = True
         self._alloc_factors()
         first = {}
         ready = [threading.Event() for _ in self.cs]
@@ -1107,7 +1189,7 @@ class _Engine:
                 break
             for ci in active:
                 it_of[ci] = it
-            stacked = self.apply(active, {ci: self.bmul(u[ci]) for ci in active}, 1)  # y = P u (246)
+            stacked = self.apply(active, {ci: self.bmul(u[ci], ci) for ci in active}, 1)  # y = P u (246)
             rr = self.rayleigh_ritz([(ci, stacked[ci]) for ci in active], feast=True)
             nxt = []
             for ci in active:
@@ -1197,20 +1279,24 @@ def _run_contours(pencil, contours, cfg, seeds, moments_override=None, solver: s
     cfg = _cfg_view(cfg)
     dp = DevicePencil.of(pencil)
     cstates = [_Contour(i, c, cfg, s, dp.n, dp.complex) for i, (c, s) in enumerate(zip(contours, seeds))]
+    _run_states(dp, cstates, cfg, moments_override, solver)
+    return cstates
+
+
+def _run_states(dp, cstates, cfg, moments_override=None, solver: str = "cirr"):
     moments = cfg.n_moments if moments_override is None else moments_override
     for wave in _waves(cstates, dp.n, _hbm_budget(dp.n, cstates)):
         eng = _Engine(dp, wave, cfg)
         if solver == "feast":
             eng.factor()
             eng.run_feast()
-        elif len(wave) > 1 and _PIPELINE:
+        elif len(wave) > 1 and _PIPELINE and not eng.multi:
             eng.run_pipelined(moments)
         else:
             eng.factor()
             eng.run(moments)
         eng.free()
         del eng
-    return cstates
 
 
 # ---------------------------------------------------------------------------
@@ -1244,6 +1330,11 @@ def solve_multi(pencil, contours, cfg: SolverConfig | None = None, solver: str =
     t0 = time.perf_counter()
     contours = list(contours)
     cstates = _run_contours(pencil, contours, cfg, [seed + i for i in range(len(contours))], solver=solver)
+    return _multi_result(cstates, t0)
+
+
+def _multi_result(cstates, t0) -> MultiResult:
+    """solve_multi's aggregation (solvers.py:325-339) over one pencil's contours."""
     results, errors = [], []
     agg = SolveStats()
     for c in cstates:
@@ -1262,6 +1353,52 @@ def solve_multi(pencil, contours, cfg: SolverConfig | None = None, solver: str =
     _dedupe(results)
     agg.elapsed = time.perf_counter() - t0
     return MultiResult(results=results, errors=errors, stats=agg)
+
+
+def solve_multi_batch(pencils, contours, cfg: SolverConfig | None = None, solver: str = "cirr",
+                      seeds=None) -> list:
+    """``[solve_multi(p, cs, cfg, solver, seed=s) for p, cs, s in ...]`` for
+    many independent pencils of one size in one batched device pass: the
+    DeepContour dataset regime (BASELINE config 2, 256 GEPs of n=256).  The
+    reference solves such a batch one ``solve_multi`` call at a time
+    (bench.py:144); here every pencil x contour x node of a wave shares one
+    batched LU, one batched solve per pass and one batched Rayleigh-Ritz round.
+
+    ``contours`` is one contour list per pencil (or one list for all);
+    ``seeds`` one seed per pencil (default 0, solve_multi's default), contour i
+    of a pencil using seed + i as solve_multi does.  Pencils whose dtype or
+    Hermitian flag differ run in separate batches.  Per-pencil errors follow
+    solve_multi: the four isolated types land in ``MultiResult.errors``, any
+    other error propagates."""
+    if solver not in ("cirr", "feast"):
+        raise ParameterError(f"unknown solver {solver!r}")
+    t0 = time.perf_counter()
+    cfg = _cfg_view(cfg)
+    dps = [DevicePencil.of(p) for p in pencils]
+    if not dps:
+        return []
+    if contours and not isinstance(contours[0], (list, tuple)):
+        contours = [list(contours)] * len(dps)
+    if len(contours) != len(dps):
+        raise DimensionError("need one contour list per pencil")
+    seeds = [0] * len(dps) if seeds is None else [int(x) for x in seeds]
+    if len(seeds) != len(dps):
+        raise DimensionError("need one seed per pencil")
+    n = dps[0].n
+    if any(d.n != n for d in dps):
+        raise DimensionError("solve_multi_batch needs pencils of one size")
+    per = []
+    for g, (d, cs, sd) in enumerate(zip(dps, contours, seeds)):
+        st = [_Contour(i, c, cfg, sd + i, n, d.complex) for i, c in enumerate(cs)]
+        for c in st:
+            c.dp = d
+        per.append(st)
+    groups: dict = {}
+    for g, d in enumerate(dps):
+        groups.setdefault((d.complex, d.hermitian), []).append(g)
+    for gs in groups.values():
+        _run_states(dps[gs[0]], [c for g in gs for c in per[g]], cfg, None, solver)
+    return [_multi_result(st, t0) for st in per]
 
 
 def _dedupe(results) -> None:

@@ -113,6 +113,43 @@ def test_getrf_getrs(lib, n, batch, K, use_dinv):
         assert mp.cpu().numpy()[j] == pytest.approx(np.abs(np.diag(lu[j])).min())
 
 
+@pytest.mark.parametrize("K,use_dinv", [(8, False), (37, True), (37, False), (2, True)])
+@pytest.mark.parametrize("n", [256, 333])
+def test_getrs_gather(lib, n, K, use_dinv):
+    """cirr_zgetrs_gather over a scattered subset of the factors equals
+    cirr_zgetrs_batched on each factor alone, bit for bit."""
+    rng = np.random.default_rng(n + K)
+    nfac = 7
+    A = rng.standard_normal((nfac, n, n)) + 1j * rng.standard_normal((nfac, n, n))
+    F = cuda(A.copy())
+    ipiv = torch.empty((nfac, n), dtype=torch.int32, device="cuda")
+    perm = torch.empty((nfac, n), dtype=torch.int32, device="cuda")
+    mp = torch.empty(nfac, dtype=torch.float64, device="cuda")
+    info = torch.empty(nfac, dtype=torch.int32, device="cuda")
+    lib.call("cirr_zgetrf_batched", P(F), n, n, n * n, nfac, P(ipiv), P(perm), P(mp), P(info), P(ws_lu(n, nfac)), S())
+    dpp = lib.call("cirr_diag_inv_bytes", n, 1)
+    dinv_t = cuda(np.zeros(dpp * nfac, dtype=np.uint8))
+    if use_dinv:
+        lib.call("cirr_diag_inverses", P(F), n, n, n * n, nfac, P(dinv_t), S())
+    pen = np.array([5, 1, 6, 2], dtype=np.int32)
+    R = rng.standard_normal((2, n, K)) + 1j * rng.standard_normal((2, n, K))
+    Rd = cuda(R)
+    rhs_of = cuda(np.array([0, 1, 1, 0], dtype=np.int32))
+    Y = torch.empty((len(pen), n, K), dtype=torch.complex128, device="cuda")
+    lib.call("cirr_zgetrs_gather", P(F), n, n, n * n, nfac, P(cuda(pen)), len(pen), P(perm), P(Rd), K, n * K,
+             P(rhs_of), K, P(Y), K, n * K, P(dinv_t) if use_dinv else 0, S())
+    got = Y.cpu().numpy()
+    for j, f in enumerate(pen):
+        Y1 = torch.empty((1, n, K), dtype=torch.complex128, device="cuda")
+        ro = cuda(np.array([rhs_of.cpu().numpy()[j]], dtype=np.int32))
+        lib.call("cirr_zgetrs_batched", P(F[f]), n, n, n * n, 1, P(perm[f]), P(Rd), K, n * K, P(ro), K, P(Y1), K,
+                 n * K, (P(dinv_t) + int(f) * dpp) if use_dinv else 0, S())
+        assert np.array_equal(got[j], Y1.cpu().numpy()[0]), (j, f)
+        r = R[rhs_of.cpu().numpy()[j]]
+        res = np.linalg.norm(A[f] @ got[j] - r) / (np.linalg.norm(A[f]) * np.linalg.norm(got[j]))
+        assert res < 1e-14, res
+
+
 def test_getrf_singular(lib):
     n = 70
     A = np.diag(np.arange(1.0, n + 1)).astype(complex)

@@ -118,3 +118,50 @@ def test_deterministic_config3():
     e1 = solve_multi(dp, contours, cfg, seed=0).eigenvalues
     e2 = solve_multi(dp, contours, cfg, seed=0).eigenvalues
     assert np.array_equal(e1, e2)
+
+
+def test_config2_batched():
+    """All 256 GEPs of config 2 in one solve_multi_batch pass (BASELINE config
+    2, the dataset regime): the same parity bar per GEP as the one-at-a-time
+    run, and the same counts and pass numbers as solve_multi."""
+    from paper_2511_01927_b200 import solve_multi_batch
+    fix = golden("oracle_config2.npz")
+    ng = int(fix["n_gep"])
+    mats = [W.config2_matrices(s) for s in range(ng)]
+    cons = [[Contour.from_json_dict(d) for d in json.loads(str(fix[f"s{s}_contours"]))] for s in range(ng)]
+    cfg = SolverConfig(n_q=16, source_cols=8, n_moments=4)
+    multis = solve_multi_batch([DevicePencil(a, b, hermitian=True) for a, b in mats], cons, cfg)
+    assert len(multis) == ng
+    for s in range(ng):
+        check(*mats[s], fix, f"s{s}_", multis[s], cons[s])
+    for s in (0, 177, ng - 1):
+        one = solve_multi(DevicePencil(*mats[s], hermitian=True), cons[s], cfg, seed=0)
+        for r1, rb in zip(one.results, multis[s].results):
+            assert r1.stats.iterations == rb.stats.iterations
+            assert r1.stats.n_linear_solves == rb.stats.n_linear_solves
+            assert np.abs(r1.eigenvalues - rb.eigenvalues).max() <= 1e-12 * np.abs(r1.eigenvalues).max()
+
+
+def test_batch_mixed_contours_and_errors():
+    """solve_multi_batch over pencils with different contour lists and seeds:
+    each entry equals solve_multi(p, cs, seed=s); a contour with no eigenvalues
+    inside is isolated as NoEigenvaluesFound in its own pencil's result."""
+    from paper_2511_01927_b200 import NoEigenvaluesFound, solve_multi_batch
+    fix = golden("oracle_config2.npz")
+    mats = [W.config2_matrices(s) for s in (3, 4)]
+    c3 = [Contour.from_json_dict(d) for d in json.loads(str(fix["s3_contours"]))]
+    c4 = [Contour.from_json_dict(d) for d in json.loads(str(fix["s4_contours"]))][:1]
+    far = Contour(shape="circle", center=complex(-1e3, 0.0), radius=1.0)
+    cfg = SolverConfig(n_q=16, source_cols=8, n_moments=4)
+    dps = [DevicePencil(a, b, hermitian=True) for a, b in mats]
+    got = solve_multi_batch(dps, [c3, c4 + [far]], cfg, seeds=[5, 9])
+    want = [solve_multi(dps[0], c3, cfg, seed=5), solve_multi(dps[1], c4 + [far], cfg, seed=9)]
+    for g, w in zip(got, want):
+        assert len(g.results) == len(w.results)
+        for rg, rw in zip(g.results, w.results):
+            if rw is None:
+                assert rg is None
+                continue
+            assert len(rg.eigenvalues) == len(rw.eigenvalues)
+            assert np.abs(rg.eigenvalues - rw.eigenvalues).max() <= 1e-12 * np.abs(rw.eigenvalues).max()
+    assert got[1].results[1] is None and isinstance(got[1].errors[1], NoEigenvaluesFound)
