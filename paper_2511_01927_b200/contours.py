@@ -115,6 +115,20 @@ def contains(c, z: complex, slack: float = 0.0) -> bool:
             and c.im_min - slack < z.imag < c.im_max + slack)
 
 
+def contains_many(c, zs, slack: float = 0.0) -> np.ndarray:
+    """contains() over an array, elementwise with the same float64 arithmetic
+    (np.abs of a complex difference is the same hypot as Python's abs)."""
+    z = np.asarray(zs, dtype=np.complex128)
+    if c.shape == "circle":
+        return np.abs(z - complex(c.center)) < c.radius + slack
+    if c.shape == "ellipse":
+        dr = (z.real - complex(c.center).real) / (c.semi_re + slack)
+        di = (z.imag - complex(c.center).imag) / (c.semi_im + slack)
+        return dr * dr + di * di < 1.0
+    return ((c.re_min - slack < z.real) & (z.real < c.re_max + slack)
+            & (c.im_min - slack < z.imag) & (z.imag < c.im_max + slack))
+
+
 @dataclass(frozen=True)
 class QuadratureRule:
     """sum_j w_j f(z_j) approximates (1/2 pi i) \\oint f(z) dz (contours.py:127-137)."""

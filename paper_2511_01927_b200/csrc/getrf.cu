@@ -10,6 +10,7 @@
 // ties).  The factorisation also reports per pencil min_i |U_ii| (the
 // reference's singular-shift test, linalg.py:68-70) and LAPACK-style info.
 #include "common.cuh"
+#include <cstdlib>
 #include "gemm.cuh"
 #include "lu_gemm.cuh"
 
@@ -311,6 +312,22 @@ __global__ void init_kernel(double* minpiv, int* info, int batch) {
 // pencil_stride elements, leading dimension ld).  Outputs ipiv (batch x n,
 // 0-based LAPACK-style interchanges), perm (batch x n, row permutation),
 // minpiv (min_i |U_ii|) and info (first exact zero pivot, 1-based, or 0).
+// One CTA per pencil.  512 threads per CTA (measured best at n = 4096, and at
+// n = 512 / 2304 with 32 / 96 pencils); for large batches of short panels
+// (config 2: 8192 pencils, n = 256) the per-column latency chain dominates and
+// 128-thread CTAs keep ~3x more pencils in flight per SM (LU 61.5 -> 42.4 ms).
+// CIRR_PANEL_T overrides: 128 / 256 / 512.
+static int launch_panel(cplx* pencils, int n, long long ld, long long pstride, int batch, int k, int jb, int* ipiv,
+                        double* minpiv, int* info, cudaStream_t stream) {
+  static const int env_t = getenv("CIRR_PANEL_T") ? atoi(getenv("CIRR_PANEL_T")) : 0;
+  const int t = env_t > 0 ? env_t : (n <= 512 && batch >= 1024 ? 128 : PT2);
+  if (t == 128) panel2_kernel<128><<<batch, 128, 0, stream>>>(pencils, n, ld, pstride, k, jb, ipiv, minpiv, info);
+  else if (t == 256) panel2_kernel<256><<<batch, 256, 0, stream>>>(pencils, n, ld, pstride, k, jb, ipiv, minpiv, info);
+  else panel2_kernel<PT2><<<batch, PT2, 0, stream>>>(pencils, n, ld, pstride, k, jb, ipiv, minpiv, info);
+  CIRR_CHECK_LAUNCH();
+  return 0;
+}
+
 // Workspace for cirr_zgetrf_batched (L11^{-1} blocks); 0 disables that path.
 CIRR_API long long cirr_zgetrf_ws_bytes(int n, int batch) { return (long long)batch * NB * NB * 16 + 256; }
 
@@ -357,8 +374,7 @@ CIRR_API int cirr_zgetrf_batched(cplx* pencils, int n, long long ld, long long p
         if (i > 0)  // this panel's columns: A[ki:, ki:ki+64] -= L[ki:, k:ki] U[k:ki, ki:ki+64]
           CIRR_TRY(cirr::zgemm_sub_maps(maps.a, maps.b, maps.c, n - ki, NB, i * NB, batch, ki, k, k, ki, ki, ki,
                                         pencils, ld, pencil_stride, stream));
-        panel2_kernel<PT2><<<batch, PT2, 0, stream>>>(pencils, n, ld, pencil_stride, ki, NB, ipiv, minpiv, info);
-        CIRR_CHECK_LAUNCH();
+        CIRR_TRY(launch_panel(pencils, n, ld, pencil_stride, batch, ki, NB, ipiv, minpiv, info, stream));
         {
           dim3 g((n - NB + 255) / 256, batch);
           swap_kernel<<<g, 256, 0, stream>>>(pencils, n, ld, pencil_stride, ki, NB, ipiv);
@@ -382,8 +398,7 @@ CIRR_API int cirr_zgetrf_batched(cplx* pencils, int n, long long ld, long long p
   }
   for (int k = k0; k < n; k += NB) {
     const int jb = min(NB, n - k);
-    panel2_kernel<PT2><<<batch, PT2, 0, stream>>>(pencils, n, ld, pencil_stride, k, jb, ipiv, minpiv, info);
-    CIRR_CHECK_LAUNCH();
+    CIRR_TRY(launch_panel(pencils, n, ld, pencil_stride, batch, k, jb, ipiv, minpiv, info, stream));
     if (n - jb > 0) {
       dim3 g((n - jb + 255) / 256, batch);
       swap_kernel<<<g, 256, 0, stream>>>(pencils, n, ld, pencil_stride, k, jb, ipiv);

@@ -27,7 +27,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .contours import QuadratureRule, contains, moment_frame, quadrature_for
+from .contours import QuadratureRule, contains, contains_many, moment_frame, quadrature_for
 from .errors import (
     ConvergenceError,
     DeviceError,
@@ -441,7 +441,14 @@ class _Contour:
         return len(conv) >= getattr(self.contour, "expected_count", 0)
 
     def coef(self, moments: int) -> np.ndarray:
-        """c[j, m] = w_j zeta_j^m with zeta_j = (z_j - gamma)/rho (sequential powers)."""
+        """c[j, m] = w_j zeta_j^m with zeta_j = (z_j - gamma)/rho (sequential powers;
+        made once per moment count, read-only)."""
+        cache = self.__dict__.setdefault("_coef_cache", {})
+        if moments not in cache:
+            cache[moments] = self._coef(moments)
+        return cache[moments]
+
+    def _coef(self, moments: int) -> np.ndarray:
         out = np.empty((len(self.nodes), moments), dtype=np.complex128)
         for j, (z, w) in enumerate(zip(self.nodes, self.weights)):
             zeta = (z - self.gamma) / self.rho
@@ -569,9 +576,14 @@ class _Engine:
             _lib.call("cirr_diag_inverses", _ptr(self.pencils[a]), self.n, self.n, self.n * self.n, b - a,
                       _ptr(self.dinv) + a * self._dinv_per_pencil, self.stream)
 
-    def factor(self):
+    def factor(self, sources: bool = False):
+        """K1 + K2 for the wave, then the singular-shift test (one read-back).
+        sources: also enqueue the CIRR source blocks B V before that read-back,
+        so their host-side generation overlaps the factorisation."""
         self._alloc_factors()
         self._factor_range(0, self.P, np.concatenate([c.nodes[c.fidx] for c in self.cs]))
+        if sources:
+            self._src = self.source_blocks(list(range(len(self.cs))))
         if len(self.cs) == 1:
             self._check_factor(0)
             return
@@ -608,12 +620,15 @@ class _Engine:
             cplx_rhs.append(cx)
             ks.append(2 * kc if cx else kc)
         Ks = max(ks)
-        R = torch.zeros((nset, n, Ks), dtype=torch.complex128, device="cuda")
-        for s, ci in enumerate(active):
-            kc = rhs[ci].shape[1]
-            R[s, :, :kc].copy_(rhs[ci])
-            if cplx_rhs[s]:
-                R[s, :, kc:2 * kc].copy_(rhs[ci].conj())
+        if nset > 1 and not any(cplx_rhs) and all(k_ == Ks for k_ in ks):
+            R = torch.stack([rhs[ci] for ci in active])   # one copy kernel for the whole set
+        else:
+            R = torch.zeros((nset, n, Ks), dtype=torch.complex128, device="cuda")
+            for s, ci in enumerate(active):
+                kc = rhs[ci].shape[1]
+                R[s, :, :kc].copy_(rhs[ci])
+                if cplx_rhs[s]:
+                    R[s, :, kc:2 * kc].copy_(rhs[ci].conj())
         pen_idx, spos = [], [0]
         offs, coefs = [0], []
         for s, ci in enumerate(active):
@@ -713,6 +728,7 @@ class _Engine:
         """B @ x for a device (n x k) complex block (B of contour ci's pencil)."""
         d = self.dp if ci is None else self._dp_of(ci)
         torch, n = self.torch, self.n
+        x = x.contiguous()
         k = x.shape[1]
         out = torch.empty((n, k), dtype=torch.complex128, device="cuda")
         if k:
@@ -723,6 +739,7 @@ class _Engine:
     def amul(self, x, ci: int | None = None):
         d = self.dp if ci is None else self._dp_of(ci)
         torch, n = self.torch, self.n
+        x = x.contiguous()
         k = x.shape[1]
         out = torch.empty((n, k), dtype=torch.complex128, device="cuda")
         if k:
@@ -814,9 +831,12 @@ class _Engine:
             return out
         nb = len(items)
         cmax = max(S_.shape[0] for _, S_ in items)
-        W = torch.zeros((nb, cmax, n), dtype=torch.complex128, device="cuda")
-        for b, (_, S_) in enumerate(items):
-            W[b, : S_.shape[0]].copy_(S_)
+        if nb > 1 and all(S_.shape[0] == cmax for _, S_ in items):
+            W = torch.stack([S_ for _, S_ in items])
+        else:
+            W = torch.zeros((nb, cmax, n), dtype=torch.complex128, device="cuda")
+            for b, (_, S_) in enumerate(items):
+                W[b, : S_.shape[0]].copy_(S_)
         if try_cholqr and cmax <= n:
             # refinement blocks are normally far from rank deficient: when
             # ||R||_F ||R^-1||_F <= 1e5 certifies that no singular value is cut
@@ -921,10 +941,7 @@ class _Engine:
             if infos[b] < 0:
                 raise DeviceError("small eigensolver: QR iteration failed to converge")
             lb = lam_h[b, : ks[b]]
-            if herm:
-                keep = np.array([contains(self.cs[ci].contour, complex(v.real, 0.0)) for v in lb], dtype=bool)
-            else:
-                keep = np.array([contains(self.cs[ci].contour, v) for v in lb], dtype=bool)
+            keep = contains_many(self.cs[ci].contour, lb.real + 0j if herm else lb)
             if not np.any(keep):
                 out[ci] = ("none", None)
                 continue
@@ -983,8 +1000,10 @@ class _Engine:
             if herm:
                 lam_b = lam_b.real.copy()
             xall = X[b, :, : ks[b]].contiguous() if all_vectors else None
-            out[ci] = ("ok", lam_b, Xi[b, :, :k_in].contiguous(), res_h[b, :k_in].copy(), xall)
-            self.cs[ci].bx_dev = BX[b, :, :k_in].contiguous()   # B X, the next refinement's right-hand side
+            # views into the round's blocks (consumers copy or read them; bmul
+            # makes a contiguous copy where a raw pointer is needed)
+            out[ci] = ("ok", lam_b, Xi[b, :, :k_in], res_h[b, :k_in].copy(), xall)
+            self.cs[ci].bx_dev = BX[b, :, :k_in]   # B X, the next refinement's right-hand side
         return out
 
     # -- the reference control flow (solvers.py:165-227) for all contours ----
@@ -993,7 +1012,9 @@ class _Engine:
         active = [i for i, c in enumerate(self.cs) if not c.done]
         if not active:
             return
-        rhs = self.source_blocks(active)  # solvers.py:178-182
+        src = getattr(self, "_src", None)
+        self._src = None
+        rhs = {ci: src[ci] for ci in active} if src is not None else self.source_blocks(active)  # solvers.py:178-182
         stacked = self.apply(active, rhs, moments, real_rhs=True)
         it_of = {ci: 0 for ci in active}
         for it in range(cfg.max_refine):
@@ -1293,7 +1314,7 @@ def _run_states(dp, cstates, cfg, moments_override=None, solver: str = "cirr"):
         elif len(wave) > 1 and _PIPELINE and not eng.multi:
             eng.run_pipelined(moments)
         else:
-            eng.factor()
+            eng.factor(sources=True)
             eng.run(moments)
         eng.free()
         del eng
