@@ -1395,16 +1395,18 @@ def solve_multi_batch(pencils, contours, cfg: SolverConfig | None = None, solver
         raise ParameterError(f"unknown solver {solver!r}")
     t0 = time.perf_counter()
     cfg = _cfg_view(cfg)
-    dps = [DevicePencil.of(p) for p in pencils]
-    if not dps:
+    pencils = list(pencils)
+    if not pencils:
         return []
+    contours = list(contours)
     if contours and not isinstance(contours[0], (list, tuple)):
-        contours = [list(contours)] * len(dps)
-    if len(contours) != len(dps):
+        contours = [contours] * len(pencils)
+    if len(contours) != len(pencils):
         raise DimensionError("need one contour list per pencil")
-    seeds = [0] * len(dps) if seeds is None else [int(x) for x in seeds]
-    if len(seeds) != len(dps):
+    seeds = [0] * len(pencils) if seeds is None else [int(x) for x in seeds]
+    if len(seeds) != len(pencils):
         raise DimensionError("need one seed per pencil")
+    dps = [DevicePencil.of(p) for p in pencils]
     n = dps[0].n
     if any(d.n != n for d in dps):
         raise DimensionError("solve_multi_batch needs pencils of one size")

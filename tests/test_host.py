@@ -108,3 +108,38 @@ def test_conjugate_pair_selection():
     assert not _Contour(0, Contour(shape="circle", center=0.2 + 0.3j, radius=0.5), cfg, 0, 10).half
     assert not _Contour(0, Contour(shape="circle", center=1.0 + 0j, radius=0.5),
                         SolverConfig(n_q=32), 0, 10).half
+
+
+def test_solve_multi_batch_validates_before_upload():
+    """solve_multi_batch argument checks run before any device work (so they
+    hold without a GPU): solver name, one contour list and one seed per pencil."""
+    from paper_2511_01927_b200.errors import DimensionError
+    a = np.eye(4)
+    c = Contour(shape="circle", center=1 + 0j, radius=0.5)
+    pen = [(a, a), (a, a)]
+    assert S.solve_multi_batch([], [[c]]) == []
+    with pytest.raises(ParameterError):
+        S.solve_multi_batch(pen, [[c], [c]], solver="lanczos")
+    with pytest.raises(DimensionError):
+        S.solve_multi_batch(pen, [[c]])
+    with pytest.raises(DimensionError):
+        S.solve_multi_batch(pen, [[c], [c]], seeds=[0])
+
+
+def test_contains_many_matches_contains():
+    """The vectorised inside test makes the same decisions as contains() on
+    boundary-hugging values of every shape."""
+    from paper_2511_01927_b200.contours import contains, contains_many
+    rng = np.random.default_rng(7)
+    shapes = [Contour(shape="circle", center=0.3 + 0.1j, radius=0.7),
+              Contour(shape="ellipse", center=-0.5 + 0j, semi_re=0.3, semi_im=0.15),
+              Contour(shape="rect", re_min=-1.0, re_max=2.0, im_min=-0.5, im_max=0.25)]
+    for c in shapes:
+        th = rng.uniform(0, 2 * np.pi, 400)
+        z = np.concatenate([c.center + 1.2 * (rng.standard_normal(400) + 1j * rng.standard_normal(400)),
+                            (complex(getattr(c, "center", 0.5 - 0.125j)) + (1 + rng.uniform(-1e-15, 1e-15, 400))
+                             * np.exp(1j * th) * getattr(c, "radius", getattr(c, "semi_re", 1.5)))])
+        for slack in (0.0, 1e-3):
+            got = contains_many(c, z, slack)
+            want = np.array([contains(c, v, slack) for v in z])
+            assert np.array_equal(got, want)
