@@ -1051,6 +1051,7 @@ class _Engine:
                 break
             stacked = self.apply(list(refine.keys()), refine, 1)
             active = list(refine.keys())
+        self.fetch_vectors()
         for ci, c in enumerate(self.cs):
             if c.done:
                 continue
@@ -1253,7 +1254,9 @@ class _Engine:
                 f"no eigenvalues inside contour (expected {getattr(c.contour, 'expected_count', 0)})")
             return
         lam, res = c.lam, c.res
-        x = c.x_dev.cpu().numpy()
+        x = c.__dict__.pop("x_host", None)
+        if x is None:
+            x = c.x_dev.cpu().numpy()
         if res.max() > cfg.tol:  # solvers.py:215-219
             conv = res <= cfg.tol
             if not np.any(conv):
@@ -1263,6 +1266,21 @@ class _Engine:
         order = np.argsort(lam)  # solvers.py:220
         c.result = EigenResult(eigenvalues=lam[order], eigenvectors=x[:, order], residuals=res[order],
                                contour=c.contour, stats=c.stats)
+
+    def fetch_vectors(self):
+        """Every finishing contour's Ritz vectors in one device concat and one
+        D2H copy (instead of one synchronising copy per contour)."""
+        torch = self.torch
+        cs = [c for c in self.cs if not c.done and not getattr(c, "fatal", False)
+              and c.lam is not None and getattr(c, "x_dev", None) is not None and c.x_dev.numel()]
+        if len(cs) < 2:
+            return
+        flat = torch.cat([c.x_dev.reshape(-1) for c in cs]).cpu().numpy()
+        off = 0
+        for c in cs:
+            sz = c.x_dev.numel()
+            c.x_host = flat[off:off + sz].reshape(tuple(c.x_dev.shape))
+            off += sz
 
     def free(self):
         for name in ("pencils", "maxabs", "ipiv", "perm", "minpiv", "info", "dinv"):
