@@ -459,6 +459,29 @@ class _Contour:
         return out
 
 
+def _pad_stack(blocks: list, dim: int, width: int):
+    """Stack 2-D device blocks into (len, ...) zero-padded to `width` along
+    their axis `dim` (0 or 1): one stack and one indexed copy per distinct
+    width instead of one copy per block (device-agnostic tensor plumbing)."""
+    import torch
+    shape = list(blocks[0].shape)
+    shape[dim] = width
+    out = torch.zeros([len(blocks)] + shape, dtype=blocks[0].dtype, device=blocks[0].device)
+    groups: dict = {}
+    for i, b in enumerate(blocks):
+        groups.setdefault(int(b.shape[dim]), []).append(i)
+    for w, idx in groups.items():
+        if w == 0:
+            continue
+        src = torch.stack([blocks[i] for i in idx])
+        sel = torch.tensor(idx, dtype=torch.long, device=out.device)
+        if dim == 0:
+            out[:, :w].index_copy_(0, sel, src)
+        else:
+            out[:, :, :w].index_copy_(0, sel, src)
+    return out
+
+
 class _Engine:
     """Batched CIRR over the contours of one wave (factors stay resident).
 
@@ -622,6 +645,8 @@ class _Engine:
         Ks = max(ks)
         if nset > 1 and not any(cplx_rhs) and all(k_ == Ks for k_ in ks):
             R = torch.stack([rhs[ci] for ci in active])   # one copy kernel for the whole set
+        elif nset > 1 and not any(cplx_rhs):
+            R = _pad_stack([rhs[ci] for ci in active], 1, Ks)
         else:
             R = torch.zeros((nset, n, Ks), dtype=torch.complex128, device="cuda")
             for s, ci in enumerate(active):
@@ -834,9 +859,7 @@ class _Engine:
         if nb > 1 and all(S_.shape[0] == cmax for _, S_ in items):
             W = torch.stack([S_ for _, S_ in items])
         else:
-            W = torch.zeros((nb, cmax, n), dtype=torch.complex128, device="cuda")
-            for b, (_, S_) in enumerate(items):
-                W[b, : S_.shape[0]].copy_(S_)
+            W = _pad_stack([S_ for _, S_ in items], 0, cmax)
         if try_cholqr and cmax <= n:
             # refinement blocks are normally far from rank deficient: when
             # ||R||_F ||R^-1||_F <= 1e5 certifies that no singular value is cut
