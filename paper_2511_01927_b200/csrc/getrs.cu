@@ -27,10 +27,16 @@ constexpr int SD_LD = SNB + 1;    // diagonal block row
 constexpr int SX_LD = SKC + 1;
 constexpr int kStageA = SNB * SA_LD;
 constexpr int kStageB = SBK * SB_LD;
-constexpr int kSolveSmem = (2 * (kStageA + kStageB) + SNB * SD_LD + SNB * SX_LD + SNB) * 16;
+// The diagonal block is kept packed (its triangle only, element (hi, lo) at
+// hi (hi + 1) / 2 + lo) in the cp.async stage area, which is idle while the
+// block is solved: 93 KB per CTA, so two CTAs share an SM.
+constexpr int kPackedD = SNB * (SNB + 1) / 2;
+static_assert(kPackedD <= 2 * (kStageA + kStageB), "packed diagonal block must fit the stage area");
+constexpr int kSolveSmem = (2 * (kStageA + kStageB) + SNB * SX_LD + SNB) * 16;
+__device__ __forceinline__ int pk_tri(int hi, int lo) { return hi * (hi + 1) / 2 + lo; }
 
 template <bool LOWER>
-__global__ void __launch_bounds__(256, 1) trsm_blocked_kernel(const cplx* __restrict__ LU, long long ld,
+__global__ void __launch_bounds__(256, 2) trsm_blocked_kernel(const cplx* __restrict__ LU, long long ld,
                                                               long long pstride, int n,
                                                               cplx* __restrict__ Y, long long ldy,
                                                               long long ystride, int K,
@@ -38,8 +44,8 @@ __global__ void __launch_bounds__(256, 1) trsm_blocked_kernel(const cplx* __rest
   extern __shared__ __align__(16) cplx ssm[];
   cplx* stA = ssm;                                   // 2 stages
   cplx* stB = ssm + 2 * kStageA;
-  cplx* D = ssm + 2 * (kStageA + kStageB);           // diagonal block
-  cplx* X = D + SNB * SD_LD;                         // RHS block
+  cplx* D = ssm;                                     // packed diagonal block (aliases the stages)
+  cplx* X = ssm + 2 * (kStageA + kStageB);           // RHS block
   cplx* dinv = X + SNB * SX_LD;
   const int b = blockIdx.y;
   const int c0 = blockIdx.x * SKC;
@@ -119,10 +125,12 @@ __global__ void __launch_bounds__(256, 1) trsm_blocked_kernel(const cplx* __rest
         __syncthreads();
       }
     }
-    // load the diagonal block and the RHS block
+    // load the diagonal block's triangle (packed) and the RHS block
     for (int e = tid; e < SNB * SNB; e += 256) {
       int r = e / SNB, c = e % SNB;
-      D[r * SD_LD + c] = (r < nbi && c < nbi) ? T[(long long)(i0 + r) * ld + i0 + c] : cmk(0.0, 0.0);
+      if (LOWER ? c <= r : r <= c)
+        D[LOWER ? pk_tri(r, c) : pk_tri(c, r)] =
+            (r < nbi && c < nbi) ? T[(long long)(i0 + r) * ld + i0 + c] : cmk(0.0, 0.0);
     }
     for (int e = tid; e < SNB * SKC; e += 256) {
       int r = e / SKC, c = e % SKC;
@@ -140,14 +148,14 @@ __global__ void __launch_bounds__(256, 1) trsm_blocked_kernel(const cplx* __rest
           cplx v = X[r * SX_LD + c];
           X[r * SX_LD + c] = cmk(v.x - cr[i][j][h], v.y - ci[i][j][h]);
         }
-    if (!LOWER && tid < SNB) dinv[tid] = tid < nbi ? crecip(D[tid * SD_LD + tid]) : cmk(0.0, 0.0);
+    if (!LOWER && tid < SNB) dinv[tid] = tid < nbi ? crecip(D[pk_tri(tid, tid)]) : cmk(0.0, 0.0);
     __syncthreads();
-    // diagonal solve: thread column c, row group g
+    // diagonal solve: thread column c, row group g (a warp reads one D element: broadcast)
     const int c = tid % SKC, g = tid / SKC;
     if (LOWER) {
       for (int i = 0; i < nbi - 1; ++i) {
         const cplx xi = X[i * SX_LD + c];
-        for (int r = i + 1 + g; r < nbi; r += 8) cfms(X[r * SX_LD + c], D[r * SD_LD + i], xi);
+        for (int r = i + 1 + g; r < nbi; r += 8) cfms(X[r * SX_LD + c], D[pk_tri(r, i)], xi);
         __syncthreads();
       }
     } else {
@@ -155,7 +163,7 @@ __global__ void __launch_bounds__(256, 1) trsm_blocked_kernel(const cplx* __rest
         const cplx xi = cmul(X[i * SX_LD + c], dinv[i]);
         __syncthreads();
         if (g == 0) X[i * SX_LD + c] = xi;
-        for (int r = g; r < i; r += 8) cfms(X[r * SX_LD + c], D[r * SD_LD + i], xi);
+        for (int r = g; r < i; r += 8) cfms(X[r * SX_LD + c], D[pk_tri(i, r)], xi);
         __syncthreads();
       }
     }
