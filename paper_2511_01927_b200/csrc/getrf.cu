@@ -53,7 +53,7 @@ __device__ __forceinline__ int block_argmax(double best, int bi, double* rv, int
 }
 
 template <int PTT>
-__global__ void __launch_bounds__(PTT) panel2_kernel(cplx* __restrict__ P, int n, long long ld, long long pstride,
+__global__ void __launch_bounds__(PTT, PTT == 128 ? 4 : 1) panel2_kernel(cplx* __restrict__ P, int n, long long ld, long long pstride,
                                                      int k, int jb, int* __restrict__ ipiv,
                                                      double* __restrict__ minpiv, int* __restrict__ info) {
   constexpr int PW2 = PTT / 32;
@@ -315,7 +315,7 @@ __global__ void init_kernel(double* minpiv, int* info, int batch) {
 // One CTA per pencil.  512 threads per CTA (measured best at n = 4096, and at
 // n = 512 / 2304 with 32 / 96 pencils); for large batches of short panels
 // (config 2: 8192 pencils, n = 256) the per-column latency chain dominates and
-// 128-thread CTAs keep ~3x more pencils in flight per SM (LU 61.5 -> 42.4 ms).
+// 128-thread CTAs keep ~4x more pencils in flight per SM (4 CTAs per SM at 128 registers; LU 61.5 -> 38.1 ms).
 // CIRR_PANEL_T overrides: 128 / 256 / 512.
 static int launch_panel(cplx* pencils, int n, long long ld, long long pstride, int batch, int k, int jb, int* ipiv,
                         double* minpiv, int* info, cudaStream_t stream) {
