@@ -17,6 +17,7 @@
 // k <= 1024.  Matrices live in a global workspace (L2 resident at these
 // sizes); every reduction is fixed-order, so results are reproducible.
 #include "common.cuh"
+#include <cstdlib>
 
 namespace {
 
@@ -90,11 +91,13 @@ __device__ __forceinline__ void rr_pair(int round, int kk, int cp, int& p, int& 
   if (p > q) { int t = p; p = q; q = t; }
 }
 
+template <bool SM>
 __global__ void __launch_bounds__(ET) herm_eig_kernel(const cplx* __restrict__ At, const cplx* __restrict__ Bt,
                                                       long long ldin, long long sin_, const int* __restrict__ kdim,
                                                       int kmax, void* ws, long long wstride,
                                                       cplx* __restrict__ lam, cplx* __restrict__ S, long long lds,
                                                       long long sS, int* __restrict__ info) {
+  extern __shared__ __align__(16) cplx hsm[];   // A and V when they fit (in_smem)
   __shared__ double red[32];
   __shared__ double rot_c[512];
   __shared__ cplx rot_s[512];
@@ -102,19 +105,24 @@ __global__ void __launch_bounds__(ET) herm_eig_kernel(const cplx* __restrict__ A
   __shared__ int s_flag, s_count;
   const int prob = blockIdx.x;
   const int k = kdim[prob];
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   EigWs w = carve(ws, wstride, prob, kmax);
   const cplx* Ai = At + (long long)prob * sin_;
   const cplx* Bi = Bt + (long long)prob * sin_;
   cplx *A = w.A, *L = w.L, *V = w.V, *T = w.T;
+  if (SM) {  // A, V in shared memory: every Jacobi round costs shared-memory latency, not an L2 round trip
+    A = hsm;
+    V = hsm + (long long)kmax * (kmax + 1);
+  }
   const int ld = kmax;
+  const int la = SM ? kmax + 1 : kmax;  // A / V row length (padded in shared memory: column walks hit distinct banks)
   if (tid == 0) s_flag = 0;
   // 1. symmetrise
   for (int e = tid; e < k * k; e += ET) {
     int r = e / k, c = e % k;
     cplx a = Ai[(long long)r * ldin + c], at = Ai[(long long)c * ldin + r];
     cplx b = Bi[(long long)r * ldin + c], bt = Bi[(long long)c * ldin + r];
-    A[r * ld + c] = cmk(0.5 * (a.x + at.x), 0.5 * (a.y - at.y));
+    A[r * la + c] = cmk(0.5 * (a.x + at.x), 0.5 * (a.y - at.y));
     L[r * ld + c] = cmk(0.5 * (b.x + bt.x), 0.5 * (b.y - bt.y));
   }
   __syncthreads();
@@ -145,15 +153,15 @@ __global__ void __launch_bounds__(ET) herm_eig_kernel(const cplx* __restrict__ A
   // 3. X = L^-1 A (column per thread), then A' = L^-1 X^H  (into T)
   for (int c = tid; c < k; c += ET) {
     for (int i = 0; i < k; ++i) {
-      cplx v = A[i * ld + c];
-      for (int l = 0; l < i; ++l) cfms(v, L[i * ld + l], A[l * ld + c]);
-      A[i * ld + c] = cscale(v, 1.0 / L[i * ld + i].x);
+      cplx v = A[i * la + c];
+      for (int l = 0; l < i; ++l) cfms(v, L[i * ld + l], A[l * la + c]);
+      A[i * la + c] = cscale(v, 1.0 / L[i * ld + i].x);
     }
   }
   __syncthreads();
   for (int c = tid; c < k; c += ET) {
     for (int i = 0; i < k; ++i) {
-      cplx v = cconj(A[c * ld + i]);
+      cplx v = cconj(A[c * la + i]);
       for (int l = 0; l < i; ++l) cfms(v, L[i * ld + l], T[l * ld + c]);
       T[i * ld + c] = cscale(v, 1.0 / L[i * ld + i].x);
     }
@@ -164,8 +172,8 @@ __global__ void __launch_bounds__(ET) herm_eig_kernel(const cplx* __restrict__ A
     int r = e / k, c = e % k;
     cplx a = T[r * ld + c], at = T[c * ld + r];
     cplx v = cmk(0.5 * (a.x + at.x), 0.5 * (a.y - at.y));
-    A[r * ld + c] = v;
-    V[r * ld + c] = cmk(r == c ? 1.0 : 0.0, 0.0);
+    A[r * la + c] = v;
+    V[r * la + c] = cmk(r == c ? 1.0 : 0.0, 0.0);
     fro += cabs2(v);
   }
   fro = sqrt(block_sum(fro, red));
@@ -182,8 +190,8 @@ __global__ void __launch_bounds__(ET) herm_eig_kernel(const cplx* __restrict__ A
         rr_pair(round, t, cp, p, q);
         rot_p[t] = p; rot_q[t] = q; rot_c[t] = 1.0; rot_s[t] = cmk(0.0, 0.0);
         if (q < k) {
-          const double app = A[p * ld + p].x, aqq = A[q * ld + q].x;
-          const cplx apq = A[p * ld + q];
+          const double app = A[p * la + p].x, aqq = A[q * la + q].x;
+          const cplx apq = A[p * la + q];
           const double ag = cabs(apq);
           if (ag > small && ag > EPS * sqrt(fabs(app)) * sqrt(fabs(aqq))) {
             double cs; cplx se;
@@ -196,40 +204,42 @@ __global__ void __launch_bounds__(ET) herm_eig_kernel(const cplx* __restrict__ A
         }
       }
       __syncthreads();
-      // columns: A <- A J, V <- V J
-      for (int e = tid; e < np * k; e += ET) {
-        const int t = e / k, r = e % k;
+      // columns: A <- A J, V <- V J (one warp per rotation, lanes over rows)
+      for (int t = wid; t < np; t += ET / 32) {
         const int p = rot_p[t], q = rot_q[t];
         if (q >= k) continue;
         const double cs = rot_c[t];
         const cplx se = rot_s[t], sec = cconj(se);
-        cplx x = A[r * ld + p], y = A[r * ld + q];
-        A[r * ld + p] = csub(cscale(x, cs), cmul(sec, y));
-        A[r * ld + q] = cadd(cmul(se, x), cscale(y, cs));
-        x = V[r * ld + p]; y = V[r * ld + q];
-        V[r * ld + p] = csub(cscale(x, cs), cmul(sec, y));
-        V[r * ld + q] = cadd(cmul(se, x), cscale(y, cs));
+        for (int r = lane; r < k; r += 32) {
+          cplx x = A[r * la + p], y = A[r * la + q];
+          A[r * la + p] = csub(cscale(x, cs), cmul(sec, y));
+          A[r * la + q] = cadd(cmul(se, x), cscale(y, cs));
+          x = V[r * la + p]; y = V[r * la + q];
+          V[r * la + p] = csub(cscale(x, cs), cmul(sec, y));
+          V[r * la + q] = cadd(cmul(se, x), cscale(y, cs));
+        }
       }
       __syncthreads();
-      // rows: A <- J^H A
-      for (int e = tid; e < np * k; e += ET) {
-        const int t = e / k, c = e % k;
+      // rows: A <- J^H A (one warp per rotation, lanes over columns)
+      for (int t = wid; t < np; t += ET / 32) {
         const int p = rot_p[t], q = rot_q[t];
         if (q >= k) continue;
         const double cs = rot_c[t];
         const cplx se = rot_s[t], sec = cconj(se);
-        cplx x = A[p * ld + c], y = A[q * ld + c];
-        A[p * ld + c] = csub(cscale(x, cs), cmul(se, y));
-        A[q * ld + c] = cadd(cmul(sec, x), cscale(y, cs));
+        for (int c = lane; c < k; c += 32) {
+          cplx x = A[p * la + c], y = A[q * la + c];
+          A[p * la + c] = csub(cscale(x, cs), cmul(se, y));
+          A[q * la + c] = cadd(cmul(sec, x), cscale(y, cs));
+        }
       }
       __syncthreads();
       for (int t = tid; t < np; t += ET) {
         const int p = rot_p[t], q = rot_q[t];
         if (q >= k) continue;
-        A[p * ld + q] = cmk(0.0, 0.0);
-        A[q * ld + p] = cmk(0.0, 0.0);
-        A[p * ld + p].y = 0.0;
-        A[q * ld + q].y = 0.0;
+        A[p * la + q] = cmk(0.0, 0.0);
+        A[q * la + p] = cmk(0.0, 0.0);
+        A[p * la + p].y = 0.0;
+        A[q * la + q].y = 0.0;
       }
       __syncthreads();
     }
@@ -238,10 +248,10 @@ __global__ void __launch_bounds__(ET) herm_eig_kernel(const cplx* __restrict__ A
   }
   // 5. sort ascending, s = L^-H W
   for (int i = tid; i < k; i += ET) {
-    const double li = A[i * ld + i].x;
+    const double li = A[i * la + i].x;
     int rank = 0;
     for (int j = 0; j < k; ++j) {
-      const double lj = A[j * ld + j].x;
+      const double lj = A[j * la + j].x;
       rank += (lj < li) || (lj == li && j < i);
     }
     w.d[i] = (double)rank;
@@ -252,7 +262,7 @@ __global__ void __launch_bounds__(ET) herm_eig_kernel(const cplx* __restrict__ A
   for (int c = tid; c < k; c += ET) {
     const int rank = (int)w.d[c];
     for (int i = k - 1; i >= 0; --i) {
-      cplx v = V[i * ld + c];
+      cplx v = V[i * la + c];
       for (int l = i + 1; l < k; ++l) cfms(v, cconj(L[l * ld + i]), T[l * ld + c]);
       v = cscale(v, 1.0 / L[i * ld + i].x);
       T[i * ld + c] = v;
@@ -705,9 +715,22 @@ CIRR_API int cirr_small_eig(int hermitian, const cplx* At, const cplx* Bt, long 
   if (kmax <= 0 || kmax > 1024 || nprob <= 0) return CIRR_EINVAL;
   long long wstride = cirr_small_eig_ws_bytes(kmax);
   wstride = (wstride + 255) / 256 * 256;
-  if (hermitian)
-    herm_eig_kernel<<<nprob, ET, 0, stream>>>(At, Bt, ldin, sin_, kdim, kmax, ws, wstride, lam, S, lds, sS, info);
-  else
+  if (hermitian) {
+    // A and V in shared memory for kmax <= 78 (2 kmax (kmax+1) complex <= 193 KB next
+    // to the 16 KB of static rotation tables); CIRR_HERM_SMEM=0 disables
+    static const bool hs = !(getenv("CIRR_HERM_SMEM") && getenv("CIRR_HERM_SMEM")[0] == '0');
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(herm_eig_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 78 * 79 * 16);
+      attr = true;
+    }
+    if (hs && kmax <= 78)
+      herm_eig_kernel<true><<<nprob, ET, (size_t)2 * kmax * (kmax + 1) * sizeof(cplx), stream>>>(
+          At, Bt, ldin, sin_, kdim, kmax, ws, wstride, lam, S, lds, sS, info);
+    else
+      herm_eig_kernel<false><<<nprob, ET, 0, stream>>>(At, Bt, ldin, sin_, kdim, kmax, ws, wstride, lam, S, lds, sS,
+                                                      info);
+  } else
     gen_eig_kernel<<<nprob, GT, 0, stream>>>(At, Bt, ldin, sin_, kdim, kmax, ws, wstride, lam, S, lds, sS, info);
   CIRR_CHECK_LAUNCH();
   return 0;

@@ -280,7 +280,7 @@ def test_orth_cholqr2(lib, c):
     assert ok.tolist() == [0, 0]
 
 
-@pytest.mark.parametrize("k", [1, 6, 64, 200])
+@pytest.mark.parametrize("k", [1, 6, 64, 80, 81, 200])
 def test_small_eig_hermitian(lib, k):
     rng = np.random.default_rng(k)
     x = rng.standard_normal((k, k)) + 1j * rng.standard_normal((k, k))
