@@ -165,3 +165,24 @@ def test_batch_mixed_contours_and_errors():
             assert len(rg.eigenvalues) == len(rw.eigenvalues)
             assert np.abs(rg.eigenvalues - rw.eigenvalues).max() <= 1e-12 * np.abs(rw.eigenvalues).max()
     assert got[1].results[1] is None and isinstance(got[1].errors[1], NoEigenvaluesFound)
+
+
+def test_batch_feast_matches_per_pencil():
+    """solve_multi_batch(solver="feast") equals feast solve_multi per pencil
+    (solvers.py:230-285 on the shared batched factors)."""
+    from paper_2511_01927_b200 import solve_multi_batch
+    fix = golden("oracle_config2.npz")
+    mats = [W.config2_matrices(s) for s in (10, 11, 12)]
+    cons = [[Contour.from_json_dict(d) for d in json.loads(str(fix[f"s{s}_contours"]))] for s in (10, 11, 12)]
+    cfg = SolverConfig(n_q=16, source_cols=8, n_moments=4)
+    dps = [DevicePencil(a, b, hermitian=True) for a, b in mats]
+    got = solve_multi_batch(dps, cons, cfg, solver="feast")
+    for g, dp, cs in zip(got, dps, cons):
+        w = solve_multi(dp, cs, cfg, solver="feast", seed=0)
+        for rg, rw in zip(g.results, w.results):
+            assert (rg is None) == (rw is None)
+            if rw is None:
+                continue
+            assert len(rg.eigenvalues) == len(rw.eigenvalues)
+            assert rg.stats.iterations == rw.stats.iterations
+            assert np.abs(rg.eigenvalues - rw.eigenvalues).max() <= 1e-12 * np.abs(rw.eigenvalues).max()
