@@ -365,7 +365,11 @@ CIRR_API int cirr_zgetrf_batched(cplx* pencils, int n, long long ld, long long p
     // factored, its rows right of it receive the same deferred updates and
     // L_ii^-1 (U rows, in place).  Row interchanges of a panel go to every
     // column outside it and commute with the deferred row-wise updates.
-    const int PB = n >= 2048 ? 8 : (n >= 1024 ? 4 : 2);
+    // CIRR_LU_PB overrides the panels per step (config 3, n = 2304: 119.0 /
+    // 119.6 / 119.1 ms at 8 / 4 / 6 -- the 256-column tail costs nothing;
+    // config 5: 5.44 s at 8 vs 5.50 s at 4)
+    static const int pb_env = getenv("CIRR_LU_PB") ? atoi(getenv("CIRR_LU_PB")) : 0;
+    const int PB = pb_env > 0 ? pb_env : (n >= 2048 ? 8 : (n >= 1024 ? 4 : 2));
     const int W = PB * NB;
     for (; k0 + W <= n; k0 += W) {
       const int k = k0, rest = n - k0 - W;
