@@ -449,6 +449,8 @@ class _Contour:
         return cache[moments]
 
     def _coef(self, moments: int) -> np.ndarray:
+        if moments == 1:  # w_j * (1+0j): exact products, so numpy's multiply gives the loop's bits
+            return (self.weights * (1.0 + 0.0j))[:, None].copy()
         out = np.empty((len(self.nodes), moments), dtype=np.complex128)
         for j, (z, w) in enumerate(zip(self.nodes, self.weights)):
             zeta = (z - self.gamma) / self.rho

@@ -160,3 +160,17 @@ def test_pad_stack_matches_per_block_copies():
     for i, b in enumerate(bl):
         ref[i, :b.shape[0]] = b
     assert torch.equal(S._pad_stack(bl, 0, 5), ref)
+
+
+def test_single_moment_coefficients_bitwise():
+    """The moments == 1 fast path equals the sequential-power loop bit for bit."""
+    for shape in ("circle", "ellipse"):
+        c = Contour(shape=shape, center=0.5 - 0.25j, radius=0.3, semi_re=0.3, semi_im=0.15)
+        st = S._Contour(0, c, S.SolverConfig(n_q=64, n_moments=8), 0, 10)
+        fast = st._coef(1)
+        loop = np.empty((len(st.nodes), 1), dtype=np.complex128)
+        for j, w in enumerate(st.weights):
+            loop[j, 0] = w * (1.0 + 0.0j)
+        assert np.array_equal(fast.view(np.float64), loop.view(np.float64))
+        assert np.array_equal(np.ascontiguousarray(fast[:, 0]).view(np.float64),
+                              np.ascontiguousarray(st._coef(4)[:, 0]).view(np.float64))
