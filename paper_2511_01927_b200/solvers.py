@@ -476,7 +476,9 @@ def _pad_stack(blocks: list, dim: int, width: int):
         if w == 0:
             continue
         src = torch.stack([blocks[i] for i in idx])
-        sel = torch.tensor(idx, dtype=torch.long, device=out.device)
+        sel = torch.tensor(idx, dtype=torch.long)
+        if out.is_cuda:  # pinned, stream-ordered upload: no host synchronisation
+            sel = sel.pin_memory().to(out.device, non_blocking=True)
         if dim == 0:
             out[:, :w].index_copy_(0, sel, src)
         else:
