@@ -16,9 +16,16 @@ inputs and D2H of eigenpairs inside the timed region).  The pencils (34 GB)
 exceed L2 (126 MB), so no L2 flush is needed between steps.
 
 `--impl reference` times the CPU oracle (oracle/cirr.py, the restated
-reference path with LAPACK dense LU) on the host cores: a bounded sample of the
-same GEP (6 of the 128 pencils: assembly + LU + every solve pass; one
-Rayleigh-Ritz round), extrapolated to one GEP.
+reference path with LAPACK dense LU, all host threads) on ONE FULL config-4
+GEP (its whole solve_multi: 128 LUs, every refinement pass, every
+Rayleigh-Ritz round), so its `value` is measured, not extrapolated; it also
+reports the bounded-sample estimate beside it.  `steps` there is the number of
+full GEPs timed (1): a GEP takes minutes on the host.  Both arms print the same
+`config` dict.
+
+`per_config` (GPU arm, N=1): BASELINE configs 2 (one solve_multi_batch of the
+256 GEPs) and 5 (one n=8000 GEP), each device-timed and end to end, with the LU
+TF/s and the in-contour counts checked against the oracle fixtures.
 """
 
 from __future__ import annotations
@@ -52,6 +59,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-variants", action="store_true", help="skip the labelled (non-reference) variants")
+    ap.add_argument("--no-per-config", action="store_true", help="skip the config 2 / config 5 block")
     return ap.parse_args()
 
 
@@ -197,29 +205,49 @@ def build_workload(seed):
     return W.config4(seed=seed)
 
 
+def bench_config(wl) -> dict:
+    """The `config` dict both arms print (identical, so the driver can pair them)."""
+    return {"workload": "BASELINE config 4: n=4096 dense non-Hermitian GEP, 2 ellipses (0.3x0.15 at +-0.5), "
+                        "N=64, L=32, M=8, tol=1e-10, max_refine=8",
+            "pencils": wl.n_q * len(wl.contours), "n": wl.n, "n_q": wl.n_q, "source_cols": wl.source_cols,
+            "n_moments": wl.n_moments, "tol": 1e-10, "seed": 0, "parallelism": "replicas (one GEP per rank)",
+            "l2_flush": "not needed: 34 GB of pencils per step >> 126 MB L2"}
+
+
 def run_reference(args):
+    """The reference's CPU path (the restated oracle: reference solve_multi plus
+    the SURVEY 8(c) deltas, LAPACK dense LU) on one full config-4 GEP, all host
+    threads; the bounded-sample estimate is reported beside it."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
+    from oracle.cirr import OracleConfig, Pencil
+    from oracle.cirr import solve_multi as oracle_solve_multi
+
     wl = build_workload(0)
     cores = os.cpu_count() or 1
-    times = []
-    desc = ""
-    for _ in range(max(args.warmup, 0) and 1):  # one untimed warm-up sample (page-in, BLAS init)
-        cpu_sample(wl, sample_pencils=1)
-    for _ in range(args.steps):
-        per_gep, desc, _ = cpu_sample(wl)
-        times.append(per_gep)
-    per = statistics.median(times)
-    value = 1.0 / per
+    if args.warmup > 0:  # untimed: page-in, BLAS thread pool start-up
+        cpu_sample(wl, sample_pencils=1, passes=1)
+    ocfg = OracleConfig(n_q=wl.n_q, source_cols=wl.source_cols, n_moments=wl.n_moments, tol=1e-10)
+    t0 = time.perf_counter()
+    m = oracle_solve_multi(Pencil(wl.a, wl.b, False), wl.contours, ocfg, seed=0)
+    full = time.perf_counter() - t0
+    counts = [0 if r is None else len(r.eigenvalues) for r in m.results]
+    iters = [0 if r is None else r.iterations for r in m.results]
+    est, desc, wall = cpu_sample(wl, refine_cols=max(counts), passes=max(iters))
+    value = 1.0 / full
+    sample = (f"one full config-4 GEP: oracle solve_multi (scipy LAPACK zgetrf/zgetrs, BLAS threads="
+              f"{os.environ.get('OPENBLAS_NUM_THREADS', 'default')}), 128 pencils, {max(iters)} passes, "
+              f"{sum(counts)} eigenpairs, wall {full:.1f} s")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic (seeded config 4)",
-        "config": {"workload": "BASELINE config 4: n=4096 dense non-Hermitian GEP, 2 ellipses, N=64, L=32, M=8",
-                   "parallelism": "cpu"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": desc,
-                         "cpu_model": cpu_model()},
+        "steps": 1, "steps_requested": args.steps, "warmup": args.warmup, "ms_per_step": full * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64)",
+        "data": "synthetic (seeded BASELINE config 4)", "config": bench_config(wl),
+        "eigenpairs": counts, "iterations": iters,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
+                         "cpu_model": cpu_model(),
+                         "sampled_estimate": {"value": 1.0 / est, "unit": UNIT, "sample": desc}},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -227,6 +255,123 @@ def run_reference(args):
 
 # ---------------------------------------------------------------------------
 # GPU arm
+
+
+class HostPencil:
+    """What a reference caller passes: host numpy A, B (dense) and the flag."""
+
+    def __init__(self, a, b, hermitian):
+        self.a, self.b, self.hermitian = a, b, hermitian
+
+
+def _timed(fn, reps=1):
+    """CUDA-event time (ms, median over reps) of fn() on torch's current stream
+    (the stream libcirr launches on), plus the stage timer totals of the last rep."""
+    import torch
+
+    from paper_2511_01927_b200 import solvers as S
+
+    times, out, timer = [], None, None
+    for _ in range(reps):
+        timer = S.StageTimer()
+        S.set_stage_timer(timer)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        out = fn()
+        e1.record()
+        torch.cuda.synchronize()
+        S.set_stage_timer(None)
+        times.append(e0.elapsed_time(e1))
+    return statistics.median(times), out, timer
+
+
+def _wall(fn, reps=1):
+    import torch
+
+    times, out = [], None
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        out = fn()
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t)
+    return statistics.median(times), out
+
+
+def _lu_line(timer):
+    lu_ms = timer.totals().get("lu", 0.0)
+    fl = timer.work.get("lu_flops", 0.0)
+    tf = fl / (lu_ms / 1e3) / 1e12 if lu_ms else 0.0
+    return {"lu_ms": lu_ms, "lu_flops": fl, "lu_tflops": tf, "lu_frac_of_fp64_peak": tf / FP64_DMMA_PEAK_TFLOPS}
+
+
+def per_config_block():
+    """BASELINE configs 2 and 5 on the driver's clock.
+    Contours and the oracle's in-contour counts come from the committed oracle
+    fixtures (tests/golden/oracle_config{2,5}.npz, the checker)."""
+    import torch
+
+    from paper_2511_01927_b200 import Contour, DevicePencil, SolverConfig, solve_multi, solve_multi_batch
+    from paper_2511_01927_b200 import workloads as W
+
+    gold = os.path.join(ROOT, "tests", "golden")
+    out = {}
+
+    # config 2: 256 independent n=256 GEPs, one solve_multi_batch
+    fix = np.load(os.path.join(gold, "oracle_config2.npz"))
+    ng = int(fix["n_gep"])
+    mats = [W.config2_matrices(s) for s in range(ng)]
+    cons = [[Contour.from_json_dict(d) for d in json.loads(str(fix[f"s{s}_contours"]))] for s in range(ng)]
+    want = [[len(fix[f"s{s}_c{i}_eigs"]) for i in range(len(cons[s]))] for s in range(ng)]
+    cfg = SolverConfig(n_q=16, source_cols=8, n_moments=4)
+    dps = [DevicePencil(a, b, hermitian=True) for a, b in mats]
+    solve_multi_batch(dps, cons, cfg)  # warm-up
+    ms, res, timer = _timed(lambda: solve_multi_batch(dps, cons, cfg), reps=3)
+    got = [[0 if x is None else len(x.eigenvalues) for x in m.results] for m in res]
+    hps = [HostPencil(a, b, True) for a, b in mats]
+    e2e_s, _ = _wall(lambda: solve_multi_batch(hps, cons, cfg), reps=3)
+    pairs = sum(map(sum, got))
+    out["config2"] = {
+        "workload": "BASELINE config 2: 256 independent n=256 2-D FD GEPs, 2 circles each, N=16, L=8, M=4 "
+                    "(one solve_multi_batch call = one step)",
+        "ms_per_step": ms, "time_per_gep_ms": ms / ng, "gep_per_s": ng / (ms / 1e3),
+        "eigenpairs_per_s": pairs / (ms / 1e3), "pencils": 16 * 2 * ng,
+        "e2e": {"value": ng / e2e_s, "unit": "GEP/s", "seconds_per_step": e2e_s,
+                "h2d_bytes_per_step": int(sum(a.nbytes + b.nbytes for a, b in mats))},
+        **_lu_line(timer), "stage_ms_per_step": {k: round(v, 3) for k, v in sorted(timer.totals().items())},
+        "counts_equal_oracle": got == want, "eigenpairs": pairs}
+    del dps, res, hps, mats
+    torch.cuda.empty_cache()
+
+    # config 5: one n=8000 GEP (128 pencils of 0.95 GiB in one wave)
+    fix = np.load(os.path.join(gold, "oracle_config5.npz"))
+    cons = [Contour.from_json_dict(d) for d in json.loads(str(fix["contours"]))]
+    want = [len(fix[f"c{i}_eigs"]) for i in range(len(cons))]
+    a, b = W.config5_matrices(0)
+    cfg = SolverConfig(n_q=32, source_cols=64, n_moments=4)
+    dp = DevicePencil(a, b, hermitian=True)
+    solve_multi(dp, cons, cfg, seed=0)  # warm-up
+    ms, m, timer = _timed(lambda: solve_multi(dp, cons, cfg, seed=0))
+    got = [0 if r is None else len(r.eigenvalues) for r in m.results]
+    worst = 0.0
+    for i, r in enumerate(m.results):
+        ref = fix[f"c{i}_eigs"]
+        if r is not None and len(r.eigenvalues) == len(ref):
+            worst = max(worst, float(np.max(np.abs(r.eigenvalues - ref) / np.abs(ref))))
+    del dp
+    torch.cuda.empty_cache()
+    e2e_s, _ = _wall(lambda: solve_multi(HostPencil(a, b, True), cons, cfg, seed=0))
+    out["config5"] = {
+        "workload": "BASELINE config 5: n=8000 3-D FD GEP, 4 circles, N=32, L=64, M=4 (one solve_multi = one step)",
+        "ms_per_step": ms, "gep_per_s": 1e3 / ms, "eigenpairs_per_s": sum(got) / (ms / 1e3), "pencils": 128,
+        "e2e": {"value": 1.0 / e2e_s, "unit": "GEP/s", "seconds_per_step": e2e_s,
+                "h2d_bytes_per_step": int(a.nbytes + b.nbytes)},
+        **_lu_line(timer), "stage_ms_per_step": {k: round(v, 3) for k, v in sorted(timer.totals().items())},
+        "counts_equal_oracle": got == want, "eigenpairs": got, "max_rel_eig_diff_vs_oracle": worst,
+        "iterations": [0 if r is None else r.stats.iterations for r in m.results]}
+    torch.cuda.empty_cache()
+    return out
 
 
 def run_cirr(args):
@@ -299,14 +444,9 @@ def run_cirr(args):
     stage_flops = work.get("lu_flops", 0.0) + work.get("solve_flops_exec", 0.0) + work.get("moment_flops", 0.0)
     stage_tflops = stage_flops / (stage_ms / 1e3) / 1e12 if stage_ms else 0.0
 
-    # e2e: public API on pinned host buffers (H2D of A, B + D2H of eigenpairs inside the region)
-    class HostPencil:
-        pass
-
-    hp = HostPencil()
-    hp.a = torch.from_numpy(wl.a).pin_memory()
-    hp.b = torch.from_numpy(wl.b).pin_memory()
-    hp.hermitian = False
+    # e2e: the public solve_multi on the plain (pageable) numpy A, B a reference
+    # caller holds -- H2D of A, B and D2H of the eigenpairs inside the region
+    hp = HostPencil(wl.a, wl.b, False)
     e2e_times = []
     h2d = 2 * wl.a.nbytes
     d2h = 0
@@ -383,15 +523,18 @@ def run_cirr(args):
         except ImportError:
             pass
 
+    per_cfg = None
+    if rank == 0 and world == 1 and not args.no_per_config:
+        del dp
+        torch.cuda.empty_cache()
+        per_cfg = per_config_block()
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "c128 (f64 DMMA)", "data": "synthetic (seeded BASELINE config 4)",
-            "config": {"workload": "BASELINE config 4: n=4096 dense non-Hermitian GEP, 2 ellipses (0.3x0.15 at "
-                                   "+-0.5), N=64, L=32, M=8, tol=1e-10, max_refine=8",
-                       "pencils": wl.n_q * len(wl.contours), "n": wl.n, "parallelism": f"replicas x{world}",
-                       "l2_flush": "not needed: 34 GB of pencils per step >> 126 MB L2"},
+            "config": bench_config(wl),
             "roofline": {"bound": "tensor", "kernel": "batched zgetrf (K2: panel + DMMA trailing GEMM)",
                          "achieved": lu_tflops, "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
                          "frac": lu_tflops / FP64_DMMA_PEAK_TFLOPS,
@@ -418,6 +561,8 @@ def run_cirr(args):
         }
         if variants:
             line["variants"] = variants
+        if per_cfg:
+            line["per_config"] = per_cfg
         if cpu is not None:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)

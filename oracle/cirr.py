@@ -410,6 +410,29 @@ def solve_multi(pencil, contours, cfg: OracleConfig | None = None, seed: int = 0
     return OracleMulti(results, errors, time.perf_counter() - t0)
 
 
+def _dedupe_complex_drops(vals_list) -> dict:
+    """Complex eigenvalues (non-Hermitian pencils): a 1-D sort does not put
+    near-equal complex values next to each other (conjugate pairs found by two
+    overlapping contours share a real part to rounding), so match by distance.
+    Candidates are visited by ascending residual (ties in input order); one is
+    dropped when a value already kept from a DIFFERENT contour lies within
+    1e-8 of the span, so each duplicate cluster keeps its smallest residual,
+    as the reference's rule does for real values (solvers.py:342-377)."""
+    vals = np.array([v[0] for v in vals_list])
+    span = float(np.abs(vals[:, None] - vals[None, :]).max())
+    tol = 1e-8 * max(span, 1e-300)
+    order = sorted(range(len(vals_list)), key=lambda t: (vals_list[t][1], t))
+    kept: list = []
+    drop: dict = {}
+    for idx in order:
+        v, ri = vals_list[idx][0], vals_list[idx][2]
+        if any(vals_list[k][2] != ri and abs(v - vals_list[k][0]) <= tol for k in kept):
+            drop.setdefault(ri, set()).add(vals_list[idx][3])
+        else:
+            kept.append(idx)
+    return drop
+
+
 def _dedupe(results):  # solvers.py:342-377; span uses |.| for complex values
     allv = [(r.eigenvalues[i], r.residuals[i], ri, i)
             for ri, r in enumerate(results) if r is not None
@@ -417,19 +440,22 @@ def _dedupe(results):  # solvers.py:342-377; span uses |.| for complex values
     if len(allv) < 2:
         return
     vals = np.array([v[0] for v in allv])
-    span = abs(vals.max() - vals.min())
-    tol = 1e-8 * max(span, 1e-300)
-    order = np.argsort(vals)
-    drop: dict = {}
-    prev = order[0]
-    for idx in order[1:]:
-        if abs(allv[idx][0] - allv[prev][0]) <= tol and allv[idx][2] != allv[prev][2]:
-            loser = idx if allv[idx][1] >= allv[prev][1] else prev
-            winner = idx if loser is prev else prev
-            drop.setdefault(allv[loser][2], set()).add(allv[loser][3])
-            prev = winner
-        else:
-            prev = idx
+    if np.iscomplexobj(vals) and np.any(vals.imag != 0):
+        drop = _dedupe_complex_drops(allv)
+    else:
+        span = abs(vals.max() - vals.min())
+        tol = 1e-8 * max(span, 1e-300)
+        order = np.argsort(vals)
+        drop: dict = {}
+        prev = order[0]
+        for idx in order[1:]:
+            if abs(allv[idx][0] - allv[prev][0]) <= tol and allv[idx][2] != allv[prev][2]:
+                loser = idx if allv[idx][1] >= allv[prev][1] else prev
+                winner = idx if loser is prev else prev
+                drop.setdefault(allv[loser][2], set()).add(allv[loser][3])
+                prev = winner
+            else:
+                prev = idx
     for ri, cols in drop.items():
         r = results[ri]
         keep = np.array([i not in cols for i in range(len(r.eigenvalues))])

@@ -8,8 +8,6 @@ reference's Python API.  See DESIGN.md and include/cirr.h.
 """
 
 from .contours import Contour, QuadratureRule, contours_from_json, contours_to_json, quadrature_for  # noqa: F401
-from .datasets import Dataset, DatasetPencil, read_dataset, read_matrix_market, write_dataset  # noqa: F401
-from .datasets import write_matrix_market  # noqa: F401
 from .errors import (  # noqa: F401
     CieigError,
     ConvergenceError,
@@ -41,8 +39,7 @@ from .solvers import (  # noqa: F401
     write_eigenvectors,
 )
 
-from .kde import Interval, IntervalPartition, SpectrumPrediction, construct_contours, find_cut  # noqa: F401
-from .kde import kde_eval, kde_sparsity  # noqa: F401
+from .kde import kde_eval  # noqa: F401
 from .scouting import SCOUT_METHODS, RitzEstimate, calibrate_margin, scout, scout_contour  # noqa: F401
 
 __version__ = "0.1.0"

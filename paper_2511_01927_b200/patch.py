@@ -12,7 +12,10 @@ Patch points:
   * ``cieig.solvers.solve_multi``, ``cieig.bench.solve_multi`` (bench.py:23,
     used at 144) and ``cieig.cli.solve_multi`` (cli.py:41, used at 194) -- the
     name-imported copies, replaced so a call batches every contour through one
-    device pass.
+    device pass;
+  * ``cieig.contours.kde_eval`` (imported by name at contours.py:20, looked up
+    at call time at :191) -- the density of the reference's own KDE contour
+    construction, evaluated on the device (kde.py).
 
 Results come back as the reference's own ``EigenResult`` / ``SolveStats`` /
 ``MultiResult`` objects and errors as the reference's own exception classes,
@@ -23,6 +26,7 @@ so reference code that catches ``cieig.errors.*`` keeps working.  FEAST
 from __future__ import annotations
 
 from . import errors as E
+from . import kde as K
 from . import solvers as S
 
 _ORIG: dict = {}
@@ -110,6 +114,7 @@ def install(cieig) -> None:
     cieig.solvers.solve_multi = sm
     cieig.bench.solve_multi = sm
     cieig.cli.solve_multi = sm
+    K.install(cieig)
 
 
 def uninstall(cieig) -> None:
@@ -120,3 +125,4 @@ def uninstall(cieig) -> None:
     cieig.solvers.solve_multi = _ORIG.pop("solvers.solve_multi")
     cieig.bench.solve_multi = _ORIG.pop("bench.solve_multi")
     cieig.cli.solve_multi = _ORIG.pop("cli.solve_multi")
+    K.uninstall(cieig)

@@ -46,14 +46,10 @@ _CHOLQR = bool(int(__import__("os").environ.get("CIRR_CHOLQR", "1")))
 _CHOLQR_KAPPA = 1e5
 # previous-round eigenvalues as QR shift hints (CIRR_QR_HINTS=0 disables)
 _QR_HINTS = bool(int(__import__("os").environ.get("CIRR_QR_HINTS", "1")))
-# CIRR_PIPELINE=1 overlaps the contours of a wave (run_pipelined: one host
-# thread + high-priority stream per contour).  Off by default: ~2 % faster on
-# config 4 (1.72 s vs 1.77 s host wall, profiles/r01_pipeline_r01.txt), not
-# enough to trade the single-stream loop's simplicity for.
-_PIPELINE = bool(int(__import__("os").environ.get("CIRR_PIPELINE", "0")))
-_TIMELINE = bool(int(__import__("os").environ.get("CIRR_TIMELINE", "0")))
-_COOP_CAP = int(__import__("os").environ.get("CIRR_COOP_CAP", "64"))
-_GEMM_CAP = int(__import__("os").environ.get("CIRR_GEMM_CAP", "0"))
+# launches put the batch (pencils of a wave) on grid.y / grid.z, whose limit
+# is 65535: a wave never holds more pencils than that
+_MAX_WAVE_PENCILS = 65535
+_MOMENT_CHUNK = 16  # cirr_moments handles up to 16 moments per launch (MAXM)
 
 
 
@@ -351,17 +347,6 @@ def _ptr(t) -> int:
     return t.data_ptr()
 
 
-_PIPE_STREAMS: dict = {}
-
-
-def _pipe_stream(dev: int, name: str, priority: int):
-    """Process-wide streams of the pipelined engine, one per (device, role)."""
-    key = (dev, name)
-    if key not in _PIPE_STREAMS:
-        _PIPE_STREAMS[key] = _torch().cuda.Stream(device=dev, priority=priority)
-    return _PIPE_STREAMS[key]
-
-
 def _h2d(x: np.ndarray):
     """Host array -> device tensor, stream-ordered on the current stream with no
     host synchronisation (pinned staging from torch's caching host allocator),
@@ -501,8 +486,7 @@ class _Engine:
         self.cfg = cfg
         self.n = dp.n
         self.multi = any(getattr(c, "dp", dp) is not dp for c in cstates)
-        self.eager_dinv = False     # run_pipelined makes them per contour with its factors
-        self._dinv_made = False
+        self.dinv = None            # diagonal-block inverses: allocated and made on first use
 
     def _dp_of(self, ci: int) -> DevicePencil:
         return getattr(self.cs[ci], "dp", None) or self.dp
@@ -550,14 +534,8 @@ class _Engine:
         self.minpiv = torch.empty(P, dtype=torch.float64, device="cuda")
         self.info = torch.empty(P, dtype=torch.int32, device="cuda")
         self._dinv_per_pencil = int(_lib.call("cirr_diag_inv_bytes", n, 1))
-        self.dinv = torch.empty(self._dinv_per_pencil * P, dtype=torch.uint8, device="cuda")
         self.contour_of = _h2d(
             np.concatenate([np.full(len(c.fidx), i, dtype=np.int32) for i, c in enumerate(self.cs)]))
-
-    def _factor_contour(self, ci: int):
-        """K1 + K2 for the pencils of contour ci only (pipelined engine)."""
-        c = self.cs[ci]
-        self._factor_range(self.node_off[ci], self.node_off[ci + 1], c.nodes[c.fidx])
 
     def _check_factor(self, ci: int):
         """Singular-shift test of contour ci (linalg.py:68-70); host sync on
@@ -577,7 +555,7 @@ class _Engine:
                 break
 
     def _factor_range(self, a: int, b: int, nodes: np.ndarray):
-        """Enqueue K1 + K2 (+ the diagonal-block inverses K3 uses) for pencils
+        """Enqueue K1 + K2 for pencils
         a..b-1 (shifts `nodes`) on the current stream, as one batched call: the
         panel steps are latency-bound per launch, so one launch over every
         pencil of the wave costs the same as one over a single contour."""
@@ -595,8 +573,6 @@ class _Engine:
             _lib.call("cirr_zgetrf_batched", _ptr(self.pencils[a]), n, n, n * n, cnt, _ptr(self.ipiv[a]),
                       _ptr(self.perm[a]), _ptr(self.minpiv[a:]), _ptr(self.info[a:]), _ptr(lws), self.stream)
         _work("lu_flops", cnt * 8.0 * n ** 3 / 3.0)
-        if self.eager_dinv:
-            self._diag_inverses(a, b)
 
     def _diag_inverses(self, a: int, b: int):
         with _stage("dinv"):
@@ -719,8 +695,16 @@ class _Engine:
                               _ptr(meta[2]), n, kc, N, _ptr(Y[offs[s]]), K, n * K, self.stream)
             del Ysol
         with _stage("moments"):
-            _lib.call("cirr_moments", _ptr(Y), K, n * K, n, K, _ptr(coef), moments, _ptr(off_t), nset,
-                      _ptr(St), n, moments * K * n, self.stream)
+            if moments <= _MOMENT_CHUNK:
+                _lib.call("cirr_moments", _ptr(Y), K, n * K, n, K, _ptr(coef), moments, _ptr(off_t), nset,
+                          _ptr(St), n, moments * K * n, self.stream)
+            else:  # the reference takes any n_moments >= 1: 16 moments per launch
+                cf = np.concatenate(coefs, axis=0)
+                for m0 in range(0, moments, _MOMENT_CHUNK):
+                    mc = min(_MOMENT_CHUNK, moments - m0)
+                    cpart = _h2d(np.ascontiguousarray(cf[:, m0:m0 + mc]))
+                    _lib.call("cirr_moments", _ptr(Y), K, n * K, n, K, _ptr(cpart), mc, _ptr(off_t), nset,
+                              _ptr(St[:, m0 * K:]), n, moments * K * n, self.stream)
         _work("moment_flops", Ptot * 8.0 * n * K * moments)
         for s, ci in enumerate(active):
             self.cs[ci].stats.n_linear_solves += len(self.cs[ci].fidx) * ks[s]
@@ -735,13 +719,14 @@ class _Engine:
     def _dinv(self, K: int):
         """Inverses of the 128x128 diagonal blocks of every factor (each
         pencil's slice is contiguous), or None when an n x K solve does not read
-        them.  Made on first use after the factorisation (the pipelined
-        engine makes them with each contour's factors)."""
+        them.  Allocated and made on first use after the factorisation, so a
+        wave whose solves never read them (small K on the left-looking kernel)
+        never holds the buffer."""
         if not int(_lib.call("cirr_zgetrs_uses_dinv", self.n, K)):
             return None
-        if not self.eager_dinv and not self._dinv_made:
+        if self.dinv is None:
+            self.dinv = self.torch.empty(self._dinv_per_pencil * self.P, dtype=self.torch.uint8, device="cuda")
             self._diag_inverses(0, self.P)
-            self._dinv_made = True
         return self.dinv
 
     def _bx(self, c, xi):
@@ -857,7 +842,7 @@ class _Engine:
                 out[ci] = ("rankzero",)
         items = [(ci, S_) for ci, S_ in items if S_.shape[0] > 0]
         if not items:
-            return out
+            return None
         nb = len(items)
         cmax = max(S_.shape[0] for _, S_ in items)
         if nb > 1 and all(S_.shape[0] == cmax for _, S_ in items):
@@ -966,7 +951,10 @@ class _Engine:
                 out[ci] = ("indefinite", IndefiniteBError(msg))
                 continue
             if infos[b] < 0:
-                raise DeviceError("small eigensolver: QR iteration failed to converge")
+                # this contour's projected QR did not converge: a per-contour
+                # ConvergenceError (isolated by solve_multi), not a process error
+                out[ci] = ("qrfail", None)
+                continue
             lb = lam_h[b, : ks[b]]
             keep = contains_many(self.cs[ci].contour, lb.real + 0j if herm else lb)
             if not np.any(keep):
@@ -1060,6 +1048,11 @@ class _Engine:
                     c.fatal = True
                     active.remove(ci)
                     continue
+                if r[0] == "qrfail":
+                    c.error = ConvergenceError(c.best_res)
+                    c.fatal = True
+                    active.remove(ci)
+                    continue
                 if r[0] == "none":
                     c.lam = None
                     active.remove(ci)
@@ -1088,140 +1081,6 @@ class _Engine:
                 continue
             self.finish(c)
 
-    # -- pipelined CIRR: one host thread per contour ------------------------
-    def run_pipelined(self, moments: int):
-        """The same per-contour control flow as ``run``, with the contours of
-        the wave overlapped.  Bulk work (K1-K3: LU, solves, moments) goes in
-        order onto one low-priority stream; each contour's Rayleigh-Ritz rounds
-        (K4-K7, latency-bound) run on its own high-priority stream from its own
-        host thread, so one contour's small eigenproblems hide under another
-        contour's solve GEMMs (the persistent GEMM takes its tiles from a
-        global counter, so it gives up SMs to them).  Every contour sees the
-        same kernels and inputs as in ``run``: results are identical."""
-        import threading
-
-        torch, n = self.torch, self.n
-        dev = torch.cuda.current_device()
-        caller = torch.cuda.current_stream()
-        # persistent streams: the caching allocator keeps per-stream pools, so
-        # fresh streams would cudaMalloc (and synchronise) on every call
-        bulk = _pipe_stream(dev, "bulk", 0)
-        bulk.wait_stream(caller)
-        self._bulk = bulk
-        self._bulk_lock = threading.Lock()
-        self._lat_streams = []
-        self._tl_events = []
-        self._tl(-1, -1, "start", bulk)
-        self.eager_dinv = True
-        self._alloc_factors()
-        first = {}
-        ready = [threading.Event() for _ in self.cs]
-        errors = []
-
-        def worker(ci):
-            try:
-                torch.cuda.set_device(dev)  # the current device is per thread
-                ready[ci].wait()
-                if ci in first:  # absent only when the caller's thread failed
-                    self._contour_loop(ci, *first[ci])
-            except BaseException as exc:  # noqa: BLE001 - re-raised on the caller's thread
-                errors.append(exc)
-
-        threads = [threading.Thread(target=worker, args=(ci,), daemon=True) for ci in range(len(self.cs))]
-        old_cap = _lib.call("cirr_set_coop_ctas", _COOP_CAP)
-        old_gemm = _lib.call("cirr_set_gemm_ctas", _GEMM_CAP)
-        for t in threads:
-            t.start()
-        try:
-            with torch.cuda.stream(bulk):
-                # one batched factorisation for the whole wave (the panel steps
-                # are latency-bound per launch, so per-contour LUs cost ~14 % more)
-                self._factor_range(0, self.P, np.concatenate([c.nodes[c.fidx] for c in self.cs]))
-                for ci, c in enumerate(self.cs):
-                    rng = np.random.default_rng(c.seed)
-                    v = rng.standard_normal((n, c.ncols)).astype(complex)  # solvers.py:178-180
-                    self._tl(ci, -1, "first0", bulk)
-                    with self._bulk_lock:
-                        rhs = self.bmul(_h2d(v))
-                        st = self.apply([ci], {ci: rhs}, moments, real_rhs=True)[ci]
-                        self._tl(ci, -1, "first1", bulk)
-                        first[ci] = (st, bulk.record_event())
-                    ready[ci].set()  # this contour's Rayleigh-Ritz may start now
-            for t in threads:
-                t.join()
-        finally:
-            for r in ready:
-                r.set()
-            _lib.call("cirr_set_coop_ctas", old_cap)
-            _lib.call("cirr_set_gemm_ctas", old_gemm)
-        caller.wait_stream(bulk)
-        for lat in self._lat_streams:
-            caller.wait_stream(lat)
-        if errors:
-            raise errors[0]
-        if _TIMELINE:
-            torch.cuda.synchronize()
-            t0 = self._tl_events[0][3]
-            for ci_, it_, name, e in self._tl_events[1:]:
-                print(f"[tl] c{ci_} it{it_} {name} {t0.elapsed_time(e):9.2f} ms", flush=True)
-
-    def _tl(self, ci, it, name, stream):
-        """Debug timeline (CIRR_TIMELINE=1): timing events on the given stream."""
-        if _TIMELINE:
-            e = self.torch.cuda.Event(enable_timing=True)
-            e.record(stream)
-            self._tl_events.append((ci, it, name, e))
-
-    def _contour_loop(self, ci: int, st, ev):
-        torch, cfg = self.torch, self.cfg
-        c = self.cs[ci]
-        lat = _pipe_stream(torch.cuda.current_device(), f"lat{ci}", -1)
-        self._lat_streams.append(lat)
-        with torch.cuda.stream(lat):
-            lat.wait_event(ev)
-            st.record_stream(lat)
-            self._check_factor(ci)
-            if c.done:
-                return
-            it_used = 0
-            for it in range(cfg.max_refine):
-                it_used = it
-                self._tl(ci, it, "rr0", lat)
-                r = self.rayleigh_ritz([(ci, st)], refine=it > 0)[ci]
-                self._tl(ci, it, "rr1", lat)
-                if r[0] == "rankzero":
-                    break
-                if r[0] == "indefinite":
-                    c.error, c.fatal = r[1], True
-                    break
-                if r[0] == "none":
-                    c.lam = None
-                    break
-                _, lam, xi, res, _ = r
-                c.lam, c.x_dev, c.res = lam, xi, res
-                c.best_res = min(c.best_res, float(res.max()))
-                if _DEBUG:
-                    print(f"[cirr] contour {ci} it {it}: inside {len(lam)} max res {res.max():.2e}", flush=True)
-                if res.max() <= cfg.tol or it + 1 >= cfg.max_refine or (
-                        cfg.early_exit and c.settled(lam, res, cfg.tol)):
-                    break
-                rhs = self._bx(c, xi)
-                ev_rhs = lat.record_event()
-                with self._bulk_lock, torch.cuda.stream(self._bulk):
-                    self._bulk.wait_event(ev_rhs)
-                    rhs.record_stream(self._bulk)
-                    self._tl(ci, it, "ap0", self._bulk)
-                    st = self.apply([ci], {ci: rhs}, 1)[ci]
-                    self._tl(ci, it, "ap1", self._bulk)
-                    ev_st = self._bulk.record_event()
-                lat.wait_event(ev_st)
-                st.record_stream(lat)
-            c.stats.iterations = it_used + 1
-            c.stats.elapsed = time.perf_counter() - c.t0
-            if getattr(c, "fatal", False):
-                return
-            self.finish(c)
-
     # -- FEAST (solvers.py:230-285) on the same resident factors -------------
     def run_feast(self):
         torch, cfg, n = self.torch, self.cfg, self.n
@@ -1248,6 +1107,9 @@ class _Engine:
                     continue
                 if r[0] == "indefinite":
                     c.error, c.fatal = r[1], True
+                    continue
+                if r[0] == "qrfail":
+                    c.error, c.fatal = ConvergenceError(c.best_res), True
                     continue
                 if r[0] == "none":  # 253-255: u = xs, keep iterating
                     if r[1] is not None:
@@ -1316,16 +1178,23 @@ class _Engine:
 
 
 def _waves(cstates: list, n: int, budget_bytes: int) -> list:
-    """Group contours (whole) into waves whose factors fit the HBM budget."""
-    per = n * n * 16
-    waves, cur, cur_bytes = [], [], 0
+    """Group contours (whole) into waves whose factors fit the HBM budget and
+    whose pencil count stays within the launch grid limit (_MAX_WAVE_PENCILS).
+    Per factored node: the n x n complex128 factor, its diagonal-block
+    inverses (made when a solve reads them) and the LU workspace share."""
+    per = n * n * 16 + int(_lib.call("cirr_diag_inv_bytes", n, 1)) + int(_lib.call("cirr_zgetrf_ws_bytes", n, 1))
+    waves, cur, cur_bytes, cur_p = [], [], 0, 0
     for c in cstates:
-        need = len(c.nodes) * per
-        if cur and cur_bytes + need > budget_bytes:
+        p = len(c.fidx)
+        if p > _MAX_WAVE_PENCILS:
+            raise ParameterError(f"n_q = {p} factored nodes per contour exceeds {_MAX_WAVE_PENCILS}")
+        need = p * per
+        if cur and (cur_bytes + need > budget_bytes or cur_p + p > _MAX_WAVE_PENCILS):
             waves.append(cur)
-            cur, cur_bytes = [], 0
+            cur, cur_bytes, cur_p = [], 0, 0
         cur.append(c)
         cur_bytes += need
+        cur_p += p
     if cur:
         waves.append(cur)
     return waves
@@ -1356,8 +1225,6 @@ def _run_states(dp, cstates, cfg, moments_override=None, solver: str = "cirr"):
         if solver == "feast":
             eng.factor()
             eng.run_feast()
-        elif len(wave) > 1 and _PIPELINE and not eng.multi:
-            eng.run_pipelined(moments)
         else:
             eng.factor(sources=True)
             eng.run(moments)
@@ -1469,6 +1336,29 @@ def solve_multi_batch(pencils, contours, cfg: SolverConfig | None = None, solver
     return [_multi_result(st, t0) for st in per]
 
 
+def _dedupe_complex_drops(vals_list) -> dict:
+    """Complex eigenvalues (non-Hermitian pencils): a 1-D sort does not put
+    near-equal complex values next to each other (conjugate pairs found by two
+    overlapping contours share a real part to rounding), so match by distance.
+    Candidates are visited by ascending residual (ties in input order); one is
+    dropped when a value already kept from a DIFFERENT contour lies within
+    1e-8 of the span, so each duplicate cluster keeps its smallest residual,
+    as the reference's rule does for real values (solvers.py:342-377)."""
+    vals = np.array([v[0] for v in vals_list])
+    span = float(np.abs(vals[:, None] - vals[None, :]).max())
+    tol = 1e-8 * max(span, 1e-300)
+    order = sorted(range(len(vals_list)), key=lambda t: (vals_list[t][1], t))
+    kept: list = []
+    drop: dict = {}
+    for idx in order:
+        v, ri = vals_list[idx][0], vals_list[idx][2]
+        if any(vals_list[k][2] != ri and abs(v - vals_list[k][0]) <= tol for k in kept):
+            drop.setdefault(ri, set()).add(vals_list[idx][3])
+        else:
+            kept.append(idx)
+    return drop
+
+
 def _dedupe(results) -> None:
     """solvers.py:342-377 (span uses |.| so complex eigenvalues work)."""
     all_vals = [(r.eigenvalues[i], r.residuals[i], ri, i) for ri, r in enumerate(results) if r is not None
@@ -1476,19 +1366,22 @@ def _dedupe(results) -> None:
     if len(all_vals) < 2:
         return
     vals = np.array([v[0] for v in all_vals])
-    span = abs(vals.max() - vals.min())
-    tol = 1e-8 * max(span, 1e-300)
-    order = np.argsort(vals)
-    drop: dict = {}
-    prev = order[0]
-    for idx in order[1:]:
-        if abs(all_vals[idx][0] - all_vals[prev][0]) <= tol and all_vals[idx][2] != all_vals[prev][2]:
-            loser = idx if all_vals[idx][1] >= all_vals[prev][1] else prev
-            winner = idx if loser is prev else prev
-            drop.setdefault(all_vals[loser][2], set()).add(all_vals[loser][3])
-            prev = winner
-        else:
-            prev = idx
+    if np.iscomplexobj(vals) and np.any(vals.imag != 0):
+        drop = _dedupe_complex_drops(all_vals)
+    else:
+        span = abs(vals.max() - vals.min())
+        tol = 1e-8 * max(span, 1e-300)
+        order = np.argsort(vals)
+        drop: dict = {}
+        prev = order[0]
+        for idx in order[1:]:
+            if abs(all_vals[idx][0] - all_vals[prev][0]) <= tol and all_vals[idx][2] != all_vals[prev][2]:
+                loser = idx if all_vals[idx][1] >= all_vals[prev][1] else prev
+                winner = idx if loser is prev else prev
+                drop.setdefault(all_vals[loser][2], set()).add(all_vals[loser][3])
+                prev = winner
+            else:
+                prev = idx
     for ri, cols in drop.items():
         r = results[ri]
         keep = np.array([i not in cols for i in range(len(r.eigenvalues))])

@@ -62,3 +62,29 @@ def thermal():
         "t20": DensePencil(csr_dense(g, "t20_a").real, csr_dense(g, "t20_b").real),
         "g": g,
     }
+
+
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def reference_cieig():
+    """The unmodified reference package staged under baseline/_ref by
+    __graft_entry__.build() (copied from /root/reference/pkg/src/cieig when
+    that exists; the copy travels to the GPU box). Skips when absent."""
+    if not os.path.isfile(os.path.join(REF_DIR, "cieig", "solvers.py")):
+        try:
+            import __graft_entry__
+            __graft_entry__.stage_reference()
+        except Exception:  # pragma: no cover
+            pass
+    if not os.path.isfile(os.path.join(REF_DIR, "cieig", "solvers.py")):
+        pytest.skip("reference package not staged under baseline/_ref (run __graft_entry__.build())")
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    import cieig
+    import cieig.bench  # noqa: F401
+    import cieig.cli  # noqa: F401
+    import cieig.contours  # noqa: F401
+    import cieig.problems  # noqa: F401
+    import cieig.solvers  # noqa: F401
+    return cieig

@@ -178,14 +178,10 @@ def config3():
 
 
 def dataset():
-    """A dataset directory written by the reference (problems.write_dataset),
-    its dense matrices and truth, and the reference's FormatError text for a
-    set of malformed inputs (tests/test_datasets.py)."""
+    """A dataset directory written by the reference (problems.write_dataset) and
+    its dense matrices and truth (tests/test_gpu_dropin.py reads it back with
+    the reference's own read_dataset and solves it on the GPU)."""
     import shutil
-    import tempfile
-
-    from cieig.errors import FormatError
-    from cieig.sparse import read_matrix_market
 
     field = rp.grf_sample(rp.Grid2D(8, 8), 1.0, 0.3, 0.25, 11)
     pencil = rp.assemble_thermal(field, 1.0)
@@ -195,45 +191,6 @@ def dataset():
     rp.write_dataset(d, pencil, field, truth)
     out = {"a": pencil.a.to_dense(), "b": pencil.b.to_dense(), "truth": truth.eigenvalues,
            "field": field.values, "problem_id": np.array(pencil.problem_id)}
-    bad = {
-        "empty": "",
-        "header": "%%MatrixMarket matrix array real general\n2 2\n",
-        "field": "%%MatrixMarket matrix coordinate pattern general\n2 2 1\n1 1\n",
-        "symmetry": "%%MatrixMarket matrix coordinate real banded\n2 2 1\n1 1 1.0\n",
-        "nosize": "%%MatrixMarket matrix coordinate real general\n% only comments\n",
-        "size": "%%MatrixMarket matrix coordinate real general\n2 two 1\n1 1 1.0\n",
-        "entry": "%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 1.0\n2 x 3.0\n",
-        "range": "%%MatrixMarket matrix coordinate real general\n2 2 1\n3 1 1.0\n",
-        "more": "%%MatrixMarket matrix coordinate real general\n2 2 1\n1 1 1.0\n2 2 2.0\n",
-        "fewer": "%%MatrixMarket matrix coordinate complex general\n2 2 2\n1 1 1.0 0.5\n",
-        "complexbad": "%%MatrixMarket matrix coordinate complex general\n2 2 1\n1 1 1.0\n",
-    }
-    tmp = tempfile.mkdtemp()
-    for name, text in bad.items():
-        fp = os.path.join(tmp, name + ".mtx")
-        with open(fp, "w") as fh:
-            fh.write(text)
-        try:
-            read_matrix_market(fp)
-            msg = "ok"
-        except FormatError as exc:
-            msg = str(exc)
-        out["bad_" + name + "_text"] = np.array(text)
-        out["bad_" + name + "_msg"] = np.array(msg)
-    # symmetric / hermitian / skew files are expanded
-    sym = {
-        "sym": "%%MatrixMarket matrix coordinate real symmetric\n3 3 3\n1 1 2.0\n2 1 -1.5\n3 2 0.25\n",
-        "herm": "%%MatrixMarket matrix coordinate complex hermitian\n2 2 2\n1 1 1.0 0.0\n2 1 0.5 0.75\n",
-        "skew": "%%MatrixMarket matrix coordinate real skew-symmetric\n2 2 1\n2 1 3.0\n",
-        "int": "%%MatrixMarket matrix coordinate integer general\n2 2 2\n1 2 7\n2 2 -4\n",
-    }
-    for name, text in sym.items():
-        fp = os.path.join(tmp, name + ".mtx")
-        with open(fp, "w") as fh:
-            fh.write(text)
-        out["sym_" + name + "_text"] = np.array(text)
-        out["sym_" + name + "_dense"] = read_matrix_market(fp).to_dense()
-    shutil.rmtree(tmp)
     np.savez_compressed(os.path.join(HERE, "ref_dataset.npz"), **out)
 
 

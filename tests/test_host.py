@@ -65,7 +65,9 @@ def test_moment_coefficients_match_oracle():
 def test_waves_group_whole_contours():
     cs = [S._Contour(i, Contour(shape="circle", center=0j, radius=1.0), S.SolverConfig(n_q=32), 0, 100)
           for i in range(5)]
-    waves = S._waves(cs, 100, budget_bytes=100 * 100 * 16 * 64)
+    from paper_2511_01927_b200 import _lib
+    per = 100 * 100 * 16 + _lib.call("cirr_diag_inv_bytes", 100, 1) + _lib.call("cirr_zgetrf_ws_bytes", 100, 1)
+    waves = S._waves(cs, 100, budget_bytes=per * 64)
     assert [len(w) for w in waves] == [2, 2, 1]
 
 
@@ -174,3 +176,45 @@ def test_single_moment_coefficients_bitwise():
         assert np.array_equal(fast.view(np.float64), loop.view(np.float64))
         assert np.array_equal(np.ascontiguousarray(fast[:, 0]).view(np.float64),
                               np.ascontiguousarray(st._coef(4)[:, 0]).view(np.float64))
+
+
+def test_dedupe_complex_conjugate_pairs_from_overlapping_contours():
+    """a lexicographic sort does not bring near-equal complex values
+    together; two overlapping contours each finding a conjugate pair must end
+    with one copy of each value, the smaller-residual one."""
+    a, b = 0.5 + 0.1j, 0.5 - 0.1j
+    eps = 1e-13
+    rs = [_res([a, b + eps * 1j, 0.9 + 0j], [1e-12, 3e-12, 1e-12]),
+          _res([b, a + eps, 0.1 + 0j], [1e-12, 5e-12, 1e-12])]
+    S._dedupe(rs)
+    union = np.concatenate([r.eigenvalues for r in rs])
+    assert len(union) == 4
+    for v in (a, b, 0.9, 0.1):
+        assert np.sum(np.abs(union - v) <= 1e-10) == 1
+    assert a in rs[0].eigenvalues and b in rs[1].eigenvalues     # the smaller residuals survive
+
+
+def test_dedupe_complex_same_contour_never_dropped():
+    rs = [_res([0.5 + 0.1j, 0.5 + 0.1j + 1e-14], [1e-12, 1e-12])]
+    rs.append(_res([2.0 + 0j], [1e-12]))
+    S._dedupe(rs)
+    assert len(rs[0].eigenvalues) == 2
+
+
+class _FakeContour:
+    def __init__(self, p):
+        self.fidx = np.arange(p)
+        self.nodes = np.zeros(p)
+
+
+def test_waves_cap_pencils_per_wave():
+    """batch indices ride on grid.y/z (<= 65535); a wave never holds
+    more pencils, whatever the byte budget."""
+    cs = [_FakeContour(16) for _ in range(4200)]          # 67200 pencils
+    waves = S._waves(cs, 16, 1 << 60)
+    assert len(waves) == 2
+    assert all(sum(len(c.fidx) for c in w) <= S._MAX_WAVE_PENCILS for w in waves)
+    assert sum(len(w) for w in waves) == 4200
+    # the byte budget counts the factor, its diagonal inverses and LU workspace
+    per = 64 * 64 * 16
+    assert len(S._waves([_FakeContour(32), _FakeContour(32)], 64, 64 * per + 1)) == 2
