@@ -18,6 +18,8 @@ from .cirr import (  # noqa: F401
     apply_projector,
     cirr_solve,
     contains,
+    feast_solve,
+    orthonormalize,
     quadrature,
     rank_truncate_svd,
     residuals,

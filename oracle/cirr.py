@@ -74,6 +74,7 @@ class OracleConfig:
     max_refine: int = 8
     tol: float = 1e-10
     rank_rel_tol: float = 1e-12
+    drop_tol: float = 1e-10
     moments: str = "centred"  # "centred" | "raw"
     lu: str = "dense"  # "dense" | "superlu"
     rr: str = "auto"  # "auto" | "hermitian" | "general"
@@ -278,6 +279,32 @@ def rank_truncate_svd(block, rel_tol=1e-12):  # linalg.py:107-119
     return u[:, :r]
 
 
+def orthonormalize(block, drop_tol=1e-10):  # linalg.py:79-104
+    """Gram-Schmidt with one re-orthogonalisation pass per column; a column
+    whose remaining norm is <= drop_tol x its original norm is dropped."""
+    b = np.array(block, dtype=np.complex128)
+    if b.ndim == 1:
+        b = b[:, None]
+    if b.shape[1] == 0:
+        raise RankZeroError("empty block")
+    kept = []
+    for j in range(b.shape[1]):
+        v = b[:, j]
+        orig = np.linalg.norm(v)
+        if orig == 0.0:
+            continue
+        for _ in range(2):
+            for q in kept:
+                v = v - q * (q.conj() @ v)
+        nrm = np.linalg.norm(v)
+        if nrm <= drop_tol * orig:
+            continue
+        kept.append(v / nrm)
+    if not kept:
+        raise RankZeroError("all columns dropped")
+    return np.column_stack(kept)
+
+
 def rayleigh_ritz(pencil: Pencil, q, mode: str):
     """solvers.py:150-158 + linalg.py:122-145; 'general' is delta 3."""
     aq = pencil.a @ q
@@ -381,6 +408,55 @@ def cirr_solve(pencil, contour, cfg: OracleConfig | None = None, seed: int = 0):
                         ctx.n_linear_solves, ctx.n_factorizations, elapsed, ranks)
 
 
+def feast_solve(pencil, contour, cfg: OracleConfig | None = None, seed: int = 0):
+    """solvers.py:230-285: filtered subspace iteration U <- orth(P U) with a
+    Rayleigh-Ritz extraction after each projector application (one moment,
+    so the moment centring delta does not apply); the general Rayleigh-Ritz
+    (delta 3) when the pencil is not Hermitian."""
+    cfg = cfg or OracleConfig()
+    t0 = time.perf_counter()
+    p = Pencil.of(pencil)
+    nodes, weights = quadrature(contour, cfg.n_q)  # 236
+    ctx = Projector(p, nodes, weights, cfg, moment_frame(contour))  # 237
+    rng = np.random.default_rng(seed)  # 238
+    ncols = cfg.cols_for(getattr(contour, "expected_count", 0))  # 239
+    u = rng.standard_normal((p.n, ncols)).astype(complex)  # 240
+    mode = cfg.rr if cfg.rr != "auto" else ("hermitian" if p.hermitian else "general")
+    best_res = np.inf
+    lam = x = res = None
+    found_any = False
+    ranks = []
+    for it in range(cfg.max_refine):  # 245
+        y = ctx.apply(u, moments=1)[0]  # 246
+        try:
+            q = orthonormalize(y, cfg.drop_tol)  # 248
+        except RankZeroError:  # 249-250
+            break
+        ranks.append(q.shape[1])
+        w, xs = rayleigh_ritz(p, q, mode)  # 251
+        keep = _inside(contour, w, mode == "hermitian")  # 252
+        u = xs  # 253: the full filtered Ritz block is the next iterate
+        if not np.any(keep):  # 254-255
+            continue
+        found_any = True
+        lam, x = w[keep], xs[:, keep]
+        res = residuals(p, lam, x)  # 258
+        best_res = min(best_res, float(res.max()))
+        if res.max() <= cfg.tol:  # 260-261
+            break
+    elapsed = time.perf_counter() - t0
+    if not found_any or lam is None:  # 269-272
+        raise NoEigenvaluesFound("no eigenvalues inside contour")
+    if res.max() > cfg.tol:  # 273-277
+        conv = res <= cfg.tol
+        if not np.any(conv):
+            raise ConvergenceError(best_res)
+        lam, x, res = lam[conv], x[:, conv], res[conv]
+    order = np.argsort(lam)  # 278
+    return OracleResult(lam[order], x[:, order], res[order], contour, it + 1,
+                        ctx.n_linear_solves, ctx.n_factorizations, elapsed, ranks)
+
+
 @dataclass
 class OracleMulti:
     results: list
@@ -393,15 +469,16 @@ class OracleMulti:
         return np.sort(np.concatenate(vals)) if vals else np.array([])
 
 
-def solve_multi(pencil, contours, cfg: OracleConfig | None = None, seed: int = 0):
+def solve_multi(pencil, contours, cfg: OracleConfig | None = None, seed: int = 0, solver: str = "cirr"):
     """solvers.py:312-339 (per-contour seed+i, isolated failures, dedupe)."""
     cfg = cfg or OracleConfig()
+    fn = {"cirr": cirr_solve, "feast": feast_solve}[solver]  # 316-318
     t0 = time.perf_counter()
     p = Pencil.of(pencil)
     results, errors = [], []
     for i, c in enumerate(contours):
         try:
-            results.append(cirr_solve(p, c, cfg, seed=seed + i))
+            results.append(fn(p, c, cfg, seed=seed + i))
             errors.append(None)
         except (NoEigenvaluesFound, ConvergenceError, SingularShiftError, RankZeroError) as exc:
             results.append(None)

@@ -177,6 +177,38 @@ def config3():
     np.savez_compressed(os.path.join(HERE, "ref_config3.npz"), **out)
 
 
+def feast():
+    """The reference's own feast_solve / solve_multi(solver="feast")
+    (solvers.py:230-285, 312-339) on thermal20 (one low-end circle at tol 1e-8
+    and the KDE contours at tol 1e-10) and on config 3 (N=32, L=40, M=1):
+    eigenvalues, residuals, iterations and n_linear_solves per contour. Pins
+    the oracle's feast_solve (tests/test_oracle_pin.py) and the GPU FEAST
+    (tests/test_gpu_feast.py)."""
+    out = {}
+    t20 = rp.assemble_thermal(rp.grf_sample(rp.Grid2D(20, 20), 1.0, 0.1, 0.2, seed=11), 1.0)
+    full = rp.dense_ground_truth(t20, 5).eigenvalues
+    mid = 0.5 * (full[0] + full[3])
+    rad = 0.5 * (full[3] + full[4]) - mid
+    out["t20_low_circle"] = np.array([mid, rad])
+    r = rs.feast_solve(t20, circle(mid, rad, 4), rs.SolverConfig(tol=1e-8), seed=0)
+    result_arrays("t20_low", r, out)
+    tt = rp.dense_ground_truth(t20, rp.target_count(t20.n))
+    _, contours = rc.construct_contours(rc.SpectrumPrediction(values=tt.eigenvalues), n_min=1, n_max=50)
+    out["t20_kde_contours"] = np.array(json.dumps([c.to_json_dict() for c in contours]))
+    m = rs.solve_multi(t20, contours, rs.SolverConfig(tol=1e-10), solver="feast", seed=0)
+    for i, rr in enumerate(m.results):
+        result_arrays(f"t20_kde{i}", rr, out)
+    wl = W.config3()
+    cfg = rs.SolverConfig(n_q=wl.n_q, source_cols=40, n_moments=1)
+    out["c3_contours"] = np.array(json.dumps([c.to_json_dict() for c in wl.contours]))
+    m = rs.solve_multi(_ref_pencil(wl.a, wl.b), _ref_contours(wl), cfg, solver="feast", seed=0)
+    for i, rr in enumerate(m.results):
+        result_arrays(f"c3_{i}", rr, out)
+    for k in [k for k in out if k.endswith("_vecs")]:
+        del out[k]                     # keep the fixture small: eigenvectors are checked by residuals
+    np.savez_compressed(os.path.join(HERE, "ref_feast.npz"), **out)
+
+
 def dataset():
     """A dataset directory written by the reference (problems.write_dataset) and
     its dense matrices and truth (tests/test_gpu_dropin.py reads it back with

@@ -60,3 +60,41 @@ def test_feast_config3_matches_oracle_counts():
         assert len(r.eigenvalues) == len(ref)
         assert np.abs(r.eigenvalues - ref).max() <= 1e-8 * np.abs(ref).max()
         assert r.residuals.max() <= 1e-10
+
+
+def _stats(r):
+    return [r.stats.n_linear_solves, r.stats.n_factorizations, r.stats.iterations]
+
+
+def test_feast_matches_reference_thermal(thermal):
+    """GPU FEAST against the reference's own feast_solve / solve_multi(feast)
+    outputs (ref_feast.npz, which also pins oracle.feast_solve): eigenvalues to
+    1e-8, the same iteration and solve counts."""
+    g = golden("ref_feast.npz")
+    mid, rad = g["t20_low_circle"]
+    r = feast_solve(thermal["t20"], circle(mid, rad, 4), SolverConfig(tol=1e-8), seed=0)
+    assert np.allclose(r.eigenvalues, g["t20_low_eigs"], rtol=1e-8)
+    assert _stats(r) == list(g["t20_low_stats"])
+    assert r.residuals.max() <= 1e-8
+    cs = [Contour.from_json_dict(d) for d in json.loads(str(g["t20_kde_contours"]))]
+    m = solve_multi(thermal["t20"], cs, SolverConfig(tol=1e-10), solver="feast", seed=0)
+    for i, rr in enumerate(m.results):
+        assert np.allclose(rr.eigenvalues, g[f"t20_kde{i}_eigs"], rtol=1e-8)
+        assert _stats(rr) == list(g[f"t20_kde{i}_stats"])
+
+
+def test_feast_matches_reference_config3():
+    """Config 3 (n=2304, 3 contours, N=32, L=40): exact counts, eigenvalues to
+    1e-8 and the reference's iteration counts per contour (4, 8, 4)."""
+    g = golden("ref_feast.npz")
+    a, b = W.config3_matrices()
+    cs = [Contour.from_json_dict(d) for d in json.loads(str(g["c3_contours"]))]
+    m = solve_multi(type("P", (), {"a": a, "b": b, "hermitian": True})(), cs,
+                    SolverConfig(n_q=32, source_cols=40, n_moments=1), solver="feast", seed=0)
+    for i, rr in enumerate(m.results):
+        assert rr is not None, m.errors[i]
+        ref = g[f"c3_{i}_eigs"]
+        assert len(rr.eigenvalues) == len(ref)
+        assert np.allclose(rr.eigenvalues, ref, rtol=1e-8)
+        assert _stats(rr) == list(g[f"c3_{i}_stats"])
+        assert rr.residuals.max() <= 1e-10

@@ -139,3 +139,34 @@ def test_config1_reference_fails_oracle_succeeds():
     o = golden("oracle_config1.npz")
     assert len(o["c0_eigs"]) == len(o["c0_truth"]) == 33
     assert float(o["c0_res"].max()) <= 1e-10
+
+
+def test_feast_oracle_matches_reference(thermal):
+    """oracle.feast_solve (reference mode: SuperLU, Hermitian RR; one moment so
+    the centring delta is moot) against the unmodified reference's feast_solve
+    (tests/golden/ref_feast.npz, make_golden.py feast): eigenvalues to 1e-10,
+    identical iteration and solve counts."""
+    g = golden("ref_feast.npz")
+    p = P(thermal["t20"])
+    mid, rad = g["t20_low_circle"]
+    r = oracle.feast_solve(p, circle(mid, rad, 4), OracleConfig(tol=1e-8, lu="superlu", rr="hermitian"), seed=0)
+    assert np.allclose(r.eigenvalues, g["t20_low_eigs"], rtol=1e-10)
+    assert [r.n_linear_solves, r.n_factorizations, r.iterations] == list(g["t20_low_stats"])
+    cs = [Contour.from_json_dict(d) for d in json.loads(str(g["t20_kde_contours"]))]
+    m = oracle.solve_multi(p, cs, OracleConfig(tol=1e-10, lu="superlu", rr="hermitian"), seed=0, solver="feast")
+    for i, rr in enumerate(m.results):
+        assert np.allclose(rr.eigenvalues, g[f"t20_kde{i}_eigs"], rtol=1e-10)
+        assert [rr.n_linear_solves, rr.n_factorizations, rr.iterations] == list(g[f"t20_kde{i}_stats"])
+
+
+@pytest.mark.slow
+def test_feast_oracle_matches_reference_config3():
+    from paper_2511_01927_b200 import workloads as W
+    g = golden("ref_feast.npz")
+    a, b = W.config3_matrices()
+    cs = [Contour.from_json_dict(d) for d in json.loads(str(g["c3_contours"]))]
+    cfg = OracleConfig(n_q=32, source_cols=40, n_moments=1, lu="superlu", rr="hermitian")
+    m = oracle.solve_multi(Pencil(a, b, True), cs, cfg, seed=0, solver="feast")
+    for i, rr in enumerate(m.results):
+        assert np.allclose(rr.eigenvalues, g[f"c3_{i}_eigs"], rtol=1e-10)
+        assert [rr.n_linear_solves, rr.n_factorizations, rr.iterations] == list(g[f"c3_{i}_stats"])
