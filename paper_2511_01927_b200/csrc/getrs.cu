@@ -609,9 +609,11 @@ static int getrs_impl(const cplx* LU, int n, long long ld, long long pencil_stri
   // GEMM tile of the right-looking path would be mostly padding there (at K = 32
   // the TMA path is still faster: 18.7 ms vs 24.3 ms for 64 pencils, n = 4096)
   cirr::OperandMaps mT, mY;
+  static const int bn_env = getenv("CIRR_SOLVE_BN") ? atoi(getenv("CIRR_SOLVE_BN")) : 0;
+  const int BN = bn_env > 0 ? bn_env : cirr::pick_tile_n(K);
   bool tma = solve_tma_path(n, K) && cirr::encode_a_map(&mT.a, LU, n, n, nfac, ld, pencil_stride) == 0 &&
-             cirr::encode_c128_map(&mY.b, Y, K, n, batch, ldy, ystride, cirr::PBN, cirr::PBK) == 0 &&
-             cirr::encode_c128_map(&mY.c, Y, K, n, batch, ldy, ystride, cirr::PBN, cirr::PBM) == 0;
+             cirr::encode_c128_map(&mY.b, Y, K, n, batch, ldy, ystride, BN, cirr::PBK) == 0 &&
+             cirr::encode_c128_map(&mY.c, Y, K, n, batch, ldy, ystride, BN, cirr::PBM) == 0;
   if (tma) {
     static bool dattr = false;
     if (!dattr) {
@@ -639,16 +641,16 @@ static int getrs_impl(const cplx* LU, int n, long long ld, long long pencil_stri
         if (lower) {
           if (nb2 > 0)  // rows i0+64.. : [L21inv L22inv] [Y_a; Y_b]
             CIRR_TRY(cirr::zgemm_sub_maps(mD, mY.b, mY.c, nb2, K, nb, batch, SNB, 0, i0, 0, i0 + SNB, 0, Y, ldy,
-                                          ystride, stream, /*beta=*/0, nblk2 * 2, slot, pmap));
+                                          ystride, stream, /*beta=*/0, nblk2 * 2, slot, pmap, BN));
           CIRR_TRY(cirr::zgemm_sub_maps(mD, mY.b, mY.c, na, K, na, batch, 0, 0, i0, 0, i0, 0, Y, ldy, ystride, stream,
-                                        /*beta=*/0, nblk2 * 2, slot, pmap));
+                                        /*beta=*/0, nblk2 * 2, slot, pmap, BN));
         } else {
           // rows i0.. : [U11inv U12inv] [Y_a; Y_b] first (reads the old Y_b), then Y_b
           CIRR_TRY(cirr::zgemm_sub_maps(mD, mY.b, mY.c, na, K, nb, batch, 0, 0, i0, 0, i0, 0, Y, ldy, ystride, stream,
-                                        /*beta=*/0, nblk2 * 2, slot, pmap));
+                                        /*beta=*/0, nblk2 * 2, slot, pmap, BN));
           if (nb2 > 0)
             CIRR_TRY(cirr::zgemm_sub_maps(mD, mY.b, mY.c, nb2, K, nb2, batch, SNB, SNB, i0 + SNB, 0, i0 + SNB, 0, Y,
-                                          ldy, ystride, stream, /*beta=*/0, nblk2 * 2, slot, pmap));
+                                          ldy, ystride, stream, /*beta=*/0, nblk2 * 2, slot, pmap, BN));
         }
         return 0;
       };
@@ -659,12 +661,12 @@ static int getrs_impl(const cplx* LU, int n, long long ld, long long pencil_stri
           const int i0 = bi * DB, nb = min(DB, n - i0);
           if (bi > sb0)  // Y[i0:i0+nb] -= L[i0:i0+nb, s0:i0] Y[s0:i0]
             CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, nb, K, i0 - s0, batch, i0, s0, s0, 0, i0, 0, Y, ldy,
-                                          ystride, stream, 1, 1, 0, pmap));
+                                          ystride, stream, 1, 1, 0, pmap, BN));
           CIRR_TRY(apply_dinv(bi, true));
         }
         if (n - s1 > 0)  // Y[s1:] -= L[s1:, s0:s1] Y[s0:s1]
           CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, n - s1, K, s1 - s0, batch, s1, s0, s0, 0, s1, 0, Y, ldy,
-                                        ystride, stream, 1, 1, 0, pmap));
+                                        ystride, stream, 1, 1, 0, pmap, BN));
       }
       const int nsb = (nblk2 + SBK - 1) / SBK;
       for (int sb = nsb - 1; sb >= 0; --sb) {  // backward: U
@@ -674,12 +676,12 @@ static int getrs_impl(const cplx* LU, int n, long long ld, long long pencil_stri
           const int i0 = bi * DB, nb = min(DB, n - i0);
           if (bi < sb1 - 1)  // Y[i0:i0+nb] -= U[i0:i0+nb, i0+nb:s1] Y[i0+nb:s1]
             CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, nb, K, s1 - i0 - nb, batch, i0, i0 + nb, i0 + nb, 0, i0,
-                                          0, Y, ldy, ystride, stream, 1, 1, 0, pmap));
+                                          0, Y, ldy, ystride, stream, 1, 1, 0, pmap, BN));
           CIRR_TRY(apply_dinv(bi, false));
         }
         if (s0 > 0)  // Y[:s0] -= U[:s0, s0:s1] Y[s0:s1]
           CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, s0, K, s1 - s0, batch, 0, s0, s0, 0, 0, 0, Y, ldy, ystride,
-                                        stream, 1, 1, 0, pmap));
+                                        stream, 1, 1, 0, pmap, BN));
       }
       return 0;
     }
@@ -690,14 +692,14 @@ static int getrs_impl(const cplx* LU, int n, long long ld, long long pencil_stri
       diag_solve_kernel<true><<<gd, 256, kDiagSmem, stream>>>(LU, ld, pencil_stride, i0, nb, Y, ldy, ystride, K, pmap);
       CIRR_CHECK_LAUNCH();
       CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, n - i0 - nb, K, nb, batch, i0 + nb, i0, i0, 0, i0 + nb, 0,
-                                    Y, ldy, ystride, stream, 1, 1, 0, pmap));
+                                    Y, ldy, ystride, stream, 1, 1, 0, pmap, BN));
     }
     for (int bi = nblk - 1; bi >= 0; --bi) {  // backward: U
       const int i0 = bi * SNB, nb = min(SNB, n - i0);
       diag_solve_kernel<false><<<gd, 256, kDiagSmem, stream>>>(LU, ld, pencil_stride, i0, nb, Y, ldy, ystride, K, pmap);
       CIRR_CHECK_LAUNCH();
       CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, i0, K, nb, batch, 0, i0, i0, 0, 0, 0, Y, ldy, ystride,
-                                    stream, 1, 1, 0, pmap));
+                                    stream, 1, 1, 0, pmap, BN));
     }
     return 0;
   }

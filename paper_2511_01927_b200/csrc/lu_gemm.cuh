@@ -29,13 +29,32 @@ constexpr int PBM = 64, PBN = 64, PBK = 16, PSTAGES = 4;
 constexpr int PCONS = 8;         // consumer warps
 constexpr int PTHREADS = (PCONS + 1) * 32;
 constexpr int P_A_BYTES = PBM * PBK * 16;
-constexpr int P_B_BYTES = PBK * PBN * 16;
-constexpr int P_STAGE_BYTES = P_A_BYTES + P_B_BYTES;
-constexpr int P_C_BYTES = PBM * PBN * 16;
 constexpr int PRING = 8;                        // tile-id ring (producer runs <= PSTAGES tiles ahead)
-constexpr int P_SMEM = PSTAGES * P_STAGE_BYTES + P_C_BYTES + 8 * (2 * PSTAGES + 2) + 4 * PRING + 1024;
 constexpr int PAK = 8;                          // complex columns per swizzled A box (128 bytes)
 constexpr int P_A_HALF = PBM * PAK * 16;        // one A box
+
+// Output tiles are 64 x BN.  The LU uses BN = 64; the blocked solves pick BN
+// from {64, 56, 48, 40, 32} to fit the right-hand-side width K (pick_tile_n:
+// the first pass's K = 32 runs as one 32-wide tile instead of a half-empty
+// 64-wide one).  Each consumer warp owns WI
+// 8-row blocks x WJ 8-column blocks of the tile (8 warps cover 8 x BN/8 blocks).
+template <int BN>
+struct TileCfg;
+template <> struct TileCfg<64> { static constexpr int WI = 4, WJ = 2; };
+template <> struct TileCfg<56> { static constexpr int WI = 1, WJ = 7; };
+template <> struct TileCfg<48> { static constexpr int WI = 2, WJ = 3; };
+template <> struct TileCfg<40> { static constexpr int WI = 1, WJ = 5; };
+template <> struct TileCfg<32> { static constexpr int WI = 2, WJ = 2; };
+template <int BN>
+struct TileBytes {
+  static constexpr int B = PBK * BN * 16;
+  static constexpr int STAGE = P_A_BYTES + B;
+  static constexpr int C = PBM * BN * 16;
+  static constexpr int SMEM = PSTAGES * STAGE + C + 8 * (2 * PSTAGES + 2) + 4 * PRING + 1024;
+};
+constexpr int P_STAGE_BYTES = TileBytes<64>::STAGE;
+constexpr int P_C_BYTES = TileBytes<64>::C;
+constexpr int P_SMEM = TileBytes<64>::SMEM;
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
@@ -80,20 +99,25 @@ struct SubGemmGeom {
   const int* a_bmap;   // optional: the A operand of batch entry b is A entry a_bmap[b] (gathered solves)
 };
 
+template <int BN>
 static __global__ void __launch_bounds__(PTHREADS, 1) zgemm_sub_tma(const __grid_constant__ CUtensorMap mapA,
                                                              const __grid_constant__ CUtensorMap mapB,
                                                              const __grid_constant__ CUtensorMap mapC,
                                                              SubGemmGeom g) {
+  constexpr int WI = TileCfg<BN>::WI, WJ = TileCfg<BN>::WJ;
+  constexpr int WARPS_N = (BN / 8) / WJ;
+  static_assert((8 / WI) * WARPS_N == PCONS, "warp layout must cover the tile");
+  constexpr int STAGE = TileBytes<BN>::STAGE, CBYTES = TileBytes<BN>::C;
   extern __shared__ __align__(1024) unsigned char psm_raw[];
   // 1024-byte alignment for the swizzled A boxes, kept in the shared window
   unsigned char* psm = psm_raw + ((1024u - (smem_u32(psm_raw) & 1023u)) & 1023u);
   const unsigned psm_s = smem_u32(psm);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(psm + PSTAGES * P_STAGE_BYTES + P_C_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(psm + PSTAGES * STAGE + CBYTES);
   uint64_t* full = bars;
   uint64_t* empty = bars + PSTAGES;
   uint64_t* cfull = bars + 2 * PSTAGES;
   uint64_t* cempty = bars + 2 * PSTAGES + 1;
-  const unsigned Cs = psm_s + PSTAGES * P_STAGE_BYTES;
+  const unsigned Cs = psm_s + PSTAGES * STAGE;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
     for (int s = 0; s < PSTAGES; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, PCONS); }
@@ -127,12 +151,12 @@ static __global__ void __launch_bounds__(PTHREADS, 1) zgemm_sub_tma(const __grid
         }
         const int b = (int)(t / tiles_per_b);
         const int rem = (int)(t % tiles_per_b);
-        const int m0 = (rem / g.tiles_n) * PBM, n0 = (rem % g.tiles_n) * PBN;
+        const int m0 = (rem / g.tiles_n) * PBM, n0 = (rem % g.tiles_n) * BN;
         const int ab = (g.a_bmap ? __ldg(g.a_bmap + b) : b) * g.a_bmul + g.a_badd;
         for (int ks = 0; ks < ksteps; ++ks) {
           if (ks > 0) mbar_wait(empty + stage, phase ^ 1);
-          unsigned char* base = psm + stage * P_STAGE_BYTES;
-          mbar_arrive_expect_tx(full + stage, P_STAGE_BYTES);
+          unsigned char* base = psm + stage * STAGE;
+          mbar_arrive_expect_tx(full + stage, STAGE);
           const int k0 = ks * PBK;
           tma_load3(base, &mapA, 2 * (g.a_col0 + k0), g.a_row0 + m0, ab, full + stage);
           tma_load3(base + P_A_HALF, &mapA, 2 * (g.a_col0 + k0 + PAK), g.a_row0 + m0, ab, full + stage);
@@ -143,8 +167,8 @@ static __global__ void __launch_bounds__(PTHREADS, 1) zgemm_sub_tma(const __grid
         // previous tile's C, i.e. while this tile's main loop runs
         if (g.beta) {
           mbar_wait(cempty, cphase ^ 1);
-          mbar_arrive_expect_tx(cfull, P_C_BYTES);
-          tma_load3(psm + PSTAGES * P_STAGE_BYTES, &mapC, 2 * (g.c_col0 + n0), g.c_row0 + m0, b, cfull);
+          mbar_arrive_expect_tx(cfull, CBYTES);
+          tma_load3(psm + PSTAGES * STAGE, &mapC, 2 * (g.c_col0 + n0), g.c_row0 + m0, b, cfull);
           cphase ^= 1;
         }
       }
@@ -158,7 +182,7 @@ static __global__ void __launch_bounds__(PTHREADS, 1) zgemm_sub_tma(const __grid
     }
   } else {
     // ---------------- consumer warps ----------------
-    const int wm = (warp >> 2) * 32, wn = (warp & 3) * 16;
+    const int wm = (warp / WARPS_N) * (WI * 8), wn = (warp % WARPS_N) * (WJ * 8);
     int stage = 0;
     unsigned phase = 0, cphase = 0;
     for (int seq = 0;; ++seq) {
@@ -168,43 +192,43 @@ static __global__ void __launch_bounds__(PTHREADS, 1) zgemm_sub_tma(const __grid
       if (t < 0) break;
       const int b = (int)(t / tiles_per_b);
       const int rem = (int)(t % tiles_per_b);
-      const int m0 = (rem / g.tiles_n) * PBM, n0 = (rem % g.tiles_n) * PBN;
+      const int m0 = (rem / g.tiles_n) * PBM, n0 = (rem % g.tiles_n) * BN;
       // two accumulator sets per 8x8 block: re += ar br - ai bi, im += ar bi + ai br
       // (16 independent chains per warp keep the DMMA pipe fed; 64 accumulator
       // registers leave room under the 168-register cap of a 9-warp CTA)
-      double are[4][2][2], aim[4][2][2];
+      double are[WI][WJ][2], aim[WI][WJ][2];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < WI; ++i)
 #pragma unroll
-        for (int j = 0; j < 2; ++j)
+        for (int j = 0; j < WJ; ++j)
 #pragma unroll
           for (int h = 0; h < 2; ++h) are[i][j][h] = aim[i][j][h] = 0.0;
       for (int ks = 0; ks < ksteps; ++ks) {
         mbar_wait(full + stage, phase);
-        const unsigned As = psm_s + stage * P_STAGE_BYTES;
+        const unsigned As = psm_s + stage * STAGE;
         const unsigned Bs = As + P_A_BYTES;
 #pragma unroll
         for (int kk = 0; kk < PBK; kk += 4) {
-          cplx af[4], bf[2];
+          cplx af[WI], bf[WJ];
 #pragma unroll
-          for (int j = 0; j < 2; ++j) bf[j] = lds_c(Bs + ((kk + (lane & 3)) * PBN + wn + j * 8 + (lane >> 2)) * 16);
+          for (int j = 0; j < WJ; ++j) bf[j] = lds_c(Bs + ((kk + (lane & 3)) * BN + wn + j * 8 + (lane >> 2)) * 16);
           // A element (r, k): box k/8, row r (128 B), 16-B chunk (k%8) ^ (r%8)
           const unsigned achunk = (((kk & 7) + (lane & 3)) ^ (lane >> 2)) << 4;
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
+          for (int i = 0; i < WI; ++i)
             af[i] = lds_c(As + (kk >> 3) * P_A_HALF + (wm + i * 8 + (lane >> 2)) * 128 + achunk);
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
+          for (int i = 0; i < WI; ++i)
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
+            for (int j = 0; j < WJ; ++j) {
               dmma884(are[i][j][0], are[i][j][1], af[i].x, bf[j].x);
               dmma884(aim[i][j][0], aim[i][j][1], af[i].x, bf[j].y);
             }
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
+          for (int i = 0; i < WI; ++i) {
             const double nai = -af[i].y;
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
+            for (int j = 0; j < WJ; ++j) {
               dmma884(are[i][j][0], are[i][j][1], nai, bf[j].y);
               dmma884(aim[i][j][0], aim[i][j][1], af[i].y, bf[j].x);
             }
@@ -227,11 +251,11 @@ static __global__ void __launch_bounds__(PTHREADS, 1) zgemm_sub_tma(const __grid
       }
       cplx* Cb = g.C + (long long)b * g.sC;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < WI; ++i) {
         const int rl = wm + i * 8 + (lane >> 2);
         const int r = m0 + rl;
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
+        for (int j = 0; j < WJ; ++j) {
           const int cl = wn + j * 8 + 2 * (lane & 3);
           const int c = n0 + cl;
           if (r < g.M) {
@@ -241,7 +265,7 @@ static __global__ void __launch_bounds__(PTHREADS, 1) zgemm_sub_tma(const __grid
                 const double pr = are[i][j][h], pi = aim[i][j][h];
                 cplx outv;
                 if (g.beta) {
-                  const cplx v = lds_c(Cs + (rl * PBN + cl + h) * 16);
+                  const cplx v = lds_c(Cs + (rl * BN + cl + h) * 16);
                   outv = cmk(v.x - pr, v.y - pi);
                 } else {
                   outv = cmk(pr, pi);
@@ -292,6 +316,23 @@ static inline int encode_a_map(CUtensorMap* map, const cplx* base, int cols, int
   return encode_c128_map(map, base, cols, rows, batch, ld, bstride, PAK, PBM, true);
 }
 
+// Tile width for a right-hand-side block of K columns: the smallest padded
+// width ceil(K / bn) * bn weighted by the measured efficiency of each tile
+// shape (n = 4096, 128 pencils: the 64-wide tile runs 32.9 TF/s, the 32-wide
+// 30.7, the 40- and 56-wide ~28.7, so K = 118 stays on 2 x 64 (65.3 ms per
+// pass vs 69.9 ms as 3 x 40) and K = 32 takes one 32-wide tile (17.9 vs 33.0 ms)).
+static inline int pick_tile_n(int K) {
+  const int cand[5] = {64, 56, 48, 40, 32};
+  const double eff[5] = {1.0, 0.87, 0.87, 0.876, 0.93};
+  int best = 64;
+  double cost = (K + 63) / 64 * 64;
+  for (int i = 1; i < 5; ++i) {
+    const double w = (double)((K + cand[i] - 1) / cand[i] * cand[i]) / eff[i];
+    if (w < cost) { best = cand[i]; cost = w; }
+  }
+  return best;
+}
+
 // Maps for the three operand roles: A (64 x 8 swizzled boxes), B (16 x 64), C (64 x 64).
 struct OperandMaps {
   CUtensorMap a, b, c;
@@ -312,12 +353,16 @@ static inline int encode_pencil_maps(PencilMaps& pm, cplx* base, int n, long lon
 static inline int zgemm_sub_maps(const CUtensorMap& mapA, const CUtensorMap& mapB, const CUtensorMap& mapC, int M, int N,
                           int K, int batch, int a_row0, int a_col0, int b_row0, int b_col0, int c_row0, int c_col0,
                           cplx* C, long long ldc, long long sC, cudaStream_t stream, int beta = 1,
-                          int a_bmul = 1, int a_badd = 0, const int* a_bmap = nullptr) {
+                          int a_bmul = 1, int a_badd = 0, const int* a_bmap = nullptr, int bn = PBN) {
   if (M <= 0 || N <= 0 || K <= 0 || batch <= 0) return 0;
   static bool attr = false;
   static int sms = 0;
   if (!attr) {
-    cudaFuncSetAttribute(zgemm_sub_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM);
+    cudaFuncSetAttribute(zgemm_sub_tma<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, TileBytes<64>::SMEM);
+    cudaFuncSetAttribute(zgemm_sub_tma<56>, cudaFuncAttributeMaxDynamicSharedMemorySize, TileBytes<56>::SMEM);
+    cudaFuncSetAttribute(zgemm_sub_tma<48>, cudaFuncAttributeMaxDynamicSharedMemorySize, TileBytes<48>::SMEM);
+    cudaFuncSetAttribute(zgemm_sub_tma<40>, cudaFuncAttributeMaxDynamicSharedMemorySize, TileBytes<40>::SMEM);
+    cudaFuncSetAttribute(zgemm_sub_tma<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, TileBytes<32>::SMEM);
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -327,13 +372,20 @@ static inline int zgemm_sub_maps(const CUtensorMap& mapA, const CUtensorMap& map
   int* ctr = cirr_tile_counter(stream);
   if (!ctr) return (int)cudaErrorMemoryAllocation;
   SubGemmGeom g{M, N, Kr, batch, a_row0, a_col0, b_row0, b_col0, c_row0, c_col0, C, ldc, sC,
-                (M + PBM - 1) / PBM, (N + PBN - 1) / PBN, beta, a_bmul, a_badd, ctr, a_bmap};
+                (M + PBM - 1) / PBM, (N + bn - 1) / bn, beta, a_bmul, a_badd, ctr, a_bmap};
   const long long tiles = (long long)g.tiles_m * g.tiles_n * batch;
   // persistent grid: every SM, or fewer when cirr_set_gemm_ctas leaves SMs to
   // latency-bound kernels on other streams (the dynamic tile scheduler adapts)
   const int cap = (g_cirr_gemm_cap > 0 && g_cirr_gemm_cap < sms) ? g_cirr_gemm_cap : sms;
   const int grid = (int)(tiles < cap ? tiles : cap);
-  zgemm_sub_tma<<<grid, PTHREADS, P_SMEM, stream>>>(mapA, mapB, mapC, g);
+  switch (bn) {
+    case 64: zgemm_sub_tma<64><<<grid, PTHREADS, TileBytes<64>::SMEM, stream>>>(mapA, mapB, mapC, g); break;
+    case 56: zgemm_sub_tma<56><<<grid, PTHREADS, TileBytes<56>::SMEM, stream>>>(mapA, mapB, mapC, g); break;
+    case 48: zgemm_sub_tma<48><<<grid, PTHREADS, TileBytes<48>::SMEM, stream>>>(mapA, mapB, mapC, g); break;
+    case 40: zgemm_sub_tma<40><<<grid, PTHREADS, TileBytes<40>::SMEM, stream>>>(mapA, mapB, mapC, g); break;
+    case 32: zgemm_sub_tma<32><<<grid, PTHREADS, TileBytes<32>::SMEM, stream>>>(mapA, mapB, mapC, g); break;
+    default: return (int)cudaErrorInvalidValue;
+  }
   cirr_note_launch();
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : (int)e;
