@@ -80,6 +80,17 @@ int cirr_diag_inverses(const cirr_cplx* LU, int n, long long ld, long long penci
  * 0 when it does not (callers may then skip cirr_diag_inverses). */
 int cirr_zgetrs_uses_dinv(int n, int K);
 
+/* K3a+K3b fused -- replaces solvers.py:121-129 as one call: the solves of
+ * cirr_zgetrs_gather (pencil_of NULL: entry j uses factor j, as
+ * cirr_zgetrs_batched) with the moment accumulation of cirr_moments (same
+ * coef/off/St layout, M <= 16) done inside the solve, block row by block row
+ * as the backward substitution finishes each one (L2-resident). */
+int cirr_zgetrs_moments(const cirr_cplx* LU, int n, long long ld, long long pencil_stride, int nfac,
+                        const int* pencil_of, int batch, const int* perm, const cirr_cplx* R, long long ldr,
+                        long long rstride, const int* rhs_of, int K, cirr_cplx* Y, long long ldy,
+                        long long ystride, const cirr_cplx* Dinv, const cirr_cplx* coef, int M, const int* off,
+                        int n_sets, cirr_cplx* St, long long ld_st, long long sstride, cudaStream_t stream);
+
 /* K3b -- replaces solvers.py:121-129 (acc[m] += w_j zeta_j^m Y_j).
  * St[c] ((M*K) x n): row m*K+col = column col of S_m of contour c, summed over
  * pencils off[c]..off[c+1]-1 in order with coef[j*M+m]. */

@@ -35,6 +35,8 @@ SIGNATURES = {
     "cirr_diag_inverses": [_P, _I, _L, _L, _I, _P, _P],
     "cirr_zgetrs_uses_dinv": [_I, _I],
     "cirr_moments": [_P, _L, _L, _I, _I, _P, _I, _P, _I, _P, _L, _L, _P],
+    "cirr_zgetrs_moments": [_P, _I, _L, _L, _I, _P, _I, _P, _P, _L, _L, _P, _I, _P, _L, _L, _P, _P, _I, _P, _I, _P,
+                            _L, _L, _P],
     "cirr_orth_ws_bytes": [_I, _I],
     "cirr_orth_phases": [_P],
     "cirr_orth": [_P, _L, _L, _I, _I, _I, _D, _P, _P, _P, _P, _L, _L, _P, _P, _P],

@@ -308,15 +308,16 @@ constexpr int MTC = 32;       // columns per tile
 // per thread), and S^T is written back through a shared-memory transpose so
 // its rows (contiguous along r) are also written in 512-byte runs.  HBM-bound:
 // each Y_j is read exactly once.
-template <int MM>
+template <int MM, int RQ>
 __global__ void __launch_bounds__(256) moments_kernel(const cplx* __restrict__ Y, long long ldy,
                                                       long long ystride, int n, int K,
                                                       const cplx* __restrict__ coef, int M,
                                                       const int* __restrict__ off, cplx* __restrict__ St,
-                                                      long long ld_st, long long sstride) {
-  __shared__ cplx tile[MTC][MTR + 1];
+                                                      long long ld_st, long long sstride, int row_lo) {
+  constexpr int TR = 8 * RQ;  // rows per tile: 32 for whole-matrix calls, 8 for the 128-row windows of a solve
+  __shared__ cplx tile[MTC][TR + 1];
   const int cidx = blockIdx.z;
-  const int r0 = blockIdx.y * MTR, c0 = blockIdx.x * MTC;
+  const int r0 = row_lo + blockIdx.y * TR, c0 = blockIdx.x * MTC;
   const int tid = threadIdx.x;
   const int j0 = off[cidx], j1 = off[cidx + 1];
   const int nj = j1 - j0;
@@ -324,30 +325,30 @@ __global__ void __launch_bounds__(256) moments_kernel(const cplx* __restrict__ Y
   // element q of this thread: row r0 + (tid >> 5) + 8 q, column c0 + (tid & 31)
   const int cl = tid & 31, rl = tid >> 5;
   const int col = c0 + cl;
-  cplx acc[4][MM];
+  cplx acc[RQ][MM];
 #pragma unroll
-  for (int q = 0; q < 4; ++q)
+  for (int q = 0; q < RQ; ++q)
 #pragma unroll
     for (int m = 0; m < MM; ++m) acc[q][m] = cmk(0.0, 0.0);
-  bool ok[4];
-  long long base[4];
+  bool ok[RQ];
+  long long base[RQ];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
+  for (int q = 0; q < RQ; ++q) {
     const int r = r0 + rl + 8 * q;
     ok[q] = r < n && col < K;
     base[q] = (long long)r * ldy + col;
   }
   const cplx* Yc = Y + (long long)j0 * ystride;
   for (int j = 0; j < nj; ++j, Yc += ystride) {
-    cplx y[4];
+    cplx y[RQ];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) y[q] = ok[q] ? Yc[base[q]] : cmk(0.0, 0.0);
+    for (int q = 0; q < RQ; ++q) y[q] = ok[q] ? Yc[base[q]] : cmk(0.0, 0.0);
 #pragma unroll
     for (int m = 0; m < MM; ++m)
       if (m < M) {
         const cplx cf = cj[j * M + m];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) cfma(acc[q][m], cf, y[q]);
+        for (int q = 0; q < RQ; ++q) cfma(acc[q][m], cf, y[q]);
       }
   }
   cplx* S = St + (long long)cidx * sstride;
@@ -355,13 +356,14 @@ __global__ void __launch_bounds__(256) moments_kernel(const cplx* __restrict__ Y
   for (int m = 0; m < MM; ++m) {
     if (m >= M) break;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) tile[cl][rl + 8 * q] = acc[q][m];
+    for (int q = 0; q < RQ; ++q) tile[cl][rl + 8 * q] = acc[q][m];
     __syncthreads();
     // write rows m*K + col of S^T: thread (rl', cl') writes S^T[c0 + rl' + 8q][r0 + cl']
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int cc = c0 + rl + 8 * q, rr = r0 + cl;
-      if (cc < K && rr < n) S[(long long)(m * K + cc) * ld_st + rr] = tile[rl + 8 * q][cl];
+    for (int q = 0; q < RQ; ++q) {
+      const int e = tid + 256 * q, ce = e / TR, re = e % TR;
+      const int cc = c0 + ce, rr = r0 + re;
+      if (cc < K && rr < n) S[(long long)(m * K + cc) * ld_st + rr] = tile[ce][re];
     }
     __syncthreads();
   }
@@ -581,14 +583,35 @@ static bool solve_tma_path(int n, int K) {
 // so callers can skip cirr_diag_inverses there.
 CIRR_API int cirr_zgetrs_uses_dinv(int n, int K) { return K <= 2 || solve_tma_path(n, K); }
 
+// Moment accumulation fused into a solve call (solvers.py:121-129): St[c] +=
+// coef[j*M+m] Y_j over the batch entries off[c]..off[c+1]-1 of contour c.
+struct MomentSpec {
+  const cplx* coef;
+  int M;
+  const int* off;
+  int n_sets;
+  cplx* St;
+  long long ld_st, sstride;
+};
+static int launch_moments(const cplx* Y, long long ldy, long long ystride, int n, int K, const cplx* coef, int M,
+                          const int* off, int n_sets, cplx* St, long long ld_st, long long sstride, int row_lo,
+                          int row_hi, cudaStream_t stream);
+static int moments_rows(const MomentSpec* ms, const cplx* Y, long long ldy, long long ystride, int n, int K,
+                        int row_lo, int row_hi, cudaStream_t stream) {
+  if (ms == nullptr) return 0;
+  return launch_moments(Y, ldy, ystride, n, K, ms->coef, ms->M, ms->off, ms->n_sets, ms->St, ms->ld_st,
+                        ms->sstride, row_lo, row_hi, stream);
+}
+
 // Solves for batch entries j = 0..batch-1 against factor pmap[j] (pmap null:
 // factor j) of the nfac factors at LU (pencil_stride apart); perm and Dinv are
 // indexed by factor, R by rhs_of[j], Y by j.
 static int getrs_impl(const cplx* LU, int n, long long ld, long long pencil_stride, int batch, int nfac,
                       const int* pmap, const int* perm, const cplx* R, long long ldr, long long rstride,
                       const int* rhs_of, int K, cplx* Y, long long ldy, long long ystride, const cplx* Dinv,
-                      cudaStream_t stream) {
+                      cudaStream_t stream, const MomentSpec* ms = nullptr) {
   if (n <= 0 || batch <= 0 || nfac <= 0 || K < 0 || ldy < K || ldr < K) return CIRR_EINVAL;
+  if (ms != nullptr && (ms->M < 1 || ms->M > MAXM || ms->n_sets <= 0)) return CIRR_EINVAL;
   if (K == 0) return 0;
   static bool attr = false;
   if (!attr) {
@@ -600,8 +623,9 @@ static int getrs_impl(const cplx* LU, int n, long long ld, long long pencil_stri
   permute_kernel<<<gp, 256, 0, stream>>>(R, ldr, rstride, rhs_of, perm, n, K, Y, ldy, ystride, pmap);
   CIRR_CHECK_LAUNCH();
   if (Dinv != nullptr && K <= 2) {  // one or two RHS: look-back triangular solves
-    if (K == 1) return trsv_lookback<1>(LU, n, ld, pencil_stride, batch, Dinv, Y, ldy, ystride, stream, pmap);
-    return trsv_lookback<2>(LU, n, ld, pencil_stride, batch, Dinv, Y, ldy, ystride, stream, pmap);
+    if (K == 1) CIRR_TRY(trsv_lookback<1>(LU, n, ld, pencil_stride, batch, Dinv, Y, ldy, ystride, stream, pmap));
+    else CIRR_TRY(trsv_lookback<2>(LU, n, ld, pencil_stride, batch, Dinv, Y, ldy, ystride, stream, pmap));
+    return moments_rows(ms, Y, ldy, ystride, n, K, 0, n, stream);
   }
   // right-looking blocked solves: per 64-row block a diagonal solve, then the
   // rank-64 update of the remaining rows on the TMA/DMMA GEMM (zgemm_sub_tma)
@@ -678,6 +702,9 @@ static int getrs_impl(const cplx* LU, int n, long long ld, long long pencil_stri
             CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, nb, K, s1 - i0 - nb, batch, i0, i0 + nb, i0 + nb, 0, i0,
                                           0, Y, ldy, ystride, stream, 1, 1, 0, pmap, BN));
           CIRR_TRY(apply_dinv(bi, false));
+          // rows i0.. are final for every entry: their moment rows now, while
+          // the block (batch x 128 x K) is still in L2
+          CIRR_TRY(moments_rows(ms, Y, ldy, ystride, n, K, i0, i0 + nb, stream));
         }
         if (s0 > 0)  // Y[:s0] -= U[:s0, s0:s1] Y[s0:s1]
           CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, s0, K, s1 - s0, batch, 0, s0, s0, 0, 0, 0, Y, ldy, ystride,
@@ -701,14 +728,14 @@ static int getrs_impl(const cplx* LU, int n, long long ld, long long pencil_stri
       CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, i0, K, nb, batch, 0, i0, i0, 0, 0, 0, Y, ldy, ystride,
                                     stream, 1, 1, 0, pmap, BN));
     }
-    return 0;
+    return moments_rows(ms, Y, ldy, ystride, n, K, 0, n, stream);
   }
   dim3 gs((K + SKC - 1) / SKC, batch);
   trsm_blocked_kernel<true><<<gs, 256, kSolveSmem, stream>>>(LU, ld, pencil_stride, n, Y, ldy, ystride, K, pmap);
   CIRR_CHECK_LAUNCH();
   trsm_blocked_kernel<false><<<gs, 256, kSolveSmem, stream>>>(LU, ld, pencil_stride, n, Y, ldy, ystride, K, pmap);
   CIRR_CHECK_LAUNCH();
-  return 0;
+  return moments_rows(ms, Y, ldy, ystride, n, K, 0, n, stream);
 }
 
 CIRR_API int cirr_zgetrs_batched(const cplx* LU, int n, long long ld, long long pencil_stride, int batch,
@@ -731,20 +758,61 @@ CIRR_API int cirr_zgetrs_gather(const cplx* LU, int n, long long ld, long long p
                     ystride, Dinv, stream);
 }
 
-// Moment blocks of n_sets contours: pencils off[c] .. off[c+1]-1 belong to
-// contour c; coef[j*M + m] = w_j zeta_j^m.  Output St[c] is (M*K) x n
-// row-major (row m*K+col = column col of S_m), ld ld_st, stride sstride.
+// Solves + moments: cirr_zgetrs_batched / cirr_zgetrs_gather whose moment
+// accumulation St[c] = sum_j coef[j*M+m] Y_j (cirr_moments' layout, M <= 16)
+// runs inside the solve: on the blocked TMA path each 128-row block of every
+// entry's Y is accumulated right after the backward step that finishes it
+// (L2-resident), so Y is not re-read from HBM by a separate moment pass.
+CIRR_API int cirr_zgetrs_moments(const cplx* LU, int n, long long ld, long long pencil_stride, int nfac,
+                                 const int* pencil_of, int batch, const int* perm, const cplx* R, long long ldr,
+                                 long long rstride, const int* rhs_of, int K, cplx* Y, long long ldy,
+                                 long long ystride, const cplx* Dinv, const cplx* coef, int M, const int* off,
+                                 int n_sets, cplx* St, long long ld_st, long long sstride, cudaStream_t stream) {
+  if (coef == nullptr || off == nullptr || St == nullptr) return CIRR_EINVAL;
+  const MomentSpec ms{coef, M, off, n_sets, St, ld_st, sstride};
+  return getrs_impl(LU, n, ld, pencil_stride, batch, pencil_of ? nfac : batch, pencil_of, perm, R, ldr, rstride,
+                    rhs_of, K, Y, ldy, ystride, Dinv, stream, &ms);
+}
+
+// Moment rows [row_lo, row_hi) of n_sets contours (rows past n are skipped):
+// pencils off[c] .. off[c+1]-1 belong to contour c; coef[j*M + m] = w_j zeta_j^m.
+// Output St[c] is (M*K) x n row-major (row m*K+col = column col of S_m), ld
+// ld_st, stride sstride.  Up to 16 moments per launch (MAXM).
+static int launch_moments(const cplx* Y, long long ldy, long long ystride, int n, int K, const cplx* coef, int M,
+                          const int* off, int n_sets, cplx* St, long long ld_st, long long sstride, int row_lo,
+                          int row_hi, cudaStream_t stream) {
+  if (row_hi > n) row_hi = n;
+  if (row_hi <= row_lo) return 0;
+  // windows of a solve (<= 128 rows) use 8-row tiles so the launch still has
+  // enough CTAs; whole-matrix calls use 32-row tiles (same sums, same order)
+  const bool win = row_hi - row_lo <= 128;
+  const int TR = win ? 8 : MTR;
+  dim3 g((K + MTC - 1) / MTC, (row_hi - row_lo + TR - 1) / TR, n_sets);
+#define CIRR_MOM(MMv, RQv) \
+  moments_kernel<MMv, RQv><<<g, 256, 0, stream>>>(Y, ldy, ystride, n, K, coef, M, off, St, ld_st, sstride, row_lo)
+  if (win) {
+    if (M <= 1) CIRR_MOM(1, 1);
+    else if (M <= 2) CIRR_MOM(2, 1);
+    else if (M <= 4) CIRR_MOM(4, 1);
+    else if (M <= 8) CIRR_MOM(8, 1);
+    else CIRR_MOM(16, 1);
+  } else {
+    if (M <= 1) CIRR_MOM(1, 4);
+    else if (M <= 2) CIRR_MOM(2, 4);
+    else if (M <= 4) CIRR_MOM(4, 4);
+    else if (M <= 8) CIRR_MOM(8, 4);
+    else CIRR_MOM(16, 4);
+  }
+#undef CIRR_MOM
+  CIRR_CHECK_LAUNCH();
+  return 0;
+}
+
+// Moment blocks of n_sets contours over all n rows (see launch_moments).
 CIRR_API int cirr_moments(const cplx* Y, long long ldy, long long ystride, int n, int K, const cplx* coef,
                           int M, const int* off, int n_sets, cplx* St, long long ld_st, long long sstride,
                           cudaStream_t stream) {
   if (n <= 0 || K < 0 || M < 1 || M > MAXM || n_sets <= 0) return CIRR_EINVAL;
   if (K == 0) return 0;
-  dim3 g((K + MTC - 1) / MTC, (n + MTR - 1) / MTR, n_sets);
-  if (M <= 1) moments_kernel<1><<<g, 256, 0, stream>>>(Y, ldy, ystride, n, K, coef, M, off, St, ld_st, sstride);
-  else if (M <= 2) moments_kernel<2><<<g, 256, 0, stream>>>(Y, ldy, ystride, n, K, coef, M, off, St, ld_st, sstride);
-  else if (M <= 4) moments_kernel<4><<<g, 256, 0, stream>>>(Y, ldy, ystride, n, K, coef, M, off, St, ld_st, sstride);
-  else if (M <= 8) moments_kernel<8><<<g, 256, 0, stream>>>(Y, ldy, ystride, n, K, coef, M, off, St, ld_st, sstride);
-  else moments_kernel<16><<<g, 256, 0, stream>>>(Y, ldy, ystride, n, K, coef, M, off, St, ld_st, sstride);
-  CIRR_CHECK_LAUNCH();
-  return 0;
+  return launch_moments(Y, ldy, ystride, n, K, coef, M, off, n_sets, St, ld_st, sstride, 0, n, stream);
 }

@@ -657,58 +657,72 @@ class _Engine:
                 runs[-1][1] = b
             else:
                 runs.append([a, b])
+        # the moment accumulation runs inside the solve call (cirr_zgetrs_moments)
+        # unless the conjugate-pair variant must first expand the solved nodes
+        fused = Psolve == Ptot and Ks == K and moments <= _MOMENT_CHUNK
         with _stage("solve"):
             dinv = self._dinv(Ks)
+            dptr = _ptr(dinv) if dinv is not None else 0
             if len(runs) > 1:
                 # scattered contours (refinement passes of a multi-pencil batch):
                 # one gathered call over their factors instead of one per run
                 pen_of = _h2d(np.concatenate([np.arange(a, b, dtype=np.int32) for a, b in pen_idx]))
-                _lib.call("cirr_zgetrs_gather", _ptr(self.pencils), n, n, n * n, self.P, _ptr(pen_of), Psolve,
-                          _ptr(self.perm), _ptr(R), Ks, n * Ks, _ptr(rhs_of), Ks, _ptr(Ysol), Ks, n * Ks,
-                          _ptr(dinv) if dinv is not None else 0, self.stream)
+                base, pen_ptr, fac_args = self.pencils, _ptr(pen_of), (_ptr(self.perm), dptr)
             else:
                 a, b = runs[0]
-                dptr = _ptr(dinv) + a * self._dinv_per_pencil if dinv is not None else 0
-                _lib.call("cirr_zgetrs_batched", _ptr(self.pencils[a]), n, n, n * n, b - a, _ptr(self.perm[a]),
-                          _ptr(R), Ks, n * Ks, _ptr(rhs_of), Ks, _ptr(Ysol), Ks, n * Ks, dptr, self.stream)
+                base, pen_ptr = self.pencils[a], 0
+                fac_args = (_ptr(self.perm[a]), _ptr(dinv) + a * self._dinv_per_pencil if dinv is not None else 0)
+            if fused:
+                _lib.call("cirr_zgetrs_moments", _ptr(base), n, n, n * n, self.P, pen_ptr, Psolve, fac_args[0],
+                          _ptr(R), Ks, n * Ks, _ptr(rhs_of), Ks, _ptr(Ysol), Ks, n * Ks, fac_args[1], _ptr(coef),
+                          moments, _ptr(off_t), nset, _ptr(St), n, moments * K * n, self.stream)
+            elif pen_ptr:
+                _lib.call("cirr_zgetrs_gather", _ptr(base), n, n, n * n, self.P, pen_ptr, Psolve, fac_args[0],
+                          _ptr(R), Ks, n * Ks, _ptr(rhs_of), Ks, _ptr(Ysol), Ks, n * Ks, fac_args[1], self.stream)
+            else:
+                _lib.call("cirr_zgetrs_batched", _ptr(base), n, n, n * n, Psolve, fac_args[0], _ptr(R), Ks, n * Ks,
+                          _ptr(rhs_of), Ks, _ptr(Ysol), Ks, n * Ks, fac_args[1], self.stream)
         _work("solve_flops", Psolve * 8.0 * n * n * Ks)
         _work("solve_flops_exec", sum((b - a) * 8.0 * n * n * k for (a, b), k in zip(pen_idx, ks)))
-        if Psolve == Ptot and Ks == K:
-            Y = Ysol
-        else:  # conjugate-pair variant: expand to every node in quadrature order
-            Y = torch.zeros((Ptot, n, K), dtype=torch.complex128, device="cuda")
-            with _stage("solve"):
-                for s, ci in enumerate(active):
-                    c = self.cs[ci]
-                    kc = rhs[ci].shape[1]
-                    N = len(c.nodes)
-                    if c.half:
-                        up = np.zeros(N, dtype=bool)
-                        up[c.fidx] = True
-                        src = spos[s] + c.mate
-                        cj = (~up).astype(np.int32)
-                        col0 = np.where(up, 0, kc if cplx_rhs[s] else 0)
-                    else:
-                        src, cj, col0 = spos[s] + np.arange(N), np.zeros(N, np.int32), np.zeros(N)
-                    meta = _h2d(np.stack([src, col0, cj]).astype(np.int32))
-                    _lib.call("cirr_copy_cols", _ptr(Ysol), Ks, n * Ks, _ptr(meta[0]), _ptr(meta[1]),
-                              _ptr(meta[2]), n, kc, N, _ptr(Y[offs[s]]), K, n * K, self.stream)
-            del Ysol
-        with _stage("moments"):
-            if moments <= _MOMENT_CHUNK:
-                _lib.call("cirr_moments", _ptr(Y), K, n * K, n, K, _ptr(coef), moments, _ptr(off_t), nset,
-                          _ptr(St), n, moments * K * n, self.stream)
-            else:  # the reference takes any n_moments >= 1: 16 moments per launch
-                cf = np.concatenate(coefs, axis=0)
-                for m0 in range(0, moments, _MOMENT_CHUNK):
-                    mc = min(_MOMENT_CHUNK, moments - m0)
-                    cpart = _h2d(np.ascontiguousarray(cf[:, m0:m0 + mc]))
-                    _lib.call("cirr_moments", _ptr(Y), K, n * K, n, K, _ptr(cpart), mc, _ptr(off_t), nset,
-                              _ptr(St[:, m0 * K:]), n, moments * K * n, self.stream)
         _work("moment_flops", Ptot * 8.0 * n * K * moments)
+        if fused:
+            del Ysol
+        else:
+            if Psolve == Ptot and Ks == K:
+                Y = Ysol
+            else:  # conjugate-pair variant: expand to every node in quadrature order
+                Y = torch.zeros((Ptot, n, K), dtype=torch.complex128, device="cuda")
+                with _stage("solve"):
+                    for s, ci in enumerate(active):
+                        c = self.cs[ci]
+                        kc = rhs[ci].shape[1]
+                        N = len(c.nodes)
+                        if c.half:
+                            up = np.zeros(N, dtype=bool)
+                            up[c.fidx] = True
+                            src = spos[s] + c.mate
+                            cj = (~up).astype(np.int32)
+                            col0 = np.where(up, 0, kc if cplx_rhs[s] else 0)
+                        else:
+                            src, cj, col0 = spos[s] + np.arange(N), np.zeros(N, np.int32), np.zeros(N)
+                        meta = _h2d(np.stack([src, col0, cj]).astype(np.int32))
+                        _lib.call("cirr_copy_cols", _ptr(Ysol), Ks, n * Ks, _ptr(meta[0]), _ptr(meta[1]),
+                                  _ptr(meta[2]), n, kc, N, _ptr(Y[offs[s]]), K, n * K, self.stream)
+                del Ysol
+            with _stage("moments"):
+                if moments <= _MOMENT_CHUNK:
+                    _lib.call("cirr_moments", _ptr(Y), K, n * K, n, K, _ptr(coef), moments, _ptr(off_t), nset,
+                              _ptr(St), n, moments * K * n, self.stream)
+                else:  # the reference takes any n_moments >= 1: 16 moments per launch
+                    cf = np.concatenate(coefs, axis=0)
+                    for m0 in range(0, moments, _MOMENT_CHUNK):
+                        mc = min(_MOMENT_CHUNK, moments - m0)
+                        cpart = _h2d(np.ascontiguousarray(cf[:, m0:m0 + mc]))
+                        _lib.call("cirr_moments", _ptr(Y), K, n * K, n, K, _ptr(cpart), mc, _ptr(off_t), nset,
+                                  _ptr(St[:, m0 * K:]), n, moments * K * n, self.stream)
+            del Y
         for s, ci in enumerate(active):
             self.cs[ci].stats.n_linear_solves += len(self.cs[ci].fidx) * ks[s]
-        del Y
         out = {}
         for s, ci in enumerate(active):
             kc = rhs[ci].shape[1]

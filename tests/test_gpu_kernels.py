@@ -237,6 +237,55 @@ def test_moments(lib, M):
             assert np.allclose(got[c, m * K:(m + 1) * K].T, ref, rtol=0, atol=1e-13 * np.abs(ref).max())
 
 
+@pytest.mark.parametrize("K,M,use_dinv,gather", [(32, 8, True, False), (118, 1, True, True), (8, 4, False, False),
+                                                  (2, 1, True, False), (37, 16, True, True)])
+@pytest.mark.parametrize("n", [333, 600])
+def test_zgetrs_moments_fused(lib, n, K, M, use_dinv, gather):
+    """cirr_zgetrs_moments (solve with the moment accumulation inside the call,
+    block row by block row on the blocked path) equals cirr_zgetrs_batched /
+    _gather followed by cirr_moments, bit for bit, for every solve path."""
+    rng = np.random.default_rng(n * K + M)
+    nodes = [3, 4]
+    nfac = 9
+    A = rng.standard_normal((nfac, n, n)) + 1j * rng.standard_normal((nfac, n, n))
+    F = cuda(A.copy())
+    ipiv = torch.empty((nfac, n), dtype=torch.int32, device="cuda")
+    perm = torch.empty((nfac, n), dtype=torch.int32, device="cuda")
+    mp = torch.empty(nfac, dtype=torch.float64, device="cuda")
+    info = torch.empty(nfac, dtype=torch.int32, device="cuda")
+    lib.call("cirr_zgetrf_batched", P(F), n, n, n * n, nfac, P(ipiv), P(perm), P(mp), P(info), P(ws_lu(n, nfac)), S())
+    dinv = 0
+    if use_dinv:
+        dinv_t = cuda(np.zeros(lib.call("cirr_diag_inv_bytes", n, nfac), dtype=np.uint8))
+        lib.call("cirr_diag_inverses", P(F), n, n, n * n, nfac, P(dinv_t), S())
+        dinv = P(dinv_t)
+    batch = sum(nodes)
+    pen_of = np.array([8, 1, 3, 0, 5, 6, 2], dtype=np.int32) if gather else None
+    R = cuda(rng.standard_normal((2, n, K)) + 1j * rng.standard_normal((2, n, K)))
+    rhs_of = cuda(np.repeat(np.arange(2, dtype=np.int32), nodes))
+    coef = cuda(rng.standard_normal((batch, M)) + 1j * rng.standard_normal((batch, M)))
+    off = cuda(np.concatenate([[0], np.cumsum(nodes)]).astype(np.int32))
+    Y1 = torch.empty((batch, n, K), dtype=torch.complex128, device="cuda")
+    Y2 = torch.empty_like(Y1)
+    S1 = torch.zeros((2, M * K, n), dtype=torch.complex128, device="cuda")
+    S2 = torch.zeros_like(S1)
+    if gather:
+        po = cuda(pen_of)
+        assert lib.call("cirr_zgetrs_gather", P(F), n, n, n * n, nfac, P(po), batch, P(perm), P(R), K, n * K,
+                        P(rhs_of), K, P(Y1), K, n * K, dinv, S()) == 0
+        pp = P(po)
+    else:
+        assert lib.call("cirr_zgetrs_batched", P(F), n, n, n * n, batch, P(perm), P(R), K, n * K, P(rhs_of), K,
+                        P(Y1), K, n * K, dinv, S()) == 0
+        pp = 0
+    assert lib.call("cirr_moments", P(Y1), K, n * K, n, K, P(coef), M, P(off), 2, P(S1), n, M * K * n, S()) == 0
+    assert lib.call("cirr_zgetrs_moments", P(F), n, n, n * n, nfac, pp, batch, P(perm), P(R), K, n * K, P(rhs_of),
+                    K, P(Y2), K, n * K, dinv, P(coef), M, P(off), 2, P(S2), n, M * K * n, S()) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(Y1, Y2)
+    assert torch.equal(S1, S2)
+
+
 def _cholqr2(lib, mats, c, kappa_max=1e5):
     """mats: list of n x c_p blocks (c_p <= c); returns (Qt rows, ok) per block."""
     nb, n = len(mats), mats[0].shape[0]
