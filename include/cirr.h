@@ -80,6 +80,19 @@ int cirr_diag_inverses(const cirr_cplx* LU, int n, long long ld, long long penci
  * 0 when it does not (callers may then skip cirr_diag_inverses). */
 int cirr_zgetrs_uses_dinv(int n, int K);
 
+/* Engine plumbing (no reference counterpart): the batched GEMM with a
+ * per-entry A operand at device address a_ptrs[b] (products with the pencils
+ * of many GEPs without stacking them), a one-launch assembly of npiece device
+ * blocks into a batched buffer (desc: device int64[8*npiece] =
+ * {src address, src ld, rows, cols, dst entry, dst column, conj, dst ld or 0}), and a
+ * stream-ordered zero fill.  Together they keep PyTorch to allocation only. */
+int cirr_gemm_ptrs(int a_kind, int M, int N, int K, int batch, const long long* a_ptrs, long long lda,
+                   const cirr_cplx* B, long long ldb, long long sB, cirr_cplx* C, long long ldc, long long sC,
+                   double alpha, int beta, cudaStream_t stream);
+int cirr_gather_blocks(int npiece, const long long* desc, long long max_elems, cirr_cplx* dst, long long ldd,
+                       long long sd, cudaStream_t stream);
+int cirr_zero(void* p, long long bytes, cudaStream_t stream);
+
 /* K3a+K3b fused -- replaces solvers.py:121-129 as one call: the solves of
  * cirr_zgetrs_gather (pencil_of NULL: entry j uses factor j, as
  * cirr_zgetrs_batched) with the moment accumulation of cirr_moments (same

@@ -23,6 +23,7 @@ struct GemmArgs {
   double alpha; int beta;             // beta: 0 -> overwrite, 1 -> accumulate
   int splits = 1;                     // split-K slices (> 1: raw partial sums into part)
   cplx* part = nullptr;               // splits x batch x M x N partials
+  const long long* a_ptrs = nullptr;  // optional: A of batch entry b at address a_ptrs[b] (sA ignored)
 };
 
 constexpr int GBM = 64, GBN = 64, GBK = 16;
@@ -56,7 +57,8 @@ __global__ void __launch_bounds__(GTHREADS, 2) gemm_kernel(GemmArgs g) {
   auto load_tile = [&](int stage, int k0) {
     unsigned char* base = gsm + stage * S::stage;
     if constexpr (A_REAL) {
-      const double* Ag = reinterpret_cast<const double*>(g.A) + (long long)b * g.sA;
+      const double* Ag = g.a_ptrs ? reinterpret_cast<const double*>(g.a_ptrs[b])
+                                  : reinterpret_cast<const double*>(g.A) + (long long)b * g.sA;
       double* As = reinterpret_cast<double*>(base);
 #pragma unroll
       for (int i = 0; i < (GBM * GBK) / GTHREADS; ++i) {
@@ -67,7 +69,8 @@ __global__ void __launch_bounds__(GTHREADS, 2) gemm_kernel(GemmArgs g) {
         cp_async8(As + r * GAR_LD + c, src, p);
       }
     } else {
-      const cplx* Ag = reinterpret_cast<const cplx*>(g.A) + (long long)b * g.sA;
+      const cplx* Ag = g.a_ptrs ? reinterpret_cast<const cplx*>(g.a_ptrs[b])
+                                : reinterpret_cast<const cplx*>(g.A) + (long long)b * g.sA;
       cplx* As = reinterpret_cast<cplx*>(base);
 #pragma unroll
       for (int i = 0; i < (GBM * GBK) / GTHREADS; ++i) {

@@ -347,6 +347,47 @@ def _ptr(t) -> int:
     return t.data_ptr()
 
 
+def _zeros(shape, dtype=None):
+    """A zero-filled device tensor: torch allocates, libcirr zero-fills (a
+    stream-ordered memset, no PyTorch kernel on the path)."""
+    torch = _torch()
+    t = torch.empty(shape, dtype=dtype or torch.complex128, device="cuda")
+    if t.numel():
+        _lib.call("cirr_zero", _ptr(t), t.numel() * t.element_size(), _stream())
+    return t
+
+
+def _piece(src, d: int, c0: int = 0, conj: bool = False, rows: int | None = None, cols: int | None = None,
+           dst_ld: int = 0):
+    """Descriptor of one 2-D complex block (a row-major view with unit column
+    stride) for _gather: its rows x cols elements go to entry d, column c0
+    (row pitch dst_ld, default the destination's)."""
+    if src.dim() == 1:
+        src = src[None, :]
+    r, c = src.shape
+    ld = src.stride(0) if r > 1 else c
+    if c > 1 and src.stride(1) != 1:
+        raise DeviceError("gather source must have unit column stride")
+    return (src.data_ptr(), ld, r if rows is None else rows, c if cols is None else cols, d, c0, 1 if conj else 0,
+            dst_ld)
+
+
+def _gather(pieces: list, dst):
+    """Copy the pieces into dst with one libcirr launch per 65535 pieces
+    (cirr_gather_blocks).  dst is (entries x rows x cols) and a piece's index
+    names its entry, or 2-D (rows x cols) and the index names its first row."""
+    if not pieces:
+        return dst
+    ld = dst.stride(-2)
+    sd = dst.stride(0)
+    for a in range(0, len(pieces), 65535):
+        part = pieces[a:a + 65535]
+        desc = _h2d(np.asarray(part, dtype=np.int64).reshape(-1))
+        mx = max(p_[2] * p_[3] for p_ in part)
+        _lib.call("cirr_gather_blocks", len(part), _ptr(desc), mx, _ptr(dst), ld, sd, _stream())
+    return dst
+
+
 def _h2d(x: np.ndarray):
     """Host array -> device tensor, stream-ordered on the current stream with no
     host synchronisation (pinned staging from torch's caching host allocator),
@@ -436,39 +477,67 @@ class _Contour:
     def _coef(self, moments: int) -> np.ndarray:
         if moments == 1:  # w_j * (1+0j): exact products, so numpy's multiply gives the loop's bits
             return (self.weights * (1.0 + 0.0j))[:, None].copy()
-        out = np.empty((len(self.nodes), moments), dtype=np.complex128)
-        for j, (z, w) in enumerate(zip(self.nodes, self.weights)):
-            zeta = (z - self.gamma) / self.rho
-            zp = 1.0 + 0.0j
-            for m in range(moments):
-                out[j, m] = w * zp
-                zp *= zeta
-        return out
+        return _coef_rows(self.nodes, self.weights, self.gamma, self.rho, moments)
+
+
+def _coef_batch(cs: list, moments: int) -> np.ndarray:
+    """The stacked moment coefficients of several contours (rows in node
+    order, contour after contour): _Contour._coef over all of them at once
+    (the same real arithmetic, so the same bits)."""
+    if len(cs) == 1:
+        return cs[0].coef(moments)
+    w = np.concatenate([c.weights for c in cs])
+    if moments == 1:
+        return (w * (1.0 + 0.0j))[:, None].copy()
+    z = np.concatenate([c.nodes for c in cs])
+    cnt = [len(c.nodes) for c in cs]
+    gamma = np.repeat(np.array([c.gamma for c in cs], dtype=np.complex128), cnt)
+    rho = np.repeat(np.array([c.rho for c in cs], dtype=np.float64), cnt)
+    return _coef_rows(z, w, gamma, rho, moments)
+
+
+def _coef_rows(z, w, gamma, rho, moments: int) -> np.ndarray:
+    # zp_0 = 1, zp_m = zp_{m-1} * zeta and c = w zp with every complex product
+    # written out in real arithmetic (rounded products, then the sum): the bits
+    # of the scalar loop (numpy's vectorised complex multiply contracts to FMA
+    # and differs in the last ulp)
+    zeta = (z - gamma) / rho
+    zr, zi = zeta.real, zeta.imag
+    wr, wi = w.real, w.imag
+    out = np.empty((len(z), moments), dtype=np.complex128)
+    pr, pi = np.ones(len(z)), np.zeros(len(z))
+    for m in range(moments):
+        out[:, m].real = wr * pr - wi * pi
+        out[:, m].imag = wr * pi + wi * pr
+        pr, pi = pr * zr - pi * zi, pr * zi + pi * zr
+    return out
 
 
 def _pad_stack(blocks: list, dim: int, width: int):
-    """Stack 2-D device blocks into (len, ...) zero-padded to `width` along
-    their axis `dim` (0 or 1): one stack and one indexed copy per distinct
-    width instead of one copy per block (device-agnostic tensor plumbing)."""
-    import torch
+    """Stack 2-D complex device blocks into (len, ...) zero-padded to `width`
+    along their axis `dim` (0 or 1): one zero fill and one cirr_gather_blocks
+    launch for the whole list."""
     shape = list(blocks[0].shape)
     shape[dim] = width
-    out = torch.zeros([len(blocks)] + shape, dtype=blocks[0].dtype, device=blocks[0].device)
-    groups: dict = {}
-    for i, b in enumerate(blocks):
-        groups.setdefault(int(b.shape[dim]), []).append(i)
-    for w, idx in groups.items():
-        if w == 0:
-            continue
-        src = torch.stack([blocks[i] for i in idx])
-        sel = torch.tensor(idx, dtype=torch.long)
-        if out.is_cuda:  # pinned, stream-ordered upload: no host synchronisation
-            sel = sel.pin_memory().to(out.device, non_blocking=True)
-        if dim == 0:
-            out[:, :w].index_copy_(0, sel, src)
-        else:
-            out[:, :, :w].index_copy_(0, sel, src)
-    return out
+    out = _zeros([len(blocks)] + shape)
+    return _gather([_piece(b, i) for i, b in enumerate(blocks) if b.numel()], out)
+
+
+_SOURCE_CACHE: dict = {}
+
+
+def _source_block(seed: int, n: int, ncols: int) -> np.ndarray:
+    """default_rng(seed).standard_normal((n, ncols)) (solvers.py:178-180),
+    memoised: many contours of a batch share a seed (solve_multi's seed + i)."""
+    key = (int(seed), int(n), int(ncols))
+    v = _SOURCE_CACHE.get(key)
+    if v is None:
+        if len(_SOURCE_CACHE) >= 64:
+            _SOURCE_CACHE.pop(next(iter(_SOURCE_CACHE)))
+        v = np.random.default_rng(seed).standard_normal((n, ncols))
+        v.setflags(write=False)
+        _SOURCE_CACHE[key] = v
+    return v
 
 
 class _Engine:
@@ -493,12 +562,27 @@ class _Engine:
 
     def _mats(self, cis: list):
         """(A, B, batch stride) for the pencils of contours cis in order: the
-        shared pencil with stride 0, else stacked copies (n^2 apart)."""
+        shared pencil with stride 0, else (A address array, B address array,
+        None) for cirr_gemm_ptrs (no stacked copies)."""
         dps = [self._dp_of(ci) for ci in cis]
         if all(d is dps[0] for d in dps):
             return dps[0].a, dps[0].b, 0
-        torch = self.torch
-        return torch.stack([d.a for d in dps]), torch.stack([d.b for d in dps]), self.n * self.n
+        key = tuple(cis)
+        cache = self.__dict__.setdefault("_mat_ptrs", {})
+        if key not in cache:
+            cache[key] = (_h2d(np.array([d.a.data_ptr() for d in dps], dtype=np.int64)),
+                          _h2d(np.array([d.b.data_ptr() for d in dps], dtype=np.int64)), None)
+        return cache[key]
+
+    def _gemm_mats(self, M, N, K, batch, mat, stride, Bt, ldb, sB, C, ldc, sC):
+        """C[b] = mat[b] @ Bt[b] with mat from _mats (shared, or address array)."""
+        kind = self.dp.gemm_kind
+        if stride is None:
+            _lib.call("cirr_gemm_ptrs", kind, M, N, K, batch, _ptr(mat), K, _ptr(Bt), ldb, sB, _ptr(C), ldc, sC, 1.0,
+                      0, self.stream)
+        else:
+            _lib.call("cirr_gemm", kind, M, N, K, batch, _ptr(mat), K, stride, _ptr(Bt), ldb, sB, _ptr(C), ldc, sC,
+                      1.0, 0, self.stream)
 
     def _pencil_runs(self, a: int, b: int):
         """Maximal ranges [lo, hi) of pencils a..b-1 that share one DevicePencil."""
@@ -612,7 +696,7 @@ class _Engine:
         torch, n = self.torch, self.n
         K = max(rhs[ci].shape[1] for ci in active)
         if K == 0:
-            return {ci: torch.zeros((0, n), dtype=torch.complex128, device="cuda") for ci in active}
+            return {ci: torch.empty((0, n), dtype=torch.complex128, device="cuda") for ci in active}
         nset = len(active)
         # solve width per contour: conjugate-pair contours with a complex
         # block solve [R | conj R] on their upper-half factors
@@ -623,29 +707,32 @@ class _Engine:
             cplx_rhs.append(cx)
             ks.append(2 * kc if cx else kc)
         Ks = max(ks)
-        if nset > 1 and not any(cplx_rhs) and all(k_ == Ks for k_ in ks):
-            R = torch.stack([rhs[ci] for ci in active])   # one copy kernel for the whole set
-        elif nset > 1 and not any(cplx_rhs):
-            R = _pad_stack([rhs[ci] for ci in active], 1, Ks)
-        else:
-            R = torch.zeros((nset, n, Ks), dtype=torch.complex128, device="cuda")
+        r0 = rhs[active[0]]
+        if nset == 1 and not cplx_rhs[0] and r0.is_contiguous():
+            R = r0.unsqueeze(0)                                # the block itself
+        else:  # one gather launch (+ a zero fill when widths differ)
+            R = _zeros((nset, n, Ks)) if any(k_ < Ks for k_ in ks) else torch.empty(
+                (nset, n, Ks), dtype=torch.complex128, device="cuda")
+            pieces = []
             for s, ci in enumerate(active):
                 kc = rhs[ci].shape[1]
-                R[s, :, :kc].copy_(rhs[ci])
-                if cplx_rhs[s]:
-                    R[s, :, kc:2 * kc].copy_(rhs[ci].conj())
+                if kc:
+                    pieces.append(_piece(rhs[ci], s))
+                    if cplx_rhs[s]:
+                        pieces.append(_piece(rhs[ci], s, kc, conj=True))
+            _gather(pieces, R)
         pen_idx, spos = [], [0]
-        offs, coefs = [0], []
+        offs = [0]
         for s, ci in enumerate(active):
             a, b = self.node_off[ci], self.node_off[ci + 1]
             pen_idx.append((a, b))
             spos.append(spos[-1] + (b - a))
             offs.append(offs[-1] + len(self.cs[ci].nodes))
-            coefs.append(self.cs[ci].coef(moments))
+        coefs = _coef_batch([self.cs[ci] for ci in active], moments)
         Psolve, Ptot = spos[-1], offs[-1]
         Ysol = torch.empty((Psolve, n, Ks), dtype=torch.complex128, device="cuda")
-        rhs_of = _h2d(np.concatenate([np.full(b - a, s, dtype=np.int32) for s, (a, b) in enumerate(pen_idx)]))
-        coef = _h2d(np.concatenate(coefs, axis=0))
+        rhs_of = _h2d(np.repeat(np.arange(nset, dtype=np.int32), [b - a for a, b in pen_idx]))
+        coef = _h2d(coefs)
         off_t = _h2d(np.asarray(offs, dtype=np.int32))
         St = torch.empty((nset, moments * K, n), dtype=torch.complex128, device="cuda")
         # solve contour ranges; ranges that are adjacent in the pencil buffer go
@@ -714,7 +801,7 @@ class _Engine:
                     _lib.call("cirr_moments", _ptr(Y), K, n * K, n, K, _ptr(coef), moments, _ptr(off_t), nset,
                               _ptr(St), n, moments * K * n, self.stream)
                 else:  # the reference takes any n_moments >= 1: 16 moments per launch
-                    cf = np.concatenate(coefs, axis=0)
+                    cf = coefs
                     for m0 in range(0, moments, _MOMENT_CHUNK):
                         mc = min(_MOMENT_CHUNK, moments - m0)
                         cpart = _h2d(np.ascontiguousarray(cf[:, m0:m0 + mc]))
@@ -723,11 +810,24 @@ class _Engine:
             del Y
         for s, ci in enumerate(active):
             self.cs[ci].stats.n_linear_solves += len(self.cs[ci].fidx) * ks[s]
-        out = {}
+        out, pieces, rows = {}, [], 0
         for s, ci in enumerate(active):
             kc = rhs[ci].shape[1]
-            # drop the zero rows a narrower block got from the common width K
-            out[ci] = St[s] if kc == K else St[s].view(moments, K, n)[:, :kc].reshape(moments * kc, n)
+            if kc == K:
+                out[ci] = St[s]
+            elif moments == 1:  # the zero rows of a narrower block are a suffix
+                out[ci] = St[s, :kc]
+            else:  # drop the zero rows inside each moment block: one gather for all
+                for m in range(moments):
+                    pieces.append(_piece(St[s, m * K:m * K + kc], rows + m * kc))
+                out[ci] = (rows, moments * kc)
+                rows += moments * kc
+        if pieces:
+            flat = torch.empty((rows, n), dtype=torch.complex128, device="cuda")
+            _gather(pieces, flat)    # entry index = destination row (stride n)
+            for ci, v in out.items():
+                if isinstance(v, tuple):
+                    out[ci] = flat[v[0]:v[0] + v[1]]
         return out
 
     def _dinv(self, K: int):
@@ -756,22 +856,26 @@ class _Engine:
         """B @ x for a device (n x k) complex block (B of contour ci's pencil)."""
         d = self.dp if ci is None else self._dp_of(ci)
         torch, n = self.torch, self.n
-        x = x.contiguous()
         k = x.shape[1]
+        if k > 1 and x.stride(1) != 1:
+            x = x.contiguous()
+        ldx = x.stride(0) if k > 1 else 1
         out = torch.empty((n, k), dtype=torch.complex128, device="cuda")
         if k:
-            _lib.call("cirr_gemm", d.gemm_kind, n, k, n, 1, _ptr(d.b), n, 0, _ptr(x), k, 0, _ptr(out), k, 0,
+            _lib.call("cirr_gemm", d.gemm_kind, n, k, n, 1, _ptr(d.b), n, 0, _ptr(x), ldx, 0, _ptr(out), k, 0,
                       1.0, 0, self.stream)
         return out
 
     def amul(self, x, ci: int | None = None):
         d = self.dp if ci is None else self._dp_of(ci)
         torch, n = self.torch, self.n
-        x = x.contiguous()
         k = x.shape[1]
+        if k > 1 and x.stride(1) != 1:
+            x = x.contiguous()
+        ldx = x.stride(0) if k > 1 else 1
         out = torch.empty((n, k), dtype=torch.complex128, device="cuda")
         if k:
-            _lib.call("cirr_gemm", d.gemm_kind, n, k, n, 1, _ptr(d.a), n, 0, _ptr(x), k, 0, _ptr(out), k, 0,
+            _lib.call("cirr_gemm", d.gemm_kind, n, k, n, 1, _ptr(d.a), n, 0, _ptr(x), ldx, 0, _ptr(out), k, 0,
                       1.0, 0, self.stream)
         return out
 
@@ -780,7 +884,7 @@ class _Engine:
         ((n, L)).astype(complex) of every active contour (solvers.py:178-182):
         one upload and one batched GEMM when the contours share L."""
         torch, n = self.torch, self.n
-        vs = {ci: np.random.default_rng(self.cs[ci].seed).standard_normal((n, self.cs[ci].ncols)) for ci in active}
+        vs = {ci: _source_block(self.cs[ci].seed, n, self.cs[ci].ncols) for ci in active}
         widths = {v.shape[1] for v in vs.values()}
         if not self.multi or len(widths) != 1:
             return {ci: self.bmul(_h2d(vs[ci].astype(complex)), ci) for ci in active}
@@ -789,8 +893,7 @@ class _Engine:
         _, B, stride = self._mats(active)
         out = torch.empty((len(active), n, k), dtype=torch.complex128, device="cuda")
         if k:
-            _lib.call("cirr_gemm", self._dp_of(active[0]).gemm_kind, n, k, n, len(active), _ptr(B), n, stride,
-                      _ptr(V), k, n * k, _ptr(out), k, n * k, 1.0, 0, self.stream)
+            self._gemm_mats(n, k, n, len(active), B, stride, V, k, n * k, out, k, n * k)
         return {ci: out[s] for s, ci in enumerate(active)}
 
     # -- K4..K7 for one contour --------------------------------------------
@@ -824,11 +927,9 @@ class _Engine:
             return None
         nb = len(items)
         cmax = max(S_.shape[0] for _, S_ in items)
-        Y = torch.zeros((nb, cmax, n), dtype=torch.complex128, device="cuda")
-        for b, (_, S_) in enumerate(items):
-            Y[b, : S_.shape[0]].copy_(S_)
-        Qt = torch.zeros((nb, cmax, n), dtype=torch.complex128, device="cuda")
-        kept = torch.zeros(nb, dtype=torch.int32, device="cuda")
+        Y = _pad_stack([S_ for _, S_ in items], 0, cmax)
+        Qt = _zeros((nb, cmax, n))
+        kept = _zeros(nb, torch.int32)
         _lib.call("cirr_orthonormalize", _ptr(Y), n, cmax * n, n, cmax, nb, float(cfg.drop_tol), _ptr(Qt), n,
                   cmax * n, _ptr(kept), st)
         return self._live(items, Qt, kept.cpu().numpy(), out)
@@ -841,13 +942,13 @@ class _Engine:
                 out[items[b][0]] = ("rankzero",)
         if not live:
             return None
-        if len(live) < nb:
-            sel = self.torch.tensor(live, dtype=self.torch.long, device="cuda")
-            Qt = Qt.index_select(0, sel)
+        kmax = int(ks[live].max())
+        if len(live) < nb or kmax < Qt.shape[1]:
+            out_q = self.torch.empty((len(live), kmax, Qt.shape[2]), dtype=Qt.dtype, device="cuda")
+            Qt = _gather([_piece(Qt[b, :kmax], i) for i, b in enumerate(live)], out_q)
             ks = ks[live]
             items = [items[b] for b in live]
-        kmax = int(ks.max())
-        return items, Qt[:, :kmax].contiguous(), ks
+        return items, Qt, ks
 
     def _basis_svd(self, items: list, out: dict, try_cholqr: bool = False):
         torch, n, cfg, st = self.torch, self.n, self.cfg, self.stream
@@ -859,20 +960,17 @@ class _Engine:
             return None
         nb = len(items)
         cmax = max(S_.shape[0] for _, S_ in items)
-        if nb > 1 and all(S_.shape[0] == cmax for _, S_ in items):
-            W = torch.stack([S_ for _, S_ in items])
-        else:
-            W = _pad_stack([S_ for _, S_ in items], 0, cmax)
+        W = _pad_stack([S_ for _, S_ in items], 0, cmax)
         if try_cholqr and cmax <= n:
             # refinement blocks are normally far from rank deficient: when
             # ||R||_F ||R^-1||_F <= 1e5 certifies that no singular value is cut
             # (rank_rel_tol <= 1e-12), the CholeskyQR2 basis spans the same
             # space as the kept singular vectors (linalg.py:107-119)
             cdim = _h2d(np.array([S_.shape[0] for _, S_ in items], dtype=np.int32))
-            Qt = torch.zeros((nb, cmax, n), dtype=torch.complex128, device="cuda")
+            Qt = _zeros((nb, cmax, n))
             ws = torch.empty(int(_lib.call("cirr_orth_cholqr2_ws_bytes", n, cmax, nb)), dtype=torch.uint8,
                              device="cuda")
-            ok = torch.zeros(nb, dtype=torch.int32, device="cuda")
+            ok = _zeros(nb, torch.int32)
             with _stage("rr.orth"):
                 _lib.call("cirr_orth_cholqr2", _ptr(W), n, cmax * n, n, cmax, nb, _ptr(cdim), _CHOLQR_KAPPA,
                           _ptr(Qt), n, cmax * n, _ptr(ws), _ptr(ok), st)
@@ -889,9 +987,9 @@ class _Engine:
         sigma = torch.empty((nb, cmax), dtype=torch.float64, device="cuda")
         order = torch.empty((nb, cmax), dtype=torch.int32, device="cuda")
         kept = torch.empty(nb, dtype=torch.int32, device="cuda")
-        Qt = torch.zeros((nb, cmax, n), dtype=torch.complex128, device="cuda")
+        Qt = _zeros((nb, cmax, n))
         ws = torch.empty(int(_lib.call("cirr_orth_ws_bytes", cmax, nb)), dtype=torch.uint8, device="cuda")
-        sweeps = torch.zeros(1, dtype=torch.int32, device="cuda")
+        sweeps = _zeros(1, torch.int32)
         with _stage("rr.orth"):
             _lib.call("cirr_orth", _ptr(W), n, cmax * n, n, cmax, nb, float(cfg.rank_rel_tol), _ptr(sigma),
                       _ptr(order), _ptr(kept), _ptr(Qt), n, cmax * n, _ptr(ws), _ptr(sweeps), st)
@@ -911,11 +1009,8 @@ class _Engine:
             AQ = torch.empty((nb, n, kmax), dtype=torch.complex128, device="cuda")
             BQ = torch.empty_like(AQ)
             Am, Bm, mstride = self._mats([ci for ci, _ in items])
-            gk = self.dp.gemm_kind
-            _lib.call("cirr_gemm", gk, n, kmax, n, nb, _ptr(Am), n, mstride, _ptr(Q), kmax, n * kmax, _ptr(AQ), kmax,
-                      n * kmax, 1.0, 0, st)
-            _lib.call("cirr_gemm", gk, n, kmax, n, nb, _ptr(Bm), n, mstride, _ptr(Q), kmax, n * kmax, _ptr(BQ), kmax,
-                      n * kmax, 1.0, 0, st)
+            self._gemm_mats(n, kmax, n, nb, Am, mstride, Q, kmax, n * kmax, AQ, kmax, n * kmax)
+            self._gemm_mats(n, kmax, n, nb, Bm, mstride, Q, kmax, n * kmax, BQ, kmax, n * kmax)
             del Am, Bm
             At = torch.empty((nb, kmax, kmax), dtype=torch.complex128, device="cuda")
             Bt = torch.empty_like(At)
@@ -927,8 +1022,8 @@ class _Engine:
         # K6: small eigenproblems
         herm = self.dp.hermitian
         kdim = _h2d(ks.astype(np.int32))
-        info = torch.zeros(nb, dtype=torch.int32, device="cuda")
-        lam = torch.zeros((nb, kmax), dtype=torch.complex128, device="cuda")
+        info = _zeros(nb, torch.int32)
+        lam = _zeros((nb, kmax))
         with _stage("rr.eigvals"):
             general_split = (not herm) and kmax <= 256 and not all_vectors
             if general_split:
@@ -939,9 +1034,7 @@ class _Engine:
                 prev = [getattr(self.cs[ci], "prev_lam", None) for ci, _ in items]
                 if _QR_HINTS and all(p_ is not None for p_ in prev):
                     hld = max(max(int(p_.shape[0]) for p_ in prev), 1)
-                    hint = torch.zeros((nb, hld), dtype=torch.complex128, device="cuda")
-                    for b, p_ in enumerate(prev):
-                        hint[b, : p_.shape[0]].copy_(p_)
+                    hint = _pad_stack([p_[None, :] for p_ in prev], 1, hld).view(nb, hld)
                     hcnt = _h2d(np.array([min(int(p_.shape[0]), 256) for p_ in prev], dtype=np.int32))
                     _lib.call("cirr_gen_eig_values_hinted", _ptr(At), _ptr(Bt), _ptr(kdim), kmax, nb, _ptr(gws),
                               _ptr(lam), _ptr(info), _ptr(hint), _ptr(hcnt), hld, st)
@@ -949,11 +1042,11 @@ class _Engine:
                     _lib.call("cirr_gen_eig_values", _ptr(At), _ptr(Bt), _ptr(kdim), kmax, nb, _ptr(gws), _ptr(lam),
                               _ptr(info), st)
                 for b, (ci, _) in enumerate(items):
-                    self.cs[ci].prev_lam = lam[b, : int(ks[b])].clone()
+                    self.cs[ci].prev_lam = lam[b, : int(ks[b])]   # a view: lam is this round's own buffer
             else:
                 wsb = int(_lib.call("cirr_small_eig_ws_bytes", kmax))
                 ews = torch.empty(nb * ((wsb + 255) // 256 * 256), dtype=torch.uint8, device="cuda")
-                Sv = torch.zeros((nb, kmax, kmax), dtype=torch.complex128, device="cuda")
+                Sv = _zeros((nb, kmax, kmax))
                 _lib.call("cirr_small_eig", 1 if herm else 0, _ptr(At), _ptr(Bt), kmax, kk, _ptr(kdim), kmax, nb,
                           _ptr(ews), _ptr(lam), _ptr(Sv), kmax, kk, _ptr(info), st)
         infos = info.cpu().numpy()
@@ -982,7 +1075,7 @@ class _Engine:
                       n * kmax, 1.0, 0, st)
             for b, (ci, _) in enumerate(items):
                 if ci in out and out[ci][0] == "none":
-                    out[ci] = ("none", X[b, :, : ks[b]].contiguous())
+                    out[ci] = ("none", X[b, :, : ks[b]])
         if not keep_idx:
             return out
         # K7: X = Q s for the inside columns, A X, B X, residuals
@@ -996,8 +1089,8 @@ class _Engine:
             lam_in[b, : len(ix)] = lam_h[b, ix]
         idx_t = _h2d(idx)
         cnt_t = _h2d(cnt)
-        Xi = torch.zeros((nb, n, kin_max), dtype=torch.complex128, device="cuda")
-        Sin = torch.zeros((nb, kmax, kin_max), dtype=torch.complex128, device="cuda")
+        Xi = _zeros((nb, n, kin_max))
+        Sin = _zeros((nb, kmax, kin_max))
         if general_split:
             scr = torch.empty(int(_lib.call("cirr_gen_eig_vec_scratch_bytes", kmax, nb, kin_max)), dtype=torch.uint8,
                               device="cuda")
@@ -1018,7 +1111,7 @@ class _Engine:
         _lib.call("cirr_gemm", 0, n, kin_max, kmax, nb, _ptr(BQ), kmax, n * kmax, _ptr(Sin), kin_max,
                   kmax * kin_max, _ptr(BX), kin_max, n * kin_max, 1.0, 0, st)
         lam_t = _h2d(lam_in)
-        res = torch.zeros((nb, kin_max), dtype=torch.float64, device="cuda")
+        res = _zeros((nb, kin_max), torch.float64)
         _lib.call("cirr_residuals", _ptr(AX), _ptr(BX), kin_max, n * kin_max, n, _ptr(lam_t), kin_max, _ptr(cnt_t),
                   kin_max, nb, _ptr(res), kin_max, st)
         res_h = res.cpu().numpy()
@@ -1028,10 +1121,11 @@ class _Engine:
             lam_b = lam_h[b, ix]
             if herm:
                 lam_b = lam_b.real.copy()
-            xall = X[b, :, : ks[b]].contiguous() if all_vectors else None
+            xall = X[b, :, : ks[b]] if all_vectors else None
             # views into the round's blocks (consumers copy or read them; bmul
             # makes a contiguous copy where a raw pointer is needed)
             out[ci] = ("ok", lam_b, Xi[b, :, :k_in], res_h[b, :k_in].copy(), xall)
+            self.cs[ci].x_base = (Xi, b)           # for the batched read-back of the vectors
             self.cs[ci].bx_dev = BX[b, :, :k_in]   # B X, the next refinement's right-hand side
         return out
 
@@ -1171,19 +1265,28 @@ class _Engine:
                                contour=c.contour, stats=c.stats)
 
     def fetch_vectors(self):
-        """Every finishing contour's Ritz vectors in one device concat and one
-        D2H copy (instead of one synchronising copy per contour)."""
+        """Every finishing contour's Ritz vectors packed by one gather launch
+        and read back with one device-to-host copy (not one per contour)."""
         torch = self.torch
         cs = [c for c in self.cs if not c.done and not getattr(c, "fatal", False)
               and c.lam is not None and getattr(c, "x_dev", None) is not None and c.x_dev.numel()]
         if len(cs) < 2:
             return
-        flat = torch.cat([c.x_dev.reshape(-1) for c in cs]).cpu().numpy()
-        off = 0
+        pieces, off = [], 0
         for c in cs:
-            sz = c.x_dev.numel()
-            c.x_host = flat[off:off + sz].reshape(tuple(c.x_dev.shape))
-            off += sz
+            r, k = c.x_dev.shape
+            pieces.append(_piece(c.x_dev, off, dst_ld=k))   # 1-D destination: entry = element offset
+            c._x_off = off
+            off += r * k
+        flat = torch.empty((off, 1), dtype=torch.complex128, device="cuda")
+        _gather(pieces, flat)
+        host = torch.empty(off, dtype=torch.complex128, pin_memory=True)
+        host.copy_(flat.view(-1), non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        h = host.numpy()
+        for c in cs:
+            r, k = c.x_dev.shape
+            c.x_host = h[c._x_off:c._x_off + r * k].reshape(r, k)
 
     def free(self):
         for name in ("pencils", "maxabs", "ipiv", "perm", "minpiv", "info", "dinv"):

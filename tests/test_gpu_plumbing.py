@@ -1,0 +1,73 @@
+"""The engine's device plumbing (cirr_gather_blocks, cirr_zero, cirr_gemm_ptrs):
+the batched stacks of right-hand sides, moment and basis blocks are built by
+libcirr launches, not PyTorch kernels, and must equal per-block copies."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+from paper_2511_01927_b200 import _lib  # noqa: E402
+from paper_2511_01927_b200 import solvers as S  # noqa: E402
+
+
+def _rand(g, *shape):
+    return torch.complex(torch.randn(*shape, generator=g, dtype=torch.float64),
+                         torch.randn(*shape, generator=g, dtype=torch.float64)).cuda()
+
+
+def test_pad_stack_matches_per_block_copies():
+    """_pad_stack builds the same zero-padded stack as one copy per block,
+    along either axis, with empty blocks and strided (view) blocks."""
+    g = torch.Generator().manual_seed(3)
+    bl = [_rand(g, 5, k) for k in (3, 1, 3, 4, 0)]
+    big = _rand(g, 5, 9)
+    bl.append(big[:, 2:6])                       # a strided view (ld 9)
+    ref = torch.zeros(6, 5, 4, dtype=torch.complex128, device="cuda")
+    for i, b in enumerate(bl):
+        ref[i, :, :b.shape[1]] = b
+    assert torch.equal(S._pad_stack(bl, 1, 4), ref)
+    bl = [_rand(g, k, 6) for k in (2, 5, 2)]
+    ref = torch.zeros(3, 5, 6, dtype=torch.complex128, device="cuda")
+    for i, b in enumerate(bl):
+        ref[i, :b.shape[0]] = b
+    assert torch.equal(S._pad_stack(bl, 0, 5), ref)
+
+
+def test_gather_conj_and_column_offsets():
+    g = torch.Generator().manual_seed(4)
+    a, b = _rand(g, 7, 3), _rand(g, 7, 2)
+    dst = S._zeros((2, 7, 6))
+    S._gather([S._piece(a, 0), S._piece(a, 0, 3, conj=True), S._piece(b, 1, 1)], dst)
+    ref = torch.zeros(2, 7, 6, dtype=torch.complex128, device="cuda")
+    ref[0, :, :3] = a
+    ref[0, :, 3:6] = a.conj()
+    ref[1, :, 1:3] = b
+    assert torch.equal(dst, ref)
+
+
+def test_zero_fill():
+    t = torch.full((3, 5), 7.0 + 1j, dtype=torch.complex128, device="cuda")
+    _lib.call("cirr_zero", t.data_ptr(), t.numel() * 16, torch.cuda.current_stream().cuda_stream)
+    assert not t.abs().sum().item()
+
+
+@pytest.mark.parametrize("kind", [0, 2])
+def test_gemm_ptrs_equals_stacked(kind):
+    """cirr_gemm_ptrs (A of entry b at an address) equals cirr_gemm on a
+    stacked copy of the same matrices, bit for bit."""
+    g = torch.Generator().manual_seed(5)
+    n, k, nb = 70, 9, 4
+    mats = [(_rand(g, n, n) if kind == 0 else torch.randn(n, n, generator=g, dtype=torch.float64).cuda())
+            for _ in range(nb)]
+    B = _rand(g, nb, n, k)
+    st = torch.cuda.current_stream().cuda_stream
+    C1 = torch.empty(nb, n, k, dtype=torch.complex128, device="cuda")
+    C2 = torch.empty_like(C1)
+    A = torch.stack(mats)
+    _lib.call("cirr_gemm", kind, n, k, n, nb, A.data_ptr(), n, n * n, B.data_ptr(), k, n * k, C1.data_ptr(), k, n * k,
+              1.0, 0, st)
+    ptrs = torch.tensor([m.data_ptr() for m in mats], dtype=torch.int64, device="cuda")
+    _lib.call("cirr_gemm_ptrs", kind, n, k, n, nb, ptrs.data_ptr(), n, B.data_ptr(), k, n * k, C2.data_ptr(), k,
+              n * k, 1.0, 0, st)
+    assert torch.equal(C1, C2)

@@ -147,23 +147,6 @@ def test_contains_many_matches_contains():
             assert np.array_equal(got, want)
 
 
-def test_pad_stack_matches_per_block_copies():
-    """_pad_stack (grouped by width) builds the same zero-padded stack as one
-    copy per block, along either axis, with empty blocks."""
-    import torch
-    g = torch.Generator().manual_seed(3)
-    bl = [torch.randn(5, k, dtype=torch.complex128, generator=g) for k in (3, 1, 3, 4, 0)]
-    ref = torch.zeros(5, 5, 4, dtype=torch.complex128)
-    for i, b in enumerate(bl):
-        ref[i, :, :b.shape[1]] = b
-    assert torch.equal(S._pad_stack(bl, 1, 4), ref)
-    bl = [torch.randn(k, 6, dtype=torch.complex128, generator=g) for k in (2, 5, 2)]
-    ref = torch.zeros(3, 5, 6, dtype=torch.complex128)
-    for i, b in enumerate(bl):
-        ref[i, :b.shape[0]] = b
-    assert torch.equal(S._pad_stack(bl, 0, 5), ref)
-
-
 def test_single_moment_coefficients_bitwise():
     """The moments == 1 fast path equals the sequential-power loop bit for bit."""
     for shape in ("circle", "ellipse"):
