@@ -132,6 +132,36 @@ def contains_many(c, zs, slack: float = 0.0) -> np.ndarray:
             & (c.im_min - slack < z.imag) & (z.imag < c.im_max + slack))
 
 
+def contains_rows(contours: list, zs: np.ndarray, counts) -> np.ndarray:
+    """contains_many for many contours at once: row b of zs (first counts[b]
+    entries) against contours[b]; the same float64 arithmetic per element."""
+    z = np.asarray(zs, dtype=np.complex128)
+    nb, k = z.shape
+    out = np.zeros((nb, k), dtype=bool)
+    valid = np.arange(k)[None, :] < np.asarray(counts)[:, None]
+    shapes = np.array([c.shape for c in contours])
+    for shape in set(shapes.tolist()):
+        rows = np.flatnonzero(shapes == shape)
+        cs = [contours[r] for r in rows]
+        zz = z[rows]
+        cen = np.array([complex(c.center) for c in cs]) if shape != "rect" else None
+        if shape == "circle":
+            d = zz - cen[:, None]
+            m = np.hypot(d.real, d.imag) < np.array([c.radius for c in cs])[:, None]
+        elif shape == "ellipse":
+            dr = (zz.real - cen.real[:, None]) / np.array([c.semi_re for c in cs])[:, None]
+            di = (zz.imag - cen.imag[:, None]) / np.array([c.semi_im for c in cs])[:, None]
+            m = dr * dr + di * di < 1.0
+        else:
+            lo_r = np.array([c.re_min for c in cs])[:, None]
+            hi_r = np.array([c.re_max for c in cs])[:, None]
+            lo_i = np.array([c.im_min for c in cs])[:, None]
+            hi_i = np.array([c.im_max for c in cs])[:, None]
+            m = (lo_r < zz.real) & (zz.real < hi_r) & (lo_i < zz.imag) & (zz.imag < hi_i)
+        out[rows] = m
+    return out & valid
+
+
 @dataclass(frozen=True)
 class QuadratureRule:
     """sum_j w_j f(z_j) approximates (1/2 pi i) \\oint f(z) dz (contours.py:127-137)."""

@@ -27,7 +27,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .contours import QuadratureRule, contains, contains_many, moment_frame, quadrature_for
+from .contours import QuadratureRule, contains, contains_many, contains_rows, moment_frame, quadrature_for
 from .errors import (
     ConvergenceError,
     DeviceError,
@@ -1051,23 +1051,24 @@ class _Engine:
                           _ptr(ews), _ptr(lam), _ptr(Sv), kmax, kk, _ptr(info), st)
         infos = info.cpu().numpy()
         lam_h = lam.cpu().numpy()
+        # solvers.py:161-162 for every contour of the round in one pass
+        inside = contains_rows([self.cs[ci].contour for ci, _ in items], lam_h.real + 0j if herm else lam_h, ks)
+        inside[infos != 0] = False
+        n_in = inside.sum(axis=1)
+        order = np.argsort(~inside, axis=1, kind="stable")   # inside columns first, in index order
         keep_idx = {}
         for b, (ci, _) in enumerate(items):
             if infos[b] > 0:
                 msg = "projected B is not positive definite" if herm else "projected B is singular"
                 out[ci] = ("indefinite", IndefiniteBError(msg))
-                continue
-            if infos[b] < 0:
+            elif infos[b] < 0:
                 # this contour's projected QR did not converge: a per-contour
                 # ConvergenceError (isolated by solve_multi), not a process error
                 out[ci] = ("qrfail", None)
-                continue
-            lb = lam_h[b, : ks[b]]
-            keep = contains_many(self.cs[ci].contour, lb.real + 0j if herm else lb)
-            if not np.any(keep):
+            elif n_in[b] == 0:
                 out[ci] = ("none", None)
-                continue
-            keep_idx[b] = np.nonzero(keep)[0]
+            else:
+                keep_idx[b] = order[b, : n_in[b]]
         X = None
         if all_vectors:
             X = torch.empty((nb, n, kmax), dtype=torch.complex128, device="cuda")
@@ -1079,14 +1080,11 @@ class _Engine:
         if not keep_idx:
             return out
         # K7: X = Q s for the inside columns, A X, B X, residuals
-        kin_max = max(len(v) for v in keep_idx.values())
-        idx = np.zeros((nb, kin_max), dtype=np.int32)
-        cnt = np.zeros(nb, dtype=np.int32)
-        lam_in = np.zeros((nb, kin_max), dtype=np.complex128)
-        for b, ix in keep_idx.items():
-            idx[b, : len(ix)] = ix
-            cnt[b] = len(ix)
-            lam_in[b, : len(ix)] = lam_h[b, ix]
+        kin_max = int(n_in.max())
+        cnt = np.where(np.isin(np.arange(nb), list(keep_idx)), n_in, 0).astype(np.int32)
+        valid = np.arange(kin_max)[None, :] < cnt[:, None]
+        idx = np.where(valid, order[:, :kin_max], 0).astype(np.int32)
+        lam_in = np.where(valid, np.take_along_axis(lam_h, idx, axis=1), 0)
         idx_t = _h2d(idx)
         cnt_t = _h2d(cnt)
         Xi = _zeros((nb, n, kin_max))

@@ -201,3 +201,21 @@ def test_waves_cap_pencils_per_wave():
     # the byte budget counts the factor, its diagonal inverses and LU workspace
     per = 64 * 64 * 16
     assert len(S._waves([_FakeContour(32), _FakeContour(32)], 64, 64 * per + 1)) == 2
+
+
+def test_contains_rows_equals_contains_many():
+    """The batched containment of a Rayleigh-Ritz round equals contains_many
+    per contour (same arithmetic), for every shape, honouring the counts."""
+    from paper_2511_01927_b200.contours import contains_many, contains_rows
+    rng = np.random.default_rng(7)
+    cs = [Contour(shape="circle", center=0.1 + 0.2j, radius=0.5),
+          Contour(shape="ellipse", center=-0.3 + 0j, semi_re=0.4, semi_im=0.2),
+          Contour(shape="rect", re_min=-0.5, re_max=0.5, im_min=-0.1, im_max=0.3),
+          Contour(shape="circle", center=1.0 + 0j, radius=0.25)]
+    z = rng.uniform(-1.2, 1.2, (4, 50)) + 1j * rng.uniform(-0.6, 0.6, (4, 50))
+    counts = [50, 17, 0, 33]
+    got = contains_rows(cs, z, counts)
+    for b, c in enumerate(cs):
+        ref = contains_many(c, z[b])
+        ref[counts[b]:] = False
+        assert np.array_equal(got[b], ref)
