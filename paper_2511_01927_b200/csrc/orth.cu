@@ -568,17 +568,36 @@ __global__ void __launch_bounds__(CT) chol_inv_smem_kernel(cplx* __restrict__ Ga
     if (tid == 0) ok[p] = 0;
     return;
   }
-  // column j of R^-1 (rows 0..j) into G[.][j]: back substitution, one thread per column
+  // R moves to the (dense, upper part of the) Gram buffer G, and its shared
+  // memory now holds X = R^-1, packed: column j of X (rows 0..j) by back
+  // substitution in thread j, reading x_k from shared memory (the previous
+  // version re-read its own results from global memory: one dependent L2 round
+  // trip per multiply-add, ~1 ms per 118 x 118 factor)
+  for (int e = tid; e < c * c; e += CT) {
+    const int i = e / c, k = e % c;
+    if (k >= i) G[(long long)i * cmax + k] = R[pk(i, k, c)];
+  }
+  __syncthreads();
+  cplx* X = R;
   for (int j = tid; j < c; j += CT) {
     for (int i = j; i >= 0; --i) {
-      double ar = (i == j) ? 1.0 : 0.0, ai = 0.0;
-      const int base = pk(i, 0, c);         // R[i][k] = R[base + k]
-      for (int k = i + 1; k <= j; ++k) {
-        const cplx rk = R[base + k], xk = G[(long long)k * cmax + j];
-        ar -= rk.x * xk.x - rk.y * xk.y;
-        ai -= rk.x * xk.y + rk.y * xk.x;
+      const cplx* Ri = G + (long long)i * cmax;
+      double ar0 = (i == j) ? 1.0 : 0.0, ai0 = 0.0, ar1 = 0.0, ai1 = 0.0;
+      int k = i + 1;
+      for (; k + 1 <= j; k += 2) {            // two independent accumulators
+        const cplx r0 = Ri[k], x0 = X[pk(k, j, c)];
+        const cplx r1 = Ri[k + 1], x1 = X[pk(k + 1, j, c)];
+        ar0 -= r0.x * x0.x - r0.y * x0.y;
+        ai0 -= r0.x * x0.y + r0.y * x0.x;
+        ar1 -= r1.x * x1.x - r1.y * x1.y;
+        ai1 -= r1.x * x1.y + r1.y * x1.x;
       }
-      G[(long long)i * cmax + j] = cscale(cmk(ar, ai), 1.0 / R[base + i].x);
+      if (k <= j) {
+        const cplx r0 = Ri[k], x0 = X[pk(k, j, c)];
+        ar0 -= r0.x * x0.x - r0.y * x0.y;
+        ai0 -= r0.x * x0.y + r0.y * x0.x;
+      }
+      X[pk(i, j, c)] = cscale(cmk(ar0 + ar1, ai0 + ai1), 1.0 / Ri[i].x);
     }
   }
   __syncthreads();
@@ -586,10 +605,10 @@ __global__ void __launch_bounds__(CT) chol_inv_smem_kernel(cplx* __restrict__ Ga
   for (int e = tid; e < c * c; e += CT) {
     const int i = e / c, k = e % c;
     if (k >= i) {
-      const cplx x = G[(long long)i * cmax + k];
+      const cplx x = X[pk(i, k, c)];
       RT[(long long)k * cmax + i] = x;
       b += cabs2(x);
-      a += cabs2(R[pk(i, k, c)]);
+      a += cabs2(G[(long long)i * cmax + k]);
     }
   }
   if (first_pass) {
