@@ -11,6 +11,8 @@
 // everything runs in one cooperative kernel with a software grid barrier
 // between dependent steps; all reductions are fixed-order (bit-reproducible).
 #include "common.cuh"
+#include <cstdlib>
+#include "cirr.h"
 
 namespace {
 
@@ -50,7 +52,8 @@ __global__ void __launch_bounds__(HT) qr_jacobi_kernel(cplx* __restrict__ W, lon
                                                         long long ldq, long long qstride, unsigned* bar,
                                                         int* counters, cplx* __restrict__ Xc,
                                                         cplx* __restrict__ Jt, cplx* __restrict__ tau,
-                                                        int max_sweeps, double tol, int* sweeps_out, int JB) {
+                                                        int max_sweeps, double tol, int* sweeps_out, int JB,
+                                                        int back) {
   __shared__ double red[4][HT / 32];
   __shared__ double sred[32];
   const int G = gridDim.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -248,6 +251,7 @@ __global__ void __launch_bounds__(HT) qr_jacobi_kernel(cplx* __restrict__ W, lon
     }
     __syncthreads();
   }
+  if (!back) return;  // C runs as blocked (WY) GEMMs after this kernel (orth_back_blocked)
   grid_barrier(bar, G);
   // Qt[p][r] = [J[:, order[r]]; 0] for r < kept[p]
   for (long long e = (long long)blockIdx.x * HT + tid; e < (long long)nprob * c * n; e += (long long)G * HT) {
@@ -295,6 +299,113 @@ __global__ void __launch_bounds__(HT) qr_jacobi_kernel(cplx* __restrict__ W, lon
 
 }  // namespace
 
+namespace {
+constexpr int WYB = 32;  // reflectors per WY block
+
+// W[p] (c x n, row j = reflector j below its diagonal, R on and above it) ->
+// V^T in place: zeros before the diagonal, the implicit unit on it.
+__global__ void wy_prep_kernel(cplx* __restrict__ W, long long ldw, long long wstride, int n, int c) {
+  const int p = blockIdx.z, j = blockIdx.y;
+  cplx* row = W + (long long)p * wstride + (long long)j * ldw;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= j && i < n; i += gridDim.x * blockDim.x)
+    row[i] = cmk(i == j ? 1.0 : 0.0, 0.0);
+}
+
+// X[p] (n x c, row-major): X[i][r] = J[i][order[r]] for i < c and r < kept[p], else 0.
+__global__ void wy_init_x_kernel(const cplx* __restrict__ Jt, const int* __restrict__ order,
+                                 const int* __restrict__ kept, int n, int c, cplx* __restrict__ X) {
+  const int p = blockIdx.z, i = blockIdx.y;
+  const long long cc = (long long)c * c;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < c; r += gridDim.x * blockDim.x) {
+    cplx v = cmk(0.0, 0.0);
+    if (i < c && r < kept[p]) v = Jt[(long long)p * cc + (long long)order[(long long)p * c + r] * c + i];
+    X[(long long)p * n * c + (long long)i * c + r] = v;
+  }
+}
+
+// T of one block (LAPACK larft, forward, columnwise): T[i][i] = tau_i,
+// T[0:i, i] = -tau_i T[0:i, 0:i] G[0:i, i] with G = V^H V (WYB x WYB).
+__global__ void wy_tfac_kernel(const cplx* __restrict__ Gm, const cplx* __restrict__ tau, int c, int j0, int nb,
+                               cplx* __restrict__ T) {
+  const int p = blockIdx.x, t = threadIdx.x;
+  const cplx* G = Gm + (long long)p * WYB * WYB;
+  const cplx* tp = tau + (long long)p * c + j0;
+  __shared__ cplx sT[WYB][WYB + 1];
+  for (int e = t; e < WYB * WYB; e += blockDim.x) sT[e / WYB][e % WYB] = cmk(0.0, 0.0);
+  __syncthreads();
+  for (int i = 0; i < nb; ++i) {
+    const cplx ti = tp[i];
+    cplx acc = cmk(0.0, 0.0);
+    if (t < i)
+      for (int l = t; l < i; ++l) cfma(acc, sT[t][l], G[(long long)l * WYB + i]);
+    __syncthreads();
+    if (t < i) sT[t][i] = cmul(cmk(-ti.x, -ti.y), acc);
+    if (t == i) sT[i][i] = ti;
+    __syncthreads();
+  }
+  cplx* Tp = T + (long long)p * WYB * WYB;
+  for (int e = t; e < WYB * WYB; e += blockDim.x) Tp[e] = sT[e / WYB][e % WYB];
+}
+}  // namespace
+
+// Phase C of cirr_orth as Level-3 products: with V^T = the reflector rows of W
+// (unit diagonal, zeros before it) and X = [J_kept; 0] (n x c), apply the WY
+// blocks from the last to the first, X -= V (T (V^H X)), then Qt = X^T.
+static int orth_back_blocked(cplx* W, long long ldw, long long wstride, int n, int c, int nprob, const int* kept,
+                             const int* order, const cplx* Jt, const cplx* tau, cplx* Qt, long long ldq,
+                             long long qstride, cudaStream_t stream) {
+  const int jmax = c < n ? c : n;
+  {
+    dim3 g(1, c, nprob);
+    wy_prep_kernel<<<g, 256, 0, stream>>>(W, ldw, wstride, n, c);
+    CIRR_CHECK_LAUNCH();
+  }
+  cplx *VT = nullptr, *X = nullptr, *Gm = nullptr, *T = nullptr, *Wk = nullptr, *Wk2 = nullptr;
+  const size_t nc = (size_t)n * c * nprob;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&VT), sizeof(cplx) * nc, stream);
+  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&X), sizeof(cplx) * nc, stream);
+  if (e == cudaSuccess)
+    e = cudaMallocAsync(reinterpret_cast<void**>(&Gm), sizeof(cplx) * (size_t)2 * WYB * WYB * nprob, stream);
+  if (e == cudaSuccess)
+    e = cudaMallocAsync(reinterpret_cast<void**>(&Wk), sizeof(cplx) * (size_t)2 * WYB * c * nprob, stream);
+  if (e != cudaSuccess) return (int)e;
+  T = Gm + (size_t)WYB * WYB * nprob;
+  Wk2 = Wk + (size_t)WYB * c * nprob;
+  const long long sv = (long long)n * c;
+  int rc = cirr_transpose(0, W, ldw, wstride, c, n, nprob, VT, c, sv, stream);   // V (n x c)
+  if (rc == 0) {
+    dim3 g((c + 127) / 128, n, nprob);
+    wy_init_x_kernel<<<g, 128, 0, stream>>>(Jt, order, kept, n, c, X);
+    rc = (int)cudaGetLastError();
+    cirr_note_launch();
+  }
+  const int nblk = (jmax + WYB - 1) / WYB;
+  for (int b = nblk - 1; rc == 0 && b >= 0; --b) {
+    const int j0 = b * WYB, nb = (jmax - j0) < WYB ? (jmax - j0) : WYB;
+    const cplx* Vh = W + (long long)j0 * ldw;   // rows j0.. of V^T (conj -> V^H)
+    // G = V^H V, T (larft)
+    rc = cirr_gemm(1, nb, nb, n, nprob, Vh, ldw, wstride, VT + j0, c, sv, Gm, WYB, WYB * WYB, 1.0, 0, stream);
+    if (rc) break;
+    wy_tfac_kernel<<<nprob, WYB, 0, stream>>>(Gm, tau, c, j0, nb, T);
+    rc = (int)cudaGetLastError();
+    cirr_note_launch();
+    if (rc) break;
+    // X -= V (T (V^H X))
+    rc = cirr_gemm(1, nb, c, n, nprob, Vh, ldw, wstride, X, c, sv, Wk, c, (long long)WYB * c, 1.0, 0, stream);
+    if (rc) break;
+    rc = cirr_gemm(0, nb, c, nb, nprob, T, WYB, WYB * WYB, Wk, c, (long long)WYB * c, Wk2, c, (long long)WYB * c,
+                   1.0, 0, stream);
+    if (rc) break;
+    rc = cirr_gemm(0, n, c, nb, nprob, VT + j0, c, sv, Wk2, c, (long long)WYB * c, X, c, sv, -1.0, 1, stream);
+  }
+  if (rc == 0) rc = cirr_transpose(0, X, c, sv, n, c, nprob, Qt, ldq, qstride, stream);
+  cudaFreeAsync(VT, stream);
+  cudaFreeAsync(X, stream);
+  cudaFreeAsync(Gm, stream);
+  cudaFreeAsync(Wk, stream);
+  return rc;
+}
+
 // Workspace bytes for cirr_orth (barrier/counters, X and J (nprob x c x c),
 // tau and sigma scratch).
 CIRR_API long long cirr_orth_ws_bytes(int c, int nprob) {
@@ -339,12 +450,17 @@ CIRR_API int cirr_orth(cplx* W, long long ldw, long long wstride, int n, int c, 
   // rotation threshold on |x^H y| / (|x||y|) for length-c rows
   double tol = 16.0 * sqrt((double)c) * 1.1102230246251565e-16;
   int max_sweeps = 60;
+  // C (Q = H_0 ... H_{c-1} [J_kept; 0]) as blocked WY products on the DMMA GEMM
+  // for wide blocks; one reflector at a time inside the kernel for narrow ones
+  static const int wy_env = getenv("CIRR_ORTH_WY") ? atoi(getenv("CIRR_ORTH_WY")) : -1;
+  int back = (wy_env >= 0 ? wy_env == 0 : c < 64) ? 1 : 0;
   void* args[] = {&W, &ldw, &wstride, &n, &c, &nprob, &rel_tol, &sigma, &order, &kept, &Qt, &ldq, &qstride,
-                  &bar, &counters, &Xc, &Jt, &tau, &max_sweeps, &tol, &sweeps_out, &jb};
+                  &bar, &counters, &Xc, &Jt, &tau, &max_sweeps, &tol, &sweeps_out, &jb, &back};
   e = cudaLaunchCooperativeKernel((void*)qr_jacobi_kernel, dim3(grid), dim3(HT), args, jsmem, stream);
   cirr_note_launch();
   if (e != cudaSuccess) return (int)e;
-  return 0;
+  if (back) return 0;
+  return orth_back_blocked(W, ldw, wstride, n, c, nprob, kept, order, Jt, tau, Qt, ldq, qstride, stream);
 }
 
 // --------------------------------------------------------------------------
