@@ -143,7 +143,8 @@ int cirr_small_eig(int hermitian, const cirr_cplx* At, const cirr_cplx* Bt, long
 /* K6 non-Hermitian (k <= 256): phase 1 eigenvalues (sorted by re, im) of
  * B~^-1 A~ via batched LU/solve, cooperative Hessenberg reduction and an
  * eigenvalue-only QR; phase 2 unit-norm eigenvectors for selected sorted
- * indices by inverse iteration + Householder back-transform. */
+ * indices by inverse iteration + Householder back-transform.  Bt = NULL:
+ * B~ = I (no LU). */
 long long cirr_gen_eig_ws_bytes(int kmax, int nprob);
 long long cirr_gen_eig_vec_scratch_bytes(int kmax, int nprob, int smax);
 int cirr_gen_eig_values(const cirr_cplx* At, const cirr_cplx* Bt, const int* kdim, int kmax, int nprob, void* ws,
@@ -159,6 +160,20 @@ int cirr_gen_eig_vectors(void* ws, const int* kdim, int kmax, int nprob, const c
                          const int* sel_cnt, int smax, void* scratch, cirr_cplx* S, long long lds, long long sS,
                          cudaStream_t stream);
 
+/* K6 non-Hermitian, refinement rounds (solvers.py:200-205 feeding 187-198):
+ * eigenpairs of (A~, B~) from approximate eigenvectors, by Newton refinement of
+ * the eigenbasis on batched DMMA GEMMs and the batched LU/solve instead of the
+ * sequential Hessenberg QR.  W0h[p] (ld ldw, stride sw) = W0^H, e.g. S^H Q for
+ * the refinement block S and its orthonormal basis Q.  lam, S as
+ * cirr_gen_eig_values / cirr_gen_eig_vectors (sorted by (re, im); unit-norm
+ * eigenvectors in that order, all k of them); info: 0 ok, -1 not converged
+ * within max_iter steps or B~ W0 singular (the caller then uses the
+ * QR path for that problem).  ws: cirr_gen_eig_refine_ws_bytes(kmax, nprob). */
+long long cirr_gen_eig_refine_ws_bytes(int kmax, int nprob);
+int cirr_gen_eig_refine(const cirr_cplx* At, const cirr_cplx* Bt, const int* kdim, int kmax, int nprob,
+                        const cirr_cplx* W0h, long long ldw, long long sw, int max_iter, void* ws, cirr_cplx* lam,
+                        cirr_cplx* S, long long lds, long long sS, int* info, cudaStream_t stream);
+
 /* Certified CholeskyQR2 basis (the fast path of cirr_orth for full-rank blocks):
  * W[p] (c x n rows = the columns of S, cdim[p] valid) -> Qt[p] (cdim[p]
  * orthonormal rows spanning range(S), zero rows after); ok[p] = 1 when
@@ -172,6 +187,10 @@ int cirr_orth_cholqr2(const cirr_cplx* W, long long ldw, long long wstride, int 
 
 /* debug: clock64 marks of the last cirr_orth launch (4 entries) */
 int cirr_orth_phases(long long* host_out);
+
+/* debug: of the last cirr_gen_eig_refine, the step at which problems 0..7
+ * converged (-1: not) and the columns the block step replaced (16 ints, host) */
+int cirr_gen_eig_refine_stats(int* host_out);
 
 /* debug: sweeps, rotations and clock64 cycles of the last eigenvalue-QR launch (8 entries) */
 int cirr_gen_eig_qr_stats(long long* host_out);

@@ -53,6 +53,9 @@ SIGNATURES = {
     "cirr_gen_eig_values": [_P, _P, _P, _I, _I, _P, _P, _P, _P],
     "cirr_gen_eig_values_hinted": [_P, _P, _P, _I, _I, _P, _P, _P, _P, _P, _I, _P],
     "cirr_gen_eig_vectors": [_P, _P, _I, _I, _P, _P, _P, _I, _P, _P, _L, _L, _P],
+    "cirr_gen_eig_refine_ws_bytes": [_I, _I],
+    "cirr_gen_eig_refine_stats": [_P],
+    "cirr_gen_eig_refine": [_P, _P, _P, _I, _I, _P, _L, _L, _I, _P, _P, _P, _L, _L, _P, _P],
     "cirr_residuals": [_P, _P, _L, _L, _I, _P, _L, _P, _I, _I, _P, _L, _P],
     "cirr_gather_cols": [_P, _L, _L, _P, _L, _P, _I, _I, _I, _P, _L, _L, _P],
     "cirr_copy_cols": [_P, _L, _L, _P, _P, _P, _I, _I, _I, _P, _L, _L, _P],
@@ -67,9 +70,11 @@ SIGNATURES = {
     "cirr_zero": [_P, _L, _P],
 }
 _RESTYPE = {"cirr_diag_inv_bytes": _L, "cirr_zgetrf_ws_bytes": _L, "cirr_small_eig_ws_bytes": _L, "cirr_launch_count": _L, "cirr_orth_ws_bytes": _L,
-            "cirr_gen_eig_ws_bytes": _L, "cirr_gen_eig_vec_scratch_bytes": _L, "cirr_orth_cholqr2_ws_bytes": _L}
+            "cirr_gen_eig_ws_bytes": _L, "cirr_gen_eig_vec_scratch_bytes": _L, "cirr_orth_cholqr2_ws_bytes": _L,
+            "cirr_gen_eig_refine_ws_bytes": _L}
 _RAW = {"cirr_zgetrs_uses_dinv", "cirr_set_coop_ctas", "cirr_set_gemm_ctas", "cirr_diag_inv_bytes", "cirr_zgetrf_ws_bytes", "cirr_small_eig_ws_bytes", "cirr_launch_count", "cirr_target_sm", "cirr_orth_ws_bytes",
-        "cirr_gen_eig_ws_bytes", "cirr_gen_eig_vec_scratch_bytes", "cirr_orth_cholqr2_ws_bytes"}
+        "cirr_gen_eig_ws_bytes", "cirr_gen_eig_vec_scratch_bytes", "cirr_orth_cholqr2_ws_bytes",
+        "cirr_gen_eig_refine_ws_bytes"}
 
 _lib = None
 

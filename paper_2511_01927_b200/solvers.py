@@ -46,6 +46,10 @@ _CHOLQR = bool(int(__import__("os").environ.get("CIRR_CHOLQR", "1")))
 _CHOLQR_KAPPA = 1e5
 # previous-round eigenvalues as QR shift hints (CIRR_QR_HINTS=0 disables)
 _QR_HINTS = bool(int(__import__("os").environ.get("CIRR_QR_HINTS", "1")))
+# refinement rounds: Newton refinement of the eigenbasis W0 = Q^H S instead of
+# the Hessenberg QR (CIRR_EIG_REFINE=0 disables; non-converged problems fall back)
+_EIG_REFINE = bool(int(__import__("os").environ.get("CIRR_EIG_REFINE", "1")))
+_EIG_REFINE_ITERS = 5
 # launches put the batch (pencils of a wave) on grid.y / grid.z, whose limit
 # is 65535: a wave never holds more pencils than that
 _MAX_WAVE_PENCILS = 65535
@@ -908,6 +912,7 @@ class _Engine:
         ("indefinite", exc)}."""
         with _stage("rr"):
             out = {}
+            self._refine_src = None
             if feast:
                 basis = self._basis_cgs2(items, out)
             else:
@@ -982,6 +987,9 @@ class _Engine:
                 if _DEBUG:
                     print(f"[cirr] orth: c={cmax} nprob={nb} certified CholeskyQR2", flush=True)
                 ks = np.array([S_.shape[0] for _, S_ in items], dtype=np.int64)
+                # full rank: range(Q) = range(S), so Q^H S is an approximate
+                # eigenbasis of the projected pencil (cirr_gen_eig_refine)
+                self._refine_src = W
                 return self._live(items, Qt, ks, out)
         # K4: one-sided Jacobi on all blocks (zero rows pad to cmax and are dropped)
         sigma = torch.empty((nb, cmax), dtype=torch.float64, device="cuda")
@@ -1024,8 +1032,19 @@ class _Engine:
         kdim = _h2d(ks.astype(np.int32))
         info = _zeros(nb, torch.int32)
         lam = _zeros((nb, kmax))
+        Sv = None
         with _stage("rr.eigvals"):
             general_split = (not herm) and kmax <= 256 and not all_vectors
+            if general_split and _EIG_REFINE and self._refine_src is not None:
+                # refinement round: the block's own columns are near eigenvectors
+                Sv = _zeros((nb, kmax, kmax))
+                if self._refine_eig(self._refine_src, Q, At, Bt, kdim, kmax, nb, lam, Sv, info):
+                    general_split = False
+                    for b, (ci, _) in enumerate(items):
+                        self.cs[ci].prev_lam = lam[b, : int(ks[b])]
+                else:
+                    Sv = None
+                    info = _zeros(nb, torch.int32)
             if general_split:
                 # eigenvalues first; eigenvectors later only for the inside ones
                 gws = torch.empty(int(_lib.call("cirr_gen_eig_ws_bytes", kmax, nb)), dtype=torch.uint8, device="cuda")
@@ -1043,7 +1062,7 @@ class _Engine:
                               _ptr(info), st)
                 for b, (ci, _) in enumerate(items):
                     self.cs[ci].prev_lam = lam[b, : int(ks[b])]   # a view: lam is this round's own buffer
-            else:
+            elif Sv is None:
                 wsb = int(_lib.call("cirr_small_eig_ws_bytes", kmax))
                 ews = torch.empty(nb * ((wsb + 255) // 256 * 256), dtype=torch.uint8, device="cuda")
                 Sv = _zeros((nb, kmax, kmax))
@@ -1126,6 +1145,29 @@ class _Engine:
             self.cs[ci].x_base = (Xi, b)           # for the batched read-back of the vectors
             self.cs[ci].bx_dev = BX[b, :, :k_in]   # B X, the next refinement's right-hand side
         return out
+
+    def _refine_eig(self, S_st, Q, At, Bt, kdim, kmax: int, nb: int, lam, Sv, info) -> bool:
+        """K6 for a refinement round: eigenpairs of (A~, B~) by Newton refinement
+        of W0 = Q^H S (cirr_gen_eig_refine).  S_st: the certified block (nb x
+        kmax x n, the columns of S as rows).  Returns False when any problem did
+        not converge (the caller then runs the QR path for the round)."""
+        torch, n, st = self.torch, self.n, self.stream
+        kk = kmax * kmax
+        W0h = torch.empty((nb, kmax, kmax), dtype=torch.complex128, device="cuda")
+        # S^H Q = conj(S^T) Q: the rows of S_st conjugated times Q (n x kmax)
+        _lib.call("cirr_gemm", 1, kmax, kmax, n, nb, _ptr(S_st), n, kmax * n, _ptr(Q), kmax, n * kmax, _ptr(W0h),
+                  kmax, kk, 1.0, 0, st)
+        ws = torch.empty(int(_lib.call("cirr_gen_eig_refine_ws_bytes", kmax, nb)), dtype=torch.uint8, device="cuda")
+        _lib.call("cirr_gen_eig_refine", _ptr(At), _ptr(Bt), _ptr(kdim), kmax, nb, _ptr(W0h), kmax, kk,
+                  _EIG_REFINE_ITERS, _ptr(ws), _ptr(lam), _ptr(Sv), kmax, kk, _ptr(info), st)
+        inf = info.cpu().numpy()
+        if _DEBUG:
+            import ctypes
+            stats = (ctypes.c_int * 16)()
+            _lib.call("cirr_gen_eig_refine_stats", ctypes.addressof(stats))
+            print(f"[cirr] eig refine k={kmax} nprob={nb} info={inf.tolist()} converged at step "
+                  f"{list(stats[:min(nb, 8)])} block columns {list(stats[8:8 + min(nb, 8)])}", flush=True)
+        return not bool((inf < 0).any())
 
     # -- the reference control flow (solvers.py:165-227) for all contours ----
     def run(self, moments: int):
