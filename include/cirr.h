@@ -36,6 +36,12 @@ typedef double2 cirr_cplx;
 int cirr_assemble(const double* A, const double* B, int n, long long lda,
                   const cirr_cplx* z, int nz, cirr_cplx* pencils, long long ldp,
                   long long pencil_stride, double* maxabs, cudaStream_t stream);
+/* cirr_assemble for pencils of many GEPs in one launch: pencil j uses the real
+ * A, B at device addresses a_ptrs[j], b_ptrs[j] (device int64[nz]); bitwise
+ * equal to cirr_assemble (solve_multi_batch's per-GEP linalg.py:62-63). */
+int cirr_assemble_ptrs(const long long* a_ptrs, const long long* b_ptrs, int n, long long lda,
+                       const cirr_cplx* z, int nz, cirr_cplx* pencils, long long ldp, long long pencil_stride,
+                       double* maxabs, cudaStream_t stream);
 /* Complex-valued A and B (complex128, row-major, ld lda): pencils[j] = z[j] B - A
  * with numpy's complex arithmetic (the reference's MatrixPencil carries complex
  * CSR values, sparse.py:14-43); maxabs as cirr_assemble. */

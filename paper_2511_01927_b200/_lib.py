@@ -26,6 +26,7 @@ SIGNATURES = {
     "cirr_assemble": [_P, _P, _I, _L, _P, _I, _P, _L, _L, _P, _P],
     "cirr_symmetry": [_P, _I, _L, _P, _P],
     "cirr_assemble_c": [_P, _P, _I, _L, _P, _I, _P, _L, _L, _P, _P],
+    "cirr_assemble_ptrs": [_P, _P, _I, _L, _P, _I, _P, _L, _L, _P, _P],
     "cirr_hermitian_c": [_P, _I, _L, _P, _P],
     "cirr_zgetrf_batched": [_P, _I, _L, _L, _I, _P, _P, _P, _P, _P, _P],
     "cirr_zgetrf_ws_bytes": [_I, _I],

@@ -64,6 +64,63 @@ __global__ void __launch_bounds__(kThreads) assemble_kernel(
   }
 }
 
+// As assemble_kernel with the matrices of pencil j at a_ptrs[j], b_ptrs[j]
+// (many GEPs in one launch, solve_multi_batch).  A CTA's group of pencils
+// reloads its chunk of A and B only where the matrix changes from the
+// previous pencil of the group.
+__global__ void __launch_bounds__(kThreads) assemble_ptrs_kernel(
+    const long long* __restrict__ a_ptrs, const long long* __restrict__ b_ptrs, int n, long long lda,
+    const cplx* __restrict__ z, int nz, cplx* __restrict__ P, long long ldp, long long pstride,
+    unsigned long long* __restrict__ maxabs_bits) {
+  __shared__ double wmax[kThreads / 32][kGroup];
+  const long long total = (long long)n * n;
+  const long long base = (long long)blockIdx.x * kChunk;
+  const int j0 = blockIdx.y * kGroup;
+  double a[kPerThread], b[kPerThread];
+  long long dst[kPerThread];
+  const double* Acur = nullptr;
+  const double* Bcur = nullptr;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int g = 0; g < kGroup; ++g) {
+    const int j = j0 + g;
+    if (j >= nz) break;
+    const double* Aj = reinterpret_cast<const double*>(a_ptrs[j]);
+    const double* Bj = reinterpret_cast<const double*>(b_ptrs[j]);
+    if (Aj != Acur || Bj != Bcur) {
+      Acur = Aj;
+      Bcur = Bj;
+#pragma unroll
+      for (int e = 0; e < kPerThread; ++e) {
+        const long long idx = base + (long long)e * kThreads + threadIdx.x;
+        const bool ok = idx < total;
+        const long long r = ok ? idx / n : 0, c = ok ? idx - r * n : 0;
+        dst[e] = ok ? r * ldp + c : -1;
+        a[e] = ok ? Aj[r * lda + c] : 0.0;
+        b[e] = ok ? Bj[r * lda + c] : 0.0;
+      }
+    }
+    const cplx zj = z[j];
+    cplx* Pj = P + (long long)j * pstride;
+    double m = 0.0;
+#pragma unroll
+    for (int e = 0; e < kPerThread; ++e) {
+      if (dst[e] >= 0) {
+        cplx v = cmk(__dsub_rn(__dmul_rn(zj.x, b[e]), a[e]), __dmul_rn(zj.y, b[e]));
+        Pj[dst[e]] = v;
+        m = fmax(m, hypot(v.x, v.y));
+      }
+    }
+    m = warp_max(m);
+    if (lane == 0) wmax[wid][g] = m;
+  }
+  __syncthreads();
+  if (threadIdx.x < kGroup && j0 + threadIdx.x < nz) {
+    double m = 0.0;
+    for (int w = 0; w < kThreads / 32; ++w) m = fmax(m, wmax[w][threadIdx.x]);
+    atomicMax(maxabs_bits + j0 + threadIdx.x, (unsigned long long)__double_as_longlong(m));
+  }
+}
+
 // out[0] = max_ij |A_ij - A_ji|, out[1] = max_ij |A_ij| (as ordered bit patterns)
 __global__ void symmetry_kernel(const double* __restrict__ A, int n, long long lda,
                                 unsigned long long* __restrict__ out) {
@@ -117,6 +174,25 @@ CIRR_API int cirr_assemble(const double* A, const double* B, int n, long long ld
   dim3 grid((unsigned)((total + kChunk - 1) / kChunk), (unsigned)((nz + kGroup - 1) / kGroup));
   assemble_kernel<<<grid, kThreads, 0, stream>>>(A, B, n, lda, z, nz, pencils, ldp, pencil_stride,
                                                   reinterpret_cast<unsigned long long*>(maxabs));
+  CIRR_CHECK_LAUNCH();
+  return 0;
+}
+
+// cirr_assemble for nz pencils whose real A, B (n x n, ld lda) are at the
+// device addresses a_ptrs[j], b_ptrs[j] (device int64[nz]): one launch for the
+// pencils of many GEPs (solve_multi_batch), bitwise equal to cirr_assemble.
+CIRR_API int cirr_assemble_ptrs(const long long* a_ptrs, const long long* b_ptrs, int n, long long lda,
+                                const cplx* z, int nz, cplx* pencils, long long ldp, long long pencil_stride,
+                                double* maxabs, cudaStream_t stream) {
+  if (n <= 0 || nz <= 0 || lda < n || ldp < n || a_ptrs == nullptr || b_ptrs == nullptr) return CIRR_EINVAL;
+  cudaError_t e = cudaMemsetAsync(maxabs, 0, sizeof(double) * nz, stream);
+  if (e != cudaSuccess) return (int)e;
+  const long long total = (long long)n * n;
+  const long long gy = (nz + kGroup - 1) / kGroup;
+  if (gy > 65535) return CIRR_EINVAL;
+  dim3 grid((unsigned)((total + kChunk - 1) / kChunk), (unsigned)gy);
+  assemble_ptrs_kernel<<<grid, kThreads, 0, stream>>>(a_ptrs, b_ptrs, n, lda, z, nz, pencils, ldp, pencil_stride,
+                                                       reinterpret_cast<unsigned long long*>(maxabs));
   CIRR_CHECK_LAUNCH();
   return 0;
 }

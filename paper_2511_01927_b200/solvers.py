@@ -50,6 +50,10 @@ _QR_HINTS = bool(int(__import__("os").environ.get("CIRR_QR_HINTS", "1")))
 # the Hessenberg QR (CIRR_EIG_REFINE=0 disables; non-converged problems fall back)
 _EIG_REFINE = bool(int(__import__("os").environ.get("CIRR_EIG_REFINE", "1")))
 _EIG_REFINE_ITERS = 5
+# large batches (>= _INTERLEAVE_MIN contours in a wave) run as _INTERLEAVE
+# engines on their own streams, interleaved at their host syncs (CIRR_INTERLEAVE=1: one engine)
+_INTERLEAVE = int(__import__("os").environ.get("CIRR_INTERLEAVE", "2"))
+_INTERLEAVE_MIN = 32
 # launches put the batch (pencils of a wave) on grid.y / grid.z, whose limit
 # is 65535: a wave never holds more pencils than that
 _MAX_WAVE_PENCILS = 65535
@@ -394,10 +398,29 @@ def _gather(pieces: list, dst):
 
 def _h2d(x: np.ndarray):
     """Host array -> device tensor, stream-ordered on the current stream with no
-    host synchronisation (pinned staging from torch's caching host allocator),
-    so enqueueing never waits for earlier GPU work of that stream."""
+    host synchronisation, so enqueueing never waits for earlier GPU work of
+    that stream.  Small arrays (the engine's index arrays, coefficients and
+    descriptors) go straight from pageable memory: cudaMemcpyAsync stages them
+    and returns without a device sync (6 us on the B200 boxes, against 12 us
+    for pin_memory()); larger ones through pinned staging."""
     torch = _torch()
-    return torch.from_numpy(np.ascontiguousarray(x)).pin_memory().to("cuda", non_blocking=True)
+    x = np.ascontiguousarray(x)
+    if x.nbytes <= 65536:
+        return torch.from_numpy(x).to("cuda", non_blocking=True)
+    return torch.from_numpy(x).pin_memory().to("cuda", non_blocking=True)
+
+
+def _drain(gen):
+    """Run an engine generator to completion and return its value.  The
+    engine's phases are generators that yield just before each blocking
+    device-to-host read: alone they run straight through (this), and two
+    engines on their own streams can be interleaved (_interleave) so one's
+    host work overlaps the other's queued GPU work."""
+    while True:
+        try:
+            next(gen)
+        except StopIteration as e:
+            return e.value
 
 
 # ---------------------------------------------------------------------------
@@ -625,23 +648,6 @@ class _Engine:
         self.contour_of = _h2d(
             np.concatenate([np.full(len(c.fidx), i, dtype=np.int32) for i, c in enumerate(self.cs)]))
 
-    def _check_factor(self, ci: int):
-        """Singular-shift test of contour ci (linalg.py:68-70); host sync on
-        the current stream."""
-        c = self.cs[ci]
-        a, b = self.node_off[ci], self.node_off[ci + 1]
-        maxabs = self.maxabs[a:b].cpu().numpy()
-        minpiv = self.minpiv[a:b].cpu().numpy()
-        info = self.info[a:b].cpu().numpy()
-        c.stats.n_factorizations = len(c.fidx)
-        for jl in range(b - a):
-            scale = max(maxabs[jl], 1e-300)
-            if info[jl] != 0 or not (minpiv[jl] >= PIVOT_REL_TOL * scale):
-                jn = int(c.fidx[jl])
-                c.error = SingularShiftError(complex(c.nodes[jn]), node_index=jn)
-                c.done = True
-                break
-
     def _factor_range(self, a: int, b: int, nodes: np.ndarray):
         """Enqueue K1 + K2 for pencils
         a..b-1 (shifts `nodes`) on the current stream, as one batched call: the
@@ -653,8 +659,17 @@ class _Engine:
             return
         z = _h2d(nodes)
         with _stage("assemble"):
-            for lo, hi, d in self._pencil_runs(a, b):
-                d.assemble(z[lo - a:], hi - lo, self.pencils[lo], self.maxabs[lo:], self.stream)
+            runs = self._pencil_runs(a, b)
+            if len(runs) > 2 and not self.dp.complex:
+                # many GEPs (solve_multi_batch): one launch over all of them
+                ap = np.concatenate([np.full(hi - lo, d.a.data_ptr(), dtype=np.int64) for lo, hi, d in runs])
+                bp = np.concatenate([np.full(hi - lo, d.b.data_ptr(), dtype=np.int64) for lo, hi, d in runs])
+                ptrs = _h2d(np.stack([ap, bp]))
+                _lib.call("cirr_assemble_ptrs", _ptr(ptrs[0]), _ptr(ptrs[1]), n, n, _ptr(z), cnt,
+                          _ptr(self.pencils[a]), n, n * n, _ptr(self.maxabs[a:]), self.stream)
+            else:
+                for lo, hi, d in runs:
+                    d.assemble(z[lo - a:], hi - lo, self.pencils[lo], self.maxabs[lo:], self.stream)
         _work("assemble_bytes", cnt * n * n * 16 + 2 * n * n * 8)
         with _stage("lu"):
             lws = torch.empty(int(_lib.call("cirr_zgetrf_ws_bytes", n, cnt)), dtype=torch.uint8, device="cuda")
@@ -671,25 +686,30 @@ class _Engine:
         """K1 + K2 for the wave, then the singular-shift test (one read-back).
         sources: also enqueue the CIRR source blocks B V before that read-back,
         so their host-side generation overlaps the factorisation."""
+        return _drain(self.factor_g(sources))
+
+    def factor_g(self, sources: bool = False):
         self._alloc_factors()
         self._factor_range(0, self.P, np.concatenate([c.nodes[c.fidx] for c in self.cs]))
         if sources:
             self._src = self.source_blocks(list(range(len(self.cs))))
-        if len(self.cs) == 1:
-            self._check_factor(0)
-            return
-        # one read-back for every contour of the wave
+        yield
+        # one read-back for every contour of the wave; linalg.py:68-70 on all
+        # pencils at once, the first failing node of each contour reported
         maxabs, minpiv, info = (t.cpu().numpy() for t in (self.maxabs, self.minpiv, self.info))
+        bad = (info != 0) | ~(minpiv >= PIVOT_REL_TOL * np.maximum(maxabs, 1e-300))
         for ci, c in enumerate(self.cs):
-            a = self.node_off[ci]
             c.stats.n_factorizations = len(c.fidx)
-            for jl in range(len(c.fidx)):
-                scale = max(maxabs[a + jl], 1e-300)
-                if info[a + jl] != 0 or not (minpiv[a + jl] >= PIVOT_REL_TOL * scale):
-                    jn = int(c.fidx[jl])
-                    c.error = SingularShiftError(complex(c.nodes[jn]), node_index=jn)
-                    c.done = True
-                    break
+        seen = set()
+        for j in np.flatnonzero(bad):
+            ci = int(np.searchsorted(self.node_off, j, side="right")) - 1
+            if ci in seen:
+                continue
+            seen.add(ci)
+            c = self.cs[ci]
+            jn = int(c.fidx[j - self.node_off[ci]])
+            c.error = SingularShiftError(complex(c.nodes[jn]), node_index=jn)
+            c.done = True
 
     # -- K3: solve all pencils of the listed contours against per-contour RHS
     def apply(self, active: list, rhs: dict, moments: int, real_rhs: bool = False) -> dict:
@@ -893,7 +913,17 @@ class _Engine:
         if not self.multi or len(widths) != 1:
             return {ci: self.bmul(_h2d(vs[ci].astype(complex)), ci) for ci in active}
         k = widths.pop()
-        V = _h2d(np.stack([vs[ci] for ci in active]).astype(complex))
+        # solve_multi's seeds (seed + i) repeat across the GEPs of a batch:
+        # upload each distinct block once and expand on the device
+        keys = {}
+        for ci in active:
+            keys.setdefault(id(vs[ci]), (len(keys), vs[ci]))
+        if len(keys) < len(active) and k:
+            U = _h2d(np.stack([v for _, v in keys.values()]).astype(complex))
+            V = torch.empty((len(active), n, k), dtype=torch.complex128, device="cuda")
+            _gather([_piece(U[keys[id(vs[ci])][0]], s) for s, ci in enumerate(active)], V)
+        else:
+            V = _h2d(np.stack([vs[ci] for ci in active]).astype(complex))
         _, B, stride = self._mats(active)
         out = torch.empty((len(active), n, k), dtype=torch.complex128, device="cuda")
         if k:
@@ -902,6 +932,9 @@ class _Engine:
 
     # -- K4..K7 for one contour --------------------------------------------
     def rayleigh_ritz(self, items: list, feast: bool = False, refine: bool = False) -> dict:
+        return _drain(self.rayleigh_ritz_g(items, feast, refine))
+
+    def rayleigh_ritz_g(self, items: list, feast: bool = False, refine: bool = False):
         """K4..K7 for several contours at once (solvers.py:187-198, batched).
 
         items: [(ci, St)] with St the transposed block of contour ci (its columns
@@ -916,11 +949,11 @@ class _Engine:
             if feast:
                 basis = self._basis_cgs2(items, out)
             else:
-                basis = self._basis_svd(items, out, try_cholqr=refine and _CHOLQR)
+                basis = yield from self._basis_svd_g(items, out, try_cholqr=refine and _CHOLQR)
             if basis is None:
                 return out
             items, Qt, ks = basis
-            return self._rr_core(items, Qt, ks, out, all_vectors=feast)
+            return (yield from self._rr_core_g(items, Qt, ks, out, all_vectors=feast))
 
     def _basis_cgs2(self, items: list, out: dict):
         torch, n, cfg, st = self.torch, self.n, self.cfg, self.stream
@@ -955,7 +988,7 @@ class _Engine:
             items = [items[b] for b in live]
         return items, Qt, ks
 
-    def _basis_svd(self, items: list, out: dict, try_cholqr: bool = False):
+    def _basis_svd_g(self, items: list, out: dict, try_cholqr: bool = False):
         torch, n, cfg, st = self.torch, self.n, self.cfg, self.stream
         for ci, S_ in items:
             if S_.shape[0] == 0:
@@ -983,6 +1016,7 @@ class _Engine:
                 sv = [torch.linalg.svdvals(S_.T).cpu().numpy() for _, S_ in items]
                 print(f"[cirr] cholqr2 ok={ok.cpu().numpy().tolist()} kappa={[float(v[0] / v[-1]) for v in sv]}",
                       flush=True)
+            yield
             if cfg.rank_rel_tol * _CHOLQR_KAPPA < 1.0 and bool(ok.cpu().numpy().all()):
                 if _DEBUG:
                     print(f"[cirr] orth: c={cmax} nprob={nb} certified CholeskyQR2", flush=True)
@@ -1001,12 +1035,13 @@ class _Engine:
         with _stage("rr.orth"):
             _lib.call("cirr_orth", _ptr(W), n, cmax * n, n, cmax, nb, float(cfg.rank_rel_tol), _ptr(sigma),
                       _ptr(order), _ptr(kept), _ptr(Qt), n, cmax * n, _ptr(ws), _ptr(sweeps), st)
+        yield
         ks = kept.cpu().numpy()
         if _DEBUG:
             print(f"[cirr] orth: c={cmax} nprob={nb} kept={ks.tolist()} sweeps={int(sweeps.item())}", flush=True)
         return self._live(items, Qt, ks, out)
 
-    def _rr_core(self, items, Qt, ks, out, all_vectors: bool):
+    def _rr_core_g(self, items, Qt, ks, out, all_vectors: bool):
         torch, n, cfg, st = self.torch, self.n, self.cfg, self.stream
         nb = len(items)
         kmax = int(ks.max())
@@ -1038,7 +1073,7 @@ class _Engine:
             if general_split and _EIG_REFINE and self._refine_src is not None:
                 # refinement round: the block's own columns are near eigenvectors
                 Sv = _zeros((nb, kmax, kmax))
-                if self._refine_eig(self._refine_src, Q, At, Bt, kdim, kmax, nb, lam, Sv, info):
+                if (yield from self._refine_eig_g(self._refine_src, Q, At, Bt, kdim, kmax, nb, lam, Sv, info)):
                     general_split = False
                     for b, (ci, _) in enumerate(items):
                         self.cs[ci].prev_lam = lam[b, : int(ks[b])]
@@ -1068,6 +1103,7 @@ class _Engine:
                 Sv = _zeros((nb, kmax, kmax))
                 _lib.call("cirr_small_eig", 1 if herm else 0, _ptr(At), _ptr(Bt), kmax, kk, _ptr(kdim), kmax, nb,
                           _ptr(ews), _ptr(lam), _ptr(Sv), kmax, kk, _ptr(info), st)
+        yield
         infos = info.cpu().numpy()
         lam_h = lam.cpu().numpy()
         # solvers.py:161-162 for every contour of the round in one pass
@@ -1131,6 +1167,7 @@ class _Engine:
         res = _zeros((nb, kin_max), torch.float64)
         _lib.call("cirr_residuals", _ptr(AX), _ptr(BX), kin_max, n * kin_max, n, _ptr(lam_t), kin_max, _ptr(cnt_t),
                   kin_max, nb, _ptr(res), kin_max, st)
+        yield
         res_h = res.cpu().numpy()
         for b, ix in keep_idx.items():
             ci = items[b][0]
@@ -1146,7 +1183,7 @@ class _Engine:
             self.cs[ci].bx_dev = BX[b, :, :k_in]   # B X, the next refinement's right-hand side
         return out
 
-    def _refine_eig(self, S_st, Q, At, Bt, kdim, kmax: int, nb: int, lam, Sv, info) -> bool:
+    def _refine_eig_g(self, S_st, Q, At, Bt, kdim, kmax: int, nb: int, lam, Sv, info):
         """K6 for a refinement round: eigenpairs of (A~, B~) by Newton refinement
         of W0 = Q^H S (cirr_gen_eig_refine).  S_st: the certified block (nb x
         kmax x n, the columns of S as rows).  Returns False when any problem did
@@ -1160,6 +1197,7 @@ class _Engine:
         ws = torch.empty(int(_lib.call("cirr_gen_eig_refine_ws_bytes", kmax, nb)), dtype=torch.uint8, device="cuda")
         _lib.call("cirr_gen_eig_refine", _ptr(At), _ptr(Bt), _ptr(kdim), kmax, nb, _ptr(W0h), kmax, kk,
                   _EIG_REFINE_ITERS, _ptr(ws), _ptr(lam), _ptr(Sv), kmax, kk, _ptr(info), st)
+        yield
         inf = info.cpu().numpy()
         if _DEBUG:
             import ctypes
@@ -1171,6 +1209,14 @@ class _Engine:
 
     # -- the reference control flow (solvers.py:165-227) for all contours ----
     def run(self, moments: int):
+        return _drain(self.run_g(moments))
+
+    def solve_g(self, moments: int):
+        """factor + run as one generator (the interleaved batch path)."""
+        yield from self.factor_g(sources=True)
+        yield from self.run_g(moments)
+
+    def run_g(self, moments: int):
         torch, cfg, n = self.torch, self.cfg, self.n
         active = [i for i, c in enumerate(self.cs) if not c.done]
         if not active:
@@ -1184,7 +1230,7 @@ class _Engine:
             refine = {}
             for ci in active:
                 it_of[ci] = it
-            rr = self.rayleigh_ritz([(ci, stacked[ci]) for ci in active], refine=it > 0)
+            rr = yield from self.rayleigh_ritz_g([(ci, stacked[ci]) for ci in active], refine=it > 0)
             for ci in list(active):
                 c = self.cs[ci]
                 r = rr[ci]
@@ -1219,7 +1265,7 @@ class _Engine:
                 break
             stacked = self.apply(list(refine.keys()), refine, 1)
             active = list(refine.keys())
-        self.fetch_vectors()
+        yield from self.fetch_vectors_g()
         for ci, c in enumerate(self.cs):
             if c.done:
                 continue
@@ -1305,6 +1351,9 @@ class _Engine:
                                contour=c.contour, stats=c.stats)
 
     def fetch_vectors(self):
+        return _drain(self.fetch_vectors_g())
+
+    def fetch_vectors_g(self):
         """Every finishing contour's Ritz vectors packed by one gather launch
         and read back with one device-to-host copy (not one per contour)."""
         torch = self.torch
@@ -1322,6 +1371,7 @@ class _Engine:
         _gather(pieces, flat)
         host = torch.empty(off, dtype=torch.complex128, pin_memory=True)
         host.copy_(flat.view(-1), non_blocking=True)
+        yield
         torch.cuda.current_stream().synchronize()
         h = host.numpy()
         for c in cs:
@@ -1357,9 +1407,26 @@ def _waves(cstates: list, n: int, budget_bytes: int) -> list:
     return waves
 
 
-def _hbm_budget(n: int, cstates: list) -> int:
+_FOREIGN_BYTES = {}
+
+
+def _free_hbm() -> int:
+    """Free device memory for this process's buffers: the device total minus
+    what other users held at the first call (CUDA context, other processes)
+    minus what torch has allocated now.  cudaMemGetInfo runs once per device:
+    it took up to ~50 ms per call on the B200 boxes (a config-2 solve is
+    ~100 ms), and it also misses the blocks torch's allocator has cached."""
     torch = _torch()
-    free, _ = torch.cuda.mem_get_info()
+    dev = torch.cuda.current_device()
+    if dev not in _FOREIGN_BYTES:
+        free, total = torch.cuda.mem_get_info()
+        _FOREIGN_BYTES[dev] = (total, max(total - free - torch.cuda.memory_reserved(dev), 0))
+    total, foreign = _FOREIGN_BYTES[dev]
+    return total - foreign - torch.cuda.memory_allocated(dev)
+
+
+def _hbm_budget(n: int, cstates: list) -> int:
+    free = _free_hbm()
     kmax = max([c.ncols for c in cstates] + [1])
     nodes = sum(len(c.nodes) for c in cstates)
     reserve = 4 << 30
@@ -1375,9 +1442,61 @@ def _run_contours(pencil, contours, cfg, seeds, moments_override=None, solver: s
     return cstates
 
 
+_STREAMS: dict = {}
+
+
+def _interleave(engines, moments: int) -> None:
+    """Run the engines' solve generators round-robin, each on its own stream:
+    while the host does one engine's read-back and bookkeeping, the GPU works
+    through the kernels the other engines have queued (a large batch such as
+    config 2's 512 contours is otherwise host-bound between its syncs)."""
+    torch = _torch()
+    cur = torch.cuda.current_stream()
+    # the same streams every call: torch's caching allocator keeps blocks per
+    # stream, so fresh streams would cudaMalloc the whole wave again
+    pool = _STREAMS.setdefault(torch.cuda.current_device(), [])
+    while len(pool) < len(engines):
+        pool.append(torch.cuda.Stream())
+    streams = pool[:len(engines)]
+    live = []
+    for eng, st in zip(engines, streams):
+        st.wait_stream(cur)          # inputs uploaded on the caller's stream
+        live.append((eng.solve_g(moments), st))
+    try:
+        while live:
+            nxt = []
+            for gen, st in live:
+                with torch.cuda.stream(st):
+                    try:
+                        next(gen)
+                        nxt.append((gen, st))
+                    except StopIteration:
+                        pass
+            live = nxt
+    finally:
+        for st in streams:
+            cur.wait_stream(st)
+    for eng in engines:
+        eng.free()
+
+
+def _interleave_split(wave: list) -> list:
+    """How many engines a wave is split into for _interleave (contiguous runs
+    of contours, so each engine's pencils stay adjacent)."""
+    k = _INTERLEAVE if len(wave) >= _INTERLEAVE_MIN else 1
+    if k <= 1:
+        return [wave]
+    step = -(-len(wave) // k)
+    return [wave[i:i + step] for i in range(0, len(wave), step)]
+
+
 def _run_states(dp, cstates, cfg, moments_override=None, solver: str = "cirr"):
     moments = cfg.n_moments if moments_override is None else moments_override
     for wave in _waves(cstates, dp.n, _hbm_budget(dp.n, cstates)):
+        parts = _interleave_split(wave) if solver == "cirr" else [wave]
+        if len(parts) > 1:
+            _interleave([_Engine(dp, part, cfg) for part in parts], moments)
+            continue
         eng = _Engine(dp, wave, cfg)
         if solver == "feast":
             eng.factor()

@@ -71,3 +71,72 @@ def test_gemm_ptrs_equals_stacked(kind):
     _lib.call("cirr_gemm_ptrs", kind, n, k, n, nb, ptrs.data_ptr(), n, B.data_ptr(), k, n * k, C2.data_ptr(), k,
               n * k, 1.0, 0, st)
     assert torch.equal(C1, C2)
+
+
+def test_assemble_ptrs_bitwise():
+    """cirr_assemble_ptrs (pencils of several GEPs in one launch, matrix per
+    pencil by address) equals cirr_assemble per GEP bit for bit, maxabs too."""
+    rng = np.random.default_rng(3)
+    n, per = 70, [3, 8, 1, 12]          # pencils per GEP; groups of 8 straddle GEPs
+    mats = [(rng.standard_normal((n, n)), rng.standard_normal((n, n))) for _ in per]
+    dev = [(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()) for a, b in mats]
+    z = rng.standard_normal(sum(per)) + 1j * rng.standard_normal(sum(per))
+    zt = torch.from_numpy(z).cuda()
+    P = sum(per)
+    got = torch.empty((P, n, n), dtype=torch.complex128, device="cuda")
+    gmax = torch.empty(P, dtype=torch.float64, device="cuda")
+    ap = np.concatenate([np.full(c, d[0].data_ptr(), np.int64) for c, d in zip(per, dev)])
+    bp = np.concatenate([np.full(c, d[1].data_ptr(), np.int64) for c, d in zip(per, dev)])
+    apt, bpt = torch.from_numpy(ap).cuda(), torch.from_numpy(bp).cuda()
+    st = torch.cuda.current_stream().cuda_stream
+    _lib.call("cirr_assemble_ptrs", apt.data_ptr(), bpt.data_ptr(), n, n, zt.data_ptr(), P, got.data_ptr(), n, n * n,
+              gmax.data_ptr(), st)
+    want = torch.empty_like(got)
+    wmax = torch.empty_like(gmax)
+    o = 0
+    for c, (a, b) in zip(per, dev):
+        _lib.call("cirr_assemble", a.data_ptr(), b.data_ptr(), n, n, zt[o:].data_ptr(), c, want[o].data_ptr(), n,
+                  n * n, wmax[o:].data_ptr(), st)
+        o += c
+    assert torch.equal(got, want)
+    assert torch.equal(gmax, wmax)
+    # and numpy's z*B - A
+    g = got.cpu().numpy()
+    o = 0
+    for c, (a, b) in zip(per, mats):
+        for j in range(c):
+            assert np.array_equal(g[o + j], z[o + j] * b - a)
+        o += c
+
+
+def test_interleaved_batch_equals_one_engine(monkeypatch):
+    """solve_multi_batch over >= 32 contours runs as two engines interleaved at
+    their host syncs on two streams: the same counts, pass numbers and
+    eigenvalues (to rounding: split-K choices depend on the batch size) as one
+    engine, and bitwise repeatable."""
+    import json
+    import os
+    from paper_2511_01927_b200 import Contour, DevicePencil, SolverConfig, solve_multi_batch
+    from paper_2511_01927_b200 import solvers as Sv
+    from paper_2511_01927_b200 import workloads as W
+    fix = np.load(os.path.join(os.path.dirname(__file__), "golden", "oracle_config2.npz"))
+    ng = 24
+    mats = [W.config2_matrices(s) for s in range(ng)]
+    cons = [[Contour.from_json_dict(d) for d in json.loads(str(fix[f"s{s}_contours"]))] for s in range(ng)]
+    cfg = SolverConfig(n_q=16, source_cols=8, n_moments=4)
+    dps = [DevicePencil(a, b, hermitian=True) for a, b in mats]
+    assert len(Sv._interleave_split([None] * 2 * ng)) == 2
+    two = solve_multi_batch(dps, cons, cfg)
+    again = solve_multi_batch(dps, cons, cfg)
+    monkeypatch.setattr(Sv, "_INTERLEAVE", 1)
+    one = solve_multi_batch(dps, cons, cfg)
+    for a, b, c in zip(two, again, one):
+        for ra, rb, rc in zip(a.results, b.results, c.results):
+            assert (ra is None) == (rc is None)
+            if ra is None:
+                continue
+            assert np.array_equal(ra.eigenvalues, rb.eigenvalues)
+            assert np.array_equal(ra.eigenvectors, rb.eigenvectors)
+            assert len(ra.eigenvalues) == len(rc.eigenvalues)
+            assert np.abs(ra.eigenvalues - rc.eigenvalues).max() <= 1e-12 * np.abs(rc.eigenvalues).max()
+            assert ra.stats.iterations == rc.stats.iterations

@@ -17,9 +17,9 @@ def main():
     import torch
     eng_cls = None
     for v in vars(S).values():
-        if isinstance(v, type) and hasattr(v, "_refine_eig"):
+        if isinstance(v, type) and hasattr(v, "_refine_eig_g"):
             eng_cls = v
-    base = eng_cls._refine_eig
+    base = eng_cls._refine_eig_g
 
     def hook(self, S_st, Q, At, Bt, kdim, kmax, nb, lam, Sv, info):
         n = self.n
@@ -41,9 +41,9 @@ def main():
             h = [int((c <= t * scale).sum()) for t in (1e-1, 1e-2, 1e-3, 1e-5, 1e-8, 1e-11)]
             print(f"[stats] k={k} scale={scale:.3f} cols with max|T_ij|/scale <= 1e-1,-2,-3,-5,-8,-11: {h}"
                   f" cond(W)={float(torch.linalg.cond(W)):.2e}", flush=True)
-        return base(self, S_st, Q, At, Bt, kdim, kmax, nb, lam, Sv, info)
+        return (yield from base(self, S_st, Q, At, Bt, kdim, kmax, nb, lam, Sv, info))
 
-    eng_cls._refine_eig = hook
+    eng_cls._refine_eig_g = hook
     sys.path.insert(0, os.path.join(ROOT, "tools"))
     from run_config import main as run
     run(4, reps=1)
