@@ -259,28 +259,54 @@ __global__ void __launch_bounds__(256) trsm_kernel(cplx* __restrict__ P, int n, 
 // Linv[b] = L11^{-1} for the unit-lower 64x64 diagonal block of panel step k
 // (|l_ij| <= 1 under partial pivoting, so the explicit inverse is benign --
 // the MAGMA trtri+gemm approach).  U12 = Linv A12 then runs on the TMA GEMM.
-constexpr int kLinvSmem = NB * (NB + 1) * 16 * 2;
+// Column j of X = L^-1 by forward substitution, x_i = -sum_{j<=k<i} L_ik x_k,
+// four threads per column splitting the k sum (two shuffles combine it): no
+// CTA barrier inside the substitution, and L, X packed lower-triangular in
+// shared memory (66 KB, three CTAs per SM).  The first version ran one
+// row-update sweep per i with a CTA barrier each (63 barriers, 133 KB, one
+// CTA per SM): 2.1 ms per launch on config 2's 8192 pencils.
+constexpr int kLinvSmem = NB * (NB + 1) * 16;   // two packed triangles
+__device__ __forceinline__ int tri(int i) { return i * (i + 1) / 2; }
 __global__ void __launch_bounds__(256) linv_kernel(const cplx* __restrict__ P, long long ld, long long pstride, int k,
                                                    cplx* __restrict__ Linv) {
   extern __shared__ cplx lsm[];
-  cplx(*L)[NB + 1] = reinterpret_cast<cplx(*)[NB + 1]>(lsm);
-  cplx(*X)[NB + 1] = reinterpret_cast<cplx(*)[NB + 1]>(lsm + NB * (NB + 1));
+  cplx* Lp = lsm;                       // L[i][c], c <= i
+  cplx* Xp = lsm + NB * (NB + 1) / 2;   // X[i][c], c <= i
   const cplx* A = P + (long long)blockIdx.x * pstride;
   for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
     const int r = e / NB, c = e % NB;
-    L[r][c] = A[(long long)(k + r) * ld + k + c];
-    X[r][c] = cmk(r == c ? 1.0 : 0.0, 0.0);
+    if (c <= r) {
+      Lp[tri(r) + c] = A[(long long)(k + r) * ld + k + c];
+      Xp[tri(r) + c] = cmk(r == c ? 1.0 : 0.0, 0.0);
+    }
   }
   __syncthreads();
-  // forward substitution on all 64 unit columns at once: thread column c, row group g
-  const int c = threadIdx.x % NB, g = threadIdx.x / NB;
-  for (int i = 0; i < NB - 1; ++i) {
-    const cplx xi = X[i][c];
-    for (int r = i + 1 + g; r < NB; r += 4) cfms(X[r][c], L[r][i], xi);
-    __syncthreads();
+  const int j = threadIdx.x >> 2, q = threadIdx.x & 3;
+  for (int i = 1; i < NB; ++i) {
+    double sr = 0.0, si = 0.0;
+    const cplx* Li = Lp + tri(i);
+    for (int kk = q; kk < i; kk += 4) {
+      if (kk >= j) {
+        const cplx a = Li[kk], x = Xp[tri(kk) + j];
+        sr = fma(a.x, x.x, sr);
+        sr = fma(-a.y, x.y, sr);
+        si = fma(a.x, x.y, si);
+        si = fma(a.y, x.x, si);
+      }
+    }
+    sr += __shfl_xor_sync(0xffffffffu, sr, 1);
+    si += __shfl_xor_sync(0xffffffffu, si, 1);
+    sr += __shfl_xor_sync(0xffffffffu, sr, 2);
+    si += __shfl_xor_sync(0xffffffffu, si, 2);
+    if (q == 0 && i > j) Xp[tri(i) + j] = cmk(-sr, -si);
+    __syncwarp();
   }
+  __syncthreads();
   cplx* out = Linv + (long long)blockIdx.x * NB * NB;
-  for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) out[e] = X[e / NB][e % NB];
+  for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
+    const int r = e / NB, c = e % NB;
+    out[e] = c <= r ? Xp[tri(r) + c] : cmk(0.0, 0.0);
+  }
 }
 
 // perm[i] = source row of row i of P*M (composition of the ipiv interchanges).

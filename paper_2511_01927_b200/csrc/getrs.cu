@@ -150,26 +150,72 @@ __global__ void __launch_bounds__(256, 2) trsm_blocked_kernel(const cplx* __rest
         }
     if (!LOWER && tid < SNB) dinv[tid] = tid < nbi ? crecip(D[pk_tri(tid, tid)]) : cmk(0.0, 0.0);
     __syncthreads();
-    // diagonal solve: thread column c, row group g (a warp reads one D element: broadcast)
-    const int c = tid % SKC, g = tid / SKC;
-    if (LOWER) {
-      for (int i = 0; i < nbi - 1; ++i) {
-        const cplx xi = X[i * SX_LD + c];
-        for (int r = i + 1 + g; r < nbi; r += 8) cfms(X[r * SX_LD + c], D[pk_tri(r, i)], xi);
-        __syncthreads();
+    // diagonal solve without CTA barriers: warp w owns columns 4w .. 4w+3,
+    // lane l rows l and l + 32 in registers; each finished row is broadcast
+    // by a shuffle (the first version ran one CTA barrier per row: 63 per
+    // block, the latency chain of config 2's small solves)
+    {
+      const int cb = warp * 4;
+      if (c0 + cb < K) {
+        cplx xr[2][4];
+#pragma unroll
+        for (int sl = 0; sl < 2; ++sl)
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) xr[sl][cc] = X[(lane + 32 * sl) * SX_LD + cb + cc];
+        if (LOWER) {
+          for (int i = 0; i < nbi - 1; ++i) {
+            const int src = i & 31;
+            const bool hi = i >= 32;
+            cplx xi[4];
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc) {
+              const cplx v = hi ? xr[1][cc] : xr[0][cc];
+              xi[cc] = cmk(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
+            }
+#pragma unroll
+            for (int sl = 0; sl < 2; ++sl) {
+              const int r = lane + 32 * sl;
+              if (r > i && r < nbi) {
+                const cplx d = D[pk_tri(r, i)];
+#pragma unroll
+                for (int cc = 0; cc < 4; ++cc) cfms(xr[sl][cc], d, xi[cc]);
+              }
+            }
+          }
+        } else {
+          for (int i = nbi - 1; i >= 0; --i) {
+            const int src = i & 31;
+            const bool hi = i >= 32;
+            const cplx di = dinv[i];
+            cplx xi[4];
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc) {
+              const cplx v = cmul(hi ? xr[1][cc] : xr[0][cc], di);
+              xi[cc] = cmk(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
+              if (lane == src) {
+                if (hi) xr[1][cc] = xi[cc];
+                else xr[0][cc] = xi[cc];
+              }
+            }
+#pragma unroll
+            for (int sl = 0; sl < 2; ++sl) {
+              const int r = lane + 32 * sl;
+              if (r < i) {
+                const cplx d = D[pk_tri(i, r)];
+#pragma unroll
+                for (int cc = 0; cc < 4; ++cc) cfms(xr[sl][cc], d, xi[cc]);
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int sl = 0; sl < 2; ++sl) {
+          const int r = lane + 32 * sl;
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc)
+            if (r < nbi && c0 + cb + cc < K) Yb[(long long)(i0 + r) * ldy + c0 + cb + cc] = xr[sl][cc];
+        }
       }
-    } else {
-      for (int i = nbi - 1; i >= 0; --i) {
-        const cplx xi = cmul(X[i * SX_LD + c], dinv[i]);
-        __syncthreads();
-        if (g == 0) X[i * SX_LD + c] = xi;
-        for (int r = g; r < i; r += 8) cfms(X[r * SX_LD + c], D[pk_tri(i, r)], xi);
-        __syncthreads();
-      }
-    }
-    for (int e = tid; e < nbi * SKC; e += 256) {
-      int r = e / SKC, cc = e % SKC;
-      if (c0 + cc < K) Yb[(long long)(i0 + r) * ldy + c0 + cc] = X[r * SX_LD + cc];
     }
     __syncthreads();
   }

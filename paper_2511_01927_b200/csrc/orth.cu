@@ -648,7 +648,8 @@ __global__ void __launch_bounds__(CT) chol_inv_smem_kernel(cplx* __restrict__ Ga
   extern __shared__ __align__(16) cplx R[];
   __shared__ double sred[32];
   __shared__ int s_fail;
-  const int p = blockIdx.x, c = cdim[p], tid = threadIdx.x;
+  const int p = blockIdx.x, c = cdim[p], tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  constexpr int NW = CT / 32;
   cplx* G = Gall + (long long)p * cmax * cmax;
   cplx* RT = RinvT_all + (long long)p * cmax * cmax;
   double dmax = 0.0;
@@ -657,8 +658,11 @@ __global__ void __launch_bounds__(CT) chol_inv_smem_kernel(cplx* __restrict__ Ga
     const int i = e / c, k = e % c;
     if (k >= i) R[pk(i, k, c)] = G[(long long)i * cmax + k];
   }
+  for (int e = tid; e < cmax * cmax; e += CT) RT[e] = cmk(0.0, 0.0);
   if (tid == 0) s_fail = (c <= 0);
   __syncthreads();
+  // Cholesky G = R^H R, packed upper rows in shared memory; the trailing
+  // update maps a warp to a row and lanes to its columns (no index division)
   for (int j = 0; j < c; ++j) {
     const double d = R[pk(j, j, c)].x;
     if (!(d > 1e-300 && d > 1e-24 * dmax && d < 1e300)) {
@@ -670,65 +674,63 @@ __global__ void __launch_bounds__(CT) chol_inv_smem_kernel(cplx* __restrict__ Ga
     if (tid == 0) R[pk(j, j, c)] = cmk(r, 0.0);
     for (int i = j + 1 + tid; i < c; i += CT) R[pk(j, i, c)] = cscale(R[pk(j, i, c)], ir);
     __syncthreads();
-    const int rest = c - j - 1;
-    for (int e = tid; e < rest * rest; e += CT) {
-      const int a = j + 1 + e / rest, b = j + 1 + e % rest;
-      if (b < a) continue;
-      cfms(R[pk(a, b, c)], cconj(R[pk(j, a, c)]), R[pk(j, b, c)]);
+    for (int a = j + 1 + wid; a < c; a += NW) {
+      const cplx ca = cconj(R[pk(j, a, c)]);
+      cplx* Ra = R + pk(a, a, c);          // row a from column a
+      const cplx* Rj = R + pk(j, a, c);    // row j from column a
+      for (int b = lane; b < c - a; b += 32) cfms(Ra[b], ca, Rj[b]);
     }
     __syncthreads();
   }
   __syncthreads();
-  for (int e = tid; e < cmax * cmax; e += CT) RT[e] = cmk(0.0, 0.0);
   if (s_fail) {
     if (tid == 0) ok[p] = 0;
     return;
   }
-  // R moves to the (dense, upper part of the) Gram buffer G, and its shared
-  // memory now holds X = R^-1, packed: column j of X (rows 0..j) by back
-  // substitution in thread j, reading x_k from shared memory (the previous
-  // version re-read its own results from global memory: one dependent L2 round
-  // trip per multiply-add, ~1 ms per 118 x 118 factor)
-  for (int e = tid; e < c * c; e += CT) {
-    const int i = e / c, k = e % c;
-    if (k >= i) G[(long long)i * cmax + k] = R[pk(i, k, c)];
-  }
-  __syncthreads();
-  cplx* X = R;
-  for (int j = tid; j < c; j += CT) {
-    for (int i = j; i >= 0; --i) {
-      const cplx* Ri = G + (long long)i * cmax;
-      double ar0 = (i == j) ? 1.0 : 0.0, ai0 = 0.0, ar1 = 0.0, ai1 = 0.0;
-      int k = i + 1;
-      for (; k + 1 <= j; k += 2) {            // two independent accumulators
-        const cplx r0 = Ri[k], x0 = X[pk(k, j, c)];
-        const cplx r1 = Ri[k + 1], x1 = X[pk(k + 1, j, c)];
-        ar0 -= r0.x * x0.x - r0.y * x0.y;
-        ai0 -= r0.x * x0.y + r0.y * x0.x;
-        ar1 -= r1.x * x1.x - r1.y * x1.y;
-        ai1 -= r1.x * x1.y + r1.y * x1.x;
+  double a = 0.0;
+  for (int e = tid; e < c * (c + 1) / 2; e += CT) a += cabs2(R[e]);
+  if (first_pass) a = block_sum(a, sred);
+  // X = R^-1 in place, column by column (R X = I, X upper):
+  // X[0:j, j] = -X[0:j, 0:j] R[0:j, j] / R_jj, X_jj = 1 / R_jj; row i's dot
+  // product in thread i.  The first version solved column j in thread j
+  // reading R from global memory (one dependent L2 round trip per
+  // multiply-add, ~1 ms per 118 x 118 factor on config 4's refinement rounds)
+  for (int j = 0; j < c; ++j) {
+    double sr0 = 0.0, si0 = 0.0, sr1 = 0.0, si1 = 0.0;
+    const int i = tid;
+    if (i < j) {
+      const cplx* Xi = R + pk(i, i, c);     // X[i][k] = Xi[k - i]
+      int k = i;
+      for (; k + 1 < j; k += 2) {
+        const cplx x0 = Xi[k - i], r0 = R[pk(k, j, c)];
+        const cplx x1 = Xi[k + 1 - i], r1 = R[pk(k + 1, j, c)];
+        sr0 = fma(x0.x, r0.x, sr0); sr0 = fma(-x0.y, r0.y, sr0);
+        si0 = fma(x0.x, r0.y, si0); si0 = fma(x0.y, r0.x, si0);
+        sr1 = fma(x1.x, r1.x, sr1); sr1 = fma(-x1.y, r1.y, sr1);
+        si1 = fma(x1.x, r1.y, si1); si1 = fma(x1.y, r1.x, si1);
       }
-      if (k <= j) {
-        const cplx r0 = Ri[k], x0 = X[pk(k, j, c)];
-        ar0 -= r0.x * x0.x - r0.y * x0.y;
-        ai0 -= r0.x * x0.y + r0.y * x0.x;
+      if (k < j) {
+        const cplx x0 = Xi[k - i], r0 = R[pk(k, j, c)];
+        sr0 = fma(x0.x, r0.x, sr0); sr0 = fma(-x0.y, r0.y, sr0);
+        si0 = fma(x0.x, r0.y, si0); si0 = fma(x0.y, r0.x, si0);
       }
-      X[pk(i, j, c)] = cscale(cmk(ar0 + ar1, ai0 + ai1), 1.0 / Ri[i].x);
     }
+    const double inv = 1.0 / R[pk(j, j, c)].x;
+    __syncthreads();
+    if (i < j) R[pk(i, j, c)] = cmk(-(sr0 + sr1) * inv, -(si0 + si1) * inv);
+    if (i == j) R[pk(j, j, c)] = cmk(inv, 0.0);
+    __syncthreads();
   }
-  __syncthreads();
-  double a = 0.0, b = 0.0;
+  double b = 0.0;
   for (int e = tid; e < c * c; e += CT) {
     const int i = e / c, k = e % c;
     if (k >= i) {
-      const cplx x = X[pk(i, k, c)];
+      const cplx x = R[pk(i, k, c)];
       RT[(long long)k * cmax + i] = x;
       b += cabs2(x);
-      a += cabs2(G[(long long)i * cmax + k]);
     }
   }
   if (first_pass) {
-    a = block_sum(a, sred);
     b = block_sum(b, sred);
     if (tid == 0) ok[p] = (sqrt(a) * sqrt(b) <= kappa_max) ? 1 : 0;
   }
