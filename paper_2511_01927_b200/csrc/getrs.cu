@@ -232,7 +232,10 @@ __global__ void __launch_bounds__(256, 2) trsm_blocked_kernel(const cplx* __rest
 constexpr int DB = 128;
 
 // X = T^-1 for the nb x nb (nb <= 64) triangular block in D (smem, ld SD_LD);
-// lower: unit diagonal; X is identity-padded outside nb.  256 threads.
+// lower: unit diagonal; X is identity-padded outside nb.  256 threads: column
+// j of X in four threads that split each dot product (two shuffles combine
+// it), so the substitution needs no CTA barrier (the first version ran one
+// barrier per row, 63 per inverse: config 4's diagonal inverses 8.3 ms).
 template <bool LOWER>
 __device__ void tri_inv64(const cplx* D, cplx* X, cplx* dinv, int nb) {
   const int tid = threadIdx.x;
@@ -242,20 +245,36 @@ __device__ void tri_inv64(const cplx* D, cplx* X, cplx* dinv, int nb) {
   }
   if (!LOWER && tid < nb) dinv[tid] = crecip(D[tid * SD_LD + tid]);
   __syncthreads();
-  const int c = tid % SNB, g = tid / SNB;
+  const int j = tid >> 2, q = tid & 3;
   if (LOWER) {
-    for (int i = 0; i < nb - 1; ++i) {
-      const cplx xi = X[i * SD_LD + c];
-      for (int r = i + 1 + g; r < nb; r += 4) cfms(X[r * SD_LD + c], D[r * SD_LD + i], xi);
-      __syncthreads();
+    for (int i = 1; i < nb; ++i) {
+      double sr = 0.0, si = 0.0;
+      for (int kk = q; kk < i; kk += 4) {
+        if (kk >= j) {
+          const cplx a = D[i * SD_LD + kk], x = X[kk * SD_LD + j];
+          sr = fma(a.x, x.x, sr); sr = fma(-a.y, x.y, sr);
+          si = fma(a.x, x.y, si); si = fma(a.y, x.x, si);
+        }
+      }
+      sr += __shfl_xor_sync(0xffffffffu, sr, 1); si += __shfl_xor_sync(0xffffffffu, si, 1);
+      sr += __shfl_xor_sync(0xffffffffu, sr, 2); si += __shfl_xor_sync(0xffffffffu, si, 2);
+      if (q == 0 && i > j) X[i * SD_LD + j] = cmk(-sr, -si);
+      __syncwarp();
     }
   } else {
     for (int i = nb - 1; i >= 0; --i) {
-      const cplx xi = cmul(X[i * SD_LD + c], dinv[i]);
-      __syncthreads();
-      if (g == 0) X[i * SD_LD + c] = xi;
-      for (int r = g; r < i; r += 4) cfms(X[r * SD_LD + c], D[r * SD_LD + i], xi);
-      __syncthreads();
+      double sr = 0.0, si = 0.0;
+      for (int kk = i + 1 + q; kk < nb; kk += 4) {
+        if (kk <= j) {
+          const cplx a = D[i * SD_LD + kk], x = X[kk * SD_LD + j];
+          sr = fma(a.x, x.x, sr); sr = fma(-a.y, x.y, sr);
+          si = fma(a.x, x.y, si); si = fma(a.y, x.x, si);
+        }
+      }
+      sr += __shfl_xor_sync(0xffffffffu, sr, 1); si += __shfl_xor_sync(0xffffffffu, si, 1);
+      sr += __shfl_xor_sync(0xffffffffu, sr, 2); si += __shfl_xor_sync(0xffffffffu, si, 2);
+      if (q == 0 && i <= j && j < nb) X[i * SD_LD + j] = cmul(cmk((i == j ? 1.0 : 0.0) - sr, -si), dinv[i]);
+      __syncwarp();
     }
   }
   __syncthreads();
