@@ -61,12 +61,58 @@ _MOMENT_CHUNK = 16  # cirr_moments handles up to 16 moments per launch (MAXM)
 
 
 
+_TORCH_OK = None
+
+
 def _torch():
+    global _TORCH_OK
+    if _TORCH_OK is not None:
+        return _TORCH_OK
     import torch
 
     if not torch.cuda.is_available():
         raise DeviceError("CUDA device not available: the CIRR path has no CPU fallback")
+    _TORCH_OK = torch
     return torch
+
+
+class _Cols:
+    """Columns [0, k) of entry b of a (batch, n, K) device block, standing in
+    for the torch view buf[b, :, :k] where the engine only needs its address,
+    shape and strides (a torch view costs ~4 us of Python; config 2 makes two
+    per contour per Rayleigh-Ritz round).  tensor() makes the real view."""
+    __slots__ = ("buf", "b", "k")
+
+    def __init__(self, buf, b: int, k: int):
+        self.buf, self.b, self.k = buf, b, k
+
+    @property
+    def shape(self):
+        return (self.buf.shape[1], self.k)
+
+    def dim(self) -> int:
+        return 2
+
+    def numel(self) -> int:
+        return self.buf.shape[1] * self.k
+
+    def stride(self, d: int) -> int:
+        return self.buf.stride(1) if d == 0 else 1
+
+    def data_ptr(self) -> int:
+        return self.buf.data_ptr() + self.b * self.buf.stride(0) * self.buf.element_size()
+
+    def tensor(self):
+        return self.buf[self.b, :, : self.k]
+
+    def cpu(self):
+        return self.tensor().cpu()
+
+    def contiguous(self):
+        return self.tensor().contiguous()
+
+    def is_contiguous(self) -> bool:
+        return self.k == self.buf.shape[2]
 
 
 # ---------------------------------------------------------------------------
@@ -733,7 +779,7 @@ class _Engine:
         Ks = max(ks)
         r0 = rhs[active[0]]
         if nset == 1 and not cplx_rhs[0] and r0.is_contiguous():
-            R = r0.unsqueeze(0)                                # the block itself
+            R = (r0.tensor() if isinstance(r0, _Cols) else r0).unsqueeze(0)   # the block itself
         else:  # one gather launch (+ a zero fill when widths differ)
             R = _zeros((nset, n, Ks)) if any(k_ < Ks for k_ in ks) else torch.empty(
                 (nset, n, Ks), dtype=torch.complex128, device="cuda")
@@ -1178,9 +1224,8 @@ class _Engine:
             xall = X[b, :, : ks[b]] if all_vectors else None
             # views into the round's blocks (consumers copy or read them; bmul
             # makes a contiguous copy where a raw pointer is needed)
-            out[ci] = ("ok", lam_b, Xi[b, :, :k_in], res_h[b, :k_in].copy(), xall)
-            self.cs[ci].x_base = (Xi, b)           # for the batched read-back of the vectors
-            self.cs[ci].bx_dev = BX[b, :, :k_in]   # B X, the next refinement's right-hand side
+            out[ci] = ("ok", lam_b, _Cols(Xi, b, k_in), res_h[b, :k_in].copy(), xall)
+            self.cs[ci].bx_dev = _Cols(BX, b, k_in)   # B X, the next refinement's right-hand side
         return out
 
     def _refine_eig_g(self, S_st, Q, At, Bt, kdim, kmax: int, nb: int, lam, Sv, info):
@@ -1253,10 +1298,12 @@ class _Engine:
                     continue
                 _, lam, xi, res, _ = r
                 c.lam, c.x_dev, c.res = lam, xi, res
-                c.best_res = min(c.best_res, float(res.max()))
+                rmax = float(res.max())
+                c.rmax = rmax
+                c.best_res = min(c.best_res, rmax)
                 if _DEBUG:
-                    print(f"[cirr] contour {ci} it {it}: inside {len(lam)} max res {res.max():.2e}", flush=True)
-                if res.max() <= cfg.tol or it + 1 >= cfg.max_refine or (
+                    print(f"[cirr] contour {ci} it {it}: inside {len(lam)} max res {rmax:.2e}", flush=True)
+                if rmax <= cfg.tol or it + 1 >= cfg.max_refine or (
                         cfg.early_exit and c.settled(lam, res, cfg.tol)):
                     active.remove(ci)
                     continue
@@ -1340,13 +1387,20 @@ class _Engine:
         x = c.__dict__.pop("x_host", None)
         if x is None:
             x = c.x_dev.cpu().numpy()
-        if res.max() > cfg.tol:  # solvers.py:215-219
+        rmax = getattr(c, "rmax", None)
+        if (float(res.max()) if rmax is None else rmax) > cfg.tol:  # solvers.py:215-219
             conv = res <= cfg.tol
             if not np.any(conv):
                 c.error = ConvergenceError(c.best_res)
                 return
             lam, x, res = lam[conv], x[:, conv], res[conv]
         order = np.argsort(lam)  # solvers.py:220
+        if lam.size < 2 or not np.any(order[1:] < order[:-1]):
+            # already in order (the Hermitian eigenvalues come back ascending):
+            # the same arrays without three fancy-index copies
+            c.result = EigenResult(eigenvalues=lam, eigenvectors=x, residuals=res, contour=c.contour,
+                                   stats=c.stats)
+            return
         c.result = EigenResult(eigenvalues=lam[order], eigenvectors=x[:, order], residuals=res[order],
                                contour=c.contour, stats=c.stats)
 

@@ -63,7 +63,10 @@ def check(a, b, fixture, tag, multi, contours):
         assert ns.max() <= 1e-10, (tag, i, ns.max())
         mine = np.linalg.norm(ax - bx * lam[None, :], axis=0) / (np.linalg.norm(ax, axis=0)
                                                                  + np.abs(lam) * np.linalg.norm(bx, axis=0))
-        assert np.allclose(mine, res.residuals, rtol=1e-6, atol=1e-15)
+        # the reference's own residual metric, recomputed here: equal to 1e-6
+        # relative, or to the evaluation's rounding floor (~n eps, 2e-14 at
+        # n = 256) for pairs converged to machine precision
+        assert np.allclose(mine, res.residuals, rtol=1e-6, atol=2e-14)
         for v in lam:
             assert contours[i].contains(complex(v))
 
