@@ -19,28 +19,37 @@
 namespace {
 
 constexpr int SNB = 64;           // block rows
-constexpr int SKC = 32;           // RHS columns per CTA
+constexpr int SKC = 32;           // RHS columns per CTA (the wide variant)
 constexpr int SBK = 16;           // GEMM k-step
 constexpr int SA_LD = SBK + 4;    // complex per A smem row
-constexpr int SB_LD = SKC + 2;    // complex per B smem row
 constexpr int SD_LD = SNB + 1;    // diagonal block row
-constexpr int SX_LD = SKC + 1;
 constexpr int kStageA = SNB * SA_LD;
-constexpr int kStageB = SBK * SB_LD;
+// The left-looking kernel in two widths: KC = 32 RHS columns per CTA (256
+// threads, 93 KB: two CTAs per SM) and KC = 16 for K <= 16 (128 threads,
+// 68 KB: three CTAs per SM, half the padded DMMA work at config 2's K = 8..16).
 // The diagonal block is kept packed (its triangle only, element (hi, lo) at
 // hi (hi + 1) / 2 + lo) in the cp.async stage area, which is idle while the
-// block is solved: 93 KB per CTA, so two CTAs share an SM.
+// block is solved.
+template <int KC>
+struct SolveCfg {
+  static constexpr int NT = 8 * KC;                 // threads
+  static constexpr int B_LD = KC + 2;               // complex per B smem row
+  static constexpr int X_LD = KC + 1;
+  static constexpr int kStageB = SBK * B_LD;
+  static constexpr int kSmem = (2 * (kStageA + kStageB) + SNB * X_LD + SNB) * 16;
+};
 constexpr int kPackedD = SNB * (SNB + 1) / 2;
-static_assert(kPackedD <= 2 * (kStageA + kStageB), "packed diagonal block must fit the stage area");
-constexpr int kSolveSmem = (2 * (kStageA + kStageB) + SNB * SX_LD + SNB) * 16;
+static_assert(kPackedD <= 2 * (kStageA + SolveCfg<16>::kStageB), "packed diagonal block must fit the stage area");
 __device__ __forceinline__ int pk_tri(int hi, int lo) { return hi * (hi + 1) / 2 + lo; }
 
-template <bool LOWER>
-__global__ void __launch_bounds__(256, 2) trsm_blocked_kernel(const cplx* __restrict__ LU, long long ld,
+template <bool LOWER, int KC>
+__global__ void __launch_bounds__(8 * KC, KC == 32 ? 2 : 3) trsm_blocked_kernel(const cplx* __restrict__ LU, long long ld,
                                                               long long pstride, int n,
                                                               cplx* __restrict__ Y, long long ldy,
                                                               long long ystride, int K,
                                                               const int* __restrict__ pmap) {
+  using CF = SolveCfg<KC>;
+  constexpr int NT = CF::NT, SB_LD = CF::B_LD, SX_LD = CF::X_LD, kStageB = CF::kStageB, SKC_ = KC;
   extern __shared__ __align__(16) cplx ssm[];
   cplx* stA = ssm;                                   // 2 stages
   cplx* stB = ssm + 2 * kStageA;
@@ -48,11 +57,11 @@ __global__ void __launch_bounds__(256, 2) trsm_blocked_kernel(const cplx* __rest
   cplx* X = ssm + 2 * (kStageA + kStageB);           // RHS block
   cplx* dinv = X + SNB * SX_LD;
   const int b = blockIdx.y;
-  const int c0 = blockIdx.x * SKC;
+  const int c0 = blockIdx.x * SKC_;
   const cplx* T = LU + (long long)(pmap ? pmap[b] : b) * pstride;
   cplx* Yb = Y + (long long)b * ystride;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = (warp >> 1) * 16, wn = (warp & 1) * 16;
+  const int wm = (warp / (KC / 16)) * 16, wn = (warp % (KC / 16)) * 16;
   const int nblk = (n + SNB - 1) / SNB;
 
   for (int step = 0; step < nblk; ++step) {
@@ -74,15 +83,15 @@ __global__ void __launch_bounds__(256, 2) trsm_blocked_kernel(const cplx* __rest
       cplx* As = stA + stage * kStageA;
       cplx* Bs = stB + stage * kStageB;
 #pragma unroll
-      for (int t = 0; t < (SNB * SBK) / 256; ++t) {
-        int e = tid + t * 256, r = e / SBK, c = e % SBK;
+      for (int t = 0; t < (SNB * SBK) / NT; ++t) {
+        int e = tid + t * NT, r = e / SBK, c = e % SBK;
         int gr = i0 + r, gc = kbeg + kk + c;
         bool p = r < nbi && gc < kend;
         cp_async16(As + r * SA_LD + c, p ? T + (long long)gr * ld + gc : T, p);
       }
 #pragma unroll
-      for (int t = 0; t < (SBK * SKC) / 256; ++t) {
-        int e = tid + t * 256, r = e / SKC, c = e % SKC;
+      for (int t = 0; t < (SBK * SKC_) / NT; ++t) {
+        int e = tid + t * NT, r = e / SKC_, c = e % SKC_;
         int gr = kbeg + kk + r, gc = c0 + c;
         bool p = gr < kend && gc < K;
         cp_async16(Bs + r * SB_LD + c, p ? Yb + (long long)gr * ldy + gc : Yb, p);
@@ -126,14 +135,14 @@ __global__ void __launch_bounds__(256, 2) trsm_blocked_kernel(const cplx* __rest
       }
     }
     // load the diagonal block's triangle (packed) and the RHS block
-    for (int e = tid; e < SNB * SNB; e += 256) {
+    for (int e = tid; e < SNB * SNB; e += NT) {
       int r = e / SNB, c = e % SNB;
       if (LOWER ? c <= r : r <= c)
         D[LOWER ? pk_tri(r, c) : pk_tri(c, r)] =
             (r < nbi && c < nbi) ? T[(long long)(i0 + r) * ld + i0 + c] : cmk(0.0, 0.0);
     }
-    for (int e = tid; e < SNB * SKC; e += 256) {
-      int r = e / SKC, c = e % SKC;
+    for (int e = tid; e < SNB * SKC_; e += NT) {
+      int r = e / SKC_, c = e % SKC_;
       X[r * SX_LD + c] = (r < nbi && c0 + c < K) ? Yb[(long long)(i0 + r) * ldy + c0 + c] : cmk(0.0, 0.0);
     }
     __syncthreads();
@@ -680,8 +689,14 @@ static int getrs_impl(const cplx* LU, int n, long long ld, long long pencil_stri
   if (K == 0) return 0;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(trsm_blocked_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSolveSmem);
-    cudaFuncSetAttribute(trsm_blocked_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSolveSmem);
+    cudaFuncSetAttribute(trsm_blocked_kernel<true, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         SolveCfg<32>::kSmem);
+    cudaFuncSetAttribute(trsm_blocked_kernel<false, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         SolveCfg<32>::kSmem);
+    cudaFuncSetAttribute(trsm_blocked_kernel<true, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         SolveCfg<16>::kSmem);
+    cudaFuncSetAttribute(trsm_blocked_kernel<false, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         SolveCfg<16>::kSmem);
     attr = true;
   }
   dim3 gp((unsigned)(((long long)n * K + 255) / 256), batch);
@@ -795,11 +810,24 @@ static int getrs_impl(const cplx* LU, int n, long long ld, long long pencil_stri
     }
     return moments_rows(ms, Y, ldy, ystride, n, K, 0, n, stream);
   }
-  dim3 gs((K + SKC - 1) / SKC, batch);
-  trsm_blocked_kernel<true><<<gs, 256, kSolveSmem, stream>>>(LU, ld, pencil_stride, n, Y, ldy, ystride, K, pmap);
-  CIRR_CHECK_LAUNCH();
-  trsm_blocked_kernel<false><<<gs, 256, kSolveSmem, stream>>>(LU, ld, pencil_stride, n, Y, ldy, ystride, K, pmap);
-  CIRR_CHECK_LAUNCH();
+  static const int kc_env = getenv("CIRR_SOLVE_KC") ? atoi(getenv("CIRR_SOLVE_KC")) : 0;
+  if (kc_env == 16 || (kc_env == 0 && K <= 16)) {
+    dim3 gs((K + 15) / 16, batch);
+    trsm_blocked_kernel<true, 16><<<gs, SolveCfg<16>::NT, SolveCfg<16>::kSmem, stream>>>(LU, ld, pencil_stride, n,
+                                                                                        Y, ldy, ystride, K, pmap);
+    CIRR_CHECK_LAUNCH();
+    trsm_blocked_kernel<false, 16><<<gs, SolveCfg<16>::NT, SolveCfg<16>::kSmem, stream>>>(LU, ld, pencil_stride, n,
+                                                                                         Y, ldy, ystride, K, pmap);
+    CIRR_CHECK_LAUNCH();
+  } else {
+    dim3 gs((K + SKC - 1) / SKC, batch);
+    trsm_blocked_kernel<true, 32><<<gs, SolveCfg<32>::NT, SolveCfg<32>::kSmem, stream>>>(LU, ld, pencil_stride, n,
+                                                                                        Y, ldy, ystride, K, pmap);
+    CIRR_CHECK_LAUNCH();
+    trsm_blocked_kernel<false, 32><<<gs, SolveCfg<32>::NT, SolveCfg<32>::kSmem, stream>>>(LU, ld, pencil_stride, n,
+                                                                                         Y, ldy, ystride, K, pmap);
+    CIRR_CHECK_LAUNCH();
+  }
   return moments_rows(ms, Y, ldy, ystride, n, K, 0, n, stream);
 }
 
