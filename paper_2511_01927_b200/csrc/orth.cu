@@ -406,6 +406,216 @@ static int orth_back_blocked(cplx* W, long long ldw, long long wstride, int n, i
   return rc;
 }
 
+// --------------------------------------------------------------------------
+// The same three phases for many small blocks (config 2: 512 blocks of
+// n = 256, c = 32): one CTA per problem with the whole block in shared memory,
+// so no grid barrier is needed (the cooperative kernel spends ~130 of them per
+// call and runs 2.2 ms per 256-block batch there).  Householder QR with a warp
+// per trailing row, one-sided Jacobi on the rows of R (circle method over all
+// c rows, a warp per pair, same rotation formulas and threshold), sort and
+// rank cut, and Q = H_0 ... H_{c-1} [J_kept; 0] with each kept column in the
+// registers of one warp.  Results equal the cooperative kernel's to rounding
+// (the Jacobi pair order differs).
+constexpr int OS_T = 256;
+constexpr int OS_NMAX = 512;          // y[OS_NMAX / 32] per lane in phase C
+__host__ __device__ constexpr long long orth_small_smem(int n, int c) {
+  return (long long)c * n * 16 + 2LL * c * c * 16 + (long long)c * 16 + (long long)c * 8 + (long long)c * 4 + 64;
+}
+
+__global__ void __launch_bounds__(OS_T) orth_small_kernel(cplx* __restrict__ W, long long ldw, long long wstride,
+                                                          int n, int c, double rel_tol, double* __restrict__ sigma,
+                                                          int* __restrict__ order, int* __restrict__ kept,
+                                                          cplx* __restrict__ Qt, long long ldq, long long qstride,
+                                                          int max_sweeps, double tol, int* __restrict__ sweeps_out) {
+  extern __shared__ __align__(16) cplx osm[];
+  cplx* A = osm;                                   // c x n: the columns of S as rows, then reflectors / R
+  cplx* X = A + (long long)c * n;                  // c x c
+  cplx* J = X + (long long)c * c;                  // c x c
+  cplx* tau = J + (long long)c * c;                // c
+  double* sg = reinterpret_cast<double*>(tau + c); // c
+  int* ord = reinterpret_cast<int*>(sg + c);       // c
+  __shared__ double sred[32];
+  __shared__ int s_rot;
+  constexpr int NW = OS_T / 32;
+  const int p = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const cplx* Wp = W + (long long)p * wstride;
+  for (int e = tid; e < c * n; e += OS_T) {
+    const int r = e / n, i = e - r * n;
+    A[e] = Wp[(long long)r * ldw + i];
+  }
+  __syncthreads();
+  const int jmax = min(c, n);
+  // ---- A: Householder QR of S (reflector j in row j of A, R above) ----
+  for (int j = 0; j < jmax; ++j) {
+    cplx* x = A + (long long)j * n;
+    double sq = 0.0;
+    for (int i = j + 1 + tid; i < n; i += OS_T) sq += cabs2(x[i]);
+    sq = block_sum(sq, sred);
+    const cplx alpha = x[j];
+    cplx t = cmk(0.0, 0.0);
+    if (sq != 0.0 || alpha.y != 0.0) {
+      double beta = sqrt(alpha.x * alpha.x + alpha.y * alpha.y + sq);
+      beta = alpha.x >= 0.0 ? -beta : beta;
+      t = cmk((beta - alpha.x) / beta, -alpha.y / beta);
+      const cplx scal = crecip(cmk(alpha.x - beta, alpha.y));
+      for (int i = j + 1 + tid; i < n; i += OS_T) x[i] = cmul(x[i], scal);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      if (sq != 0.0 || alpha.y != 0.0) x[j] = cmk(alpha.x >= 0.0 ? -sqrt(alpha.x * alpha.x + alpha.y * alpha.y + sq)
+                                                                 : sqrt(alpha.x * alpha.x + alpha.y * alpha.y + sq),
+                                                  0.0);
+      tau[j] = t;
+    }
+    if (t.x != 0.0 || t.y != 0.0) {
+      const cplx tc = cconj(t);
+      for (int q = j + 1 + wid; q < c; q += NW) {
+        cplx* y = A + (long long)q * n;
+        double wr = 0.0, wi = 0.0;
+        for (int i = j + lane; i < n; i += 32) {
+          const cplx vi = i == j ? cmk(1.0, 0.0) : x[i];
+          const cplx g = cconjmul(vi, y[i]);
+          wr += g.x;
+          wi += g.y;
+        }
+        wr = warp_sum(wr);
+        wi = warp_sum(wi);
+        const cplx f = cmul(tc, cmk(wr, wi));
+        for (int i = j + lane; i < n; i += 32) {
+          const cplx vi = i == j ? cmk(1.0, 0.0) : x[i];
+          cfms(y[i], vi, f);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // ---- B: one-sided Jacobi on the rows of X = R^H, rotations into J ----
+  for (int e = tid; e < c * c; e += OS_T) {
+    const int a = e / c, i = e - a * c;
+    X[e] = (a <= i && a < jmax) ? cconj(A[(long long)i * n + a]) : cmk(0.0, 0.0);
+    J[e] = cmk(a == i ? 1.0 : 0.0, 0.0);
+  }
+  __syncthreads();
+  const int lp = c + (c & 1);
+  int sweep = 0;
+  for (; sweep < max_sweeps && c > 1; ++sweep) {
+    if (tid == 0) s_rot = 0;
+    __syncthreads();
+    for (int round = 0; round < lp - 1; ++round) {
+      for (int pk = wid; pk < lp / 2; pk += NW) {
+        int a, b2;
+        rr_pair(round, pk, lp, a, b2);
+        if (a >= c || b2 >= c) continue;
+        if (a > b2) { const int tt = a; a = b2; b2 = tt; }
+        cplx* xa = X + (long long)a * c;
+        cplx* xb = X + (long long)b2 * c;
+        double al = 0.0, be = 0.0, gr = 0.0, gi = 0.0;
+        for (int i = lane; i < c; i += 32) {
+          const cplx x = xa[i], y = xb[i];
+          al += cabs2(x);
+          be += cabs2(y);
+          const cplx g = cconjmul(x, y);
+          gr += g.x;
+          gi += g.y;
+        }
+        al = warp_sum(al); be = warp_sum(be); gr = warp_sum(gr); gi = warp_sum(gi);
+        const double ag = hypot(gr, gi);
+        if (al > 0.0 && be > 0.0 && ag > tol * sqrt(al) * sqrt(be)) {
+          const double zeta = (be - al) / (2.0 * ag);
+          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          const double cs = 1.0 / sqrt(1.0 + t * t), sn = t * cs;
+          const cplx se = cmk(sn * gr / ag, sn * gi / ag);
+          const cplx sec = cconj(se);
+          cplx* ja = J + (long long)a * c;
+          cplx* jb = J + (long long)b2 * c;
+          for (int i = lane; i < c; i += 32) {
+            const cplx x = xa[i], y = xb[i];
+            xa[i] = csub(cscale(x, cs), cmul(sec, y));
+            xb[i] = cadd(cmul(se, x), cscale(y, cs));
+            const cplx u = ja[i], w = jb[i];
+            ja[i] = csub(cscale(u, cs), cmul(sec, w));
+            jb[i] = cadd(cmul(se, u), cscale(w, cs));
+          }
+          if (lane == 0) atomicAdd(&s_rot, 1);
+        }
+      }
+      __syncthreads();
+    }
+    if (s_rot == 0) { ++sweep; break; }
+    __syncthreads();
+  }
+  if (tid == 0) atomicMax(sweeps_out, sweep);
+  // ---- C: sigma, descending order, rank cut, Q ----
+  for (int a = wid; a < c; a += NW) {
+    double s2 = 0.0;
+    for (int i = lane; i < c; i += 32) s2 += cabs2(X[(long long)a * c + i]);
+    s2 = warp_sum(s2);
+    if (lane == 0) sg[a] = sqrt(s2);
+  }
+  __syncthreads();
+  double smax = 0.0;
+  for (int a = 0; a < c; ++a) smax = fmax(smax, sg[a]);
+  for (int a = tid; a < c; a += OS_T) {
+    const double sa = sg[a];
+    int rank = 0;
+    for (int b3 = 0; b3 < c; ++b3) {
+      const double sb = sg[b3];
+      rank += (sb > sa) || (sb == sa && b3 < a);
+    }
+    ord[rank] = a;
+    order[(long long)p * c + rank] = a;
+    sigma[(long long)p * c + rank] = sa;
+  }
+  int k = 0;
+  if (smax > 0.0)
+    for (int a = 0; a < c; ++a) k += sg[a] >= rel_tol * smax;
+  if (tid == 0) kept[p] = k;
+  __syncthreads();
+  constexpr int NY = OS_NMAX / 32;
+  for (int r = wid; r < k; r += NW) {
+    const int a = ord[r];
+    cplx y[NY];
+#pragma unroll
+    for (int s2 = 0; s2 < NY; ++s2) {
+      const int i = lane + 32 * s2;
+      y[s2] = (i < c && i < n) ? J[(long long)a * c + i] : cmk(0.0, 0.0);
+    }
+    for (int j = jmax - 1; j >= 0; --j) {
+      const cplx t = tau[j];
+      if (t.x == 0.0 && t.y == 0.0) continue;
+      const cplx* v = A + (long long)j * n;
+      double wr = 0.0, wi = 0.0;
+#pragma unroll
+      for (int s2 = 0; s2 < NY; ++s2) {
+        const int i = lane + 32 * s2;
+        if (i >= j && i < n) {
+          const cplx vi = i == j ? cmk(1.0, 0.0) : v[i];
+          const cplx g = cconjmul(vi, y[s2]);
+          wr += g.x;
+          wi += g.y;
+        }
+      }
+      wr = warp_sum(wr);
+      wi = warp_sum(wi);
+      const cplx f = cmul(t, cmk(wr, wi));
+#pragma unroll
+      for (int s2 = 0; s2 < NY; ++s2) {
+        const int i = lane + 32 * s2;
+        if (i >= j && i < n) {
+          const cplx vi = i == j ? cmk(1.0, 0.0) : v[i];
+          cfms(y[s2], vi, f);
+        }
+      }
+    }
+    cplx* q = Qt + (long long)p * qstride + (long long)r * ldq;
+#pragma unroll
+    for (int s2 = 0; s2 < NY; ++s2) {
+      const int i = lane + 32 * s2;
+      if (i < n) q[i] = y[s2];
+    }
+  }
+}
+
 // Workspace bytes for cirr_orth (barrier/counters, X and J (nprob x c x c),
 // tau and sigma scratch).
 CIRR_API long long cirr_orth_ws_bytes(int c, int nprob) {
@@ -430,6 +640,19 @@ CIRR_API int cirr_orth(cplx* W, long long ldw, long long wstride, int n, int c, 
   cplx* tau = Jt + (long long)nprob * c * c;
   cudaError_t e = cudaMemsetAsync(ws, 0, 4096, stream);
   if (e != cudaSuccess) return (int)e;
+  // many small blocks: one CTA per problem, all in shared memory
+  // (CIRR_ORTH_SMALL=0 forces the cooperative kernel)
+  static const int small_env = getenv("CIRR_ORTH_SMALL") ? atoi(getenv("CIRR_ORTH_SMALL")) : 1;
+  const long long osm = orth_small_smem(n, c);
+  if (small_env != 0 && nprob >= 16 && n <= OS_NMAX && osm <= 200 * 1024) {
+    if ((e = cudaMemsetAsync(sweeps_out, 0, sizeof(int), stream)) != cudaSuccess) return (int)e;
+    cudaFuncSetAttribute(orth_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    const double tol_s = 16.0 * sqrt((double)c) * 1.1102230246251565e-16;
+    orth_small_kernel<<<nprob, OS_T, (size_t)osm, stream>>>(W, ldw, wstride, n, c, rel_tol, sigma, order, kept, Qt,
+                                                            ldq, qstride, 60, tol_s, sweeps_out);
+    CIRR_CHECK_LAUNCH();
+    return 0;
+  }
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

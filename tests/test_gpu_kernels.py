@@ -192,6 +192,44 @@ def test_orth_graded(lib, n, c):
     assert resid <= 1e-12 * ref[0] + (ref[k] if k < c else 0.0)
 
 
+@pytest.mark.parametrize("n,c,nprob", [(256, 32, 40), (300, 17, 16), (64, 64, 20)])
+def test_orth_small_batch(lib, n, c, nprob):
+    """Many small blocks take the one-CTA-per-problem kernel (whole block in
+    shared memory): singular values, rank cut, orthonormality and span against
+    numpy's SVD per problem, graded spectra down to 1e-14 as in test_orth_graded."""
+    rng = np.random.default_rng(n + c)
+    mats, Ws = [], []
+    for p_ in range(nprob):
+        U, _ = np.linalg.qr(rng.standard_normal((n, c)) + 1j * rng.standard_normal((n, c)))
+        V, _ = np.linalg.qr(rng.standard_normal((c, c)) + 1j * rng.standard_normal((c, c)))
+        s = np.logspace(0, -(14 if p_ % 2 else 6), c)
+        s[(s > 2e-13) & (s < 5e-12)] = 1e-11
+        m = (U * s) @ V.conj().T
+        mats.append(m)
+        Ws.append(m.T)
+    W = cuda(np.ascontiguousarray(np.stack(Ws)))
+    sig = torch.empty((nprob, c), dtype=torch.float64, device="cuda")
+    order = torch.empty((nprob, c), dtype=torch.int32, device="cuda")
+    kept = torch.empty(nprob, dtype=torch.int32, device="cuda")
+    Qt = torch.zeros((nprob, c, n), dtype=torch.complex128, device="cuda")
+    ws = torch.empty(lib.call("cirr_orth_ws_bytes", c, nprob), dtype=torch.uint8, device="cuda")
+    sw = torch.zeros(1, dtype=torch.int32, device="cuda")
+    lib.call("cirr_orth", P(W), n, c * n, n, c, nprob, 1e-12, P(sig), P(order), P(kept), P(Qt), n, c * n, P(ws),
+             P(sw), S())
+    ks, got, qs = kept.cpu().numpy(), sig.cpu().numpy(), Qt.cpu().numpy()
+    assert 0 < sw.item() <= 60
+    for p_, m in enumerate(mats):
+        ref = np.linalg.svd(m, compute_uv=False)
+        k = int(ks[p_])
+        assert np.allclose(got[p_], ref, rtol=1e-3, atol=1e-15)
+        assert np.allclose(got[p_, :k], ref[:k], rtol=1e-6, atol=1e-15)
+        assert k == int(np.count_nonzero(ref >= 1e-12 * ref[0]))
+        q = qs[p_, :k].T
+        assert np.abs(q.conj().T @ q - np.eye(k)).max() < 1e-11
+        resid = np.linalg.norm(m - q @ (q.conj().T @ m), 2)
+        assert resid <= 1e-12 * ref[0] + (ref[k] if k < c else 0.0)
+
+
 @pytest.mark.parametrize("kind,M,N,K,batch,beta", [(1, 118, 118, 4096, 2, 0), (1, 70, 33, 2000, 3, 1),
                                                     (2, 4096, 118, 4096, 1, 0), (0, 5, 7, 4096, 1, 1)])
 def test_gemm_splitk(lib, kind, M, N, K, batch, beta):
