@@ -174,6 +174,23 @@ class QuadratureRule:
         return len(self.nodes)
 
 
+_UNIT_NODES: dict = {}
+
+
+def _unit_nodes(n_q: int):
+    """exp(i theta_j), cos theta_j, sin theta_j of the midpoint rule (read-only,
+    memoised per n_q: the same arrays bit for bit, made once instead of per
+    contour -- config 2 builds 512 rules per batch)."""
+    v = _UNIT_NODES.get(n_q)
+    if v is None:
+        theta = 2.0 * np.pi * (np.arange(n_q) + 0.5) / n_q
+        v = (np.exp(1j * theta), np.cos(theta), np.sin(theta))
+        for a in v:
+            a.setflags(write=False)
+        _UNIT_NODES[n_q] = v
+    return v
+
+
 def quadrature_for(contour, n_q: int = 32) -> QuadratureRule:
     """Nodes/weights normalised so sum_j w_j/(z_j - c) -> 1 for an enclosed pole.
 
@@ -185,13 +202,10 @@ def quadrature_for(contour, n_q: int = 32) -> QuadratureRule:
     if n_q < 4 or n_q % 2 != 0:
         raise ParameterError("n_q must be even and >= 4")
     if contour.shape in ("circle", "ellipse"):
-        j = np.arange(n_q)
-        theta = 2.0 * np.pi * (j + 0.5) / n_q
+        rot, ct, st = _unit_nodes(n_q)
         if contour.shape == "circle":
-            rot = np.exp(1j * theta)
             return QuadratureRule(nodes=contour.center + contour.radius * rot,
                                   weights=contour.radius * rot / n_q)
-        ct, st = np.cos(theta), np.sin(theta)
         a, b = contour.semi_re, contour.semi_im
         return QuadratureRule(nodes=contour.center + (a * ct + 1j * b * st),
                               weights=(b * ct + 1j * a * st) / n_q)
