@@ -150,6 +150,38 @@ def test_getrs_gather(lib, n, K, use_dinv):
         assert res < 1e-14, res
 
 
+@pytest.mark.parametrize("n", [70, 256])
+def test_getrf_large_batch_short_panels(lib, n):
+    """Large batches of short panels (config 2's regime: the 128-thread panel,
+    4 CTAs per SM): solutions, pivots and pivot magnitudes as LAPACK's for a
+    sample of the 1024 factors; min |U_ii| as reported."""
+    batch = 1024
+    rng = np.random.default_rng(n + 7)
+    A = rng.standard_normal((batch, n, n)) + 1j * rng.standard_normal((batch, n, n))
+    F = cuda(A.copy())
+    ipiv = torch.empty((batch, n), dtype=torch.int32, device="cuda")
+    perm = torch.empty((batch, n), dtype=torch.int32, device="cuda")
+    mp = torch.empty(batch, dtype=torch.float64, device="cuda")
+    info = torch.empty(batch, dtype=torch.int32, device="cuda")
+    lib.call("cirr_zgetrf_batched", P(F), n, n, n * n, batch, P(ipiv), P(perm), P(mp), P(info), P(ws_lu(n, batch)),
+             S())
+    assert (info.cpu().numpy() == 0).all()
+    K = 5
+    R = rng.standard_normal((1, n, K)) + 1j * rng.standard_normal((1, n, K))
+    rhs_of = cuda(np.zeros(batch, dtype=np.int32))
+    Y = torch.empty((batch, n, K), dtype=torch.complex128, device="cuda")
+    lib.call("cirr_zgetrs_batched", P(F), n, n, n * n, batch, P(perm), P(cuda(R)), K, n * K, P(rhs_of), K, P(Y), K,
+             n * K, 0, S())
+    y, lu, piv_h, mph = Y.cpu().numpy(), F.cpu().numpy(), ipiv.cpu().numpy(), mp.cpu().numpy()
+    for j in list(range(0, batch, 97)) + [batch - 1]:
+        res = np.linalg.norm(A[j] @ y[j] - R[0]) / (np.linalg.norm(A[j]) * np.linalg.norm(y[j]))
+        assert res < 1e-14, (j, res)
+        lu_ref, piv_ref = sla.lu_factor(A[j])
+        assert np.array_equal(piv_h[j], piv_ref), j          # izamax pivoting, first index on ties
+        assert np.allclose(np.abs(np.diag(lu[j])), np.abs(np.diag(lu_ref)), rtol=1e-9)
+        assert mph[j] == pytest.approx(np.abs(np.diag(lu[j])).min())
+
+
 def test_getrf_singular(lib):
     n = 70
     A = np.diag(np.arange(1.0, n + 1)).astype(complex)
