@@ -140,3 +140,32 @@ def test_interleaved_batch_equals_one_engine(monkeypatch):
             assert len(ra.eigenvalues) == len(rc.eigenvalues)
             assert np.abs(ra.eigenvalues - rc.eigenvalues).max() <= 1e-12 * np.abs(rc.eigenvalues).max()
             assert ra.stats.iterations == rc.stats.iterations
+
+
+def test_interleaved_batch_isolates_errors():
+    """Errors stay per contour when the batch runs as interleaved engines: a
+    contour with nothing inside (NoEigenvaluesFound) in the second engine's
+    half does not disturb its neighbours, which equal solve_multi's results."""
+    import json
+    import os
+    from paper_2511_01927_b200 import (Contour, DevicePencil, NoEigenvaluesFound, SolverConfig, solve_multi,
+                                       solve_multi_batch)
+    from paper_2511_01927_b200 import workloads as W
+    fix = np.load(os.path.join(os.path.dirname(__file__), "golden", "oracle_config2.npz"))
+    ng = 20
+    mats = [W.config2_matrices(s) for s in range(ng)]
+    cons = [[Contour.from_json_dict(d) for d in json.loads(str(fix[f"s{s}_contours"]))] for s in range(ng)]
+    far = Contour(shape="circle", center=complex(-1e3, 0.0), radius=1.0)
+    cons[15] = cons[15] + [far]
+    cfg = SolverConfig(n_q=16, source_cols=8, n_moments=4)
+    dps = [DevicePencil(a, b, hermitian=True) for a, b in mats]
+    got = solve_multi_batch(dps, cons, cfg)
+    assert got[15].results[2] is None and isinstance(got[15].errors[2], NoEigenvaluesFound)
+    for s in (0, 14, 15, 19):
+        want = solve_multi(dps[s], cons[s], cfg, seed=0)
+        for rg, rw in zip(got[s].results, want.results):
+            assert (rg is None) == (rw is None)
+            if rw is None:
+                continue
+            assert len(rg.eigenvalues) == len(rw.eigenvalues)
+            assert np.abs(rg.eigenvalues - rw.eigenvalues).max() <= 1e-12 * np.abs(rw.eigenvalues).max()
