@@ -60,6 +60,18 @@ int cirr_symmetry(const double* A, int n, long long lda, double* out, cudaStream
 int cirr_zgetrf_batched(cirr_cplx* pencils, int n, long long ld, long long pencil_stride,
                         int batch, int* ipiv, int* perm, double* minpiv, int* info, void* ws,
                         cudaStream_t stream);
+/* Banded pencils (the stencil configs 1/2/3/5, stored dense): the same LU on
+ * the band only -- panel rows stop at k+jb+kl, interchanges and U blocks at
+ * column k+jb+kl+ku (fill-in bound), trailing updates cover kl x (kl+ku).  The
+ * skipped entries are exact zeros, so the factors are bitwise those of
+ * cirr_zgetrf_batched.  lbw: batch ints (zeroed by the caller) raised to L's
+ * final lower bandwidth when interchanges move L entries beyond kl. */
+int cirr_zgetrf_band(cirr_cplx* pencils, int n, long long ld, long long pencil_stride, int batch, int kl, int ku,
+                     int* ipiv, int* perm, double* minpiv, int* info, int* lbw, void* ws, cudaStream_t stream);
+/* out[0] = max(i-j), out[1] = max(j-i) over the nonzeros of an n x n real
+ * (is_complex 0) or complex128 matrix, raised with atomicMax (zero out first;
+ * one call per matrix gives the union of A's and B's patterns). */
+int cirr_bandwidth(const void* M, int is_complex, int n, long long ld, int* out, cudaStream_t stream);
 /* ws bytes for cirr_zgetrf_batched (L11^-1 blocks; ws may be NULL: slower TRSM path) */
 long long cirr_zgetrf_ws_bytes(int n, int batch);
 
@@ -109,6 +121,16 @@ int cirr_zgetrs_moments(const cirr_cplx* LU, int n, long long ld, long long penc
                         long long rstride, const int* rhs_of, int K, cirr_cplx* Y, long long ldy,
                         long long ystride, const cirr_cplx* Dinv, const cirr_cplx* coef, int M, const int* off,
                         int n_sets, cirr_cplx* St, long long ld_st, long long sstride, cudaStream_t stream);
+
+/* cirr_zgetrs_moments / _gather / _batched in one entry, cut to the factors'
+ * bandwidths klL (L below the diagonal: max(kl, lbw of cirr_zgetrf_band)) and
+ * kuU (U above: kl + ku); -1 = dense.  pencil_of NULL: entry j uses factor j;
+ * coef NULL: no moment accumulation.  Bitwise equal to the dense entries. */
+int cirr_zgetrs_band(const cirr_cplx* LU, int n, long long ld, long long pencil_stride, int nfac,
+                     const int* pencil_of, int batch, const int* perm, const cirr_cplx* R, long long ldr,
+                     long long rstride, const int* rhs_of, int K, cirr_cplx* Y, long long ldy, long long ystride,
+                     const cirr_cplx* Dinv, const cirr_cplx* coef, int M, const int* off, int n_sets,
+                     cirr_cplx* St, long long ld_st, long long sstride, int klL, int kuU, cudaStream_t stream);
 
 /* K3b -- replaces solvers.py:121-129 (acc[m] += w_j zeta_j^m Y_j).
  * St[c] ((M*K) x n): row m*K+col = column col of S_m of contour c, summed over

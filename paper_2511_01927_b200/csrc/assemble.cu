@@ -305,3 +305,40 @@ CIRR_API int cirr_hermitian_c(const cplx* A, int n, long long lda, double* out, 
   CIRR_CHECK_LAUNCH();
   return 0;
 }
+
+// --------------------------------------------------------------------------
+// Band structure of the pencils (configs 1/2/3/5 are stencils stored dense):
+// out[0] = max(i - j), out[1] = max(j - i) over the nonzero entries of the
+// n x n matrix M (real f64 or complex128, row-major, ld), each raised with
+// atomicMax (zero them first to start; call once per matrix for a union).
+namespace {
+__global__ void bandwidth_kernel(const double* __restrict__ M, int cw, int n, long long ld, int* __restrict__ out) {
+  int kl = 0, ku = 0;
+  const long long total = (long long)n * n;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(e / n), c = (int)(e - (long long)r * n);
+    const double* x = M + ((long long)r * ld + c) * cw;
+    const bool nz = x[0] != 0.0 || (cw == 2 && x[1] != 0.0);
+    if (nz) {
+      kl = max(kl, r - c);
+      ku = max(ku, c - r);
+    }
+  }
+  kl = __reduce_max_sync(0xffffffffu, kl);
+  ku = __reduce_max_sync(0xffffffffu, ku);
+  if ((threadIdx.x & 31) == 0) {
+    if (kl > 0) atomicMax(out, kl);
+    if (ku > 0) atomicMax(out + 1, ku);
+  }
+}
+}  // namespace
+
+CIRR_API int cirr_bandwidth(const void* M, int is_complex, int n, long long ld, int* out, cudaStream_t stream) {
+  if (n <= 0 || ld < n || M == nullptr || out == nullptr) return CIRR_EINVAL;
+  const long long total = (long long)n * n;
+  const int blocks = (int)((total + 255) / 256 < 148 * 8 ? (total + 255) / 256 : 148 * 8);
+  bandwidth_kernel<<<blocks, 256, 0, stream>>>(reinterpret_cast<const double*>(M), is_complex ? 2 : 1, n, ld, out);
+  CIRR_CHECK_LAUNCH();
+  return 0;
+}

@@ -55,7 +55,11 @@ __device__ __forceinline__ int block_argmax(double best, int bi, double* rv, int
 template <int PTT>
 __global__ void __launch_bounds__(PTT, PTT == 128 ? 4 : 1) panel2_kernel(cplx* __restrict__ P, int n, long long ld, long long pstride,
                                                      int k, int jb, int* __restrict__ ipiv,
-                                                     double* __restrict__ minpiv, int* __restrict__ info) {
+                                                     double* __restrict__ minpiv, int* __restrict__ info, int rend,
+                                                     int* __restrict__ lbw) {
+  // rows [k, rend) can be nonzero in the panel columns (rend = n for a dense
+  // pencil, k + jb + kl for a banded one); the rows below are exact zeros there
+  // and stay so, so they are skipped.  ipiv is indexed with the full order n.
   constexpr int PW2 = PTT / 32;
   __shared__ double rv[PW2];
   __shared__ int ri[PW2];
@@ -69,14 +73,14 @@ __global__ void __launch_bounds__(PTT, PTT == 128 ? 4 : 1) panel2_kernel(cplx* _
   // candidate for the next pivot column: strided search of column k once per panel
   double best = -1.0;
   int bi = 0x7fffffff;
-  for (int r = k + tid; r < n; r += PTT) arg_better(best, bi, cabs1(A[(long long)r * ld + k]), r);
+  for (int r = k + tid; r < rend; r += PTT) arg_better(best, bi, cabs1(A[(long long)r * ld + k]), r);
 
   for (int c0 = 0; c0 < jb; c0 += IB) {
     const int ib = min(IB, jb - c0);
     for (int c = c0; c < c0 + ib; ++c) {
       const int row0 = k + c;
       int p = block_argmax<PW2>(best, bi, rv, ri);
-      if (p >= n) p = row0;  // empty candidate set cannot happen for row0 < n; keep LAPACK-safe
+      if (p >= rend) p = row0;  // empty candidate set cannot happen for row0 < n; keep LAPACK-safe
       if (tid == 0) piv[row0] = p;
       // swap rows row0 <-> p over the panel width; prow = the new row0
       for (int cc = tid; cc < jb; cc += PTT) {
@@ -88,6 +92,8 @@ __global__ void __launch_bounds__(PTT, PTT == 128 ? 4 : 1) panel2_kernel(cplx* _
           *x = yv;
           *y = xv;
           prow[cc] = yv;
+          // an L entry of an earlier column of this panel moving down
+          if (lbw != nullptr && cc < c && (xv.x != 0.0 || xv.y != 0.0)) atomicMax(lbw + blockIdx.x, p - (k + cc));
         } else {
           prow[cc] = xv;
         }
@@ -110,13 +116,13 @@ __global__ void __launch_bounds__(PTT, PTT == 128 ? 4 : 1) panel2_kernel(cplx* _
       bi = 0x7fffffff;
       constexpr int RSTEP = 4 * PW2;  // rows per CTA pass of one row group
       constexpr int RU = 8;           // row groups in flight per thread
-      for (int rb = row0 + 1 + wid * 4; rb < n; rb += RU * RSTEP) {
+      for (int rb = row0 + 1 + wid * 4; rb < rend; rb += RU * RSTEP) {
         cplx v[RU];
         bool act[RU];
 #pragma unroll
         for (int q = 0; q < RU; ++q) {
           const int r = rb + q * RSTEP + (lane >> 3);
-          act[q] = r < n;
+          act[q] = r < rend;
           v[q] = (act[q] && g >= cl && g < ib) ? A[(long long)r * ld + k + c0 + g] : cmk(0.0, 0.0);
         }
 #pragma unroll
@@ -162,13 +168,13 @@ __global__ void __launch_bounds__(PTT, PTT == 128 ? 4 : 1) panel2_kernel(cplx* _
       const int h = lane >> 4, q16 = lane & 15;
       best = -1.0;
       bi = 0x7fffffff;
-      for (int rA = r0 + ib + wid * 2 + h; rA < n; rA += 4 * PW2) {
+      for (int rA = r0 + ib + wid * 2 + h; rA < rend; rA += 4 * PW2) {
         // two rows per thread (rA and rA + 2*PW2): all their loads in flight together
         const int rr2[2] = {rA, rA + 2 * PW2};
         cplx l[2][IB], v[2][4];
 #pragma unroll
         for (int u2 = 0; u2 < 2; ++u2) {
-          const bool ok = rr2[u2] < n;
+          const bool ok = rr2[u2] < rend;
           const cplx* lr = A + (long long)rr2[u2] * ld + k + c0;
 #pragma unroll
           for (int i = 0; i < IB; ++i) l[u2][i] = (ok && i < ib) ? lr[i] : cmk(0.0, 0.0);
@@ -181,7 +187,7 @@ __global__ void __launch_bounds__(PTT, PTT == 128 ? 4 : 1) panel2_kernel(cplx* _
         }
 #pragma unroll
         for (int u2 = 0; u2 < 2; ++u2) {
-          if (rr2[u2] >= n) continue;
+          if (rr2[u2] >= rend) continue;
           cplx* dst = A + (long long)rr2[u2] * ld + k + c0 + ib;
 #pragma unroll
           for (int t = 0; t < 4; ++t) {
@@ -205,22 +211,39 @@ __global__ void __launch_bounds__(PTT, PTT == 128 ? 4 : 1) panel2_kernel(cplx* _
   }
 }
 
-// Apply interchanges ipiv[k .. k+jb) to the columns outside the panel.
+// Apply interchanges ipiv[k .. k+jb) to the columns outside the panel: all of
+// [0, k) (the L part, LAPACK convention) and [k + jb, cend) (cend = n dense,
+// k + jb + kl + ku banded: U's fill-in bound).  lbw (per pencil, optional)
+// records max (row - col) over the nonzero L entries the swaps move: with
+// row interchanges an L entry can end up more than kl below the diagonal, and
+// the band-limited solves need L's final lower bandwidth.
 __global__ void swap_kernel(cplx* __restrict__ P, int n, long long ld, long long pstride, int k, int jb,
-                            const int* __restrict__ ipiv) {
-  const int other = n - jb;
+                            const int* __restrict__ ipiv, int cend, int* __restrict__ lbw) {
+  const int other = k + (cend - k - jb);
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= other) return;
-  const int col = t < k ? t : t + jb;
-  cplx* A = P + (long long)blockIdx.y * pstride;
-  const int* piv = ipiv + (long long)blockIdx.y * n;
-  for (int i = 0; i < jb; ++i) {
-    const int r1 = k + i, r2 = piv[k + i];
-    if (r1 != r2) {
-      cplx* x = A + (long long)r1 * ld + col;
-      cplx* y = A + (long long)r2 * ld + col;
-      cplx tt = *x; *x = *y; *y = tt;
+  int bw = 0;
+  if (t < other) {
+    const int col = t < k ? t : t + jb;
+    cplx* A = P + (long long)blockIdx.y * pstride;
+    const int* piv = ipiv + (long long)blockIdx.y * n;
+    for (int i = 0; i < jb; ++i) {
+      const int r1 = k + i, r2 = piv[k + i];
+      if (r1 != r2) {
+        cplx* x = A + (long long)r1 * ld + col;
+        cplx* y = A + (long long)r2 * ld + col;
+        const cplx tt = *x, yy = *y;
+        *x = yy;
+        *y = tt;
+        if (col < k) {
+          if (tt.x != 0.0 || tt.y != 0.0) bw = max(bw, r2 - col);
+          if (yy.x != 0.0 || yy.y != 0.0) bw = max(bw, r1 - col);
+        }
+      }
     }
+  }
+  if (lbw != nullptr) {
+    bw = __reduce_max_sync(0xffffffffu, bw);
+    if ((threadIdx.x & 31) == 0 && bw > 0) atomicMax(lbw + blockIdx.y, bw);
   }
 }
 
@@ -344,12 +367,15 @@ __global__ void init_kernel(double* minpiv, int* info, int batch) {
 // 128-thread CTAs keep ~4x more pencils in flight per SM (4 CTAs per SM at 128 registers; LU 61.5 -> 38.1 ms).
 // CIRR_PANEL_T overrides: 128 / 256 / 512.
 static int launch_panel(cplx* pencils, int n, long long ld, long long pstride, int batch, int k, int jb, int* ipiv,
-                        double* minpiv, int* info, cudaStream_t stream) {
+                        double* minpiv, int* info, int rend, int* lbw, cudaStream_t stream) {
   static const int env_t = getenv("CIRR_PANEL_T") ? atoi(getenv("CIRR_PANEL_T")) : 0;
-  const int t = env_t > 0 ? env_t : (n <= 512 && batch >= 1024 ? 128 : PT2);
-  if (t == 128) panel2_kernel<128><<<batch, 128, 0, stream>>>(pencils, n, ld, pstride, k, jb, ipiv, minpiv, info);
-  else if (t == 256) panel2_kernel<256><<<batch, 256, 0, stream>>>(pencils, n, ld, pstride, k, jb, ipiv, minpiv, info);
-  else panel2_kernel<PT2><<<batch, PT2, 0, stream>>>(pencils, n, ld, pstride, k, jb, ipiv, minpiv, info);
+  const int m = rend - k;   // rows the panel can have nonzero
+  const int t = env_t > 0 ? env_t : (m <= 512 && batch >= 1024 ? 128 : PT2);
+  if (t == 128)
+    panel2_kernel<128><<<batch, 128, 0, stream>>>(pencils, n, ld, pstride, k, jb, ipiv, minpiv, info, rend, lbw);
+  else if (t == 256)
+    panel2_kernel<256><<<batch, 256, 0, stream>>>(pencils, n, ld, pstride, k, jb, ipiv, minpiv, info, rend, lbw);
+  else panel2_kernel<PT2><<<batch, PT2, 0, stream>>>(pencils, n, ld, pstride, k, jb, ipiv, minpiv, info, rend, lbw);
   CIRR_CHECK_LAUNCH();
   return 0;
 }
@@ -357,9 +383,21 @@ static int launch_panel(cplx* pencils, int n, long long ld, long long pstride, i
 // Workspace for cirr_zgetrf_batched (L11^{-1} blocks); 0 disables that path.
 CIRR_API long long cirr_zgetrf_ws_bytes(int n, int batch) { return (long long)batch * NB * NB * 16 + 256; }
 
-CIRR_API int cirr_zgetrf_batched(cplx* pencils, int n, long long ld, long long pencil_stride, int batch,
-                                 int* ipiv, int* perm, double* minpiv, int* info, void* ws, cudaStream_t stream) {
-  if (n <= 0 || batch <= 0 || ld < n) return CIRR_EINVAL;
+// Banded pencils (kl sub-, ku superdiagonals, the stencil configs 1/2/3/5)
+// run the same kernels on the band only: the panel's rows stop at
+// k + jb + kl, the interchanges and the U blocks at column k + jb + kl + ku
+// (U's fill-in bound), the trailing updates cover the kl rows x (kl + ku)
+// columns that can be nonzero.  Everything outside is an exact zero that the
+// full LU would only add zeros to, so the factors are bitwise those of the
+// dense LU.  kl = ku = n - 1 is the dense LU.  lbw (per pencil, zeroed by the
+// caller, optional) receives L's final lower bandwidth beyond kl.
+static int getrf_impl(cplx* pencils, int n, long long ld, long long pencil_stride, int batch, int kl, int ku,
+                      int* ipiv, int* perm, double* minpiv, int* info, int* lbw, void* ws, cudaStream_t stream) {
+  if (n <= 0 || batch <= 0 || ld < n || kl < 0 || ku < 0) return CIRR_EINVAL;
+  kl = min(kl, n - 1);
+  ku = min(ku, n - 1);
+  auto rend = [&](int k, int jb) { return (int)min((long long)n, (long long)k + jb + kl); };
+  auto cend = [&](int k, int jb) { return (int)min((long long)n, (long long)k + jb + kl + ku); };
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrsmSmem);
@@ -401,16 +439,17 @@ CIRR_API int cirr_zgetrf_batched(cplx* pencils, int n, long long ld, long long p
       const int k = k0, rest = n - k0 - W;
       for (int i = 0; i < PB; ++i) {
         const int ki = k + i * NB;
-        if (i > 0)  // this panel's columns: A[ki:, ki:ki+64] -= L[ki:, k:ki] U[k:ki, ki:ki+64]
-          CIRR_TRY(cirr::zgemm_sub_maps(maps.a, maps.b, maps.c, n - ki, NB, i * NB, batch, ki, k, k, ki, ki, ki,
+        const int re = rend(ki, NB), ce = cend(ki, NB);
+        if (i > 0)  // this panel's columns: A[ki:re, ki:ki+64] -= L[ki:re, k:ki] U[k:ki, ki:ki+64]
+          CIRR_TRY(cirr::zgemm_sub_maps(maps.a, maps.b, maps.c, re - ki, NB, i * NB, batch, ki, k, k, ki, ki, ki,
                                         pencils, ld, pencil_stride, stream));
-        CIRR_TRY(launch_panel(pencils, n, ld, pencil_stride, batch, ki, NB, ipiv, minpiv, info, stream));
+        CIRR_TRY(launch_panel(pencils, n, ld, pencil_stride, batch, ki, NB, ipiv, minpiv, info, re, lbw, stream));
         {
-          dim3 g((n - NB + 255) / 256, batch);
-          swap_kernel<<<g, 256, 0, stream>>>(pencils, n, ld, pencil_stride, ki, NB, ipiv);
+          dim3 g((ki + ce - ki - NB + 255) / 256, batch);
+          swap_kernel<<<g, 256, 0, stream>>>(pencils, n, ld, pencil_stride, ki, NB, ipiv, ce, lbw);
           CIRR_CHECK_LAUNCH();
         }
-        const int right = n - ki - NB;  // columns right of this panel
+        const int right = ce - ki - NB;  // columns right of this panel that can be nonzero
         if (right > 0) {
           linv_kernel<<<batch, 256, kLinvSmem, stream>>>(pencils, ld, pencil_stride, ki, linv);
           CIRR_CHECK_LAUNCH();
@@ -421,20 +460,22 @@ CIRR_API int cirr_zgetrf_batched(cplx* pencils, int n, long long ld, long long p
                                         pencils, ld, pencil_stride, stream, /*beta=*/0));
         }
       }
-      if (rest > 0)  // trailing update with k = W
-        CIRR_TRY(cirr::zgemm_sub_maps(maps.a, maps.b, maps.c, rest, rest, W, batch, k + W, k, k, k + W, k + W, k + W,
-                                      pencils, ld, pencil_stride, stream));
+      if (rest > 0)  // trailing update with k = W (rows/columns that can be nonzero)
+        CIRR_TRY(cirr::zgemm_sub_maps(maps.a, maps.b, maps.c, rend(k, W) - k - W, cend(k, W) - k - W, W, batch,
+                                      k + W, k, k, k + W, k + W, k + W, pencils, ld, pencil_stride, stream));
     }
   }
   for (int k = k0; k < n; k += NB) {
     const int jb = min(NB, n - k);
-    CIRR_TRY(launch_panel(pencils, n, ld, pencil_stride, batch, k, jb, ipiv, minpiv, info, stream));
-    if (n - jb > 0) {
-      dim3 g((n - jb + 255) / 256, batch);
-      swap_kernel<<<g, 256, 0, stream>>>(pencils, n, ld, pencil_stride, k, jb, ipiv);
+    const int re = rend(k, jb), ce = cend(k, jb);
+    CIRR_TRY(launch_panel(pencils, n, ld, pencil_stride, batch, k, jb, ipiv, minpiv, info, re, lbw, stream));
+    if (k + ce - k - jb > 0) {
+      dim3 g((k + ce - k - jb + 255) / 256, batch);
+      swap_kernel<<<g, 256, 0, stream>>>(pencils, n, ld, pencil_stride, k, jb, ipiv, ce, lbw);
       CIRR_CHECK_LAUNCH();
     }
-    const int rest = n - k - jb;
+    const int rest = ce - k - jb;     // columns right of the panel that can be nonzero
+    const int rrest = re - k - jb;    // rows below it that can be nonzero
     if (rest > 0) {
       if (use_linv && jb == NB) {
         // U12 = L11^{-1} A12 as a TMA/DMMA GEMM (each output tile reads exactly
@@ -449,9 +490,10 @@ CIRR_API int cirr_zgetrf_batched(cplx* pencils, int n, long long ld, long long p
         CIRR_CHECK_LAUNCH();
       }
       if (jb % cirr::PBK == 0 && use_tma) {
-        CIRR_TRY(cirr::lu_update_tma(maps, pencils, n, ld, pencil_stride, batch, k, jb, stream));
-      } else {
-        cirr::GemmArgs ga{rest, rest, jb, batch,
+        CIRR_TRY(cirr::zgemm_sub_maps(maps.a, maps.b, maps.c, rrest, rest, jb, batch, k + jb, k, k, k + jb, k + jb,
+                                      k + jb, pencils, ld, pencil_stride, stream));
+      } else if (rrest > 0) {
+        cirr::GemmArgs ga{rrest, rest, jb, batch,
                           pencils + (long long)(k + jb) * ld + k, ld, pencil_stride,
                           pencils + (long long)k * ld + k + jb, ld, pencil_stride,
                           pencils + (long long)(k + jb) * ld + k + jb, ld, pencil_stride,
@@ -467,4 +509,20 @@ CIRR_API int cirr_zgetrf_batched(cplx* pencils, int n, long long ld, long long p
     CIRR_CHECK_LAUNCH();
   }
   return 0;
+}
+
+CIRR_API int cirr_zgetrf_batched(cplx* pencils, int n, long long ld, long long pencil_stride, int batch,
+                                 int* ipiv, int* perm, double* minpiv, int* info, void* ws, cudaStream_t stream) {
+  return getrf_impl(pencils, n, ld, pencil_stride, batch, n - 1, n - 1, ipiv, perm, minpiv, info, nullptr, ws,
+                    stream);
+}
+
+// cirr_zgetrf_batched for pencils with kl sub- and ku superdiagonals (the
+// union pattern of A and B, cirr_bandwidth); lbw: batch ints zeroed by the
+// caller, each raised to the lower bandwidth the interchanges give L beyond kl
+// (the solves take max(kl, lbw) and kl + ku).
+CIRR_API int cirr_zgetrf_band(cplx* pencils, int n, long long ld, long long pencil_stride, int batch, int kl,
+                              int ku, int* ipiv, int* perm, double* minpiv, int* info, int* lbw, void* ws,
+                              cudaStream_t stream) {
+  return getrf_impl(pencils, n, ld, pencil_stride, batch, kl, ku, ipiv, perm, minpiv, info, lbw, ws, stream);
 }

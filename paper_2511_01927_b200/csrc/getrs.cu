@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(8 * KC, KC == 32 ? 2 : 3) trsm_blocked_kernel(
                                                               long long pstride, int n,
                                                               cplx* __restrict__ Y, long long ldy,
                                                               long long ystride, int K,
-                                                              const int* __restrict__ pmap) {
+                                                              const int* __restrict__ pmap, int klL, int kuU) {
   using CF = SolveCfg<KC>;
   constexpr int NT = CF::NT, SB_LD = CF::B_LD, SX_LD = CF::X_LD, kStageB = CF::kStageB, SKC_ = KC;
   extern __shared__ __align__(16) cplx ssm[];
@@ -69,8 +69,12 @@ __global__ void __launch_bounds__(8 * KC, KC == 32 ? 2 : 3) trsm_blocked_kernel(
     const int i0 = bi * SNB;
     const int nbi = min(SNB, n - i0);
     // k-range of the off-diagonal product
-    const int kbeg = LOWER ? 0 : i0 + nbi;
-    const int kend = LOWER ? i0 : n;
+    // off-diagonal range, cut to the band: L_ik = 0 for i - k > klL and
+    // U_ik = 0 for k - i > kuU
+    // (the lower start on the k-step grid of the full range, so every k-step
+    // sums the same products as the dense solve: bitwise equal results)
+    const int kbeg = LOWER ? max(0, i0 - (klL + SBK - 1) / SBK * SBK) : i0 + nbi;
+    const int kend = LOWER ? i0 : min(n, i0 + nbi + kuU);
     const int klen = kend - kbeg;
 
     double cr[2][2][2], ci[2][2][2];
@@ -683,8 +687,14 @@ static int moments_rows(const MomentSpec* ms, const cplx* Y, long long ldy, long
 static int getrs_impl(const cplx* LU, int n, long long ld, long long pencil_stride, int batch, int nfac,
                       const int* pmap, const int* perm, const cplx* R, long long ldr, long long rstride,
                       const int* rhs_of, int K, cplx* Y, long long ldy, long long ystride, const cplx* Dinv,
-                      cudaStream_t stream, const MomentSpec* ms = nullptr) {
+                      cudaStream_t stream, const MomentSpec* ms = nullptr, int klL = -1, int kuU = -1) {
   if (n <= 0 || batch <= 0 || nfac <= 0 || K < 0 || ldy < K || ldr < K) return CIRR_EINVAL;
+  // factor bandwidths (L below, U above the diagonal); -1 = dense.  Every
+  // product below is cut to the rows / k-range the band allows: the skipped
+  // blocks are exact zeros, so the results are bitwise those of the full solve.
+  klL = (klL < 0 || klL > n - 1) ? n - 1 : klL;
+  kuU = (kuU < 0 || kuU > n - 1) ? n - 1 : kuU;
+  auto up16 = [](int x) { return (x + 15) / 16 * 16; };
   if (ms != nullptr && (ms->M < 1 || ms->M > MAXM || ms->n_sets <= 0)) return CIRR_EINVAL;
   if (K == 0) return 0;
   static bool attr = false;
@@ -763,14 +773,18 @@ static int getrs_impl(const cplx* LU, int n, long long ld, long long pencil_stri
         const int s0 = sb0 * DB, s1 = min(n, sb1 * DB);
         for (int bi = sb0; bi < sb1; ++bi) {
           const int i0 = bi * DB, nb = min(DB, n - i0);
-          if (bi > sb0)  // Y[i0:i0+nb] -= L[i0:i0+nb, s0:i0] Y[s0:i0]
-            CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, nb, K, i0 - s0, batch, i0, s0, s0, 0, i0, 0, Y, ldy,
+          if (bi > sb0) {  // Y[i0:i0+nb] -= L[i0:i0+nb, kb:i0] Y[kb:i0], kb >= s0 cut to the band
+            const int kb = max(s0, i0 - up16(min(i0 - s0, klL)));
+            CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, nb, K, i0 - kb, batch, i0, kb, kb, 0, i0, 0, Y, ldy,
                                           ystride, stream, 1, 1, 0, pmap, BN));
+          }
           CIRR_TRY(apply_dinv(bi, true));
         }
-        if (n - s1 > 0)  // Y[s1:] -= L[s1:, s0:s1] Y[s0:s1]
-          CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, n - s1, K, s1 - s0, batch, s1, s0, s0, 0, s1, 0, Y, ldy,
-                                        ystride, stream, 1, 1, 0, pmap, BN));
+        if (n - s1 > 0) {  // Y[s1:s1+m] -= L[s1:s1+m, kb:s1] Y[kb:s1] (m = klL rows below can be nonzero)
+          const int kb = max(s0, s1 - up16(min(s1 - s0, klL)));
+          CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, min(n - s1, klL), K, s1 - kb, batch, s1, kb, kb, 0, s1, 0,
+                                        Y, ldy, ystride, stream, 1, 1, 0, pmap, BN));
+        }
       }
       const int nsb = (nblk2 + SBK - 1) / SBK;
       for (int sb = nsb - 1; sb >= 0; --sb) {  // backward: U
@@ -778,17 +792,22 @@ static int getrs_impl(const cplx* LU, int n, long long ld, long long pencil_stri
         const int s0 = sb0 * DB, s1 = min(n, sb1 * DB);
         for (int bi = sb1 - 1; bi >= sb0; --bi) {
           const int i0 = bi * DB, nb = min(DB, n - i0);
-          if (bi < sb1 - 1)  // Y[i0:i0+nb] -= U[i0:i0+nb, i0+nb:s1] Y[i0+nb:s1]
-            CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, nb, K, s1 - i0 - nb, batch, i0, i0 + nb, i0 + nb, 0, i0,
-                                          0, Y, ldy, ystride, stream, 1, 1, 0, pmap, BN));
+          if (bi < sb1 - 1) {  // Y[i0:i0+nb] -= U[i0:i0+nb, i0+nb:ke] Y[i0+nb:ke], ke <= s1 cut to the band
+            const int ke = min(s1, i0 + nb + up16(min(s1 - i0 - nb, kuU)));
+            if (ke > i0 + nb)
+              CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, nb, K, ke - i0 - nb, batch, i0, i0 + nb, i0 + nb, 0, i0,
+                                            0, Y, ldy, ystride, stream, 1, 1, 0, pmap, BN));
+          }
           CIRR_TRY(apply_dinv(bi, false));
           // rows i0.. are final for every entry: their moment rows now, while
           // the block (batch x 128 x K) is still in L2
           CIRR_TRY(moments_rows(ms, Y, ldy, ystride, n, K, i0, i0 + nb, stream));
         }
-        if (s0 > 0)  // Y[:s0] -= U[:s0, s0:s1] Y[s0:s1]
-          CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, s0, K, s1 - s0, batch, 0, s0, s0, 0, 0, 0, Y, ldy, ystride,
-                                        stream, 1, 1, 0, pmap, BN));
+        if (s0 > 0) {  // Y[r0:s0] -= U[r0:s0, s0:ke] Y[s0:ke] (rows within kuU above, their columns)
+          const int r0 = max(0, s0 - kuU), ke = min(s1, s0 + up16(min(s1 - s0, kuU)));
+          CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, s0 - r0, K, ke - s0, batch, r0, s0, s0, 0, r0, 0, Y, ldy,
+                                        ystride, stream, 1, 1, 0, pmap, BN));
+        }
       }
       return 0;
     }
@@ -798,14 +817,15 @@ static int getrs_impl(const cplx* LU, int n, long long ld, long long pencil_stri
       const int i0 = bi * SNB, nb = min(SNB, n - i0);
       diag_solve_kernel<true><<<gd, 256, kDiagSmem, stream>>>(LU, ld, pencil_stride, i0, nb, Y, ldy, ystride, K, pmap);
       CIRR_CHECK_LAUNCH();
-      CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, n - i0 - nb, K, nb, batch, i0 + nb, i0, i0, 0, i0 + nb, 0,
-                                    Y, ldy, ystride, stream, 1, 1, 0, pmap, BN));
+      CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, min(n - i0 - nb, klL), K, nb, batch, i0 + nb, i0, i0, 0,
+                                    i0 + nb, 0, Y, ldy, ystride, stream, 1, 1, 0, pmap, BN));
     }
     for (int bi = nblk - 1; bi >= 0; --bi) {  // backward: U
       const int i0 = bi * SNB, nb = min(SNB, n - i0);
       diag_solve_kernel<false><<<gd, 256, kDiagSmem, stream>>>(LU, ld, pencil_stride, i0, nb, Y, ldy, ystride, K, pmap);
       CIRR_CHECK_LAUNCH();
-      CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, i0, K, nb, batch, 0, i0, i0, 0, 0, 0, Y, ldy, ystride,
+      const int r0 = max(0, i0 - kuU);
+      CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, i0 - r0, K, nb, batch, r0, i0, i0, 0, r0, 0, Y, ldy, ystride,
                                     stream, 1, 1, 0, pmap, BN));
     }
     return moments_rows(ms, Y, ldy, ystride, n, K, 0, n, stream);
@@ -814,18 +834,18 @@ static int getrs_impl(const cplx* LU, int n, long long ld, long long pencil_stri
   if (kc_env == 16 || (kc_env == 0 && K <= 16)) {
     dim3 gs((K + 15) / 16, batch);
     trsm_blocked_kernel<true, 16><<<gs, SolveCfg<16>::NT, SolveCfg<16>::kSmem, stream>>>(LU, ld, pencil_stride, n,
-                                                                                        Y, ldy, ystride, K, pmap);
+                                                                                        Y, ldy, ystride, K, pmap, klL, kuU);
     CIRR_CHECK_LAUNCH();
     trsm_blocked_kernel<false, 16><<<gs, SolveCfg<16>::NT, SolveCfg<16>::kSmem, stream>>>(LU, ld, pencil_stride, n,
-                                                                                         Y, ldy, ystride, K, pmap);
+                                                                                         Y, ldy, ystride, K, pmap, klL, kuU);
     CIRR_CHECK_LAUNCH();
   } else {
     dim3 gs((K + SKC - 1) / SKC, batch);
     trsm_blocked_kernel<true, 32><<<gs, SolveCfg<32>::NT, SolveCfg<32>::kSmem, stream>>>(LU, ld, pencil_stride, n,
-                                                                                        Y, ldy, ystride, K, pmap);
+                                                                                        Y, ldy, ystride, K, pmap, klL, kuU);
     CIRR_CHECK_LAUNCH();
     trsm_blocked_kernel<false, 32><<<gs, SolveCfg<32>::NT, SolveCfg<32>::kSmem, stream>>>(LU, ld, pencil_stride, n,
-                                                                                         Y, ldy, ystride, K, pmap);
+                                                                                         Y, ldy, ystride, K, pmap, klL, kuU);
     CIRR_CHECK_LAUNCH();
   }
   return moments_rows(ms, Y, ldy, ystride, n, K, 0, n, stream);
@@ -865,6 +885,21 @@ CIRR_API int cirr_zgetrs_moments(const cplx* LU, int n, long long ld, long long 
   const MomentSpec ms{coef, M, off, n_sets, St, ld_st, sstride};
   return getrs_impl(LU, n, ld, pencil_stride, batch, pencil_of ? nfac : batch, pencil_of, perm, R, ldr, rstride,
                     rhs_of, K, Y, ldy, ystride, Dinv, stream, &ms);
+}
+
+// cirr_zgetrs_moments / cirr_zgetrs_gather / cirr_zgetrs_batched in one entry
+// with the factors' bandwidths: klL (L below the diagonal: max(kl, the lbw of
+// cirr_zgetrf_band)) and kuU (U above it: kl + ku); -1 = dense.  pencil_of
+// NULL: entry j uses factor j; coef NULL: no moments.
+CIRR_API int cirr_zgetrs_band(const cplx* LU, int n, long long ld, long long pencil_stride, int nfac,
+                              const int* pencil_of, int batch, const int* perm, const cplx* R, long long ldr,
+                              long long rstride, const int* rhs_of, int K, cplx* Y, long long ldy, long long ystride,
+                              const cplx* Dinv, const cplx* coef, int M, const int* off, int n_sets, cplx* St,
+                              long long ld_st, long long sstride, int klL, int kuU, cudaStream_t stream) {
+  if (coef != nullptr && (off == nullptr || St == nullptr)) return CIRR_EINVAL;
+  const MomentSpec ms{coef, M, off, n_sets, St, ld_st, sstride};
+  return getrs_impl(LU, n, ld, pencil_stride, batch, pencil_of ? nfac : batch, pencil_of, perm, R, ldr, rstride,
+                    rhs_of, K, Y, ldy, ystride, Dinv, stream, coef ? &ms : nullptr, klL, kuU);
 }
 
 // Moment rows [row_lo, row_hi) of n_sets contours (rows past n are skipped):

@@ -53,7 +53,25 @@ _EIG_REFINE_ITERS = 5
 # large batches (>= _INTERLEAVE_MIN contours in a wave) run as _INTERLEAVE
 # engines on their own streams, interleaved at their host syncs (CIRR_INTERLEAVE=1: one engine)
 _INTERLEAVE = int(__import__("os").environ.get("CIRR_INTERLEAVE", "2"))
-_INTERLEAVE_MIN = 32
+_INTERLEAVE_MIN = int(__import__("os").environ.get("CIRR_INTERLEAVE_MIN", "32"))
+# banded pencils factor and solve on the band only (CIRR_BAND=0: always the dense ranges)
+_BAND = bool(int(__import__("os").environ.get("CIRR_BAND", "1")))
+
+
+def _band_lu_flops(n: int, kl: int, ku: int) -> float:
+    """Algorithmic complex LU flops of an n x n pencil with kl sub- and ku
+    superdiagonals: sum over columns of 8 (rows below) (columns right, fill-in
+    included); 8 n^3 / 3 for a dense one."""
+    c = np.arange(n, dtype=np.float64)
+    rest = n - 1.0 - c
+    return float(8.0 * np.sum(np.minimum(kl, rest) * np.minimum(kl + ku, rest)))
+
+
+def _band_solve_flops(n: int, kl: int, ku: int, K: int) -> float:
+    """Complex flops of one L and one U solve with K right-hand sides on
+    factors of lower / upper bandwidth kl / ku (8 n^2 K dense)."""
+    i = np.arange(n, dtype=np.float64)
+    return float(8.0 * K * (np.sum(np.minimum(i, kl)) + np.sum(np.minimum(n - 1.0 - i, ku))))
 # launches put the batch (pencils of a wave) on grid.y / grid.z, whose limit
 # is 65535: a wave never holds more pencils than that
 _MAX_WAVE_PENCILS = 65535
@@ -318,6 +336,26 @@ class DevicePencil:
         self.a = a.to("cuda", non_blocking=True).to(dt).contiguous()
         self.b = b.to("cuda", non_blocking=True).to(dt).contiguous()
         self.hermitian = bool(hermitian) if hermitian else self._device_symmetric()
+
+    def band_async(self, out):
+        """Enqueue the union band of A and B into the device int pair out
+        (zeroed by the caller): max(i - j), max(j - i) over the nonzeros."""
+        st = _stream()
+        for m in (self.a, self.b):
+            _lib.call("cirr_bandwidth", _ptr(m), 1 if self.complex else 0, self.n, self.n, _ptr(out), st)
+
+    @staticmethod
+    def bands(dps) -> list:
+        """(kl, ku) of each DevicePencil (cached on it): one device pass over
+        each uncached A and B, one read-back for all of them."""
+        todo = [d for d in dps if getattr(d, "_band", None) is None]
+        if todo:
+            buf = _zeros((len(todo), 2), _torch().int32)
+            for i, d in enumerate(todo):
+                d.band_async(buf[i])
+            for d, (kl, ku) in zip(todo, buf.cpu().numpy().tolist()):
+                d._band = (int(kl), int(ku))
+        return [d._band for d in dps]
 
     @classmethod
     def of(cls, pencil):
@@ -701,6 +739,16 @@ class _Engine:
         self.perm = torch.empty((P, n), dtype=torch.int32, device="cuda")
         self.minpiv = torch.empty(P, dtype=torch.float64, device="cuda")
         self.info = torch.empty(P, dtype=torch.int32, device="cuda")
+        self.lbw = _zeros(P, torch.int32)
+        # the wave's band: the widest of its pencils (dense: n - 1, n - 1)
+        n = self.n
+        if _BAND:
+            bands = DevicePencil.bands([self._dp_of(ci) for ci in range(len(self.cs))])
+            self.kl = min(n - 1, max(b_[0] for b_ in bands))
+            self.ku = min(n - 1, max(b_[1] for b_ in bands))
+        else:
+            self.kl = self.ku = n - 1
+        self.klL, self.kuU = n - 1, n - 1   # factor bandwidths, known after the factor read-back
         self._dinv_per_pencil = int(_lib.call("cirr_diag_inv_bytes", n, 1))
         self.contour_of = _h2d(
             np.concatenate([np.full(len(c.fidx), i, dtype=np.int32) for i, c in enumerate(self.cs)]))
@@ -728,11 +776,15 @@ class _Engine:
                 for lo, hi, d in runs:
                     d.assemble(z[lo - a:], hi - lo, self.pencils[lo], self.maxabs[lo:], self.stream)
         _work("assemble_bytes", cnt * n * n * 16 + 2 * n * n * 8)
+        kl, ku = self.kl, self.ku
         with _stage("lu"):
             lws = torch.empty(int(_lib.call("cirr_zgetrf_ws_bytes", n, cnt)), dtype=torch.uint8, device="cuda")
-            _lib.call("cirr_zgetrf_batched", _ptr(self.pencils[a]), n, n, n * n, cnt, _ptr(self.ipiv[a]),
-                      _ptr(self.perm[a]), _ptr(self.minpiv[a:]), _ptr(self.info[a:]), _ptr(lws), self.stream)
-        _work("lu_flops", cnt * 8.0 * n ** 3 / 3.0)
+            # banded pencils (the stencil configs): the LU on the band only,
+            # bitwise the dense factors; lbw collects L's bandwidth after pivoting
+            _lib.call("cirr_zgetrf_band", _ptr(self.pencils[a]), n, n, n * n, cnt, kl, ku, _ptr(self.ipiv[a]),
+                      _ptr(self.perm[a]), _ptr(self.minpiv[a:]), _ptr(self.info[a:]), _ptr(self.lbw[a:]),
+                      _ptr(lws), self.stream)
+        _work("lu_flops", cnt * _band_lu_flops(n, kl, ku))
 
     def _diag_inverses(self, a: int, b: int):
         with _stage("dinv"):
@@ -753,7 +805,10 @@ class _Engine:
         yield
         # one read-back for every contour of the wave; linalg.py:68-70 on all
         # pencils at once, the first failing node of each contour reported
-        maxabs, minpiv, info = (t.cpu().numpy() for t in (self.maxabs, self.minpiv, self.info))
+        maxabs, minpiv, info, lbw = (t.cpu().numpy() for t in (self.maxabs, self.minpiv, self.info, self.lbw))
+        n = self.n
+        self.klL = min(n - 1, max(self.kl, int(lbw.max(initial=0))))
+        self.kuU = min(n - 1, self.kl + self.ku)
         bad = (info != 0) | ~(minpiv >= PIVOT_REL_TOL * np.maximum(maxabs, 1e-300))
         for ci, c in enumerate(self.cs):
             c.stats.n_factorizations = len(c.fidx)
@@ -840,18 +895,16 @@ class _Engine:
                 a, b = runs[0]
                 base, pen_ptr = self.pencils[a], 0
                 fac_args = (_ptr(self.perm[a]), _ptr(dinv) + a * self._dinv_per_pencil if dinv is not None else 0)
-            if fused:
-                _lib.call("cirr_zgetrs_moments", _ptr(base), n, n, n * n, self.P, pen_ptr, Psolve, fac_args[0],
-                          _ptr(R), Ks, n * Ks, _ptr(rhs_of), Ks, _ptr(Ysol), Ks, n * Ks, fac_args[1], _ptr(coef),
-                          moments, _ptr(off_t), nset, _ptr(St), n, moments * K * n, self.stream)
-            elif pen_ptr:
-                _lib.call("cirr_zgetrs_gather", _ptr(base), n, n, n * n, self.P, pen_ptr, Psolve, fac_args[0],
-                          _ptr(R), Ks, n * Ks, _ptr(rhs_of), Ks, _ptr(Ysol), Ks, n * Ks, fac_args[1], self.stream)
-            else:
-                _lib.call("cirr_zgetrs_batched", _ptr(base), n, n, n * n, Psolve, fac_args[0], _ptr(R), Ks, n * Ks,
-                          _ptr(rhs_of), Ks, _ptr(Ysol), Ks, n * Ks, fac_args[1], self.stream)
-        _work("solve_flops", Psolve * 8.0 * n * n * Ks)
-        _work("solve_flops_exec", sum((b - a) * 8.0 * n * n * k for (a, b), k in zip(pen_idx, ks)))
+            # one entry for the fused (moments), gathered and plain solves, cut
+            # to the factors' band (bitwise the dense solves)
+            mom = (_ptr(coef), moments, _ptr(off_t), nset, _ptr(St), n, moments * K * n) if fused else \
+                (0, 0, 0, 0, 0, 0, 0)
+            _lib.call("cirr_zgetrs_band", _ptr(base), n, n, n * n, self.P, pen_ptr, Psolve, fac_args[0], _ptr(R), Ks,
+                      n * Ks, _ptr(rhs_of), Ks, _ptr(Ysol), Ks, n * Ks, fac_args[1], *mom, self.klL, self.kuU,
+                      self.stream)
+        _work("solve_flops", Psolve * _band_solve_flops(n, self.klL, self.kuU, Ks))
+        _work("solve_flops_exec", sum((b - a) * _band_solve_flops(n, self.klL, self.kuU, k)
+                                      for (a, b), k in zip(pen_idx, ks)))
         _work("moment_flops", Ptot * 8.0 * n * K * moments)
         if fused:
             del Ysol

@@ -447,3 +447,67 @@ def _small(lib, a, b, k, herm):
     lib.call("cirr_small_eig", herm, P(cuda(a)), P(cuda(b)), k, k * k, P(kd), k, 1, P(ws), P(lam), P(s), k, k * k,
              P(info), S())
     return lam.cpu().numpy(), s.cpu().numpy(), info.item()
+
+
+def _banded(rng, batch, n, kl, ku):
+    A = rng.standard_normal((batch, n, n)) + 1j * rng.standard_normal((batch, n, n))
+    i, j = np.indices((n, n))
+    A[:, (i - j > kl) | (j - i > ku)] = 0.0
+    return A
+
+
+@pytest.mark.parametrize("n,batch,kl,ku", [(100, 3, 3, 5), (256, 2, 16, 16), (700, 2, 40, 10), (2304, 2, 48, 48),
+                                           (256, 1100, 16, 16), (300, 2, 0, 7)])
+def test_band_lu_and_solves_bitwise(lib, n, batch, kl, ku):
+    """The band-limited LU and solves (cirr_zgetrf_band, cirr_zgetrs_band) on
+    banded pencils give bitwise the factors, pivots and solutions of the dense
+    entries -- the skipped blocks are exact zeros -- and L's reported lower
+    bandwidth bounds its nonzeros."""
+    rng = np.random.default_rng(n + kl)
+    A = _banded(rng, batch, n, kl, ku)
+    outs = {}
+    for mode in ("dense", "band"):
+        F = cuda(A.copy())
+        ipiv = torch.empty((batch, n), dtype=torch.int32, device="cuda")
+        perm = torch.empty((batch, n), dtype=torch.int32, device="cuda")
+        mp = torch.empty(batch, dtype=torch.float64, device="cuda")
+        info = torch.empty(batch, dtype=torch.int32, device="cuda")
+        lbw = torch.zeros(batch, dtype=torch.int32, device="cuda")
+        if mode == "dense":
+            lib.call("cirr_zgetrf_batched", P(F), n, n, n * n, batch, P(ipiv), P(perm), P(mp), P(info),
+                     P(ws_lu(n, batch)), S())
+        else:
+            lib.call("cirr_zgetrf_band", P(F), n, n, n * n, batch, kl, ku, P(ipiv), P(perm), P(mp), P(info), P(lbw),
+                     P(ws_lu(n, batch)), S())
+        outs[mode] = (F, ipiv, perm, mp, lbw)
+    Fd, Fb = outs["dense"][0], outs["band"][0]
+    assert torch.equal(Fd, Fb)
+    assert torch.equal(outs["dense"][1], outs["band"][1]) and torch.equal(outs["dense"][3], outs["band"][3])
+    klL = max(kl, int(outs["band"][4].max().item()))
+    kuU = min(n - 1, kl + ku)
+    lu = Fb.cpu().numpy()
+    i, j = np.indices((n, n))
+    low = np.abs(lu[:, (i - j > klL)]).max(initial=0.0)
+    upp = np.abs(lu[:, (j - i > kuU)]).max(initial=0.0)
+    assert low == 0.0 and upp == 0.0, (klL, kuU, low, upp)
+    perm = outs["band"][2]
+    for K, use_dinv in ((8, False), (37, True), (37, False)):
+        dinv = 0
+        if use_dinv:
+            dinv_t = cuda(np.zeros(lib.call("cirr_diag_inv_bytes", n, batch), dtype=np.uint8))
+            lib.call("cirr_diag_inverses", P(Fb), n, n, n * n, batch, P(dinv_t), S())
+            dinv = P(dinv_t)
+        R = rng.standard_normal((1, n, K)) + 1j * rng.standard_normal((1, n, K))
+        Rt = cuda(R)
+        rhs_of = cuda(np.zeros(batch, dtype=np.int32))
+        Yd = torch.empty((batch, n, K), dtype=torch.complex128, device="cuda")
+        Yb = torch.empty_like(Yd)
+        lib.call("cirr_zgetrs_batched", P(Fb), n, n, n * n, batch, P(perm), P(Rt), K, n * K, P(rhs_of), K, P(Yd), K,
+                 n * K, dinv, S())
+        lib.call("cirr_zgetrs_band", P(Fb), n, n, n * n, batch, 0, batch, P(perm), P(Rt), K, n * K, P(rhs_of), K,
+                 P(Yb), K, n * K, dinv, 0, 0, 0, 0, 0, 0, 0, klL, kuU, S())
+        assert torch.equal(Yd, Yb), (K, use_dinv)
+        y = Yb.cpu().numpy()
+        for b in (0, batch - 1):
+            res = np.linalg.norm(A[b] @ y[b] - R[0]) / (np.linalg.norm(A[b]) * np.linalg.norm(y[b]))
+            assert res < 1e-13, (K, b, res)
