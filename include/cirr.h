@@ -72,6 +72,10 @@ int cirr_zgetrf_band(cirr_cplx* pencils, int n, long long ld, long long pencil_s
  * (is_complex 0) or complex128 matrix, raised with atomicMax (zero out first;
  * one call per matrix gives the union of A's and B's patterns). */
 int cirr_bandwidth(const void* M, int is_complex, int n, long long ld, int* out, cudaStream_t stream);
+/* cirr_bandwidth for count (<= 65535) matrices at device addresses ptrs[i]
+ * (device int64[count]), one launch: out[2i], out[2i+1] (zeroed first). */
+int cirr_bandwidth_ptrs(const long long* ptrs, int count, int is_complex, int n, long long ld, int* out,
+                        cudaStream_t stream);
 /* ws bytes for cirr_zgetrf_batched (L11^-1 blocks; ws may be NULL: slower TRSM path) */
 long long cirr_zgetrf_ws_bytes(int n, int batch);
 

@@ -32,6 +32,7 @@ SIGNATURES = {
     "cirr_zgetrf_ws_bytes": [_I, _I],
     "cirr_zgetrf_band": [_P, _I, _L, _L, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P],
     "cirr_bandwidth": [_P, _I, _I, _L, _P, _P],
+    "cirr_bandwidth_ptrs": [_P, _I, _I, _I, _L, _P, _P],
     "cirr_zgetrs_band": [_P, _I, _L, _L, _I, _P, _I, _P, _P, _L, _L, _P, _I, _P, _L, _L, _P, _P, _I, _P, _I, _P,
                          _L, _L, _I, _I, _P],
     "cirr_zgetrs_batched": [_P, _I, _L, _L, _I, _P, _P, _L, _L, _P, _I, _P, _L, _L, _P, _P],

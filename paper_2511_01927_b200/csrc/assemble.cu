@@ -312,7 +312,11 @@ CIRR_API int cirr_hermitian_c(const cplx* A, int n, long long lda, double* out, 
 // n x n matrix M (real f64 or complex128, row-major, ld), each raised with
 // atomicMax (zero them first to start; call once per matrix for a union).
 namespace {
-__global__ void bandwidth_kernel(const double* __restrict__ M, int cw, int n, long long ld, int* __restrict__ out) {
+__global__ void bandwidth_kernel(const double* __restrict__ M0, const long long* __restrict__ ptrs, int cw, int n,
+                                 long long ld, int* __restrict__ out0) {
+  // matrix blockIdx.y: M0 itself, or the one at ptrs[blockIdx.y]
+  const double* M = ptrs ? reinterpret_cast<const double*>(ptrs[blockIdx.y]) : M0;
+  int* out = out0 + 2 * blockIdx.y;
   int kl = 0, ku = 0;
   const long long total = (long long)n * n;
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
@@ -338,7 +342,23 @@ CIRR_API int cirr_bandwidth(const void* M, int is_complex, int n, long long ld, 
   if (n <= 0 || ld < n || M == nullptr || out == nullptr) return CIRR_EINVAL;
   const long long total = (long long)n * n;
   const int blocks = (int)((total + 255) / 256 < 148 * 8 ? (total + 255) / 256 : 148 * 8);
-  bandwidth_kernel<<<blocks, 256, 0, stream>>>(reinterpret_cast<const double*>(M), is_complex ? 2 : 1, n, ld, out);
+  bandwidth_kernel<<<blocks, 256, 0, stream>>>(reinterpret_cast<const double*>(M), nullptr, is_complex ? 2 : 1, n, ld,
+                                               out);
+  CIRR_CHECK_LAUNCH();
+  return 0;
+}
+
+// cirr_bandwidth for count matrices at the device addresses ptrs[i]
+// (device int64[count]) in one launch: out[2 i], out[2 i + 1] (zeroed first).
+CIRR_API int cirr_bandwidth_ptrs(const long long* ptrs, int count, int is_complex, int n, long long ld, int* out,
+                                 cudaStream_t stream) {
+  if (n <= 0 || ld < n || ptrs == nullptr || out == nullptr || count < 0 || count > 65535) return CIRR_EINVAL;
+  if (count == 0) return 0;
+  const long long total = (long long)n * n;
+  long long bx = (total + 255) / 256;
+  const long long cap = (148LL * 8 + count - 1) / count;
+  if (bx > cap) bx = cap < 1 ? 1 : cap;
+  bandwidth_kernel<<<dim3((unsigned)bx, count), 256, 0, stream>>>(nullptr, ptrs, is_complex ? 2 : 1, n, ld, out);
   CIRR_CHECK_LAUNCH();
   return 0;
 }

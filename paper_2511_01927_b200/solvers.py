@@ -20,6 +20,7 @@ Deviations from the reference (all documented in DESIGN.md section 3):
 
 from __future__ import annotations
 
+import functools
 import struct
 import time
 from dataclasses import dataclass
@@ -58,6 +59,7 @@ _INTERLEAVE_MIN = int(__import__("os").environ.get("CIRR_INTERLEAVE_MIN", "32"))
 _BAND = bool(int(__import__("os").environ.get("CIRR_BAND", "1")))
 
 
+@functools.lru_cache(maxsize=64)
 def _band_lu_flops(n: int, kl: int, ku: int) -> float:
     """Algorithmic complex LU flops of an n x n pencil with kl sub- and ku
     superdiagonals: sum over columns of 8 (rows below) (columns right, fill-in
@@ -67,11 +69,16 @@ def _band_lu_flops(n: int, kl: int, ku: int) -> float:
     return float(8.0 * np.sum(np.minimum(kl, rest) * np.minimum(kl + ku, rest)))
 
 
-def _band_solve_flops(n: int, kl: int, ku: int, K: int) -> float:
-    """Complex flops of one L and one U solve with K right-hand sides on
-    factors of lower / upper bandwidth kl / ku (8 n^2 K dense)."""
+@functools.lru_cache(maxsize=64)
+def _band_solve_unit(n: int, kl: int, ku: int) -> float:
+    """Complex flops per right-hand side of one L and one U solve on factors
+    of lower / upper bandwidth kl / ku (8 n^2 dense)."""
     i = np.arange(n, dtype=np.float64)
-    return float(8.0 * K * (np.sum(np.minimum(i, kl)) + np.sum(np.minimum(n - 1.0 - i, ku))))
+    return float(8.0 * (np.sum(np.minimum(i, kl)) + np.sum(np.minimum(n - 1.0 - i, ku))))
+
+
+def _band_solve_flops(n: int, kl: int, ku: int, K: int) -> float:
+    return K * _band_solve_unit(n, kl, ku)
 # launches put the batch (pencils of a wave) on grid.y / grid.z, whose limit
 # is 65535: a wave never holds more pencils than that
 _MAX_WAVE_PENCILS = 65535
@@ -337,24 +344,27 @@ class DevicePencil:
         self.b = b.to("cuda", non_blocking=True).to(dt).contiguous()
         self.hermitian = bool(hermitian) if hermitian else self._device_symmetric()
 
-    def band_async(self, out):
-        """Enqueue the union band of A and B into the device int pair out
-        (zeroed by the caller): max(i - j), max(j - i) over the nonzeros."""
-        st = _stream()
-        for m in (self.a, self.b):
-            _lib.call("cirr_bandwidth", _ptr(m), 1 if self.complex else 0, self.n, self.n, _ptr(out), st)
-
     @staticmethod
     def bands(dps) -> list:
-        """(kl, ku) of each DevicePencil (cached on it): one device pass over
-        each uncached A and B, one read-back for all of them."""
+        """(kl, ku) of each DevicePencil (cached on it): one batched device pass
+        over the uncached A and B (cirr_bandwidth_ptrs, grouped by order and
+        dtype), one read-back for all of them."""
         todo = [d for d in dps if getattr(d, "_band", None) is None]
         if todo:
-            buf = _zeros((len(todo), 2), _torch().int32)
-            for i, d in enumerate(todo):
-                d.band_async(buf[i])
-            for d, (kl, ku) in zip(todo, buf.cpu().numpy().tolist()):
-                d._band = (int(kl), int(ku))
+            torch = _torch()
+            groups: dict = {}
+            for d in todo:
+                groups.setdefault((d.n, d.complex), []).append(d)
+            bufs = []
+            for (n, cx), ds in groups.items():
+                ptrs = _h2d(np.array([[d.a.data_ptr(), d.b.data_ptr()] for d in ds], dtype=np.int64).reshape(-1))
+                buf = _zeros((2 * len(ds), 2), torch.int32)
+                _lib.call("cirr_bandwidth_ptrs", _ptr(ptrs), 2 * len(ds), 1 if cx else 0, n, n, _ptr(buf), _stream())
+                bufs.append((ds, buf))
+            for ds, buf in bufs:
+                v = buf.cpu().numpy().reshape(len(ds), 2, 2).max(axis=1)
+                for d, (kl, ku) in zip(ds, v.tolist()):
+                    d._band = (int(kl), int(ku))
         return [d._band for d in dps]
 
     @classmethod
@@ -903,8 +913,8 @@ class _Engine:
                       n * Ks, _ptr(rhs_of), Ks, _ptr(Ysol), Ks, n * Ks, fac_args[1], *mom, self.klL, self.kuU,
                       self.stream)
         _work("solve_flops", Psolve * _band_solve_flops(n, self.klL, self.kuU, Ks))
-        _work("solve_flops_exec", sum((b - a) * _band_solve_flops(n, self.klL, self.kuU, k)
-                                      for (a, b), k in zip(pen_idx, ks)))
+        _work("solve_flops_exec", _band_solve_unit(n, self.klL, self.kuU) * sum((b - a) * k
+                                                                             for (a, b), k in zip(pen_idx, ks)))
         _work("moment_flops", Ptot * 8.0 * n * K * moments)
         if fused:
             del Ysol

@@ -169,3 +169,27 @@ def test_interleaved_batch_isolates_errors():
                 continue
             assert len(rg.eigenvalues) == len(rw.eigenvalues)
             assert np.abs(rg.eigenvalues - rw.eigenvalues).max() <= 1e-12 * np.abs(rw.eigenvalues).max()
+
+
+@pytest.mark.parametrize("cx", [False, True])
+def test_bandwidth_detection(cx):
+    """cirr_bandwidth / cirr_bandwidth_ptrs report max(i - j) and max(j - i)
+    over the nonzeros (what the band-limited LU is cut to)."""
+    rng = np.random.default_rng(11)
+    n = 97
+    mats, want = [], []
+    for kl, ku in [(0, 0), (3, 7), (96, 1), (12, 96), (5, 5)]:
+        m = rng.standard_normal((n, n)) + (1j * rng.standard_normal((n, n)) if cx else 0)
+        i, j = np.indices((n, n))
+        m[(i - j > kl) | (j - i > ku)] = 0
+        mats.append(torch.from_numpy(np.ascontiguousarray(m)).cuda())
+        want.append((kl, ku))
+    st = torch.cuda.current_stream().cuda_stream
+    for m, w in zip(mats, want):
+        out = torch.zeros(2, dtype=torch.int32, device="cuda")
+        _lib.call("cirr_bandwidth", m.data_ptr(), int(cx), n, n, out.data_ptr(), st)
+        assert tuple(out.cpu().tolist()) == w
+    ptrs = torch.tensor([m.data_ptr() for m in mats], dtype=torch.int64, device="cuda")
+    out = torch.zeros((len(mats), 2), dtype=torch.int32, device="cuda")
+    _lib.call("cirr_bandwidth_ptrs", ptrs.data_ptr(), len(mats), int(cx), n, n, out.data_ptr(), st)
+    assert [tuple(r) for r in out.cpu().tolist()] == want
