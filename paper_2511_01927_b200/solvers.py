@@ -819,6 +819,8 @@ class _Engine:
         n = self.n
         self.klL = min(n - 1, max(self.kl, int(lbw.max(initial=0))))
         self.kuU = min(n - 1, self.kl + self.ku)
+        if _DEBUG:
+            print(f"[cirr] band kl={self.kl} ku={self.ku} -> factors klL={self.klL} kuU={self.kuU} (n={n})", flush=True)
         bad = (info != 0) | ~(minpiv >= PIVOT_REL_TOL * np.maximum(maxabs, 1e-300))
         for ci, c in enumerate(self.cs):
             c.stats.n_factorizations = len(c.fidx)
