@@ -19,6 +19,10 @@
 #include "common.cuh"
 #include <cstdlib>
 
+// herm_eig_kernel<SM, MODE>: the MODE 1 / 2 instances return before the
+// Jacobi loops (reported as unreachable)
+#pragma nv_diag_suppress 128
+
 namespace {
 
 constexpr int ET = 1024;
@@ -91,12 +95,23 @@ __device__ __forceinline__ void rr_pair(int round, int kk, int cp, int& p, int& 
   if (p > q) { int t = p; p = q; q = t; }
 }
 
-template <bool SM>
+// MODE 0: the whole solve (Jacobi on A' = L^-1 A~ L^-H in this CTA).
+// MODE 1: stop after A' -- write it as the rows of W (W[j][i] = A'[i][j], the
+//         column-as-row layout of cirr_orth) for the cooperative one-sided
+//         Jacobi across the GPU, keep L and A'.
+// MODE 2: finish from that SVD: A' HPD means its singular vectors are its
+//         eigenvectors and sigma its eigenvalues; every pair is checked by its
+//         Rayleigh quotient (an indefinite A' has lambda = -sigma somewhere),
+//         and a failing problem gets info = -2 for a MODE 0 rerun.
+// MODE 3: MODE 0 only for the problems MODE 2 flagged.
+template <bool SM, int MODE = 0>
 __global__ void __launch_bounds__(ET) herm_eig_kernel(const cplx* __restrict__ At, const cplx* __restrict__ Bt,
                                                       long long ldin, long long sin_, const int* __restrict__ kdim,
                                                       int kmax, void* ws, long long wstride,
                                                       cplx* __restrict__ lam, cplx* __restrict__ S, long long lds,
-                                                      long long sS, int* __restrict__ info) {
+                                                      long long sS, int* __restrict__ info,
+                                                      const cplx* __restrict__ Qt = nullptr,
+                                                      const double* __restrict__ sigma = nullptr) {
   extern __shared__ __align__(16) cplx hsm[];   // A and V when they fit (in_smem)
   __shared__ double red[32];
   __shared__ double rot_c[512];
@@ -106,6 +121,8 @@ __global__ void __launch_bounds__(ET) herm_eig_kernel(const cplx* __restrict__ A
   const int prob = blockIdx.x;
   const int k = kdim[prob];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (MODE == 3 && info[prob] != -2) return;
+  if (MODE == 2 && info[prob] != 0) return;   // Cholesky failure in MODE 1
   EigWs w = carve(ws, wstride, prob, kmax);
   const cplx* Ai = At + (long long)prob * sin_;
   const cplx* Bi = Bt + (long long)prob * sin_;
@@ -117,6 +134,55 @@ __global__ void __launch_bounds__(ET) herm_eig_kernel(const cplx* __restrict__ A
   const int ld = kmax;
   const int la = SM ? kmax + 1 : kmax;  // A / V row length (padded in shared memory: column walks hit distinct banks)
   if (tid == 0) s_flag = 0;
+  if (MODE == 2) {
+    // Rayleigh check and the eigenvectors from the SVD (Qt row r = u_r, sigma descending)
+    __syncthreads();
+    const cplx* Qp = Qt + (long long)prob * kmax * kmax;
+    const double* sg = sigma + (long long)prob * kmax;
+    const double smax = sg[0];
+    // V[i][r] = u_r[i]; T[i][r] = (A' u_r)[i]
+    for (int e = tid; e < k * k; e += ET) {
+      const int i = e / k, r = e % k;
+      V[i * ld + r] = Qp[(long long)r * kmax + i];
+    }
+    __syncthreads();
+    for (int e = tid; e < k * k; e += ET) {
+      const int i = e / k, r = e % k;
+      cplx v = cmk(0.0, 0.0);
+      for (int l = 0; l < k; ++l) cfma(v, A[i * ld + l], V[l * ld + r]);
+      T[i * ld + r] = v;
+    }
+    __syncthreads();
+    for (int r = wid; r < k; r += ET / 32) {
+      double re = 0.0, pad = 0.0;
+      for (int i = lane; i < kmax; i += 32) {
+        if (i < k) re += cconjmul(V[i * ld + r], T[i * ld + r]).x;
+        else pad += cabs2(Qp[(long long)r * kmax + i]);
+      }
+      re = warp_sum(re);
+      pad = warp_sum(pad);
+      if (lane == 0 && (!(fabs(re - sg[r]) <= 1e-10 * smax) || !(sg[r] > 1e-13 * smax) || pad > 1e-20)) s_flag = 1;
+    }
+    __syncthreads();
+    if (s_flag) {
+      if (tid == 0) info[prob] = -2;
+      return;
+    }
+    // eigenvalues ascending: sigma is descending, so rank r -> k - 1 - r; s = L^-H u
+    for (int r = tid; r < k; r += ET) lam[(long long)prob * kmax + (k - 1 - r)] = cmk(sg[r], 0.0);
+    cplx* Sp = S + (long long)prob * sS;
+    for (int c = tid; c < k; c += ET) {
+      const int rank = k - 1 - c;
+      for (int i = k - 1; i >= 0; --i) {
+        cplx v = V[i * ld + c];
+        for (int l = i + 1; l < k; ++l) cfms(v, cconj(L[l * ld + i]), T[l * ld + c]);
+        v = cscale(v, 1.0 / L[i * ld + i].x);
+        T[i * ld + c] = v;
+        Sp[(long long)i * lds + rank] = v;
+      }
+    }
+    return;
+  }
   // 1. symmetrise
   for (int e = tid; e < k * k; e += ET) {
     int r = e / k, c = e % k;
@@ -178,6 +244,15 @@ __global__ void __launch_bounds__(ET) herm_eig_kernel(const cplx* __restrict__ A
   }
   fro = sqrt(block_sum(fro, red));
   __syncthreads();
+  if (MODE == 1) {
+    // A' for the cooperative SVD: W[j][i] = A'[i][j] (T), zero padded to kmax
+    for (int e = tid; e < kmax * kmax; e += ET) {
+      const int j = e / kmax, i = e % kmax;
+      T[e] = (i < k && j < k) ? A[i * la + j] : cmk(0.0, 0.0);
+    }
+    if (tid == 0) info[prob] = 0;
+    return;
+  }
   // 4. parallel cyclic Jacobi
   const int cp = k + (k & 1), np = cp / 2;
   const double small = 1e-300 + 1e-18 * fro;
@@ -700,9 +775,15 @@ __global__ void __launch_bounds__(GT) gen_eig_kernel(const cplx* __restrict__ At
 }  // namespace
 
 // Workspace bytes per problem for cirr_small_eig.
-CIRR_API long long cirr_small_eig_ws_bytes(int kmax) {
-  return (long long)kmax * kmax * 16 * 4 + (long long)kmax * 16 * 4 + (long long)kmax * 8 * 4 + 256;
+static long long small_eig_slot(int kmax) {
+  return ((long long)kmax * kmax * 16 * 4 + (long long)kmax * 16 * 4 + (long long)kmax * 8 * 4 + 256 + 255) / 256 * 256;
 }
+// per-problem share of the cooperative-SVD path's shared region (Qt, sigma,
+// order, kept, sweeps and cirr_orth's own workspace), placed after the slots
+static long long small_eig_extra(int kmax) {
+  return ((long long)kmax * kmax * 16 * 3 + (long long)kmax * 16 * 2 + 8192 + 255) / 256 * 256;
+}
+CIRR_API long long cirr_small_eig_ws_bytes(int kmax) { return small_eig_slot(kmax) + small_eig_extra(kmax); }
 
 // Eigen-decomposition of nprob projected pencils (A~, B~), each k_b x k_b
 // (kdim device array, k_b <= kmax <= 1024), row-major with ld ldin and batch
@@ -713,8 +794,39 @@ CIRR_API int cirr_small_eig(int hermitian, const cplx* At, const cplx* Bt, long 
                             const int* kdim, int kmax, int nprob, void* ws, cplx* lam, cplx* S, long long lds,
                             long long sS, int* info, cudaStream_t stream) {
   if (kmax <= 0 || kmax > 1024 || nprob <= 0) return CIRR_EINVAL;
-  long long wstride = cirr_small_eig_ws_bytes(kmax);
-  wstride = (wstride + 255) / 256 * 256;
+  // per-problem slots of small_eig_slot bytes, then the shared region (the
+  // caller allocates nprob x cirr_small_eig_ws_bytes)
+  const long long wstride = small_eig_slot(kmax);
+  static const bool coop = !(getenv("CIRR_HERM_COOP") && getenv("CIRR_HERM_COOP")[0] == '0');
+  if (hermitian && kmax > 78 && nprob <= 64 && coop) {
+    // one-sided Jacobi of the HPD A' = L^-1 A~ L^-H across the whole GPU
+    // (cirr_orth's cooperative kernel) instead of one CTA per problem;
+    // MODE 2 checks every pair and MODE 3 redoes a problem whose A' was not
+    // definite
+    unsigned char* shared = reinterpret_cast<unsigned char*>(ws) + (long long)nprob * wstride;
+    const long long kk = (long long)kmax * kmax;
+    cplx* Qt = reinterpret_cast<cplx*>(shared);
+    double* sigma = reinterpret_cast<double*>(Qt + (long long)nprob * kk);
+    int* order = reinterpret_cast<int*>(sigma + (long long)nprob * kmax);
+    int* kept = order + (long long)nprob * kmax;
+    int* sweeps = kept + nprob;
+    unsigned char* ows = reinterpret_cast<unsigned char*>(((uintptr_t)(sweeps + 1) + 255) & ~(uintptr_t)255);
+    if ((ows - shared) + cirr_orth_ws_bytes(kmax, nprob) > (long long)nprob * small_eig_extra(kmax)) return CIRR_EINVAL;
+    herm_eig_kernel<false, 1><<<nprob, ET, 0, stream>>>(At, Bt, ldin, sin_, kdim, kmax, ws, wstride, lam, S, lds,
+                                                        sS, info);
+    CIRR_CHECK_LAUNCH();
+    // W = the T block of each slot (kmax x kmax rows, slot stride)
+    cplx* W0 = reinterpret_cast<cplx*>(reinterpret_cast<unsigned char*>(ws) + 3 * kk * 16);
+    CIRR_TRY(cirr_orth(W0, kmax, wstride / 16, kmax, kmax, nprob, 0.0, sigma, order, kept, Qt, kmax, kk, ows, sweeps,
+                       stream));
+    herm_eig_kernel<false, 2><<<nprob, ET, 0, stream>>>(At, Bt, ldin, sin_, kdim, kmax, ws, wstride, lam, S, lds,
+                                                        sS, info, Qt, sigma);
+    CIRR_CHECK_LAUNCH();
+    herm_eig_kernel<false, 3><<<nprob, ET, 0, stream>>>(At, Bt, ldin, sin_, kdim, kmax, ws, wstride, lam, S, lds,
+                                                        sS, info);
+    CIRR_CHECK_LAUNCH();
+    return 0;
+  }
   if (hermitian) {
     // A and V in shared memory for kmax <= 78 (2 kmax (kmax+1) complex <= 193 KB next
     // to the 16 KB of static rotation tables); CIRR_HERM_SMEM=0 disables

@@ -218,11 +218,16 @@ __global__ void __launch_bounds__(PTT, PTT == 128 ? 4 : 1) panel2_kernel(cplx* _
 // row interchanges an L entry can end up more than kl below the diagonal, and
 // the band-limited solves need L's final lower bandwidth.
 __global__ void swap_kernel(cplx* __restrict__ P, int n, long long ld, long long pstride, int k, int jb,
-                            const int* __restrict__ ipiv, int cend, int* __restrict__ lbw) {
+                            const int* __restrict__ ipiv, int cend, int* __restrict__ lbw, int kl) {
   const int other = k + (cend - k - jb);
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  // banded: the rows swapped here (<= k + jb + kl) have their L entries in
+  // columns >= k - max(kl, lbw) (lbw as of this launch: the earlier panels'
+  // drift and this panel's own, recorded before); the columns left of that
+  // are zeros in both rows
+  const int lmin = (lbw != nullptr && kl < n - 1) ? max(0, k - max(kl, lbw[blockIdx.y])) : 0;
   int bw = 0;
-  if (t < other) {
+  if (t < other && (t >= k || t >= lmin)) {
     const int col = t < k ? t : t + jb;
     cplx* A = P + (long long)blockIdx.y * pstride;
     const int* piv = ipiv + (long long)blockIdx.y * n;
@@ -446,7 +451,7 @@ static int getrf_impl(cplx* pencils, int n, long long ld, long long pencil_strid
         CIRR_TRY(launch_panel(pencils, n, ld, pencil_stride, batch, ki, NB, ipiv, minpiv, info, re, lbw, stream));
         {
           dim3 g((ki + ce - ki - NB + 255) / 256, batch);
-          swap_kernel<<<g, 256, 0, stream>>>(pencils, n, ld, pencil_stride, ki, NB, ipiv, ce, lbw);
+          swap_kernel<<<g, 256, 0, stream>>>(pencils, n, ld, pencil_stride, ki, NB, ipiv, ce, lbw, kl);
           CIRR_CHECK_LAUNCH();
         }
         const int right = ce - ki - NB;  // columns right of this panel that can be nonzero
@@ -471,7 +476,7 @@ static int getrf_impl(cplx* pencils, int n, long long ld, long long pencil_strid
     CIRR_TRY(launch_panel(pencils, n, ld, pencil_stride, batch, k, jb, ipiv, minpiv, info, re, lbw, stream));
     if (k + ce - k - jb > 0) {
       dim3 g((k + ce - k - jb + 255) / 256, batch);
-      swap_kernel<<<g, 256, 0, stream>>>(pencils, n, ld, pencil_stride, k, jb, ipiv, ce, lbw);
+      swap_kernel<<<g, 256, 0, stream>>>(pencils, n, ld, pencil_stride, k, jb, ipiv, ce, lbw, kl);
       CIRR_CHECK_LAUNCH();
     }
     const int rest = ce - k - jb;     // columns right of the panel that can be nonzero

@@ -430,6 +430,42 @@ def test_small_eig_general(lib, k):
     assert rel.max() < 1e-11
 
 
+@pytest.mark.parametrize("ks", [[100], [256, 200, 130], [90, 90]])
+def test_small_eig_hermitian_definite_batch(lib, ks):
+    """k > 78 with A~ positive definite (the projected stiffness of configs 3/5):
+    the one-sided Jacobi across the GPU (cirr_orth on A' = L^-1 A~ L^-H) gives
+    eigh's eigenvalues and B~-orthonormal eigenvectors; padded problems of
+    different sizes in one batch.  (The indefinite cases of
+    test_small_eig_hermitian take the per-CTA fallback.)"""
+    kmax, nb = max(ks), len(ks)
+    rng = np.random.default_rng(sum(ks))
+    A = np.zeros((nb, kmax, kmax), complex)
+    B = np.zeros((nb, kmax, kmax), complex)
+    for p_, k in enumerate(ks):
+        x = rng.standard_normal((k, k)) + 1j * rng.standard_normal((k, k))
+        A[p_, :k, :k] = x @ x.conj().T / k + np.diag(rng.uniform(0.5, 2.0, k))
+        y = rng.standard_normal((k, k)) + 1j * rng.standard_normal((k, k))
+        B[p_, :k, :k] = y @ y.conj().T / k + np.eye(k)
+    kd = torch.tensor(ks, dtype=torch.int32, device="cuda")
+    wsb = lib.call("cirr_small_eig_ws_bytes", kmax)
+    ws = torch.empty(nb * ((wsb + 255) // 256 * 256), dtype=torch.uint8, device="cuda")
+    lam = torch.zeros((nb, kmax), dtype=torch.complex128, device="cuda")
+    s = torch.zeros((nb, kmax, kmax), dtype=torch.complex128, device="cuda")
+    info = torch.zeros(nb, dtype=torch.int32, device="cuda")
+    lib.call("cirr_small_eig", 1, P(cuda(A)), P(cuda(B)), kmax, kmax * kmax, P(kd), kmax, nb, P(ws), P(lam), P(s),
+             kmax, kmax * kmax, P(info), S())
+    assert (info.cpu().numpy() == 0).all()
+    lh, sh = lam.cpu().numpy(), s.cpu().numpy()
+    for p_, k in enumerate(ks):
+        a, b = A[p_, :k, :k], B[p_, :k, :k]
+        w = sla.eigh(a, b, eigvals_only=True)
+        got, x = lh[p_, :k].real, sh[p_, :k, :k]
+        assert np.allclose(got, w, rtol=1e-10, atol=1e-12 * np.abs(w).max()), (p_, np.abs(got - w).max())
+        r = a @ x - (b @ x) * got[None, :]
+        assert np.abs(r).max() <= 1e-10 * (np.linalg.norm(a) + np.abs(got).max() * np.linalg.norm(b))
+        assert np.abs(x.conj().T @ b @ x - np.eye(k)).max() < 1e-10
+
+
 def test_small_eig_indefinite(lib):
     a = np.eye(2, dtype=complex)
     b = np.diag([1.0, -1.0]).astype(complex)
