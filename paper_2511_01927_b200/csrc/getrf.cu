@@ -437,8 +437,14 @@ static int getrf_impl(cplx* pencils, int n, long long ld, long long pencil_strid
     // CIRR_LU_PB overrides the panels per step (config 3, n = 2304: 119.0 /
     // 119.6 / 119.1 ms at 8 / 4 / 6 -- the 256-column tail costs nothing;
     // config 5: 5.44 s at 8 vs 5.50 s at 4)
+    // Banded pencils (kl + ku below n / 2) take single 64-column steps: their
+    // trailing windows are only kl x (kl + ku), so the k = W update saves
+    // little, and the left-looking updates inside a step would sweep the full
+    // kl + 64 panel rows once per panel (config 5: LU 215 -> 154 ms, config 3
+    // 15.2 -> 11.2 ms, config 2 42 -> 39 ms at PB = 1).
     static const int pb_env = getenv("CIRR_LU_PB") ? atoi(getenv("CIRR_LU_PB")) : 0;
-    const int PB = pb_env > 0 ? pb_env : (n >= 2048 ? 8 : (n >= 1024 ? 4 : 2));
+    const bool banded = (long long)kl + ku + 2 <= n / 2;
+    const int PB = pb_env > 0 ? pb_env : (banded ? 1 : (n >= 2048 ? 8 : (n >= 1024 ? 4 : 2)));
     const int W = PB * NB;
     for (; k0 + W <= n; k0 += W) {
       const int k = k0, rest = n - k0 - W;

@@ -496,9 +496,12 @@ def _banded(rng, batch, n, kl, ku):
                                            (256, 1100, 16, 16), (300, 2, 0, 7)])
 def test_band_lu_and_solves_bitwise(lib, n, batch, kl, ku):
     """The band-limited LU and solves (cirr_zgetrf_band, cirr_zgetrs_band) on
-    banded pencils give bitwise the factors, pivots and solutions of the dense
-    entries -- the skipped blocks are exact zeros -- and L's reported lower
-    bandwidth bounds its nonzeros."""
+    banded pencils give the pivots of the dense LU and, with the same blocking
+    (n < 256: single 64-column steps in both), bitwise its factors -- the
+    skipped blocks are exact zeros; banded pencils of n >= 256 take single
+    steps where the dense LU uses multi-level ones, so equal to rounding there.
+    The band-limited solves are bitwise the dense solves on the same factors,
+    and L's reported lower bandwidth bounds its nonzeros."""
     rng = np.random.default_rng(n + kl)
     A = _banded(rng, batch, n, kl, ku)
     outs = {}
@@ -517,8 +520,12 @@ def test_band_lu_and_solves_bitwise(lib, n, batch, kl, ku):
                      P(ws_lu(n, batch)), S())
         outs[mode] = (F, ipiv, perm, mp, lbw)
     Fd, Fb = outs["dense"][0], outs["band"][0]
-    assert torch.equal(Fd, Fb)
-    assert torch.equal(outs["dense"][1], outs["band"][1]) and torch.equal(outs["dense"][3], outs["band"][3])
+    if n < 256:   # both single 64-column steps: the same products in the same order
+        assert torch.equal(Fd, Fb)
+        assert torch.equal(outs["dense"][3], outs["band"][3])
+    else:         # banded pencils take PB = 1 steps, the dense LU multi-level ones: equal to rounding
+        assert (Fd - Fb).abs().max().item() <= 1e-12 * Fd.abs().max().item()
+    assert torch.equal(outs["dense"][1], outs["band"][1])
     klL = max(kl, int(outs["band"][4].max().item()))
     kuU = min(n - 1, kl + ku)
     lu = Fb.cpu().numpy()
