@@ -53,7 +53,7 @@ __device__ __forceinline__ int block_argmax(double best, int bi, double* rv, int
 }
 
 template <int PTT>
-__global__ void __launch_bounds__(PTT, PTT == 128 ? 4 : 1) panel2_kernel(cplx* __restrict__ P, int n, long long ld, long long pstride,
+__global__ void __launch_bounds__(PTT, PTT == 32 ? 16 : (PTT == 64 ? 8 : (PTT == 128 ? 4 : 1))) panel2_kernel(cplx* __restrict__ P, int n, long long ld, long long pstride,
                                                      int k, int jb, int* __restrict__ ipiv,
                                                      double* __restrict__ minpiv, int* __restrict__ info, int rend,
                                                      int* __restrict__ lbw) {
@@ -375,8 +375,12 @@ static int launch_panel(cplx* pencils, int n, long long ld, long long pstride, i
                         double* minpiv, int* info, int rend, int* lbw, cudaStream_t stream) {
   static const int env_t = getenv("CIRR_PANEL_T") ? atoi(getenv("CIRR_PANEL_T")) : 0;
   const int m = rend - k;   // rows the panel can have nonzero
-  const int t = env_t > 0 ? env_t : (m <= 512 && batch >= 1024 ? 128 : PT2);
-  if (t == 128)
+  const int t = env_t > 0 ? env_t : (batch >= 1024 ? (m <= 128 ? 32 : (m <= 512 ? 128 : PT2)) : PT2);
+  if (t == 32)
+    panel2_kernel<32><<<batch, 32, 0, stream>>>(pencils, n, ld, pstride, k, jb, ipiv, minpiv, info, rend, lbw);
+  else if (t == 64)
+    panel2_kernel<64><<<batch, 64, 0, stream>>>(pencils, n, ld, pstride, k, jb, ipiv, minpiv, info, rend, lbw);
+  else if (t == 128)
     panel2_kernel<128><<<batch, 128, 0, stream>>>(pencils, n, ld, pstride, k, jb, ipiv, minpiv, info, rend, lbw);
   else if (t == 256)
     panel2_kernel<256><<<batch, 256, 0, stream>>>(pencils, n, ld, pstride, k, jb, ipiv, minpiv, info, rend, lbw);
