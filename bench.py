@@ -24,8 +24,9 @@ full GEPs timed (1): a GEP takes minutes on the host.  Both arms print the same
 `config` dict.
 
 `per_config` (GPU arm, N=1): BASELINE configs 2 (one solve_multi_batch of the
-256 GEPs) and 5 (one n=8000 GEP), each device-timed and end to end, with the LU
-TF/s and the in-contour counts checked against the oracle fixtures.
+256 GEPs), 1, 3 and 5 (one solve_multi each), each device-timed and end to end,
+with the LU TF/s (band flops for the banded pencils) and the in-contour counts
+checked against the oracle fixtures.
 """
 
 from __future__ import annotations
@@ -308,9 +309,9 @@ def _lu_line(timer):
 
 
 def per_config_block():
-    """BASELINE configs 2 and 5 on the driver's clock.
+    """BASELINE configs 1, 2, 3 and 5 on the driver's clock.
     Contours and the oracle's in-contour counts come from the committed oracle
-    fixtures (tests/golden/oracle_config{2,5}.npz, the checker)."""
+    fixtures (tests/golden/oracle_config{1,2,3,5}.npz, the checker)."""
     import torch
 
     from paper_2511_01927_b200 import Contour, DevicePencil, SolverConfig, solve_multi, solve_multi_batch
@@ -345,32 +346,39 @@ def per_config_block():
     del dps, res, hps, mats
     torch.cuda.empty_cache()
 
-    # config 5: one n=8000 GEP (128 pencils of 0.95 GiB in one wave)
-    fix = np.load(os.path.join(gold, "oracle_config5.npz"))
-    cons = [Contour.from_json_dict(d) for d in json.loads(str(fix["contours"]))]
-    want = [len(fix[f"c{i}_eigs"]) for i in range(len(cons))]
-    a, b = W.config5_matrices(0)
-    cfg = SolverConfig(n_q=32, source_cols=64, n_moments=4)
-    dp = DevicePencil(a, b, hermitian=True)
-    solve_multi(dp, cons, cfg, seed=0)  # warm-up
-    ms, m, timer = _timed(lambda: solve_multi(dp, cons, cfg, seed=0))
-    got = [0 if r is None else len(r.eigenvalues) for r in m.results]
-    worst = 0.0
-    for i, r in enumerate(m.results):
-        ref = fix[f"c{i}_eigs"]
-        if r is not None and len(r.eigenvalues) == len(ref):
-            worst = max(worst, float(np.max(np.abs(r.eigenvalues - ref) / np.abs(ref))))
-    del dp
-    torch.cuda.empty_cache()
-    e2e_s, _ = _wall(lambda: solve_multi(HostPencil(a, b, True), cons, cfg, seed=0))
-    out["config5"] = {
-        "workload": "BASELINE config 5: n=8000 3-D FD GEP, 4 circles, N=32, L=64, M=4 (one solve_multi = one step)",
-        "ms_per_step": ms, "gep_per_s": 1e3 / ms, "eigenpairs_per_s": sum(got) / (ms / 1e3), "pencils": 128,
-        "e2e": {"value": 1.0 / e2e_s, "unit": "GEP/s", "seconds_per_step": e2e_s,
-                "h2d_bytes_per_step": int(a.nbytes + b.nbytes)},
-        **_lu_line(timer), "stage_ms_per_step": {k: round(v, 3) for k, v in sorted(timer.totals().items())},
-        "counts_equal_oracle": got == want, "eigenpairs": got, "max_rel_eig_diff_vs_oracle": worst,
-        "iterations": [0 if r is None else r.stats.iterations for r in m.results]}
+    # configs 1, 3, 5: one solve_multi each (config 5: 128 pencils of n=8000 in one wave)
+    single = {
+        1: ("BASELINE config 1: n=512 1-D FD GEP (tridiagonal), 2 circles, N=32, L=16, M=4", W.config1_matrices, (32, 16, 4)),
+        3: ("BASELINE config 3: n=2304 2-D FD GEP, 3 circles, N=32, L=32, M=4", W.config3_matrices, (32, 32, 4)),
+        5: ("BASELINE config 5: n=8000 3-D FD GEP, 4 circles, N=32, L=64, M=4", W.config5_matrices, (32, 64, 4)),
+    }
+    for cno, (label, mk, (nq, L, M)) in single.items():
+        fix = np.load(os.path.join(gold, f"oracle_config{cno}.npz"))
+        cons = [Contour.from_json_dict(d) for d in json.loads(str(fix["contours"]))]
+        want = [len(fix[f"c{i}_eigs"]) for i in range(len(cons))]
+        a, b = mk()
+        cfg = SolverConfig(n_q=nq, source_cols=L, n_moments=M)
+        dp = DevicePencil(a, b, hermitian=True)
+        solve_multi(dp, cons, cfg, seed=0)  # warm-up
+        ms, m, timer = _timed(lambda: solve_multi(dp, cons, cfg, seed=0), reps=3)
+        got = [0 if r is None else len(r.eigenvalues) for r in m.results]
+        worst = 0.0
+        for i, r in enumerate(m.results):
+            ref = fix[f"c{i}_eigs"]
+            if r is not None and len(r.eigenvalues) == len(ref):
+                worst = max(worst, float(np.max(np.abs(r.eigenvalues - ref) / np.abs(ref))))
+        del dp
+        torch.cuda.empty_cache()
+        e2e_s, _ = _wall(lambda: solve_multi(HostPencil(a, b, True), cons, cfg, seed=0), reps=3)
+        out[f"config{cno}"] = {
+            "workload": label + " (one solve_multi = one step)",
+            "ms_per_step": ms, "gep_per_s": 1e3 / ms, "eigenpairs_per_s": sum(got) / (ms / 1e3),
+            "pencils": nq * len(cons), "n": int(a.shape[0]),
+            "e2e": {"value": 1.0 / e2e_s, "unit": "GEP/s", "seconds_per_step": e2e_s,
+                    "h2d_bytes_per_step": int(a.nbytes + b.nbytes)},
+            **_lu_line(timer), "stage_ms_per_step": {k: round(v, 3) for k, v in sorted(timer.totals().items())},
+            "counts_equal_oracle": got == want, "eigenpairs": got, "max_rel_eig_diff_vs_oracle": worst,
+            "iterations": [0 if r is None else r.stats.iterations for r in m.results]}
     torch.cuda.empty_cache()
     return out
 
@@ -507,6 +515,14 @@ def run_cirr(args):
                                             + vwork.get("moment_flops", 0.0)) / args.steps,
                 "max_rel_eig_diff_vs_record": diff}
 
+    # per-config block before the CPU samples: the host BLAS threads those
+    # leave behind slow the host-side work of config 2's batch (94 vs 74 ms)
+    per_cfg = None
+    if rank == 0 and world == 1 and not args.no_per_config:
+        del dp
+        torch.cuda.empty_cache()
+        per_cfg = per_config_block()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         passes = max(iters) if iters else 8
@@ -523,12 +539,6 @@ def run_cirr(args):
             cpu["single_thread"] = {"value": 1.0 / per1, "unit": UNIT, "cores": 1, "sample": desc1}
         except ImportError:
             pass
-
-    per_cfg = None
-    if rank == 0 and world == 1 and not args.no_per_config:
-        del dp
-        torch.cuda.empty_cache()
-        per_cfg = per_config_block()
 
     if rank == 0:
         line = {

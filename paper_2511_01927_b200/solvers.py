@@ -270,6 +270,18 @@ def _dense(m) -> np.ndarray:
     return np.asarray(m)
 
 
+_HOST_POOL = None
+
+
+def _host_pool():
+    global _HOST_POOL
+    if _HOST_POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+
+        _HOST_POOL = ThreadPoolExecutor(max_workers=8, thread_name_prefix="cirr-stage")
+    return _HOST_POOL
+
+
 def _upload(torch, x: np.ndarray):
     """Host matrix -> device.  Large matrices go through pinned staging (torch's
     caching host allocator) and an async copy: config 4's 134 MB A takes
@@ -372,6 +384,60 @@ class DevicePencil:
         if isinstance(pencil, DevicePencil):
             return pencil
         return cls(pencil.a, pencil.b, getattr(pencil, "hermitian", None))
+
+    @classmethod
+    def of_many(cls, pencils) -> list:
+        """``[DevicePencil.of(p) for p in pencils]`` with the host pencils of one
+        order and dtype staged into one pinned buffer by a few host threads
+        (numpy's copies release the GIL) and moved in one async H2D copy.
+        Config 2's 256 pencils: 38 ms as 512 pageable copies.  Each matrix
+        starts on a 256-byte boundary of the staging buffer."""
+        torch = _torch()
+        out = [p if isinstance(p, DevicePencil) else None for p in pencils]
+        groups: dict = {}
+        for i, p in enumerate(pencils):
+            if out[i] is not None:
+                continue
+            if isinstance(p.a, torch.Tensor) or isinstance(p.b, torch.Tensor):
+                out[i] = cls.of(p)
+                continue
+            a = np.asarray(_dense(p.a))
+            b = np.asarray(_dense(p.b))
+            if a.ndim != 2 or a.shape[0] != a.shape[1] or a.shape != b.shape:
+                raise DimensionError("pencil matrices must be square and equally sized")
+            cx = any(np.iscomplexobj(m) and np.abs(m.imag).max(initial=0.0) != 0.0 for m in (a, b))
+            if not cx:
+                a, b = a.real, b.real
+            groups.setdefault((a.shape[0], cx), []).append((i, a, b, getattr(p, "hermitian", None)))
+        for (n, cx), items in groups.items():
+            if len(items) == 1:
+                i, a, b, h = items[0]
+                out[i] = cls(a, b, h)
+                continue
+            tdt = torch.complex128 if cx else torch.float64
+            esz = 16 if cx else 8
+            slot = -(-n * n * esz // 256) * 256 // esz
+            buf = torch.empty(len(items) * 2 * slot, dtype=tdt, pin_memory=True)
+            view = buf.numpy()
+
+            def fill(js, view=view, items=items, slot=slot, n=n):
+                for j in js:
+                    _, a, b, _ = items[j]
+                    view[(2 * j) * slot:(2 * j) * slot + n * n].reshape(n, n)[...] = a
+                    view[(2 * j + 1) * slot:(2 * j + 1) * slot + n * n].reshape(n, n)[...] = b
+
+            nt = min(8, len(items))
+            list(_host_pool().map(fill, [range(t, len(items), nt) for t in range(nt)]))
+            dev = buf.to("cuda", non_blocking=True)
+            for j, (i, _, _, h) in enumerate(items):
+                d = cls.__new__(cls)
+                d.complex = cx
+                d.n = n
+                d.a = dev[(2 * j) * slot:(2 * j) * slot + n * n].view(n, n)
+                d.b = dev[(2 * j + 1) * slot:(2 * j + 1) * slot + n * n].view(n, n)
+                d.hermitian = bool(h) if h else d._device_symmetric()
+                out[i] = d
+        return out
 
 
 def _is_symmetric(m: np.ndarray, rel_tol: float = 1e-12) -> bool:  # sparse.py:83-87
@@ -1724,7 +1790,7 @@ def solve_multi_batch(pencils, contours, cfg: SolverConfig | None = None, solver
     seeds = [0] * len(pencils) if seeds is None else [int(x) for x in seeds]
     if len(seeds) != len(pencils):
         raise DimensionError("need one seed per pencil")
-    dps = [DevicePencil.of(p) for p in pencils]
+    dps = DevicePencil.of_many(pencils)
     n = dps[0].n
     if any(d.n != n for d in dps):
         raise DimensionError("solve_multi_batch needs pencils of one size")

@@ -193,3 +193,36 @@ def test_bandwidth_detection(cx):
     out = torch.zeros((len(mats), 2), dtype=torch.int32, device="cuda")
     _lib.call("cirr_bandwidth_ptrs", ptrs.data_ptr(), len(mats), int(cx), n, n, out.data_ptr(), st)
     assert [tuple(r) for r in out.cpu().tolist()] == want
+
+
+def test_of_many_staged_upload():
+    """DevicePencil.of_many: host pencils of one order and dtype share one
+    pinned staging buffer and H2D copy; every matrix equals its per-pencil
+    upload bitwise, 256-byte aligned, with mixed orders, dtypes and pass-through."""
+    rng = np.random.default_rng(5)
+
+    class P:
+        def __init__(self, a, b, h=None):
+            self.a, self.b, self.hermitian = a, b, h
+
+    def sym(n, cx=False):
+        m = rng.standard_normal((n, n)) + (1j * rng.standard_normal((n, n)) if cx else 0)
+        return m + m.conj().T
+
+    items = []
+    for n in (37, 37, 37, 64, 64):
+        items.append(P(sym(n), np.eye(n) * 2.0 + 0.01 * sym(n), True))
+    items.append(P(sym(37, True), np.eye(37) + 0j, None))
+    items.append(P(sym(37, True), np.eye(37) + 0j, None))
+    items.append(P(sym(37) + 0j, np.eye(37) + 0j, None))  # complex dtype, zero imaginary part
+    items.append(S.DevicePencil(sym(37), np.eye(37), True))
+    items.append(P(torch.from_numpy(sym(37)), torch.eye(37, dtype=torch.float64), True))
+    got = S.DevicePencil.of_many(items)
+    for p, d in zip(items, got):
+        ref = S.DevicePencil.of(p)
+        if isinstance(p, S.DevicePencil):
+            assert d is p
+        assert d.n == ref.n and d.complex == ref.complex and d.hermitian == ref.hermitian
+        assert d.a.dtype == ref.a.dtype and d.a.is_contiguous() and d.b.is_contiguous()
+        assert d.a.data_ptr() % 256 == 0 and d.b.data_ptr() % 256 == 0
+        assert torch.equal(d.a, ref.a) and torch.equal(d.b, ref.b)
