@@ -271,6 +271,12 @@ int cirr_set_coop_ctas(int ctas);
  * (0 = every SM, the default).  Returns the previous cap. */
 int cirr_set_gemm_ctas(int ctas);
 
+/* Memory: callback run when a stream-ordered scratch allocation (split-K
+ * partials, look-back flags, WY workspaces) fails because another allocator
+ * holds the free HBM -- the Python host passes a function that empties
+ * PyTorch's cache; the allocation is then retried once.  NULL clears it. */
+void cirr_set_oom_handler(void (*fn)(void));
+
 #ifdef __cplusplus
 }
 #endif

@@ -13,7 +13,7 @@ import os
 from .errors import DeviceError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcirr.so")
+LIB_PATH = os.environ.get("CIRR_LIB") or os.path.join(_HERE, "libcirr.so")  # CIRR_LIB: A/B builds (dev)
 EINVAL = 100000
 
 _P = ctypes.c_void_p
@@ -70,6 +70,7 @@ SIGNATURES = {
     "cirr_target_sm": [],
     "cirr_set_coop_ctas": [_I],
     "cirr_set_gemm_ctas": [_I],
+    "cirr_set_oom_handler": [_P],
     "cirr_launch_count": [],
     "cirr_gemm_ptrs": [_I, _I, _I, _I, _I, _P, _L, _P, _L, _L, _P, _L, _L, _D, _I, _P],
     "cirr_gather_blocks": [_I, _P, _L, _P, _L, _L, _P],
@@ -97,8 +98,32 @@ def load(path: str = LIB_PATH):
         fn = getattr(lib, name)
         fn.argtypes = argt
         fn.restype = _RESTYPE.get(name, _I)
+    _install_oom_handler(lib)
     _lib = lib
     return lib
+
+
+_OOM_CB = None
+
+
+def _install_oom_handler(lib):
+    """cirr_set_oom_handler: a failed scratch allocation inside libcirr empties
+    PyTorch's caching allocator (which may hold the free HBM) and retries."""
+    global _OOM_CB
+    proto = ctypes.CFUNCTYPE(None)
+
+    def handler():
+        try:
+            import torch
+
+            torch.cuda.empty_cache()
+        except Exception:  # noqa: BLE001 -- a callback must not raise into C
+            pass
+
+    _OOM_CB = proto(handler)
+    lib.cirr_set_oom_handler.argtypes = [proto]
+    lib.cirr_set_oom_handler.restype = None
+    lib.cirr_set_oom_handler(_OOM_CB)
 
 
 def call(name: str, *args):

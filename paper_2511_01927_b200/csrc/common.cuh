@@ -21,6 +21,12 @@ inline void cirr_note_launch() { __atomic_fetch_add(&g_cirr_launches, 1, __ATOMI
 // tile scheduler of the persistent GEMM (gemm.cu); zero between launches.
 int* cirr_tile_counter(cudaStream_t stream);
 
+// Stream-ordered scratch (cudaMallocAsync).  When the pool cannot grow -- the
+// caller's allocator (PyTorch's caching allocator) holds the rest of HBM --
+// the handler set by cirr_set_oom_handler runs (it releases that cache) and the
+// allocation is retried once.
+cudaError_t cirr_malloc_async(void** p, size_t bytes, cudaStream_t stream);
+
 // Cap on the CTAs of the cooperative latency-bound kernels (0 = whole GPU);
 // set by cirr_set_coop_ctas so they can run beside the bulk GEMMs.
 extern int g_cirr_coop_cap;

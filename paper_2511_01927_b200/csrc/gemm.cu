@@ -158,6 +158,22 @@ int* cirr_tile_counter(cudaStream_t stream) {
   return pool->base + 2 * (pool->streams.size() - 1);
 }
 
+namespace {
+void (*g_oom_handler)(void) = nullptr;
+}
+
+CIRR_API void cirr_set_oom_handler(void (*fn)(void)) { g_oom_handler = fn; }
+
+cudaError_t cirr_malloc_async(void** p, size_t bytes, cudaStream_t stream) {
+  cudaError_t e = cudaMallocAsync(p, bytes, stream);
+  if (e == cudaErrorMemoryAllocation && g_oom_handler) {
+    cudaGetLastError();  // clear the failed allocation's error
+    g_oom_handler();
+    e = cudaMallocAsync(p, bytes, stream);
+  }
+  return e;
+}
+
 // Number of kernels launched by this library since load (host counter).
 CIRR_API long long cirr_launch_count(void) { return __atomic_load_n(&g_cirr_launches, __ATOMIC_RELAXED); }
 

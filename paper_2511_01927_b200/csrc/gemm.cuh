@@ -230,8 +230,8 @@ inline int gemm_launch(const GemmArgs& g0, cudaStream_t stream) {
   cudaError_t e;
   if (splits > 1) {
     g.splits = splits;
-    e = cudaMallocAsync(reinterpret_cast<void**>(&g.part), sizeof(cplx) * (size_t)splits * g.batch * g.M * g.N,
-                        stream);
+    e = cirr_malloc_async(reinterpret_cast<void**>(&g.part), sizeof(cplx) * (size_t)splits * g.batch * g.M * g.N,
+                          stream);
     if (e != cudaSuccess) return (int)e;
   }
   dim3 grid((g.N + GBN - 1) / GBN, (g.M + GBM - 1) / GBM, g.batch * g.splits);

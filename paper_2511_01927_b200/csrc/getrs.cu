@@ -605,7 +605,7 @@ int trsv_lookback(const cplx* LU, int n, long long ld, long long pstride, int ba
                   long long ldy, long long ystride, cudaStream_t stream, const int* pmap) {
   const int nblk = (n + TV_BS - 1) / TV_BS;
   int* flags = nullptr;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&flags), sizeof(int) * 2 * (size_t)nblk * batch, stream);
+  cudaError_t e = cirr_malloc_async(reinterpret_cast<void**>(&flags), sizeof(int) * 2 * (size_t)nblk * batch, stream);
   if (e != cudaSuccess) return (int)e;
   if ((e = cudaMemsetAsync(flags, 0, sizeof(int) * 2 * (size_t)nblk * batch, stream)) != cudaSuccess) return (int)e;
   dim3 g(nblk, batch);

@@ -362,13 +362,16 @@ static int orth_back_blocked(cplx* W, long long ldw, long long wstride, int n, i
   }
   cplx *VT = nullptr, *X = nullptr, *Gm = nullptr, *T = nullptr, *Wk = nullptr, *Wk2 = nullptr;
   const size_t nc = (size_t)n * c * nprob;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&VT), sizeof(cplx) * nc, stream);
-  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&X), sizeof(cplx) * nc, stream);
+  cudaError_t e = cirr_malloc_async(reinterpret_cast<void**>(&VT), sizeof(cplx) * nc, stream);
+  if (e == cudaSuccess) e = cirr_malloc_async(reinterpret_cast<void**>(&X), sizeof(cplx) * nc, stream);
   if (e == cudaSuccess)
-    e = cudaMallocAsync(reinterpret_cast<void**>(&Gm), sizeof(cplx) * (size_t)2 * WYB * WYB * nprob, stream);
+    e = cirr_malloc_async(reinterpret_cast<void**>(&Gm), sizeof(cplx) * (size_t)2 * WYB * WYB * nprob, stream);
   if (e == cudaSuccess)
-    e = cudaMallocAsync(reinterpret_cast<void**>(&Wk), sizeof(cplx) * (size_t)2 * WYB * c * nprob, stream);
-  if (e != cudaSuccess) return (int)e;
+    e = cirr_malloc_async(reinterpret_cast<void**>(&Wk), sizeof(cplx) * (size_t)2 * WYB * c * nprob, stream);
+  if (e != cudaSuccess) {
+    for (cplx* q : {VT, X, Gm}) if (q) cudaFreeAsync(q, stream);
+    return (int)e;
+  }
   T = Gm + (size_t)WYB * WYB * nprob;
   Wk2 = Wk + (size_t)WYB * c * nprob;
   const long long sv = (long long)n * c;

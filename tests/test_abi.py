@@ -13,7 +13,7 @@ LIB = os.path.join(ROOT, "paper_2511_01927_b200", "libcirr.so")
 
 def declared():
     text = open(os.path.join(ROOT, "include", "cirr.h")).read()
-    return sorted(set(re.findall(r"^(?:int|long long)\s+(cirr_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^(?:int|long long|void)\s+(cirr_\w+)\s*\(", text, re.M)))
 
 
 @pytest.fixture(scope="module")
