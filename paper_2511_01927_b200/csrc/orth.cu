@@ -32,6 +32,72 @@ constexpr int JB_MAX = 8;   // rows per Jacobi block (fewer for wide blocks: 4 *
 __device__ long long g_orth_phase[4];
 #define ORTH_MARK(i) do { if (blockIdx.x == 0 && threadIdx.x == 0) g_orth_phase[i] = clock64(); } while (0)
 
+// One Householder step of the QR of S (rows of W are the columns of S): the
+// reflector of column j (one CTA per problem), then H_j^H applied to columns
+// j+1 .. qend-1 (one CTA per problem x column), a grid barrier after each.
+__device__ void householder_step(cplx* __restrict__ W, long long ldw, long long wstride, int n, int c, int nprob,
+                                 int j, int qend, cplx* __restrict__ tau, unsigned* bar, double (*red)[HT / 32],
+                                 double* sred) {
+  const int G = gridDim.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (int p = blockIdx.x; p < nprob; p += G) {
+    cplx* x = W + (long long)p * wstride + (long long)j * ldw;
+    double sq = 0.0;
+    for (int i = j + 1 + tid; i < n; i += HT) sq += cabs2(x[i]);
+    sq = block_sum(sq, sred);
+    const cplx alpha = x[j];
+    cplx t = cmk(0.0, 0.0);
+    if (sq != 0.0 || alpha.y != 0.0) {
+      double beta = sqrt(alpha.x * alpha.x + alpha.y * alpha.y + sq);
+      beta = alpha.x >= 0.0 ? -beta : beta;
+      t = cmk((beta - alpha.x) / beta, -alpha.y / beta);
+      const cplx scal = crecip(cmk(alpha.x - beta, alpha.y));
+      for (int i = j + 1 + tid; i < n; i += HT) x[i] = cmul(x[i], scal);
+      __syncthreads();
+      if (tid == 0) x[j] = cmk(beta, 0.0);
+    }
+    if (tid == 0) tau[(long long)p * c + j] = t;
+  }
+  grid_barrier(bar, G);
+  const int rest = qend - j - 1;
+  const long long items = (long long)nprob * (rest > 0 ? rest : 0);
+  for (long long it = blockIdx.x; it < items; it += G) {
+    const int p = (int)(it / rest), q = j + 1 + (int)(it % rest);
+    const cplx t = tau[(long long)p * c + j];
+    if (t.x == 0.0 && t.y == 0.0) continue;
+    const cplx* v = W + (long long)p * wstride + (long long)j * ldw;
+    cplx* y = W + (long long)p * wstride + (long long)q * ldw;
+    double wr = 0.0, wi = 0.0;
+    for (int i = j + tid; i < n; i += HT) {
+      const cplx vi = i == j ? cmk(1.0, 0.0) : v[i];
+      const cplx g = cconjmul(vi, y[i]);
+      wr += g.x;
+      wi += g.y;
+    }
+    wr = warp_sum(wr); wi = warp_sum(wi);
+    __syncthreads();
+    if (lane == 0) { red[0][wid] = wr; red[1][wid] = wi; }
+    __syncthreads();
+    wr = 0.0; wi = 0.0;
+    for (int w2 = 0; w2 < HT / 32; ++w2) { wr += red[0][w2]; wi += red[1][w2]; }
+    const cplx f = cmul(cconj(t), cmk(wr, wi));
+    for (int i = j + tid; i < n; i += HT) {
+      const cplx vi = i == j ? cmk(1.0, 0.0) : v[i];
+      cfms(y[i], vi, f);
+    }
+  }
+  grid_barrier(bar, G);
+}
+
+// Panel of the blocked QR: Householder steps j0 .. j1-1, each applied only to
+// the panel's own later columns (the rest of S gets the block as WY products).
+__global__ void __launch_bounds__(HT) qr_panel_kernel(cplx* __restrict__ W, long long ldw, long long wstride, int n,
+                                                      int c, int nprob, int j0, int j1, cplx* __restrict__ tau,
+                                                      unsigned* bar) {
+  __shared__ double red[4][HT / 32];
+  __shared__ double sred[32];
+  for (int j = j0; j < j1; ++j) householder_step(W, ldw, wstride, n, c, nprob, j, j1, tau, bar, red, sred);
+}
+
 // --------------------------------------------------------------------------
 // QR-preconditioned one-sided Jacobi (the production path).
 //
@@ -53,7 +119,7 @@ __global__ void __launch_bounds__(HT) qr_jacobi_kernel(cplx* __restrict__ W, lon
                                                         int* counters, cplx* __restrict__ Xc,
                                                         cplx* __restrict__ Jt, cplx* __restrict__ tau,
                                                         int max_sweeps, double tol, int* sweeps_out, int JB,
-                                                        int back) {
+                                                        int back, int do_qr) {
   __shared__ double red[4][HT / 32];
   __shared__ double sred[32];
   const int G = gridDim.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -61,55 +127,8 @@ __global__ void __launch_bounds__(HT) qr_jacobi_kernel(cplx* __restrict__ W, lon
   const long long cc = (long long)c * c;
   ORTH_MARK(0);
   // ---------------- A: Householder QR ----------------
-  for (int j = 0; j < jmax; ++j) {
-    for (int p = blockIdx.x; p < nprob; p += G) {
-      cplx* x = W + (long long)p * wstride + (long long)j * ldw;
-      double sq = 0.0;
-      for (int i = j + 1 + tid; i < n; i += HT) sq += cabs2(x[i]);
-      sq = block_sum(sq, sred);
-      const cplx alpha = x[j];
-      cplx t = cmk(0.0, 0.0);
-      if (sq != 0.0 || alpha.y != 0.0) {
-        double beta = sqrt(alpha.x * alpha.x + alpha.y * alpha.y + sq);
-        beta = alpha.x >= 0.0 ? -beta : beta;
-        t = cmk((beta - alpha.x) / beta, -alpha.y / beta);
-        const cplx scal = crecip(cmk(alpha.x - beta, alpha.y));
-        for (int i = j + 1 + tid; i < n; i += HT) x[i] = cmul(x[i], scal);
-        __syncthreads();
-        if (tid == 0) x[j] = cmk(beta, 0.0);
-      }
-      if (tid == 0) tau[(long long)p * c + j] = t;
-    }
-    grid_barrier(bar, G);
-    const int rest = c - j - 1;
-    const long long items = (long long)nprob * rest;
-    for (long long it = blockIdx.x; it < items; it += G) {
-      const int p = (int)(it / rest), q = j + 1 + (int)(it % rest);
-      const cplx t = tau[(long long)p * c + j];
-      if (t.x == 0.0 && t.y == 0.0) continue;
-      const cplx* v = W + (long long)p * wstride + (long long)j * ldw;
-      cplx* y = W + (long long)p * wstride + (long long)q * ldw;
-      double wr = 0.0, wi = 0.0;
-      for (int i = j + tid; i < n; i += HT) {
-        const cplx vi = i == j ? cmk(1.0, 0.0) : v[i];
-        const cplx g = cconjmul(vi, y[i]);
-        wr += g.x;
-        wi += g.y;
-      }
-      wr = warp_sum(wr); wi = warp_sum(wi);
-      __syncthreads();
-      if (lane == 0) { red[0][wid] = wr; red[1][wid] = wi; }
-      __syncthreads();
-      wr = 0.0; wi = 0.0;
-      for (int w2 = 0; w2 < HT / 32; ++w2) { wr += red[0][w2]; wi += red[1][w2]; }
-      const cplx f = cmul(cconj(t), cmk(wr, wi));
-      for (int i = j + tid; i < n; i += HT) {
-        const cplx vi = i == j ? cmk(1.0, 0.0) : v[i];
-        cfms(y[i], vi, f);
-      }
-    }
-    grid_barrier(bar, G);
-  }
+  if (do_qr)
+    for (int j = 0; j < jmax; ++j) householder_step(W, ldw, wstride, n, c, nprob, j, c, tau, bar, red, sred);
   ORTH_MARK(1);
   // ---------------- B: Jacobi on the rows of R ----------------
   // Xc[p][a][i] = conj(R[a][i]) (R[a][i] = W[p][i][a] for a <= i < c, a < jmax), Jt = I
@@ -347,6 +366,86 @@ __global__ void wy_tfac_kernel(const cplx* __restrict__ Gm, const cplx* __restri
   for (int e = t; e < WYB * WYB; e += blockDim.x) Tp[e] = sT[e / WYB][e % WYB];
 }
 }  // namespace
+
+namespace {
+// Panel j0 .. j0+nb-1 of the blocked QR as explicit reflectors: VT[p] (WYB x n,
+// row m = v_{j0+m}: zeros before j0+m, 1 on it) and Vn[p] = VT[p]^T (n x WYB).
+__global__ void qr_panel_v_kernel(const cplx* __restrict__ W, long long ldw, long long wstride, int n, int j0, int nb,
+                                  cplx* __restrict__ VT, cplx* __restrict__ Vn) {
+  const int p = blockIdx.z, m = blockIdx.y;
+  const int j = j0 + m;
+  const cplx* row = W + (long long)p * wstride + (long long)j * ldw;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const cplx v = m >= nb ? cmk(0.0, 0.0) : (i < j ? cmk(0.0, 0.0) : (i == j ? cmk(1.0, 0.0) : row[i]));
+    VT[(long long)p * WYB * n + (long long)m * n + i] = v;
+    Vn[(long long)p * n * WYB + (long long)i * WYB + m] = v;
+  }
+}
+}  // namespace
+
+// Phase A of cirr_orth blocked: panels of WYB columns factored by
+// qr_panel_kernel (cooperative, one CTA per problem x column), the rest of S
+// updated per panel as S_t -= V (T^H (V^H S_t)) on the batched GEMM.  In the
+// row layout of W (S_t^T = W_t, rest x n) the three products are
+// Q1 = conj(W_t) V (= conj(V^H S_t)^T), Q2 = Q1 T, W_t -= conj(Q2) V^T.
+// The per-column grid-wide pass over all later columns (~100 us per column
+// at n = 8000, c = 256, 4 problems) shrinks to the panel's own columns.
+static int orth_qr_blocked(cplx* W, long long ldw, long long wstride, int n, int c, int nprob, cplx* tau,
+                           unsigned* bar, int cap, cudaStream_t stream) {
+  const int jmax = c < n ? c : n;
+  cplx *VT = nullptr, *Vn = nullptr, *Gm = nullptr, *Q1 = nullptr;
+  const size_t nv = (size_t)n * WYB * nprob;
+  cudaError_t e = cirr_malloc_async(reinterpret_cast<void**>(&VT), sizeof(cplx) * 2 * nv, stream);
+  if (e == cudaSuccess)
+    e = cirr_malloc_async(reinterpret_cast<void**>(&Gm), sizeof(cplx) * (size_t)2 * WYB * WYB * nprob, stream);
+  if (e == cudaSuccess)
+    e = cirr_malloc_async(reinterpret_cast<void**>(&Q1), sizeof(cplx) * (size_t)2 * WYB * c * nprob, stream);
+  if (e != cudaSuccess) {
+    for (cplx* q : {VT, Gm}) if (q) cudaFreeAsync(q, stream);
+    return (int)e;
+  }
+  Vn = VT + nv;
+  cplx* T = Gm + (size_t)WYB * WYB * nprob;
+  cplx* Q2 = Q1 + (size_t)WYB * c * nprob;
+  const long long sv = (long long)n * WYB, sq = (long long)c * WYB, st = (long long)WYB * WYB;
+  int rc = 0;
+  for (int j0 = 0; rc == 0 && j0 < jmax; j0 += WYB) {
+    const int nb = (jmax - j0) < WYB ? (jmax - j0) : WYB;
+    const int j1 = j0 + nb;
+    long long want = (long long)nprob * nb;
+    int grid = (int)(want < cap ? want : cap);
+    int j0v = j0, j1v = j1;
+    void* args[] = {&W, &ldw, &wstride, &n, &c, &nprob, &j0v, &j1v, &tau, &bar};
+    rc = (int)cudaLaunchCooperativeKernel((void*)qr_panel_kernel, dim3(grid), dim3(HT), args, 0, stream);
+    cirr_note_launch();
+    const int rest = c - j1;
+    if (rc || rest <= 0) continue;
+    {
+      dim3 g((n + 255) / 256, WYB, nprob);
+      qr_panel_v_kernel<<<g, 256, 0, stream>>>(W, ldw, wstride, n, j0, nb, VT, Vn);
+      rc = (int)cudaGetLastError();
+      cirr_note_launch();
+      if (rc) break;
+    }
+    // G = V^H V, T (larft)
+    rc = cirr_gemm(1, nb, nb, n, nprob, VT, n, sv, Vn, WYB, sv, Gm, WYB, st, 1.0, 0, stream);
+    if (rc) break;
+    wy_tfac_kernel<<<nprob, WYB, 0, stream>>>(Gm, tau, c, j0, nb, T);
+    rc = (int)cudaGetLastError();
+    cirr_note_launch();
+    if (rc) break;
+    cplx* Wt = W + (long long)j1 * ldw;
+    rc = cirr_gemm(1, rest, WYB, n, nprob, Wt, ldw, wstride, Vn, WYB, sv, Q1, WYB, sq, 1.0, 0, stream);
+    if (rc) break;
+    rc = cirr_gemm(0, rest, WYB, WYB, nprob, Q1, WYB, sq, T, WYB, st, Q2, WYB, sq, 1.0, 0, stream);
+    if (rc) break;
+    rc = cirr_gemm(1, rest, n, WYB, nprob, Q2, WYB, sq, VT, n, sv, Wt, ldw, wstride, -1.0, 1, stream);
+  }
+  cudaFreeAsync(VT, stream);
+  cudaFreeAsync(Gm, stream);
+  cudaFreeAsync(Q1, stream);
+  return rc;
+}
 
 // Phase C of cirr_orth as Level-3 products: with V^T = the reflector rows of W
 // (unit diagonal, zeros before it) and X = [J_kept; 0] (n x c), apply the WY
@@ -680,8 +779,20 @@ CIRR_API int cirr_orth(cplx* W, long long ldw, long long wstride, int n, int c, 
   // for wide blocks; one reflector at a time inside the kernel for narrow ones
   static const int wy_env = getenv("CIRR_ORTH_WY") ? atoi(getenv("CIRR_ORTH_WY")) : -1;
   int back = (wy_env >= 0 ? wy_env == 0 : c < 64) ? 1 : 0;
+  // A (Householder QR) blocked for wide blocks: panels of WYB columns plus WY
+  // updates of the rest on the GEMM (CIRR_ORTH_QRB=0: one column at a time
+  // inside the cooperative kernel)
+  static const int qrb_env = getenv("CIRR_ORTH_QRB") ? atoi(getenv("CIRR_ORTH_QRB")) : -1;
+  int do_qr = (qrb_env >= 0 ? qrb_env == 0 : (c < 64 || n < 1024)) ? 1 : 0;
+  if (!do_qr) {
+    int pcap = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pcap, qr_panel_kernel, HT, 0);
+    pcap = sms * (pcap < 2 ? pcap : 2);
+    if (g_cirr_coop_cap > 0 && pcap > g_cirr_coop_cap) pcap = g_cirr_coop_cap;
+    CIRR_TRY(orth_qr_blocked(W, ldw, wstride, n, c, nprob, tau, bar, pcap < 1 ? 1 : pcap, stream));
+  }
   void* args[] = {&W, &ldw, &wstride, &n, &c, &nprob, &rel_tol, &sigma, &order, &kept, &Qt, &ldq, &qstride,
-                  &bar, &counters, &Xc, &Jt, &tau, &max_sweeps, &tol, &sweeps_out, &jb, &back};
+                  &bar, &counters, &Xc, &Jt, &tau, &max_sweeps, &tol, &sweeps_out, &jb, &back, &do_qr};
   e = cudaLaunchCooperativeKernel((void*)qr_jacobi_kernel, dim3(grid), dim3(HT), args, jsmem, stream);
   cirr_note_launch();
   if (e != cudaSuccess) return (int)e;
