@@ -724,9 +724,12 @@ static int getrs_impl(const cplx* LU, int n, long long ld, long long pencil_stri
   // the TMA path is still faster: 18.7 ms vs 24.3 ms for 64 pencils, n = 4096)
   cirr::OperandMaps mT, mY;
   static const int bn_env = getenv("CIRR_SOLVE_BN") ? atoi(getenv("CIRR_SOLVE_BN")) : 0;
-  const int BN = bn_env > 0 ? bn_env : cirr::pick_tile_n(K);
+  // swizzled B boxes for the right-hand sides (CIRR_SOLVE_BSWZ=0: one plain box per stage)
+  static const bool kBswz = getenv("CIRR_SOLVE_BSWZ") ? atoi(getenv("CIRR_SOLVE_BSWZ")) != 0 : true;
+  const int BN = bn_env > 0 ? bn_env : cirr::pick_tile_n(K, kBswz);
   bool tma = solve_tma_path(n, K) && cirr::encode_a_map(&mT.a, LU, n, n, nfac, ld, pencil_stride) == 0 &&
-             cirr::encode_c128_map(&mY.b, Y, K, n, batch, ldy, ystride, BN, cirr::PBK) == 0 &&
+             (kBswz ? cirr::encode_b_swz_map(&mY.b, Y, K, n, batch, ldy, ystride)
+                    : cirr::encode_c128_map(&mY.b, Y, K, n, batch, ldy, ystride, BN, cirr::PBK)) == 0 &&
              cirr::encode_c128_map(&mY.c, Y, K, n, batch, ldy, ystride, BN, cirr::PBM) == 0;
   if (tma) {
     static bool dattr = false;
@@ -755,16 +758,16 @@ static int getrs_impl(const cplx* LU, int n, long long ld, long long pencil_stri
         if (lower) {
           if (nb2 > 0)  // rows i0+64.. : [L21inv L22inv] [Y_a; Y_b]
             CIRR_TRY(cirr::zgemm_sub_maps(mD, mY.b, mY.c, nb2, K, nb, batch, SNB, 0, i0, 0, i0 + SNB, 0, Y, ldy,
-                                          ystride, stream, /*beta=*/0, nblk2 * 2, slot, pmap, BN));
+                                          ystride, stream, /*beta=*/0, nblk2 * 2, slot, pmap, BN, kBswz));
           CIRR_TRY(cirr::zgemm_sub_maps(mD, mY.b, mY.c, na, K, na, batch, 0, 0, i0, 0, i0, 0, Y, ldy, ystride, stream,
-                                        /*beta=*/0, nblk2 * 2, slot, pmap, BN));
+                                        /*beta=*/0, nblk2 * 2, slot, pmap, BN, kBswz));
         } else {
           // rows i0.. : [U11inv U12inv] [Y_a; Y_b] first (reads the old Y_b), then Y_b
           CIRR_TRY(cirr::zgemm_sub_maps(mD, mY.b, mY.c, na, K, nb, batch, 0, 0, i0, 0, i0, 0, Y, ldy, ystride, stream,
-                                        /*beta=*/0, nblk2 * 2, slot, pmap, BN));
+                                        /*beta=*/0, nblk2 * 2, slot, pmap, BN, kBswz));
           if (nb2 > 0)
             CIRR_TRY(cirr::zgemm_sub_maps(mD, mY.b, mY.c, nb2, K, nb2, batch, SNB, SNB, i0 + SNB, 0, i0 + SNB, 0, Y,
-                                          ldy, ystride, stream, /*beta=*/0, nblk2 * 2, slot, pmap, BN));
+                                          ldy, ystride, stream, /*beta=*/0, nblk2 * 2, slot, pmap, BN, kBswz));
         }
         return 0;
       };
@@ -776,14 +779,14 @@ static int getrs_impl(const cplx* LU, int n, long long ld, long long pencil_stri
           if (bi > sb0) {  // Y[i0:i0+nb] -= L[i0:i0+nb, kb:i0] Y[kb:i0], kb >= s0 cut to the band
             const int kb = max(s0, i0 - up16(min(i0 - s0, klL)));
             CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, nb, K, i0 - kb, batch, i0, kb, kb, 0, i0, 0, Y, ldy,
-                                          ystride, stream, 1, 1, 0, pmap, BN));
+                                          ystride, stream, 1, 1, 0, pmap, BN, kBswz));
           }
           CIRR_TRY(apply_dinv(bi, true));
         }
         if (n - s1 > 0) {  // Y[s1:s1+m] -= L[s1:s1+m, kb:s1] Y[kb:s1] (m = klL rows below can be nonzero)
           const int kb = max(s0, s1 - up16(min(s1 - s0, klL)));
           CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, min(n - s1, klL), K, s1 - kb, batch, s1, kb, kb, 0, s1, 0,
-                                        Y, ldy, ystride, stream, 1, 1, 0, pmap, BN));
+                                        Y, ldy, ystride, stream, 1, 1, 0, pmap, BN, kBswz));
         }
       }
       const int nsb = (nblk2 + SBK - 1) / SBK;
@@ -796,7 +799,7 @@ static int getrs_impl(const cplx* LU, int n, long long ld, long long pencil_stri
             const int ke = min(s1, i0 + nb + up16(min(s1 - i0 - nb, kuU)));
             if (ke > i0 + nb)
               CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, nb, K, ke - i0 - nb, batch, i0, i0 + nb, i0 + nb, 0, i0,
-                                            0, Y, ldy, ystride, stream, 1, 1, 0, pmap, BN));
+                                            0, Y, ldy, ystride, stream, 1, 1, 0, pmap, BN, kBswz));
           }
           CIRR_TRY(apply_dinv(bi, false));
           // rows i0.. are final for every entry: their moment rows now, while
@@ -806,7 +809,7 @@ static int getrs_impl(const cplx* LU, int n, long long ld, long long pencil_stri
         if (s0 > 0) {  // Y[r0:s0] -= U[r0:s0, s0:ke] Y[s0:ke] (rows within kuU above, their columns)
           const int r0 = max(0, s0 - kuU), ke = min(s1, s0 + up16(min(s1 - s0, kuU)));
           CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, s0 - r0, K, ke - s0, batch, r0, s0, s0, 0, r0, 0, Y, ldy,
-                                        ystride, stream, 1, 1, 0, pmap, BN));
+                                        ystride, stream, 1, 1, 0, pmap, BN, kBswz));
         }
       }
       return 0;
@@ -818,7 +821,7 @@ static int getrs_impl(const cplx* LU, int n, long long ld, long long pencil_stri
       diag_solve_kernel<true><<<gd, 256, kDiagSmem, stream>>>(LU, ld, pencil_stride, i0, nb, Y, ldy, ystride, K, pmap);
       CIRR_CHECK_LAUNCH();
       CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, min(n - i0 - nb, klL), K, nb, batch, i0 + nb, i0, i0, 0,
-                                    i0 + nb, 0, Y, ldy, ystride, stream, 1, 1, 0, pmap, BN));
+                                    i0 + nb, 0, Y, ldy, ystride, stream, 1, 1, 0, pmap, BN, kBswz));
     }
     for (int bi = nblk - 1; bi >= 0; --bi) {  // backward: U
       const int i0 = bi * SNB, nb = min(SNB, n - i0);
@@ -826,7 +829,7 @@ static int getrs_impl(const cplx* LU, int n, long long ld, long long pencil_stri
       CIRR_CHECK_LAUNCH();
       const int r0 = max(0, i0 - kuU);
       CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, i0 - r0, K, nb, batch, r0, i0, i0, 0, r0, 0, Y, ldy, ystride,
-                                    stream, 1, 1, 0, pmap, BN));
+                                    stream, 1, 1, 0, pmap, BN, kBswz));
     }
     return moments_rows(ms, Y, ldy, ystride, n, K, 0, n, stream);
   }

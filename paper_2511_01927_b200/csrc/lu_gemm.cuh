@@ -32,12 +32,21 @@ constexpr int P_A_BYTES = PBM * PBK * 16;
 constexpr int PRING = 8;                        // tile-id ring (producer runs <= PSTAGES tiles ahead)
 constexpr int PAK = 8;                          // complex columns per swizzled A box (128 bytes)
 constexpr int P_A_HALF = PBM * PAK * 16;        // one A box
+constexpr int P_B_BOX = PBK * PAK * 16;         // one swizzled 16 x 8 B box (2 KB)
 
 // Output tiles are 64 x BN.  The LU uses BN = 64; the blocked solves pick BN
 // from {64, 56, 48, 40, 32} to fit the right-hand-side width K (pick_tile_n:
 // the first pass's K = 32 runs as one 32-wide tile instead of a half-empty
 // 64-wide one).  Each consumer warp owns WI
 // 8-row blocks x WJ 8-column blocks of the tile (8 warps cover 8 x BN/8 blocks).
+//
+// BSW (the solves): the B slice arrives as BN/8 boxes of 16 x 8 with the
+// 128-byte swizzle, and the four k of each DMMA step are k = 2q + s inside an
+// 8-wide box (q = lane % 4, s = step parity), so the A- and B-fragment loads
+// of every quarter-warp hit eight distinct 16-byte bank groups.  Unswizzled,
+// the B loads are 4-way conflicted: harmless at BN = 64 (6 loads per 32 DMMAs;
+// the LU keeps it, the extra boxes cost it 0.6 %), but the narrow tiles (one
+// A and up to seven B loads per 4 WJ DMMAs) were shared-memory bound.
 template <int BN>
 struct TileCfg;
 template <> struct TileCfg<64> { static constexpr int WI = 4, WJ = 2; };
@@ -99,7 +108,7 @@ struct SubGemmGeom {
   const int* a_bmap;   // optional: the A operand of batch entry b is A entry a_bmap[b] (gathered solves)
 };
 
-template <int BN>
+template <int BN, bool BSW>
 static __global__ void __launch_bounds__(PTHREADS, 1) zgemm_sub_tma(const __grid_constant__ CUtensorMap mapA,
                                                              const __grid_constant__ CUtensorMap mapB,
                                                              const __grid_constant__ CUtensorMap mapC,
@@ -160,7 +169,14 @@ static __global__ void __launch_bounds__(PTHREADS, 1) zgemm_sub_tma(const __grid
           const int k0 = ks * PBK;
           tma_load3(base, &mapA, 2 * (g.a_col0 + k0), g.a_row0 + m0, ab, full + stage);
           tma_load3(base + P_A_HALF, &mapA, 2 * (g.a_col0 + k0 + PAK), g.a_row0 + m0, ab, full + stage);
-          tma_load3(base + P_A_BYTES, &mapB, 2 * (g.b_col0 + n0), g.b_row0 + k0, b, full + stage);
+          if constexpr (BSW) {
+#pragma unroll
+            for (int jb = 0; jb < BN / PAK; ++jb)
+              tma_load3(base + P_A_BYTES + jb * P_B_BOX, &mapB, 2 * (g.b_col0 + n0 + jb * PAK), g.b_row0 + k0, b,
+                        full + stage);
+          } else {
+            tma_load3(base + P_A_BYTES, &mapB, 2 * (g.b_col0 + n0), g.b_row0 + k0, b, full + stage);
+          }
           if (++stage == PSTAGES) { stage = 0; phase ^= 1; }
         }
         // C block of this tile: requested once the consumers released the
@@ -208,15 +224,20 @@ static __global__ void __launch_bounds__(PTHREADS, 1) zgemm_sub_tma(const __grid
         const unsigned As = psm_s + stage * STAGE;
         const unsigned Bs = As + P_A_BYTES;
 #pragma unroll
-        for (int kk = 0; kk < PBK; kk += 4) {
+        for (int ts = 0; ts < PBK / 4; ++ts) {
           cplx af[WI], bf[WJ];
+          // DMMA step ts covers k = 8 (ts / 2) + k8, k8 = 2q + (ts % 2) (BSW) or 4 (ts % 2) + q.
+          // A element (r, k): box k/8, row r (128 B), 16-B chunk (k%8) ^ (r%8);
+          // B element (k, c), BSW: box c/8, row k (128 B), 16-B chunk (c%8) ^ (k%8)
+          const int k8 = BSW ? 2 * (lane & 3) + (ts & 1) : 4 * (ts & 1) + (lane & 3);
+          const unsigned sw = (unsigned)(k8 ^ (lane >> 2)) << 4;
 #pragma unroll
-          for (int j = 0; j < WJ; ++j) bf[j] = lds_c(Bs + ((kk + (lane & 3)) * BN + wn + j * 8 + (lane >> 2)) * 16);
-          // A element (r, k): box k/8, row r (128 B), 16-B chunk (k%8) ^ (r%8)
-          const unsigned achunk = (((kk & 7) + (lane & 3)) ^ (lane >> 2)) << 4;
+          for (int j = 0; j < WJ; ++j)
+            bf[j] = BSW ? lds_c(Bs + ((wn + j * 8) / PAK) * P_B_BOX + ((ts >> 1) * 8 + k8) * 128 + sw)
+                        : lds_c(Bs + (((ts >> 1) * 8 + k8) * BN + wn + j * 8 + (lane >> 2)) * 16);
 #pragma unroll
           for (int i = 0; i < WI; ++i)
-            af[i] = lds_c(As + (kk >> 3) * P_A_HALF + (wm + i * 8 + (lane >> 2)) * 128 + achunk);
+            af[i] = lds_c(As + (ts >> 1) * P_A_HALF + (wm + i * 8 + (lane >> 2)) * 128 + sw);
 #pragma unroll
           for (int i = 0; i < WI; ++i)
 #pragma unroll
@@ -316,14 +337,25 @@ static inline int encode_a_map(CUtensorMap* map, const cplx* base, int cols, int
   return encode_c128_map(map, base, cols, rows, batch, ld, bstride, PAK, PBM, true);
 }
 
+// B-operand map of the solves: 16 x 8 boxes with the 128-byte swizzle (BSW).
+static inline int encode_b_swz_map(CUtensorMap* map, const cplx* base, int cols, int rows, int batch, long long ld,
+                                   long long bstride) {
+  return encode_c128_map(map, base, cols, rows, batch, ld, bstride, PAK, PBK, true);
+}
+
 // Tile width for a right-hand-side block of K columns: the smallest padded
 // width ceil(K / bn) * bn weighted by the measured efficiency of each tile
-// shape (n = 4096, 128 pencils: the 64-wide tile runs 32.9 TF/s, the 32-wide
-// 30.7, the 40- and 56-wide ~28.7, so K = 118 stays on 2 x 64 (65.3 ms per
-// pass vs 69.9 ms as 3 x 40) and K = 32 takes one 32-wide tile (17.9 vs 33.0 ms)).
-static inline int pick_tile_n(int K) {
+// shape (n = 4096, 128 pencils, padded TF/s relative to the 64-wide tile;
+// tools/solve_bn_sweep.sh).  Unswizzled B (BSW off) the narrow tiles were
+// shared-memory bound (56: 0.87, 48: 0.87, 40: 0.876, 32: 0.93); with the
+// swizzled boxes every width runs within 2.5 % of the 64-wide tile, so
+// K = 118 takes 3 x 40 (62.0 ms per pass vs 65.3 ms as 2 x 64), K = 110
+// 2 x 56 (58.6 vs 65.2 ms) and K = 32 one 32-wide tile.
+static inline int pick_tile_n(int K, bool bswz = true) {
   const int cand[5] = {64, 56, 48, 40, 32};
-  const double eff[5] = {1.0, 0.87, 0.87, 0.876, 0.93};
+  const double eff_plain[5] = {1.0, 0.87, 0.87, 0.876, 0.93};
+  const double eff_swz[5] = {1.0, 0.976, 0.997, 0.99, 0.997};
+  const double* eff = bswz ? eff_swz : eff_plain;
   int best = 64;
   double cost = (K + 63) / 64 * 64;
   for (int i = 1; i < 5; ++i) {
@@ -353,16 +385,22 @@ static inline int encode_pencil_maps(PencilMaps& pm, cplx* base, int n, long lon
 static inline int zgemm_sub_maps(const CUtensorMap& mapA, const CUtensorMap& mapB, const CUtensorMap& mapC, int M, int N,
                           int K, int batch, int a_row0, int a_col0, int b_row0, int b_col0, int c_row0, int c_col0,
                           cplx* C, long long ldc, long long sC, cudaStream_t stream, int beta = 1,
-                          int a_bmul = 1, int a_badd = 0, const int* a_bmap = nullptr, int bn = PBN) {
+                          int a_bmul = 1, int a_badd = 0, const int* a_bmap = nullptr, int bn = PBN,
+                          bool bswz = false) {
   if (M <= 0 || N <= 0 || K <= 0 || batch <= 0) return 0;
   static bool attr = false;
   static int sms = 0;
   if (!attr) {
-    cudaFuncSetAttribute(zgemm_sub_tma<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, TileBytes<64>::SMEM);
-    cudaFuncSetAttribute(zgemm_sub_tma<56>, cudaFuncAttributeMaxDynamicSharedMemorySize, TileBytes<56>::SMEM);
-    cudaFuncSetAttribute(zgemm_sub_tma<48>, cudaFuncAttributeMaxDynamicSharedMemorySize, TileBytes<48>::SMEM);
-    cudaFuncSetAttribute(zgemm_sub_tma<40>, cudaFuncAttributeMaxDynamicSharedMemorySize, TileBytes<40>::SMEM);
-    cudaFuncSetAttribute(zgemm_sub_tma<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, TileBytes<32>::SMEM);
+    cudaFuncSetAttribute(zgemm_sub_tma<64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TileBytes<64>::SMEM);
+    cudaFuncSetAttribute(zgemm_sub_tma<56, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TileBytes<56>::SMEM);
+    cudaFuncSetAttribute(zgemm_sub_tma<48, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TileBytes<48>::SMEM);
+    cudaFuncSetAttribute(zgemm_sub_tma<40, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TileBytes<40>::SMEM);
+    cudaFuncSetAttribute(zgemm_sub_tma<32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TileBytes<32>::SMEM);
+    cudaFuncSetAttribute(zgemm_sub_tma<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TileBytes<64>::SMEM);
+    cudaFuncSetAttribute(zgemm_sub_tma<56, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TileBytes<56>::SMEM);
+    cudaFuncSetAttribute(zgemm_sub_tma<48, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TileBytes<48>::SMEM);
+    cudaFuncSetAttribute(zgemm_sub_tma<40, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TileBytes<40>::SMEM);
+    cudaFuncSetAttribute(zgemm_sub_tma<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TileBytes<32>::SMEM);
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -378,14 +416,22 @@ static inline int zgemm_sub_maps(const CUtensorMap& mapA, const CUtensorMap& map
   // latency-bound kernels on other streams (the dynamic tile scheduler adapts)
   const int cap = (g_cirr_gemm_cap > 0 && g_cirr_gemm_cap < sms) ? g_cirr_gemm_cap : sms;
   const int grid = (int)(tiles < cap ? tiles : cap);
-  switch (bn) {
-    case 64: zgemm_sub_tma<64><<<grid, PTHREADS, TileBytes<64>::SMEM, stream>>>(mapA, mapB, mapC, g); break;
-    case 56: zgemm_sub_tma<56><<<grid, PTHREADS, TileBytes<56>::SMEM, stream>>>(mapA, mapB, mapC, g); break;
-    case 48: zgemm_sub_tma<48><<<grid, PTHREADS, TileBytes<48>::SMEM, stream>>>(mapA, mapB, mapC, g); break;
-    case 40: zgemm_sub_tma<40><<<grid, PTHREADS, TileBytes<40>::SMEM, stream>>>(mapA, mapB, mapC, g); break;
-    case 32: zgemm_sub_tma<32><<<grid, PTHREADS, TileBytes<32>::SMEM, stream>>>(mapA, mapB, mapC, g); break;
+#define CIRR_SUB_TMA(BNV, SW) \
+  zgemm_sub_tma<BNV, SW><<<grid, PTHREADS, TileBytes<BNV>::SMEM, stream>>>(mapA, mapB, mapC, g)
+  switch (bn * 2 + (bswz ? 1 : 0)) {
+    case 128: CIRR_SUB_TMA(64, false); break;
+    case 112: CIRR_SUB_TMA(56, false); break;
+    case 96: CIRR_SUB_TMA(48, false); break;
+    case 80: CIRR_SUB_TMA(40, false); break;
+    case 64: CIRR_SUB_TMA(32, false); break;
+    case 129: CIRR_SUB_TMA(64, true); break;
+    case 113: CIRR_SUB_TMA(56, true); break;
+    case 97: CIRR_SUB_TMA(48, true); break;
+    case 81: CIRR_SUB_TMA(40, true); break;
+    case 65: CIRR_SUB_TMA(32, true); break;
     default: return (int)cudaErrorInvalidValue;
   }
+#undef CIRR_SUB_TMA
   cirr_note_launch();
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : (int)e;
