@@ -42,3 +42,45 @@ def sum_over_ranks(value: float, device=None) -> float:
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
+
+
+def solve_multi_batch_sharded(pencils, contours, cfg=None, solver: str = "cirr", seeds=None, *, gather: bool = True,
+                              solve_fn=None):
+    """``solve_multi_batch`` over the ranks of the default process group (one
+    rank per GPU): rank r solves the contiguous block ``shard(len(pencils), r,
+    world)`` of the independent GEPs on its own device, with no data-path
+    collective.  ``gather=True`` hands every rank all results in input order
+    (one ``all_gather_object`` of the host-side results, after the solves);
+    ``gather=False`` returns ``(indices, results)`` of this rank's block.
+    ``contours`` / ``seeds`` as in solve_multi_batch (one list per pencil, or
+    one list for all).  ``solve_fn`` replaces solve_multi_batch (same
+    signature), e.g. to run the host logic without a GPU."""
+    import torch.distributed as dist
+
+    pencils = list(pencils)
+    contours = list(contours)
+    if contours and not isinstance(contours[0], (list, tuple)):
+        contours = [contours] * len(pencils)
+    if len(contours) != len(pencils):
+        raise ValueError("need one contour list per pencil")
+    seeds = [0] * len(pencils) if seeds is None else [int(x) for x in seeds]
+    if len(seeds) != len(pencils):
+        raise ValueError("need one seed per pencil")
+    on = dist.is_available() and dist.is_initialized()
+    rank, world = (dist.get_rank(), dist.get_world_size()) if on else (0, 1)
+    mine = shard(len(pencils), rank, world)
+    if solve_fn is None:
+        from .solvers import solve_multi_batch as solve_fn
+    res = solve_fn([pencils[i] for i in mine], [contours[i] for i in mine], cfg, solver,
+                   [seeds[i] for i in mine]) if mine else []
+    if not gather:
+        return mine, res
+    if world == 1:
+        return list(res)
+    parts = [None] * world
+    dist.all_gather_object(parts, (mine, list(res)))
+    out = [None] * len(pencils)
+    for idx, rs in parts:
+        for i, r in zip(idx, rs):
+            out[i] = r
+    return out
