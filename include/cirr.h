@@ -255,6 +255,17 @@ int cirr_transpose(int conj, const cirr_cplx* in, long long ldi, long long si, i
 int cirr_kde_eval(const double* ts, int nt, const double* eigs, int ne, double coef, double* out,
                   cudaStream_t stream);
 
+/* Int8 tensor-core path of the k = 512 trailing updates of K2 (no reference
+ * counterpart; the reference factors with SuperLU in FP64, linalg.py:55-71):
+ * C -= A B for `batch` complex128 problems (row-major, strides in elements) by
+ * the Ozaki splitting -- rows of A and columns of B scaled by powers of two and
+ * cut into eight signed 7-bit digits, the 36 digit products exact in int32 on
+ * tcgen05.mma kind::i8, recombined in integers and converted once to FP64.
+ * K must be a multiple of 32.  Error per k-term below 2^-53 rowmax(A) colmax(B). */
+int cirr_ozaki_zgemm_sub(const cirr_cplx* A, long long lda, long long sA, const cirr_cplx* B, long long ldb,
+                         long long sB, cirr_cplx* C, long long ldc, long long sC, int M, int N, int K, int batch,
+                         cudaStream_t stream);
+
 /* number of kernels this library has launched since it was loaded (host counter) */
 long long cirr_launch_count(void);
 

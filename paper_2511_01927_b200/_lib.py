@@ -75,6 +75,7 @@ SIGNATURES = {
     "cirr_gemm_ptrs": [_I, _I, _I, _I, _I, _P, _L, _P, _L, _L, _P, _L, _L, _D, _I, _P],
     "cirr_gather_blocks": [_I, _P, _L, _P, _L, _L, _P],
     "cirr_zero": [_P, _L, _P],
+    "cirr_ozaki_zgemm_sub": [_P, _L, _L, _P, _L, _L, _P, _L, _L, _I, _I, _I, _I, _P],
 }
 _RESTYPE = {"cirr_diag_inv_bytes": _L, "cirr_zgetrf_ws_bytes": _L, "cirr_small_eig_ws_bytes": _L, "cirr_launch_count": _L, "cirr_orth_ws_bytes": _L,
             "cirr_gen_eig_ws_bytes": _L, "cirr_gen_eig_vec_scratch_bytes": _L, "cirr_orth_cholqr2_ws_bytes": _L,

@@ -1,0 +1,504 @@
+// Complex128 GEMM update C -= A B on the 5th-generation tensor cores by the
+// Ozaki splitting: every row of A and every column of B is scaled by a power of
+// two and cut into eight signed 7-bit digits (int8 slices; 6 + 7 x 7 = 55 bits
+// below the row / column maximum), the digit products A_p B_q with p + q <= 7
+// are exact int32 sums on tcgen05.mma kind::i8 (SASS UTCIMMA) with the
+// accumulators of the eight weights d = p + q side by side in tensor memory
+// (8 x 64 columns = all 512), and the epilogue recombines them in integer
+// arithmetic (two int64 per element), converts once to FP64, applies the two
+// scales and subtracts from C.  The truncation error per k-term is below
+// 2^-53 rowmax(A) colmax(B): that of an FP64 GEMM up to the usual bound, with
+// integer (order-independent, bitwise reproducible) accumulation.
+//
+// Replaces, for the k = 512 trailing updates of the dense LU, the DMMA kernel
+// zgemm_sub_tma (lu_gemm.cuh): B200's FP64 tensor peak is 37.1 TF/s (measured,
+// tools/fp64_peak.cu), its int8 tensor peak 4.5 POPS; 36 slice products of the
+// real 2m x 2n x 2k embedding cost 288 mnk int8 operations per 8 mnk flops.
+//
+// Complex embedding: A' = [Re A | Im A] (m x 2k), and for complex column j of
+// B two rows of B'^T: [Re b_j ; -Im b_j] (real part of the product) and
+// [Im b_j ; Re b_j] (imaginary part), so the accumulator columns are
+// interleaved (re, im) like complex128 memory.
+//
+// Reference: this is the LU of z_j B - A behind linalg.py:55-71 (splu); the
+// reference calls SuperLU in FP64.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cfloat>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "ozaki.cuh"
+
+namespace cirr {
+namespace {
+
+constexpr int OS = 8;         // slices
+constexpr int OBM = 128;      // accumulator rows = TMEM lanes
+constexpr int OBN = 64;       // accumulator columns (real) = 32 complex columns
+constexpr int OKB = 64;       // bytes of K' per stage (rows of the 64-byte swizzle)
+constexpr int ONSTAGE = 2;
+constexpr int OTHREADS = 320; // warp 0: TMA producer, warp 1: MMA issuer, warps 2-9: epilogue
+constexpr int OA_SLICE = OBM * OKB, OB_SLICE = OBN * OKB;
+constexpr int OSTAGE = OS * (OA_SLICE + OB_SLICE);
+constexpr int OSMEM = ONSTAGE * OSTAGE + 1024 + 256;
+
+__device__ __forceinline__ unsigned osmem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void ombar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(osmem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void ombar_arrive(uint64_t* bar) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}" ::"r"(osmem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void ombar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}"
+               ::"r"(osmem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void ombar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(osmem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void otma_load4(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                           uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
+      ::"r"(osmem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(osmem_u32(bar)) : "memory");
+}
+// K-major operand tile with the 64-byte swizzle: rows of 64 bytes, groups of
+// eight rows 512 bytes apart (stride byte offset), descriptor version 1,
+// layout type 4 (SWIZZLE_64B).  A K step of 32 bytes advances the start address.
+__device__ __forceinline__ uint64_t oumma_desc(unsigned saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(512 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)4 << 61;
+  return d;
+}
+__device__ __forceinline__ void oumma_i8(unsigned tmem_d, uint64_t da, uint64_t db, unsigned idesc, unsigned acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}"
+      ::"r"(tmem_d), "l"(da), "l"(db), "r"(idesc), "r"(acc) : "memory");
+}
+__device__ __forceinline__ void oumma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(osmem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void otmem_ld16(unsigned taddr, unsigned* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr) : "memory");
+}
+
+struct OzGeom {
+  int M, N;          // rows, complex columns of C
+  int K2;            // bytes of K' = 2 K
+  int batch;
+  int tiles_m, tiles_n;
+  cplx* C; long long ldc, sC;
+  const double* sa;  // [batch][M]   2^(e_i - 6)
+  const double* sb;  // [batch][N]   2^(f_j - 6)
+};
+
+__global__ void __launch_bounds__(OTHREADS, 1) ozaki_gemm_kernel(const __grid_constant__ CUtensorMap mapA,
+                                                                 const __grid_constant__ CUtensorMap mapB, OzGeom g) {
+  extern __shared__ __align__(1024) uint8_t osmem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)osmem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(smem + ONSTAGE * OSTAGE);
+  uint64_t* empty = full + ONSTAGE;
+  uint64_t* tfull = empty + ONSTAGE;
+  uint64_t* tempty = tfull + 1;
+  unsigned* tmem_slot = (unsigned*)(tempty + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ONSTAGE; ++s) { ombar_init(&full[s], 1); ombar_init(&empty[s], 1); }
+    ombar_init(tfull, 1);
+    ombar_init(tempty, 8);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(osmem_u32(tmem_slot)) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const unsigned tmem = *tmem_slot;
+
+  const int per = g.tiles_m * g.tiles_n;
+  const int ntiles = per * g.batch;
+  const int nkb = g.K2 / OKB;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int it = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int b = t / per, r = t - b * per;
+        const int m0 = (r / g.tiles_n) * OBM, n0 = (r % g.tiles_n) * OBN;
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int st = it % ONSTAGE;
+          const unsigned ph = (it / ONSTAGE) & 1;
+          ombar_wait(&empty[st], ph ^ 1);
+          ombar_arrive_expect_tx(&full[st], OSTAGE);
+          uint8_t* base = smem + st * OSTAGE;
+#pragma unroll
+          for (int s = 0; s < OS; ++s) {
+            otma_load4(base + s * OA_SLICE, &mapA, kb * OKB, m0, s, b, &full[st]);
+            otma_load4(base + OS * OA_SLICE + s * OB_SLICE, &mapB, kb * OKB, n0, s, b, &full[st]);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // instruction descriptor: D = S32, A = B = signed int8, both K-major, N >> 3, M >> 4
+      constexpr unsigned idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((unsigned)(OBN >> 3) << 17) | ((unsigned)(OBM >> 4) << 24);
+      int it = 0, tl = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+        ombar_wait(tempty, (tl & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int st = it % ONSTAGE;
+          const unsigned ph = (it / ONSTAGE) & 1;
+          ombar_wait(&full[st], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const unsigned abase = osmem_u32(smem + st * OSTAGE), bbase = abase + OS * OA_SLICE;
+#pragma unroll
+          for (int ks = 0; ks < OKB / 32; ++ks) {
+#pragma unroll
+            for (int d = 0; d < OS; ++d) {
+#pragma unroll
+              for (int p = 0; p <= d; ++p) {
+                const int q = d - p;
+                oumma_i8(tmem + d * OBN, oumma_desc(abase + p * OA_SLICE + ks * 32),
+                         oumma_desc(bbase + q * OB_SLICE + ks * 32), idesc, (kb > 0 || ks > 0 || p > 0) ? 1u : 0u);
+              }
+            }
+          }
+          oumma_commit(&empty[st]);
+        }
+        oumma_commit(tfull);
+      }
+    }
+  } else {
+    // Eight epilogue warps: warp w reads TMEM lanes 32 (w % 4) .. + 31 (its
+    // hardware quadrant) and the 32-column half (w - 2) / 4 of every
+    // accumulator.  The weighted sum of the eight accumulators of an element
+    // is formed in two int64 (weights 2^-21 and 2^-49), converted once; the
+    // TMEM is handed back to the MMA warp before C is touched, so the next
+    // tile's products run under this tile's read-modify-write of C.
+    const int quad = warp & 3;
+    const int half = (warp - 2) >> 2;
+    int tl = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+      const int b = t / per, r = t - b * per;
+      const int m0 = (r / g.tiles_n) * OBM, n0 = (r % g.tiles_n) * OBN;
+      const int row = m0 + quad * 32 + lane;
+      const int col0 = (n0 >> 1) + half * 16;   // first complex column of this thread
+      const bool rok = row < g.M;
+      cplx* crow = g.C + (long long)b * g.sC + (long long)row * g.ldc + col0;
+      const double* sbp = g.sb + (long long)b * g.N + col0;
+      if (rok && col0 < g.N) {
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(crow));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(crow + 8));
+      }
+      const double sai = rok ? g.sa[(long long)b * g.M + row] : 0.0;
+      double v[32];
+      ombar_wait(tfull, tl & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+      for (int c = 0; c < 32; c += 16) {
+        unsigned v0[16], v1[16], v2[16], v3[16];
+        long long hi[16];
+        const unsigned ta = tmem + ((unsigned)(quad * 32) << 16) + half * 32 + c;
+        otmem_ld16(ta + 0 * OBN, v0);
+        otmem_ld16(ta + 1 * OBN, v1);
+        otmem_ld16(ta + 2 * OBN, v2);
+        otmem_ld16(ta + 3 * OBN, v3);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          hi[j] = ((long long)(int)v0[j] << 21) + ((long long)(int)v1[j] << 14) + ((long long)(int)v2[j] << 7) +
+                  (long long)(int)v3[j];
+        otmem_ld16(ta + 4 * OBN, v0);
+        otmem_ld16(ta + 5 * OBN, v1);
+        otmem_ld16(ta + 6 * OBN, v2);
+        otmem_ld16(ta + 7 * OBN, v3);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const long long lo = ((long long)(int)v0[j] << 21) + ((long long)(int)v1[j] << 14) +
+                               ((long long)(int)v2[j] << 7) + (long long)(int)v3[j];
+          v[c + j] = fma((double)lo, 0x1p-49, (double)hi[j] * 0x1p-21);
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) ombar_arrive(tempty);
+      if (rok) {
+        if (col0 + 16 <= g.N) {
+          cplx cv[16];
+          double sc[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) cv[j] = crow[j];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) sc[j] = sai * sbp[j];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            cv[j].x = fma(-v[2 * j], sc[j], cv[j].x);
+            cv[j].y = fma(-v[2 * j + 1], sc[j], cv[j].y);
+          }
+#pragma unroll
+          for (int j = 0; j < 16; ++j) crow[j] = cv[j];
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            if (col0 + j < g.N) {
+              const double sc = sai * sbp[j];
+              cplx cv = crow[j];
+              cv.x = fma(-v[2 * j], sc, cv.x);
+              cv.y = fma(-v[2 * j + 1], sc, cv.y);
+              crow[j] = cv;
+            }
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+}
+
+// Eight signed 7-bit digits of t (|t| < 64): t = sum_s d_s 2^(-7 s) up to 2^-49.
+// Slice s of sixteen consecutive values packed into one 16-byte vector.
+__device__ __forceinline__ void pack_slice(double (&t)[16], uint4& out, bool negate) {
+  unsigned w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const double d = rint(t[j]);
+    t[j] = (t[j] - d) * 128.0;
+    const int di = negate ? -(int)d : (int)d;
+    w[j >> 2] |= ((unsigned)di & 0xffu) << (8 * (j & 3));
+  }
+  out = make_uint4(w[0], w[1], w[2], w[3]);
+}
+__device__ __forceinline__ uint4 negate_bytes(uint4 v) {
+  // per-byte two's complement negation (digits lie in [-64, 64], no overflow)
+  auto neg = [](unsigned x) { return __vsub4(0u, x); };
+  return make_uint4(neg(v.x), neg(v.y), neg(v.z), neg(v.w));
+}
+__device__ __forceinline__ void scale_of(double mx, bool bad, double& scale, double& inv) {
+  int e = 0;
+  if (mx > 0.0) e = ilogb(mx) + 1;
+  e = max(-900, min(1000, e));
+  scale = bad ? nan("") : ldexp(1.0, e - 6);
+  inv = ldexp(1.0, 6 - e);
+}
+
+// A (M x K complex, row-major) -> slices [batch][OS][M][2K] int8 and sa[batch][M].
+// One warp per row.
+__global__ void __launch_bounds__(256) ozaki_split_a_kernel(const cplx* __restrict__ A, long long lda, long long sA,
+                                                            int M, int K, int8_t* __restrict__ out,
+                                                            double* __restrict__ sa) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row = blockIdx.x * 8 + warp, b = blockIdx.y;
+  if (row >= M) return;
+  const cplx* a = A + (long long)b * sA + (long long)row * lda;
+  double mx = 0.0;
+  bool bad = false;
+  for (int kk = lane; kk < K; kk += 32) {
+    const cplx v = a[kk];
+    const double m1 = fmax(fabs(v.x), fabs(v.y));
+    bad |= !(fabs(v.x) <= DBL_MAX) || !(fabs(v.y) <= DBL_MAX);
+    mx = fmax(mx, m1);
+  }
+  mx = warp_max(mx);
+  bad = __any_sync(0xffffffffu, bad);
+  double scale, inv;
+  scale_of(mx, bad, scale, inv);
+  if (lane == 0) sa[(long long)b * M + row] = scale;
+  const long long K2 = 2LL * K;
+  for (int kk0 = lane * 16; kk0 < K; kk0 += 512) {
+    double tr[16], ti[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const cplx v = a[kk0 + j];
+      tr[j] = bad ? 0.0 : v.x * inv;
+      ti[j] = bad ? 0.0 : v.y * inv;
+    }
+#pragma unroll
+    for (int s = 0; s < OS; ++s) {
+      uint4 pr, pi;
+      pack_slice(tr, pr, false);
+      pack_slice(ti, pi, false);
+      int8_t* o = out + (((long long)b * OS + s) * M + row) * K2;
+      *reinterpret_cast<uint4*>(o + kk0) = pr;
+      *reinterpret_cast<uint4*>(o + K + kk0) = pi;
+    }
+  }
+}
+
+// Column maxima of B (K x N complex, row-major): sb[batch][N].
+__global__ void __launch_bounds__(256) ozaki_colscale_kernel(const cplx* __restrict__ B, long long ldb, long long sB,
+                                                             int K, int N, double* __restrict__ sb) {
+  const int j = blockIdx.x * 256 + threadIdx.x, b = blockIdx.y;
+  if (j >= N) return;
+  const cplx* p = B + (long long)b * sB + j;
+  double mx = 0.0;
+  bool bad = false;
+#pragma unroll 4
+  for (int k = 0; k < K; ++k) {
+    const cplx v = p[(long long)k * ldb];
+    const double m1 = fmax(fabs(v.x), fabs(v.y));
+    bad |= !(fabs(v.x) <= DBL_MAX) || !(fabs(v.y) <= DBL_MAX);
+    mx = fmax(mx, m1);
+  }
+  double scale, inv;
+  scale_of(mx, bad, scale, inv);
+  sb[(long long)b * N + j] = scale;
+}
+
+// B (K x N complex, row-major) -> slices [batch][OS][2N][2K] int8 (row 2j:
+// [Re b_j ; -Im b_j], row 2j+1: [Im b_j ; Re b_j]).  A thread takes column j
+// and sixteen consecutive k.
+__global__ void __launch_bounds__(256) ozaki_split_b_kernel(const cplx* __restrict__ B, long long ldb, long long sB,
+                                                            int K, int N, const double* __restrict__ sb,
+                                                            int8_t* __restrict__ out) {
+  const int j = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int kk0 = (blockIdx.y * 8 + (threadIdx.x >> 5)) * 16;
+  const int b = blockIdx.z;
+  if (j >= N || kk0 >= K) return;
+  const double scale = sb[(long long)b * N + j];
+  const bool bad = !(scale <= DBL_MAX);
+  const double inv = bad ? 0.0 : 1.0 / scale;
+  const cplx* p = B + (long long)b * sB + (long long)kk0 * ldb + j;
+  double tr[16], ti[16];
+#pragma unroll
+  for (int t = 0; t < 16; ++t) {
+    const cplx v = p[(long long)t * ldb];
+    tr[t] = bad ? 0.0 : v.x * inv;
+    ti[t] = bad ? 0.0 : v.y * inv;
+  }
+  const long long K2 = 2LL * K;
+#pragma unroll
+  for (int s = 0; s < OS; ++s) {
+    uint4 pr, pi;
+    pack_slice(tr, pr, false);
+    pack_slice(ti, pi, false);
+    int8_t* o = out + (((long long)b * OS + s) * (2LL * N) + 2 * j) * K2;
+    *reinterpret_cast<uint4*>(o + kk0) = pr;
+    *reinterpret_cast<uint4*>(o + K + kk0) = negate_bytes(pi);
+    *reinterpret_cast<uint4*>(o + K2 + kk0) = pi;
+    *reinterpret_cast<uint4*>(o + K2 + K + kk0) = pr;
+  }
+}
+
+int encode_slice_map(CUtensorMap* map, const int8_t* base, long long K2, long long rows, int batch, int box_rows) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return (int)cudaErrorNotSupported;
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  cuuint64_t dims[4] = {(cuuint64_t)K2, (cuuint64_t)rows, (cuuint64_t)OS, (cuuint64_t)batch};
+  cuuint64_t strides[3] = {(cuuint64_t)K2, (cuuint64_t)(K2 * rows), (cuuint64_t)(K2 * rows * OS)};
+  cuuint32_t box[4] = {(cuuint32_t)OKB, (cuuint32_t)box_rows, 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(base), dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : (int)cudaErrorInvalidValue;
+}
+
+}  // namespace
+
+bool ozaki_shape_ok(int M, int N, int K) { return M > 0 && N > 0 && K >= 32 && K % 32 == 0 && K <= 4096; }
+
+long long ozaki_ws_bytes_per_entry(int M, int N, int K) {
+  return (long long)OS * 2 * K * ((long long)M + 2LL * N) + 8LL * (M + N) + 512;
+}
+
+// C -= A B for `batch` independent complex128 problems (row-major; strides in
+// elements).  Workspace comes from the stream-ordered pool, in chunks of
+// entries bounded by CIRR_OZAKI_WS_MB (default 4096 MiB).
+int ozaki_zgemm_sub(const cplx* A, long long lda, long long sA, const cplx* B, long long ldb, long long sB, cplx* C,
+                    long long ldc, long long sC, int M, int N, int K, int batch, cudaStream_t stream) {
+  if (!ozaki_shape_ok(M, N, K) || batch <= 0) return CIRR_EINVAL;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(ozaki_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, OSMEM);
+    if (e != cudaSuccess) return (int)e;
+    attr = true;
+  }
+  static const long long ws_mb = getenv("CIRR_OZAKI_WS_MB") ? atoll(getenv("CIRR_OZAKI_WS_MB")) : 4096;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const long long K2 = 2LL * K;
+  const long long a_bytes = (long long)OS * M * K2, b_bytes = (long long)OS * 2 * N * K2;
+  const long long per = a_bytes + b_bytes;
+  int chunk = (int)max(1LL, min((long long)batch, (ws_mb << 20) / per));
+  int8_t* ws = nullptr;
+  double* scales = nullptr;
+  cudaError_t e = cirr_malloc_async((void**)&ws, (size_t)chunk * per, stream);
+  if (e != cudaSuccess) return (int)e;
+  e = cirr_malloc_async((void**)&scales, (size_t)chunk * (M + N) * sizeof(double), stream);
+  if (e != cudaSuccess) { cudaFreeAsync(ws, stream); return (int)e; }
+  int rc = 0;
+  for (int b0 = 0; b0 < batch && rc == 0; b0 += chunk) {
+    const int nb = min(chunk, batch - b0);
+    int8_t* wa = ws;
+    int8_t* wb = ws + (long long)nb * a_bytes;
+    double* sa = scales;
+    double* sb = scales + (long long)nb * M;
+    ozaki_split_a_kernel<<<dim3((M + 7) / 8, nb), 256, 0, stream>>>(A + (long long)b0 * sA, lda, sA, M, K, wa, sa);
+    cirr_note_launch();
+    ozaki_colscale_kernel<<<dim3((N + 255) / 256, nb), 256, 0, stream>>>(B + (long long)b0 * sB, ldb, sB, K, N, sb);
+    cirr_note_launch();
+    ozaki_split_b_kernel<<<dim3((N + 31) / 32, (K + 127) / 128, nb), 256, 0, stream>>>(B + (long long)b0 * sB, ldb,
+                                                                                      sB, K, N, sb, wb);
+    cirr_note_launch();
+    CUtensorMap mA, mB;
+    if (encode_slice_map(&mA, wa, K2, M, nb, OBM) != 0 || encode_slice_map(&mB, wb, K2, 2LL * N, nb, OBN) != 0) {
+      rc = (int)cudaErrorInvalidValue;
+      break;
+    }
+    OzGeom g{};
+    g.M = M; g.N = N; g.K2 = (int)K2; g.batch = nb;
+    g.tiles_m = (M + OBM - 1) / OBM;
+    g.tiles_n = (2 * N + OBN - 1) / OBN;
+    g.C = C + (long long)b0 * sC; g.ldc = ldc; g.sC = sC;
+    g.sa = sa; g.sb = sb;
+    const long long ntiles = (long long)g.tiles_m * g.tiles_n * nb;
+    const int grid = (int)min((long long)sms, ntiles);
+    ozaki_gemm_kernel<<<grid, OTHREADS, OSMEM, stream>>>(mA, mB, g);
+    cirr_note_launch();
+    cudaError_t le = cudaGetLastError();
+    if (le != cudaSuccess) rc = (int)le;
+  }
+  cudaFreeAsync(ws, stream);
+  cudaFreeAsync(scales, stream);
+  return rc;
+}
+
+}  // namespace cirr
+
+// C-ABI test entry: C -= A B through the Ozaki int8 path (tests/test_gpu_ozaki.py).
+CIRR_API int cirr_ozaki_zgemm_sub(const cirr_cplx* A, long long lda, long long sA, const cirr_cplx* B, long long ldb,
+                                  long long sB, cirr_cplx* C, long long ldc, long long sC, int M, int N, int K,
+                                  int batch, cudaStream_t stream) {
+  return cirr::ozaki_zgemm_sub(A, lda, sA, B, ldb, sB, C, ldc, sC, M, N, K, batch, stream);
+}

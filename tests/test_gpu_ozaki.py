@@ -1,0 +1,126 @@
+"""The int8 tensor-core (Ozaki splitting) GEMM update against numpy: the error
+must stay at the FP64 GEMM level relative to rowmax(A) * colmax(B), also for
+badly scaled rows and columns, ragged shapes and sub-blocks of larger arrays."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not torch.cuda.is_available():
+        pytest.fail("gpu test without CUDA")
+    from paper_2511_01927_b200 import _lib
+    return _lib
+
+
+def S():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def crandn(rng, *shape):
+    return rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+
+
+def bound(A, B):
+    """|error_ij| <= K * 2^-50 * rowmax_i(A) * colmax_j(B) (3 bits of slack on the 2^-53 per-term bound)."""
+    K = A.shape[-1]
+    ra = np.maximum(np.abs(A.real), np.abs(A.imag)).max(axis=-1)
+    cb = np.maximum(np.abs(B.real), np.abs(B.imag)).max(axis=-2)
+    return K * 2.0 ** -50 * ra[..., :, None] * cb[..., None, :]
+
+
+@pytest.mark.parametrize("shape", [(128, 32, 32), (256, 64, 512), (200, 45, 96), (1000, 333, 512), (130, 1, 64)])
+def test_ozaki_matches_numpy(lib, shape):
+    M, N, K = shape
+    rng = np.random.default_rng(M + N + K)
+    batch = 3
+    A = crandn(rng, batch, M, K)
+    B = crandn(rng, batch, K, N)
+    C0 = crandn(rng, batch, M, N)
+    C = torch.from_numpy(C0.copy()).cuda()
+    dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    rc = lib.call("cirr_ozaki_zgemm_sub", dA.data_ptr(), K, M * K, dB.data_ptr(), N, K * N, C.data_ptr(), N, M * N,
+                  M, N, K, batch, S())
+    assert rc == 0
+    torch.cuda.synchronize()
+    ref = C0 - A @ B
+    err = np.abs(C.cpu().numpy() - ref)
+    assert (err <= bound(A, B) + 4e-16 * np.abs(ref)).all(), err.max()
+
+
+def test_ozaki_graded_rows_and_columns(lib):
+    """Rows of A and columns of B spanning 60 orders of magnitude keep their own relative accuracy."""
+    M, N, K = 256, 96, 128
+    rng = np.random.default_rng(7)
+    A = crandn(rng, 1, M, K) * (10.0 ** rng.uniform(-30, 30, (1, M, 1)))
+    B = crandn(rng, 1, K, N) * (10.0 ** rng.uniform(-30, 30, (1, 1, N)))
+    C0 = np.zeros((1, M, N), dtype=np.complex128)
+    C = torch.from_numpy(C0.copy()).cuda()
+    dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    assert lib.call("cirr_ozaki_zgemm_sub", dA.data_ptr(), K, M * K, dB.data_ptr(), N, K * N, C.data_ptr(), N, M * N,
+                    M, N, K, 1, S()) == 0
+    torch.cuda.synchronize()
+    err = np.abs(C.cpu().numpy() + A @ B)
+    assert (err <= bound(A, B)).all()
+
+
+def test_ozaki_subblocks_in_place(lib):
+    """The LU's use: A, B and C are blocks of one array (leading dimension n, batch stride n*n)."""
+    n, k0, W = 768, 64, 128
+    rng = np.random.default_rng(3)
+    P0 = crandn(rng, 2, n, n)
+    P = torch.from_numpy(P0.copy()).cuda()
+    base = P.data_ptr()
+    r0 = k0 + W
+    m = n - r0
+    off = lambda r, c: base + 16 * (r * n + c)
+    assert lib.call("cirr_ozaki_zgemm_sub", off(r0, k0), n, n * n, off(k0, r0), n, n * n, off(r0, r0), n, n * n,
+                    m, m, W, 2, S()) == 0
+    torch.cuda.synchronize()
+    ref = P0.copy()
+    ref[:, r0:, r0:] -= P0[:, r0:, k0:r0] @ P0[:, k0:r0, r0:]
+    got = P.cpu().numpy()
+    assert np.array_equal(got[:, :r0, :], P0[:, :r0, :]) and np.array_equal(got[:, r0:, :r0], P0[:, r0:, :r0])
+    err = np.abs(got[:, r0:, r0:] - ref[:, r0:, r0:])
+    assert (err <= bound(P0[:, r0:, k0:r0], P0[:, k0:r0, r0:]) + 4e-16 * np.abs(ref[:, r0:, r0:])).all()
+
+
+def test_ozaki_zero_and_nonfinite(lib):
+    """Zero rows / columns give exact zeros; a NaN poisons its row (as the FP64 GEMM would)."""
+    M, N, K = 128, 32, 64
+    rng = np.random.default_rng(5)
+    A = crandn(rng, 1, M, K)
+    B = crandn(rng, 1, K, N)
+    A[0, 3, :] = 0
+    B[0, :, 5] = 0
+    A[0, 9, 2] = np.nan
+    C = torch.zeros((1, M, N), dtype=torch.complex128, device="cuda")
+    dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    assert lib.call("cirr_ozaki_zgemm_sub", dA.data_ptr(), K, M * K, dB.data_ptr(), N, K * N, C.data_ptr(), N, M * N,
+                    M, N, K, 1, S()) == 0
+    torch.cuda.synchronize()
+    got = C.cpu().numpy()[0]
+    assert (got[3] == 0).all() and (got[:, 5][np.arange(M) != 9] == 0).all()
+    assert np.isnan(got[9]).all()
+    ok = np.ones(M, dtype=bool)
+    ok[9] = False
+    assert np.isfinite(got[ok]).all()
+
+
+def test_ozaki_deterministic(lib):
+    M, N, K = 384, 200, 512
+    rng = np.random.default_rng(11)
+    A, B = crandn(rng, 2, M, K), crandn(rng, 2, K, N)
+    dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    outs = []
+    for _ in range(2):
+        C = torch.zeros((2, M, N), dtype=torch.complex128, device="cuda")
+        assert lib.call("cirr_ozaki_zgemm_sub", dA.data_ptr(), K, M * K, dB.data_ptr(), N, K * N, C.data_ptr(), N,
+                        M * N, M, N, K, 2, S()) == 0
+        torch.cuda.synchronize()
+        outs.append(C.cpu().numpy())
+    assert np.array_equal(outs[0].view(np.float64), outs[1].view(np.float64))
