@@ -266,6 +266,26 @@ int cirr_ozaki_zgemm_sub(const cirr_cplx* A, long long lda, long long sA, const 
                          long long sB, cirr_cplx* C, long long ldc, long long sC, int M, int N, int K, int batch,
                          cudaStream_t stream);
 
+/* Int8 path of the blocked solves (K3): the factors are constant over the
+ * solve passes of a run (solvers.py:113-130 applies the same LU every pass), so
+ * their digit slices are cut once after cirr_zgetrf_batched into a caller-owned
+ * buffer of cirr_ozaki_factor_bytes(n, nfac) bytes (0: shape not taken -- n
+ * must be a multiple of 512, at least 1024) and registered under the LU
+ * address; the k = 512 trailing updates of every later cirr_zgetrs_* call on
+ * those factors (any sub-range of them, dense bandwidths) then run on the int8
+ * tensor cores.  Release before the factors or the buffer are freed or
+ * refactored. */
+long long cirr_ozaki_factor_bytes(int n, int nfac);
+int cirr_ozaki_split_factors(const cirr_cplx* LU, int n, long long ld, long long pencil_stride, int nfac,
+                             void* cache, cudaStream_t stream);
+int cirr_ozaki_release(const cirr_cplx* LU);
+
+/* Arithmetic of the dense LU's k = 512 trailing updates (K2): 0 = FP64 DMMA
+ * (zgemm_sub_tma), 1 = the int8 tensor-core path above.  Banded pencils and the
+ * in-step updates always take DMMA.  Returns the previous mode; any other
+ * argument only queries.  Environment default: CIRR_LU_GEMM=int8 | dmma. */
+int cirr_set_lu_gemm(int mode);
+
 /* number of kernels this library has launched since it was loaded (host counter) */
 long long cirr_launch_count(void);
 

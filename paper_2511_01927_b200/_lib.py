@@ -75,12 +75,16 @@ SIGNATURES = {
     "cirr_gemm_ptrs": [_I, _I, _I, _I, _I, _P, _L, _P, _L, _L, _P, _L, _L, _D, _I, _P],
     "cirr_gather_blocks": [_I, _P, _L, _P, _L, _L, _P],
     "cirr_zero": [_P, _L, _P],
+    "cirr_set_lu_gemm": [_I],
+    "cirr_ozaki_factor_bytes": [_I, _I],
+    "cirr_ozaki_split_factors": [_P, _I, _L, _L, _I, _P, _P],
+    "cirr_ozaki_release": [_P],
     "cirr_ozaki_zgemm_sub": [_P, _L, _L, _P, _L, _L, _P, _L, _L, _I, _I, _I, _I, _P],
 }
-_RESTYPE = {"cirr_diag_inv_bytes": _L, "cirr_zgetrf_ws_bytes": _L, "cirr_small_eig_ws_bytes": _L, "cirr_launch_count": _L, "cirr_orth_ws_bytes": _L,
+_RESTYPE = {"cirr_ozaki_factor_bytes": _L, "cirr_diag_inv_bytes": _L, "cirr_zgetrf_ws_bytes": _L, "cirr_small_eig_ws_bytes": _L, "cirr_launch_count": _L, "cirr_orth_ws_bytes": _L,
             "cirr_gen_eig_ws_bytes": _L, "cirr_gen_eig_vec_scratch_bytes": _L, "cirr_orth_cholqr2_ws_bytes": _L,
             "cirr_gen_eig_refine_ws_bytes": _L}
-_RAW = {"cirr_zgetrs_uses_dinv", "cirr_set_coop_ctas", "cirr_set_gemm_ctas", "cirr_diag_inv_bytes", "cirr_zgetrf_ws_bytes", "cirr_small_eig_ws_bytes", "cirr_launch_count", "cirr_target_sm", "cirr_orth_ws_bytes",
+_RAW = {"cirr_set_lu_gemm", "cirr_ozaki_factor_bytes", "cirr_zgetrs_uses_dinv", "cirr_set_coop_ctas", "cirr_set_gemm_ctas", "cirr_diag_inv_bytes", "cirr_zgetrf_ws_bytes", "cirr_small_eig_ws_bytes", "cirr_launch_count", "cirr_target_sm", "cirr_orth_ws_bytes",
         "cirr_gen_eig_ws_bytes", "cirr_gen_eig_vec_scratch_bytes", "cirr_orth_cholqr2_ws_bytes",
         "cirr_gen_eig_refine_ws_bytes"}
 

@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include "gemm.cuh"
 #include "lu_gemm.cuh"
+#include "ozaki.cuh"
 
 namespace {
 
@@ -405,6 +406,8 @@ static int getrf_impl(cplx* pencils, int n, long long ld, long long pencil_strid
   if (n <= 0 || batch <= 0 || ld < n || kl < 0 || ku < 0) return CIRR_EINVAL;
   kl = min(kl, n - 1);
   ku = min(ku, n - 1);
+  // digit slices kept for earlier factors in this memory are stale now
+  cirr::ozaki_invalidate(pencils, ((long long)(batch - 1) * pencil_stride + (long long)(n - 1) * ld + n) * 16);
   auto rend = [&](int k, int jb) { return (int)min((long long)n, (long long)k + jb + kl); };
   auto cend = [&](int k, int jb) { return (int)min((long long)n, (long long)k + jb + kl + ku); };
   static bool attr = false;
@@ -475,9 +478,20 @@ static int getrf_impl(cplx* pencils, int n, long long ld, long long pencil_strid
                                         pencils, ld, pencil_stride, stream, /*beta=*/0));
         }
       }
-      if (rest > 0)  // trailing update with k = W (rows/columns that can be nonzero)
-        CIRR_TRY(cirr::zgemm_sub_maps(maps.a, maps.b, maps.c, rend(k, W) - k - W, cend(k, W) - k - W, W, batch,
-                                      k + W, k, k, k + W, k + W, k + W, pencils, ld, pencil_stride, stream));
+      if (rest > 0) {  // trailing update with k = W (rows/columns that can be nonzero)
+        const int tm = rend(k, W) - k - W, tn = cend(k, W) - k - W;
+        if (cirr::ozaki_enabled() && !banded && W >= 256 && cirr::ozaki_shape_ok(tm, tn, W)) {
+          // int8 tensor cores (ozaki.cu): ~1.6x the DMMA kernel at this shape
+          const cplx* a = pencils + (long long)(k + W) * ld + k;
+          const cplx* b = pencils + (long long)k * ld + k + W;
+          cplx* c = pencils + (long long)(k + W) * ld + k + W;
+          CIRR_TRY(cirr::ozaki_zgemm_sub(a, ld, pencil_stride, b, ld, pencil_stride, c, ld, pencil_stride, tm, tn, W,
+                                         batch, stream));
+        } else {
+          CIRR_TRY(cirr::zgemm_sub_maps(maps.a, maps.b, maps.c, tm, tn, W, batch, k + W, k, k, k + W, k + W, k + W,
+                                        pencils, ld, pencil_stride, stream));
+        }
+      }
     }
   }
   for (int k = k0; k < n; k += NB) {

@@ -15,6 +15,7 @@
 #include "common.cuh"
 #include <cstdlib>
 #include "lu_gemm.cuh"
+#include "ozaki.cuh"
 
 namespace {
 
@@ -785,8 +786,15 @@ static int getrs_impl(const cplx* LU, int n, long long ld, long long pencil_stri
         }
         if (n - s1 > 0) {  // Y[s1:s1+m] -= L[s1:s1+m, kb:s1] Y[kb:s1] (m = klL rows below can be nonzero)
           const int kb = max(s0, s1 - up16(min(s1 - s0, klL)));
-          CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, min(n - s1, klL), K, s1 - kb, batch, s1, kb, kb, 0, s1, 0,
-                                        Y, ldy, ystride, stream, 1, 1, 0, pmap, BN, kBswz));
+          // int8 tensor cores on the factor slices kept after the factorisation (ozaki.cu), else DMMA
+          int orc = -1;
+          if (klL >= n - 1)
+            orc = cirr::ozaki_cached_update(LU, n, kb, s1 - kb, s1, n - s1, Y + (long long)kb * ldy, ldy, ystride,
+                                            Y + (long long)s1 * ldy, ldy, ystride, K, batch, pmap, stream);
+          if (orc > 0) return orc;
+          if (orc < 0)
+            CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, min(n - s1, klL), K, s1 - kb, batch, s1, kb, kb, 0, s1, 0,
+                                          Y, ldy, ystride, stream, 1, 1, 0, pmap, BN, kBswz));
         }
       }
       const int nsb = (nblk2 + SBK - 1) / SBK;
@@ -808,8 +816,14 @@ static int getrs_impl(const cplx* LU, int n, long long ld, long long pencil_stri
         }
         if (s0 > 0) {  // Y[r0:s0] -= U[r0:s0, s0:ke] Y[s0:ke] (rows within kuU above, their columns)
           const int r0 = max(0, s0 - kuU), ke = min(s1, s0 + up16(min(s1 - s0, kuU)));
-          CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, s0 - r0, K, ke - s0, batch, r0, s0, s0, 0, r0, 0, Y, ldy,
-                                        ystride, stream, 1, 1, 0, pmap, BN, kBswz));
+          int orc = -1;
+          if (kuU >= n - 1)
+            orc = cirr::ozaki_cached_update(LU, n, s0, ke - s0, 0, s0, Y + (long long)s0 * ldy, ldy, ystride, Y, ldy,
+                                            ystride, K, batch, pmap, stream);
+          if (orc > 0) return orc;
+          if (orc < 0)
+            CIRR_TRY(cirr::zgemm_sub_maps(mT.a, mY.b, mY.c, s0 - r0, K, ke - s0, batch, r0, s0, s0, 0, r0, 0, Y, ldy,
+                                          ystride, stream, 1, 1, 0, pmap, BN, kBswz));
         }
       }
       return 0;

@@ -26,6 +26,7 @@
 #include <cudaTypedefs.h>
 #include <cfloat>
 #include <cstdlib>
+#include <mutex>
 
 #include "common.cuh"
 #include "ozaki.cuh"
@@ -101,8 +102,12 @@ struct OzGeom {
   int batch;
   int tiles_m, tiles_n;
   cplx* C; long long ldc, sC;
-  const double* sa;  // [batch][M]   2^(e_i - 6)
+  const double* sa;  // [A tensor index][sa_stride]   2^(e_i - 6), row a_row0 + i
   const double* sb;  // [batch][N]   2^(f_j - 6)
+  long long sa_stride;
+  int a_row0;        // first row of A inside its slice tensor (TMA coordinate 1)
+  int a_mul, a_add;  // A tensor index (TMA coordinate 3) of entry b: abatch(b) * a_mul + a_add
+  const int* a_bmap; // optional: abatch(b) = a_bmap[b] (gathered solves), else b
 };
 
 __global__ void __launch_bounds__(OTHREADS, 1) ozaki_gemm_kernel(const __grid_constant__ CUtensorMap mapA,
@@ -141,6 +146,7 @@ __global__ void __launch_bounds__(OTHREADS, 1) ozaki_gemm_kernel(const __grid_co
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const int b = t / per, r = t - b * per;
         const int m0 = (r / g.tiles_n) * OBM, n0 = (r % g.tiles_n) * OBN;
+        const int ab = (g.a_bmap ? g.a_bmap[b] : b) * g.a_mul + g.a_add;
         for (int kb = 0; kb < nkb; ++kb, ++it) {
           const int st = it % ONSTAGE;
           const unsigned ph = (it / ONSTAGE) & 1;
@@ -149,7 +155,7 @@ __global__ void __launch_bounds__(OTHREADS, 1) ozaki_gemm_kernel(const __grid_co
           uint8_t* base = smem + st * OSTAGE;
 #pragma unroll
           for (int s = 0; s < OS; ++s) {
-            otma_load4(base + s * OA_SLICE, &mapA, kb * OKB, m0, s, b, &full[st]);
+            otma_load4(base + s * OA_SLICE, &mapA, kb * OKB, g.a_row0 + m0, s, ab, &full[st]);
             otma_load4(base + OS * OA_SLICE + s * OB_SLICE, &mapB, kb * OKB, n0, s, b, &full[st]);
           }
         }
@@ -208,7 +214,8 @@ __global__ void __launch_bounds__(OTHREADS, 1) ozaki_gemm_kernel(const __grid_co
         asm volatile("prefetch.global.L2 [%0];" ::"l"(crow));
         asm volatile("prefetch.global.L2 [%0];" ::"l"(crow + 8));
       }
-      const double sai = rok ? g.sa[(long long)b * g.M + row] : 0.0;
+      const int ab = (g.a_bmap ? g.a_bmap[b] : b) * g.a_mul + g.a_add;
+      const double sai = rok ? g.sa[(long long)ab * g.sa_stride + g.a_row0 + row] : 0.0;
       double v[32];
       ombar_wait(tfull, tl & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -306,7 +313,7 @@ __device__ __forceinline__ void scale_of(double mx, bool bad, double& scale, dou
 // One warp per row.
 __global__ void __launch_bounds__(256) ozaki_split_a_kernel(const cplx* __restrict__ A, long long lda, long long sA,
                                                             int M, int K, int8_t* __restrict__ out,
-                                                            double* __restrict__ sa) {
+                                                            double* __restrict__ sa, int ob_mul, int ob_add) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row = blockIdx.x * 8 + warp, b = blockIdx.y;
   if (row >= M) return;
@@ -323,7 +330,8 @@ __global__ void __launch_bounds__(256) ozaki_split_a_kernel(const cplx* __restri
   bad = __any_sync(0xffffffffu, bad);
   double scale, inv;
   scale_of(mx, bad, scale, inv);
-  if (lane == 0) sa[(long long)b * M + row] = scale;
+  const long long ob = (long long)b * ob_mul + ob_add;
+  if (lane == 0) sa[ob * M + row] = scale;
   const long long K2 = 2LL * K;
   for (int kk0 = lane * 16; kk0 < K; kk0 += 512) {
     double tr[16], ti[16];
@@ -338,7 +346,7 @@ __global__ void __launch_bounds__(256) ozaki_split_a_kernel(const cplx* __restri
       uint4 pr, pi;
       pack_slice(tr, pr, false);
       pack_slice(ti, pi, false);
-      int8_t* o = out + (((long long)b * OS + s) * M + row) * K2;
+      int8_t* o = out + ((ob * OS + s) * M + row) * K2;
       *reinterpret_cast<uint4*>(o + kk0) = pr;
       *reinterpret_cast<uint4*>(o + K + kk0) = pi;
     }
@@ -400,7 +408,8 @@ __global__ void __launch_bounds__(256) ozaki_split_b_kernel(const cplx* __restri
   }
 }
 
-int encode_slice_map(CUtensorMap* map, const int8_t* base, long long K2, long long rows, int batch, int box_rows) {
+int encode_slice_map(CUtensorMap* map, const int8_t* base, long long K2, long long rows, long long batch,
+                     int box_rows) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
@@ -420,7 +429,162 @@ int encode_slice_map(CUtensorMap* map, const int8_t* base, long long K2, long lo
   return r == CUDA_SUCCESS ? 0 : (int)cudaErrorInvalidValue;
 }
 
+
+// ---- factor slices kept for the solves ------------------------------------
+// The factors do not change between the solve passes of a CIRR run, so their
+// slices are cut once after the factorisation (cirr_ozaki_split_factors) into a
+// caller-owned buffer and every k = 512 trailing update of the blocked solves
+// reads them: per factor and 512-column block sb a tensor [OS][n][1024] of the
+// rows' digits over those columns (rows above the block are U's, rows below
+// L's), plus the row scales [n].
+struct OzCache {
+  const cplx* LU;
+  long long pstride;
+  int n, nfac, nsb;
+  int8_t* slices;
+  double* scales;
+};
+constexpr int OZ_W = 512;
+constexpr int OZ_MAXCACHE = 16;
+OzCache g_oz_cache[OZ_MAXCACHE];
+int g_oz_ncache = 0;
+std::mutex g_oz_mutex;
+
+bool oz_lookup(const cplx* LU, int n, OzCache& out, long long& f0) {
+  std::lock_guard<std::mutex> lk(g_oz_mutex);
+  for (int i = 0; i < g_oz_ncache; ++i) {
+    const OzCache& c = g_oz_cache[i];
+    if (c.n != n || LU < c.LU) continue;
+    const long long d = LU - c.LU;
+    if (d % c.pstride != 0 || d / c.pstride >= c.nfac) continue;
+    out = c;
+    f0 = d / c.pstride;
+    return true;
+  }
+  return false;
+}
+
 }  // namespace
+
+long long ozaki_factor_bytes(int n, int nfac) {
+  if (n < 2 * OZ_W || n % OZ_W != 0 || nfac <= 0) return 0;
+  const long long nsb = n / OZ_W;
+  return (long long)nfac * nsb * ((long long)OS * n * 2 * OZ_W + 8LL * n) + 512;
+}
+
+int ozaki_split_factors(const cplx* LU, int n, long long ld, long long pstride, int nfac, void* cache,
+                        cudaStream_t stream) {
+  if (ozaki_factor_bytes(n, nfac) == 0 || cache == nullptr) return CIRR_EINVAL;
+  const int nsb = n / OZ_W;
+  OzCache c{LU, pstride, n, nfac, nsb, reinterpret_cast<int8_t*>(cache), nullptr};
+  const long long slice_bytes = (long long)nfac * nsb * OS * n * 2 * OZ_W;
+  c.scales = reinterpret_cast<double*>(c.slices + ((slice_bytes + 255) & ~255LL));
+  for (int sb = 0; sb < nsb; ++sb) {
+    ozaki_split_a_kernel<<<dim3((n + 7) / 8, nfac), 256, 0, stream>>>(LU + (long long)sb * OZ_W, ld, pstride, n, OZ_W,
+                                                                       c.slices, c.scales, nsb, sb);
+    CIRR_CHECK_LAUNCH();
+  }
+  std::lock_guard<std::mutex> lk(g_oz_mutex);
+  for (int i = 0; i < g_oz_ncache; ++i)
+    if (g_oz_cache[i].LU == LU) { g_oz_cache[i] = c; return 0; }
+  if (g_oz_ncache == OZ_MAXCACHE) {  // oldest entry out
+    for (int i = 1; i < OZ_MAXCACHE; ++i) g_oz_cache[i - 1] = g_oz_cache[i];
+    --g_oz_ncache;
+  }
+  g_oz_cache[g_oz_ncache++] = c;
+  return 0;
+}
+
+// Drop every registration whose factors overlap [p, p + bytes): called by the
+// LU itself (new factors in that memory make the slices stale) and by release.
+void ozaki_invalidate(const void* p, long long bytes) {
+  std::lock_guard<std::mutex> lk(g_oz_mutex);
+  const char* lo = reinterpret_cast<const char*>(p);
+  const char* hi = lo + bytes;
+  int k = 0;
+  for (int i = 0; i < g_oz_ncache; ++i) {
+    const OzCache& c = g_oz_cache[i];
+    const char* clo = reinterpret_cast<const char*>(c.LU);
+    const char* chi = clo + ((long long)(c.nfac - 1) * c.pstride + (long long)c.n * c.n) * 16;
+    if (clo < hi && lo < chi) continue;
+    g_oz_cache[k++] = c;
+  }
+  g_oz_ncache = k;
+}
+
+int ozaki_release(const cplx* LU) {
+  ozaki_invalidate(LU, 16);
+  return 0;
+}
+
+// C -= A B where A = rows a_row0 .. a_row0 + M of the factor's column block
+// col0 .. col0 + 512, read from the slices kept by ozaki_split_factors; entry b
+// uses factor (LU - registered base) / stride + (pmap ? pmap[b] : b).  Returns
+// -1 when the slices are not there (the caller takes the DMMA path).
+int ozaki_cached_update(const cplx* LU, int n, int col0, int kw, int a_row0, int M, const cplx* B, long long ldb,
+                        long long sB, cplx* C, long long ldc, long long sC, int N, int batch, const int* pmap,
+                        cudaStream_t stream) {
+  if (!ozaki_enabled() || kw != OZ_W || col0 % OZ_W != 0 || M <= 0 || N <= 0 || batch <= 0) return -1;
+  OzCache c;
+  long long f0 = 0;
+  if (!oz_lookup(LU, n, c, f0)) return -1;
+  const long long K2 = 2LL * OZ_W;
+  const long long b_bytes = (long long)OS * 2 * N * K2;
+  int8_t* wb = nullptr;
+  double* sb = nullptr;
+  cudaError_t e = cirr_malloc_async((void**)&wb, (size_t)batch * b_bytes, stream);
+  if (e != cudaSuccess) return (int)e;
+  e = cirr_malloc_async((void**)&sb, (size_t)batch * N * sizeof(double), stream);
+  if (e != cudaSuccess) { cudaFreeAsync(wb, stream); return (int)e; }
+  int rc = 0;
+  ozaki_colscale_kernel<<<dim3((N + 255) / 256, batch), 256, 0, stream>>>(B, ldb, sB, OZ_W, N, sb);
+  cirr_note_launch();
+  ozaki_split_b_kernel<<<dim3((N + 31) / 32, (OZ_W + 127) / 128, batch), 256, 0, stream>>>(B, ldb, sB, OZ_W, N, sb, wb);
+  cirr_note_launch();
+  CUtensorMap mA, mB;
+  if (encode_slice_map(&mA, c.slices, K2, n, (long long)c.nfac * c.nsb, OBM) != 0 ||
+      encode_slice_map(&mB, wb, K2, 2LL * N, batch, OBN) != 0) {
+    rc = (int)cudaErrorInvalidValue;
+  } else {
+    static int sms = 0;
+    if (!sms) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaFuncSetAttribute(ozaki_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, OSMEM);
+    }
+    OzGeom g{};
+    g.M = M; g.N = N; g.K2 = (int)K2; g.batch = batch;
+    g.tiles_m = (M + OBM - 1) / OBM;
+    g.tiles_n = (2 * N + OBN - 1) / OBN;
+    g.C = C; g.ldc = ldc; g.sC = sC;
+    g.sa = c.scales; g.sb = sb;
+    g.sa_stride = n; g.a_row0 = a_row0;
+    g.a_mul = c.nsb; g.a_add = (int)(f0 * c.nsb + col0 / OZ_W);
+    g.a_bmap = pmap;
+    const long long ntiles = (long long)g.tiles_m * g.tiles_n * batch;
+    ozaki_gemm_kernel<<<(int)min((long long)sms, ntiles), OTHREADS, OSMEM, stream>>>(mA, mB, g);
+    cirr_note_launch();
+    cudaError_t le = cudaGetLastError();
+    if (le != cudaSuccess) rc = (int)le;
+  }
+  cudaFreeAsync(wb, stream);
+  cudaFreeAsync(sb, stream);
+  return rc;
+}
+
+namespace {
+}  // namespace
+
+// 0: FP64 DMMA trailing updates; 1: int8 tensor-core (Ozaki) trailing updates
+// for the dense LU's k = 512 steps.  CIRR_LU_GEMM=int8 / dmma sets the default.
+int g_cirr_lu_gemm = [] {
+  const char* e = getenv("CIRR_LU_GEMM");
+  if (!e) return 0;
+  return (e[0] == 'i' || e[0] == '1') ? 1 : 0;
+}();
+
+bool ozaki_enabled() { return g_cirr_lu_gemm == 1; }
 
 bool ozaki_shape_ok(int M, int N, int K) { return M > 0 && N > 0 && K >= 32 && K % 32 == 0 && K <= 4096; }
 
@@ -438,6 +602,15 @@ int ozaki_zgemm_sub(const cplx* A, long long lda, long long sA, const cplx* B, l
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(ozaki_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, OSMEM);
     if (e != cudaSuccess) return (int)e;
+    // keep the slice workspace in the stream-ordered pool between calls (the
+    // default pool gives everything back at every synchronisation)
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t cur = 0, want = 6ULL << 30;
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &cur);
+      if (cur < want) cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &want);
+    }
     attr = true;
   }
   static const long long ws_mb = getenv("CIRR_OZAKI_WS_MB") ? atoll(getenv("CIRR_OZAKI_WS_MB")) : 4096;
@@ -464,7 +637,7 @@ int ozaki_zgemm_sub(const cplx* A, long long lda, long long sA, const cplx* B, l
     int8_t* wb = ws + (long long)nb * a_bytes;
     double* sa = scales;
     double* sb = scales + (long long)nb * M;
-    ozaki_split_a_kernel<<<dim3((M + 7) / 8, nb), 256, 0, stream>>>(A + (long long)b0 * sA, lda, sA, M, K, wa, sa);
+    ozaki_split_a_kernel<<<dim3((M + 7) / 8, nb), 256, 0, stream>>>(A + (long long)b0 * sA, lda, sA, M, K, wa, sa, 1, 0);
     cirr_note_launch();
     ozaki_colscale_kernel<<<dim3((N + 255) / 256, nb), 256, 0, stream>>>(B + (long long)b0 * sB, ldb, sB, K, N, sb);
     cirr_note_launch();
@@ -482,6 +655,7 @@ int ozaki_zgemm_sub(const cplx* A, long long lda, long long sA, const cplx* B, l
     g.tiles_n = (2 * N + OBN - 1) / OBN;
     g.C = C + (long long)b0 * sC; g.ldc = ldc; g.sC = sC;
     g.sa = sa; g.sb = sb;
+    g.sa_stride = M; g.a_row0 = 0; g.a_mul = 1; g.a_add = 0; g.a_bmap = nullptr;
     const long long ntiles = (long long)g.tiles_m * g.tiles_n * nb;
     const int grid = (int)min((long long)sms, ntiles);
     ozaki_gemm_kernel<<<grid, OTHREADS, OSMEM, stream>>>(mA, mB, g);
@@ -496,7 +670,20 @@ int ozaki_zgemm_sub(const cplx* A, long long lda, long long sA, const cplx* B, l
 
 }  // namespace cirr
 
-// C-ABI test entry: C -= A B through the Ozaki int8 path (tests/test_gpu_ozaki.py).
+CIRR_API long long cirr_ozaki_factor_bytes(int n, int nfac) { return cirr::ozaki_factor_bytes(n, nfac); }
+CIRR_API int cirr_ozaki_split_factors(const cirr_cplx* LU, int n, long long ld, long long pencil_stride, int nfac,
+                                      void* cache, cudaStream_t stream) {
+  return cirr::ozaki_split_factors(LU, n, ld, pencil_stride, nfac, cache, stream);
+}
+CIRR_API int cirr_ozaki_release(const cirr_cplx* LU) { return cirr::ozaki_release(LU); }
+
+CIRR_API int cirr_set_lu_gemm(int mode) {
+  const int prev = cirr::g_cirr_lu_gemm;
+  if (mode == 0 || mode == 1) cirr::g_cirr_lu_gemm = mode;
+  return prev;
+}
+
+// C-ABI entry: C -= A B through the Ozaki int8 path (tests/test_gpu_ozaki.py).
 CIRR_API int cirr_ozaki_zgemm_sub(const cirr_cplx* A, long long lda, long long sA, const cirr_cplx* B, long long ldb,
                                   long long sB, cirr_cplx* C, long long ldc, long long sC, int M, int N, int K,
                                   int batch, cudaStream_t stream) {

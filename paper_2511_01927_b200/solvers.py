@@ -754,6 +754,7 @@ class _Engine:
         self.n = dp.n
         self.multi = any(getattr(c, "dp", dp) is not dp for c in cstates)
         self.dinv = None            # diagonal-block inverses: allocated and made on first use
+        self.ozbuf = None           # int8 digit slices of the factors (blocked solves), made on first use
 
     def _dp_of(self, ci: int) -> DevicePencil:
         return getattr(self.cs[ci], "dp", None) or self.dp
@@ -964,6 +965,8 @@ class _Engine:
         with _stage("solve"):
             dinv = self._dinv(Ks)
             dptr = _ptr(dinv) if dinv is not None else 0
+            if dinv is not None:
+                self._oz_slices(Ks)
             if len(runs) > 1:
                 # scattered contours (refinement passes of a multi-pencil batch):
                 # one gathered call over their factors instead of one per run
@@ -1054,6 +1057,26 @@ class _Engine:
             self.dinv = self.torch.empty(self._dinv_per_pencil * self.P, dtype=self.torch.uint8, device="cuda")
             self._diag_inverses(0, self.P)
         return self.dinv
+
+    def _oz_slices(self, K: int):
+        """Digit slices of the factors for the int8 tensor-core trailing
+        updates of the blocked solves (cirr_ozaki_split_factors): cut once
+        after the factorisation, on the first solve wide enough to take the
+        blocked path, when the int8 mode is on, the factors are dense, n is a
+        multiple of 512 and the buffer (as large as the factors) fits."""
+        if self.ozbuf is not None or K <= 16:
+            return
+        self.ozbuf = False
+        n = self.n
+        if not int(_lib.call("cirr_set_lu_gemm", -1)) or self.klL < n - 1 or self.kuU < n - 1:
+            return
+        nbytes = int(_lib.call("cirr_ozaki_factor_bytes", n, self.P))
+        if nbytes == 0 or nbytes + (12 << 30) > _free_hbm():
+            return
+        with _stage("solve.ozsplit"):
+            self.ozbuf = self.torch.empty(nbytes, dtype=self.torch.uint8, device="cuda")
+            _lib.call("cirr_ozaki_split_factors", _ptr(self.pencils), n, n, n * n, self.P, _ptr(self.ozbuf),
+                      self.stream)
 
     def _bx(self, c, xi):
         """B X for the inside Ritz vectors: the product kept from the residual
@@ -1575,7 +1598,9 @@ class _Engine:
             c.x_host = h[c._x_off:c._x_off + r * k].reshape(r, k)
 
     def free(self):
-        for name in ("pencils", "maxabs", "ipiv", "perm", "minpiv", "info", "dinv"):
+        if getattr(self, "ozbuf", None) is not None and self.ozbuf is not False and hasattr(self, "pencils"):
+            _lib.call("cirr_ozaki_release", _ptr(self.pencils))
+        for name in ("pencils", "maxabs", "ipiv", "perm", "minpiv", "info", "dinv", "ozbuf"):
             if hasattr(self, name):
                 delattr(self, name)
 

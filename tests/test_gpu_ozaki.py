@@ -124,3 +124,89 @@ def test_ozaki_deterministic(lib):
         torch.cuda.synchronize()
         outs.append(C.cpu().numpy())
     assert np.array_equal(outs[0].view(np.float64), outs[1].view(np.float64))
+
+
+@pytest.fixture
+def int8_mode(lib):
+    prev = lib.call("cirr_set_lu_gemm", 1)
+    yield
+    lib.call("cirr_set_lu_gemm", prev)
+
+
+def _factor(lib, A):
+    batch, n, _ = A.shape
+    F = torch.from_numpy(A.copy()).cuda()
+    ipiv = torch.empty((batch, n), dtype=torch.int32, device="cuda")
+    perm = torch.empty((batch, n), dtype=torch.int32, device="cuda")
+    mp = torch.empty(batch, dtype=torch.float64, device="cuda")
+    info = torch.empty(batch, dtype=torch.int32, device="cuda")
+    ws = torch.zeros(lib.call("cirr_zgetrf_ws_bytes", n, batch), dtype=torch.uint8, device="cuda")
+    lib.call("cirr_zgetrf_batched", F.data_ptr(), n, n, n * n, batch, ipiv.data_ptr(), perm.data_ptr(),
+             mp.data_ptr(), info.data_ptr(), ws.data_ptr(), S())
+    torch.cuda.synchronize()
+    assert (info.cpu().numpy() == 0).all()
+    return F, ipiv, perm
+
+
+def test_int8_lu_and_cached_solves(lib, int8_mode):
+    """Dense LU with int8 trailing updates, then blocked solves whose k = 512
+    updates read the kept factor slices: backward error at the FP64 level, the
+    same pivots as the DMMA LU, gathered sub-ranges of the factors included."""
+    import scipy.linalg as sla
+    n, batch, K = 2048, 3, 40
+    rng = np.random.default_rng(2048)
+    A = crandn(rng, batch, n, n)
+    F, ipiv, perm = _factor(lib, A)
+    lib.call("cirr_set_lu_gemm", 0)
+    F0, ipiv0, _ = _factor(lib, A)
+    lib.call("cirr_set_lu_gemm", 1)
+    assert np.array_equal(ipiv.cpu().numpy(), ipiv0.cpu().numpy())
+    dlu = (F - F0).abs().max().item() / F0.abs().max().item()
+    assert dlu < 1e-11, dlu
+    dinv = torch.zeros(lib.call("cirr_diag_inv_bytes", n, batch), dtype=torch.uint8, device="cuda")
+    lib.call("cirr_diag_inverses", F.data_ptr(), n, n, n * n, batch, dinv.data_ptr(), S())
+    nbytes = lib.call("cirr_ozaki_factor_bytes", n, batch)
+    assert nbytes > batch * n * n * 16
+    cache = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    launches0 = lib.call("cirr_launch_count")
+    lib.call("cirr_ozaki_split_factors", F.data_ptr(), n, n, n * n, batch, cache.data_ptr(), S())
+    assert lib.call("cirr_launch_count") - launches0 == n // 512
+    R = crandn(rng, 2, n, K)
+    dR = torch.from_numpy(R).cuda()
+
+    def solve(first, cnt):
+        rhs_of = torch.from_numpy((np.arange(cnt, dtype=np.int32) % 2)).cuda()
+        Y = torch.empty((cnt, n, K), dtype=torch.complex128, device="cuda")
+        dpp = lib.call("cirr_diag_inv_bytes", n, 1)
+        lib.call("cirr_zgetrs_batched", F[first].data_ptr(), n, n, n * n, cnt, perm[first].data_ptr(), dR.data_ptr(),
+                 K, n * K, rhs_of.data_ptr(), K, Y.data_ptr(), K, n * K, dinv.data_ptr() + first * dpp, S())
+        torch.cuda.synchronize()
+        return Y.cpu().numpy()
+
+    l0 = lib.call("cirr_launch_count")
+    y = solve(0, batch)
+    with_cache = lib.call("cirr_launch_count") - l0
+    for j in range(batch):
+        res = np.linalg.norm(A[j] @ y[j] - R[j % 2]) / (np.linalg.norm(A[j]) * np.linalg.norm(y[j]))
+        assert res < 1e-14, res
+    y1 = solve(1, 2)   # a sub-range of the registered factors
+    for j in range(2):
+        res = np.linalg.norm(A[1 + j] @ y1[j] - R[j % 2]) / (np.linalg.norm(A[1 + j]) * np.linalg.norm(y1[j]))
+        assert res < 1e-14, res
+    lib.call("cirr_ozaki_release", F.data_ptr())
+    l0 = lib.call("cirr_launch_count")
+    y2 = solve(0, batch)   # slices released: DMMA path, same solutions to rounding
+    without = lib.call("cirr_launch_count") - l0
+    assert with_cache != without          # the cached path really ran (3 launches per update instead of 1)
+    assert np.abs(y2 - y).max() / np.abs(y).max() < 1e-10
+    # a new factorisation in the same memory drops stale slices by itself
+    lib.call("cirr_ozaki_split_factors", F.data_ptr(), n, n, n * n, batch, cache.data_ptr(), S())
+    F.copy_(torch.from_numpy(A))
+    ws = torch.zeros(lib.call("cirr_zgetrf_ws_bytes", n, batch), dtype=torch.uint8, device="cuda")
+    mp = torch.empty(batch, dtype=torch.float64, device="cuda")
+    info = torch.empty(batch, dtype=torch.int32, device="cuda")
+    lib.call("cirr_zgetrf_batched", F.data_ptr(), n, n, n * n, batch, ipiv.data_ptr(), perm.data_ptr(),
+             mp.data_ptr(), info.data_ptr(), ws.data_ptr(), S())
+    l0 = lib.call("cirr_launch_count")
+    solve(0, batch)
+    assert lib.call("cirr_launch_count") - l0 == without
