@@ -283,7 +283,7 @@ int cirr_ozaki_release(const cirr_cplx* LU);
 /* Arithmetic of the dense LU's k = 512 trailing updates (K2): 0 = FP64 DMMA
  * (zgemm_sub_tma), 1 = the int8 tensor-core path above.  Banded pencils and the
  * in-step updates always take DMMA.  Returns the previous mode; any other
- * argument only queries.  Environment default: CIRR_LU_GEMM=int8 | dmma. */
+ * argument only queries.  Default 1; CIRR_LU_GEMM=dmma starts in mode 0. */
 int cirr_set_lu_gemm(int mode);
 
 /* number of kernels this library has launched since it was loaded (host counter) */

@@ -36,12 +36,13 @@ namespace {
 
 constexpr int OS = 8;         // slices
 constexpr int OBM = 128;      // accumulator rows = TMEM lanes
-constexpr int OBN = 64;       // accumulator columns (real) = 32 complex columns
-constexpr int OKB = 64;       // bytes of K' per stage (rows of the 64-byte swizzle)
+constexpr int OBN = 128;      // accumulator columns (real) = 64 complex columns
+constexpr int OKB = 64;       // bytes of K' per stage (rows of the 64-byte swizzle) = two MMA K steps
 constexpr int ONSTAGE = 2;
 constexpr int OTHREADS = 320; // warp 0: TMA producer, warp 1: MMA issuer, warps 2-9: epilogue
 constexpr int OA_SLICE = OBM * OKB, OB_SLICE = OBN * OKB;
-constexpr int OSTAGE = OS * (OA_SLICE + OB_SLICE);
+constexpr int OSLOT_A = 4, OSLOT_B = 7;   // slice tiles a stage holds (largest sweep: 4 of A, 7 of B)
+constexpr int OSTAGE = OSLOT_A * OA_SLICE + OSLOT_B * OB_SLICE;
 constexpr int OSMEM = ONSTAGE * OSTAGE + 1024 + 256;
 
 __device__ __forceinline__ unsigned osmem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -74,9 +75,9 @@ __device__ __forceinline__ uint64_t oumma_desc(unsigned saddr) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFF);
   d |= (uint64_t)1 << 16;
-  d |= (uint64_t)(512 >> 4) << 32;
+  d |= (uint64_t)((8 * OKB) >> 4) << 32;
   d |= (uint64_t)1 << 46;
-  d |= (uint64_t)4 << 61;
+  d |= (uint64_t)(OKB == 64 ? 4 : 6) << 61;
   return d;
 }
 __device__ __forceinline__ void oumma_i8(unsigned tmem_d, uint64_t da, uint64_t db, unsigned idesc, unsigned acc) {
@@ -84,6 +85,25 @@ __device__ __forceinline__ void oumma_i8(unsigned tmem_d, uint64_t da, uint64_t 
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
       " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}"
       ::"r"(tmem_d), "l"(da), "l"(db), "r"(idesc), "r"(acc) : "memory");
+}
+__device__ __forceinline__ void otma_load4_mc(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                              uint64_t* bar, unsigned short mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6], %7;"
+      ::"r"(osmem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(osmem_u32(bar)), "h"(mask) : "memory");
+}
+__device__ __forceinline__ void oumma_commit_mc(uint64_t* bar, unsigned short mask) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+               ::"r"(osmem_u32(bar)), "h"(mask) : "memory");
+}
+__device__ __forceinline__ void ocluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ unsigned ocluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
 }
 __device__ __forceinline__ void oumma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(osmem_u32(bar)) : "memory");
@@ -110,7 +130,7 @@ struct OzGeom {
   const int* a_bmap; // optional: abatch(b) = a_bmap[b] (gathered solves), else b
 };
 
-__global__ void __launch_bounds__(OTHREADS, 1) ozaki_gemm_kernel(const __grid_constant__ CUtensorMap mapA,
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OTHREADS, 1) ozaki_gemm_kernel(const __grid_constant__ CUtensorMap mapA,
                                                                  const __grid_constant__ CUtensorMap mapB, OzGeom g) {
   extern __shared__ __align__(1024) uint8_t osmem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)osmem_raw + 1023) & ~(uintptr_t)1023);
@@ -122,7 +142,7 @@ __global__ void __launch_bounds__(OTHREADS, 1) ozaki_gemm_kernel(const __grid_co
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < ONSTAGE; ++s) { ombar_init(&full[s], 1); ombar_init(&empty[s], 1); }
+    for (int s = 0; s < ONSTAGE; ++s) { ombar_init(&full[s], 1); ombar_init(&empty[s], 2); }
     ombar_init(tfull, 1);
     ombar_init(tempty, 8);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -133,30 +153,53 @@ __global__ void __launch_bounds__(OTHREADS, 1) ozaki_gemm_kernel(const __grid_co
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  ocluster_sync();   // both CTAs' barriers exist before any remote arrive or multicast
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const unsigned tmem = *tmem_slot;
 
-  const int per = g.tiles_m * g.tiles_n;
+  // A cluster of two CTAs takes two row tiles (2 tmp, 2 tmp + 1) of the same
+  // column tile: each loads its own A slices and half of the B slices, the
+  // latter multicast into both CTAs' shared memory (the kernel is bound by L2
+  // to shared-memory traffic; this removes a quarter of it).  Both CTAs run the
+  // same trip counts; a stage is free when both CTAs' MMAs have read it.
+  const unsigned crank = ocluster_rank();
+  const int tiles_mp = (g.tiles_m + 1) >> 1;
+  const int per = tiles_mp * g.tiles_n;
   const int ntiles = per * g.batch;
   const int nkb = g.K2 / OKB;
+  const int cl_id = blockIdx.x >> 1, cl_n = gridDim.x >> 1;
 
+  // Every output tile (128 rows x 128 real columns) is produced in two passes:
+  // pass 0 forms the accumulators of the weights d = 0..3 (one sweep over K:
+  // 10 slice products among slices 0..3 of both operands), pass 1 those of
+  // d = 4..7 in two sweeps over K (A 0..3 x B 1..7: 16 products, then A 4..7 x
+  // B 0..3: 10 products), so a stage never holds more than 4 + 7 slice tiles
+  // (88 KB; two stages).  Four 128-column accumulators fill the 512 TMEM
+  // columns; with N = 128 an MMA reads (128 + 128) x 32 bytes of shared memory
+  // per 64 tensor cycles -- exactly the 128 B/clk the SM delivers (N = 64 with
+  // all eight accumulators side by side was bound there: 85 % shared-memory
+  // pipe, 52 % tensor pipe, profiles/r02_ozaki_gemm_n64_raw.csv).
   if (warp == 0) {
     if (lane == 0) {
       int it = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (int t = cl_id; t < ntiles; t += cl_n) {
         const int b = t / per, r = t - b * per;
-        const int m0 = (r / g.tiles_n) * OBM, n0 = (r % g.tiles_n) * OBN;
+        const int m0 = (2 * (r / g.tiles_n) + (int)crank) * OBM, n0 = (r % g.tiles_n) * OBN;
         const int ab = (g.a_bmap ? g.a_bmap[b] : b) * g.a_mul + g.a_add;
-        for (int kb = 0; kb < nkb; ++kb, ++it) {
-          const int st = it % ONSTAGE;
-          const unsigned ph = (it / ONSTAGE) & 1;
-          ombar_wait(&empty[st], ph ^ 1);
-          ombar_arrive_expect_tx(&full[st], OSTAGE);
-          uint8_t* base = smem + st * OSTAGE;
-#pragma unroll
-          for (int s = 0; s < OS; ++s) {
-            otma_load4(base + s * OA_SLICE, &mapA, kb * OKB, g.a_row0 + m0, s, ab, &full[st]);
-            otma_load4(base + OS * OA_SLICE + s * OB_SLICE, &mapB, kb * OKB, n0, s, b, &full[st]);
+        // sweep 0: A 0..3 x B 0..3 (d <= 3); sweep 1: A 0..3 x B 1..7 and sweep 2: A 4..7 x B 0..3 (d = 4..7)
+        for (int sw = 0; sw < 3; ++sw) {
+          const int a0 = sw == 2 ? 4 : 0, b0 = sw == 1 ? 1 : 0, nb = sw == 1 ? 7 : 4;
+          for (int kb = 0; kb < nkb; ++kb, ++it) {
+            const int st = it % ONSTAGE;
+            const unsigned ph = (it / ONSTAGE) & 1;
+            ombar_wait(&empty[st], ph ^ 1);
+            ombar_arrive_expect_tx(&full[st], 4 * OA_SLICE + nb * OB_SLICE);
+            uint8_t* base = smem + st * OSTAGE;
+            for (int s = 0; s < 4; ++s)
+              otma_load4(base + s * OA_SLICE, &mapA, kb * OKB, g.a_row0 + m0, a0 + s, ab, &full[st]);
+            for (int s = (int)crank; s < nb; s += 2)
+              otma_load4_mc(base + OSLOT_A * OA_SLICE + s * OB_SLICE, &mapB, kb * OKB, n0, b0 + s, b, &full[st],
+                            (unsigned short)3);
           }
         }
       }
@@ -165,113 +208,127 @@ __global__ void __launch_bounds__(OTHREADS, 1) ozaki_gemm_kernel(const __grid_co
     if (lane == 0) {
       // instruction descriptor: D = S32, A = B = signed int8, both K-major, N >> 3, M >> 4
       constexpr unsigned idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((unsigned)(OBN >> 3) << 17) | ((unsigned)(OBM >> 4) << 24);
-      int it = 0, tl = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
-        ombar_wait(tempty, (tl & 1) ^ 1);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        for (int kb = 0; kb < nkb; ++kb, ++it) {
-          const int st = it % ONSTAGE;
-          const unsigned ph = (it / ONSTAGE) & 1;
-          ombar_wait(&full[st], ph);
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const unsigned abase = osmem_u32(smem + st * OSTAGE), bbase = abase + OS * OA_SLICE;
+      int it = 0, vt = 0;
+      for (int t = cl_id; t < ntiles; t += cl_n) {
+        for (int sw = 0; sw < 3; ++sw) {
+          if (sw < 2) {  // sweeps 0 and 1 start a fresh accumulator set
+            ombar_wait(tempty, (vt & 1) ^ 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            ++vt;
+          }
+          for (int kb = 0; kb < nkb; ++kb, ++it) {
+            const int st = it % ONSTAGE;
+            const unsigned ph = (it / ONSTAGE) & 1;
+            ombar_wait(&full[st], ph);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const unsigned abase = osmem_u32(smem + st * OSTAGE), bbase = abase + OSLOT_A * OA_SLICE;
 #pragma unroll
-          for (int ks = 0; ks < OKB / 32; ++ks) {
+            for (int ks = 0; ks < OKB / 32; ++ks) {
+              const unsigned ak = abase + ks * 32, bk = bbase + ks * 32;
+              if (sw == 0) {         // slots: A_p at p, B_q at q; d = p + q <= 3
 #pragma unroll
-            for (int d = 0; d < OS; ++d) {
+                for (int d = 0; d < 4; ++d)
 #pragma unroll
-              for (int p = 0; p <= d; ++p) {
-                const int q = d - p;
-                oumma_i8(tmem + d * OBN, oumma_desc(abase + p * OA_SLICE + ks * 32),
-                         oumma_desc(bbase + q * OB_SLICE + ks * 32), idesc, (kb > 0 || ks > 0 || p > 0) ? 1u : 0u);
+                  for (int p = 0; p <= d; ++p)
+                    oumma_i8(tmem + d * OBN, oumma_desc(ak + p * OA_SLICE), oumma_desc(bk + (d - p) * OB_SLICE),
+                             idesc, (kb > 0 || ks > 0 || p > 0) ? 1u : 0u);
+              } else if (sw == 1) {  // slots: A_p at p (p <= 3), B_q at q - 1 (q = 1..7); d = 4..7
+#pragma unroll
+                for (int d = 4; d < 8; ++d)
+#pragma unroll
+                  for (int p = 0; p < 4; ++p)
+                    oumma_i8(tmem + (d - 4) * OBN, oumma_desc(ak + p * OA_SLICE),
+                             oumma_desc(bk + (d - p - 1) * OB_SLICE), idesc, (kb > 0 || ks > 0 || p > 0) ? 1u : 0u);
+              } else {               // slots: A_p at p - 4 (p = 4..7), B_q at q (q <= 3); d = 4..7
+#pragma unroll
+                for (int d = 4; d < 8; ++d)
+#pragma unroll
+                  for (int p = 4; p <= d; ++p)
+                    oumma_i8(tmem + (d - 4) * OBN, oumma_desc(ak + (p - 4) * OA_SLICE),
+                             oumma_desc(bk + (d - p) * OB_SLICE), idesc, 1u);
               }
             }
+            oumma_commit_mc(&empty[st], (unsigned short)3);
           }
-          oumma_commit(&empty[st]);
+          if (sw != 1) oumma_commit(tfull);
         }
-        oumma_commit(tfull);
       }
     }
   } else {
     // Eight epilogue warps: warp w reads TMEM lanes 32 (w % 4) .. + 31 (its
-    // hardware quadrant) and the 32-column half (w - 2) / 4 of every
-    // accumulator.  The weighted sum of the eight accumulators of an element
-    // is formed in two int64 (weights 2^-21 and 2^-49), converted once; the
-    // TMEM is handed back to the MMA warp before C is touched, so the next
-    // tile's products run under this tile's read-modify-write of C.
+    // hardware quadrant) and the 64-column half (w - 2) / 4 of the four
+    // accumulators.  Their weighted sum is formed in one int64 and converted
+    // once (weight 2^-21 after pass 0, 2^-49 after pass 1); the TMEM goes back
+    // to the MMA warp before C is touched, so the next pass runs under this
+    // pass's read-modify-write of C.  Both passes of an element are applied by
+    // the same thread, in order.
     const int quad = warp & 3;
     const int half = (warp - 2) >> 2;
-    int tl = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+    int vt = 0;
+    for (int t = cl_id; t < ntiles; t += cl_n) {
       const int b = t / per, r = t - b * per;
-      const int m0 = (r / g.tiles_n) * OBM, n0 = (r % g.tiles_n) * OBN;
+      const int m0 = (2 * (r / g.tiles_n) + (int)crank) * OBM, n0 = (r % g.tiles_n) * OBN;
       const int row = m0 + quad * 32 + lane;
-      const int col0 = (n0 >> 1) + half * 16;   // first complex column of this thread
+      const int col0 = (n0 >> 1) + half * 32;   // first complex column of this thread
       const bool rok = row < g.M;
       cplx* crow = g.C + (long long)b * g.sC + (long long)row * g.ldc + col0;
       const double* sbp = g.sb + (long long)b * g.N + col0;
       if (rok && col0 < g.N) {
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(crow));
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(crow + 8));
+#pragma unroll
+        for (int j = 0; j < 32; j += 8) asm volatile("prefetch.global.L2 [%0];" ::"l"(crow + j));
       }
       const int ab = (g.a_bmap ? g.a_bmap[b] : b) * g.a_mul + g.a_add;
       const double sai = rok ? g.sa[(long long)ab * g.sa_stride + g.a_row0 + row] : 0.0;
-      double v[32];
-      ombar_wait(tfull, tl & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      for (int pass = 0; pass < 2; ++pass, ++vt) {
+        const double sw = sai * (pass ? 0x1p-49 : 0x1p-21);
+        double v[64];
+        ombar_wait(tfull, vt & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
-      for (int c = 0; c < 32; c += 16) {
-        unsigned v0[16], v1[16], v2[16], v3[16];
-        long long hi[16];
-        const unsigned ta = tmem + ((unsigned)(quad * 32) << 16) + half * 32 + c;
-        otmem_ld16(ta + 0 * OBN, v0);
-        otmem_ld16(ta + 1 * OBN, v1);
-        otmem_ld16(ta + 2 * OBN, v2);
-        otmem_ld16(ta + 3 * OBN, v3);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        for (int c = 0; c < 64; c += 16) {
+          unsigned v0[16], v1[16], v2[16], v3[16];
+          const unsigned ta = tmem + ((unsigned)(quad * 32) << 16) + half * 64 + c;
+          otmem_ld16(ta + 0 * OBN, v0);
+          otmem_ld16(ta + 1 * OBN, v1);
+          otmem_ld16(ta + 2 * OBN, v2);
+          otmem_ld16(ta + 3 * OBN, v3);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-          hi[j] = ((long long)(int)v0[j] << 21) + ((long long)(int)v1[j] << 14) + ((long long)(int)v2[j] << 7) +
-                  (long long)(int)v3[j];
-        otmem_ld16(ta + 4 * OBN, v0);
-        otmem_ld16(ta + 5 * OBN, v1);
-        otmem_ld16(ta + 6 * OBN, v2);
-        otmem_ld16(ta + 7 * OBN, v3);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const long long lo = ((long long)(int)v0[j] << 21) + ((long long)(int)v1[j] << 14) +
-                               ((long long)(int)v2[j] << 7) + (long long)(int)v3[j];
-          v[c + j] = fma((double)lo, 0x1p-49, (double)hi[j] * 0x1p-21);
+          for (int j = 0; j < 16; ++j)
+            v[c + j] = (double)(((long long)(int)v0[j] << 21) + ((long long)(int)v1[j] << 14) +
+                                ((long long)(int)v2[j] << 7) + (long long)(int)v3[j]);
         }
-      }
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) ombar_arrive(tempty);
-      if (rok) {
-        if (col0 + 16 <= g.N) {
-          cplx cv[16];
-          double sc[16];
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) ombar_arrive(tempty);
+        if (rok) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) cv[j] = crow[j];
+          for (int h = 0; h < 32; h += 16) {
+            if (col0 + h + 16 <= g.N) {
+              cplx cv[16];
+              double sc[16];
 #pragma unroll
-          for (int j = 0; j < 16; ++j) sc[j] = sai * sbp[j];
+              for (int j = 0; j < 16; ++j) cv[j] = crow[h + j];
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            cv[j].x = fma(-v[2 * j], sc[j], cv[j].x);
-            cv[j].y = fma(-v[2 * j + 1], sc[j], cv[j].y);
-          }
+              for (int j = 0; j < 16; ++j) sc[j] = sw * sbp[h + j];
 #pragma unroll
-          for (int j = 0; j < 16; ++j) crow[j] = cv[j];
-        } else {
+              for (int j = 0; j < 16; ++j) {
+                cv[j].x = fma(-v[2 * (h + j)], sc[j], cv[j].x);
+                cv[j].y = fma(-v[2 * (h + j) + 1], sc[j], cv[j].y);
+              }
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            if (col0 + j < g.N) {
-              const double sc = sai * sbp[j];
-              cplx cv = crow[j];
-              cv.x = fma(-v[2 * j], sc, cv.x);
-              cv.y = fma(-v[2 * j + 1], sc, cv.y);
-              crow[j] = cv;
+              for (int j = 0; j < 16; ++j) crow[h + j] = cv[j];
+            } else {
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                if (col0 + h + j < g.N) {
+                  const double sc = sw * sbp[h + j];
+                  cplx cv = crow[h + j];
+                  cv.x = fma(-v[2 * (h + j)], sc, cv.x);
+                  cv.y = fma(-v[2 * (h + j) + 1], sc, cv.y);
+                  crow[h + j] = cv;
+                }
+              }
             }
           }
         }
@@ -280,6 +337,7 @@ __global__ void __launch_bounds__(OTHREADS, 1) ozaki_gemm_kernel(const __grid_co
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  ocluster_sync();   // no multicast or remote arrive may land in a CTA that has left
   if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
 }
 
@@ -424,7 +482,8 @@ int encode_slice_map(CUtensorMap* map, const int8_t* base, long long K2, long lo
   cuuint32_t box[4] = {(cuuint32_t)OKB, (cuuint32_t)box_rows, 1, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(base), dims, strides, box, estr,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, OKB == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : (int)cudaErrorInvalidValue;
 }
@@ -562,8 +621,8 @@ int ozaki_cached_update(const cplx* LU, int n, int col0, int kw, int a_row0, int
     g.sa_stride = n; g.a_row0 = a_row0;
     g.a_mul = c.nsb; g.a_add = (int)(f0 * c.nsb + col0 / OZ_W);
     g.a_bmap = pmap;
-    const long long ntiles = (long long)g.tiles_m * g.tiles_n * batch;
-    ozaki_gemm_kernel<<<(int)min((long long)sms, ntiles), OTHREADS, OSMEM, stream>>>(mA, mB, g);
+    const long long npairs = (long long)((g.tiles_m + 1) / 2) * g.tiles_n * batch;
+    ozaki_gemm_kernel<<<2 * (int)min((long long)(sms / 2), npairs), OTHREADS, OSMEM, stream>>>(mA, mB, g);
     cirr_note_launch();
     cudaError_t le = cudaGetLastError();
     if (le != cudaSuccess) rc = (int)le;
@@ -576,12 +635,13 @@ int ozaki_cached_update(const cplx* LU, int n, int col0, int kw, int a_row0, int
 namespace {
 }  // namespace
 
-// 0: FP64 DMMA trailing updates; 1: int8 tensor-core (Ozaki) trailing updates
-// for the dense LU's k = 512 steps.  CIRR_LU_GEMM=int8 / dmma sets the default.
+// 0: FP64 DMMA trailing updates; 1 (default): int8 tensor-core (Ozaki) trailing
+// updates for the dense LU's k = 512 steps and the blocked solves.
+// CIRR_LU_GEMM=dmma | int8 sets the initial mode, cirr_set_lu_gemm changes it.
 int g_cirr_lu_gemm = [] {
   const char* e = getenv("CIRR_LU_GEMM");
-  if (!e) return 0;
-  return (e[0] == 'i' || e[0] == '1') ? 1 : 0;
+  if (!e) return 1;
+  return (e[0] == 'd' || e[0] == 'f' || e[0] == '0') ? 0 : 1;
 }();
 
 bool ozaki_enabled() { return g_cirr_lu_gemm == 1; }
@@ -656,8 +716,8 @@ int ozaki_zgemm_sub(const cplx* A, long long lda, long long sA, const cplx* B, l
     g.C = C + (long long)b0 * sC; g.ldc = ldc; g.sC = sC;
     g.sa = sa; g.sb = sb;
     g.sa_stride = M; g.a_row0 = 0; g.a_mul = 1; g.a_add = 0; g.a_bmap = nullptr;
-    const long long ntiles = (long long)g.tiles_m * g.tiles_n * nb;
-    const int grid = (int)min((long long)sms, ntiles);
+    const long long npairs = (long long)((g.tiles_m + 1) / 2) * g.tiles_n * nb;
+    const int grid = 2 * (int)min((long long)(sms / 2), npairs);
     ozaki_gemm_kernel<<<grid, OTHREADS, OSMEM, stream>>>(mA, mB, g);
     cirr_note_launch();
     cudaError_t le = cudaGetLastError();
