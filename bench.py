@@ -48,6 +48,9 @@ sys.path.insert(0, ROOT)
 FP64_DMMA_PEAK_TFLOPS = 37.1  # tools/fp64_peak.cu on this pool's B200 (profiles/fp64_peak_r01.jsonl)
 METRIC = "CIRR GEP solves per second (config 4: n=4096 dense non-Hermitian, 2 ellipses x 64 nodes, L=32, M=8)"
 UNIT = "GEP/s"
+# complex128 in and out; the k = 512 updates of the dense LU and of the blocked solves as exact int8 digit
+# products (Ozaki splitting, 55 bits per operand) on tcgen05, every other GEMM in FP64 on DMMA
+DTYPE = "c128 (int8 slice products on tcgen05 for the k=512 LU/solve updates, f64 DMMA elsewhere)"
 
 
 def parse():
@@ -189,10 +192,10 @@ def cpu_model() -> str:
 
 def lu_traffic():
     """DRAM bytes of the LU stage per step, measured by ncu on this code
-    (profiles/r02_v4_lu_traffic.json, TAG=_v4 tools/ncu_r02.sh: dram__bytes_read +
+    (profiles/r02_v5_lu_traffic.json, TAG=_v5 tools/ncu_r02.sh: dram__bytes_read +
     dram__bytes_write over every LU kernel of one solve_multi); null when the
     profile is absent."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r02_v4_lu_traffic.json")
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r02_v5_lu_traffic.json")
     try:
         with open(path) as f:
             d = json.load(f)
@@ -306,6 +309,51 @@ def _lu_line(timer):
     fl = timer.work.get("lu_flops", 0.0)
     tf = fl / (lu_ms / 1e3) / 1e12 if lu_ms else 0.0
     return {"lu_ms": lu_ms, "lu_flops": fl, "lu_tflops": tf, "lu_frac_of_fp64_peak": tf / FP64_DMMA_PEAK_TFLOPS}
+
+
+INT8_PEAK_TOPS = 4570.0   # measured: tools/i8_peak.cu, back-to-back tcgen05.mma kind::i8 (M128 N128 K32), 148 SMs
+
+
+def int8_kernel_roofline():
+    """The int8 (Ozaki) trailing update timed alone at the LU's largest step
+    (m = 3584, k = 512, 16 pencils; the step processes 128 in chunks): CUDA
+    events over the split kernels + ozaki_gemm_kernel on the launching stream.
+    int8 operations: 36 slice products x 2 x m x 2n x 2k = 288 mnk."""
+    import torch
+    from paper_2511_01927_b200 import _lib
+
+    m, W, batch, reps = 3584, 512, 16, 5
+    n = m + W
+    g = torch.Generator(device="cuda").manual_seed(0)
+    P = torch.randn((batch, n, n), dtype=torch.complex128, device="cuda", generator=g)
+    st = torch.cuda.current_stream().cuda_stream
+    base = P.data_ptr()
+    off = lambda r, c: base + 16 * (r * n + c)
+
+    def run():
+        _lib.call("cirr_ozaki_zgemm_sub", off(W, 0), n, n * n, off(0, W), n, n * n, off(W, W), n, n * n, m, m, W,
+                  batch, st)
+
+    for _ in range(2):
+        run()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        run()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    ops = 288.0 * m * m * W * batch
+    del P
+    torch.cuda.empty_cache()
+    return {"kernel": "ozaki_gemm_kernel + splits (tcgen05.mma kind::i8, one k = 512 trailing update, m = 3584, "
+                      "16 pencils, timed alone)",
+            "bound": "tensor", "achieved": ops / (ms / 1e3) / 1e12, "peak": INT8_PEAK_TOPS, "unit": "TOP/s (int8)",
+            "frac": ops / (ms / 1e3) / 1e12 / INT8_PEAK_TOPS,
+            "peak_source": "measured tcgen05.mma kind::i8 issue rate, burst (tools/i8_peak.cu; MEASURED_PEAKS.json "
+                           "has bf16 only: 2 x its 1633.6 bf16 TF/s burst = 3267)",
+            "fp64_equivalent_tflops": 8.0 * m * m * W * batch / (ms / 1e3) / 1e12, "ms": ms}
+
 
 
 def per_config_block():
@@ -483,8 +531,11 @@ def run_cirr(args):
             "early_exit": "stop refining a contour once its converged set is unchanged across two passes",
             "conjugate_pairs+early_exit": "both of the above",
         }
+        labels["fp64_dmma"] = ("every GEMM in FP64 on DMMA (cirr_set_lu_gemm(0)): the reference's own arithmetic "
+                               "type on the tensor cores, the path of record before the int8 slices")
         for name, label in labels.items():
             vcfg = dataclasses.replace(cfg, conjugate_pairs="conjugate_pairs" in name, early_exit="early_exit" in name)
+            _lib.call("cirr_set_lu_gemm", 0 if name == "fp64_dmma" else 1)
             solve_multi(dp, wl.contours, vcfg, seed=0)
             vt = S.StageTimer()
             S.set_stage_timer(vt)
@@ -506,8 +557,12 @@ def run_cirr(args):
                     for lam in rr.eigenvalues:
                         diff = max(diff, float(np.min(np.abs(rv.eigenvalues - lam)) / abs(lam)))
             vwork = dict(vt.work)
+            if name == "fp64_dmma":
+                variants[name + "_stage_ms"] = {k: v / args.steps for k, v in sorted(vt.totals().items())}
+            _lib.call("cirr_set_lu_gemm", 1)
             variants[name] = {
-                "label": "variant, not the reference's algorithm: " + label,
+                "label": ("variant (same algorithm, FP64 arithmetic): " if name == "fp64_dmma" else
+                          "variant, not the reference's algorithm: ") + label,
                 "value": world * args.steps / (vms / 1e3), "unit": UNIT, "ms_per_step": vms / args.steps,
                 "eigenpairs": vcounts, "iterations": [r.stats.iterations if r is not None else 0 for r in vm.results],
                 "n_factorizations": vm.stats.n_factorizations, "n_linear_solves": vm.stats.n_linear_solves,
@@ -540,18 +595,30 @@ def run_cirr(args):
         except ImportError:
             pass
 
+    int8_roof = None
+    if rank == 0:
+        try:
+            int8_roof = int8_kernel_roofline()
+        except Exception as exc:  # the measurement is evidence, not the product: report why it is missing
+            int8_roof = {"error": repr(exc)}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": per_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "c128 (f64 DMMA)", "data": "synthetic (seeded BASELINE config 4)",
+            "vs_baseline": None, "dtype": DTYPE, "data": "synthetic (seeded BASELINE config 4)",
             "config": bench_config(wl),
-            "roofline": {"bound": "tensor", "kernel": "batched zgetrf (K2: panel + DMMA trailing GEMM)",
+            "roofline": {"bound": "tensor", "kernel": "batched zgetrf (K2: panel + trailing updates; the k = 512 "
+                                                      "updates on int8 tensor cores, the rest on FP64 DMMA)",
                          "achieved": lu_tflops, "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
                          "frac": lu_tflops / FP64_DMMA_PEAK_TFLOPS,
                          "peak_source": "measured DMMA.8x8x4 FP64 peak (tools/fp64_peak.cu; "
                                         "MEASURED_PEAKS.json has no FP64 entry)",
-                         "algorithmic": "8 n^3 / 3 per pencil x 128 pencils per step",
+                         "algorithmic": "8 n^3 / 3 per pencil x 128 pencils per step (FP64-equivalent flops)",
+                         "note": "frac exceeds 1 because 82 % of the LU's flops (the k = 512 trailing updates) run as "
+                                 "exact int8 slice products on tcgen05 (4.57 POPS measured) instead of FP64 DMMA "
+                                 "(37.1 TF/s): see int8_kernel for that kernel against its own peak, and "
+                                 "variants.fp64_dmma for the all-FP64 path",
+                         "int8_kernel": int8_roof,
                          **lu_traffic()},
             "lu_plus_moment_stage": {"tflops": stage_tflops, "frac_of_fp64_peak": stage_tflops / FP64_DMMA_PEAK_TFLOPS,
                                      "flops_per_step": stage_flops / args.steps,

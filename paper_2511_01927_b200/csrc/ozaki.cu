@@ -38,9 +38,10 @@ constexpr int OS = 8;         // slices
 constexpr int OBM = 128;      // accumulator rows = TMEM lanes
 constexpr int OBN = 128;      // accumulator columns (real) = 64 complex columns
 constexpr int OKB = 64;       // bytes of K' per stage (rows of the 64-byte swizzle) = two MMA K steps
-constexpr int ONSTAGE = 2;
+constexpr int ONSTAGE = 3;
 constexpr int OTHREADS = 320; // warp 0: TMA producer, warp 1: MMA issuer, warps 2-9: epilogue
-constexpr int OA_SLICE = OBM * OKB, OB_SLICE = OBN * OKB;
+constexpr int OBNH = OBN / 2;   // rows of a B slice tile held by each CTA of the pair (cta_group::2)
+constexpr int OA_SLICE = OBM * OKB, OB_SLICE = OBNH * OKB;
 constexpr int OSLOT_A = 4, OSLOT_B = 7;   // slice tiles a stage holds (largest sweep: 4 of A, 7 of B)
 constexpr int OSTAGE = OSLOT_A * OA_SLICE + OSLOT_B * OB_SLICE;
 constexpr int OSMEM = ONSTAGE * OSTAGE + 1024 + 256;
@@ -61,6 +62,13 @@ __device__ __forceinline__ void ombar_wait(uint64_t* bar, unsigned parity) {
       "{\n .reg .pred p;\n WAIT_%=:\n"
       " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
       " @!p bra WAIT_%=;\n}" ::"r"(osmem_u32(bar)), "r"(parity) : "memory");
+}
+// wait with cluster-scope acquire (arrivals come from the other CTA of the pair)
+__device__ __forceinline__ void ombar_wait_cluster(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAITC_%=:\n"
+      " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAITC_%=;\n}" ::"r"(osmem_u32(bar)), "r"(parity) : "memory");
 }
 __device__ __forceinline__ void otma_load4(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
                                            uint64_t* bar) {
@@ -92,6 +100,32 @@ __device__ __forceinline__ void otma_load4_mc(void* dst, const CUtensorMap* map,
       "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster"
       " [%0], [%1, {%2, %3, %4, %5}], [%6], %7;"
       ::"r"(osmem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(osmem_u32(bar)), "h"(mask) : "memory");
+}
+// TMA load into this CTA's shared memory, completion on the pair leader's barrier
+__device__ __forceinline__ void otma_load4_pair(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                                unsigned leader_bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];"
+      ::"r"(osmem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(leader_bar) : "memory");
+}
+__device__ __forceinline__ unsigned omapa(const void* p, unsigned rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(osmem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void ombar_arrive_cluster(unsigned cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void oumma2_i8(unsigned tmem_d, uint64_t da, uint64_t db, unsigned idesc, unsigned acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}"
+      ::"r"(tmem_d), "l"(da), "l"(db), "r"(idesc), "r"(acc) : "memory");
+}
+__device__ __forceinline__ void oumma2_commit_mc(uint64_t* bar, unsigned short mask) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+               ::"r"(osmem_u32(bar)), "h"(mask) : "memory");
 }
 __device__ __forceinline__ void oumma_commit_mc(uint64_t* bar, unsigned short mask) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
@@ -142,14 +176,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OTHREADS, 1) ozaki_g
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < ONSTAGE; ++s) { ombar_init(&full[s], 1); ombar_init(&empty[s], 2); }
+    for (int s = 0; s < ONSTAGE; ++s) { ombar_init(&full[s], 1); ombar_init(&empty[s], 1); }
     ombar_init(tfull, 1);
-    ombar_init(tempty, 8);
+    ombar_init(tempty, 16);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(osmem_u32(tmem_slot)) : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(osmem_u32(tmem_slot)) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -193,26 +227,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OTHREADS, 1) ozaki_g
             const int st = it % ONSTAGE;
             const unsigned ph = (it / ONSTAGE) & 1;
             ombar_wait(&empty[st], ph ^ 1);
-            ombar_arrive_expect_tx(&full[st], 4 * OA_SLICE + nb * OB_SLICE);
+            // both CTAs' tiles complete on the leader's barrier (the MMA issuer lives there)
+            if (crank == 0) ombar_arrive_expect_tx(&full[st], 2 * (4 * OA_SLICE + nb * OB_SLICE));
+            const unsigned lbar = omapa(&full[st], 0);
             uint8_t* base = smem + st * OSTAGE;
             for (int s = 0; s < 4; ++s)
-              otma_load4(base + s * OA_SLICE, &mapA, kb * OKB, g.a_row0 + m0, a0 + s, ab, &full[st]);
-            for (int s = (int)crank; s < nb; s += 2)
-              otma_load4_mc(base + OSLOT_A * OA_SLICE + s * OB_SLICE, &mapB, kb * OKB, n0, b0 + s, b, &full[st],
-                            (unsigned short)3);
+              otma_load4_pair(base + s * OA_SLICE, &mapA, kb * OKB, g.a_row0 + m0, a0 + s, ab, lbar);
+            for (int s = 0; s < nb; ++s)
+              otma_load4_pair(base + OSLOT_A * OA_SLICE + s * OB_SLICE, &mapB, kb * OKB, n0 + (int)crank * OBNH,
+                              b0 + s, b, lbar);
           }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // instruction descriptor: D = S32, A = B = signed int8, both K-major, N >> 3, M >> 4
-      constexpr unsigned idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((unsigned)(OBN >> 3) << 17) | ((unsigned)(OBM >> 4) << 24);
+    if (lane == 0 && crank == 0) {
+      // instruction descriptor: D = S32, A = B = signed int8, both K-major, N >> 3, M >> 4 (M = 256 over the CTA pair)
+      constexpr unsigned idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((unsigned)(OBN >> 3) << 17) | ((unsigned)((2 * OBM) >> 4) << 24);
       int it = 0, vt = 0;
       for (int t = cl_id; t < ntiles; t += cl_n) {
         for (int sw = 0; sw < 3; ++sw) {
           if (sw < 2) {  // sweeps 0 and 1 start a fresh accumulator set
-            ombar_wait(tempty, (vt & 1) ^ 1);
+            ombar_wait_cluster(tempty, (vt & 1) ^ 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             ++vt;
           }
@@ -230,27 +266,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OTHREADS, 1) ozaki_g
                 for (int d = 0; d < 4; ++d)
 #pragma unroll
                   for (int p = 0; p <= d; ++p)
-                    oumma_i8(tmem + d * OBN, oumma_desc(ak + p * OA_SLICE), oumma_desc(bk + (d - p) * OB_SLICE),
+                    oumma2_i8(tmem + d * OBN, oumma_desc(ak + p * OA_SLICE), oumma_desc(bk + (d - p) * OB_SLICE),
                              idesc, (kb > 0 || ks > 0 || p > 0) ? 1u : 0u);
               } else if (sw == 1) {  // slots: A_p at p (p <= 3), B_q at q - 1 (q = 1..7); d = 4..7
 #pragma unroll
                 for (int d = 4; d < 8; ++d)
 #pragma unroll
                   for (int p = 0; p < 4; ++p)
-                    oumma_i8(tmem + (d - 4) * OBN, oumma_desc(ak + p * OA_SLICE),
+                    oumma2_i8(tmem + (d - 4) * OBN, oumma_desc(ak + p * OA_SLICE),
                              oumma_desc(bk + (d - p - 1) * OB_SLICE), idesc, (kb > 0 || ks > 0 || p > 0) ? 1u : 0u);
               } else {               // slots: A_p at p - 4 (p = 4..7), B_q at q (q <= 3); d = 4..7
 #pragma unroll
                 for (int d = 4; d < 8; ++d)
 #pragma unroll
                   for (int p = 4; p <= d; ++p)
-                    oumma_i8(tmem + (d - 4) * OBN, oumma_desc(ak + (p - 4) * OA_SLICE),
+                    oumma2_i8(tmem + (d - 4) * OBN, oumma_desc(ak + (p - 4) * OA_SLICE),
                              oumma_desc(bk + (d - p) * OB_SLICE), idesc, 1u);
               }
             }
-            oumma_commit_mc(&empty[st], (unsigned short)3);
+            oumma2_commit_mc(&empty[st], (unsigned short)3);
           }
-          if (sw != 1) oumma_commit(tfull);
+          if (sw != 1) oumma2_commit_mc(tfull, (unsigned short)3);
         }
       }
     }
@@ -300,7 +336,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OTHREADS, 1) ozaki_g
         }
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
-        if (lane == 0) ombar_arrive(tempty);
+        if (lane == 0) ombar_arrive_cluster(omapa(tempty, 0));
         if (rok) {
 #pragma unroll
           for (int h = 0; h < 32; h += 16) {
@@ -338,7 +374,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OTHREADS, 1) ozaki_g
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   ocluster_sync();   // no multicast or remote arrive may land in a CTA that has left
-  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
 }
 
 // Eight signed 7-bit digits of t (|t| < 64): t = sum_s d_s 2^(-7 s) up to 2^-49.
@@ -602,7 +638,7 @@ int ozaki_cached_update(const cplx* LU, int n, int col0, int kw, int a_row0, int
   cirr_note_launch();
   CUtensorMap mA, mB;
   if (encode_slice_map(&mA, c.slices, K2, n, (long long)c.nfac * c.nsb, OBM) != 0 ||
-      encode_slice_map(&mB, wb, K2, 2LL * N, batch, OBN) != 0) {
+      encode_slice_map(&mB, wb, K2, 2LL * N, batch, OBNH) != 0) {
     rc = (int)cudaErrorInvalidValue;
   } else {
     static int sms = 0;
@@ -705,7 +741,7 @@ int ozaki_zgemm_sub(const cplx* A, long long lda, long long sA, const cplx* B, l
                                                                                       sB, K, N, sb, wb);
     cirr_note_launch();
     CUtensorMap mA, mB;
-    if (encode_slice_map(&mA, wa, K2, M, nb, OBM) != 0 || encode_slice_map(&mB, wb, K2, 2LL * N, nb, OBN) != 0) {
+    if (encode_slice_map(&mA, wa, K2, M, nb, OBM) != 0 || encode_slice_map(&mB, wb, K2, 2LL * N, nb, OBNH) != 0) {
       rc = (int)cudaErrorInvalidValue;
       break;
     }

@@ -8,7 +8,8 @@ import json
 import sys
 
 LU_KERNELS = ("assemble_kernel", "panel2_kernel", "swap_kernel", "linv_kernel", "zgemm_sub_tma", "perm_kernel",
-              "init_kernel", "diag_inv128_kernel")
+              "init_kernel", "diag_inv128_kernel", "ozaki_gemm_kernel", "ozaki_split_a_kernel", "ozaki_split_b_kernel",
+              "ozaki_colscale_kernel")
 SCALE = {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0}
 
 
