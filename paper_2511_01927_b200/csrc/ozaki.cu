@@ -150,6 +150,18 @@ __device__ __forceinline__ void otmem_ld16(unsigned taddr, unsigned* v) {
       : "r"(taddr) : "memory");
 }
 
+// 16 TMEM lanes x 32 columns: lane l of the warp gets, for repetition j = 0..3, columns
+// 8 j + 2 (l % 4) + {0, 1} of row l / 4 (registers 4 j + 0, 1) and of row l / 4 + 8
+// (registers 4 j + 2, 3): two adjacent accumulator columns = one complex element,
+// four lanes = 64 contiguous bytes of a row of C.
+__device__ __forceinline__ void otmem_ld_16x256b_x4(unsigned taddr, unsigned* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x256b.x4.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr) : "memory");
+}
+
 struct OzGeom {
   int M, N;          // rows, complex columns of C
   int K2;            // bytes of K' = 2 K
@@ -300,71 +312,76 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OTHREADS, 1) ozaki_g
     // the same thread, in order.
     const int quad = warp & 3;
     const int half = (warp - 2) >> 2;
+    const int tr = lane >> 2, tc = lane & 3;
     int vt = 0;
     for (int t = cl_id; t < ntiles; t += cl_n) {
       const int b = t / per, r = t - b * per;
       const int m0 = (2 * (r / g.tiles_n) + (int)crank) * OBM, n0 = (r % g.tiles_n) * OBN;
-      const int row = m0 + quad * 32 + lane;
-      const int col0 = (n0 >> 1) + half * 32;   // first complex column of this thread
-      const bool rok = row < g.M;
-      cplx* crow = g.C + (long long)b * g.sC + (long long)row * g.ldc + col0;
+      // this thread: rows row0 + 16 hh + 8 rr (hh, rr in {0, 1}), complex columns col0 + 16 cg + 4 j (cg < 2, j < 4)
+      const int row0 = m0 + quad * 32 + tr;
+      const int col0 = (n0 >> 1) + half * 32 + tc;
+      cplx* cbase = g.C + (long long)b * g.sC + (long long)row0 * g.ldc + col0;
       const double* sbp = g.sb + (long long)b * g.N + col0;
-      if (rok && col0 < g.N) {
-#pragma unroll
-        for (int j = 0; j < 32; j += 8) asm volatile("prefetch.global.L2 [%0];" ::"l"(crow + j));
-      }
       const int ab = (g.a_bmap ? g.a_bmap[b] : b) * g.a_mul + g.a_add;
-      const double sai = rok ? g.sa[(long long)ab * g.sa_stride + g.a_row0 + row] : 0.0;
+      const double* sap = g.sa + (long long)ab * g.sa_stride + g.a_row0 + row0;
+      double sar[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int rw = row0 + 8 * q;
+        sar[q] = rw < g.M ? sap[8 * q] : 0.0;
+        if (rw < g.M && col0 < g.N) {
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(cbase + (long long)(8 * q) * g.ldc));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(cbase + (long long)(8 * q) * g.ldc + 16));
+        }
+      }
+      double sbc[8];
+#pragma unroll
+      for (int cj = 0; cj < 8; ++cj) sbc[cj] = (col0 + 4 * cj < g.N) ? sbp[4 * cj] : 0.0;
       for (int pass = 0; pass < 2; ++pass, ++vt) {
-        const double sw = sai * (pass ? 0x1p-49 : 0x1p-21);
+        const double pw = pass ? 0x1p-49 : 0x1p-21;
         double v[64];
         ombar_wait(tfull, vt & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
-        for (int c = 0; c < 64; c += 16) {
+        for (int hc = 0; hc < 4; ++hc) {   // hc = 2 hh + cg
           unsigned v0[16], v1[16], v2[16], v3[16];
-          const unsigned ta = tmem + ((unsigned)(quad * 32) << 16) + half * 64 + c;
-          otmem_ld16(ta + 0 * OBN, v0);
-          otmem_ld16(ta + 1 * OBN, v1);
-          otmem_ld16(ta + 2 * OBN, v2);
-          otmem_ld16(ta + 3 * OBN, v3);
+          const unsigned ta = tmem + ((unsigned)(quad * 32 + (hc >> 1) * 16) << 16) + half * 64 + (hc & 1) * 32;
+          otmem_ld_16x256b_x4(ta + 0 * OBN, v0);
+          otmem_ld_16x256b_x4(ta + 1 * OBN, v1);
+          otmem_ld_16x256b_x4(ta + 2 * OBN, v2);
+          otmem_ld_16x256b_x4(ta + 3 * OBN, v3);
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
           for (int j = 0; j < 16; ++j)
-            v[c + j] = (double)(((long long)(int)v0[j] << 21) + ((long long)(int)v1[j] << 14) +
-                                ((long long)(int)v2[j] << 7) + (long long)(int)v3[j]);
+            v[hc * 16 + j] = (double)(((long long)(int)v0[j] << 21) + ((long long)(int)v1[j] << 14) +
+                                      ((long long)(int)v2[j] << 7) + (long long)(int)v3[j]);
         }
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
         if (lane == 0) ombar_arrive_cluster(omapa(tempty, 0));
-        if (rok) {
+        // C -= v sa sb: each warp instruction touches 8 rows x 64 contiguous bytes
 #pragma unroll
-          for (int h = 0; h < 32; h += 16) {
-            if (col0 + h + 16 <= g.N) {
-              cplx cv[16];
-              double sc[16];
+        for (int hh = 0; hh < 2; ++hh) {
 #pragma unroll
-              for (int j = 0; j < 16; ++j) cv[j] = crow[h + j];
+          for (int rr = 0; rr < 2; ++rr) {
+            const int q = 2 * hh + rr;
+            if (row0 + 8 * q < g.M) {
+              cplx* crow = cbase + (long long)(8 * q) * g.ldc;
+              const double sr = sar[q] * pw;
+              cplx cv[8];
 #pragma unroll
-              for (int j = 0; j < 16; ++j) sc[j] = sw * sbp[h + j];
+              for (int cj = 0; cj < 8; ++cj)
+                if (col0 + 4 * cj < g.N) cv[cj] = crow[4 * cj];
 #pragma unroll
-              for (int j = 0; j < 16; ++j) {
-                cv[j].x = fma(-v[2 * (h + j)], sc[j], cv[j].x);
-                cv[j].y = fma(-v[2 * (h + j) + 1], sc[j], cv[j].y);
+              for (int cj = 0; cj < 8; ++cj) {
+                const int vi = (2 * hh + (cj >> 2)) * 16 + 4 * (cj & 3) + 2 * rr;
+                const double sc = sr * sbc[cj];
+                cv[cj].x = fma(-v[vi], sc, cv[cj].x);
+                cv[cj].y = fma(-v[vi + 1], sc, cv[cj].y);
               }
 #pragma unroll
-              for (int j = 0; j < 16; ++j) crow[h + j] = cv[j];
-            } else {
-#pragma unroll
-              for (int j = 0; j < 16; ++j) {
-                if (col0 + h + j < g.N) {
-                  const double sc = sw * sbp[h + j];
-                  cplx cv = crow[h + j];
-                  cv.x = fma(-v[2 * (h + j)], sc, cv.x);
-                  cv.y = fma(-v[2 * (h + j) + 1], sc, cv.y);
-                  crow[h + j] = cv;
-                }
-              }
+              for (int cj = 0; cj < 8; ++cj)
+                if (col0 + 4 * cj < g.N) crow[4 * cj] = cv[cj];
             }
           }
         }
