@@ -519,6 +519,117 @@ __global__ void __launch_bounds__(256) ozaki_split_b_kernel(const cplx* __restri
   }
 }
 
+// B (K x N complex, row-major, K <= 512) -> column scales and slices in one
+// launch: a CTA takes eight columns of one entry, stages the K x 8 block in
+// shared memory (128-byte rows of B: coalesced), reduces the column maxima,
+// and for every slice writes the sixteen rows (2j: [Re b_j ; -Im b_j], 2j+1:
+// [Im b_j ; Re b_j]) -- contiguous in the slice tensor -- through a 16 KB
+// staging block as one coalesced copy.  Replaces ozaki_colscale_kernel +
+// ozaki_split_b_kernel (thread-per-column maxima, scattered 16-byte stores).
+constexpr int OFB_COLS = 8, OFB_KMAX = 512, OFB_KP = OFB_KMAX + 4;
+constexpr int OFB_SMEM = 2 * OFB_COLS * OFB_KP * 8 + 2 * OFB_COLS * 2 * OFB_KMAX + 1024;
+__global__ void __launch_bounds__(256) ozaki_split_b_fused_kernel(const cplx* __restrict__ B, long long ldb,
+                                                                  long long sB, int K, int N, double* __restrict__ sb,
+                                                                  int8_t* __restrict__ out) {
+  extern __shared__ __align__(16) uint8_t fsm[];
+  double* pre = reinterpret_cast<double*>(fsm);                 // [8][KP]
+  double* pim = pre + OFB_COLS * OFB_KP;                        // [8][KP]
+  int8_t* stage = reinterpret_cast<int8_t*>(pim + OFB_COLS * OFB_KP);   // [16 rows][2K]
+  double* cmax = reinterpret_cast<double*>(stage + 2 * OFB_COLS * 2 * OFB_KMAX);  // [8 warps][8] then [8]
+  __shared__ int sbad[OFB_COLS];
+  const int j0 = blockIdx.x * OFB_COLS, b = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ncol = min(OFB_COLS, N - j0);
+  if (threadIdx.x < OFB_COLS) sbad[threadIdx.x] = 0;
+  __syncthreads();
+  {  // load: thread (k = t / 8 + 32 i, c = t % 8); a warp reads four 128-byte rows
+    const int c = threadIdx.x & 7;
+    const cplx* p = B + (long long)b * sB + j0 + c;
+    double mx = 0.0;
+    bool bad = false;
+    for (int k = threadIdx.x >> 3; k < K; k += 32) {
+      cplx v = cmk(0.0, 0.0);
+      if (c < ncol) v = p[(long long)k * ldb];
+      pre[c * OFB_KP + k] = v.x;
+      pim[c * OFB_KP + k] = v.y;
+      bad |= !(fabs(v.x) <= DBL_MAX) || !(fabs(v.y) <= DBL_MAX);
+      mx = fmax(mx, fmax(fabs(v.x), fabs(v.y)));
+    }
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+    if (lane < 8) cmax[warp * 8 + lane] = mx;
+    if (bad) sbad[c] = 1;
+  }
+  __syncthreads();
+  if (threadIdx.x < OFB_COLS) {
+    double mx = 0.0;
+    for (int w = 0; w < 8; ++w) mx = fmax(mx, cmax[w * 8 + threadIdx.x]);
+    double scale, inv;
+    scale_of(mx, sbad[threadIdx.x] != 0, scale, inv);
+    if ((int)threadIdx.x < ncol) sb[(long long)b * N + j0 + threadIdx.x] = scale;
+    cmax[64 + threadIdx.x] = sbad[threadIdx.x] ? 0.0 : inv;
+  }
+  __syncthreads();
+  // digits: warp = column, lane = k mod 32 (conflict-free reads of the planes)
+  const int c = warp;
+  const double inv = cmax[64 + c];
+  double tr[16], ti[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int k = lane + 32 * i;
+    tr[i] = k < K ? pre[c * OFB_KP + k] * inv : 0.0;
+    ti[i] = k < K ? pim[c * OFB_KP + k] * inv : 0.0;
+  }
+  const int K2 = 2 * K;
+  const long long rows2n = 2LL * N;
+  for (int s = 0; s < OS; ++s) {
+    int8_t* r0 = stage + (2 * c) * K2;       // row 2j:   [re ; -im]
+    int8_t* r1 = r0 + K2;                    // row 2j+1: [im ;  re]
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int k = lane + 32 * i;
+      const double dr = rint(tr[i]), di = rint(ti[i]);
+      tr[i] = (tr[i] - dr) * 128.0;
+      ti[i] = (ti[i] - di) * 128.0;
+      if (k < K) {
+        const int8_t br = (int8_t)(int)dr, bi = (int8_t)(int)di;
+        r0[k] = br;
+        r0[K + k] = (int8_t)(-(int)di);
+        r1[k] = bi;
+        r1[K + k] = br;
+      }
+    }
+    __syncthreads();
+    // rows 2 j0 .. 2 j0 + 2 ncol of slice s are contiguous in the slice tensor
+    int8_t* dst = out + (((long long)b * OS + s) * rows2n + 2LL * j0) * K2;
+    const int nvec = (2 * ncol * K2) >> 4;
+    for (int v = threadIdx.x; v < nvec; v += 256)
+      reinterpret_cast<uint4*>(dst)[v] = reinterpret_cast<const uint4*>(stage)[v];
+    __syncthreads();
+  }
+}
+
+// column scales + slices of B: the fused kernel for K <= 512, else the two-kernel path
+int split_b(const cplx* B, long long ldb, long long sB, int K, int N, int batch, double* sb, int8_t* wb,
+            cudaStream_t stream) {
+  if (K <= OFB_KMAX) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(ozaki_split_b_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, OFB_SMEM);
+      attr = true;
+    }
+    ozaki_split_b_fused_kernel<<<dim3((N + OFB_COLS - 1) / OFB_COLS, batch), 256, OFB_SMEM, stream>>>(B, ldb, sB, K, N,
+                                                                                                     sb, wb);
+    cirr_note_launch();
+    return 0;
+  }
+  ozaki_colscale_kernel<<<dim3((N + 255) / 256, batch), 256, 0, stream>>>(B, ldb, sB, K, N, sb);
+  cirr_note_launch();
+  ozaki_split_b_kernel<<<dim3((N + 31) / 32, (K + 127) / 128, batch), 256, 0, stream>>>(B, ldb, sB, K, N, sb, wb);
+  cirr_note_launch();
+  return 0;
+}
+
 int encode_slice_map(CUtensorMap* map, const int8_t* base, long long K2, long long rows, long long batch,
                      int box_rows) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
@@ -649,10 +760,7 @@ int ozaki_cached_update(const cplx* LU, int n, int col0, int kw, int a_row0, int
   e = cirr_malloc_async((void**)&sb, (size_t)batch * N * sizeof(double), stream);
   if (e != cudaSuccess) { cudaFreeAsync(wb, stream); return (int)e; }
   int rc = 0;
-  ozaki_colscale_kernel<<<dim3((N + 255) / 256, batch), 256, 0, stream>>>(B, ldb, sB, OZ_W, N, sb);
-  cirr_note_launch();
-  ozaki_split_b_kernel<<<dim3((N + 31) / 32, (OZ_W + 127) / 128, batch), 256, 0, stream>>>(B, ldb, sB, OZ_W, N, sb, wb);
-  cirr_note_launch();
+  split_b(B, ldb, sB, OZ_W, N, batch, sb, wb, stream);
   CUtensorMap mA, mB;
   if (encode_slice_map(&mA, c.slices, K2, n, (long long)c.nfac * c.nsb, OBM) != 0 ||
       encode_slice_map(&mB, wb, K2, 2LL * N, batch, OBNH) != 0) {
@@ -752,11 +860,7 @@ int ozaki_zgemm_sub(const cplx* A, long long lda, long long sA, const cplx* B, l
     double* sb = scales + (long long)nb * M;
     ozaki_split_a_kernel<<<dim3((M + 7) / 8, nb), 256, 0, stream>>>(A + (long long)b0 * sA, lda, sA, M, K, wa, sa, 1, 0);
     cirr_note_launch();
-    ozaki_colscale_kernel<<<dim3((N + 255) / 256, nb), 256, 0, stream>>>(B + (long long)b0 * sB, ldb, sB, K, N, sb);
-    cirr_note_launch();
-    ozaki_split_b_kernel<<<dim3((N + 31) / 32, (K + 127) / 128, nb), 256, 0, stream>>>(B + (long long)b0 * sB, ldb,
-                                                                                      sB, K, N, sb, wb);
-    cirr_note_launch();
+    split_b(B + (long long)b0 * sB, ldb, sB, K, N, nb, sb, wb, stream);
     CUtensorMap mA, mB;
     if (encode_slice_map(&mA, wa, K2, M, nb, OBM) != 0 || encode_slice_map(&mB, wb, K2, 2LL * N, nb, OBNH) != 0) {
       rc = (int)cudaErrorInvalidValue;
