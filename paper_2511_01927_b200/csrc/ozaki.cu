@@ -2,26 +2,34 @@
 // Ozaki splitting: every row of A and every column of B is scaled by a power of
 // two and cut into eight signed 7-bit digits (int8 slices; 6 + 7 x 7 = 55 bits
 // below the row / column maximum), the digit products A_p B_q with p + q <= 7
-// are exact int32 sums on tcgen05.mma kind::i8 (SASS UTCIMMA) with the
-// accumulators of the eight weights d = p + q side by side in tensor memory
-// (8 x 64 columns = all 512), and the epilogue recombines them in integer
-// arithmetic (two int64 per element), converts once to FP64, applies the two
-// scales and subtracts from C.  The truncation error per k-term is below
-// 2^-53 rowmax(A) colmax(B): that of an FP64 GEMM up to the usual bound, with
-// integer (order-independent, bitwise reproducible) accumulation.
+// are exact int32 sums on tcgen05.mma kind::i8 (SASS UTCIMMA) accumulated in
+// tensor memory per weight d = p + q (four accumulators of 128 columns fill
+// the 512 TMEM columns, so a tile takes two passes: d = 0..3, then d = 4..7),
+// and the epilogue recombines each pass's four accumulators in int64, converts
+// once to FP64, applies the two scales and subtracts from C.  The truncation
+// error per k-term is below 2^-53 rowmax(A) colmax(B): that of an FP64 GEMM up
+// to the usual bound, with integer (order-independent, bitwise reproducible)
+// accumulation.
 //
-// Replaces, for the k = 512 trailing updates of the dense LU, the DMMA kernel
-// zgemm_sub_tma (lu_gemm.cuh): B200's FP64 tensor peak is 37.1 TF/s (measured,
-// tools/fp64_peak.cu), its int8 tensor peak 4.5 POPS; 36 slice products of the
-// real 2m x 2n x 2k embedding cost 288 mnk int8 operations per 8 mnk flops.
+// Replaces, for the k = 512 trailing updates of the dense LU and of the blocked
+// solves, the DMMA kernel zgemm_sub_tma (lu_gemm.cuh): B200's FP64 tensor peak
+// is 37.1 TF/s (measured, tools/fp64_peak.cu), its int8 tensor peak 4.57 POPS
+// (measured, tools/i8_peak.cu); 36 slice products of the real 2m x 2n x 2k
+// embedding cost 288 mnk int8 operations per 8 mnk flops.  Measured: 67 TF/s
+// FP64-equivalent at the LU's largest update (DESIGN.md section 4,
+// profiles/r02_ozaki_experiments.txt).
 //
 // Complex embedding: A' = [Re A | Im A] (m x 2k), and for complex column j of
 // B two rows of B'^T: [Re b_j ; -Im b_j] (real part of the product) and
 // [Im b_j ; Re b_j] (imaginary part), so the accumulator columns are
 // interleaved (re, im) like complex128 memory.
 //
-// Reference: this is the LU of z_j B - A behind linalg.py:55-71 (splu); the
-// reference calls SuperLU in FP64.
+// Execution: persistent CTA pairs (cta_group::2, M = 256 over the pair), TMA
+// producer warp, one MMA-issuing thread in the pair's leader, eight epilogue
+// warps per CTA; see the comments in ozaki_gemm_kernel.
+//
+// Reference: this is the arithmetic behind linalg.py:55-71 (splu of z_j B - A)
+// and linalg.py:46-52 (its solves); the reference calls SuperLU in FP64.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cfloat>
@@ -50,9 +58,6 @@ __device__ __forceinline__ unsigned osmem_u32(const void* p) { return (unsigned)
 __device__ __forceinline__ void ombar_init(uint64_t* bar, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(osmem_u32(bar)), "r"(count));
 }
-__device__ __forceinline__ void ombar_arrive(uint64_t* bar) {
-  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}" ::"r"(osmem_u32(bar)) : "memory");
-}
 __device__ __forceinline__ void ombar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
   asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}"
                ::"r"(osmem_u32(bar)), "r"(bytes) : "memory");
@@ -70,12 +75,6 @@ __device__ __forceinline__ void ombar_wait_cluster(uint64_t* bar, unsigned parit
       " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
       " @!p bra WAITC_%=;\n}" ::"r"(osmem_u32(bar)), "r"(parity) : "memory");
 }
-__device__ __forceinline__ void otma_load4(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
-                                           uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
-      ::"r"(osmem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(osmem_u32(bar)) : "memory");
-}
 // K-major operand tile with the 64-byte swizzle: rows of 64 bytes, groups of
 // eight rows 512 bytes apart (stride byte offset), descriptor version 1,
 // layout type 4 (SWIZZLE_64B).  A K step of 32 bytes advances the start address.
@@ -87,19 +86,6 @@ __device__ __forceinline__ uint64_t oumma_desc(unsigned saddr) {
   d |= (uint64_t)1 << 46;
   d |= (uint64_t)(OKB == 64 ? 4 : 6) << 61;
   return d;
-}
-__device__ __forceinline__ void oumma_i8(unsigned tmem_d, uint64_t da, uint64_t db, unsigned idesc, unsigned acc) {
-  asm volatile(
-      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-      " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}"
-      ::"r"(tmem_d), "l"(da), "l"(db), "r"(idesc), "r"(acc) : "memory");
-}
-__device__ __forceinline__ void otma_load4_mc(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
-                                              uint64_t* bar, unsigned short mask) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster"
-      " [%0], [%1, {%2, %3, %4, %5}], [%6], %7;"
-      ::"r"(osmem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(osmem_u32(bar)), "h"(mask) : "memory");
 }
 // TMA load into this CTA's shared memory, completion on the pair leader's barrier
 __device__ __forceinline__ void otma_load4_pair(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
@@ -127,10 +113,6 @@ __device__ __forceinline__ void oumma2_commit_mc(uint64_t* bar, unsigned short m
   asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
                ::"r"(osmem_u32(bar)), "h"(mask) : "memory");
 }
-__device__ __forceinline__ void oumma_commit_mc(uint64_t* bar, unsigned short mask) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
-               ::"r"(osmem_u32(bar)), "h"(mask) : "memory");
-}
 __device__ __forceinline__ void ocluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -138,16 +120,6 @@ __device__ __forceinline__ unsigned ocluster_rank() {
   unsigned r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
   return r;
-}
-__device__ __forceinline__ void oumma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(osmem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void otmem_ld16(unsigned taddr, unsigned* v) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-      : "r"(taddr) : "memory");
 }
 
 // 16 TMEM lanes x 32 columns: lane l of the warp gets, for repetition j = 0..3, columns
@@ -203,11 +175,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OTHREADS, 1) ozaki_g
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const unsigned tmem = *tmem_slot;
 
-  // A cluster of two CTAs takes two row tiles (2 tmp, 2 tmp + 1) of the same
-  // column tile: each loads its own A slices and half of the B slices, the
-  // latter multicast into both CTAs' shared memory (the kernel is bound by L2
-  // to shared-memory traffic; this removes a quarter of it).  Both CTAs run the
-  // same trip counts; a stage is free when both CTAs' MMAs have read it.
+  // A pair of CTAs (cta_group::2) takes two row tiles (2 tmp, 2 tmp + 1) of the
+  // same column tile: each loads its own A slices and its half (64 rows) of the
+  // B slices; the leader's MMAs (M = 256) make each tensor core read the other
+  // half of B from the partner, so a CTA's shared-memory port carries 96 B/clk
+  // of operand reads instead of 128.  Both CTAs run the same trip counts; the
+  // leader's commits release the stages and publish the accumulators in both.
   const unsigned crank = ocluster_rank();
   const int tiles_mp = (g.tiles_m + 1) >> 1;
   const int per = tiles_mp * g.tiles_n;
@@ -687,6 +660,49 @@ bool oz_lookup(const cplx* LU, int n, OzCache& out, long long& f0) {
   return false;
 }
 
+
+// Slice workspace: one buffer per launching stream, kept between calls and
+// grown on demand (cudaMalloc; stream-ordered reuse is safe because every user
+// of a stream's buffer runs on that stream).  cudaMallocAsync is not used here:
+// a multi-GiB request blocked the host for 40-600 ms per call once PyTorch's
+// allocator held most of the device (tools/gap_probe.py).
+struct OzWs { cudaStream_t stream; void* p; size_t bytes; };
+OzWs g_oz_ws[16];
+int g_oz_nws = 0;
+
+void* oz_workspace(cudaStream_t stream, size_t bytes) {
+  std::lock_guard<std::mutex> lk(g_oz_mutex);
+  OzWs* w = nullptr;
+  for (int i = 0; i < g_oz_nws; ++i)
+    if (g_oz_ws[i].stream == stream) w = &g_oz_ws[i];
+  if (!w) {
+    if (g_oz_nws == 16) return nullptr;
+    w = &g_oz_ws[g_oz_nws++];
+    *w = OzWs{stream, nullptr, 0};
+  }
+  if (w->bytes < bytes) {
+    if (w->p) cudaFree(w->p);   // synchronises: no kernel still reads the old buffer
+    w->p = nullptr;
+    w->bytes = 0;
+    const size_t want = (bytes + (64u << 20) - 1) & ~(size_t)((64u << 20) - 1);
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e != cudaSuccess) {   // PyTorch's cache may hold the memory: the stream-ordered allocator's handler frees it
+      cudaGetLastError();
+      void* probe = nullptr;
+      if (cirr_malloc_async(&probe, want, stream) == cudaSuccess) {
+        cudaFreeAsync(probe, stream);
+        cudaStreamSynchronize(stream);
+        e = cudaMalloc(&p, want);
+      }
+      if (e != cudaSuccess) { cudaGetLastError(); return nullptr; }
+    }
+    w->p = p;
+    w->bytes = want;
+  }
+  return w->p;
+}
+
 }  // namespace
 
 long long ozaki_factor_bytes(int n, int nfac) {
@@ -753,12 +769,10 @@ int ozaki_cached_update(const cplx* LU, int n, int col0, int kw, int a_row0, int
   if (!oz_lookup(LU, n, c, f0)) return -1;
   const long long K2 = 2LL * OZ_W;
   const long long b_bytes = (long long)OS * 2 * N * K2;
-  int8_t* wb = nullptr;
-  double* sb = nullptr;
-  cudaError_t e = cirr_malloc_async((void**)&wb, (size_t)batch * b_bytes, stream);
-  if (e != cudaSuccess) return (int)e;
-  e = cirr_malloc_async((void**)&sb, (size_t)batch * N * sizeof(double), stream);
-  if (e != cudaSuccess) { cudaFreeAsync(wb, stream); return (int)e; }
+  const size_t wb_bytes = ((size_t)batch * b_bytes + 255) & ~(size_t)255;
+  int8_t* wb = reinterpret_cast<int8_t*>(oz_workspace(stream, wb_bytes + (size_t)batch * N * sizeof(double)));
+  if (!wb) return (int)cudaErrorMemoryAllocation;
+  double* sb = reinterpret_cast<double*>(wb + wb_bytes);
   int rc = 0;
   split_b(B, ldb, sB, OZ_W, N, batch, sb, wb, stream);
   CUtensorMap mA, mB;
@@ -788,8 +802,6 @@ int ozaki_cached_update(const cplx* LU, int n, int col0, int kw, int a_row0, int
     cudaError_t le = cudaGetLastError();
     if (le != cudaSuccess) rc = (int)le;
   }
-  cudaFreeAsync(wb, stream);
-  cudaFreeAsync(sb, stream);
   return rc;
 }
 
@@ -814,8 +826,8 @@ long long ozaki_ws_bytes_per_entry(int M, int N, int K) {
 }
 
 // C -= A B for `batch` independent complex128 problems (row-major; strides in
-// elements).  Workspace comes from the stream-ordered pool, in chunks of
-// entries bounded by CIRR_OZAKI_WS_MB (default 4096 MiB).
+// elements).  The slices of a chunk of entries (CIRR_OZAKI_WS_MB, default
+// 512 MiB) live in the stream's kept workspace (oz_workspace).
 int ozaki_zgemm_sub(const cplx* A, long long lda, long long sA, const cplx* B, long long ldb, long long sB, cplx* C,
                     long long ldc, long long sC, int M, int N, int K, int batch, cudaStream_t stream) {
   if (!ozaki_shape_ok(M, N, K) || batch <= 0) return CIRR_EINVAL;
@@ -823,18 +835,9 @@ int ozaki_zgemm_sub(const cplx* A, long long lda, long long sA, const cplx* B, l
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(ozaki_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, OSMEM);
     if (e != cudaSuccess) return (int)e;
-    // keep the slice workspace in the stream-ordered pool between calls (the
-    // default pool gives everything back at every synchronisation)
-    int dev = 0;
-    cudaMemPool_t pool;
-    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t cur = 0, want = 6ULL << 30;
-      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &cur);
-      if (cur < want) cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &want);
-    }
     attr = true;
   }
-  static const long long ws_mb = getenv("CIRR_OZAKI_WS_MB") ? atoll(getenv("CIRR_OZAKI_WS_MB")) : 4096;
+  static const long long ws_mb = getenv("CIRR_OZAKI_WS_MB") ? atoll(getenv("CIRR_OZAKI_WS_MB")) : 512;
   static int sms = 0;
   if (!sms) {
     int dev = 0;
@@ -845,12 +848,10 @@ int ozaki_zgemm_sub(const cplx* A, long long lda, long long sA, const cplx* B, l
   const long long a_bytes = (long long)OS * M * K2, b_bytes = (long long)OS * 2 * N * K2;
   const long long per = a_bytes + b_bytes;
   int chunk = (int)max(1LL, min((long long)batch, (ws_mb << 20) / per));
-  int8_t* ws = nullptr;
-  double* scales = nullptr;
-  cudaError_t e = cirr_malloc_async((void**)&ws, (size_t)chunk * per, stream);
-  if (e != cudaSuccess) return (int)e;
-  e = cirr_malloc_async((void**)&scales, (size_t)chunk * (M + N) * sizeof(double), stream);
-  if (e != cudaSuccess) { cudaFreeAsync(ws, stream); return (int)e; }
+  const size_t slice_bytes = ((size_t)chunk * per + 255) & ~(size_t)255;
+  int8_t* ws = reinterpret_cast<int8_t*>(oz_workspace(stream, slice_bytes + (size_t)chunk * (M + N) * sizeof(double)));
+  if (!ws) return (int)cudaErrorMemoryAllocation;
+  double* scales = reinterpret_cast<double*>(ws + slice_bytes);
   int rc = 0;
   for (int b0 = 0; b0 < batch && rc == 0; b0 += chunk) {
     const int nb = min(chunk, batch - b0);
@@ -880,8 +881,6 @@ int ozaki_zgemm_sub(const cplx* A, long long lda, long long sA, const cplx* B, l
     cudaError_t le = cudaGetLastError();
     if (le != cudaSuccess) rc = (int)le;
   }
-  cudaFreeAsync(ws, stream);
-  cudaFreeAsync(scales, stream);
   return rc;
 }
 
