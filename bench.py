@@ -192,10 +192,10 @@ def cpu_model() -> str:
 
 def lu_traffic():
     """DRAM bytes of the LU stage per step, measured by ncu on this code
-    (profiles/r02_v5_lu_traffic.json, TAG=_v5 tools/ncu_r02.sh: dram__bytes_read +
+    (profiles/r02_v7_lu_traffic.json, TAG=_v7 tools/ncu_r02.sh: dram__bytes_read +
     dram__bytes_write over every LU kernel of one solve_multi); null when the
     profile is absent."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r02_v5_lu_traffic.json")
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r02_v7_lu_traffic.json")
     try:
         with open(path) as f:
             d = json.load(f)
