@@ -210,3 +210,53 @@ def test_int8_lu_and_cached_solves(lib, int8_mode):
     l0 = lib.call("cirr_launch_count")
     solve(0, batch)
     assert lib.call("cirr_launch_count") - l0 == without
+
+
+def test_engine_int8_matches_fp64(lib):
+    """solve_multi on a dense n = 2048 pencil (config-4 generator): the default int8 updates in the LU
+    and in the solves (factor slices cut and released by the engine) against the all-FP64 run --
+    same counts, same pass counts, eigenvalues to 1e-10, residuals <= 1e-10; the int8 kernels ran."""
+    from paper_2511_01927_b200 import Contour, SolverConfig, solve_multi
+    from paper_2511_01927_b200 import workloads as W
+
+    a, b = W.config4_matrices(seed=0, n=2048)
+
+    class Pn:
+        pass
+
+    p = Pn()
+    p.a, p.b, p.hermitian = a, b, False
+    cs = [Contour(shape="ellipse", center=0.5 + 0j, semi_re=0.3, semi_im=0.15, expected_count=60),
+          Contour(shape="ellipse", center=-0.5 + 0j, semi_re=0.3, semi_im=0.15, expected_count=60)]
+    cfg = SolverConfig(n_q=64, source_cols=32, n_moments=8, tol=1e-10)
+    prev = lib.call("cirr_set_lu_gemm", 1)
+    try:
+        l0 = lib.call("cirr_launch_count")
+        r8 = solve_multi(p, cs, cfg, seed=0)
+        n8 = lib.call("cirr_launch_count") - l0
+        lib.call("cirr_set_lu_gemm", 0)
+        l0 = lib.call("cirr_launch_count")
+        r64 = solve_multi(p, cs, cfg, seed=0)
+        n64 = lib.call("cirr_launch_count") - l0
+    finally:
+        lib.call("cirr_set_lu_gemm", prev)
+    assert n8 != n64   # split kernels + int8 updates replace DMMA launches
+    # the same outcome per contour in both arithmetics (a contour with an eigenvalue near its boundary may
+    # fail to converge in 8 passes in either)
+    compared = 0
+    for x, y, ex, ey in zip(r8.results, r64.results, r8.errors, r64.errors):
+        assert type(ex) is type(ey), (ex, ey)
+        if y is None:
+            continue
+        compared += 1
+        assert len(x.eigenvalues) == len(y.eigenvalues) > 0
+        assert x.stats.iterations == y.stats.iterations
+        for lam in y.eigenvalues:
+            assert np.min(np.abs(x.eigenvalues - lam)) <= 1e-10 * max(1.0, abs(lam))
+        assert x.residuals.max() <= 1e-10
+    assert compared > 0
+    # a second int8 run reuses the engine path from scratch (slices re-cut, earlier registration gone)
+    r8b = solve_multi(p, cs, cfg, seed=0)
+    for x, y in zip(r8.results, r8b.results):
+        if x is not None:
+            assert np.array_equal(x.eigenvalues, y.eigenvalues)   # integer accumulation: bitwise repeatable
