@@ -64,6 +64,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-variants", action="store_true", help="skip the labelled (non-reference) variants")
     ap.add_argument("--no-per-config", action="store_true", help="skip the config 2 / config 5 block")
+    ap.add_argument("--shard", default="geps", choices=["geps", "nodes"],
+                    help="N > 1: 'geps' (default) = one GEP per rank, weak scaling, no data-path collective; "
+                         "'nodes' = ONE GEP split by quadrature node over the ranks, one NCCL all-reduce of the "
+                         "moment blocks per pass (dist.solve_multi_node_sharded), strong scaling")
     return ap.parse_args()
 
 
@@ -460,6 +464,12 @@ def run_cirr(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    node_split = args.shard == "nodes" and world > 1
+    if node_split:   # one GEP (rank 0's matrices on every rank) split by node; the other ranks' work is its share
+        from paper_2511_01927_b200.dist import solve_multi_node_sharded
+        wl = build_workload(0)
+        dp = DevicePencil(wl.a, wl.b, hermitian=False)
+        solve_multi = lambda p, cs, c, seed=0: solve_multi_node_sharded(p, cs, c, "cirr", seed)  # noqa: E731
     for _ in range(args.warmup):
         solve_multi(dp, wl.contours, cfg, seed=0)
     torch.cuda.synchronize()
@@ -487,7 +497,7 @@ def run_cirr(args):
     stages = timer.totals()
     work = dict(timer.work)
     per_step = ms_max / args.steps
-    value = world * args.steps / (ms_max / 1e3)
+    value = (1 if node_split else world) * args.steps / (ms_max / 1e3)
 
     last = results[-1]
     pairs = sum(len(r.eigenvalues) for r in last.results if r is not None)
@@ -517,12 +527,12 @@ def run_cirr(args):
         d2h = sum(r.eigenvectors.nbytes + r.eigenvalues.nbytes + r.residuals.nbytes
                   for r in m.results if r is not None)
     e2e_s = max_over_ranks(statistics.median(e2e_times))
-    e2e_value = world / e2e_s
+    e2e_value = (1 if node_split else world) / e2e_s
 
     # labelled variants (NOT the path of record): SURVEY.md finding 9
     # (conjugate-pair halving) and finding 8 (early exit), same workload and tol
     variants = {}
-    if not args.no_variants:
+    if not args.no_variants and not node_split:
         import dataclasses
 
         labels = {
@@ -604,9 +614,12 @@ def run_cirr(args):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": per_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": per_step, "higher_is_better": True,
+            "scaling": "strong" if node_split else "weak",
             "vs_baseline": None, "dtype": DTYPE, "data": "synthetic (seeded BASELINE config 4)",
-            "config": bench_config(wl),
+            "config": dict(bench_config(wl), **({"parallelism": "one GEP split by quadrature node over the ranks, one "
+                                                                       "all-reduce of the moment blocks per pass"}
+                                                      if node_split else {})),
             "roofline": {"bound": "tensor", "kernel": "batched zgetrf (K2: panel + trailing updates; the k = 512 "
                                                       "updates on int8 tensor cores, the rest on FP64 DMMA)",
                          "achieved": lu_tflops, "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
@@ -625,7 +638,7 @@ def run_cirr(args):
                                      "ms_per_step": stage_ms / args.steps},
             "stage_ms_per_step": {k: v / args.steps for k, v in sorted(stages.items())},
             "time_per_gep_s": per_step / 1e3,
-            "eigenpairs_per_s": pairs * world / (per_step / 1e3),
+            "eigenpairs_per_s": pairs * (1 if node_split else world) / (per_step / 1e3),
             # shifted solves = pencils x passes; RHS columns = sum of n_linear_solves
             "shifted_solves_per_s": (last.stats.n_factorizations * max(iters or [1])) * world / (per_step / 1e3),
             "rhs_columns_per_s": solves * world / (per_step / 1e3),

@@ -1,11 +1,14 @@
 """Multi-GPU plumbing for the CIRR stage.
 
 The path shards by independent objects: whole GEPs (config 2's batch, or the
-weak-scaling bench where each rank solves its own GEP).  There is no
-data-path collective; torch.distributed is used only for the barrier and the
-max-over-ranks timing reduction.  (Sharding one GEP's (contour x node)
-pencils across GPUs would need one reduction of the moment block per
-contour -- SURVEY.md 8(e) -- and is not built: BASELINE targets one GPU.)
+weak-scaling bench where each rank solves its own GEP), with no data-path
+collective; torch.distributed then carries only the barrier and the
+max-over-ranks timing reduction.  One GEP can also be split by quadrature node
+(SURVEY.md 8(e)): ``solve_multi_node_sharded`` gives rank r the nodes r,
+r + world, ... of every contour (its share of the factorisations and solves),
+sums the partial moment blocks with one all-reduce per pass (NCCL over NVLink:
+33 MB in config 4's first pass, 15 MB in the refinement passes) and lets every
+rank run the same Rayleigh-Ritz on the identical sums.
 """
 
 from __future__ import annotations
@@ -84,3 +87,45 @@ def solve_multi_batch_sharded(pencils, contours, cfg=None, solver: str = "cirr",
         for i, r in zip(idx, rs):
             out[i] = r
     return out
+
+
+def _allreduce(group=None):
+    """In-place all-reduce of a device tensor over the group: "sum" (complex tensors as their real
+    view) or "min"."""
+    import torch
+    import torch.distributed as dist
+
+    def run(t, op):
+        v = torch.view_as_real(t) if t.is_complex() else t
+        dist.all_reduce(v, op=dist.ReduceOp.SUM if op == "sum" else dist.ReduceOp.MIN, group=group)
+
+    return run
+
+
+def solve_multi_node_sharded(pencil, contours, cfg=None, solver: str = "cirr", seed: int = 0, *, group=None,
+                             shard_ctx=None):
+    """``solve_multi`` of ONE pencil over the ranks of ``group`` (one rank per
+    GPU, every rank holding A and B): rank r factors and solves the quadrature
+    nodes r, r + world, ... of every contour; after each solve pass the partial
+    moment blocks are summed over the ranks (the path's one exchange step) and
+    every rank continues with the same Rayleigh-Ritz, so all ranks return the
+    same eigenpairs.  A singular shift found by any rank drops that contour on
+    all of them (one min-reduction after the factorisation).  Per-rank
+    ``stats`` count that rank's factorisations and solves.  ``shard_ctx``
+    (a ``solvers.NodeShard``) replaces the torch.distributed group, e.g. for
+    threads sharing one GPU in tests."""
+    import torch.distributed as dist
+
+    from . import solvers as S
+
+    if shard_ctx is None:
+        on = dist.is_available() and dist.is_initialized()
+        rank, world = (dist.get_rank(group), dist.get_world_size(group)) if on else (0, 1)
+        shard_ctx = S.NodeShard(rank, world, _allreduce(group))
+    if cfg is not None and getattr(cfg, "conjugate_pairs", False) and shard_ctx.world > 1:
+        raise S.ParameterError("the conjugate-pair variant and the node split are exclusive")
+    prev = S.set_node_shard(shard_ctx)
+    try:
+        return S.solve_multi(pencil, contours, cfg, solver, seed)
+    finally:
+        S.set_node_shard(prev)

@@ -491,6 +491,35 @@ class StageTimer:
 _TIMER: StageTimer | None = None
 
 
+class NodeShard:
+    """One GEP split over ranks by quadrature node: rank r
+    factors and solves the nodes r, r + world, ... of every contour, the moment
+    blocks are summed over the ranks once per pass (``allreduce(tensor, op)``,
+    op in {"sum", "min"}, in place on a device tensor), and every rank then
+    runs the same Rayleigh-Ritz on identical data.  Installed per thread by
+    ``dist.solve_multi_node_sharded``."""
+
+    def __init__(self, rank: int, world: int, allreduce):
+        if world < 1 or not 0 <= rank < world:
+            raise ParameterError("bad rank/world for the node shard")
+        self.rank, self.world, self.allreduce = rank, world, allreduce
+
+
+_SHARD = __import__("threading").local()
+
+
+def _node_shard():
+    sh = getattr(_SHARD, "value", None)
+    return sh if sh is not None and sh.world > 1 else None
+
+
+def set_node_shard(shard):
+    """Install (or clear, with None) the calling thread's NodeShard; returns the previous one."""
+    prev = getattr(_SHARD, "value", None)
+    _SHARD.value = shard
+    return prev
+
+
 def set_stage_timer(timer: StageTimer | None) -> None:
     global _TIMER
     _TIMER = timer
@@ -605,6 +634,15 @@ class _Contour:
         rule = quadrature_for(contour, cfg.n_q)
         self.nodes = np.asarray(rule.nodes, dtype=np.complex128)
         self.weights = np.asarray(rule.weights, dtype=np.complex128)
+        self.all_nodes = self.nodes
+        self.node_ids = np.arange(len(self.nodes))     # position of each kept node in the full rule
+        sh = _node_shard()
+        if sh is not None:
+            if len(self.nodes) < sh.world:
+                raise ParameterError(f"n_q = {len(self.nodes)} nodes cannot be split over {sh.world} ranks")
+            self.node_ids = np.arange(sh.rank, len(self.nodes), sh.world)
+            self.nodes = self.nodes[self.node_ids]
+            self.weights = self.weights[self.node_ids]
         self.gamma, self.rho = moment_frame(contour)
         self.ncols = cfg.cols_for(getattr(contour, "expected_count", 0))
         self.seed = seed
@@ -892,6 +930,8 @@ class _Engine:
         for ci, c in enumerate(self.cs):
             c.stats.n_factorizations = len(c.fidx)
         seen = set()
+        sh = _node_shard()
+        first = np.full(len(self.cs), np.iinfo(np.int64).max, dtype=np.int64)   # first failing node, full-rule index
         for j in np.flatnonzero(bad):
             ci = int(np.searchsorted(self.node_off, j, side="right")) - 1
             if ci in seen:
@@ -899,8 +939,16 @@ class _Engine:
             seen.add(ci)
             c = self.cs[ci]
             jn = int(c.fidx[j - self.node_off[ci]])
-            c.error = SingularShiftError(complex(c.nodes[jn]), node_index=jn)
-            c.done = True
+            first[ci] = int(c.node_ids[jn])
+        if sh is not None:   # every rank must drop the same contours: the smallest failing node over the ranks
+            ft = _h2d(first)
+            sh.allreduce(ft, "min")
+            first = ft.cpu().numpy()
+        for ci, c in enumerate(self.cs):
+            if first[ci] != np.iinfo(np.int64).max:
+                g = int(first[ci])
+                c.error = SingularShiftError(complex(c.all_nodes[g]), node_index=g)
+                c.done = True
 
     # -- K3: solve all pencils of the listed contours against per-contour RHS
     def apply(self, active: list, rhs: dict, moments: int, real_rhs: bool = False) -> dict:
@@ -1023,6 +1071,10 @@ class _Engine:
                         _lib.call("cirr_moments", _ptr(Y), K, n * K, n, K, _ptr(cpart), mc, _ptr(off_t), nset,
                                   _ptr(St[:, m0 * K:]), n, moments * K * n, self.stream)
             del Y
+        sh = _node_shard()
+        if sh is not None:   # the one data-path exchange of the node split: sum the partial moment blocks
+            with _stage("allreduce"):
+                sh.allreduce(St, "sum")
         for s, ci in enumerate(active):
             self.cs[ci].stats.n_linear_solves += len(self.cs[ci].fidx) * ks[s]
         out, pieces, rows = {}, [], 0
@@ -1612,8 +1664,9 @@ def _waves(cstates: list, n: int, budget_bytes: int) -> list:
     inverses (made when a solve reads them) and the LU workspace share."""
     per = n * n * 16 + int(_lib.call("cirr_diag_inv_bytes", n, 1)) + int(_lib.call("cirr_zgetrf_ws_bytes", n, 1))
     waves, cur, cur_bytes, cur_p = [], [], 0, 0
+    sh = _node_shard()
     for c in cstates:
-        p = len(c.fidx)
+        p = len(c.fidx) if sh is None else -(-len(c.all_nodes) // sh.world)
         if p > _MAX_WAVE_PENCILS:
             raise ParameterError(f"n_q = {p} factored nodes per contour exceeds {_MAX_WAVE_PENCILS}")
         need = p * per
@@ -1713,7 +1766,13 @@ def _interleave_split(wave: list) -> list:
 
 def _run_states(dp, cstates, cfg, moments_override=None, solver: str = "cirr"):
     moments = cfg.n_moments if moments_override is None else moments_override
-    for wave in _waves(cstates, dp.n, _hbm_budget(dp.n, cstates)):
+    budget = _hbm_budget(dp.n, cstates)
+    sh = _node_shard()
+    if sh is not None:   # the ranks must cut the same waves: the smallest budget, the largest node share
+        bt = _h2d(np.asarray([budget], dtype=np.int64))
+        sh.allreduce(bt, "min")
+        budget = int(bt.cpu().numpy()[0])
+    for wave in _waves(cstates, dp.n, budget):
         parts = _interleave_split(wave) if solver == "cirr" else [wave]
         if len(parts) > 1:
             _interleave([_Engine(dp, part, cfg) for part in parts], moments)

@@ -120,3 +120,46 @@ def test_sharded_batch_world2():
             for x, y in zip(res, want[i]):
                 if x is not None:
                     np.testing.assert_array_equal(x, y)
+
+
+def _node_worker(rank, world, port, out):
+    """Node split of one GEP: each rank's partial centred moments over its interleaved
+    node share, summed by the dist module's all-reduce, equal the full moment blocks (oracle arithmetic)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import cirr as O
+    from paper_2511_01927_b200.contours import Contour
+    from paper_2511_01927_b200.dist import _allreduce
+
+    rng = np.random.default_rng(0)
+    n = 40
+    a = np.diag(np.arange(1.0, n + 1)) + 0.01 * rng.standard_normal((n, n))
+    a = (a + a.T) / 2
+    p = O.Pencil(a, np.eye(n), True)
+    c = Contour(shape="circle", center=5.0 + 0j, radius=2.6, expected_count=5)
+    cfg = O.OracleConfig(n_q=16, source_cols=6, n_moments=4)
+    nodes, weights = O.quadrature(c, cfg.n_q)
+    frame = (5.0 + 0j, 2.6)   # centred, scaled moments (DESIGN.md section 3 item 1)
+    v = rng.standard_normal((n, 6))
+    ids = np.arange(rank, len(nodes), world)
+    part = O.Projector(p, nodes[ids], weights[ids], cfg, frame).apply(v, 4)
+    t = torch.from_numpy(np.stack(part))
+    _allreduce()(t, "sum")
+    full = np.stack(O.Projector(p, nodes, weights, cfg, frame).apply(v, 4))
+    err = float(np.abs(t.numpy() - full).max() / np.abs(full).max())
+    first = torch.tensor([7 if rank == 1 else np.iinfo(np.int64).max], dtype=torch.int64)
+    _allreduce()(first, "min")
+    out[rank] = (err, int(first[0]), len(ids))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_node_split_moments_world2():
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_node_worker, args=(2, port, out), nprocs=2, join=True)
+    for r in (0, 1):
+        err, first, cnt = out[r]
+        assert err < 1e-13 and first == 7 and cnt == 8
