@@ -388,7 +388,7 @@ __device__ __forceinline__ uint4 negate_bytes(uint4 v) {
 __device__ __forceinline__ void scale_of(double mx, bool bad, double& scale, double& inv) {
   int e = 0;
   if (mx > 0.0) e = ilogb(mx) + 1;
-  e = max(-900, min(1000, e));
+  e = max(-1000, min(1024, e));   // 2^(e - 6) and 2^(6 - e) stay finite powers of two
   scale = bad ? nan("") : ldexp(1.0, e - 6);
   inv = ldexp(1.0, 6 - e);
 }

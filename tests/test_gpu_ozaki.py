@@ -89,6 +89,28 @@ def test_ozaki_subblocks_in_place(lib):
     assert (err <= bound(P0[:, r0:, k0:r0], P0[:, k0:r0, r0:]) + 4e-16 * np.abs(ref[:, r0:, r0:])).all()
 
 
+def test_ozaki_extreme_magnitudes(lib):
+    """Rows near the top and the bottom of the FP64 range keep their relative accuracy (the power-of-two
+    scales stay finite)."""
+    M, N, K = 128, 32, 64
+    rng = np.random.default_rng(9)
+    A = crandn(rng, 1, M, K)
+    B = crandn(rng, 1, K, N)
+    A[0, 0] *= 1e300
+    A[0, 1] *= 1e-290
+    B[0, :, 2] *= 1e-290
+    C = torch.zeros((1, M, N), dtype=torch.complex128, device="cuda")
+    dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    assert lib.call("cirr_ozaki_zgemm_sub", dA.data_ptr(), K, M * K, dB.data_ptr(), N, K * N, C.data_ptr(), N, M * N,
+                    M, N, K, 1, S()) == 0
+    torch.cuda.synchronize()
+    got = -C.cpu().numpy()[0]
+    with np.errstate(over="ignore", under="ignore"):
+        ref = (A @ B)[0]
+    for (i, j) in [(0, 5), (1, 5), (7, 2), (0, 2)]:
+        assert abs(got[i, j] - ref[i, j]) <= 1e-13 * abs(ref[i, j]) + 1e-300, (i, j, got[i, j], ref[i, j])
+
+
 def test_ozaki_zero_and_nonfinite(lib):
     """Zero rows / columns give exact zeros; a NaN poisons its row (as the FP64 GEMM would)."""
     M, N, K = 128, 32, 64
