@@ -161,12 +161,19 @@ class SolverConfig:
     # Labelled variant (SURVEY.md finding 8): stop refining a contour once its
     # converged set (pairs with residual <= tol) is unchanged across two passes.
     early_exit: bool = False
+    # Arithmetic of the k = 512 updates of dense factorisations and solves:
+    # None keeps the library mode (default int8: exact digit products on the
+    # tcgen05 tensor cores, DESIGN.md section 3 item 8; CIRR_LU_GEMM=dmma or
+    # cirr_set_lu_gemm(0) change it), "int8" / "f64" set it for this call.
+    arith: str | None = None
 
     def __post_init__(self):
         if self.n_q < 4 or self.n_moments < 1 or self.max_refine < 1:
             raise ParameterError("counts must be >= 1 (n_q >= 4)")
         if self.tol <= 0:
             raise ParameterError("tol must be positive")
+        if self.arith not in (None, "int8", "f64"):
+            raise ParameterError("arith must be None, 'int8' or 'f64'")
 
     def cols_for(self, expected_count: int) -> int:
         if self.source_cols is not None:
@@ -184,7 +191,8 @@ def _cfg_view(cfg) -> SolverConfig:
                         max_refine=cfg.max_refine, tol=cfg.tol, rank_rel_tol=cfg.rank_rel_tol,
                         drop_tol=getattr(cfg, "drop_tol", 1e-10),
                         conjugate_pairs=bool(getattr(cfg, "conjugate_pairs", False)),
-                        early_exit=bool(getattr(cfg, "early_exit", False)))
+                        early_exit=bool(getattr(cfg, "early_exit", False)),
+                        arith=getattr(cfg, "arith", None))
 
 
 @dataclass
@@ -1765,6 +1773,17 @@ def _interleave_split(wave: list) -> list:
 
 
 def _run_states(dp, cstates, cfg, moments_override=None, solver: str = "cirr"):
+    arith = getattr(cfg, "arith", None)
+    if arith is None:
+        return _run_states_mode(dp, cstates, cfg, moments_override, solver)
+    prev = int(_lib.call("cirr_set_lu_gemm", 1 if arith == "int8" else 0))   # library-wide while this call runs
+    try:
+        return _run_states_mode(dp, cstates, cfg, moments_override, solver)
+    finally:
+        _lib.call("cirr_set_lu_gemm", prev)
+
+
+def _run_states_mode(dp, cstates, cfg, moments_override=None, solver: str = "cirr"):
     moments = cfg.n_moments if moments_override is None else moments_override
     budget = _hbm_budget(dp.n, cstates)
     sh = _node_shard()

@@ -277,6 +277,14 @@ def test_engine_int8_matches_fp64(lib):
             assert np.min(np.abs(x.eigenvalues - lam)) <= 1e-10 * max(1.0, abs(lam))
         assert x.residuals.max() <= 1e-10
     assert compared > 0
+    # the per-call switch selects the same two paths and restores the library mode
+    import dataclasses
+    mode0 = lib.call("cirr_set_lu_gemm", -1)
+    rf = solve_multi(p, cs, dataclasses.replace(cfg, arith="f64"), seed=0)
+    assert lib.call("cirr_set_lu_gemm", -1) == mode0
+    for x, y in zip(rf.results, r64.results):
+        if y is not None:
+            assert np.array_equal(x.eigenvalues, y.eigenvalues)
     # a second int8 run reuses the engine path from scratch (slices re-cut, earlier registration gone)
     r8b = solve_multi(p, cs, cfg, seed=0)
     for x, y in zip(r8.results, r8b.results):

@@ -219,3 +219,11 @@ def test_contains_rows_equals_contains_many():
         ref = contains_many(c, z[b])
         ref[counts[b]:] = False
         assert np.array_equal(got[b], ref)
+
+
+def test_solver_config_arith_option():
+    from paper_2511_01927_b200 import SolverConfig
+    from paper_2511_01927_b200.errors import ParameterError
+    assert SolverConfig().arith is None and SolverConfig(arith="f64").arith == "f64"
+    with pytest.raises(ParameterError):
+        SolverConfig(arith="fp16")
