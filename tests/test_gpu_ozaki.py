@@ -33,7 +33,8 @@ def bound(A, B):
     return K * 2.0 ** -50 * ra[..., :, None] * cb[..., None, :]
 
 
-@pytest.mark.parametrize("shape", [(128, 32, 32), (256, 64, 512), (200, 45, 96), (1000, 333, 512), (130, 1, 64)])
+@pytest.mark.parametrize("shape", [(128, 32, 32), (256, 64, 512), (200, 45, 96), (1000, 333, 512), (130, 1, 64),
+                                   (256, 40, 1024), (384, 70, 4096)])
 def test_ozaki_matches_numpy(lib, shape):
     M, N, K = shape
     rng = np.random.default_rng(M + N + K)
