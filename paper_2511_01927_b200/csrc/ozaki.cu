@@ -676,7 +676,11 @@ void* oz_workspace(cudaStream_t stream, size_t bytes) {
   for (int i = 0; i < g_oz_nws; ++i)
     if (g_oz_ws[i].stream == stream) w = &g_oz_ws[i];
   if (!w) {
-    if (g_oz_nws == 16) return nullptr;
+    if (g_oz_nws == 16) {   // a 17th stream: the oldest buffer goes (cudaFree synchronises the device)
+      if (g_oz_ws[0].p) cudaFree(g_oz_ws[0].p);
+      for (int i = 1; i < 16; ++i) g_oz_ws[i - 1] = g_oz_ws[i];
+      --g_oz_nws;
+    }
     w = &g_oz_ws[g_oz_nws++];
     *w = OzWs{stream, nullptr, 0};
   }

@@ -291,3 +291,20 @@ def test_engine_int8_matches_fp64(lib):
     for x, y in zip(r8.results, r8b.results):
         if x is not None:
             assert np.array_equal(x.eigenvalues, y.eigenvalues)   # integer accumulation: bitwise repeatable
+
+
+def test_ozaki_many_streams(lib):
+    """More launching streams than workspace slots: the oldest workspace is recycled, results stay right."""
+    M, N, K = 128, 16, 32
+    rng = np.random.default_rng(21)
+    A, B = crandn(rng, 1, M, K), crandn(rng, 1, K, N)
+    dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    ref = -(A @ B)
+    streams = [torch.cuda.Stream() for _ in range(20)]
+    for st in streams:
+        with torch.cuda.stream(st):
+            C = torch.zeros((1, M, N), dtype=torch.complex128, device="cuda")
+            assert lib.call("cirr_ozaki_zgemm_sub", dA.data_ptr(), K, M * K, dB.data_ptr(), N, K * N, C.data_ptr(), N,
+                            M * N, M, N, K, 1, st.cuda_stream) == 0
+            st.synchronize()
+            assert np.abs(C.cpu().numpy() - ref).max() < 1e-13
