@@ -555,9 +555,11 @@ __global__ void __launch_bounds__(256) ozaki_split_b_fused_kernel(const cplx* __
   }
   const int K2 = 2 * K;
   const long long rows2n = 2LL * N;
+  // each warp stages and writes its own two rows (2 K2 contiguous bytes of the slice tensor): no CTA barrier
+  int8_t* r0 = stage + (2 * c) * K2;       // row 2j:   [re ; -im]
+  int8_t* r1 = r0 + K2;                    // row 2j+1: [im ;  re]
+  const bool live = c < ncol;
   for (int s = 0; s < OS; ++s) {
-    int8_t* r0 = stage + (2 * c) * K2;       // row 2j:   [re ; -im]
-    int8_t* r1 = r0 + K2;                    // row 2j+1: [im ;  re]
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       const int k = lane + 32 * i;
@@ -572,13 +574,14 @@ __global__ void __launch_bounds__(256) ozaki_split_b_fused_kernel(const cplx* __
         r1[K + k] = br;
       }
     }
-    __syncthreads();
-    // rows 2 j0 .. 2 j0 + 2 ncol of slice s are contiguous in the slice tensor
-    int8_t* dst = out + (((long long)b * OS + s) * rows2n + 2LL * j0) * K2;
-    const int nvec = (2 * ncol * K2) >> 4;
-    for (int v = threadIdx.x; v < nvec; v += 256)
-      reinterpret_cast<uint4*>(dst)[v] = reinterpret_cast<const uint4*>(stage)[v];
-    __syncthreads();
+    __syncwarp();
+    if (live) {
+      int8_t* dst = out + (((long long)b * OS + s) * rows2n + 2LL * (j0 + c)) * K2;
+      const int nvec = (2 * K2) >> 4;
+      for (int v = lane; v < nvec; v += 32)
+        reinterpret_cast<uint4*>(dst)[v] = reinterpret_cast<const uint4*>(r0)[v];
+    }
+    __syncwarp();
   }
 }
 
