@@ -643,6 +643,8 @@ def run_cirr(args):
             "shifted_solves_per_s": (last.stats.n_factorizations * max(iters or [1])) * world / (per_step / 1e3),
             "rhs_columns_per_s": solves * world / (per_step / 1e3),
             "eigenpairs": counts, "iterations": iters,
+            # the reference's residual metric (solvers.py:140-147) of the returned pairs, computed in FP64
+            "max_residual": max([float(r.residuals.max()) for r in last.results if r is not None] or [None]),
             "n_factorizations": last.stats.n_factorizations, "n_linear_solves": solves,
             "executed_flops_per_step": stage_flops / args.steps,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
