@@ -204,6 +204,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OTHREADS, 1) ozaki_g
       for (int t = cl_id; t < ntiles; t += cl_n) {
         const int b = t / per, r = t - b * per;
         const int m0 = (2 * (r / g.tiles_n) + (int)crank) * OBM, n0 = (r % g.tiles_n) * OBN;
+        // the last column tile is as narrow as the columns left (multiple of 16): each CTA holds half of it
+        const int ntile = min(OBN, (2 * g.N - n0 + 15) & ~15);
         const int ab = (g.a_bmap ? g.a_bmap[b] : b) * g.a_mul + g.a_add;
         // sweep 0: A 0..3 x B 0..3 (d <= 3); sweep 1: A 0..3 x B 1..7 and sweep 2: A 4..7 x B 0..3 (d = 4..7)
         for (int sw = 0; sw < 3; ++sw) {
@@ -219,7 +221,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OTHREADS, 1) ozaki_g
             for (int s = 0; s < 4; ++s)
               otma_load4_pair(base + s * OA_SLICE, &mapA, kb * OKB, g.a_row0 + m0, a0 + s, ab, lbar);
             for (int s = 0; s < nb; ++s)
-              otma_load4_pair(base + OSLOT_A * OA_SLICE + s * OB_SLICE, &mapB, kb * OKB, n0 + (int)crank * OBNH,
+              otma_load4_pair(base + OSLOT_A * OA_SLICE + s * OB_SLICE, &mapB, kb * OKB, n0 + (int)crank * (ntile >> 1),
                               b0 + s, b, lbar);
           }
         }
@@ -228,9 +230,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OTHREADS, 1) ozaki_g
   } else if (warp == 1) {
     if (lane == 0 && crank == 0) {
       // instruction descriptor: D = S32, A = B = signed int8, both K-major, N >> 3, M >> 4 (M = 256 over the CTA pair)
-      constexpr unsigned idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((unsigned)(OBN >> 3) << 17) | ((unsigned)((2 * OBM) >> 4) << 24);
+      constexpr unsigned idesc0 = (2u << 4) | (1u << 7) | (1u << 10) | ((unsigned)((2 * OBM) >> 4) << 24);
       int it = 0, vt = 0;
       for (int t = cl_id; t < ntiles; t += cl_n) {
+        const int n0 = ((t % per) % g.tiles_n) * OBN;
+        const unsigned idesc = idesc0 | ((unsigned)(min(OBN, (2 * g.N - n0 + 15) & ~15) >> 3) << 17);
         for (int sw = 0; sw < 3; ++sw) {
           if (sw < 2) {  // sweeps 0 and 1 start a fresh accumulator set
             ombar_wait_cluster(tempty, (vt & 1) ^ 1);
