@@ -186,6 +186,21 @@ def test_int8_lu_and_cached_solves(lib, int8_mode):
     assert np.array_equal(ipiv.cpu().numpy(), ipiv0.cpu().numpy())
     dlu = (F - F0).abs().max().item() / F0.abs().max().item()
     assert dlu < 1e-11, dlu
+
+    def backward_error(Ft, piv, j=0):
+        """max |P A - L U| / (n max|A|) of pencil j, formed in FP64 on the host."""
+        lu = Ft[j].cpu().numpy()
+        L = np.tril(lu, -1) + np.eye(n)
+        U = np.triu(lu)
+        pa = A[j].copy()
+        for i, pi in enumerate(piv[j].cpu().numpy()):
+            if pi != i:
+                pa[[i, pi]] = pa[[pi, i]]
+        return np.abs(pa - L @ U).max() / (n * np.abs(A[j]).max())
+
+    be8, be64 = backward_error(F, ipiv), backward_error(F0, ipiv0)
+    # the int8 updates are as accurate as the FP64 ones (both far below n u max|A|)
+    assert be8 < 2.0 ** -52 and be8 <= 2.0 * be64 + 2.0 ** -60, (be8, be64)
     dinv = torch.zeros(lib.call("cirr_diag_inv_bytes", n, batch), dtype=torch.uint8, device="cuda")
     lib.call("cirr_diag_inverses", F.data_ptr(), n, n, n * n, batch, dinv.data_ptr(), S())
     nbytes = lib.call("cirr_ozaki_factor_bytes", n, batch)
