@@ -1134,7 +1134,11 @@ class _Engine:
         if nbytes == 0 or nbytes + (12 << 30) > _free_hbm():
             return
         with _stage("solve.ozsplit"):
-            self.ozbuf = self.torch.empty(nbytes, dtype=self.torch.uint8, device="cuda")
+            try:
+                self.ozbuf = self.torch.empty(nbytes, dtype=self.torch.uint8, device="cuda")
+            except self.torch.cuda.OutOfMemoryError:   # fragmented cache: the solves stay on FP64 DMMA
+                self.ozbuf = False
+                return
             _lib.call("cirr_ozaki_split_factors", _ptr(self.pencils), n, n, n * n, self.P, _ptr(self.ozbuf),
                       self.stream)
 
